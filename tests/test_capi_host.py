@@ -1,0 +1,113 @@
+"""CPU-side checks of the product library: it loads without a GPU, exports every
+symbol include/rtnq_capi.h declares, its geometry helpers agree with the oracle,
+the selective-precision plan logic matches the reference, and compute entry
+points fail loudly (no CPU fallback) when there is no device."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2505_15909_b200 as rq
+from conftest import ROOT, has_gpu
+from oracle import KERNEL, NATIVE, ROW_MAJOR
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "rtnq_capi.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)  # declarations only, not comments
+    return sorted(set(re.findall(r"^[a-z0-9_ ]+\**\s*\**(rtnq_[a-z0-9_]+)\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = rq.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_geometry_matches_oracle(oracle):
+    rng = np.random.default_rng(5)
+    for kind, ok in ((rq.ROW_MAJOR, ROW_MAJOR), (rq.KERNEL_INTERLEAVED, KERNEL), (rq.NATIVE, NATIVE)):
+        for bits in (4, 8):
+            for rows, cols in ((16, 64), (17, 5), (33, 96), (300, 520)):
+                lay = rq.layout(kind)
+                assert rq.layout_bytes(lay, bits, rows, cols) == oracle.layout_bytes(ok, bits, rows, cols)
+                for _ in range(50):
+                    r, c = int(rng.integers(rows)), int(rng.integers(cols))
+                    assert rq.layout_index(lay, bits, rows, cols, r, c) == \
+                        oracle.layout_index(ok, bits, rows, cols, r, c)
+    with pytest.raises(rq.ShapeError):
+        rq.layout_index(rq.layout(rq.ROW_MAJOR), 4, 2, 2, 2, 0)
+    assert rq.groups_per_row(128, False, 256) == 2
+    with pytest.raises(rq.ShapeError):
+        rq.groups_per_row(128, False, 200)
+    with pytest.raises(rq.InvalidInputError):
+        rq.groups_per_row(96, False, 192)
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_compute_fails_loudly_without_gpu():
+    with pytest.raises(rq.CudaError):
+        rq.quantize_tensor(np.ones((2, 4), np.float32), 4, 4)
+
+
+# ---- selective precision (plan.hpp); the reference's test_plan.cpp cases -------------
+
+def test_plan_golden(golden_plan):
+    z = golden_plan
+    for text, canon, status, offset, table in zip(z["texts"], z["canon"], z["status"],
+                                                  z["offset"], z["tables"]):
+        text = str(text)
+        if status == 0:
+            t, c = rq.plan.resolve(text, 80)
+            assert c == str(canon), text
+            assert np.array_equal(t.ravel(), table), text
+        elif status == 4:
+            with pytest.raises(rq.PlanError) as e:
+                rq.plan.resolve(text, 80)
+            want = None if offset == -1 else int(offset)
+            assert e.value.offset == want, (text, e.value.offset, want)
+        else:
+            with pytest.raises(rq.Error):
+                rq.plan.resolve(text, 80)
+
+
+def test_plan_kats():
+    # proj/tests/test_plan.cpp:112-153
+    t, _ = rq.plan.resolve("first:1 modules:1+3+4", 80)
+    assert t[0].tolist() == [8, 4, 8, 8] and (t == 8).sum() == 3
+    t, _ = rq.plan.resolve("middle:2", 6)
+    assert [list(r) for r in t] == [[4] * 4, [4] * 4, [8] * 4, [8] * 4, [4] * 4, [4] * 4]
+    t, _ = rq.plan.resolve("last:3", 10)
+    assert (t == 8).sum() == 12 and t[6, 3] == 4 and t[7, 0] == 8
+    with pytest.raises(rq.PlanError):
+        rq.plan.resolve("first:7", 6)
+    with pytest.raises(rq.PlanError):
+        rq.plan.resolve("explicit:4", 4)
+    # canonical rendering round trip (test_plan.cpp:90-110)
+    for text in ("first:0 modules:1+2+3+4 base:4 high:8", "middle:2 modules:2 base:4 high:8",
+                 "last:7 modules:none base:4 high:8", "explicit:0,5,7 modules:3+4 base:4 high:8"):
+        assert rq.plan.canonical(text) == text
+    assert rq.plan.canonical("explicit:7,0,5") == "explicit:0,5,7 modules:1+2+3+4 base:4 high:8"
+
+
+def test_effective_bits(golden_plan):
+    # uniform manifest: exact 4 / 6 / 5 bits (test_plan.cpp:155-174)
+    rows4, cols4 = [64] * 4, [64] * 4
+    for text, want in (("first:0", 4.0), ("first:8", 8.0), ("first:4", 6.0), ("middle:2", 5.0)):
+        t, _ = rq.plan.resolve(text, 8)
+        assert rq.plan.effective_bits(t, rows4, cols4, 32) == want
+    t, _ = rq.plan.resolve("first:0", 8)
+    assert rq.plan.effective_bits(t, rows4, cols4, 32, include_scales=True) == 4.5
+    # 70B manifest (plan.cpp:275-286): explicit:0 modules:4 and first:1 modules:1+3+4
+    r70 = [8192 + 2048, 8192, 2 * 28672, 8192]
+    c70 = [8192, 8192, 8192, 28672]
+    eff = golden_plan["eff"]
+    t, _ = rq.plan.resolve("explicit:0 modules:4", 80)
+    assert rq.plan.effective_bits(t, r70, c70, 128) == eff[0]
+    assert rq.plan.effective_bits(t, r70, c70, 128, include_scales=True) == eff[1]
+    t, _ = rq.plan.resolve("first:1 modules:1+3+4", 80)
+    e1 = rq.plan.effective_bits(t, r70, c70, 128)
+    assert e1 == eff[2] and abs((e1 - 4.0) - 47.0 / 1020.0) < 1e-12

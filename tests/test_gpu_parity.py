@@ -1,0 +1,254 @@
+"""GPU parity: every rtnq kernel against the oracle and the reference's golden vectors.
+
+Bit-exact: quantize-and-pack (all layouts, f32/f16 scales), relayout, dequantize,
+and the reference-exact GEMMs (gemm_fused / gemm_dequant / gemm_oracle / gemm_float)
+through the host C-ABI.  The tensor-core linear is checked against the f64 oracle
+within the tolerance stated in each test.
+"""
+import numpy as np
+import pytest
+
+import paper_2505_15909_b200 as rq
+from oracle import KERNEL, NATIVE, ROW_MAJOR
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def bf16_exact(x):
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    return (x.view(np.uint32) & 0xFFFF0000).view(np.float32)
+
+
+def rel_frob(x, ref):
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    den = np.sqrt((ref ** 2).sum())
+    num = np.sqrt(((x - ref) ** 2).sum())
+    return num if den == 0 else num / den
+
+
+# ---- host C-ABI (reference-identical results) ------------------------------------------
+
+def test_host_api_matches_golden(golden_qg):
+    for name, z in golden_qg.items():
+        rows, cols, bits, g, ragged, m, tr, tc = (int(v) for v in z["meta"])
+        data, scales = rq.quantize_tensor(z["w"], bits, g, bool(ragged))
+        assert np.array_equal(data, z["data"]), name
+        assert np.array_equal(scales, z["scales"]), name
+        k = rq.reshuffle(data, rq.layout(rq.ROW_MAJOR), rq.layout(rq.KERNEL_INTERLEAVED, tr, tc),
+                         bits, rows, cols)
+        assert np.array_equal(k, z["kernel"]), name
+        back = rq.reshuffle(k, rq.layout(rq.KERNEL_INTERLEAVED, tr, tc), rq.layout(rq.ROW_MAJOR),
+                            bits, rows, cols)
+        assert np.array_equal(back, data), name
+        klay = rq.layout(rq.KERNEL_INTERLEAVED, tr, tc)
+        deq = rq.dequantize_tensor(k, klay, bits, rows, cols, g, scales, bool(ragged))
+        assert np.array_equal(deq, z["deq"]), name
+        a = z["a"]
+        f = rq.gemm_fused(a, k, klay, bits, rows, g, scales, bool(ragged))
+        assert np.array_equal(f.view(np.uint32), z["fused"].view(np.uint32)), name
+        d = rq.gemm_dequant(a, data, rq.layout(rq.ROW_MAJOR), bits, rows, g, scales, bool(ragged))
+        assert np.array_equal(d.view(np.uint32), z["dequant"].view(np.uint32)), name
+        o = rq.gemm_oracle(a, data, rq.layout(rq.ROW_MAJOR), bits, rows, g, scales, bool(ragged))
+        assert np.array_equal(o.view(np.uint32), z["oracle"].view(np.uint32)), name
+
+
+def test_host_api_kats():
+    # test_quant.cpp:33-91, test_packing.cpp:38-58, test_gemm.cpp:61-90
+    assert rq.compute_scale([1.0, -2.0, 3.75], 4) == 0.5
+    assert rq.compute_scale([-7.5], 4) == 1.0
+    assert rq.compute_scale(np.zeros(64), 8) == 1.0
+    for bad in ([], [1.0, np.nan], [np.inf]):
+        with pytest.raises(rq.InvalidInputError):
+            rq.compute_scale(bad, 4)
+    codes, s = rq.quantize_group([1.0, -2.0, 3.75], 4)
+    assert s == 0.5 and codes.tolist() == [2, -4, 7]
+    codes, s = rq.quantize_group([-7.5], 4)
+    assert s == 1.0 and codes.tolist() == [-8]
+    assert rq.dequantize_group([2, -4, 7], 0.5, 4).tolist() == [1.0, -2.0, 3.5]
+    with pytest.raises(rq.CorruptDataError):
+        rq.dequantize_group([9], 1.0, 4)
+    # hand products 15 / -5 through every path
+    logical = np.array([[1, 2, 3, 4], [-4, -3, -2, -1]], np.int8)
+    rm = np.array([0x9A, 0xCB, 0x54, 0x76], np.uint8)  # pack(logical, 4)
+    klay = rq.layout(rq.KERNEL_INTERLEAVED)
+    k = rq.reshuffle(rm, rq.layout(rq.ROW_MAJOR), klay, 4, 2, 4)
+    sc = np.array([[0.5], [0.25]], np.float32)
+    a = np.array([[1, 2, 3, 4]], np.float32)
+    for out in (rq.gemm_fused(a, k, klay, 4, 2, 4, sc), rq.gemm_dequant(a, rm, rq.layout(), 4, 2, 4, sc),
+                rq.gemm_oracle(a, rm, rq.layout(), 4, 2, 4, sc)):
+        assert out.tolist() == [[15.0, -5.0]]
+    del logical
+    # error classes (test_gemm.cpp:174-190)
+    with pytest.raises(rq.ShapeError):
+        rq.gemm_fused(a, rm, rq.layout(), 4, 2, 4, sc)  # row-major into the fused path
+    with pytest.raises(rq.InvalidInputError):
+        rq.gemm_auto(a, k, klay, 4, 2, 4, sc, threshold=0)
+    bad = a.copy()
+    bad[0, 1] = np.nan
+    with pytest.raises(rq.InvalidInputError):
+        rq.gemm_fused(bad, k, klay, 4, 2, 4, sc)
+
+
+def test_gemm_auto_dispatch():
+    # test_gemm.cpp:151-172 / acceptance.cpp:290-307
+    rng = np.random.default_rng(59)
+    w = rng.uniform(-1, 1, (8, 32)).astype(np.float32)
+    data, sc = rq.quantize_tensor(w, 4, 16)
+    klay = rq.layout(rq.KERNEL_INTERLEAVED)
+    k = rq.reshuffle(data, rq.layout(), klay, 4, 8, 32)
+    a1 = rng.uniform(-1, 1, (1023, 32)).astype(np.float32)
+    out, path = rq.gemm_auto(a1, k, klay, 4, 8, 16, sc, 1024)
+    assert path == rq.PATH_FUSED and np.array_equal(out, rq.gemm_fused(a1, k, klay, 4, 8, 16, sc))
+    a2 = rng.uniform(-1, 1, (1024, 32)).astype(np.float32)
+    out, path = rq.gemm_auto(a2, k, klay, 4, 8, 16, sc, 1024)
+    assert path == rq.PATH_DEQUANT_FIRST
+    assert np.array_equal(out, rq.gemm_dequant(a2, k, klay, 4, 8, 16, sc))
+
+
+def test_quantize_random_vs_oracle(oracle):
+    """Bit-exact quantize for shapes on both the fused and the generic path."""
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        bits = 4 if trial % 2 else 8
+        g = int(2 ** rng.integers(0, 9))
+        cols = int(max(g, 128) * rng.integers(1, 4)) if trial % 3 else int(rng.integers(1, 300))
+        ragged = cols % g != 0
+        rows = int(rng.integers(1, 70))
+        amp = float(2.0 ** rng.integers(-20, 20))
+        w = rng.uniform(-amp, amp, (rows, cols)).astype(np.float32)
+        codes, scales = oracle.quantize(w, bits, g, ragged)
+        data, s2 = rq.quantize_tensor(w, bits, g, ragged)
+        assert np.array_equal(s2, scales)
+        assert np.array_equal(data, oracle.pack(codes, bits))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16"])
+@pytest.mark.parametrize("bits,g,rows,cols", [(4, 128, 300, 512), (8, 128, 64, 1024), (4, 32, 48, 256),
+                                               (8, 4096, 40, 4096), (4, 64, 17, 200), (8, 1, 5, 9)])
+def test_device_quantize_pack_all_layouts(oracle, dtype, bits, g, rows, cols):
+    ragged = cols % g != 0
+    tdt = getattr(torch, dtype)
+    gen = torch.Generator(device="cuda").manual_seed(rows * cols + bits)
+    w = (torch.rand(rows, cols, device="cuda", generator=gen) * 2 - 1).to(tdt)
+    w[0, : min(cols, 3)] = 0  # partially-zero group
+    if rows > 2:
+        w[2] = 0  # all-zero groups -> scale 1.0
+    q = rq.quantize_pack(w, bits, g, ragged, native=True, row_major=True, kernel=True,
+                         scales_f32=True, scales_f16=True)
+    wf = w.float().cpu().numpy()
+    codes, scales = oracle.quantize(wf, bits, g, ragged)
+    assert np.array_equal(q.scales_f32.cpu().numpy(), scales)
+    s16 = oracle.f16_round(scales)
+    assert np.array_equal(q.scales_f16.cpu().numpy().view(np.uint16), s16)
+    assert np.array_equal(q.codes_row_major.cpu().numpy(), oracle.pack(codes, bits))
+    assert np.array_equal(q.codes_kernel.cpu().numpy(), oracle.encode(codes, bits, KERNEL))
+    assert np.array_equal(q.codes.cpu().numpy(), oracle.encode(codes, bits, NATIVE))
+    gpr = scales.shape[1]
+    assert np.array_equal(q.scales.cpu().numpy().view(np.uint16), oracle.native_scales(s16, rows, gpr))
+    # device relayout row-major -> native equals the kernel's native output
+    nat = rq.relayout(q.codes_row_major, rq.layout(rq.ROW_MAJOR), rq.layout(rq.NATIVE), bits, rows, cols)
+    assert torch.equal(nat, q.codes)
+    ns = rq.native_scales(q.scales_f32, rows, gpr)
+    assert torch.equal(ns, q.scales)
+
+
+def test_quantize_flags_non_finite():
+    w = torch.ones(16, 128, device="cuda")
+    w[3, 7] = float("nan")
+    with pytest.raises(rq.InvalidInputError):
+        rq.quantize_pack(w, 4, 128)
+    w[3, 7] = float("inf")
+    with pytest.raises(rq.InvalidInputError):
+        rq.quantize_pack(w, 8, 32)
+
+
+def test_dequantize_native_bf16(oracle):
+    rows, cols, bits, g = 64, 256, 4, 64
+    w = torch.randn(rows, cols, device="cuda")
+    q = rq.quantize_pack(w, bits, g, scales_f32=True)
+    out = rq.dequantize(q.codes, rq.layout(rq.NATIVE), bits, rows, cols, g, q.scales, rq.F16,
+                        rq.SCALES_NATIVE, torch.float32)
+    codes, scales = oracle.quantize(w.cpu().numpy(), bits, g)
+    s16 = oracle.f16_round(scales).view(np.float16).astype(np.float32)
+    assert np.array_equal(out.cpu().numpy(), oracle.dequantize(codes, s16, g))
+
+
+# ---- tensor-core linear ------------------------------------------------------------------
+
+def _make(oracle, n, k, bits, g, seed, ragged=False):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    w = ((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+    q = rq.quantize_pack(w, bits, g, ragged)
+    codes, scales = oracle.quantize(w.float().cpu().numpy(), bits, g, ragged)
+    s16w = oracle.f16_round(scales).view(np.float16).astype(np.float32)
+    return q, codes, s16w
+
+
+TOL = 1e-5  # rel. Frobenius vs the f64 oracle (reference gate 1e-4, acceptance.cpp:281-282)
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("m", [1, 3, 8, 16, 17, 32, 64, 80])
+def test_linear_tensor_core_vs_oracle(oracle, bits, m):
+    n, k, g = 528, 1024, 128
+    q, codes, s16w = _make(oracle, n, k, bits, g, seed=m * 7 + bits)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+    out = rq.linear(a, q, out_dtype=torch.float32)
+    ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+    assert rel_frob(out.cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("bits,g,k,act", [(4, 16, 256, "bfloat16"), (4, 32, 512, "float16"),
+                                          (4, 64, 192, "bfloat16"), (8, 16, 96, "float16"),
+                                          (8, 32, 320, "bfloat16"), (8, 8192, 4096, "bfloat16"),
+                                          (4, 4096, 1024, "float16"), (8, 512, 1536, "float16")])
+def test_linear_groups_dtypes(oracle, bits, g, k, act):
+    n, m = 200, 5
+    q, codes, s16w = _make(oracle, n, k, bits, g, seed=k + g, ragged=k % g != 0)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(getattr(torch, act))
+    for odt in (torch.float32, torch.bfloat16, torch.float16):
+        out = rq.linear(a, q, out_dtype=odt)
+        ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+        tol = TOL if odt == torch.float32 else 8e-3  # one 16-bit output rounding
+        assert rel_frob(out.float().cpu().numpy(), ref) <= tol, odt
+
+
+def test_linear_deterministic_and_split_invariant(oracle, monkeypatch):
+    n, k, bits, g, m = 4096, 4096, 4, 128, 16
+    q, codes, s16w = _make(oracle, n, k, bits, g, seed=1)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+    o1 = rq.linear(a, q, out_dtype=torch.float32)
+    o2 = rq.linear(a, q, out_dtype=torch.float32)
+    assert torch.equal(o1, o2)  # run-to-run bit identity (deterministic stream-K fixup)
+    for ctas in ("1", "7", "64", "300"):
+        monkeypatch.setenv("RTNQ_WGEMM_CTAS", ctas)
+        ws = rq.Workspace(device="cuda")
+        o3 = rq.linear(a, q, out_dtype=torch.float32, workspace=ws)
+        assert rel_frob(o3.cpu().numpy(), o1.cpu().numpy()) <= 1e-6, ctas
+    ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+    assert rel_frob(o1.cpu().numpy(), ref) <= TOL
+
+
+LLAMA_8B = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "down": (4096, 14336)}
+
+
+@pytest.mark.parametrize("name", list(LLAMA_8B))
+@pytest.mark.parametrize("bits", [4, 8])
+def test_linear_llama_shapes_vs_dequant_reference(name, bits):
+    """Full-size Llama-3.1-8B shapes: compare against a torch f64 GEMM over the
+    exactly dequantized weights (size-independent check: same math, f64 sums)."""
+    n, k = LLAMA_8B[name]
+    g = 128 if bits == 4 else k  # W8 per-channel, as in BASELINE config 3
+    w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
+    q = rq.quantize_pack(w, bits, g, ragged=False)
+    wd = rq.dequantize(q.codes, rq.layout(rq.NATIVE), bits, n, k, g, q.scales, rq.F16,
+                       rq.SCALES_NATIVE, torch.float32)
+    for m in (1, 4, 16):
+        a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+        out = rq.linear(a, q, out_dtype=torch.float32)
+        ref = a.double() @ wd.double().t()
+        err = ((out.double() - ref).norm() / ref.norm()).item()
+        assert err <= TOL, (name, bits, m, err)
