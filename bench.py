@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- W4/W8 weight-only GEMM weight-streaming throughput on B200.
+
+Workload (BASELINE.json configs[1]): the four linears of every Llama-3.1-8B
+decoder layer (32 layers x {qkv 6144x4096, o 4096x4096, gate_up 28672x4096,
+down 4096x14336}), W4A16 g128 (or W8A16 per-channel with --bits 8), bf16
+activations, one decode batch per step.  A step streams all 32 x 112.46 MB of
+packed weights once (3.6 GB >> 126 MB L2, so no L2 flush is needed between
+steps).  value = algorithmic weight bytes (codes + f16 scales) / step time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--bits 4|8]
+  python bench.py --impl reference     # the reference CPU gemm_fused, same metric
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §6 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LLAMA8B = [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]
+LAYERS = 32
+METRIC = "W4/W8 GEMM weight HBM GB/s (% of peak) at batch 1-16; decode layer us/token"
+
+
+def group_for(bits):
+    """W4: g128 (configs[1]); W8: per-channel = one group per row (configs[2]),
+    expressed like the reference as the next power of two >= k, ragged."""
+    if bits == 4:
+        return lambda k: 128
+    return lambda k: 1 << (k - 1).bit_length()
+
+
+def weight_bytes(n, k, bits, g):
+    gpr = -(-k // g)
+    return n * k * bits // 8 + n * gpr * 2
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Polls SM clocks and throttle reasons through NVML during the timed region."""
+
+    def __init__(self, index=0, period=0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.index = period, index
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {
+                getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+                getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+                getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+                getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+                getattr(N, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for bit, name in names.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML missing: report nothing rather than guess
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def ncu_traffic(bits, batch):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"w{bits}_m{batch}")
+
+
+# ---------------------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_15909_b200 as rq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    bits, B = args.bits, args.batch
+    g_of = group_for(bits)
+
+    # ---- weights: synthetic bf16, quantized + packed on the GPU (our own kernel) ----
+    torch.manual_seed(1234 + rank)
+    layers = []
+    for li in range(LAYERS):
+        mods = []
+        for name, n, k in LLAMA8B:
+            w = ((torch.rand(n, k, device=dev) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+            mods.append(rq.quantize_pack(w, bits, g_of(k), ragged=k % g_of(k) != 0,
+                                         check=(li == 0)))
+            del w
+        layers.append(mods)
+    torch.cuda.synchronize()
+    step_bytes = sum(weight_bytes(n, k, bits, g_of(k)) for _, n, k in LLAMA8B) * LAYERS
+
+    x = torch.empty(B, 4096, device=dev).uniform_(-1, 1).to(torch.bfloat16)
+    h = torch.empty(B, 14336, device=dev).uniform_(-1, 1).to(torch.bfloat16)
+    outs = {name: torch.empty(B, n, device=dev, dtype=torch.bfloat16) for name, n, _ in LLAMA8B}
+    ws = rq.Workspace(device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for mods in layers:
+            for (name, n, k), q in zip(LLAMA8B, mods):
+                rq.linear(x if k == 4096 else h, q, out=outs[name], workspace=ws, stream=stream,
+                          pdl=args.pdl)
+
+    # warm up once eagerly (sizes the workspace), then capture one step in a CUDA graph
+    with torch.cuda.stream(stream):
+        step()
+    stream.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    launches_per_step = LAYERS * len(LLAMA8B) * (-(-B // 64))
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms / steps
+
+    def replay(gr):
+        with torch.cuda.stream(stream):  # CUDAGraph.replay() uses the current stream
+            gr.replay()
+
+    with ClockSampler(local) as clk:
+        ms = timed(lambda: replay(graph), args.steps, args.warmup)
+    value = step_bytes * world / (ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+
+    # per-batch sweep (same graph structure, re-captured per batch)
+    sweep = {}
+    for b in args.sweep:
+        if b == B:
+            sweep[str(b)] = round(value / world, 1)
+            continue
+        xb = torch.empty(b, 4096, device=dev).uniform_(-1, 1).to(torch.bfloat16)
+        hb = torch.empty(b, 14336, device=dev).uniform_(-1, 1).to(torch.bfloat16)
+        ob = {name: torch.empty(b, n, device=dev, dtype=torch.bfloat16) for name, n, _ in LLAMA8B}
+
+        def stepb():
+            for mods in layers:
+                for (name, n, k), q in zip(LLAMA8B, mods):
+                    rq.linear(xb if k == 4096 else hb, q, out=ob[name], workspace=ws,
+                              stream=stream, pdl=args.pdl)
+        with torch.cuda.stream(stream):
+            stepb()
+        stream.synchronize()
+        gb = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gb, stream=stream):
+            stepb()
+        msb = timed(lambda: replay(gb), max(3, args.steps // 2), args.warmup)
+        sweep[str(b)] = round(step_bytes / (msb * 1e-3) / 1e9, 1)
+
+    # ---- e2e: pinned host activations in, host outputs back, through the public API ----
+    hx = torch.empty(B, 4096, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory()
+    hh = torch.empty(B, 14336, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory()
+    hout = {name: torch.empty(B, n, dtype=torch.bfloat16).pin_memory() for name, n, _ in LLAMA8B}
+    h2d = (hx.numel() + hh.numel()) * 2
+    d2h = sum(t.numel() for t in hout.values()) * 2
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            x.copy_(hx, non_blocking=True)
+            h.copy_(hh, non_blocking=True)
+            graph.replay()
+            for name, t in hout.items():
+                t.copy_(outs[name], non_blocking=True)
+
+    ms_e2e = timed(e2e_step, args.steps, args.warmup)
+    e2e = step_bytes * world / (ms_e2e * 1e-3) / 1e9
+
+    # dominant kernel = the tensor-core GEMM: every launch in the step is one of them
+    per_launch_bytes = step_bytes / (LAYERS * len(LLAMA8B))
+    achieved = step_bytes / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"u{bits} weights x bf16 activations, f32 accumulate", "data": "synthetic",
+        "config": {"workload": f"Llama-3.1-8B decoder-layer linears x{LAYERS} layers, W{bits}A16 "
+                               f"{'g128' if bits == 4 else 'per-channel'}, decode batch {B}",
+                   "batch": B, "layers": LAYERS, "bits": bits,
+                   "group": 128 if bits == 4 else "per-channel",
+                   "weight_bytes_per_step": step_bytes,
+                   "l2": "inputs larger than L2 (3.6 GB of weights per step), no flush",
+                   "parallelism": f"dp{world} (independent replicas)" if world > 1 else "single GPU",
+                   "pct_of_hbm_peak": round(100 * achieved / peak, 1),
+                   "sweep_gbs_by_batch": sweep},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(bits, B), "peak_source": peak_src,
+                     "kernel": "rtnq_b200::wg::wgemm_kernel",
+                     "algorithmic_bytes_per_launch": round(per_launch_bytes)},
+        "e2e": {"value": round(e2e, 1), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, layers_cpu=layers[0], bits=bits, B=B, g_of=g_of)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, layers_cpu, bits, B, g_of, budget_s=None):
+    """Reference gemm_fused (oracle/_ref) on the host cores, one layer's 4 linears per rep."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import KERNEL, Ref
+
+    if not Ref.available():
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref/librtnq_ref.so not built"}
+    import paper_2505_15909_b200 as rq
+    ref = Ref()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    budget = budget_s if budget_s is not None else args.cpu_seconds
+    # weights in the reference's own kernel_interleaved(16,4) layout + f32 scales,
+    # produced bit-exactly by our quantize kernel (the reference's reshuffle of a
+    # whole 8B layer takes ~3.5 s on 8 cores; its output is identical)
+    prep = []
+    for (name, n, k) in LLAMA8B:
+        w = ((torch.rand(n, k, device="cuda") * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+        q = rq.quantize_pack(w, bits, g_of(k), ragged=k % g_of(k) != 0, native=False, kernel=True,
+                             scales_f32=True)
+        prep.append((n, k, q.codes_kernel.cpu().numpy(), q.scales_f32.cpu().numpy()))
+    rng = np.random.default_rng(0)
+    acts = {k: rng.uniform(-1, 1, (B, k)).astype(np.float32) for k in (4096, 14336)}
+    nbytes, t0, reps = 0, time.perf_counter(), 0
+    while True:
+        for n, k, kern, sc in prep:
+            ref.gemm("fused", acts[k], kern, n, bits, g_of(k), sc, KERNEL, ragged=k % g_of(k) != 0)
+            nbytes += weight_bytes(n, k, bits, g_of(k))
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= budget or reps >= 50:
+            break
+    return {"value": round(nbytes / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"{reps} x (4 Llama-3.1-8B layer linears, batch {B}) through the reference "
+                      f"gemm_fused, set_threads({cores}), {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation, same metric/config."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import KERNEL, Ref
+    bits, B = args.bits, args.batch
+    g_of = group_for(bits)
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/librtnq_ref.so was not built (needs /root/reference)"}))
+        return
+    ref = Ref()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    rng = np.random.default_rng(0)
+    prep = []
+    for (name, n, k) in LLAMA8B:  # reference quantize + reshuffle, untimed (model load)
+        w = (rng.uniform(-1, 1, (n, k)) * (3.0 / k) ** 0.5).astype(np.float32)
+        rg = k % g_of(k) != 0
+        data, sc = ref.quantize(w, bits, g_of(k), rg)
+        kern = ref.reshuffle(data, n, k, bits, g_of(k), sc, 0, KERNEL, ragged=rg)
+        prep.append((n, k, kern, sc))
+    acts = {k: rng.uniform(-1, 1, (B, k)).astype(np.float32) for k in (4096, 14336)}
+    step_bytes = sum(weight_bytes(n, k, bits, g_of(k)) for _, n, k in LLAMA8B)
+
+    def step():
+        for n, k, kern, sc in prep:
+            ref.gemm("fused", acts[k], kern, n, bits, g_of(k), sc, KERNEL, ragged=k % g_of(k) != 0)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = step_bytes / dt / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 activations, u4/u8 codes (reference CPU)",
+        "data": "synthetic",
+        "config": {"workload": f"Llama-3.1-8B decoder-layer linears, W{bits}A16, decode batch {B}; "
+                               "each reference step = one layer's 4 linears (bounded sample)",
+                   "batch": B, "bits": bits},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} steps x one layer's 4 linears via gemm_fused"},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--bits", type=int, default=4, choices=(4, 8))
+    ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",")], default=[1, 4, 16])
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pdl", dest="pdl", action="store_false",
+                    help="launch the GEMMs without programmatic dependent launch")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        args.steps = min(args.steps, 5)
+        args.warmup = min(args.warmup, 1)
+        return run_reference(args)
+    run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -154,6 +154,20 @@ rtnq_status rtnq_dev_linear(const void* a, int a_dtype, int64_t m, int64_t k,
                             int64_t threshold, int* chosen, int32_t* err_flag, void* workspace,
                             size_t workspace_bytes, void* stream);
 
+/* rtnq_dev_linear with launch flags.  RTNQ_FLAG_PDL launches the tensor-core
+ * kernel with programmatic dependent launch: its weight prefetch starts before
+ * the previous kernel in the stream finishes (only activations wait), so the
+ * caller asserts that the previous kernel does not write this weight's codes or
+ * scales -- true for every linear of a decode step. */
+#define RTNQ_FLAG_PDL 1u
+rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
+                               const uint8_t* codes, rtnq_layout layout, int bits, int64_t n,
+                               int64_t g, int ragged, const void* scales, int scales_dtype,
+                               int scales_order, void* out, int out_dtype, int path,
+                               int64_t threshold, int* chosen, int32_t* err_flag,
+                               void* workspace, size_t workspace_bytes, void* stream,
+                               unsigned flags);
+
 /* gemm_float (gemm.cpp:111-119): dense f32 weights, blocked accumulation. */
 rtnq_status rtnq_dev_gemm_float(const float* a, int64_t m, int64_t k, const float* w, int64_t n,
                                 int64_t block, float* out, void* stream);

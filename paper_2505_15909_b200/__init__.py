@@ -83,6 +83,9 @@ def lib():
     L.rtnq_dev_linear_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _i64, _i32, Layout]
     L.rtnq_dev_linear.argtypes = [_p, _i32, _i64, _i64, _p, Layout, _i32, _i64, _i64, _i32, _p,
                                   _i32, _i32, _p, _i32, _i32, _i64, _p, _p, _p, _sz, _p]
+    L.rtnq_dev_linear_ex.argtypes = [_p, _i32, _i64, _i64, _p, Layout, _i32, _i64, _i64, _i32,
+                                     _p, _i32, _i32, _p, _i32, _i32, _i64, _p, _p, _p, _sz, _p,
+                                     C.c_uint]
     L.rtnq_dev_gemm_float.argtypes = [_p, _i64, _i64, _p, _i64, _i64, _p, _p]
     L.rtnq_dev_check_flag.argtypes = [_p, _p]
     L.rtnq_device_info.argtypes = [_p, _p, _p]
@@ -247,11 +250,17 @@ class Workspace:
 _default_ws = {}
 
 
-def linear(a, qw: QuantWeight, out=None, out_dtype=None, *, path=PATH_FUSED,
-           threshold=DEFAULT_THRESHOLD, workspace: Workspace | None = None, stream=None):
-    """out[m, n] = a[m, k] @ W^T with W = codes * scales (rtnq_dev_linear).
+FLAG_PDL = 1
 
-    The tensor-core path runs for bf16/f16 ``a`` against the native layout."""
+
+def linear(a, qw: QuantWeight, out=None, out_dtype=None, *, path=PATH_FUSED,
+           threshold=DEFAULT_THRESHOLD, workspace: Workspace | None = None, stream=None,
+           pdl=False):
+    """out[m, n] = a[m, k] @ W^T with W = codes * scales (rtnq_dev_linear_ex).
+
+    The tensor-core path runs for bf16/f16 ``a`` against the native layout.
+    ``pdl=True`` lets the weight prefetch overlap the previous kernel (the caller
+    asserts that kernel does not write this weight)."""
     torch = _torch()
     assert a.is_cuda and a.dim() == 2 and a.is_contiguous() and a.shape[1] == qw.cols
     m = a.shape[0]
@@ -263,10 +272,11 @@ def linear(a, qw: QuantWeight, out=None, out_dtype=None, *, path=PATH_FUSED,
         workspace = _default_ws.setdefault(a.device, Workspace(wsb, a.device))
     buf = workspace.ensure(wsb)
     chosen = C.c_int(-1)
-    _check(lib().rtnq_dev_linear(
+    _check(lib().rtnq_dev_linear_ex(
         _ptr(a), _dt(a), m, qw.cols, _ptr(qw.codes), lay, qw.bits, qw.rows, qw.group,
         int(qw.ragged), _ptr(qw.scales), F16, SCALES_NATIVE, _ptr(out), _dt(out), path,
-        threshold, C.byref(chosen), None, _ptr(buf), buf.numel(), _stream(stream)))
+        threshold, C.byref(chosen), None, _ptr(buf), buf.numel(), _stream(stream),
+        FLAG_PDL if pdl else 0))
     return out
 
 

@@ -252,6 +252,17 @@ rtnq_status rtnq_dev_linear(const void* a, int a_dtype, int64_t m, int64_t k,
                             int64_t g, int ragged, const void* scales, int sdtype, int sorder,
                             void* out, int odtype, int path, int64_t threshold, int* chosen,
                             int32_t* err, void* ws, size_t ws_bytes, void* stream) {
+    return rtnq_dev_linear_ex(a, a_dtype, m, k, codes, layout, bits, n, g, ragged, scales, sdtype,
+                              sorder, out, odtype, path, threshold, chosen, err, ws, ws_bytes,
+                              stream, 0u);
+}
+
+rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
+                               const uint8_t* codes, rtnq_layout layout, int bits, int64_t n,
+                               int64_t g, int ragged, const void* scales, int sdtype, int sorder,
+                               void* out, int odtype, int path, int64_t threshold, int* chosen,
+                               int32_t* err, void* ws, size_t ws_bytes, void* stream,
+                               unsigned flags) {
     if (!valid_bits(bits)) return fail(RTNQ_E_INVALID_INPUT, "bits must be 4 or 8");
     RTNQ_TRY(check_layout(layout));
     if (m < 0 || n < 0 || k < 0) return fail(RTNQ_E_SHAPE, "negative tensor dimension");
@@ -273,8 +284,11 @@ rtnq_status rtnq_dev_linear(const void* a, int a_dtype, int64_t m, int64_t k,
         if (ws_bytes < need)
             return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " +
                                                   std::to_string(need) + " bytes");
+        if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(codes) |
+             reinterpret_cast<uintptr_t>(scales)) & 15)
+            return fail(RTNQ_E_INVALID_INPUT, "tensor-core path needs 16-byte aligned operands");
         WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
-                    out, odtype, ws, ws_bytes};
+                    out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
         RTNQ_CUDA(launch_wgemm(A, st));
         return RTNQ_OK;
     }

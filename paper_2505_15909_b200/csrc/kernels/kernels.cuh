@@ -57,6 +57,7 @@ struct WgemmArgs {
     int out_dtype;
     void* workspace;
     size_t ws_bytes;
+    bool pdl;              // launch with programmatic dependent launch (RTNQ_FLAG_PDL)
 };
 // Validates the shape for the tensor-core path; returns a message or nullptr.
 const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);

@@ -524,6 +524,11 @@ const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t
     return nullptr;
 }
 
+// Workspace: [counters: fixed 64 KiB][stream-K partial slots].  The counters sit
+// at a fixed offset so that, whatever shapes share one workspace, partial data
+// never lands on a counter (they self-reset to zero and must start at zero).
+constexpr size_t kCounterBytes = 64 * 1024;  // 16384 row-blocks (>= 2M channels)
+
 size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t g) {
     (void)g;
     const int64_t kb = native_kblock(bits);
@@ -532,8 +537,7 @@ size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t 
     const int64_t NS = (n + 15) / 16, NB = (NS + strips - 1) / strips;
     const int64_t U = NB * (k / kb > 0 ? k / kb : 1);
     const int G = wg::ctas_for(U);
-    const size_t counters = size_t(((NS + 7) / 8 * 4 + 255) / 256 * 256);
-    return counters + size_t(G) * 2 * 256 * (mt * nt8 * 4) * sizeof(float);
+    return kCounterBytes + size_t(G) * 2 * 256 * (mt * nt8 * 4) * sizeof(float);
 }
 
 cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
@@ -548,7 +552,8 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
     p.KBLK = A.k / kb;
     p.out_dtype = A.out_dtype;
     p.counters = static_cast<int*>(A.workspace);
-    const bool pdl = std::getenv("RTNQ_NO_PDL") == nullptr;
+    p.partials = reinterpret_cast<float*>(static_cast<char*>(A.workspace) + kCounterBytes);
+    if ((p.NS + 7) / 8 > int64_t(kCounterBytes / 4)) return cudaErrorInvalidValue;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
     for (int64_t m0 = 0; m0 < A.m; m0 += 64) {  // decode batches: one pass per 64 tokens
         p.M = A.m - m0 < 64 ? A.m - m0 : 64;
@@ -558,9 +563,9 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
         p.NB = (p.NS + strips - 1) / strips;
         p.U = p.NB * p.KBLK;
         p.G = wg::ctas_for(p.U);
-        const int64_t nb_max = (p.NS + 7) / 8;  // counters sized for the smallest row-block
-        p.partials = reinterpret_cast<float*>(static_cast<char*>(A.workspace) +
-                                              (nb_max * 4 + 255) / 256 * 256);
+        // PDL only between chunks of this call or when the caller vouches that the
+        // previous kernel in the stream does not write this layer's weights.
+        const bool pdl = A.pdl || m0 > 0;
         cudaError_t e;
         if (A.bits == 4)
             e = A.a_dtype == RTNQ_BF16 ? wg::launch_bits<4, RTNQ_BF16>(p, nt8, st, pdl)

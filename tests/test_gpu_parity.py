@@ -72,7 +72,7 @@ def test_host_api_kats():
         rq.dequantize_group([9], 1.0, 4)
     # hand products 15 / -5 through every path
     logical = np.array([[1, 2, 3, 4], [-4, -3, -2, -1]], np.int8)
-    rm = np.array([0x9A, 0xCB, 0x54, 0x76], np.uint8)  # pack(logical, 4)
+    rm = np.array([0xA9, 0xCB, 0x54, 0x76], np.uint8)  # pack(logical, 4)
     klay = rq.layout(rq.KERNEL_INTERLEAVED)
     k = rq.reshuffle(rm, rq.layout(rq.ROW_MAJOR), klay, 4, 2, 4)
     sc = np.array([[0.5], [0.25]], np.float32)
@@ -241,9 +241,9 @@ def test_linear_llama_shapes_vs_dequant_reference(name, bits):
     """Full-size Llama-3.1-8B shapes: compare against a torch f64 GEMM over the
     exactly dequantized weights (size-independent check: same math, f64 sums)."""
     n, k = LLAMA_8B[name]
-    g = 128 if bits == 4 else k  # W8 per-channel, as in BASELINE config 3
+    g = 128 if bits == 4 else 1 << (k - 1).bit_length()  # W8 per-channel (configs[2])
     w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
-    q = rq.quantize_pack(w, bits, g, ragged=False)
+    q = rq.quantize_pack(w, bits, g, ragged=k % g != 0)
     wd = rq.dequantize(q.codes, rq.layout(rq.NATIVE), bits, n, k, g, q.scales, rq.F16,
                        rq.SCALES_NATIVE, torch.float32)
     for m in (1, 4, 16):
