@@ -37,6 +37,9 @@ constexpr int kThreads = (kConsumerWarps + 1) * 32;
 // row-blocks halve activation re-reads), 1 above (keeps the f32 block + group
 // accumulators of 4..8 n8 tiles in registers: 9 warps leave 168 regs/thread).
 __host__ __device__ constexpr int mt_for(int nt8) { return nt8 <= 2 ? 2 : 1; }
+// Two co-resident CTAs per SM (two producer warps, twice the bytes in flight)
+// while the accumulators fit in 96 registers; one CTA for 64-token batches.
+__host__ __device__ constexpr int ctas_per_sm(int nt8) { return nt8 >= 8 ? 1 : 2; }
 
 struct Params {
     const void* a;
@@ -45,10 +48,18 @@ struct Params {
     void* out;
     float* partials;
     int* counters;
-    int64_t M, N, K, g;
-    int64_t NS, NB, KBLK, U;
-    int G;
+    int64_t N, K;
+    int M;            // tokens in this launch (<= 64)
+    int NS;           // 16-row strips (ceil(N / 16))
+    int NB;           // row-blocks (ceil(NS / STRIPS))
+    int KBLK;         // k-blocks (K / KB)
+    int U;            // units = NB * KBLK
+    int G;            // CTAs
     int out_dtype;
+    int scale_groups;   // scale groups per stage: 1 (g >= KB) or KB / g
+    int steps_per_group;  // k16 steps per group when g < KB, else 0
+    int kb_group_mask;  // g >= KB and g < K: g/KB - 1 (flush when (kb+1) & mask == 0); -1: never
+    int kb_per_group_shift;  // log2(g / KB) when g >= KB and g < K
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------
@@ -220,10 +231,10 @@ __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
 }
 
 template <int BITS, int AT, int NT8, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const Params p) {
     using GG = Geo<BITS, NT8, STAGES>;
     constexpr int KB = GG::KB, STEPS = GG::STEPS, MT = GG::MT, STRIPS = GG::STRIPS;
-    constexpr int kCodeBytes = GG::CODE_BYTES, kStripsPerBlock = STRIPS, kBlockRows = GG::ROWS;
+    constexpr int CODE_BYTES = GG::CODE_BYTES, ROWS = GG::ROWS;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * GG::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
@@ -231,11 +242,11 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
-    const int64_t u0 = int64_t(c) * p.U / p.G, u1 = int64_t(c + 1) * p.U / p.G;
+    const int u0 = int(int64_t(c) * p.U / p.G), u1 = int(int64_t(c + 1) * p.U / p.G);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1 + 32);  // producer expect_tx + 32 lanes' cp.async arrivals
             mbar_init(&empty[s], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -244,47 +255,67 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
     grid_dep_launch();
 
     if (warp == kConsumerWarps) {
-        // ===================== producer warp =====================
-        const int64_t n_units = u1 - u0;
-        const int prologue = int(n_units < STAGES ? n_units : STAGES);
-        auto stage_ptr = [&](int s) { return smem + s * GG::STAGE_BYTES; };
-        auto weights = [&](int64_t u, int s) {
-            const int64_t b = u / p.KBLK, kb = u % p.KBLK;
-            const int strips = int(min(int64_t(kStripsPerBlock), p.NS - b * int64_t(kStripsPerBlock)));
-            uint8_t* st = stage_ptr(s);
-            if (lane == 0) {
-                const uint32_t bytes = uint32_t(strips * 512 + (p.g >= KB ? 1 : KB / p.g) * strips * 32 +
-                                                p.M * KB * 2);
-                mbar_expect_tx(&full[s], bytes);
-            }
-            __syncwarp();
-            if (lane == 0)
-                bulk_g2s(st, p.codes + (kb * p.NS + b * kStripsPerBlock) * 512,
-                         uint32_t(strips * 512), &full[s]);
-            const int ng = p.g >= KB ? 1 : int(KB / p.g);
-            if (lane >= 1 && lane <= ng) {
-                const int q = lane - 1;
-                const int64_t grp = p.g >= KB ? (kb * KB) / p.g : kb * ng + q;
-                bulk_g2s(st + kCodeBytes + q * STRIPS * 32,
-                         p.scales + (grp * p.NS + b * kStripsPerBlock) * 16,
-                         uint32_t(strips * 32), &full[s]);
+        // ===================== producer warp (all 32 lanes issue copies) =====================
+        const int n_units = u1 - u0;
+        const int prologue = n_units < STAGES ? n_units : STAGES;
+        const uint32_t act_bytes = uint32_t(KB * 2);
+        const int64_t a_row = p.K * 2;
+        // Codes + scales: one TMA bulk copy each (a bulk-copy instruction costs ~70
+        // cycles of producer issue, so a stage uses as few as possible).
+        auto weights = [&](int b, int kb, int s) {
+            if (lane != 0) return;
+            const int strips = min(STRIPS, p.NS - b * STRIPS);
+            uint8_t* st = smem + s * GG::STAGE_BYTES;
+            mbar_expect_tx(&full[s], uint32_t(strips * 512 + p.scale_groups * strips * 32));
+            bulk_g2s(st, p.codes + (int64_t(kb) * p.NS + b * STRIPS) * 512, uint32_t(strips * 512),
+                     &full[s]);
+            for (int q = 0; q < p.scale_groups; ++q) {
+                const int64_t grp = p.steps_per_group ? int64_t(kb) * p.scale_groups + q
+                                    : (p.kb_group_mask < 0 ? 0 : kb >> p.kb_per_group_shift);
+                bulk_g2s(st + CODE_BYTES + q * STRIPS * 32,
+                         p.scales + (grp * p.NS + b * STRIPS) * 16, uint32_t(strips * 32),
+                         &full[s]);
             }
         };
-        auto acts = [&](int64_t u, int s) {
-            const int64_t kb = u % p.KBLK;
-            uint8_t* dst = stage_ptr(s) + kCodeBytes + GG::SCALE_BYTES;
-            const uint8_t* src = static_cast<const uint8_t*>(p.a) + kb * KB * 2;
-            for (int64_t r = lane; r < p.M; r += 32)
-                bulk_g2s(dst + r * GG::ASTRIDE, src + r * p.K * 2, uint32_t(KB * 2), &full[s]);
+        // Activations: 16-byte cp.async (LDGSTS) per lane -- M rows x KB*2 bytes is
+        // too fragmented for bulk copies.  Each lane then arms the stage's mbarrier
+        // to fire when its copies land (cp.async.mbarrier.arrive.noinc).
+        auto acts = [&](int kb, int s) {
+            const uint32_t dst = smem_u32(smem + s * GG::STAGE_BYTES + CODE_BYTES + GG::SCALE_BYTES);
+            const uint8_t* src = static_cast<const uint8_t*>(p.a) + int64_t(kb) * (KB * 2);
+            constexpr int CHUNKS = KB * 2 / 16;  // 16-byte chunks per row
+            for (int i = lane; i < p.M * CHUNKS; i += 32) {
+                const int r = i / CHUNKS, ch = i % CHUNKS;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 dst + r * GG::ASTRIDE + ch * 16),
+                             "l"(src + r * a_row + ch * 16)
+                             : "memory");
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                             smem_u32(&full[s]))
+                         : "memory");
         };
-        for (int it = 0; it < prologue; ++it) weights(u0 + it, it);
+        {
+            int b = u0 / p.KBLK, kb = u0 - b * p.KBLK;
+            for (int it = 0; it < prologue; ++it) {
+                weights(b, kb, it);
+                if (++kb == p.KBLK) kb = 0, ++b;
+            }
+        }
         grid_dep_wait();  // activations are produced by the previous kernel
-        for (int it = 0; it < prologue; ++it) acts(u0 + it, it);
-        for (int64_t it = prologue; it < n_units; ++it) {
-            const int s = int(it % STAGES);
-            mbar_wait(&empty[s], uint32_t(((it / STAGES) - 1) & 1));
-            weights(u0 + it, s);
-            acts(u0 + it, s);
+        int b = u0 / p.KBLK, kb = u0 - b * p.KBLK;
+        for (int it = 0; it < prologue; ++it) {
+            acts(kb, it);
+            if (++kb == p.KBLK) kb = 0, ++b;
+        }
+        int s = prologue % STAGES;
+        uint32_t phase = prologue == STAGES ? 0u : 1u;  // parity of the empty phase to await
+        for (int it = prologue; it < n_units; ++it) {
+            mbar_wait(&empty[s], phase);
+            weights(b, kb, s);
+            acts(kb, s);
+            if (++kb == p.KBLK) kb = 0, ++b;
+            if (++s == STAGES) s = 0, phase ^= 1u;
         }
         return;
     }
@@ -292,7 +323,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
     // ===================== consumer warps =====================
     const int gid = lane >> 2, tig = lane & 3;
     float acc[MT][NT8][4], blk[MT][NT8][4];
-    int64_t cur_b = -1, seg_kb0 = 0;
 
     auto zero = [](float (&x)[MT][NT8][4]) {
 #pragma unroll
@@ -304,8 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
     };
 
     // Row-block epilogue: direct store, or partial + deterministic last-arriver combine.
-    auto epilogue = [&](int64_t b, int64_t kb_begin, int64_t kb_end) {
-        const int strips = int(min(int64_t(kStripsPerBlock), p.NS - b * int64_t(kStripsPerBlock)));
+    auto epilogue = [&](int b, bool sole_owner) {
+        const int strips = min(STRIPS, p.NS - b * STRIPS);
         auto write = [&](float (&v)[MT][NT8][4]) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
@@ -315,13 +345,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
                 for (int nt = 0; nt < NT8; ++nt)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const int64_t n = b * kBlockRows + strip * 16 + gid + 8 * (i >> 1);
-                        const int64_t m = nt * 8 + 2 * tig + (i & 1);
-                        if (n < p.N && m < p.M) store_out(p.out, p.out_dtype, m * p.N + n, v[mt][nt][i]);
+                        const int64_t n = int64_t(b) * ROWS + strip * 16 + gid + 8 * (i >> 1);
+                        const int m = nt * 8 + 2 * tig + (i & 1);
+                        if (n < p.N && m < p.M)
+                            store_out(p.out, p.out_dtype, int64_t(m) * p.N + n, v[mt][nt][i]);
                     }
             }
         };
-        if (kb_begin == 0 && kb_end == p.KBLK) {  // sole owner of this row-block
+        if (sole_owner) {
             write(acc);
             return;
         }
@@ -337,8 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
                                                   acc[mt][nt][3]);
         __threadfence();
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        const int c_first = cta_of(b * p.KBLK, p.U, p.G);
-        const int c_last = cta_of((b + 1) * p.KBLK - 1, p.U, p.G);
+        const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
+        const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
         if (tid == 0) {
             const int prev = atomicAdd(p.counters + b, 1);
             const int last = prev == c_last - c_first;
@@ -351,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
         float sum[MT][NT8][4];
         zero(sum);
         for (int cc = c_first; cc <= c_last; ++cc) {  // fixed order: deterministic
-            const int64_t cu0 = int64_t(cc) * p.U / p.G;
+            const int cu0 = int(int64_t(cc) * p.U / p.G);
             const int cs = 2 * cc + (b == cu0 / p.KBLK ? 0 : 1);
             const float4* src =
                 reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * 256 + tid) * PER);
@@ -369,77 +400,50 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
         write(sum);
     };
 
-    const uint32_t smem_base = smem_u32(smem);
-    // ldmatrix row address (within a stage's activation tile) for this lane
-    const int lrow = lane & 7, lmat = lane >> 3;
-
-    for (int64_t u = u0, it = 0; u < u1; ++u, ++it) {
-        const int64_t b = u / p.KBLK, kb = u % p.KBLK;
-        if (b != cur_b) {
-            if (cur_b >= 0) epilogue(cur_b, seg_kb0, p.KBLK);
-            cur_b = b;
-            seg_kb0 = kb;
-            zero(acc);
-            zero(blk);
-        }
-        const int s = int(it % STAGES);
-        mbar_wait(&full[s], uint32_t((it / STAGES) & 1));
-        const uint8_t* st = smem + s * GG::STAGE_BYTES;
-        const uint32_t st_act = smem_base + s * GG::STAGE_BYTES + kCodeBytes + GG::SCALE_BYTES;
-        const int strips = int(min(int64_t(kStripsPerBlock), p.NS - b * int64_t(kStripsPerBlock)));
-        bool live[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) live[mt] = MT * warp + mt < strips;
-
-        uint32_t wv[MT][4];  // this lane's 16 bytes of each of its strips
+    // acc += S * blk for scale slot q of stage `st`, then clear blk
+    auto flush = [&](const uint8_t* st, int q) {
+        const uint32_t* sw = reinterpret_cast<const uint32_t*>(st + CODE_BYTES + q * STRIPS * 32);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-            uint4 q = make_uint4(0, 0, 0, 0);
-            if (live[mt])
-                q = *reinterpret_cast<const uint4*>(st + ((MT * warp + mt) * 32 + lane) * 16);
+            const uint32_t h2 = sw[(MT * warp + mt) * 8 + gid];
+            const float2 sc = __half22float2(*reinterpret_cast<const __half2*>(&h2));
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) {
+                acc[mt][nt][0] = fmaf(sc.x, blk[mt][nt][0], acc[mt][nt][0]);
+                acc[mt][nt][1] = fmaf(sc.x, blk[mt][nt][1], acc[mt][nt][1]);
+                acc[mt][nt][2] = fmaf(sc.y, blk[mt][nt][2], acc[mt][nt][2]);
+                acc[mt][nt][3] = fmaf(sc.y, blk[mt][nt][3], acc[mt][nt][3]);
+                blk[mt][nt][0] = blk[mt][nt][1] = blk[mt][nt][2] = blk[mt][nt][3] = 0.0f;
+            }
+        }
+    };
+
+    // One stage: MT strips x STEPS k16 steps x NT8 token tiles.
+    auto compute = [&](const uint8_t* st, uint32_t st_act, int live_strips) {
+        uint32_t wv[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const uint4 q =
+                *reinterpret_cast<const uint4*>(st + ((MT * warp + mt) * 32 + lane) * 16);
             wv[mt][0] = q.x;
             wv[mt][1] = q.y;
             wv[mt][2] = q.z;
             wv[mt][3] = q.w;
         }
-
-        const int64_t k0 = kb * KB;
-        const bool last_of_segment = (u + 1 == u1) || (kb + 1 == p.KBLK);
-        auto flush = [&](int q) {
-            // scales of rows (gid, gid+8) of both strips for group slot q of this stage
-            const uint32_t* sw = reinterpret_cast<const uint32_t*>(st + kCodeBytes + q * STRIPS * 32);
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const uint32_t h2 = sw[(MT * warp + mt) * 8 + gid];
-                const float slo = __half2float(__ushort_as_half(uint16_t(h2 & 0xFFFF)));
-                const float shi = __half2float(__ushort_as_half(uint16_t(h2 >> 16)));
-#pragma unroll
-                for (int nt = 0; nt < NT8; ++nt) {
-                    acc[mt][nt][0] = fmaf(slo, blk[mt][nt][0], acc[mt][nt][0]);
-                    acc[mt][nt][1] = fmaf(slo, blk[mt][nt][1], acc[mt][nt][1]);
-                    acc[mt][nt][2] = fmaf(shi, blk[mt][nt][2], acc[mt][nt][2]);
-                    acc[mt][nt][3] = fmaf(shi, blk[mt][nt][3], acc[mt][nt][3]);
-                    blk[mt][nt][0] = blk[mt][nt][1] = blk[mt][nt][2] = blk[mt][nt][3] = 0.0f;
-                }
-            }
-        };
-        const int steps_per_group = p.g >= KB ? STEPS : int(p.g / 16);
-
+        const uint32_t a_base = st_act + (lane & 7) * GG::ASTRIDE + (lane >> 3) * 16;
 #pragma unroll
         for (int j2 = 0; j2 < STEPS; j2 += 2) {
-            // B fragments for k16 steps j2, j2+1 of every n8 tile (one ldmatrix.x4 each)
             uint32_t bf[NT8][4];
 #pragma unroll
-            for (int nt = 0; nt < NT8; ++nt) {
-                const uint32_t addr = st_act + (nt * 8 + lrow) * GG::ASTRIDE + (j2 * 16 + lmat * 8) * 2;
-                ldsm_x4(addr, bf[nt][0], bf[nt][1], bf[nt][2], bf[nt][3]);
-            }
+            for (int nt = 0; nt < NT8; ++nt)
+                ldsm_x4(a_base + nt * 8 * GG::ASTRIDE + j2 * 32, bf[nt][0], bf[nt][1], bf[nt][2],
+                        bf[nt][3]);
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
                 const int j = j2 + jj;
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
-                    if (!live[mt]) continue;
+                    if (MT > 1 && MT * warp + mt >= live_strips) continue;
                     uint32_t af[4];
                     if constexpr (BITS == 4) dequant4<AT>(wv[mt][j], af);
                     else dequant8<AT>(wv[mt][2 * j], wv[mt][2 * j + 1], af);
@@ -447,13 +451,39 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_kernel(const Params p) {
                     for (int nt = 0; nt < NT8; ++nt)
                         mma16816<AT>(blk[mt][nt], af, bf[nt][2 * jj], bf[nt][2 * jj + 1]);
                 }
-                if (p.g < KB && ((j + 1) % steps_per_group) == 0) flush(j / steps_per_group);
+                if (p.steps_per_group && ((j + 1) % p.steps_per_group) == 0)
+                    flush(st, j / p.steps_per_group);
             }
         }
-        if (p.g >= KB && (((k0 + KB) % p.g) == 0 || last_of_segment)) flush(0);
+    };
+
+    const uint32_t smem_base = smem_u32(smem);
+    int b = u0 / p.KBLK, kb = u0 - b * p.KBLK;
+    int seg_kb0 = kb;
+    int live = min(STRIPS, p.NS - b * STRIPS);
+    int s = 0;
+    uint32_t phase = 0;
+    zero(acc);
+    zero(blk);
+    for (int u = u0; u < u1; ++u) {
+        mbar_wait(&full[s], phase);
+        const uint8_t* st = smem + s * GG::STAGE_BYTES;
+        if (MT * warp < live)
+            compute(st, smem_base + s * GG::STAGE_BYTES + CODE_BYTES + GG::SCALE_BYTES, live);
+        const bool seg_end = (u + 1 == u1) || (kb + 1 == p.KBLK);
+        if (!p.steps_per_group && (seg_end || ((kb + 1) & p.kb_group_mask) == 0)) flush(st, 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        if (u + 1 == u1) epilogue(b, seg_kb0, kb + 1);
+        if (++s == STAGES) s = 0, phase ^= 1u;
+        if (seg_end) {
+            epilogue(b, seg_kb0 == 0 && kb + 1 == p.KBLK);
+            zero(acc);
+            if (++kb == p.KBLK) kb = 0, ++b;
+            seg_kb0 = kb;
+            live = min(STRIPS, p.NS - b * STRIPS);
+        } else {
+            ++kb;
+        }
     }
 }
 
@@ -471,8 +501,8 @@ int sm_count() {
 
 int nt8_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 8; }
 
-int ctas_for(int64_t U) {
-    int G = sm_count();
+int ctas_for(int64_t U, int nt8) {  // a full wave (env override for tests/tuning)
+    int G = ctas_per_sm(nt8) * sm_count();
     if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
     if (G < 1) G = 1;
     return int(U < G ? U : G);
@@ -536,7 +566,7 @@ size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t 
     const int64_t strips = 8 * mt;
     const int64_t NS = (n + 15) / 16, NB = (NS + strips - 1) / strips;
     const int64_t U = NB * (k / kb > 0 ? k / kb : 1);
-    const int G = wg::ctas_for(U);
+    const int G = wg::ctas_for(U, nt8);
     return kCounterBytes + size_t(G) * 2 * 256 * (mt * nt8 * 4) * sizeof(float);
 }
 
@@ -547,22 +577,38 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
     p.scales = A.scales;
     p.N = A.n;
     p.K = A.k;
-    p.g = A.g >= A.k ? (int64_t(1) << 62) : A.g;  // one group spanning the row
-    p.NS = (A.n + 15) / 16;
-    p.KBLK = A.k / kb;
+    p.NS = int((A.n + 15) / 16);
+    p.KBLK = int(A.k / kb);
+    if (A.g >= A.k) {  // one group spanning the row (per-channel)
+        p.scale_groups = 1;
+        p.steps_per_group = 0;
+        p.kb_group_mask = -1;
+        p.kb_per_group_shift = 0;
+    } else if (A.g >= kb) {
+        p.scale_groups = 1;
+        p.steps_per_group = 0;
+        p.kb_group_mask = int(A.g / kb) - 1;
+        p.kb_per_group_shift = __builtin_ctzll(uint64_t(A.g / kb));
+    } else {
+        p.scale_groups = int(kb / A.g);
+        p.steps_per_group = int(A.g / 16);
+        p.kb_group_mask = 0;
+        p.kb_per_group_shift = 0;
+    }
     p.out_dtype = A.out_dtype;
     p.counters = static_cast<int*>(A.workspace);
     p.partials = reinterpret_cast<float*>(static_cast<char*>(A.workspace) + kCounterBytes);
     if ((p.NS + 7) / 8 > int64_t(kCounterBytes / 4)) return cudaErrorInvalidValue;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
     for (int64_t m0 = 0; m0 < A.m; m0 += 64) {  // decode batches: one pass per 64 tokens
-        p.M = A.m - m0 < 64 ? A.m - m0 : 64;
+        p.M = int(A.m - m0 < 64 ? A.m - m0 : 64);
         p.a = static_cast<const char*>(A.a) + m0 * A.k * 2;
         p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
         const int nt8 = wg::nt8_for(p.M), strips = 8 * wg::mt_for(nt8);
         p.NB = (p.NS + strips - 1) / strips;
+        if (int64_t(p.NB) * p.KBLK >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
         p.U = p.NB * p.KBLK;
-        p.G = wg::ctas_for(p.U);
+        p.G = wg::ctas_for(p.U, nt8);
         // PDL only between chunks of this call or when the caller vouches that the
         // previous kernel in the stream does not write this layer's weights.
         const bool pdl = A.pdl || m0 > 0;
