@@ -154,22 +154,30 @@ void ro_unpack(const uint8_t* bytes, int64_t n, int bits, int8_t* out) {
 }
 
 /* Native layout (this repository's GEMM operand order).  Rows
- * form 16-row strips (one mma.m16n8k16 A tile); columns form k-blocks of 64
- * (4-bit) or 32 (8-bit) codes = 16 bytes per lane.  Order: k-block-major,
- * then strip, then lane (32), then 16 bytes.  Inside a lane, each k16 step is
- * one 32-bit (4-bit) or 64-bit (8-bit) word holding that lane's 8 A-fragment
+ * form 16-row strips (one mma.m16n8k16 A tile), 16 strips a 256-row row-block;
+ * columns form k-blocks of 64 (4-bit) or 32 (8-bit) codes = 16 bytes per lane.
+ * Order: row-block, then k-block, then strip within the block, then lane (32),
+ * then 16 bytes -- a row-block is one contiguous run along K.  The last
+ * row-block may hold fewer than 16 strips.  Inside a lane, each k16 step is one
+ * 32-bit (4-bit) or 64-bit (8-bit) word holding that lane's 8 A-fragment
  * elements a0..a7 in the order the register dequantizer consumes them. */
 static int64_t native_kblock(int bits) { return bits == 4 ? 64 : 32; }
 
+/* index of the 512-byte (strip, k-block) chunk */
+static int64_t native_chunk(int64_t ns, int64_t kblk, int64_t strip, int64_t b) {
+    int64_t rb = strip / 16, sl = strip % 16;
+    int64_t in_rb = ns - rb * 16 < 16 ? ns - rb * 16 : 16;
+    return rb * 16 * kblk + b * in_rb + sl;
+}
+
 static int64_t native_index(int bits, int64_t rows, int64_t cols, int64_t r, int64_t c) {
-    int64_t ns = (rows + 15) / 16, kb = native_kblock(bits);
-    (void)cols;
+    int64_t ns = (rows + 15) / 16, kb = native_kblock(bits), kblk = (cols + kb - 1) / kb;
     int64_t s = r / 16, rr = r % 16, b = c / kb, cc = c % kb;
     int64_t j = cc / 16, kk = cc % 16;
     int64_t gid = rr % 8, hi_row = rr / 8, tig = (kk % 8) / 2, hi_k = kk / 8, lo = kk % 2;
     int64_t lane = 4 * gid + tig;
     int64_t e = 4 * hi_k + 2 * hi_row + lo; /* PTX m16n8k16 A fragment element */
-    int64_t base = ((b * ns + s) * 32 + lane);
+    int64_t base = native_chunk(ns, kblk, s, b) * 32 + lane;
     if (bits == 4) {
         int64_t nib = (e % 2) * 4 + e / 2; /* word nibble j <-> reg (j%4), half j/4 */
         return base * 32 + j * 8 + nib;
@@ -233,16 +241,18 @@ void ro_decode_layout(const uint8_t* data, int64_t rows, int64_t cols, int bits,
 
 int64_t ro_native_scale_count(int64_t rows, int64_t gpr) { return gpr * ((rows + 15) / 16) * 16; }
 
-/* Native scale order [group][strip][gid][half]; row = 16*strip + 8*half + gid.
- * Padded rows get 0. */
+/* Native scale order [row-block][group][strip in block][gid][half] (the code
+ * layout's chunk order with groups in place of k-blocks); row = 16*strip +
+ * 8*half + gid.  Padded rows get 0. */
 void ro_native_scales(const uint16_t* s16, int64_t rows, int64_t gpr, uint16_t* out) {
     int64_t ns = (rows + 15) / 16;
-    for (int64_t j = 0; j < gpr; ++j)
-        for (int64_t s = 0; s < ns; ++s)
+    for (int64_t s = 0; s < ns; ++s)
+        for (int64_t j = 0; j < gpr; ++j)
             for (int64_t gid = 0; gid < 8; ++gid)
                 for (int64_t h = 0; h < 2; ++h) {
                     int64_t r = 16 * s + 8 * h + gid;
-                    out[((j * ns + s) * 8 + gid) * 2 + h] = r < rows ? s16[r * gpr + j] : 0;
+                    out[(native_chunk(ns, gpr, s, j) * 8 + gid) * 2 + h] =
+                        r < rows ? s16[r * gpr + j] : 0;
                 }
 }
 

@@ -67,20 +67,36 @@ struct Layout {
 
 __host__ __device__ __forceinline__ int64_t native_kblock(int bits) { return bits == 4 ? 64 : 32; }
 
-// Native layout.  16-row strips x k-blocks of 64 (4-bit) or 32
-// (8-bit) codes; k-block-major, then strip, then lane, then the lane's 16
-// bytes.  Each k16 step of a lane is one word of the mma.m16n8k16 A fragment
-// (a0..a7), in the order the register dequantizer consumes it.
-__host__ __device__ __forceinline__ int64_t native_slot(int bits, int64_t rows, int64_t r,
-                                                        int64_t c) {
+// Native layout.  Rows form 16-row strips (one mma.m16n8k16 A
+// tile); 16 strips form a 256-row row-block.  Columns form k-blocks of 64 (4-bit)
+// or 32 (8-bit) codes = 16 bytes per lane.  Byte order:
+//   [row-block][k-block][strip in block][lane 0..31][16 bytes]
+// so every row-block's codes are one contiguous run along K (a GEMM CTA streams
+// contiguous memory) and one (row-block, k-block) is a contiguous 8 KiB tile.
+// The last row-block may hold fewer than 16 strips.  Inside a lane's 16 bytes each
+// k16 step is one word of the A fragment (a0..a7), in the order the register
+// dequantizer consumes it.
+constexpr int kNativeBlockStrips = 16;
+
+__host__ __device__ __forceinline__ int64_t native_chunk(int64_t ns, int64_t kblk, int64_t strip,
+                                                         int64_t b) {
+    const int64_t rb = strip / kNativeBlockStrips, sl = strip % kNativeBlockStrips;
+    const int64_t in_rb = ns - rb * kNativeBlockStrips < kNativeBlockStrips
+                              ? ns - rb * kNativeBlockStrips : kNativeBlockStrips;
+    return rb * kNativeBlockStrips * kblk + b * in_rb + sl;  // index of the 512-byte chunk
+}
+
+__host__ __device__ __forceinline__ int64_t native_slot(int bits, int64_t rows, int64_t cols,
+                                                        int64_t r, int64_t c) {
     const int64_t ns = (rows + 15) / 16, kb = native_kblock(bits);
+    const int64_t kblk = (cols + kb - 1) / kb;
     const int64_t s = r >> 4, rr = r & 15, b = c / kb, cc = c % kb;
     const int64_t j = cc >> 4, kk = cc & 15;
     const int64_t gid = rr & 7, hi_row = rr >> 3, tig = (kk & 7) >> 1, hi_k = kk >> 3,
                   lo = kk & 1;
     const int64_t lane = 4 * gid + tig;
     const int64_t e = 4 * hi_k + 2 * hi_row + lo;
-    const int64_t base = (b * ns + s) * 32 + lane;
+    const int64_t base = native_chunk(ns, kblk, s, b) * 32 + lane;
     if (bits == 4) return base * 32 + j * 8 + (e & 1) * 4 + (e >> 1);
     return base * 16 + j * 8 + (e >> 2) * 4 + (e & 1) * 2 + ((e >> 1) & 1);
 }
@@ -89,6 +105,7 @@ __host__ __device__ __forceinline__ int64_t native_slot(int bits, int64_t rows, 
 __host__ __device__ __forceinline__ bool native_coords(int bits, int64_t rows, int64_t cols,
                                                        int64_t slot, int64_t* r, int64_t* c) {
     const int64_t ns = (rows + 15) / 16, kb = native_kblock(bits);
+    const int64_t kblk = (cols + kb - 1) / kb;
     int64_t e, j, rest;
     if (bits == 4) {
         const int64_t nib = slot & 7;
@@ -103,8 +120,12 @@ __host__ __device__ __forceinline__ bool native_coords(int bits, int64_t rows, i
         e = (byte >> 2) * 4 + (b2 & 1) * 2 + (b2 >> 1);
     }
     const int64_t lane = rest & 31;
-    const int64_t bs = rest >> 5;
-    const int64_t s = bs % ns, b = bs / ns;
+    const int64_t chunk = rest >> 5;
+    const int64_t per_rb = int64_t(kNativeBlockStrips) * kblk;
+    const int64_t rb = chunk / per_rb, off = chunk % per_rb;
+    const int64_t in_rb = ns - rb * kNativeBlockStrips < kNativeBlockStrips
+                              ? ns - rb * kNativeBlockStrips : kNativeBlockStrips;
+    const int64_t b = off / in_rb, s = rb * kNativeBlockStrips + off % in_rb;
     const int64_t gid = lane >> 2, tig = lane & 3;
     const int64_t hi_k = e >> 2, hi_row = (e >> 1) & 1, lo = e & 1;
     *r = 16 * s + gid + 8 * hi_row;
@@ -115,7 +136,7 @@ __host__ __device__ __forceinline__ bool native_coords(int bits, int64_t rows, i
 __host__ __device__ __forceinline__ int64_t layout_slot(const Layout& L, int bits, int64_t rows,
                                                         int64_t cols, int64_t r, int64_t c) {
     if (L.kind == RTNQ_ROW_MAJOR) return r * cols + c;
-    if (L.kind == RTNQ_NATIVE_SM100) return native_slot(bits, rows, r, c);
+    if (L.kind == RTNQ_NATIVE_SM100) return native_slot(bits, rows, cols, r, c);
     const int64_t tpr = (cols + L.tc - 1) / L.tc;  // packing.cpp:62-65
     const int64_t tile = (r / L.tr) * tpr + c / L.tc;
     return tile * L.tr * L.tc + (c % L.tc) * L.tr + r % L.tr;
@@ -154,17 +175,19 @@ __device__ __forceinline__ int code_at_slot(const uint8_t* data, int bits, int64
     return int((slot & 1) ? (b >> 4) : (b & 0x0F)) - 8;
 }
 
-// Native scale order [group][strip][gid][half] (row = 16*strip + 8*half + gid).
-__host__ __device__ __forceinline__ int64_t native_scale_index(int64_t rows, int64_t r,
-                                                               int64_t group) {
+// Native scale order [row-block][group][strip in block][gid][half], f16, with
+// row = 16*strip + 8*half + gid: a row-block's scales are one contiguous run
+// along K, like its codes.  Padded rows hold 0.
+__host__ __device__ __forceinline__ int64_t native_scale_index(int64_t rows, int64_t gpr,
+                                                               int64_t r, int64_t group) {
     const int64_t ns = (rows + 15) / 16;
-    return ((group * ns + (r >> 4)) * 8 + (r & 7)) * 2 + ((r >> 3) & 1);
+    return (native_chunk(ns, gpr, r >> 4, group) * 8 + (r & 7)) * 2 + ((r >> 3) & 1);
 }
 
 __device__ __forceinline__ float load_scale(const void* scales, int dtype, int order,
                                             int64_t rows, int64_t gpr, int64_t r,
                                             int64_t group) {
-    const int64_t i = order == RTNQ_SCALES_NATIVE ? native_scale_index(rows, r, group)
+    const int64_t i = order == RTNQ_SCALES_NATIVE ? native_scale_index(rows, gpr, r, group)
                                                   : r * gpr + group;
     return load_elem(scales, dtype, i);
 }

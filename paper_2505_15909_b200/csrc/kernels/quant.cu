@@ -41,7 +41,7 @@ __global__ void group_scales_kernel(const void* __restrict__ w, int dtype, int64
         if (s32) s32[r * gpr + j] = s;
         const uint16_t h = __half_as_ushort(__float2half_rn(s));
         if (s16) s16[r * gpr + j] = h;
-        if (s16n) s16n[native_scale_index(rows, r, j)] = h;
+        if (s16n) s16n[native_scale_index(rows, gpr, r, j)] = h;
     }
 }
 
@@ -119,9 +119,14 @@ __global__ void native_scales_kernel(const void* __restrict__ scales, int dtype,
     const int64_t ns = (rows + 15) / 16, n = gpr * ns * 16;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t half = i & 1, gid = (i >> 1) & 7, sj = i >> 4;
-        const int64_t s = sj % ns, j = sj / ns;
-        const int64_t r = 16 * s + 8 * half + gid;
+        // invert native_scale_index: i -> (chunk, gid, half) -> (strip, group)
+        const int64_t half = i & 1, gid = (i >> 1) & 7, chunk = i >> 4;
+        const int64_t per_rb = int64_t(kNativeBlockStrips) * gpr;
+        const int64_t rb = chunk / per_rb, off = chunk % per_rb;
+        const int64_t in_rb = ns - rb * kNativeBlockStrips < kNativeBlockStrips
+                                  ? ns - rb * kNativeBlockStrips : kNativeBlockStrips;
+        const int64_t j = off / in_rb, strip = rb * kNativeBlockStrips + off % in_rb;
+        const int64_t r = 16 * strip + 8 * half + gid;
         uint16_t h = 0;
         if (r < rows) {
             if (dtype == RTNQ_F16) h = static_cast<const uint16_t*>(scales)[r * gpr + j];

@@ -121,7 +121,7 @@ quant_fused_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, int64
             if (s32) s32[r * gpr + j] = s;
             const uint16_t h = __half_as_ushort(__float2half_rn(s));
             if (s16) s16[r * gpr + j] = h;
-            if (s16n) s16n[native_scale_index(rows, r, j)] = h;
+            if (s16n) s16n[native_scale_index(rows, gpr, r, j)] = h;
         }
     }
 #pragma unroll
@@ -189,7 +189,7 @@ quant_fused_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, int64
                 p |= uint32_t(sc[rr][cc] + 8) << (4 * ((e & 1) * 4 + (e >> 1)));
             }
             const int64_t kb = cb * 2 + q;
-            *reinterpret_cast<uint32_t*>(nat + (kb * ns + strip) * 512 + o) = p;
+            *reinterpret_cast<uint32_t*>(nat + native_chunk(ns, cols / 64, strip, kb) * 512 + o) = p;
         } else {
             const int q = t >> 6, o = 8 * (t & 63), lane = o >> 4, j = (o & 15) >> 3;
             const int gid = lane >> 2, tig = lane & 3;
@@ -202,7 +202,8 @@ quant_fused_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, int64
                 w2[pb >> 2] |= uint32_t(uint8_t(sc[rr][cc] + 128)) << (8 * (pb & 3));
             }
             const int64_t kb = cb * 4 + q;
-            *reinterpret_cast<uint2*>(nat + (kb * ns + strip) * 512 + o) = make_uint2(w2[0], w2[1]);
+            *reinterpret_cast<uint2*>(nat + native_chunk(ns, cols / 32, strip, kb) * 512 + o) =
+                make_uint2(w2[0], w2[1]);
         }
     }
 }

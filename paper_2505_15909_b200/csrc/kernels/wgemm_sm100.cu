@@ -1,25 +1,29 @@
-// wgemm_sm100.cu -- W4A16 / W8A16 weight-only GEMM for decode batches (m <= 64).
+// wgemm_sm100.cu -- W4A16 / W8A16 weight-only GEMM for decode batches.
 //
 // out[m][n] = sum_k a[m][k] * code[n][k] * S[n][k/g]   (gemm.hpp:18-27)
 //
 // Design:
 //  * Weights are the M operand of mma.m16n8k16 (16 output channels per tile),
-//    tokens the N operand, so a batch of 1..8 tokens costs one n8 tile.
-//  * Codes are stored in the native layout (common.cuh): for a CTA row-block of
-//    256 channels x one k-block (64 4-bit / 32 8-bit codes) the 8 KiB of codes are
-//    contiguous, so ONE cp.async.bulk (TMA, UBLKCP) moves each pipeline stage;
-//    group scales (native order) and the activation rows ride on the same
-//    mbarrier.  A dedicated producer warp keeps STAGES stages in flight.
-//  * Each lane's 16-byte slice of a stage is its own A fragments: one LDS.128,
-//    then LOP3/PRMT magic-number dequantization to bf16x2/f16x2 codes (exact
-//    integers), mma into a per-group f32 block accumulator, and one FFMA per
-//    element per group: acc += S * block -- the reference's accumulation
-//    structure (gemm.cpp:69-87), with the scale applied in f32 (exact codes, no
-//    f16 code*scale rounding).
+//    tokens the N operand: a batch of 1..8 tokens costs one n8 tile.
+//  * Native layout (common.cuh): a 256-channel row-block is one contiguous run
+//    along K, so each CTA streams contiguous memory; a pipeline stage is two
+//    k-blocks (16 KiB of codes) moved by ONE cp.async.bulk (TMA, UBLKCP), plus one
+//    bulk copy for the stage's f16 group scales.  Activations (a few hundred
+//    bytes per token and stage, too fragmented for bulk copies) come in with
+//    16-byte cp.async (LDGSTS) from the producer warp's 32 lanes, completing on
+//    the same mbarrier (cp.async.mbarrier.arrive.noinc).
+//  * Each lane's 16 bytes of a (strip, k-block) tile are its own A fragments: one
+//    LDS.128, then LOP3/PRMT magic-number dequantization to exact bf16x2/f16x2
+//    codes, mma into a per-group f32 block accumulator, and one FFMA per element
+//    per group: acc += S * block -- the reference's accumulation structure
+//    (gemm.cpp:69-87) with the scale applied in f32.
 //  * Stream-K: the (row-block, k-block) units are split evenly over the grid;
 //    row-blocks shared by several CTAs are combined by the last CTA to arrive,
-//    always summing the partials in CTA order (deterministic, no float atomics).
-//  * PDL: weight prefetch for the first STAGES stages is issued before
+//    summing the partials in CTA order (deterministic, no float atomics).
+//  * Occupancy: 1..8-token and 9..16-token batches run 4 consumer warps x 4
+//    strips with two CTAs per SM (two producers, ~128 KiB in flight per SM);
+//    17..32-token batches run 8 consumer warps x 2 strips, one CTA per SM.
+//  * PDL (opt-in): weight prefetch for the first stages is issued before
 //    griddepcontrol.wait; only the activation copies wait for the producer grid.
 #include <cuda_runtime.h>
 
@@ -31,15 +35,8 @@
 namespace rtnq_b200 {
 namespace wg {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-// m16 strips per consumer warp: 2 for decode batches <= 16 tokens (256-channel
-// row-blocks halve activation re-reads), 1 above (keeps the f32 block + group
-// accumulators of 4..8 n8 tiles in registers: 9 warps leave 168 regs/thread).
-__host__ __device__ constexpr int mt_for(int nt8) { return nt8 <= 2 ? 2 : 1; }
-// Two co-resident CTAs per SM (two producer warps, twice the bytes in flight)
-// while the accumulators fit in 96 registers; one CTA for 64-token batches.
-__host__ __device__ constexpr int ctas_per_sm(int nt8) { return nt8 >= 8 ? 1 : 2; }
+constexpr int kStrips = kNativeBlockStrips;  // 16 strips = 256 channels per row-block
+constexpr int kKPS = 2;                      // k-blocks per pipeline stage
 
 struct Params {
     const void* a;
@@ -49,17 +46,15 @@ struct Params {
     float* partials;
     int* counters;
     int64_t N, K;
-    int M;            // tokens in this launch (<= 64)
-    int NS;           // 16-row strips (ceil(N / 16))
-    int NB;           // row-blocks (ceil(NS / STRIPS))
-    int KBLK;         // k-blocks (K / KB)
-    int U;            // units = NB * KBLK
-    int G;            // CTAs
+    int M;       // tokens in this launch (<= 32)
+    int NS;      // 16-row strips (ceil(N / 16))
+    int NB;      // row-blocks (ceil(NS / 16))
+    int KBLK;    // k-blocks (K / KB)
+    int GPR;     // scale groups per row
+    int U;       // units = NB * KBLK
+    int G;       // CTAs
     int out_dtype;
-    int scale_groups;   // scale groups per stage: 1 (g >= KB) or KB / g
-    int steps_per_group;  // k16 steps per group when g < KB, else 0
-    int kb_group_mask;  // g >= KB and g < K: g/KB - 1 (flush when (kb+1) & mask == 0); -1: never
-    int kb_per_group_shift;  // log2(g / KB) when g >= KB and g < K
+    int log2g;   // log2(group size); 30 when one group spans the row
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------
@@ -209,17 +204,16 @@ __device__ __forceinline__ void store_out(void* out, int dt, int64_t i, float v)
 }
 
 // ---- compile-time geometry ---------------------------------------------------------------
-template <int BITS, int NT8, int STAGES>
+template <int BITS, int NT8, int CW, int STAGES>
 struct Geo {
-    static constexpr int MT = mt_for(NT8);                   // strips per warp
-    static constexpr int STRIPS = MT * kConsumerWarps;       // strips per row-block
-    static constexpr int ROWS = 16 * STRIPS;                 // channels per row-block
-    static constexpr int CODE_BYTES = STRIPS * 512;          // one k-block of a row-block
+    static constexpr int MT = kStrips / CW;                  // strips per consumer warp
+    static constexpr int THREADS = (CW + 1) * 32;
     static constexpr int KB = BITS == 4 ? 64 : 32;           // codes per k-block
-    static constexpr int STEPS = KB / 16;                    // k16 steps per stage
+    static constexpr int STEPS = KB / 16;                    // k16 steps per k-block
     static constexpr int MPAD = NT8 * 8;                     // padded tokens
-    static constexpr int ASTRIDE = KB * 2 + 16;              // bytes per smem activation row
-    static constexpr int SCALE_BYTES = STEPS * STRIPS * 32;  // up to KB/16 groups per stage
+    static constexpr int ASTRIDE = kKPS * KB * 2 + 16;       // bytes per smem activation row
+    static constexpr int CODE_BYTES = kKPS * kStrips * 512;  // 16 KiB
+    static constexpr int SCALE_BYTES = kKPS * STEPS * kStrips * 32;  // up to KB/16 groups/k-block
     static constexpr int ACT_BYTES = MPAD * ASTRIDE;
     static constexpr int STAGE_BYTES = (CODE_BYTES + SCALE_BYTES + ACT_BYTES + 127) / 128 * 128;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16;
@@ -230,11 +224,34 @@ __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
     return int(((u + 1) * G - 1) / U);
 }
 
-template <int BITS, int AT, int NT8, int STAGES>
-__global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const Params p) {
-    using GG = Geo<BITS, NT8, STAGES>;
-    constexpr int KB = GG::KB, STEPS = GG::STEPS, MT = GG::MT, STRIPS = GG::STRIPS;
-    constexpr int CODE_BYTES = GG::CODE_BYTES, ROWS = GG::ROWS;
+// The stage sequence of CTA c: consecutive chunks of <= kKPS k-blocks that never
+// cross a row-block (segment) boundary.  Producer and consumers walk it alike.
+struct Walker {
+    int u, u1, b, kb, KBLK;
+    __device__ Walker(int u0_, int u1_, int KBLK_) : u(u0_), u1(u1_), KBLK(KBLK_) {
+        b = u0_ / KBLK_;
+        kb = u0_ - b * KBLK_;
+    }
+    __device__ bool more() const { return u < u1; }
+    __device__ int chunk() const {  // k-blocks in the current stage
+        const int left_seg = KBLK - kb, left = u1 - u;
+        const int n = left_seg < left ? left_seg : left;
+        return n < kKPS ? n : kKPS;
+    }
+    __device__ bool seg_end(int n) const { return kb + n == KBLK || u + n == u1; }
+    __device__ void advance(int n) {
+        u += n;
+        kb += n;
+        if (kb == KBLK) kb = 0, ++b;
+    }
+};
+
+template <int BITS, int AT, int NT8, int CW, int STAGES>
+__global__ void __launch_bounds__(Geo<BITS, NT8, CW, STAGES>::THREADS, CW == 4 ? 2 : 1)
+wgemm_kernel(const Params p) {
+    using GG = Geo<BITS, NT8, CW, STAGES>;
+    constexpr int KB = GG::KB, STEPS = GG::STEPS, MT = GG::MT;
+    constexpr int CODE_BYTES = GG::CODE_BYTES;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * GG::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
@@ -243,49 +260,41 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int u0 = int(int64_t(c) * p.U / p.G), u1 = int(int64_t(c + 1) * p.U / p.G);
+    const int gmask = (1 << p.log2g) - 1;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1 + 32);  // producer expect_tx + 32 lanes' cp.async arrivals
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     grid_dep_launch();
 
-    if (warp == kConsumerWarps) {
-        // ===================== producer warp (all 32 lanes issue copies) =====================
-        const int n_units = u1 - u0;
-        const int prologue = n_units < STAGES ? n_units : STAGES;
-        const uint32_t act_bytes = uint32_t(KB * 2);
+    if (warp == CW) {
+        // ===================== producer warp =====================
         const int64_t a_row = p.K * 2;
-        // Codes + scales: one TMA bulk copy each (a bulk-copy instruction costs ~70
-        // cycles of producer issue, so a stage uses as few as possible).
-        auto weights = [&](int b, int kb, int s) {
+        auto weights = [&](const Walker& w, int n, int s) {
             if (lane != 0) return;
-            const int strips = min(STRIPS, p.NS - b * STRIPS);
+            const int strips = min(kStrips, p.NS - w.b * kStrips);
+            const int g0 = (w.kb * KB) >> p.log2g, g1 = ((w.kb + n) * KB - 1) >> p.log2g;
+            const uint32_t code_bytes = uint32_t(n * strips * 512);
+            const uint32_t scale_bytes = uint32_t((g1 - g0 + 1) * strips * 32);
             uint8_t* st = smem + s * GG::STAGE_BYTES;
-            mbar_expect_tx(&full[s], uint32_t(strips * 512 + p.scale_groups * strips * 32));
-            bulk_g2s(st, p.codes + (int64_t(kb) * p.NS + b * STRIPS) * 512, uint32_t(strips * 512),
-                     &full[s]);
-            for (int q = 0; q < p.scale_groups; ++q) {
-                const int64_t grp = p.steps_per_group ? int64_t(kb) * p.scale_groups + q
-                                    : (p.kb_group_mask < 0 ? 0 : kb >> p.kb_per_group_shift);
-                bulk_g2s(st + CODE_BYTES + q * STRIPS * 32,
-                         p.scales + (grp * p.NS + b * STRIPS) * 16, uint32_t(strips * 32),
-                         &full[s]);
-            }
+            mbar_expect_tx(&full[s], code_bytes + scale_bytes);
+            bulk_g2s(st, p.codes + (int64_t(w.b) * kStrips * p.KBLK + int64_t(w.kb) * strips) * 512,
+                     code_bytes, &full[s]);
+            bulk_g2s(st + CODE_BYTES,
+                     p.scales + (int64_t(w.b) * kStrips * p.GPR + int64_t(g0) * strips) * 16,
+                     scale_bytes, &full[s]);
         };
-        // Activations: 16-byte cp.async (LDGSTS) per lane -- M rows x KB*2 bytes is
-        // too fragmented for bulk copies.  Each lane then arms the stage's mbarrier
-        // to fire when its copies land (cp.async.mbarrier.arrive.noinc).
-        auto acts = [&](int kb, int s) {
+        auto acts = [&](const Walker& w, int n, int s) {
             const uint32_t dst = smem_u32(smem + s * GG::STAGE_BYTES + CODE_BYTES + GG::SCALE_BYTES);
-            const uint8_t* src = static_cast<const uint8_t*>(p.a) + int64_t(kb) * (KB * 2);
-            constexpr int CHUNKS = KB * 2 / 16;  // 16-byte chunks per row
-            for (int i = lane; i < p.M * CHUNKS; i += 32) {
-                const int r = i / CHUNKS, ch = i % CHUNKS;
+            const uint8_t* src = static_cast<const uint8_t*>(p.a) + int64_t(w.kb) * (KB * 2);
+            const int chunks = n * (KB * 2 / 16);  // 16-byte chunks per row
+            for (int i = lane; i < p.M * chunks; i += 32) {
+                const int r = i / chunks, ch = i - r * chunks;
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                                  dst + r * GG::ASTRIDE + ch * 16),
                              "l"(src + r * a_row + ch * 16)
@@ -295,26 +304,32 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
                              smem_u32(&full[s]))
                          : "memory");
         };
+        // Prologue: weights for the first STAGES stages before waiting on the
+        // producer grid (PDL); activations after.
+        Walker w(u0, u1, p.KBLK);
+        int pro = 0;
         {
-            int b = u0 / p.KBLK, kb = u0 - b * p.KBLK;
-            for (int it = 0; it < prologue; ++it) {
-                weights(b, kb, it);
-                if (++kb == p.KBLK) kb = 0, ++b;
+            Walker t = w;
+            for (; pro < STAGES && t.more(); ++pro) {
+                const int n = t.chunk();
+                weights(t, n, pro);
+                t.advance(n);
             }
         }
-        grid_dep_wait();  // activations are produced by the previous kernel
-        int b = u0 / p.KBLK, kb = u0 - b * p.KBLK;
-        for (int it = 0; it < prologue; ++it) {
-            acts(kb, it);
-            if (++kb == p.KBLK) kb = 0, ++b;
+        grid_dep_wait();
+        for (int i = 0; i < pro; ++i) {
+            const int n = w.chunk();
+            acts(w, n, i);
+            w.advance(n);
         }
-        int s = prologue % STAGES;
-        uint32_t phase = prologue == STAGES ? 0u : 1u;  // parity of the empty phase to await
-        for (int it = prologue; it < n_units; ++it) {
+        int s = pro % STAGES;
+        uint32_t phase = pro == STAGES ? 0u : 1u;
+        while (w.more()) {
+            const int n = w.chunk();
             mbar_wait(&empty[s], phase);
-            weights(b, kb, s);
-            acts(kb, s);
-            if (++kb == p.KBLK) kb = 0, ++b;
+            weights(w, n, s);
+            acts(w, n, s);
+            w.advance(n);
             if (++s == STAGES) s = 0, phase ^= 1u;
         }
         return;
@@ -322,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
 
     // ===================== consumer warps =====================
     const int gid = lane >> 2, tig = lane & 3;
+    constexpr int NTHREADS = CW * 32;
     float acc[MT][NT8][4], blk[MT][NT8][4];
 
     auto zero = [](float (&x)[MT][NT8][4]) {
@@ -335,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
 
     // Row-block epilogue: direct store, or partial + deterministic last-arriver combine.
     auto epilogue = [&](int b, bool sole_owner) {
-        const int strips = min(STRIPS, p.NS - b * STRIPS);
+        const int strips = min(kStrips, p.NS - b * kStrips);
         auto write = [&](float (&v)[MT][NT8][4]) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
@@ -345,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
                 for (int nt = 0; nt < NT8; ++nt)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const int64_t n = int64_t(b) * ROWS + strip * 16 + gid + 8 * (i >> 1);
+                        const int64_t n = int64_t(b) * (kStrips * 16) + strip * 16 + gid + 8 * (i >> 1);
                         const int m = nt * 8 + 2 * tig + (i & 1);
                         if (n < p.N && m < p.M)
                             store_out(p.out, p.out_dtype, int64_t(m) * p.N + n, v[mt][nt][i]);
@@ -357,52 +373,72 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
             return;
         }
         constexpr int PER = MT * NT8 * 4;
-        const int tid = threadIdx.x;  // 0..255
+        const int tid = threadIdx.x;
         const int slot = 2 * c + (b == u0 / p.KBLK ? 0 : 1);
-        float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(slot) * 256 + tid) * PER);
+        float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(slot) * NTHREADS + tid) * PER);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NT8; ++nt)
                 mine[mt * NT8 + nt] = make_float4(acc[mt][nt][0], acc[mt][nt][1], acc[mt][nt][2],
                                                   acc[mt][nt][3]);
-        __threadfence();
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        // Publish: the CTA barrier orders every thread's partial stores before thread
+        // 0's gpu-scope release (fences are cumulative); the last arriver's acquire
+        // makes all contributors' partials visible before its CTA-wide reads.
+        asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
         const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
         const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
         if (tid == 0) {
-            const int prev = atomicAdd(p.counters + b, 1);
+            int prev;
+            asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                         : "=r"(prev)
+                         : "l"(p.counters + b)
+                         : "memory");
             const int last = prev == c_last - c_first;
             if (last) p.counters[b] = 0;  // self-reset for the next launch
             *flag = last;
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
         if (!*flag) return;
-        __threadfence();
         float sum[MT][NT8][4];
         zero(sum);
-        for (int cc = c_first; cc <= c_last; ++cc) {  // fixed order: deterministic
-            const int cu0 = int(int64_t(cc) * p.U / p.G);
-            const int cs = 2 * cc + (b == cu0 / p.KBLK ? 0 : 1);
-            const float4* src =
-                reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * 256 + tid) * PER);
+        // contributors after the first start inside row-block b: their slot for b
+        // is their first-segment slot
+        const int first_bit = int(int64_t(c_first) * p.U / p.G) / p.KBLK == b ? 0 : 1;
+        constexpr int BATCH = MT * NT8 >= 8 ? 1 : 2;
+        for (int c0 = c_first; c0 <= c_last; c0 += BATCH) {
+            float4 x[BATCH][MT * NT8];
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
+            for (int q = 0; q < BATCH; ++q) {
+                const int cc = c0 + q;
+                if (cc > c_last) break;
+                const int cs = 2 * cc + (cc == c_first ? first_bit : 0);
+                const float4* src =
+                    reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * NTHREADS + tid) * PER);
 #pragma unroll
-                for (int nt = 0; nt < NT8; ++nt) {
-                    const float4 x = __ldcg(src + mt * NT8 + nt);
-                    sum[mt][nt][0] += x.x;
-                    sum[mt][nt][1] += x.y;
-                    sum[mt][nt][2] += x.z;
-                    sum[mt][nt][3] += x.w;
-                }
+                for (int i = 0; i < MT * NT8; ++i) x[q][i] = __ldcg(src + i);
+            }
+#pragma unroll
+            for (int q = 0; q < BATCH; ++q) {
+                if (c0 + q > c_last) break;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < NT8; ++nt) {
+                        const float4 v = x[q][mt * NT8 + nt];
+                        sum[mt][nt][0] += v.x;
+                        sum[mt][nt][1] += v.y;
+                        sum[mt][nt][2] += v.z;
+                        sum[mt][nt][3] += v.w;
+                    }
+            }
         }
         write(sum);
     };
 
-    // acc += S * blk for scale slot q of stage `st`, then clear blk
-    auto flush = [&](const uint8_t* st, int q) {
-        const uint32_t* sw = reinterpret_cast<const uint32_t*>(st + CODE_BYTES + q * STRIPS * 32);
+    // acc += S * blk with the scales of group slot q of the stage, then clear blk.
+    auto flush = [&](const uint8_t* sc_base, int strips, int q) {
+        const uint32_t* sw = reinterpret_cast<const uint32_t*>(sc_base + q * strips * 32);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const uint32_t h2 = sw[(MT * warp + mt) * 8 + gid];
@@ -418,71 +454,81 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT8)) wgemm_kernel(const
         }
     };
 
-    // One stage: MT strips x STEPS k16 steps x NT8 token tiles.
-    auto compute = [&](const uint8_t* st, uint32_t st_act, int live_strips) {
-        uint32_t wv[MT][4];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            const uint4 q =
-                *reinterpret_cast<const uint4*>(st + ((MT * warp + mt) * 32 + lane) * 16);
-            wv[mt][0] = q.x;
-            wv[mt][1] = q.y;
-            wv[mt][2] = q.z;
-            wv[mt][3] = q.w;
-        }
-        const uint32_t a_base = st_act + (lane & 7) * GG::ASTRIDE + (lane >> 3) * 16;
-#pragma unroll
-        for (int j2 = 0; j2 < STEPS; j2 += 2) {
-            uint32_t bf[NT8][4];
-#pragma unroll
-            for (int nt = 0; nt < NT8; ++nt)
-                ldsm_x4(a_base + nt * 8 * GG::ASTRIDE + j2 * 32, bf[nt][0], bf[nt][1], bf[nt][2],
-                        bf[nt][3]);
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-                const int j = j2 + jj;
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    if (MT > 1 && MT * warp + mt >= live_strips) continue;
-                    uint32_t af[4];
-                    if constexpr (BITS == 4) dequant4<AT>(wv[mt][j], af);
-                    else dequant8<AT>(wv[mt][2 * j], wv[mt][2 * j + 1], af);
-#pragma unroll
-                    for (int nt = 0; nt < NT8; ++nt)
-                        mma16816<AT>(blk[mt][nt], af, bf[nt][2 * jj], bf[nt][2 * jj + 1]);
-                }
-                if (p.steps_per_group && ((j + 1) % p.steps_per_group) == 0)
-                    flush(st, j / p.steps_per_group);
-            }
-        }
-    };
-
     const uint32_t smem_base = smem_u32(smem);
-    int b = u0 / p.KBLK, kb = u0 - b * p.KBLK;
-    int seg_kb0 = kb;
-    int live = min(STRIPS, p.NS - b * STRIPS);
+    const uint32_t a_lane = (lane & 7) * GG::ASTRIDE + (lane >> 3) * 16;  // ldmatrix row address
+    Walker w(u0, u1, p.KBLK);
+    int seg_kb0 = w.kb;
     int s = 0;
     uint32_t phase = 0;
     zero(acc);
     zero(blk);
-    for (int u = u0; u < u1; ++u) {
+    while (w.more()) {
+        const int n = w.chunk();
+        const bool seg_end = w.seg_end(n);
+        const int strips = min(kStrips, p.NS - w.b * kStrips);
         mbar_wait(&full[s], phase);
         const uint8_t* st = smem + s * GG::STAGE_BYTES;
-        if (MT * warp < live)
-            compute(st, smem_base + s * GG::STAGE_BYTES + CODE_BYTES + GG::SCALE_BYTES, live);
-        const bool seg_end = (u + 1 == u1) || (kb + 1 == p.KBLK);
-        if (!p.steps_per_group && (seg_end || ((kb + 1) & p.kb_group_mask) == 0)) flush(st, 0);
+        const uint8_t* sc = st + CODE_BYTES;
+        const uint32_t st_act = smem_base + s * GG::STAGE_BYTES + CODE_BYTES + GG::SCALE_BYTES;
+        const int g0 = (w.kb * KB) >> p.log2g;
+        if (MT * warp < strips) {
+#pragma unroll
+            for (int kbl = 0; kbl < kKPS; ++kbl) {
+                if (kbl >= n) break;
+                const int kbg = w.kb + kbl;
+                uint32_t wv[MT][4];  // this lane's 16 bytes of each of its strips
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    uint4 q = make_uint4(0, 0, 0, 0);
+                    if (MT * warp + mt < strips)
+                        q = *reinterpret_cast<const uint4*>(
+                            st + ((kbl * strips + MT * warp + mt) * 32 + lane) * 16);
+                    wv[mt][0] = q.x;
+                    wv[mt][1] = q.y;
+                    wv[mt][2] = q.z;
+                    wv[mt][3] = q.w;
+                }
+#pragma unroll
+                for (int j2 = 0; j2 < STEPS; j2 += 2) {
+                    uint32_t bf[NT8][4];
+#pragma unroll
+                    for (int nt = 0; nt < NT8; ++nt)
+                        ldsm_x4(st_act + a_lane + nt * 8 * GG::ASTRIDE + (kbl * KB + j2 * 16) * 2,
+                                bf[nt][0], bf[nt][1], bf[nt][2], bf[nt][3]);
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const int j = j2 + jj;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            uint32_t af[4];
+                            if constexpr (BITS == 4) dequant4<AT>(wv[mt][j], af);
+                            else dequant8<AT>(wv[mt][2 * j], wv[mt][2 * j + 1], af);
+#pragma unroll
+                            for (int nt = 0; nt < NT8; ++nt)
+                                mma16816<AT>(blk[mt][nt], af, bf[nt][2 * jj], bf[nt][2 * jj + 1]);
+                        }
+                        // group boundary after this k16 step (groups of 16/32 codes)
+                        const int knext = kbg * KB + (j + 1) * 16;
+                        if (p.log2g < (BITS == 4 ? 6 : 5) && (knext & gmask) == 0)
+                            flush(sc, strips, ((knext - 1) >> p.log2g) - g0);
+                    }
+                }
+                // group boundary or segment end after this k-block (groups >= KB)
+                if (p.log2g >= (BITS == 4 ? 6 : 5) &&
+                    ((((kbg + 1) * KB) & gmask) == 0 || (seg_end && kbl == n - 1)))
+                    flush(sc, strips, ((kbg * KB) >> p.log2g) - g0);
+            }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (++s == STAGES) s = 0, phase ^= 1u;
         if (seg_end) {
-            epilogue(b, seg_kb0 == 0 && kb + 1 == p.KBLK);
+            epilogue(w.b, seg_kb0 == 0 && w.kb + n == p.KBLK);
             zero(acc);
-            if (++kb == p.KBLK) kb = 0, ++b;
-            seg_kb0 = kb;
-            live = min(STRIPS, p.NS - b * STRIPS);
+            w.advance(n);
+            seg_kb0 = w.kb;
         } else {
-            ++kb;
+            w.advance(n);
         }
     }
 }
@@ -499,7 +545,9 @@ int sm_count() {
     return n;
 }
 
-int nt8_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 8; }
+int nt8_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : 4; }
+int cw_for(int nt8) { return nt8 <= 2 ? 4 : 8; }
+int ctas_per_sm(int nt8) { return cw_for(nt8) == 4 ? 2 : 1; }
 
 int ctas_for(int64_t U, int nt8) {  // a full wave (env override for tests/tuning)
     int G = ctas_per_sm(nt8) * sm_count();
@@ -508,20 +556,21 @@ int ctas_for(int64_t U, int nt8) {  // a full wave (env override for tests/tunin
     return int(U < G ? U : G);
 }
 
-template <int BITS, int AT, int NT8, int STAGES>
+template <int BITS, int AT, int NT8, int CW, int STAGES>
 cudaError_t launch_t(const Params& p, cudaStream_t st, bool pdl) {
-    constexpr int smem = Geo<BITS, NT8, STAGES>::SMEM;
-    auto kern = wgemm_kernel<BITS, AT, NT8, STAGES>;
+    using GG = Geo<BITS, NT8, CW, STAGES>;
+    auto kern = wgemm_kernel<BITS, AT, NT8, CW, STAGES>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             GG::SMEM);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(p.G));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
+    cfg.blockDim = dim3(GG::THREADS);
+    cfg.dynamicSmemBytes = GG::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -531,13 +580,14 @@ cudaError_t launch_t(const Params& p, cudaStream_t st, bool pdl) {
     return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
+// Stage counts keep two CTAs per SM under ~113 KiB of shared memory each (4
+// consumer warps) or one CTA per SM under 227 KiB (8 consumer warps).
 template <int BITS, int AT>
 cudaError_t launch_bits(const Params& p, int nt8, cudaStream_t st, bool pdl) {
     switch (nt8) {
-        case 1: return launch_t<BITS, AT, 1, 8>(p, st, pdl);
-        case 2: return launch_t<BITS, AT, 2, 8>(p, st, pdl);
-        case 4: return launch_t<BITS, AT, 4, 6>(p, st, pdl);
-        default: return launch_t<BITS, AT, 8, 5>(p, st, pdl);
+        case 1: return launch_t<BITS, AT, 1, 4, 4>(p, st, pdl);
+        case 2: return launch_t<BITS, AT, 2, 4, 4>(p, st, pdl);
+        default: return launch_t<BITS, AT, 4, 8, 7>(p, st, pdl);
     }
 }
 
@@ -550,24 +600,29 @@ const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t
     const int64_t kb = native_kblock(bits);
     if (k % kb != 0) return "k must be a multiple of 64 (4-bit) / 32 (8-bit) for the tensor-core path";
     if (!(g >= k || g % 16 == 0)) return "group size must be a multiple of 16 (or span the row)";
-    if (g < kb && kb % g != 0) return "unsupported group size";
+    if (k >= (int64_t(1) << 30)) return "k too large";
     return nullptr;
 }
 
 // Workspace: [counters: fixed 64 KiB][stream-K partial slots].  The counters sit
 // at a fixed offset so that, whatever shapes share one workspace, partial data
 // never lands on a counter (they self-reset to zero and must start at zero).
-constexpr size_t kCounterBytes = 64 * 1024;  // 16384 row-blocks (>= 2M channels)
+constexpr size_t kCounterBytes = 64 * 1024;  // 16384 row-blocks (>= 4M channels)
 
 size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t g) {
     (void)g;
     const int64_t kb = native_kblock(bits);
-    const int nt8 = wg::nt8_for(m < 64 ? m : 64), mt = wg::mt_for(nt8);
-    const int64_t strips = 8 * mt;
-    const int64_t NS = (n + 15) / 16, NB = (NS + strips - 1) / strips;
+    const int nt8 = wg::nt8_for(m < 32 ? m : 32);
+    const int64_t NS = (n + 15) / 16, NB = (NS + wg::kStrips - 1) / wg::kStrips;
     const int64_t U = NB * (k / kb > 0 ? k / kb : 1);
-    const int G = wg::ctas_for(U, nt8);
-    return kCounterBytes + size_t(G) * 2 * 256 * (mt * nt8 * 4) * sizeof(float);
+    size_t part = 0;
+    for (int t : {1, 2, 4}) {  // every variant a call may launch (token chunks of <= 32)
+        if (t > nt8) break;
+        const int G = wg::ctas_for(U, t);
+        const size_t need = size_t(G) * 2 * (16 * 32 * t * 4) * sizeof(float);
+        part = need > part ? need : part;
+    }
+    return kCounterBytes + part;
 }
 
 cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
@@ -578,36 +633,22 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
     p.N = A.n;
     p.K = A.k;
     p.NS = int((A.n + 15) / 16);
+    p.NB = (p.NS + wg::kStrips - 1) / wg::kStrips;
     p.KBLK = int(A.k / kb);
-    if (A.g >= A.k) {  // one group spanning the row (per-channel)
-        p.scale_groups = 1;
-        p.steps_per_group = 0;
-        p.kb_group_mask = -1;
-        p.kb_per_group_shift = 0;
-    } else if (A.g >= kb) {
-        p.scale_groups = 1;
-        p.steps_per_group = 0;
-        p.kb_group_mask = int(A.g / kb) - 1;
-        p.kb_per_group_shift = __builtin_ctzll(uint64_t(A.g / kb));
-    } else {
-        p.scale_groups = int(kb / A.g);
-        p.steps_per_group = int(A.g / 16);
-        p.kb_group_mask = 0;
-        p.kb_per_group_shift = 0;
-    }
+    p.GPR = int(A.g >= A.k ? 1 : (A.k + A.g - 1) / A.g);
+    p.log2g = A.g >= A.k ? 30 : __builtin_ctzll(uint64_t(A.g));
     p.out_dtype = A.out_dtype;
     p.counters = static_cast<int*>(A.workspace);
     p.partials = reinterpret_cast<float*>(static_cast<char*>(A.workspace) + kCounterBytes);
-    if ((p.NS + 7) / 8 > int64_t(kCounterBytes / 4)) return cudaErrorInvalidValue;
+    if (p.NB > int(kCounterBytes / 4) || int64_t(p.NB) * p.KBLK >= (int64_t(1) << 31))
+        return cudaErrorInvalidValue;
+    p.U = p.NB * p.KBLK;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
-    for (int64_t m0 = 0; m0 < A.m; m0 += 64) {  // decode batches: one pass per 64 tokens
-        p.M = int(A.m - m0 < 64 ? A.m - m0 : 64);
+    for (int64_t m0 = 0; m0 < A.m; m0 += 32) {  // decode batches: one pass per 32 tokens
+        p.M = int(A.m - m0 < 32 ? A.m - m0 : 32);
         p.a = static_cast<const char*>(A.a) + m0 * A.k * 2;
         p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
-        const int nt8 = wg::nt8_for(p.M), strips = 8 * wg::mt_for(nt8);
-        p.NB = (p.NS + strips - 1) / strips;
-        if (int64_t(p.NB) * p.KBLK >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-        p.U = p.NB * p.KBLK;
+        const int nt8 = wg::nt8_for(p.M);
         p.G = wg::ctas_for(p.U, nt8);
         // PDL only between chunks of this call or when the caller vouches that the
         // previous kernel in the stream does not write this layer's weights.
