@@ -55,6 +55,7 @@ struct Params {
     int G;       // CTAs
     int out_dtype;
     int log2g;   // log2(group size); 30 when one group spans the row
+    int debug;   // RTNQ_WGEMM_DEBUG=2: producer skips all copies (compute-only profiling)
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------
@@ -282,6 +283,10 @@ wgemm_kernel(const Params p) {
             const uint32_t code_bytes = uint32_t(n * strips * 512);
             const uint32_t scale_bytes = uint32_t((g1 - g0 + 1) * strips * 32);
             uint8_t* st = smem + s * GG::STAGE_BYTES;
+            if (p.debug & 2) {
+                mbar_expect_tx(&full[s], 0);
+                return;
+            }
             mbar_expect_tx(&full[s], code_bytes + scale_bytes);
             bulk_g2s(st, p.codes + (int64_t(w.b) * kStrips * p.KBLK + int64_t(w.kb) * strips) * 512,
                      code_bytes, &full[s]);
@@ -293,7 +298,7 @@ wgemm_kernel(const Params p) {
             const uint32_t dst = smem_u32(smem + s * GG::STAGE_BYTES + CODE_BYTES + GG::SCALE_BYTES);
             const uint8_t* src = static_cast<const uint8_t*>(p.a) + int64_t(w.kb) * (KB * 2);
             const int chunks = n * (KB * 2 / 16);  // 16-byte chunks per row
-            for (int i = lane; i < p.M * chunks; i += 32) {
+            for (int i = lane; i < ((p.debug & 2) ? 0 : p.M * chunks); i += 32) {
                 const int r = i / chunks, ch = i - r * chunks;
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                                  dst + r * GG::ASTRIDE + ch * 16),
@@ -638,6 +643,7 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
     p.GPR = int(A.g >= A.k ? 1 : (A.k + A.g - 1) / A.g);
     p.log2g = A.g >= A.k ? 30 : __builtin_ctzll(uint64_t(A.g));
     p.out_dtype = A.out_dtype;
+    if (const char* e = std::getenv("RTNQ_WGEMM_DEBUG")) p.debug = std::atoi(e);
     p.counters = static_cast<int*>(A.workspace);
     p.partials = reinterpret_cast<float*>(static_cast<char*>(A.workspace) + kCounterBytes);
     if (p.NB > int(kCounterBytes / 4) || int64_t(p.NB) * p.KBLK >= (int64_t(1) << 31))
