@@ -153,37 +153,36 @@ void ro_unpack(const uint8_t* bytes, int64_t n, int bits, int8_t* out) {
     }
 }
 
-/* Native layout (this repository's GEMM operand order).  Rows
- * form 16-row strips (one mma.m16n8k16 A tile), 16 strips a 256-row row-block;
- * columns form k-blocks of 64 (4-bit) or 32 (8-bit) codes = 16 bytes per lane.
- * Order: row-block, then k-block, then strip within the block, then lane (32),
- * then 16 bytes -- a row-block is one contiguous run along K.  The last
- * row-block may hold fewer than 16 strips.  Inside a lane, each k16 step is one
- * 32-bit (4-bit) or 64-bit (8-bit) word holding that lane's 8 A-fragment
- * elements a0..a7 in the order the register dequantizer consumes them. */
-static int64_t native_kblock(int bits) { return bits == 4 ? 64 : 32; }
+/* Native layout (this repository's GEMM operand order): the
+ * tcgen05 A-operand order.  Rows form 128-row row-blocks (the last may be
+ * shorter); columns form k-blocks of 64 codes (zero-padded).  Each row owns
+ * 16-byte chunks (2 per k-block for 4-bit, 4 for 8-bit); within a (row-block,
+ * k-block) the chunk c of every row is stored consecutively, chunks in (k-block,
+ * c) order, row-blocks one after another -- a row-block is one contiguous run
+ * along K.  Inside a chunk each 32-bit word holds one k16 step's codes in the
+ * order the dequantizer emits TMEM columns {k, k+1}:
+ *   4-bit word: nibble j = code (j < 4 ? 2j : 2(j-4)+1) of its 8-code group;
+ *   8-bit word: byte b   = code 2(b&1) + (b>>1)        of its 4-code group. */
+static int64_t native_rows_in(int64_t rows, int64_t rb) {
+    int64_t left = rows - rb * 128;
+    return left < 128 ? left : 128;
+}
 
-/* index of the 512-byte (strip, k-block) chunk */
-static int64_t native_chunk(int64_t ns, int64_t kblk, int64_t strip, int64_t b) {
-    int64_t rb = strip / 16, sl = strip % 16;
-    int64_t in_rb = ns - rb * 16 < 16 ? ns - rb * 16 : 16;
-    return rb * 16 * kblk + b * in_rb + sl;
+static int64_t native_chunk(int bits, int64_t rows, int64_t kblk, int64_t r, int64_t kb,
+                            int64_t c) {
+    int64_t cpr = bits == 4 ? 2 : 4, rb = r / 128;
+    return rb * 128 * kblk * cpr + (kb * cpr + c) * native_rows_in(rows, rb) + r % 128;
 }
 
 static int64_t native_index(int bits, int64_t rows, int64_t cols, int64_t r, int64_t c) {
-    int64_t ns = (rows + 15) / 16, kb = native_kblock(bits), kblk = (cols + kb - 1) / kb;
-    int64_t s = r / 16, rr = r % 16, b = c / kb, cc = c % kb;
-    int64_t j = cc / 16, kk = cc % 16;
-    int64_t gid = rr % 8, hi_row = rr / 8, tig = (kk % 8) / 2, hi_k = kk / 8, lo = kk % 2;
-    int64_t lane = 4 * gid + tig;
-    int64_t e = 4 * hi_k + 2 * hi_row + lo; /* PTX m16n8k16 A fragment element */
-    int64_t base = native_chunk(ns, kblk, s, b) * 32 + lane;
+    int64_t kblk = (cols + 63) / 64, kb = c / 64, kk = c % 64;
     if (bits == 4) {
-        int64_t nib = (e % 2) * 4 + e / 2; /* word nibble j <-> reg (j%4), half j/4 */
-        return base * 32 + j * 8 + nib;
+        int64_t ch = kk / 32, cc = kk % 32, w = cc / 8, q = cc % 8;
+        int64_t j = (q % 2) ? 4 + q / 2 : q / 2;
+        return native_chunk(4, rows, kblk, r, kb, ch) * 32 + w * 8 + j;
     }
-    int64_t byte = (e / 4) * 4 + (e % 2) * 2 + (e / 2) % 2; /* words [a0 a2 a1 a3][a4 a6 a5 a7] */
-    return base * 16 + j * 8 + byte;
+    int64_t ch = kk / 16, cc = kk % 16, w = cc / 4, q = cc % 4;
+    return native_chunk(8, rows, kblk, r, kb, ch) * 16 + w * 4 + 2 * (q % 2) + q / 2;
 }
 
 /* layout_index, packing.cpp:57-66 (+ the native kind). */
@@ -198,11 +197,9 @@ int64_t ro_layout_index(int kind, int tr, int tc, int bits, int64_t rows, int64_
 
 /* layout_slots, packing.cpp:68-73 (+ native). */
 int64_t ro_layout_slots(int kind, int tr, int tc, int bits, int64_t rows, int64_t cols) {
+    (void)bits;
     if (kind == RO_ROW_MAJOR) return rows * cols;
-    if (kind == RO_NATIVE) {
-        int64_t kb = native_kblock(bits);
-        return ((rows + 15) / 16 * 16) * ((cols + kb - 1) / kb * kb);
-    }
+    if (kind == RO_NATIVE) return rows * ((cols + 63) / 64 * 64);
     return ((rows + tr - 1) / tr * tr) * ((cols + tc - 1) / tc * tc);
 }
 
@@ -239,21 +236,18 @@ void ro_decode_layout(const uint8_t* data, int64_t rows, int64_t cols, int bits,
         }
 }
 
-int64_t ro_native_scale_count(int64_t rows, int64_t gpr) { return gpr * ((rows + 15) / 16) * 16; }
 
-/* Native scale order [row-block][group][strip in block][gid][half] (the code
- * layout's chunk order with groups in place of k-blocks); row = 16*strip +
- * 8*half + gid.  Padded rows get 0. */
+/* Native scale order: per 128-row row-block, [group][row] with the block's
+ * row count padded to 8; padded rows get 0. */
+int64_t ro_native_scale_count(int64_t rows, int64_t gpr) { return gpr * ((rows + 7) / 8 * 8); }
+
 void ro_native_scales(const uint16_t* s16, int64_t rows, int64_t gpr, uint16_t* out) {
-    int64_t ns = (rows + 15) / 16;
-    for (int64_t s = 0; s < ns; ++s)
-        for (int64_t j = 0; j < gpr; ++j)
-            for (int64_t gid = 0; gid < 8; ++gid)
-                for (int64_t h = 0; h < 2; ++h) {
-                    int64_t r = 16 * s + 8 * h + gid;
-                    out[(native_chunk(ns, gpr, s, j) * 8 + gid) * 2 + h] =
-                        r < rows ? s16[r * gpr + j] : 0;
-                }
+    memset(out, 0, (size_t)ro_native_scale_count(rows, gpr) * 2);
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t j = 0; j < gpr; ++j) {
+            int64_t rb = r / 128, r8 = (native_rows_in(rows, rb) + 7) / 8 * 8;
+            out[rb * 128 * gpr + j * r8 + r % 128] = s16[r * gpr + j];
+        }
 }
 
 /* dequantize_tensor, quant.cpp:143-171: float(code) * scale (one f32 multiply). */

@@ -149,7 +149,7 @@ int64_t rtnq_layout_index(rtnq_layout l, int bits, int64_t rows, int64_t cols, i
     return layout_slot(to_layout(l), bits, rows, cols, r, c);
 }
 
-int64_t rtnq_native_scale_count(int64_t rows, int64_t gpr) { return gpr * ((rows + 15) / 16) * 16; }
+int64_t rtnq_native_scale_count(int64_t rows, int64_t gpr) { return gpr * ((rows + 7) / 8 * 8); }
 
 // ---- device API ----------------------------------------------------------------------
 

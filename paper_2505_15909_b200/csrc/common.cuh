@@ -65,71 +65,78 @@ struct Layout {
     int tr, tc;
 };
 
-__host__ __device__ __forceinline__ int64_t native_kblock(int bits) { return bits == 4 ? 64 : 32; }
+// Native layout: the tcgen05 A-operand order.  Rows form
+// 128-row row-blocks (one M=128 UMMA tile; the last block may be shorter);
+// columns form k-blocks of 64 codes (zero-padded).  Each (row-block, k-block)
+// tile stores, for each 16-byte chunk c of a row (2 chunks per row for 4-bit,
+// 4 for 8-bit), the chunks of all rows of the block consecutively:
+//   byte = ((rb_base + (kb * CPR + c) * rows(rb) + row) * 16 + byte_in_chunk
+// so a row-block is one contiguous run along K (a GEMM CTA streams contiguous
+// memory), and a warp reading chunk c of 32 consecutive rows issues one
+// conflict-free 512-byte LDS.128.  Inside a chunk, every 32-bit word holds 8
+// (4-bit) or 4 (8-bit) codes of one k16 step in the order the register
+// dequantizer emits TMEM columns {k, k+1}:
+//   4-bit word: nibble j = code (j < 4 ? 2j : 2(j-4)+1) of its 8-code group
+//   8-bit word: byte b   = code 2(b&1) + (b>>1)        of its 4-code group
+constexpr int kNativeRows = 128;  // rows per row-block (UMMA M)
+constexpr int kNativeKB = 64;     // codes per k-block
 
-// Native layout.  Rows form 16-row strips (one mma.m16n8k16 A
-// tile); 16 strips form a 256-row row-block.  Columns form k-blocks of 64 (4-bit)
-// or 32 (8-bit) codes = 16 bytes per lane.  Byte order:
-//   [row-block][k-block][strip in block][lane 0..31][16 bytes]
-// so every row-block's codes are one contiguous run along K (a GEMM CTA streams
-// contiguous memory) and one (row-block, k-block) is a contiguous 8 KiB tile.
-// The last row-block may hold fewer than 16 strips.  Inside a lane's 16 bytes each
-// k16 step is one word of the A fragment (a0..a7), in the order the register
-// dequantizer consumes it.
-constexpr int kNativeBlockStrips = 16;
+__host__ __device__ __forceinline__ int64_t native_kblock(int bits) {
+    (void)bits;
+    return kNativeKB;
+}
+__host__ __device__ __forceinline__ int native_cpr(int bits) { return bits == 4 ? 2 : 4; }
 
-__host__ __device__ __forceinline__ int64_t native_chunk(int64_t ns, int64_t kblk, int64_t strip,
-                                                         int64_t b) {
-    const int64_t rb = strip / kNativeBlockStrips, sl = strip % kNativeBlockStrips;
-    const int64_t in_rb = ns - rb * kNativeBlockStrips < kNativeBlockStrips
-                              ? ns - rb * kNativeBlockStrips : kNativeBlockStrips;
-    return rb * kNativeBlockStrips * kblk + b * in_rb + sl;  // index of the 512-byte chunk
+__host__ __device__ __forceinline__ int64_t native_rows_in(int64_t rows, int64_t rb) {
+    const int64_t left = rows - rb * kNativeRows;
+    return left < kNativeRows ? left : kNativeRows;
+}
+
+// 16-byte chunk index of (row r, k-block kb, chunk c).
+__host__ __device__ __forceinline__ int64_t native_chunk(int bits, int64_t rows, int64_t kblk,
+                                                         int64_t r, int64_t kb, int64_t c) {
+    const int64_t rb = r / kNativeRows, cpr = native_cpr(bits);
+    return rb * kNativeRows * kblk * cpr + (kb * cpr + c) * native_rows_in(rows, rb) +
+           r % kNativeRows;
 }
 
 __host__ __device__ __forceinline__ int64_t native_slot(int bits, int64_t rows, int64_t cols,
                                                         int64_t r, int64_t c) {
-    const int64_t ns = (rows + 15) / 16, kb = native_kblock(bits);
-    const int64_t kblk = (cols + kb - 1) / kb;
-    const int64_t s = r >> 4, rr = r & 15, b = c / kb, cc = c % kb;
-    const int64_t j = cc >> 4, kk = cc & 15;
-    const int64_t gid = rr & 7, hi_row = rr >> 3, tig = (kk & 7) >> 1, hi_k = kk >> 3,
-                  lo = kk & 1;
-    const int64_t lane = 4 * gid + tig;
-    const int64_t e = 4 * hi_k + 2 * hi_row + lo;
-    const int64_t base = native_chunk(ns, kblk, s, b) * 32 + lane;
-    if (bits == 4) return base * 32 + j * 8 + (e & 1) * 4 + (e >> 1);
-    return base * 16 + j * 8 + (e >> 2) * 4 + (e & 1) * 2 + ((e >> 1) & 1);
+    const int64_t kblk = (cols + kNativeKB - 1) / kNativeKB;
+    const int64_t kb = c / kNativeKB, kk = c % kNativeKB;
+    if (bits == 4) {
+        const int64_t ch = kk >> 5, cc = kk & 31;  // chunk, code within chunk
+        const int64_t w = cc >> 3, q = cc & 7;     // word, code within the word's group
+        const int64_t j = (q & 1) ? 4 + (q >> 1) : (q >> 1);
+        return native_chunk(4, rows, kblk, r, kb, ch) * 32 + w * 8 + j;
+    }
+    const int64_t ch = kk >> 4, cc = kk & 15;
+    const int64_t w = cc >> 2, q = cc & 3;
+    return native_chunk(8, rows, kblk, r, kb, ch) * 16 + w * 4 + 2 * (q & 1) + (q >> 1);
 }
 
 // Inverse of native_slot: slot -> (r, c); returns false for padding slots.
 __host__ __device__ __forceinline__ bool native_coords(int bits, int64_t rows, int64_t cols,
                                                        int64_t slot, int64_t* r, int64_t* c) {
-    const int64_t ns = (rows + 15) / 16, kb = native_kblock(bits);
-    const int64_t kblk = (cols + kb - 1) / kb;
-    int64_t e, j, rest;
+    const int64_t kblk = (cols + kNativeKB - 1) / kNativeKB, cpr = native_cpr(bits);
+    int64_t chunk, cc;
     if (bits == 4) {
-        const int64_t nib = slot & 7;
-        j = (slot >> 3) & 3;
-        rest = slot >> 5;
-        e = 2 * (nib & 3) + (nib >> 2);
+        chunk = slot >> 5;
+        const int64_t within = slot & 31, w = within >> 3, j = within & 7;
+        cc = w * 8 + (j < 4 ? 2 * j : 2 * (j - 4) + 1);
     } else {
-        const int64_t byte = slot & 7;
-        j = (slot >> 3) & 1;
-        rest = slot >> 4;
-        const int64_t b2 = byte & 3;
-        e = (byte >> 2) * 4 + (b2 & 1) * 2 + (b2 >> 1);
+        chunk = slot >> 4;
+        const int64_t within = slot & 15, w = within >> 2, b = within & 3;
+        cc = w * 4 + 2 * (b & 1) + (b >> 1);
     }
-    const int64_t lane = rest & 31;
-    const int64_t chunk = rest >> 5;
-    const int64_t per_rb = int64_t(kNativeBlockStrips) * kblk;
+    const int64_t per_rb = int64_t(kNativeRows) * kblk * cpr;
     const int64_t rb = chunk / per_rb, off = chunk % per_rb;
-    const int64_t in_rb = ns - rb * kNativeBlockStrips < kNativeBlockStrips
-                              ? ns - rb * kNativeBlockStrips : kNativeBlockStrips;
-    const int64_t b = off / in_rb, s = rb * kNativeBlockStrips + off % in_rb;
-    const int64_t gid = lane >> 2, tig = lane & 3;
-    const int64_t hi_k = e >> 2, hi_row = (e >> 1) & 1, lo = e & 1;
-    *r = 16 * s + gid + 8 * hi_row;
-    *c = b * kb + j * 16 + 2 * tig + 8 * hi_k + lo;
+    const int64_t rin = native_rows_in(rows, rb);
+    if (rin <= 0) return false;
+    const int64_t kbc = off / rin, row = off % rin;
+    const int64_t kb = kbc / cpr, ch = kbc % cpr;
+    *r = rb * kNativeRows + row;
+    *c = kb * kNativeKB + ch * (bits == 4 ? 32 : 16) + cc;
     return *r < rows && *c < cols;
 }
 
@@ -161,10 +168,8 @@ __host__ __device__ __forceinline__ bool layout_coords(const Layout& L, int bits
 __host__ __device__ __forceinline__ int64_t layout_slots_of(const Layout& L, int bits,
                                                             int64_t rows, int64_t cols) {
     if (L.kind == RTNQ_ROW_MAJOR) return rows * cols;
-    if (L.kind == RTNQ_NATIVE_SM100) {
-        const int64_t kb = native_kblock(bits);
-        return ((rows + 15) / 16 * 16) * ((cols + kb - 1) / kb * kb);
-    }
+    if (L.kind == RTNQ_NATIVE_SM100)
+        return rows * ((cols + kNativeKB - 1) / kNativeKB * kNativeKB);
     return ((rows + L.tr - 1) / L.tr * L.tr) * ((cols + L.tc - 1) / L.tc * L.tc);
 }
 
@@ -175,13 +180,16 @@ __device__ __forceinline__ int code_at_slot(const uint8_t* data, int bits, int64
     return int((slot & 1) ? (b >> 4) : (b & 0x0F)) - 8;
 }
 
-// Native scale order [row-block][group][strip in block][gid][half], f16, with
-// row = 16*strip + 8*half + gid: a row-block's scales are one contiguous run
-// along K, like its codes.  Padded rows hold 0.
+// Native scale order: per 128-row row-block, [group][row] with the row count
+// padded to 8 (so a block's scales for consecutive groups are one contiguous,
+// 16-byte-aligned run); padded rows hold 0.
+__host__ __device__ __forceinline__ int64_t native_scale_rows8(int64_t rows, int64_t rb) {
+    return (native_rows_in(rows, rb) + 7) / 8 * 8;
+}
 __host__ __device__ __forceinline__ int64_t native_scale_index(int64_t rows, int64_t gpr,
                                                                int64_t r, int64_t group) {
-    const int64_t ns = (rows + 15) / 16;
-    return (native_chunk(ns, gpr, r >> 4, group) * 8 + (r & 7)) * 2 + ((r >> 3) & 1);
+    const int64_t rb = r / kNativeRows;
+    return rb * kNativeRows * gpr + group * native_scale_rows8(rows, rb) + r % kNativeRows;
 }
 
 __device__ __forceinline__ float load_scale(const void* scales, int dtype, int order,

@@ -116,19 +116,16 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ codes, Layout L, int 
 
 __global__ void native_scales_kernel(const void* __restrict__ scales, int dtype, int64_t rows,
                                      int64_t gpr, uint16_t* __restrict__ out) {
-    const int64_t ns = (rows + 15) / 16, n = gpr * ns * 16;
+    const int64_t n = gpr * ((rows + 7) / 8 * 8);
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
-        // invert native_scale_index: i -> (chunk, gid, half) -> (strip, group)
-        const int64_t half = i & 1, gid = (i >> 1) & 7, chunk = i >> 4;
-        const int64_t per_rb = int64_t(kNativeBlockStrips) * gpr;
-        const int64_t rb = chunk / per_rb, off = chunk % per_rb;
-        const int64_t in_rb = ns - rb * kNativeBlockStrips < kNativeBlockStrips
-                                  ? ns - rb * kNativeBlockStrips : kNativeBlockStrips;
-        const int64_t j = off / in_rb, strip = rb * kNativeBlockStrips + off % in_rb;
-        const int64_t r = 16 * strip + 8 * half + gid;
+        // invert native_scale_index: i -> (row-block, group, row)
+        const int64_t rb = i / (int64_t(kNativeRows) * gpr), off = i % (int64_t(kNativeRows) * gpr);
+        const int64_t r8 = native_scale_rows8(rows, rb);
+        const int64_t j = off / r8, row = off % r8;
+        const int64_t r = rb * kNativeRows + row;
         uint16_t h = 0;
-        if (r < rows) {
+        if (row < native_rows_in(rows, rb)) {
             if (dtype == RTNQ_F16) h = static_cast<const uint16_t*>(scales)[r * gpr + j];
             else h = __half_as_ushort(__float2half_rn(load_elem(scales, dtype, r * gpr + j)));
         }
@@ -206,7 +203,7 @@ void launch_dequant(const uint8_t* codes, Layout L, int bits, int64_t rows, int6
 
 void launch_native_scales(const void* scales, int dtype, int64_t rows, int64_t gpr,
                           uint16_t* out, cudaStream_t st) {
-    const int64_t n = gpr * ((rows + 15) / 16) * 16;
+    const int64_t n = gpr * ((rows + 7) / 8 * 8);
     if (n == 0) return;
     native_scales_kernel<<<grid_for(n), 256, 0, st>>>(scales, dtype, rows, gpr, out);
 }

@@ -175,35 +175,36 @@ quant_fused_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, int64
         }
     }
 
-    // ---- native: whole 512-byte k-blocks ----
+    // ---- native: 16 rows x 2 k-blocks of the tcgen05 row-run layout ----
     if (nat) {
-        const int64_t ns = (rows + 15) / 16;
+        const int64_t kblk = cols / kNativeKB;
         if constexpr (BITS == 4) {
-            const int q = t >> 7, o = 4 * (t & 127), lane = o >> 4, j = (o & 15) >> 2;
-            const int gid = lane >> 2, tig = lane & 3;
+            const int w = t & 3, row = (t >> 2) & 15, c = (t >> 6) & 1, kbl = t >> 7;
             uint32_t p = 0;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int rr = gid + 8 * ((e >> 1) & 1);
-                const int cc = q * 64 + j * 16 + 2 * tig + 8 * (e >> 2) + (e & 1);
-                p |= uint32_t(sc[rr][cc] + 8) << (4 * ((e & 1) * 4 + (e >> 1)));
+            for (int j = 0; j < 8; ++j) {
+                const int q = j < 4 ? 2 * j : 2 * (j - 4) + 1;
+                p |= uint32_t(sc[row][kbl * 64 + c * 32 + w * 8 + q] + 8) << (4 * j);
             }
-            const int64_t kb = cb * 2 + q;
-            *reinterpret_cast<uint32_t*>(nat + native_chunk(ns, cols / 64, strip, kb) * 512 + o) = p;
+            const int64_t r = strip * kTileR + row;
+            if (r < rows)
+                *reinterpret_cast<uint32_t*>(
+                    nat + native_chunk(4, rows, kblk, r, cb * 2 + kbl, c) * 16 + 4 * w) = p;
         } else {
-            const int q = t >> 6, o = 8 * (t & 63), lane = o >> 4, j = (o & 15) >> 3;
-            const int gid = lane >> 2, tig = lane & 3;
+            const int wp = t & 1, row = (t >> 1) & 15, c = (t >> 5) & 3, kbl = t >> 7;
             uint32_t w2[2] = {0, 0};
 #pragma unroll
-            for (int pb = 0; pb < 8; ++pb) {
-                const int e = (pb >> 2) * 4 + (pb & 1) * 2 + ((pb >> 1) & 1);
-                const int rr = gid + 8 * ((e >> 1) & 1);
-                const int cc = q * 32 + j * 16 + 2 * tig + 8 * (e >> 2) + (e & 1);
-                w2[pb >> 2] |= uint32_t(uint8_t(sc[rr][cc] + 128)) << (8 * (pb & 3));
-            }
-            const int64_t kb = cb * 4 + q;
-            *reinterpret_cast<uint2*>(nat + native_chunk(ns, cols / 32, strip, kb) * 512 + o) =
-                make_uint2(w2[0], w2[1]);
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int q = 2 * (b & 1) + (b >> 1);
+                    w2[h] |= uint32_t(uint8_t(sc[row][kbl * 64 + c * 16 + (2 * wp + h) * 4 + q] + 128))
+                             << (8 * b);
+                }
+            const int64_t r = strip * kTileR + row;
+            if (r < rows)
+                *reinterpret_cast<uint2*>(nat + native_chunk(8, rows, kblk, r, cb * 2 + kbl, c) * 16 +
+                                          8 * wp) = make_uint2(w2[0], w2[1]);
         }
     }
 }
