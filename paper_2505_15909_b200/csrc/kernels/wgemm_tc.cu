@@ -2,29 +2,33 @@
 //
 // out[m][n] = sum_k a[m][k] * code[n][k] * S[n][k/g]   (gemm.hpp:18-27)
 //
-// One CTA computes a 128-row (output channel) x NT-token tile over a stream-K
-// range of 64-code k-blocks.  Warp roles:
-//   warp 4  producer: one cp.async.bulk (TMA) per stage for the codes of up to
-//           KPS k-blocks (the native layout makes a row-block contiguous along K),
-//           one for their f16 group scales, and 16-byte cp.async for the
-//           activations, written directly in the UMMA K-major core-matrix order;
-//           all complete on the stage's mbarrier.
-//   warps 0-3 dequantizers: warp q owns TMEM lanes 32q..32q+31 = rows 32q+lane.
-//           Each thread turns its row's codes into exact bf16/f16 integers with
-//           LOP3/PRMT magic numbers and writes them with tcgen05.st straight into
-//           a TMEM A-operand ring slot (32 columns = one k-block).  The same warps
-//           are the epilogue: per quantization group they tcgen05.ld the f32
-//           block accumulator and do acc += S[row][group] * block in registers --
-//           the reference's block-then-scale structure (gemm.cpp:69-87) with
-//           exact codes and the scale applied in f32.
-//   warp 5  MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.
-//           kind::f16 with A in TMEM, B (activations) from shared memory and D in
-//           TMEM (M=128, N=NT, K=16), and tcgen05.commit's to free A slots, smem
-//           stages and publish finished group accumulators.
+// One persistent CTA per SM computes 128-row (output channel) x NT-token tiles
+// over a stream-K range of 64-code k-blocks, walked in units of two k-blocks
+// (one stage, one A-ring slot, one synchronisation step).  Four decoupled warp
+// roles joined by mbarriers:
+//   warp 12 producer: per unit, one cp.async.bulk (TMA engine) for the codes (the
+//           native layout makes a row-block one contiguous run along K) plus
+//           16-byte cp.async for the activations, written in the UMMA K-major
+//           core-matrix order; both complete on the stage mbarrier.
+//   warps 0-7 dequantizers: warp w owns TMEM lanes 32(w&3).. = rows 32(w&3)+lane
+//           of the units with parity w>>2 (two warps per SM sub-partition hide
+//           each other's latency).  Each thread turns its row's codes into exact
+//           bf16/f16 integers with LOP3/PRMT magic numbers and tcgen05.st's them
+//           into the unit's TMEM A-ring slot.
+//   warp 13 MMA issuer: a single thread issues tcgen05.mma.cta_group::1.kind::f16,
+//           A (weights) from TMEM, B (activations) from shared memory, D in TMEM
+//           (M=128, N=NT, K=16), one D buffer per quantization group, and
+//           tcgen05.commit's to free A slots and stages and publish finished groups.
+//   warps 8-11 epilogue: per quantization group, tcgen05.ld of the f32 block sum
+//           and acc += S[row][group] * block in registers -- the reference's
+//           block-then-scale structure (gemm.cpp:69-87) with exact integer codes
+//           and the f16 group scale applied in f32.  The scale is read straight
+//           from global memory (one coalesced 64-byte load per warp per group).
 // Stream-K: the (row-block, k-block) units are split evenly over the grid;
 // row-blocks shared by several CTAs are combined by the last CTA to arrive,
 // summing partials in CTA order (deterministic; no float atomics).
 // PDL (opt-in): weight prefetch for the first stages precedes griddepcontrol.wait.
+#include <cuda.h>  // CUtensorMap (the map is encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -37,11 +41,18 @@ namespace tc {
 
 constexpr int kRows = kNativeRows;  // 128: UMMA M
 constexpr int kKB = kNativeKB;      // 64 codes per k-block
-constexpr int kRA = 4;              // TMEM A-operand ring slots (k-blocks)
-constexpr int kDequantWarps = 4;
-constexpr int kThreads = (kDequantWarps + 2) * 32;
+constexpr int kKPU = 2;             // k-blocks per unit (one A-ring slot = 64 TMEM columns)
+constexpr int kDequantWarps = 8;    // warps 0-7: quadrant w & 3, unit parity w >> 2
+constexpr int kEpiWarps = 4;        // warps 8-11: quadrant w & 3
+constexpr int kEpiWarp0 = 8;
+constexpr int kProducerWarp = 12;
+constexpr int kMmaWarp = 13;
+constexpr int kThreads = 14 * 32;
+constexpr int kRA = 4;              // A-ring slots (4 x 64 = 256 TMEM columns)
+constexpr int kTmemCols = 512;      // one CTA per SM owns all of TMEM
 
 struct Params {
+    CUtensorMap tmap_a;  // activations as [k-chunk][token][8 elements]; OOB (m >= M, k >= K) -> 0
     const void* a;
     const uint8_t* codes;
     const uint16_t* scales;
@@ -50,6 +61,7 @@ struct Params {
     int* counters;
     int64_t N, K;
     int M;      // tokens in this launch (<= NT)
+    int m0;     // first token of this launch (TMA coordinate)
     int NB;     // 128-row row-blocks
     int KBLK;   // 64-code k-blocks
     int GPR;    // scale groups per row
@@ -57,7 +69,9 @@ struct Params {
     int G;      // CTAs
     int out_dtype;
     int log2g;  // log2(group); 30 when one group spans the row
-    int debug;  // RTNQ_WGEMM_DEBUG=2: producer copies nothing (compute-only profiling)
+    int full_k; // K rounded to the MMA step (groups past K fold into the last group)
+    int debug;  // RTNQ_WGEMM_DEBUG bits (profiling only): 2 no copies, 4 no MMA, 8 no tcgen05.st,
+                //   16 no tcgen05.ld, 32 per-CTA globaltimer stamps into the counter region
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------
@@ -80,10 +94,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred P;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n"
         "@!P bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "n"(10000000)  // suspend-time hint (ns): sleep, don't spin
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -92,6 +106,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
             "r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -203,41 +229,41 @@ __device__ __forceinline__ void store_out(void* out, int dt, int64_t i, float v)
 }
 
 // ---- geometry ------------------------------------------------------------------------------
-template <int BITS, int NT, int STAGES>
+template <int BITS, int NT>
 struct Geo {
     static constexpr int CPR = BITS == 4 ? 2 : 4;                  // 16-B chunks / row / k-block
-    static constexpr int KPS = BITS == 4 ? 4 : 2;                  // k-blocks per stage
-    static constexpr int CODE_BYTES = KPS * CPR * kRows * 16;      // 16 KiB
-    static constexpr int MAX_GROUPS = KPS * kKB / 16;              // groups of >= 16 codes
-    static constexpr int SCALE_BYTES = MAX_GROUPS * kRows * 2;
-    static constexpr int ACT_KCH = KPS * kKB / 8;                  // 16-B k-chunks per token row
-    static constexpr int ACT_BYTES = NT * ACT_KCH * 16;
-    static constexpr int ACT_OFF = CODE_BYTES + SCALE_BYTES;
+    static constexpr int CODE_BYTES = kKPU * CPR * kRows * 16;     // 8 KiB (W4) / 16 KiB (W8)
+    static constexpr int ACT_KCH = kKPU * kKB / 8;                 // 16-B k-chunks per unit
+    static constexpr int ACT_BYTES = NT * ACT_KCH * 16;            // one TMA box [chunk][token][16 B]
+    static constexpr int ACT_OFF = CODE_BYTES;
     static constexpr int STAGE_BYTES = (ACT_OFF + ACT_BYTES + 1023) / 1024 * 1024;
+    static constexpr int STAGES_FIT = (220 * 1024) / STAGE_BYTES / 2 * 2;
+    static constexpr int STAGES = STAGES_FIT > 16 ? 16 : STAGES_FIT;  // even: parity-owned
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-    static constexpr int SMEM = BAR_OFF + 1024 + 1024;  // barriers + alignment slack
-    static constexpr int NDB_MAX = 8;                     // D buffers (2 per group in a k-block)
-    static constexpr int TMEM_COLS = 256;                 // A ring 128 + D <= 128
+    static constexpr int SMEM = BAR_OFF + 1024 + 1024;            // barriers + alignment slack
+    static constexpr int D_COL0 = kRA * kKPU * 32;                // 256
+    static constexpr int ND_FIT = (kTmemCols - D_COL0) / NT;
+    static constexpr int ND = ND_FIT > 16 ? 16 : ND_FIT;         // group accumulators
+    static_assert(STAGES >= 4 && ND >= 2 && (ND & (ND - 1)) == 0, "tile does not fit");
 };
 
 __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
     return int(((u + 1) * G - 1) / U);
 }
 
-// The stage sequence of a CTA: chunks of <= KPS k-blocks that never cross a
-// row-block (segment) boundary.  Producer, MMA issuer and dequantizers walk it alike.
+// The unit sequence of a CTA: chunks of <= kKPU k-blocks that never cross a
+// row-block (segment) boundary.  Every role walks it alike.
 struct Walker {
-    int u, u1, b, kb, KBLK, KPS;
-    __device__ Walker(int u0_, int u1_, int KBLK_, int KPS_)
-        : u(u0_), u1(u1_), KBLK(KBLK_), KPS(KPS_) {
+    int u, u1, b, kb, KBLK;
+    __device__ Walker(int u0_, int u1_, int KBLK_) : u(u0_), u1(u1_), KBLK(KBLK_) {
         b = u0_ / KBLK_;
         kb = u0_ - b * KBLK_;
     }
     __device__ bool more() const { return u < u1; }
-    __device__ int chunk() const {
-        const int left_seg = KBLK - kb, left = u1 - u;
+    __device__ int chunk() const {  // units start at even k-blocks (group-aligned for g >= 128)
+        const int left_seg = KBLK - kb, left = u1 - u, cap = kKPU - (kb & 1);
         const int n = left_seg < left ? left_seg : left;
-        return n < KPS ? n : KPS;
+        return n < cap ? n : cap;
     }
     __device__ bool seg_end(int n) const { return kb + n == KBLK || u + n == u1; }
     __device__ void advance(int n) {
@@ -247,50 +273,162 @@ struct Walker {
     }
 };
 
-template <int BITS, int AT, int NT, int STAGES, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) wgemm_tc_kernel(const Params p) {
-    using GG = Geo<BITS, NT, STAGES>;
-    constexpr int CPR = GG::CPR, KPS = GG::KPS;
+// Does a quantization group end after the k16 step whose last code is knext-1?
+// Steps past the end of the row (zero padding) fold into the row's last group.
+__device__ __forceinline__ bool group_ends(int knext, int gmask, int full_k, bool last_step) {
+    return last_step || (((knext & gmask) == 0) && knext <= full_k);
+}
+
+// Bit kk set: a group's accumulator is complete after k16 step kk of the unit that
+// starts at code kbase and has `steps` steps.  For g >= 128 a unit (which starts at an
+// even k-block) lies inside one group, so only its last step can end one.
+__device__ __forceinline__ uint32_t unit_ends(int kbase, int steps, bool seg_end, int log2g,
+                                              int gmask, int full_k) {
+    if (log2g >= 7) {
+        const int kn = kbase + steps * 16;
+        return (seg_end || (((kn & gmask) == 0) && kn <= full_k)) ? 1u << (steps - 1) : 0u;
+    }
+    uint32_t e = 0;
+#pragma unroll
+    for (int kk = 0; kk < kKPU * 4; ++kk)
+        if (kk < steps && group_ends(kbase + (kk + 1) * 16, gmask, full_k, seg_end && kk == steps - 1))
+            e |= 1u << kk;
+    return e;
+}
+
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* d) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+          "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+          "=r"(d[14]), "=r"(d[15])
+        : "r"(taddr)
+        : "memory");
+}
+
+// Warp-uniform issue: every lane executes the asm, elect.sync picks one lane to issue,
+// so the compiler sees no divergence (no per-MMA ELECT/R2UR loop).
+__device__ __forceinline__ void umma_f16_elect(uint32_t d_addr, uint32_t a_addr, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_addr),
+        "r"(a_addr), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// All k16 steps of a unit into one accumulator in one asm block: 4 (one k-block) or
+// 8 (two) MMAs, a_addr advancing 8 TMEM columns and the B descriptor 256 bytes per step.
+template <int STEPS, uint32_t BSTEP>
+__device__ __forceinline__ void umma_unit_elect(uint32_t d_addr, uint32_t a_addr, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+    static_assert(STEPS == 4 || STEPS == 8, "");
+    if constexpr (STEPS == 4)
+        asm volatile(
+            "{\n.reg .pred e, p, t;\n.reg .b32 a1, a2, a3;\n.reg .b64 b1, b2, b3;\n"
+            "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
+            "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\n"
+            "add.u64 b1, %2, %5;\nadd.u64 b2, b1, %5;\nadd.u64 b3, b2, %5;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n}\n" ::"r"(d_addr),
+            "r"(a_addr), "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(BSTEP)
+            : "memory");
+    else
+        asm volatile(
+            "{\n.reg .pred e, p, t;\n.reg .b32 a1, a2, a3, a4, a5, a6, a7;\n"
+            ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
+            "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
+            "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\nadd.u32 a4, %1, 32;\n"
+            "add.u32 a5, %1, 40;\nadd.u32 a6, %1, 48;\nadd.u32 a7, %1, 56;\n"
+            "add.u64 b1, %2, %5;\nadd.u64 b2, b1, %5;\nadd.u64 b3, b2, %5;\nadd.u64 b4, b3, %5;\n"
+            "add.u64 b5, b4, %5;\nadd.u64 b6, b5, %5;\nadd.u64 b7, b6, %5;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, t;\n}\n" ::"r"(d_addr),
+            "r"(a_addr), "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(BSTEP)
+            : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// Profiling-only instrumentation (RTNQ_WGEMM_DEBUG & 32): per-CTA globaltimer stamps,
+// read back by rtnq_wgemm_debug_read.
+__device__ unsigned long long g_wgemm_dbg[1024 * 64];
+__device__ __forceinline__ void stamp(const Params& p, int slot) {
+    if (!(p.debug & 32)) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_wgemm_dbg[blockIdx.x * 64 + slot] = t;
+}
+
+// PROF=true (RTNQ_WGEMM_DEBUG & 32) accumulates, per role, the SM cycles each wait
+// blocks, in registers, and stores them at the end (profiling builds only).
+#define PWAIT(bar, par, slot)                                   \
+    do {                                                        \
+        if constexpr (PROF) {                                   \
+            const long long t0_ = clock64();                    \
+            mbar_wait(bar, par);                                \
+            pacc[slot] += clock64() - t0_;                      \
+        } else {                                                \
+            mbar_wait(bar, par);                                \
+        }                                                       \
+    } while (0)
+
+template <int BITS, int AT, int NT, bool PROF>
+__global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params p) {
+    using GG = Geo<BITS, NT>;
+    constexpr int CPR = GG::CPR, STAGES = GG::STAGES, ND = GG::ND;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);
-    uint64_t* full = bars;                      // [STAGES] producer -> consumers
-    uint64_t* empty = full + STAGES;            // [STAGES] consumers -> producer
-    uint64_t* a_full = empty + STAGES;          // [kRA] dequant -> MMA
-    uint64_t* a_empty = a_full + kRA;           // [kRA] MMA -> dequant
-    uint64_t* d_full = a_empty + kRA;           // [NDB_MAX] MMA -> epilogue
-    uint64_t* d_empty = d_full + GG::NDB_MAX;   // [NDB_MAX] epilogue -> MMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + GG::NDB_MAX);
+    uint64_t* full = bars;                  // [STAGES] producer -> dequant + MMA
+    uint64_t* empty = full + STAGES;        // [STAGES] dequant + MMA -> producer
+    uint64_t* a_full = empty + STAGES;      // [kRA] dequant -> MMA
+    uint64_t* a_empty = a_full + kRA;       // [kRA] MMA -> dequant
+    uint64_t* d_full = a_empty + kRA;       // [ND] MMA -> epilogue
+    uint64_t* d_empty = d_full + ND;        // [ND] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + ND);
     volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
+    if (threadIdx.x == 0) stamp(p, 0);
     const int u0 = int(int64_t(c) * p.U / p.G), u1 = int(int64_t(c + 1) * p.U / p.G);
     const int gmask = (1 << p.log2g) - 1;
-    // D buffers: 2 per group that can end inside one k-block (groups of >= 16 codes)
-    const int gpkb = p.log2g >= 6 ? 1 : (kKB >> p.log2g);
-    const int ndb = 2 * gpkb;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1 + 32);           // expect_tx arrive + 32 lanes' cp.async
-            mbar_init(&empty[s], kDequantWarps + 1);  // dequant warps + MMA commit
+            mbar_init(&full[s], 1);        // producer's arrive.expect_tx (codes + activations)
+            mbar_init(&empty[s], 4 + 1);   // the parity's 4 dequant warps + MMA commit
         }
         for (int i = 0; i < kRA; ++i) {
-            mbar_init(&a_full[i], kDequantWarps);
+            mbar_init(&a_full[i], 4);
             mbar_init(&a_empty[i], 1);
         }
-        for (int i = 0; i < GG::NDB_MAX; ++i) {
+        for (int i = 0; i < ND; ++i) {
             mbar_init(&d_full[i], 1);
-            mbar_init(&d_empty[i], kDequantWarps);
+            mbar_init(&d_empty[i], kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == kDequantWarps + 1) {  // MMA warp owns the TMEM allocation
+    if (warp == kMmaWarp) {  // the MMA warp owns the TMEM allocation
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "n"(GG::TMEM_COLS));
+                     "n"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -298,48 +436,45 @@ __global__ void __launch_bounds__(kThreads, MINB) wgemm_tc_kernel(const Params p
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     grid_dep_launch();
+    if (threadIdx.x == 0) stamp(p, 1);
+    long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long prof_t0 = PROF ? clock64() : 0;
+    auto prof_store = [&](int base) {  // slots base..base+7 = phases, base+8 = role time
+        if constexpr (PROF) {
+            for (int i = 0; i < 8; ++i) g_wgemm_dbg[blockIdx.x * 64 + base + i] = pacc[i];
+            g_wgemm_dbg[blockIdx.x * 64 + base + 8] = clock64() - prof_t0;
+        }
+    };
+#define PT_BEGIN(v) long long v = PROF ? clock64() : 0
+#define PT_END(v, slot) do { if constexpr (PROF) pacc[slot] += clock64() - v; } while (0)
 
-    if (warp == kDequantWarps) {
+    if (warp == kProducerWarp) {
         // ===================== producer =====================
         const int64_t a_row = p.K * 2;
+        // Codes: one bulk copy of the unit's contiguous run.  Activations: one TMA box
+        // of 16 k-chunks x NT tokens.  Both complete on full[s] (one expected arrival).
         auto weights = [&](const Walker& w, int n, int s) {
             if (lane != 0) return;
             const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
-            const int rows8 = (rows + 7) / 8 * 8;
-            const int g0 = (w.kb * kKB) >> p.log2g, g1 = ((w.kb + n) * kKB - 1) >> p.log2g;
             const uint32_t code_bytes = uint32_t(n * CPR * rows * 16);
-            const uint32_t scale_bytes = uint32_t((g1 - g0 + 1) * rows8 * 2);
-            uint8_t* st = smem + s * GG::STAGE_BYTES;
-            if (p.debug & 2) {
-                mbar_expect_tx(&full[s], 0);
-                return;
-            }
-            mbar_expect_tx(&full[s], code_bytes + scale_bytes);
-            bulk_g2s(st,
+            if (p.debug & (2 | 128)) return;
+            mbar_expect_tx_only(&full[s], code_bytes);
+            bulk_g2s(smem + s * GG::STAGE_BYTES,
                      p.codes + (int64_t(w.b) * kRows * p.KBLK * CPR + int64_t(w.kb) * CPR * rows) * 16,
                      code_bytes, &full[s]);
-            bulk_g2s(st + GG::CODE_BYTES,
-                     p.scales + int64_t(w.b) * kRows * p.GPR + int64_t(g0) * rows8, scale_bytes,
-                     &full[s]);
         };
         auto acts = [&](const Walker& w, int n, int s) {
-            const uint32_t dst = smem_u32(smem + s * GG::STAGE_BYTES + GG::ACT_OFF);
-            const uint8_t* src = static_cast<const uint8_t*>(p.a) + int64_t(w.kb) * (kKB * 2);
-            const int kch = n * (kKB / 8);  // 16-byte chunks per token in this stage
-            const int total = (p.debug & 2) ? 0 : p.M * kch;
-            for (int i = lane; i < total; i += 32) {
-                const int t = i / kch, ch = i - t * kch;
-                // UMMA K-major core-matrix order: [token/8][k-chunk][token%8][16 B]
-                const uint32_t d = dst + ((t >> 3) * GG::ACT_KCH + ch) * 128 + (t & 7) * 16;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
-                             "l"(src + t * a_row + ch * 16)
-                             : "memory");
+            (void)n;
+            if (lane != 0) return;
+            if (p.debug & (2 | 64)) {
+                mbar_arrive(&full[s]);
+                return;
             }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                             smem_u32(&full[s]))
-                         : "memory");
+            mbar_expect_tx(&full[s], GG::ACT_BYTES);
+            tma_load_3d(smem + s * GG::STAGE_BYTES + GG::ACT_OFF, &p.tmap_a, 0, p.m0,
+                        w.kb * (kKB / 8), &full[s]);
         };
-        Walker w(u0, u1, p.KBLK, KPS);
+        Walker w(u0, u1, p.KBLK);
         int pro = 0;
         {
             Walker t = w;
@@ -359,109 +494,159 @@ __global__ void __launch_bounds__(kThreads, MINB) wgemm_tc_kernel(const Params p
         uint32_t ph = pro == STAGES ? 0u : 1u;
         while (w.more()) {
             const int n = w.chunk();
-            mbar_wait(&empty[s], ph);
+            PWAIT(&empty[s], ph, 0);
+            long long t1 = PROF ? clock64() : 0;
             weights(w, n, s);
+            if constexpr (PROF) { __syncwarp(); const long long t2 = clock64(); pacc[1] += t2 - t1; t1 = t2; }
             acts(w, n, s);
+            if constexpr (PROF) { __syncwarp(); pacc[2] += clock64() - t1; }
             w.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
-    } else if (warp == kDequantWarps + 1) {
-        // ===================== MMA issuer =====================
+        if (lane == 0) stamp(p, 2), prof_store(8);
+    } else if (warp == kMmaWarp) {
+        // ===================== MMA issuer (warp-uniform, one lane issues) =====================
         constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
         constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                    (uint32_t(NT >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
-        const uint32_t d_col0 = kRA * 32;
-        Walker w(u0, u1, p.KBLK, KPS);
-        int s = 0, ra = 0;
+        // B descriptor: K-major, no swizzle, smem [k-chunk][token][16 B]: LBO = NT*16 B
+        // (next k core matrix), SBO = 128 B (next 8 tokens); start address per stage/step.
+        constexpr uint64_t bdesc_hi = (uint64_t((NT * 16) >> 4) << 16) |
+                                      (uint64_t(128 >> 4) << 32) | (1ull << 46);
+        constexpr uint32_t kStep = (2 * NT * 16) >> 4;  // one k16 step = 2 k-chunks
+        const uint32_t act0 = smem_u32(smem + GG::ACT_OFF);
+        const uint32_t d_base = tmem + GG::D_COL0;
+        Walker w(u0, u1, p.KBLK);
+        int s = 0, slot = 0, ord = 0;
         uint32_t ph = 0, pha = 0;
-        int ord = 0;        // groups finished so far (D buffer = ord % ndb)
-        bool fresh = true;  // next MMA starts a group
+        uint32_t acc_flag = 0;  // 0: the next MMA starts a group
         while (w.more()) {
+            PT_BEGIN(tu);
             const int n = w.chunk();
             const bool seg_end = w.seg_end(n);
-            mbar_wait(&full[s], ph);
+            const int steps = n * 4, kbase = w.kb * kKB;
+            // k16 steps after which a group's accumulator is complete
+            const uint32_t ends = unit_ends(kbase, steps, seg_end, p.log2g, gmask, p.full_k);
+            PT_END(tu, 3);
+            PWAIT(&full[s], ph, 0);
+            PWAIT(&a_full[slot], pha, 1);
             tc_fence_after();
-            const uint32_t act = smem_u32(smem + s * GG::STAGE_BYTES + GG::ACT_OFF);
-            for (int kbl = 0; kbl < n; ++kbl) {
-                const int kb = w.kb + kbl;
-                mbar_wait(&a_full[ra], pha);
-                tc_fence_after();
+            PT_BEGIN(tm);
+            const uint64_t bdesc0 = bdesc_hi | uint64_t(((act0 + s * GG::STAGE_BYTES) >> 4) & 0x3FFFu);
+            const uint32_t a_base = tmem + slot * (kKPU * 32);
+            if ((ends & ~(1u << (steps - 1))) == 0) {
+                // fast path: the whole unit feeds one group accumulator (g >= 128)
+                const int buf = ord & (ND - 1);
+                if (acc_flag == 0 && ord >= ND) {
+                    PWAIT(&d_empty[buf], uint32_t((ord / ND - 1) & 1), 2);
+                    tc_fence_after();
+                }
+                if (!(p.debug & 4)) {
+                    if (steps == 8)
+                        umma_unit_elect<8, kStep>(d_base + buf * NT, a_base, bdesc0, idesc, acc_flag);
+                    else
+                        umma_unit_elect<4, kStep>(d_base + buf * NT, a_base, bdesc0, idesc, acc_flag);
+                }
+                acc_flag = 1;
+                if (ends) {
+                    tc_commit_elect(&d_full[buf]);
+                    ++ord;
+                    acc_flag = 0;
+                }
+            } else
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int buf = ord % ndb;
-                    if (fresh && ord >= ndb) {  // buffer reuse: wait for its epilogue
-                        mbar_wait(&d_empty[buf], uint32_t((ord / ndb - 1) & 1));
+            for (int kk = 0; kk < kKPU * 4; ++kk) {
+                if (kk < steps) {
+                    const int buf = ord & (ND - 1);
+                    if (acc_flag == 0 && ord >= ND) {  // buffer reuse: wait for its epilogue
+                        PWAIT(&d_empty[buf], uint32_t((ord / ND - 1) & 1), 2);
                         tc_fence_after();
                     }
-                    if (lane == 0) {
-                        const uint32_t sa = act + (kbl * 4 + t) * 2 * 128;
-                        const uint64_t bdesc = uint64_t((sa >> 4) & 0x3FFFu) |
-                                               (uint64_t(128 >> 4) << 16) |
-                                               (uint64_t((GG::ACT_KCH * 128) >> 4) << 32) |
-                                               (1ull << 46);
-                        const uint32_t d_addr = tmem + d_col0 + buf * NT;
-                        const uint32_t a_addr = tmem + ra * 32 + t * 8;
-                        asm volatile(
-                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
-                                d_addr),
-                            "r"(a_addr), "l"(bdesc), "r"(idesc), "r"(fresh ? 0 : 1)
-                            : "memory");
-                    }
-                    __syncwarp();
-                    fresh = false;
-                    const int knext = kb * kKB + (t + 1) * 16;
-                    if ((knext & gmask) == 0 || (seg_end && kbl == n - 1 && t == 3)) {
-                        if (lane == 0) tc_commit(&d_full[buf]);
+                    if (!(p.debug & 4))
+                        umma_f16_elect(d_base + buf * NT, a_base + kk * 8,
+                                       bdesc0 + uint64_t(kk * kStep), idesc, acc_flag);
+                    acc_flag = 1;
+                    if (ends & (1u << kk)) {
+                        tc_commit_elect(&d_full[buf]);
                         ++ord;
-                        fresh = true;
+                        acc_flag = 0;
                     }
                 }
-                if (lane == 0) tc_commit(&a_empty[ra]);
-                if (++ra == kRA) ra = 0, pha ^= 1u;
             }
-            if (lane == 0) tc_commit(&empty[s]);  // activations of this stage consumed
-            __syncwarp();
+            PT_END(tm, 4);
+            PT_BEGIN(tc);
+            tc_commit_elect(&a_empty[slot]);
+            tc_commit_elect(&empty[s]);  // activations of this stage consumed
+            PT_END(tc, 5);
             w.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
-            if (seg_end) fresh = true;
+            if (++slot == kRA) slot = 0, pha ^= 1u;
         }
-    } else {
-        // ===================== dequantizers + epilogue =====================
-        const int q = warp;                      // TMEM lane quadrant
-        const int row = q * 32 + lane;           // row within the row-block
+        if (lane == 0) stamp(p, 3), prof_store(20);
+    } else if (warp < kDequantWarps) {
+        // ===================== dequantizers =====================
+        const int q = warp & 3, par = warp >> 2;
+        const int row = q * 32 + lane;  // row within the row-block = TMEM lane
         const uint32_t lane_base = uint32_t(q * 32) << 16;
-        const uint32_t d_col0 = kRA * 32;
-        float acc[NT];
+        Walker w(u0, u1, p.KBLK);
+        int i = 0;  // unit index within this CTA
+        while (w.more()) {
+            const int n = w.chunk();
+            if ((i & 1) == par) {
+                const int s = i % STAGES, slot = i % kRA;
+                const uint32_t ph = uint32_t(i / STAGES) & 1u, pha = uint32_t(i / kRA) & 1u;
+                const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
+                PWAIT(&full[s], ph, 0);
+                const uint8_t* st = smem + s * GG::STAGE_BYTES + row * 16;
+                uint4 v[kKPU * CPR];
 #pragma unroll
-        for (int i = 0; i < NT; ++i) acc[i] = 0.0f;
-        // Groups whose accumulator is pending (finished in the previous k-block):
-        // consumed one k-block later so the MMAs have landed.
-        int pend_mask = 0, pend_ord0 = 0;  // bit t: a group ended after k16 step t
-        float pend_s[4] = {0, 0, 0, 0};
-        int ord = 0;
-
-        auto drain = [&]() {
+                for (int j = 0; j < kKPU * CPR; ++j)
+                    if (j < n * CPR) v[j] = *reinterpret_cast<const uint4*>(st + j * rows * 16);
+                uint32_t col[kKPU * 32];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (!(pend_mask & (1 << t))) continue;
-                const int o = pend_ord0 + __popc(pend_mask & ((1 << t) - 1)), buf = o % ndb;
-                mbar_wait(&d_full[buf], uint32_t((o / ndb) & 1));
-                tc_fence_after();
-                const float sc = pend_s[t];
-#pragma unroll
-                for (int j = 0; j < NT; j += 16) {
-                    float v[16];
-                    tmem_ld16(tmem + lane_base + d_col0 + buf * NT + j, v);
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) acc[j + e] = fmaf(sc, v[e], acc[j + e]);
+                for (int j = 0; j < kKPU * CPR; ++j) {
+                    if constexpr (BITS == 4) {
+                        dequant4<AT>(v[j].x, col + j * 16 + 0);
+                        dequant4<AT>(v[j].y, col + j * 16 + 4);
+                        dequant4<AT>(v[j].z, col + j * 16 + 8);
+                        dequant4<AT>(v[j].w, col + j * 16 + 12);
+                    } else {
+                        dequant8<AT>(v[j].x, col + j * 8 + 0);
+                        dequant8<AT>(v[j].y, col + j * 8 + 2);
+                        dequant8<AT>(v[j].z, col + j * 8 + 4);
+                        dequant8<AT>(v[j].w, col + j * 8 + 6);
+                    }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // codes of this unit consumed
+                if (i >= kRA) {
+                    PWAIT(&a_empty[slot], pha ^ 1u, 1);
+                    tc_fence_after();
+                }
+                const uint32_t ta = tmem + lane_base + slot * (kKPU * 32);
+                if (!(p.debug & 8)) {
+                    tmem_st32(ta, col);
+                    if (n > 1) tmem_st32(ta + 32, col + 32);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&d_empty[buf]);
+                if (lane == 0) mbar_arrive(&a_full[slot]);
             }
-            pend_mask = 0;
-        };
+            w.advance(n);
+            ++i;
+        }
+        if (threadIdx.x == 0) stamp(p, 4);
+        if (threadIdx.x == 0) prof_store(32);
+    } else if (warp < kEpiWarp0 + kEpiWarps) {
+        // ===================== epilogue =====================
+        const int q = warp & 3;  // TMEM lane quadrant
+        const int row = q * 32 + lane;
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+        float acc[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[j] = 0.0f;
 
         auto epilogue = [&](int b, bool sole_owner) {
             const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
@@ -479,12 +664,12 @@ __global__ void __launch_bounds__(kThreads, MINB) wgemm_tc_kernel(const Params p
             const int slot = 2 * c + (b == u0 / p.KBLK ? 0 : 1);
             float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(slot) * kRows + row) * NT);
 #pragma unroll
-            for (int i = 0; i < NT / 4; ++i)
-                mine[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+            for (int j = 0; j < NT / 4; ++j)
+                mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
             asm volatile("bar.sync 1, 128;" ::: "memory");
             const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
             const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
-            if (threadIdx.x == 0) {
+            if (et == 0) {
                 int prev;
                 asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
                              : "=r"(prev)
@@ -498,92 +683,81 @@ __global__ void __launch_bounds__(kThreads, MINB) wgemm_tc_kernel(const Params p
             if (!*flag) return;
             float sum[NT];
 #pragma unroll
-            for (int i = 0; i < NT; ++i) sum[i] = 0.0f;
+            for (int j = 0; j < NT; ++j) sum[j] = 0.0f;
             const int first_bit = int(int64_t(c_first) * p.U / p.G) / p.KBLK == b ? 0 : 1;
             for (int cc = c_first; cc <= c_last; ++cc) {  // fixed order: deterministic
                 const int cs = 2 * cc + (cc == c_first ? first_bit : 0);
                 const float4* src =
                     reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * kRows + row) * NT);
 #pragma unroll
-                for (int i = 0; i < NT / 4; ++i) {
-                    const float4 x = __ldcg(src + i);
-                    sum[4 * i] += x.x;
-                    sum[4 * i + 1] += x.y;
-                    sum[4 * i + 2] += x.z;
-                    sum[4 * i + 3] += x.w;
+                for (int j = 0; j < NT / 4; ++j) {
+                    const float4 x = __ldcg(src + j);
+                    sum[4 * j] += x.x;
+                    sum[4 * j + 1] += x.y;
+                    sum[4 * j + 2] += x.z;
+                    sum[4 * j + 3] += x.w;
                 }
             }
             write(sum);
         };
 
-        Walker w(u0, u1, p.KBLK, KPS);
+        Walker w(u0, u1, p.KBLK);
         int seg_kb0 = w.kb;
-        int s = 0, ra = 0, rause = 0;
-        uint32_t ph = 0, pha = 0;
+        int ord = 0;
         while (w.more()) {
             const int n = w.chunk();
             const bool seg_end = w.seg_end(n);
             const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
             const int rows8 = (rows + 7) / 8 * 8;
-            const int g0 = (w.kb * kKB) >> p.log2g;
-            mbar_wait(&full[s], ph);
-            const uint8_t* st = smem + s * GG::STAGE_BYTES;
-            const __half* sc = reinterpret_cast<const __half*>(st + GG::CODE_BYTES);
-            for (int kbl = 0; kbl < n; ++kbl) {
-                const int kb = w.kb + kbl;
-                if (rause >= kRA) mbar_wait(&a_empty[ra], pha ^ 1u);
-                uint32_t col[32];
-                if constexpr (BITS == 4) {
+            const __half* sc_row =
+                reinterpret_cast<const __half*>(p.scales) + int64_t(w.b) * kRows * p.GPR + row;
+            const int steps = n * 4, kbase = w.kb * kKB;
+            uint32_t ends = unit_ends(kbase, steps, seg_end, p.log2g, gmask, p.full_k);
+            while (ends) {
+                const int kk = __ffs(ends) - 1;
+                ends &= ends - 1;
+                const int knext = kbase + (kk + 1) * 16;
+                int grp = (knext - 1) >> p.log2g;
+                grp = grp < p.GPR ? grp : p.GPR - 1;
+                // the scale a few groups ahead goes to L1 now, so this load hits later
+                if (grp + 4 < p.GPR && row < rows)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(sc_row + int64_t(grp + 4) * rows8));
+                const float sc =
+                    row < rows ? __half2float(__ldg(sc_row + int64_t(grp) * rows8)) : 0.0f;
+                const int buf = ord & (ND - 1);
+                PWAIT(&d_full[buf], uint32_t((ord / ND) & 1), 0);
+                tc_fence_after();
 #pragma unroll
-                    for (int ch = 0; ch < CPR; ++ch) {
-                        const uint4 v = *reinterpret_cast<const uint4*>(
-                            st + ((kbl * CPR + ch) * rows + row) * 16);
-                        dequant4<AT>(v.x, col + ch * 16 + 0);
-                        dequant4<AT>(v.y, col + ch * 16 + 4);
-                        dequant4<AT>(v.z, col + ch * 16 + 8);
-                        dequant4<AT>(v.w, col + ch * 16 + 12);
-                    }
-                } else {
+                for (int j = 0; j < NT; j += 32) {
+                    uint32_t v[32];
+                    if (!(p.debug & 16)) {
+                        tmem_ld16_nw(tmem + lane_base + GG::D_COL0 + buf * NT + j, v);
+                        if constexpr (NT >= 32)
+                            tmem_ld16_nw(tmem + lane_base + GG::D_COL0 + buf * NT + j + 16, v + 16);
+                    } else {
 #pragma unroll
-                    for (int ch = 0; ch < CPR; ++ch) {
-                        const uint4 v = *reinterpret_cast<const uint4*>(
-                            st + ((kbl * CPR + ch) * rows + row) * 16);
-                        dequant8<AT>(v.x, col + ch * 8 + 0);
-                        dequant8<AT>(v.y, col + ch * 8 + 2);
-                        dequant8<AT>(v.z, col + ch * 8 + 4);
-                        dequant8<AT>(v.w, col + ch * 8 + 6);
+                        for (int e = 0; e < 32; ++e) v[e] = 0;
                     }
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (j + 32 >= NT) {  // last read of this buffer: hand it back
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&d_empty[buf]);
+                    }
+                    constexpr int W = NT < 32 ? NT : 32;
+#pragma unroll
+                    for (int e = 0; e < W; ++e)
+                        acc[j + e] = fmaf(sc, __uint_as_float(v[e]), acc[j + e]);
                 }
-                tmem_st32(tmem + lane_base + ra * 32, col);
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&a_full[ra]);
-                if (++ra == kRA) ra = 0, pha ^= 1u;
-                ++rause;
-                // accumulators of the previous k-block's groups are ready by now
-                drain();
-                // groups finishing in this k-block (group ends, or the segment ends)
-                pend_ord0 = ord;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int knext = kb * kKB + (t + 1) * 16;
-                    if ((knext & gmask) == 0 || (seg_end && kbl == n - 1 && t == 3)) {
-                        const int grp = (knext - 1) >> p.log2g;
-                        pend_s[t] = __half2float(sc[(grp - g0) * rows8 + row]);
-                        pend_mask |= 1 << t;
-                        ++ord;
-                    }
-                }
+                ++ord;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // codes + scales of this stage consumed
-            if (++s == STAGES) s = 0, ph ^= 1u;
             if (seg_end) {
-                drain();
+                if (et == 0) stamp(p, 5);
                 epilogue(w.b, seg_kb0 == 0 && w.kb + n == p.KBLK);
+                if (et == 0) stamp(p, 6);
+                if (et == 0) prof_store(44);
 #pragma unroll
-                for (int i = 0; i < NT; ++i) acc[i] = 0.0f;
+                for (int j = 0; j < NT; ++j) acc[j] = 0.0f;
                 w.advance(n);
                 seg_kb0 = w.kb;
             } else {
@@ -593,10 +767,10 @@ __global__ void __launch_bounds__(kThreads, MINB) wgemm_tc_kernel(const Params p
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == kDequantWarps + 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "n"(GG::TMEM_COLS));
+                     "n"(kTmemCols));
     }
 }
 
@@ -612,27 +786,21 @@ int sm_count() {
     return n;
 }
 
-// Token tile: the MMA N.  M=128 UMMA needs N % 16 == 0; the TMEM budget (A ring
-// 128 columns + D buffers <= 128 columns) caps N by the D buffers a group size needs.
-int nt_for(int64_t m, int64_t g) {
-    const int ndb = g >= 64 ? 2 : 2 * int(64 / g);
-    const int cap = 128 / ndb;  // 64 (g >= 64), 32 (g = 32), 16 (g = 16)
-    int nt = m <= 16 ? 16 : m <= 32 ? 32 : 64;
-    return nt < cap ? nt : cap;
-}
-int ctas_per_sm(int nt) { return nt <= 32 ? 2 : 1; }
+// Token tile = the MMA N (M=128 UMMA needs N % 16 == 0).
+int nt_for(int64_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : 64; }
 
 int ctas_for(int64_t U, int nt) {
-    int G = ctas_per_sm(nt) * sm_count();
+    (void)nt;
+    int G = sm_count();  // persistent: one CTA per SM (it owns all 512 TMEM columns)
     if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
     if (G < 1) G = 1;
     return int(U < G ? U : G);
 }
 
-template <int BITS, int AT, int NT, int STAGES, int MINB>
+template <int BITS, int AT, int NT, bool PROF>
 cudaError_t launch_t(const Params& p, cudaStream_t st, bool pdl) {
-    using GG = Geo<BITS, NT, STAGES>;
-    auto kern = wgemm_tc_kernel<BITS, AT, NT, STAGES, MINB>;
+    using GG = Geo<BITS, NT>;
+    auto kern = wgemm_tc_kernel<BITS, AT, NT, PROF>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e =
@@ -653,23 +821,39 @@ cudaError_t launch_t(const Params& p, cudaStream_t st, bool pdl) {
     return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-// Stages: two CTAs per SM must each stay under ~110 KiB of shared memory.
 template <int BITS, int AT>
 cudaError_t launch_bits(const Params& p, int nt, cudaStream_t st, bool pdl) {
+    if (p.debug & 32) {
+        switch (nt) {
+            case 16: return launch_t<BITS, AT, 16, true>(p, st, pdl);
+            case 32: return launch_t<BITS, AT, 32, true>(p, st, pdl);
+            default: return launch_t<BITS, AT, 64, true>(p, st, pdl);
+        }
+    }
     switch (nt) {
-        case 16: return launch_t<BITS, AT, 16, BITS == 4 ? 3 : 4, 2>(p, st, pdl);
-        case 32: return launch_t<BITS, AT, 32, 3, 2>(p, st, pdl);
-        default: return launch_t<BITS, AT, 64, 4, 1>(p, st, pdl);
+        case 16: return launch_t<BITS, AT, 16, false>(p, st, pdl);
+        case 32: return launch_t<BITS, AT, 32, false>(p, st, pdl);
+        default: return launch_t<BITS, AT, 64, false>(p, st, pdl);
     }
 }
 
 }  // namespace tc
 
+extern "C" int rtnq_wgemm_debug_read(void* host, size_t bytes, int reset) {
+    if (bytes > sizeof(tc::g_wgemm_dbg)) bytes = sizeof(tc::g_wgemm_dbg);
+    if (cudaMemcpyFromSymbol(host, tc::g_wgemm_dbg, bytes) != cudaSuccess) return 1;
+    if (reset) {
+        static unsigned long long zeros[1024 * 64];
+        if (cudaMemcpyToSymbol(tc::g_wgemm_dbg, zeros, sizeof(zeros)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+
 const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype) {
     (void)m;
     (void)n;
     if (a_dtype != RTNQ_BF16 && a_dtype != RTNQ_F16) return "activations must be bf16 or f16";
-    if (k % 64 != 0) return "k must be a multiple of 64 for the tensor-core path";
+    if (k % 8 != 0) return "k must be a multiple of 8 for the tensor-core path";
     if (!(g >= k || g % 16 == 0)) return "group size must be a multiple of 16 (or span the row)";
     if (k >= (int64_t(1) << 29)) return "k too large";
     return nullptr;
@@ -683,15 +867,33 @@ constexpr size_t kCounterBytes = 64 * 1024;  // 16384 row-blocks (2M channels)
 size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t g) {
     (void)bits;
     const int64_t NB = (n + tc::kRows - 1) / tc::kRows;
-    const int64_t U = NB * (k / 64 > 0 ? k / 64 : 1);
+    const int64_t U = NB * ((k + 63) / 64 > 0 ? (k + 63) / 64 : 1);
     size_t part = 0;
+    (void)g;
     for (int nt : {16, 32, 64}) {  // every tile a call may launch
-        if (nt > tc::nt_for(m, g)) break;
+        if (nt > tc::nt_for(m)) break;
         const int G = tc::ctas_for(U, nt);
         const size_t need = size_t(G) * 2 * tc::kRows * nt * sizeof(float);
         part = need > part ? need : part;
     }
     return kCounterBytes + part;
+}
+
+// Activations [m][k] viewed as a 3-D tensor (8 elements, token, k-chunk) so one TMA box
+// {8, nt, 16} lands in shared memory as [k-chunk][token][16 B] -- UMMA K-major core
+// matrices.  Tokens >= m and chunks past k are out of bounds and arrive as zeros.
+static cudaError_t encode_act_map(CUtensorMap* map, const void* a, int a_dtype, int64_t m,
+                                  int64_t k, int nt) {
+    const cuuint64_t dims[3] = {8, cuuint64_t(m), cuuint64_t(k / 8)};
+    const cuuint64_t strides[2] = {cuuint64_t(k * 2), 16};
+    const cuuint32_t box[3] = {8, cuuint32_t(nt), 16};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = cuTensorMapEncodeTiled(
+        map, a_dtype == RTNQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+        3, const_cast<void*>(a), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
@@ -701,7 +903,8 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
     p.N = A.n;
     p.K = A.k;
     p.NB = int((A.n + tc::kRows - 1) / tc::kRows);
-    p.KBLK = int(A.k / 64);
+    p.KBLK = int((A.k + 63) / 64);
+    p.full_k = int((A.k + 15) / 16 * 16);
     p.GPR = int(A.g >= A.k ? 1 : (A.k + A.g - 1) / A.g);
     p.log2g = A.g >= A.k ? 30 : __builtin_ctzll(uint64_t(A.g));
     p.out_dtype = A.out_dtype;
@@ -712,12 +915,14 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
         return cudaErrorInvalidValue;
     p.U = p.NB * p.KBLK;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
-    const int nt_max = tc::nt_for(A.m, A.g);
+    const int nt_max = tc::nt_for(A.m);
     for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {  // one pass per token tile
         p.M = int(A.m - m0 < nt_max ? A.m - m0 : nt_max);
         p.a = static_cast<const char*>(A.a) + m0 * A.k * 2;
         p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
-        const int nt = tc::nt_for(p.M, A.g);
+        const int nt = tc::nt_for(p.M);
+        p.m0 = int(m0);
+        if (cudaError_t e = encode_act_map(&p.tmap_a, A.a, A.a_dtype, A.m, A.k, nt)) return e;
         p.G = tc::ctas_for(p.U, nt);
         const bool pdl = A.pdl || m0 > 0;
         cudaError_t e;

@@ -1,0 +1,67 @@
+// kernels.cuh -- launcher declarations shared by the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../common.cuh"
+
+namespace rtnq_b200 {
+
+// quant.cu
+void launch_group_scales(const void* w, int dtype, int64_t rows, int64_t cols, int bits,
+                         int64_t g, int64_t gpr, float* s32, uint16_t* s16, uint16_t* s16n,
+                         int32_t* err, cudaStream_t st);
+void launch_codes(const void* w, int dtype, int64_t rows, int64_t cols, int bits, int64_t g,
+                  int64_t gpr, const float* s32, int8_t* codes, cudaStream_t st);
+void launch_encode_from_logical(const int8_t* logical, Layout dst, int bits, int64_t rows,
+                                int64_t cols, uint8_t* out, cudaStream_t st);
+void launch_relayout(const uint8_t* src, Layout from, uint8_t* dst, Layout to, int bits,
+                     int64_t rows, int64_t cols, cudaStream_t st);
+void launch_dequant(const uint8_t* codes, Layout L, int bits, int64_t rows, int64_t cols,
+                    int64_t g, int64_t gpr, const void* scales, int sdtype, int sorder,
+                    void* out, int odtype, cudaStream_t st);
+void launch_native_scales(const void* scales, int dtype, int64_t rows, int64_t gpr,
+                          uint16_t* out, cudaStream_t st);
+void launch_decode(const uint8_t* src, Layout L, int bits, int64_t rows, int64_t cols,
+                   int8_t* out, cudaStream_t st);
+void launch_check_finite(const void* p, int dtype, int64_t n, int32_t* err, cudaStream_t st);
+
+// quant_fused.cu: one-pass quantize+pack for 16 x 128 tiles.  Returns false
+// (launching nothing) when the shape is outside the fused kernel's domain.
+bool quant_fused_supported(int64_t rows, int64_t cols, int bits, int64_t g);
+void launch_quant_fused(const void* w, int dtype, int64_t rows, int64_t cols, int bits,
+                        int64_t g, uint8_t* rm, uint8_t* k164, uint8_t* nat, float* s32,
+                        uint16_t* s16, uint16_t* s16n, int32_t* err, cudaStream_t st);
+
+// gemm_exact.cu
+void launch_gemm_fused_exact(const float* a, int64_t m, int64_t k, const uint8_t* codes,
+                             Layout L, int bits, int64_t n, int64_t g, int64_t gpr,
+                             const float* scales, float* out, cudaStream_t st);
+void launch_dense_blocked(const float* a, int64_t m, int64_t k, const float* w, int64_t n,
+                          int64_t blk, float* out, cudaStream_t st);
+void launch_gemm_oracle(const float* a, int64_t m, int64_t k, const uint8_t* codes, Layout L,
+                        int bits, int64_t n, int64_t g, int64_t gpr, const float* scales,
+                        float* out, cudaStream_t st);
+
+// wgemm_sm100.cu: tensor-core W4A16 / W8A16 over the native layout.
+struct WgemmArgs {
+    const void* a;         // m x k, bf16 or f16, row-major
+    int a_dtype;           // RTNQ_BF16 | RTNQ_F16
+    int64_t m, n, k;
+    const uint8_t* codes;  // native layout
+    const uint16_t* scales;  // f16, native order
+    int bits;
+    int64_t g;             // group size (g >= k: one group per row)
+    void* out;             // m x n, row-major
+    int out_dtype;
+    void* workspace;
+    size_t ws_bytes;
+    bool pdl;              // launch with programmatic dependent launch (RTNQ_FLAG_PDL)
+};
+// Validates the shape for the tensor-core path; returns a message or nullptr.
+const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);
+size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t g);
+cudaError_t launch_wgemm(const WgemmArgs& args, cudaStream_t st);
+
+}  // namespace rtnq_b200

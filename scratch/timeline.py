@@ -1,25 +1,37 @@
-import os, sys, torch, numpy as np
+"""RTNQ_WGEMM_DEBUG=32 instrumentation: per-CTA stamps and blocked cycles per role/barrier."""
+import os, sys, ctypes, torch, numpy as np
 sys.path.insert(0, os.getcwd())
+os.environ["RTNQ_WGEMM_DEBUG"] = str(32 | int(os.environ.get("DBG", "0")))
 import paper_2505_15909_b200 as rq
-os.environ["RTNQ_WGEMM_DEBUG"] = os.environ.get("DBG", "4")
-B = int(os.environ.get("B", "16"))
-# warm the clocks
+L = rq.lib()
+B = int(os.environ.get("B", "16")); bits = int(os.environ.get("BITS", "4"))
 a = torch.randn(8192, 8192, device="cuda")
-for _ in range(50): a @ a
+for _ in range(30): a @ a
+names = ["start", "tmem", "prod_end", "mma_end", "deq_end", "epi_seg_end", "combine_end"]
+waits = {8: "prod wait empty", 9: "prod weights()", 10: "prod acts()", 16: "prod total",
+         20: "mma wait full", 21: "mma wait a_full", 22: "mma wait d_empty", 23: "mma ends-mask",
+         24: "mma issue block", 25: "mma 2 commits", 28: "mma total",
+         32: "deq0 wait full", 33: "deq0 wait a_empty", 40: "deq0 total",
+         44: "epi0 wait d_full", 52: "epi0 total(last seg)"}
+buf = np.zeros(1024 * 64, np.uint64)
 for name, n, k in [("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]:
     w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
-    q = rq.quantize_pack(w, 4, 128)
+    g = 128 if bits == 4 else 1 << (k - 1).bit_length()
+    q = rq.quantize_pack(w, bits, g, ragged=k % g != 0)
     x = torch.empty(B, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
-    ws = rq.Workspace(device="cuda")
+    ws = rq.Workspace(nbytes=1 << 22, device="cuda")
     for _ in range(3): rq.linear(x, q, workspace=ws)
     torch.cuda.synchronize()
-    ts = ws.buf[32768:32768 + 296 * 64].view(torch.int64).view(-1, 8).cpu().numpy().astype(np.float64)
-    ts = ts[ts[:, 0] > 0]
-    t0 = ts[:, 0].min()
-    r = ts.copy(); r[:, [0,1,2,3,4,6]] = (ts[:, [0,1,2,3,4,6]] - t0) / 1000.0
-    last = r[:, 5] > 0
-    print(f"{name} B={B}: CTAs={len(r)} first-data med={np.median(r[:,1]):.2f} last-stage[med,max]=({np.median(r[:,2]):.2f},{r[:,2].max():.2f}) "
-          f"published[med,max]=({np.median(r[:,4]):.2f},{r[:,4].max():.2f}) end[med,max]=({np.median(r[:,3]):.2f},{r[:,3].max():.2f}) "
-          f"combiners={last.sum()} combine-dur[med,max]=({np.median(r[last,6]-r[last,4]):.2f},{(r[last,6]-r[last,4]).max():.2f}) us")
-    o = np.argsort(-r[:, 3])[:5]
-    for i in o: print("   slow CTA", i, np.round(r[i], 2))
+    L.rtnq_wgemm_debug_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes), 1)
+    rq.linear(x, q, workspace=ws)
+    torch.cuda.synchronize()
+    L.rtnq_wgemm_debug_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes), 1)
+    d = buf.reshape(1024, 64).astype(np.float64)
+    d = d[d[:, 0] > 0]
+    t0 = d[:, 0].min()
+    r = (d[:, :7] - t0) / 1000.0
+    print(f"{name} W{bits} B={B} CTAs={len(r)} (us from first CTA start; median / max)")
+    for i, nm in enumerate(names):
+        print(f"   {nm:12s} {np.median(r[:, i]):8.2f} {r[:, i].max():8.2f}")
+    for sl, nm in waits.items():
+        print(f"   {nm:24s} kcyc median {np.median(d[:, sl])/1e3:8.2f} max {d[:, sl].max()/1e3:8.2f}")
