@@ -258,7 +258,7 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
                      "traffic": ncu_traffic(bits, B), "peak_source": peak_src,
-                     "kernel": "rtnq_b200::wg::wgemm_kernel",
+                     "kernel": "rtnq_b200::tc::wgemm_tc_kernel",
                      "algorithmic_bytes_per_launch": round(per_launch_bytes)},
         "e2e": {"value": round(e2e, 1), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},

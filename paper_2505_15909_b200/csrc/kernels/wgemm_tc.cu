@@ -2,33 +2,33 @@
 //
 // out[m][n] = sum_k a[m][k] * code[n][k] * S[n][k/g]   (gemm.hpp:18-27)
 //
-// One persistent CTA per SM computes 128-row (output channel) x NT-token tiles
-// over a stream-K range of 64-code k-blocks, walked in units of two k-blocks
-// (one stage, one A-ring slot, one synchronisation step).  Four decoupled warp
-// roles joined by mbarriers:
-//   warp 12 producer: per unit, one cp.async.bulk (TMA engine) for the codes (the
-//           native layout makes a row-block one contiguous run along K) plus
-//           16-byte cp.async for the activations, written in the UMMA K-major
-//           core-matrix order; both complete on the stage mbarrier.
-//   warps 0-7 dequantizers: warp w owns TMEM lanes 32(w&3).. = rows 32(w&3)+lane
-//           of the units with parity w>>2 (two warps per SM sub-partition hide
-//           each other's latency).  Each thread turns its row's codes into exact
-//           bf16/f16 integers with LOP3/PRMT magic numbers and tcgen05.st's them
-//           into the unit's TMEM A-ring slot.
-//   warp 13 MMA issuer: a single thread issues tcgen05.mma.cta_group::1.kind::f16,
-//           A (weights) from TMEM, B (activations) from shared memory, D in TMEM
-//           (M=128, N=NT, K=16), one D buffer per quantization group, and
-//           tcgen05.commit's to free A slots and stages and publish finished groups.
-//   warps 8-11 epilogue: per quantization group, tcgen05.ld of the f32 block sum
-//           and acc += S[row][group] * block in registers -- the reference's
-//           block-then-scale structure (gemm.cpp:69-87) with exact integer codes
-//           and the f16 group scale applied in f32.  The scale is read straight
-//           from global memory (one coalesced 64-byte load per warp per group).
-// Stream-K: the (row-block, k-block) units are split evenly over the grid;
-// row-blocks shared by several CTAs are combined by the last CTA to arrive,
-// summing partials in CTA order (deterministic; no float atomics).
+// One persistent CTA per SM computes 128-row (output channel) x NT-token tiles over
+// a stream-K range of 64-code k-blocks, walked in units of 16 KiB of codes (4
+// k-blocks at W4, 2 at W8): one stage, one TMEM A-ring slot, one synchronisation
+// step.  Four decoupled warp roles joined by mbarriers:
+//   warp 12    producer: per unit, one cp.async.bulk for the codes (the native layout
+//              makes a row-block one contiguous run along K), one for the unit's f16
+//              group scales, and one TMA tensor load for the activations, landing as
+//              UMMA K-major core matrices; all three complete on the stage mbarrier.
+//   warps 0-7  dequantizers: warp w owns TMEM lanes 32(w&3).. = rows 32(w&3)+lane of
+//              the units with parity w>>2 (two warps per SM sub-partition hide each
+//              other's latency).  Each thread turns its row's codes into exact bf16/f16
+//              integers with LOP3/PRMT magic numbers and tcgen05.st's them into the
+//              unit's TMEM A-ring slot.
+//   warps 13-14 MMA issuers, one per unit parity: one elected lane issues
+//              tcgen05.mma.cta_group::1.kind::f16 -- A (weights) from TMEM, B
+//              (activations) from shared memory, D in TMEM, M=128, N=NT, K=16.  Every
+//              unit owns one accumulator per quantization group it touches, so units
+//              are independent and the two parities run as two pipelines.
+//   warps 8-11 epilogue: per unit and group, tcgen05.ld of the f32 block sum and
+//              acc += S[row][group] * block in registers -- the reference's
+//              block-then-scale structure (gemm.cpp:69-87) with exact integer codes and
+//              the f16 group scale applied in f32.
+// Stream-K: the (row-block, k-block) units are split evenly over the grid; row-blocks
+// shared by several CTAs are combined by the last CTA to arrive, summing partials in
+// CTA order (deterministic; no float atomics).
 // PDL (opt-in): weight prefetch for the first stages precedes griddepcontrol.wait.
-#include <cuda.h>  // CUtensorMap (the map is encoded through the runtime's driver entry point)
+#include <cuda.h>  // CUtensorMap
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -41,19 +41,17 @@ namespace tc {
 
 constexpr int kRows = kNativeRows;  // 128: UMMA M
 constexpr int kKB = kNativeKB;      // 64 codes per k-block
-constexpr int kKPU = 2;             // k-blocks per unit (one A-ring slot = 64 TMEM columns)
 constexpr int kDequantWarps = 8;    // warps 0-7: quadrant w & 3, unit parity w >> 2
 constexpr int kEpiWarps = 4;        // warps 8-11: quadrant w & 3
 constexpr int kEpiWarp0 = 8;
 constexpr int kProducerWarp = 12;
-constexpr int kMmaWarp = 13;
-constexpr int kThreads = 14 * 32;
-constexpr int kRA = 4;              // A-ring slots (4 x 64 = 256 TMEM columns)
+constexpr int kMmaWarp = 13;        // warps 13-14: MMA issuers, unit parity w - 13
+constexpr int kThreads = 15 * 32;
 constexpr int kTmemCols = 512;      // one CTA per SM owns all of TMEM
+constexpr int kACols = 256;         // A ring; accumulators use the other 256 columns
 
 struct Params {
     CUtensorMap tmap_a;  // activations as [k-chunk][token][8 elements]; OOB (m >= M, k >= K) -> 0
-    const void* a;
     const uint8_t* codes;
     const uint16_t* scales;
     void* out;
@@ -65,13 +63,12 @@ struct Params {
     int NB;     // 128-row row-blocks
     int KBLK;   // 64-code k-blocks
     int GPR;    // scale groups per row
-    int U;      // units = NB * KBLK
+    int U;      // (row-block, k-block) pairs = NB * KBLK
     int G;      // CTAs
     int out_dtype;
     int log2g;  // log2(group); 30 when one group spans the row
-    int full_k; // K rounded to the MMA step (groups past K fold into the last group)
     int debug;  // RTNQ_WGEMM_DEBUG bits (profiling only): 2 no copies, 4 no MMA, 8 no tcgen05.st,
-                //   16 no tcgen05.ld, 32 per-CTA globaltimer stamps into the counter region
+                //   16 no tcgen05.ld, 32 per-role timing (rtnq_wgemm_debug_read)
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------
@@ -119,6 +116,9 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
@@ -228,74 +228,6 @@ __device__ __forceinline__ void store_out(void* out, int dt, int64_t i, float v)
     else static_cast<__half*>(out)[i] = __float2half_rn(v);
 }
 
-// ---- geometry ------------------------------------------------------------------------------
-template <int BITS, int NT>
-struct Geo {
-    static constexpr int CPR = BITS == 4 ? 2 : 4;                  // 16-B chunks / row / k-block
-    static constexpr int CODE_BYTES = kKPU * CPR * kRows * 16;     // 8 KiB (W4) / 16 KiB (W8)
-    static constexpr int ACT_KCH = kKPU * kKB / 8;                 // 16-B k-chunks per unit
-    static constexpr int ACT_BYTES = NT * ACT_KCH * 16;            // one TMA box [chunk][token][16 B]
-    static constexpr int ACT_OFF = CODE_BYTES;
-    static constexpr int STAGE_BYTES = (ACT_OFF + ACT_BYTES + 1023) / 1024 * 1024;
-    static constexpr int STAGES_FIT = (220 * 1024) / STAGE_BYTES / 2 * 2;
-    static constexpr int STAGES = STAGES_FIT > 16 ? 16 : STAGES_FIT;  // even: parity-owned
-    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-    static constexpr int SMEM = BAR_OFF + 1024 + 1024;            // barriers + alignment slack
-    static constexpr int D_COL0 = kRA * kKPU * 32;                // 256
-    static constexpr int ND_FIT = (kTmemCols - D_COL0) / NT;
-    static constexpr int ND = ND_FIT > 16 ? 16 : ND_FIT;         // group accumulators
-    static_assert(STAGES >= 4 && ND >= 2 && (ND & (ND - 1)) == 0, "tile does not fit");
-};
-
-__device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
-    return int(((u + 1) * G - 1) / U);
-}
-
-// The unit sequence of a CTA: chunks of <= kKPU k-blocks that never cross a
-// row-block (segment) boundary.  Every role walks it alike.
-struct Walker {
-    int u, u1, b, kb, KBLK;
-    __device__ Walker(int u0_, int u1_, int KBLK_) : u(u0_), u1(u1_), KBLK(KBLK_) {
-        b = u0_ / KBLK_;
-        kb = u0_ - b * KBLK_;
-    }
-    __device__ bool more() const { return u < u1; }
-    __device__ int chunk() const {  // units start at even k-blocks (group-aligned for g >= 128)
-        const int left_seg = KBLK - kb, left = u1 - u, cap = kKPU - (kb & 1);
-        const int n = left_seg < left ? left_seg : left;
-        return n < cap ? n : cap;
-    }
-    __device__ bool seg_end(int n) const { return kb + n == KBLK || u + n == u1; }
-    __device__ void advance(int n) {
-        u += n;
-        kb += n;
-        if (kb == KBLK) kb = 0, ++b;
-    }
-};
-
-// Does a quantization group end after the k16 step whose last code is knext-1?
-// Steps past the end of the row (zero padding) fold into the row's last group.
-__device__ __forceinline__ bool group_ends(int knext, int gmask, int full_k, bool last_step) {
-    return last_step || (((knext & gmask) == 0) && knext <= full_k);
-}
-
-// Bit kk set: a group's accumulator is complete after k16 step kk of the unit that
-// starts at code kbase and has `steps` steps.  For g >= 128 a unit (which starts at an
-// even k-block) lies inside one group, so only its last step can end one.
-__device__ __forceinline__ uint32_t unit_ends(int kbase, int steps, bool seg_end, int log2g,
-                                              int gmask, int full_k) {
-    if (log2g >= 7) {
-        const int kn = kbase + steps * 16;
-        return (seg_end || (((kn & gmask) == 0) && kn <= full_k)) ? 1u << (steps - 1) : 0u;
-    }
-    uint32_t e = 0;
-#pragma unroll
-    for (int kk = 0; kk < kKPU * 4; ++kk)
-        if (kk < steps && group_ends(kbase + (kk + 1) * 16, gmask, full_k, seg_end && kk == steps - 1))
-            e |= 1u << kk;
-    return e;
-}
-
 __device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* d) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -364,8 +296,97 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
         : "memory");
 }
 
-// Profiling-only instrumentation (RTNQ_WGEMM_DEBUG & 32): per-CTA globaltimer stamps,
-// read back by rtnq_wgemm_debug_read.
+// ---- geometry ------------------------------------------------------------------------------
+template <int BITS, int NT>
+struct Geo {
+    static constexpr int KPU = BITS == 4 ? 4 : 2;                  // k-blocks per unit
+    static constexpr int BLK = KPU * kKB;                          // codes per unit (aligned)
+    static constexpr int LOG2BLK = BITS == 4 ? 8 : 7;
+    static constexpr int STEPS = BLK / 16;                         // k16 MMA steps per unit
+    static constexpr int CPR = BITS == 4 ? 2 : 4;                  // 16-B chunks / row / k-block
+    static constexpr int CODE_BYTES = KPU * CPR * kRows * 16;      // 16 KiB
+    static constexpr int SCALE_OFF = CODE_BYTES;                   // the unit's f16 group scales
+    static constexpr int SCALE_BYTES = (BLK / 16) * kRows * 2;     // <= BLK/16 groups (g = 16)
+    static constexpr int ACT_KCH = BLK / 8;                        // 16-B k-chunks per unit
+    static constexpr int ACT_OFF = SCALE_OFF + SCALE_BYTES;
+    static constexpr int ACT_BYTES = NT * ACT_KCH * 16;            // one TMA box [chunk][token][16 B]
+    static constexpr int STAGE_BYTES = (ACT_OFF + ACT_BYTES + 1023) / 1024 * 1024;
+    static constexpr int MB_BYTES = 12 * 1024;                     // scale mailbox (see kernel)
+    static constexpr int STAGES_FIT = (220 * 1024 - MB_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int MB_OFF = BAR_OFF + 1024;
+    static constexpr int SMEM = MB_OFF + MB_BYTES + 1024;          // + alignment slack
+    static constexpr int SLOT_COLS = KPU * 32;                     // bf16x2 columns per unit
+    static constexpr int RA_MAX = 8, ND_MAX = 16, MB_MAX = 24;     // barrier array sizes
+    static_assert(STAGES >= 3, "tile does not fit");
+};
+
+// TMEM split between accumulators (nd x NT columns, nd a power of two with room for
+// two units' worth when possible) and the A ring (the rest, ra slots).
+struct TmemSplit {
+    int nd, ra, d_col0;
+};
+__device__ __forceinline__ TmemSplit tmem_split(int nt, int slot_cols, int gpu) {
+    int nd = nt == 16 ? 8 : 4;
+    while (nd < 2 * gpu && nd * 2 * nt <= 256) nd *= 2;
+    while (nd < gpu) nd *= 2;  // the host guarantees gpu * nt <= 256
+    const int d_col0 = kTmemCols - nd * nt;
+    int ra = d_col0 / slot_cols;
+    ra = ra > 8 ? 8 : ra;
+    return {nd, ra, d_col0};
+}
+
+__device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
+    return int(((u + 1) * G - 1) / U);
+}
+
+// The unit sequence of a CTA: runs of <= KPU k-blocks that stay inside one KPU-aligned
+// block and one row-block (segment).  Every role walks it alike.
+template <int KPU>
+struct Walker {
+    int u, u1, b, kb, KBLK;
+    __device__ Walker(int u0_, int u1_, int KBLK_) : u(u0_), u1(u1_), KBLK(KBLK_) {
+        b = u0_ / KBLK_;
+        kb = u0_ - b * KBLK_;
+    }
+    __device__ bool more() const { return u < u1; }
+    __device__ int chunk() const {
+        const int left_seg = KBLK - kb, left = u1 - u, cap = KPU - (kb & (KPU - 1));
+        const int n = left_seg < left ? left_seg : left;
+        return n < cap ? n : cap;
+    }
+    __device__ bool seg_end(int n) const { return kb + n == KBLK || u + n == u1; }
+    __device__ void advance(int n) {
+        u += n;
+        kb += n;
+        if (kb == KBLK) kb = 0, ++b;
+    }
+};
+
+// Accumulator slot j of a unit covers the intersection of the unit [kbase, kend) with
+// the j-th group-sized piece of its aligned block; returns its first k16 step and count.
+__device__ __forceinline__ void subgroup(int kbase, int kend, int blk, int lg, int j, int* k0,
+                                         int* cnt) {
+    const int lo0 = blk + (j << lg), hi0 = lo0 + (1 << lg);
+    const int lo = lo0 > kbase ? lo0 : kbase, hi = hi0 < kend ? hi0 : kend;
+    *k0 = (lo - kbase) >> 4;
+    *cnt = hi > lo ? (hi - lo) >> 4 : 0;
+}
+
+// A position in a ring of n mbarrier-guarded slots, advanced incrementally: no runtime
+// division on the per-unit critical path.  ph is the parity of the current use.
+struct Ring {
+    int idx = 0, n;
+    uint32_t ph = 0;
+    __device__ explicit Ring(int n_) : n(n_) {}
+    __device__ void next() {
+        if (++idx == n) idx = 0, ph ^= 1u;
+    }
+};
+
+// Profiling-only instrumentation (RTNQ_WGEMM_DEBUG & 32): per-CTA globaltimer stamps and
+// per-role blocked/total cycles, read back by rtnq_wgemm_debug_read.
 __device__ unsigned long long g_wgemm_dbg[1024 * 64];
 __device__ __forceinline__ void stamp(const Params& p, int slot) {
     if (!(p.debug & 32)) return;
@@ -373,9 +394,6 @@ __device__ __forceinline__ void stamp(const Params& p, int slot) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_wgemm_dbg[blockIdx.x * 64 + slot] = t;
 }
-
-// PROF=true (RTNQ_WGEMM_DEBUG & 32) accumulates, per role, the SM cycles each wait
-// blocks, in registers, and stores them at the end (profiling builds only).
 #define PWAIT(bar, par, slot)                                   \
     do {                                                        \
         if constexpr (PROF) {                                   \
@@ -387,35 +405,62 @@ __device__ __forceinline__ void stamp(const Params& p, int slot) {
         }                                                       \
     } while (0)
 
+// Issue `cnt` k16 steps into one accumulator (the first step overwrites it).
+template <uint32_t KSTEP>
+__device__ __forceinline__ void issue_steps(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc,
+                                            int cnt) {
+    int done = 0;
+    for (; cnt - done >= 8; done += 8)
+        umma_unit_elect<8, KSTEP>(d, a + done * 8, bd + uint64_t(done * KSTEP), idesc, done);
+    if (cnt - done >= 4) {
+        umma_unit_elect<4, KSTEP>(d, a + done * 8, bd + uint64_t(done * KSTEP), idesc, done);
+        done += 4;
+    }
+    for (; done < cnt; ++done)
+        umma_f16_elect(d, a + done * 8, bd + uint64_t(done * KSTEP), idesc, done);
+}
+
+// PROF=true (RTNQ_WGEMM_DEBUG & 32) accumulates per-role wait cycles in registers.
 template <int BITS, int AT, int NT, bool PROF>
 __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params p) {
     using GG = Geo<BITS, NT>;
-    constexpr int CPR = GG::CPR, STAGES = GG::STAGES, ND = GG::ND;
+    constexpr int CPR = GG::CPR, STAGES = GG::STAGES, KPU = GG::KPU;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);
-    uint64_t* full = bars;                  // [STAGES] producer -> dequant + MMA
-    uint64_t* empty = full + STAGES;        // [STAGES] dequant + MMA -> producer
-    uint64_t* a_full = empty + STAGES;      // [kRA] dequant -> MMA
-    uint64_t* a_empty = a_full + kRA;       // [kRA] MMA -> dequant
-    uint64_t* d_full = a_empty + kRA;       // [ND] MMA -> epilogue
-    uint64_t* d_empty = d_full + ND;        // [ND] epilogue -> MMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + ND);
+    uint64_t* full = bars;                  // [STAGES] producer -> dequant, MMA, epilogue
+    uint64_t* empty = full + STAGES;        // [STAGES] dequant + MMA + epilogue -> producer
+    uint64_t* a_full = empty + STAGES;      // [RA] dequant -> MMA
+    uint64_t* a_empty = a_full + GG::RA_MAX;  // [RA] MMA -> dequant
+    uint64_t* d_full = a_empty + GG::RA_MAX;  // [ND] MMA -> epilogue
+    uint64_t* d_empty = d_full + GG::ND_MAX;  // [ND] epilogue -> MMA
+    uint64_t* m_full = d_empty + GG::ND_MAX;  // [MB] dequant -> epilogue (scale mailbox)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_full + GG::MB_MAX);
+    __half* mbox = reinterpret_cast<__half*>(smem + GG::MB_OFF);  // [MB][gpu][128 rows]
     volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     if (threadIdx.x == 0) stamp(p, 0);
     const int u0 = int(int64_t(c) * p.U / p.G), u1 = int(int64_t(c + 1) * p.U / p.G);
-    const int gmask = (1 << p.log2g) - 1;
+    // accumulator slots per unit: one per group-sized piece of the aligned block
+    const int lg = p.log2g < GG::LOG2BLK ? p.log2g : GG::LOG2BLK;
+    const int gpu = 1 << (GG::LOG2BLK - lg);
+    const TmemSplit tsp = tmem_split(NT, GG::SLOT_COLS, gpu);
+    const int ND = tsp.nd, RA = tsp.ra;
+    // Mailbox entry e = unit % MB carries the unit's group scales from its dequant warps
+    // to the epilogue.  Reusing it for unit i needs the epilogue done with unit i - MB:
+    // dequant(i) follows a_empty(i - RA) <- MMA(i - RA) <- d_empty of unit i - RA - ND/gpu.
+    const int MB = RA + ND / gpu;
+    const int lnd = __ffs(ND) - 1;  // ND is a power of two
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);        // producer's arrive.expect_tx (codes + activations)
-            mbar_init(&empty[s], 4 + 1);   // the parity's 4 dequant warps + MMA commit
+            mbar_init(&full[s], 1);                          // producer's arrive.expect_tx
+            mbar_init(&empty[s], 4 + 1);                     // dequant parity + MMA
         }
-        for (int i = 0; i < kRA; ++i) {
+        for (int i = 0; i < RA; ++i) {
             mbar_init(&a_full[i], 4);
             mbar_init(&a_empty[i], 1);
         }
@@ -423,9 +468,10 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
             mbar_init(&d_full[i], 1);
             mbar_init(&d_empty[i], kEpiWarps);
         }
+        for (int i = 0; i < MB; ++i) mbar_init(&m_full[i], 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == kMmaWarp) {  // the MMA warp owns the TMEM allocation
+    if (warp == kMmaWarp) {  // the first MMA warp owns the TMEM allocation
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "n"(kTmemCols));
@@ -437,36 +483,42 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     const uint32_t tmem = *tmem_slot;
     grid_dep_launch();
     if (threadIdx.x == 0) stamp(p, 1);
-    long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long prof_t0 = PROF ? clock64() : 0;
-    auto prof_store = [&](int base) {  // slots base..base+7 = phases, base+8 = role time
-        if constexpr (PROF) {
-            for (int i = 0; i < 8; ++i) g_wgemm_dbg[blockIdx.x * 64 + base + i] = pacc[i];
-            g_wgemm_dbg[blockIdx.x * 64 + base + 8] = clock64() - prof_t0;
-        }
-    };
+    long long pacc[4] = {0, 0, 0, 0};
 #define PT_BEGIN(v) long long v = PROF ? clock64() : 0
 #define PT_END(v, slot) do { if constexpr (PROF) pacc[slot] += clock64() - v; } while (0)
+    const long long prof_t0 = PROF ? clock64() : 0;
+    auto prof_store = [&](int base) {  // slots base..base+3 = waits, base+4 = role time
+        if constexpr (PROF) {
+            for (int i = 0; i < 4; ++i) g_wgemm_dbg[blockIdx.x * 64 + base + i] = pacc[i];
+            g_wgemm_dbg[blockIdx.x * 64 + base + 4] = clock64() - prof_t0;
+        }
+    };
 
     if (warp == kProducerWarp) {
         // ===================== producer =====================
-        const int64_t a_row = p.K * 2;
-        // Codes: one bulk copy of the unit's contiguous run.  Activations: one TMA box
-        // of 16 k-chunks x NT tokens.  Both complete on full[s] (one expected arrival).
-        auto weights = [&](const Walker& w, int n, int s) {
-            if (lane != 0) return;
+        // Codes and the unit's group scales: bulk copies of contiguous runs.  Activations:
+        // one TMA box of BLK/8 k-chunks x NT tokens.  All complete on full[s].
+        auto weights = [&](const Walker<KPU>& w, int n, int s) {
+            if (lane != 0 || (p.debug & 2)) return;
             const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
+            const int rows8 = (rows + 7) / 8 * 8, kbase = w.kb * kKB;
             const uint32_t code_bytes = uint32_t(n * CPR * rows * 16);
-            if (p.debug & (2 | 128)) return;
-            mbar_expect_tx_only(&full[s], code_bytes);
-            bulk_g2s(smem + s * GG::STAGE_BYTES,
+            const int g0 = kbase >> p.log2g;
+            int g1 = (kbase + n * kKB - 1) >> p.log2g;
+            g1 = g1 < p.GPR ? g1 : p.GPR - 1;
+            const uint32_t scale_bytes = uint32_t((g1 - g0 + 1) * rows8 * 2);
+            uint8_t* st = smem + s * GG::STAGE_BYTES;
+            mbar_expect_tx_only(&full[s], code_bytes + scale_bytes);
+            bulk_g2s(st,
                      p.codes + (int64_t(w.b) * kRows * p.KBLK * CPR + int64_t(w.kb) * CPR * rows) * 16,
                      code_bytes, &full[s]);
+            bulk_g2s(st + GG::SCALE_OFF,
+                     p.scales + int64_t(w.b) * kRows * p.GPR + int64_t(g0) * rows8, scale_bytes,
+                     &full[s]);
         };
-        auto acts = [&](const Walker& w, int n, int s) {
-            (void)n;
+        auto acts = [&](const Walker<KPU>& w, int s) {
             if (lane != 0) return;
-            if (p.debug & (2 | 64)) {
+            if (p.debug & 2) {
                 mbar_arrive(&full[s]);
                 return;
             }
@@ -474,10 +526,10 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
             tma_load_3d(smem + s * GG::STAGE_BYTES + GG::ACT_OFF, &p.tmap_a, 0, p.m0,
                         w.kb * (kKB / 8), &full[s]);
         };
-        Walker w(u0, u1, p.KBLK);
+        Walker<KPU> w(u0, u1, p.KBLK);
         int pro = 0;
         {
-            Walker t = w;
+            Walker<KPU> t = w;
             for (; pro < STAGES && t.more(); ++pro) {
                 const int n = t.chunk();
                 weights(t, n, pro);
@@ -486,26 +538,41 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         }
         grid_dep_wait();  // activations come from the previous kernel
         for (int i = 0; i < pro; ++i) {
-            const int n = w.chunk();
-            acts(w, n, i);
-            w.advance(n);
+            acts(w, i);
+            w.advance(w.chunk());
         }
-        int s = pro % STAGES;
-        uint32_t ph = pro == STAGES ? 0u : 1u;
+        Ring st(STAGES);  // stage ring position of unit `pro` onward
+        for (int i = 0; i < pro; ++i) st.next();
+        // L2 prefetch runs kPrefetch units ahead of the stage ring, so DRAM latency is
+        // covered by L2 rather than by shared-memory stages
+        constexpr int kPrefetch = 8;
+        Walker<KPU> pf = w;
+        auto prefetch_unit = [&](const Walker<KPU>& x) {
+            const int n = x.chunk(), rows = min(kRows, int(p.N - int64_t(x.b) * kRows));
+            if (lane == 0 && !(p.debug & 2))
+                prefetch_l2(p.codes + (int64_t(x.b) * kRows * p.KBLK * CPR + int64_t(x.kb) * CPR * rows) * 16,
+                            uint32_t(n * CPR * rows * 16));
+        };
+        for (int i = 0; i < kPrefetch && pf.more(); ++i) {
+            prefetch_unit(pf);
+            pf.advance(pf.chunk());
+        }
         while (w.more()) {
-            const int n = w.chunk();
-            PWAIT(&empty[s], ph, 0);
-            long long t1 = PROF ? clock64() : 0;
+            const int n = w.chunk(), s = st.idx;
+            if (pf.more()) {
+                prefetch_unit(pf);
+                pf.advance(pf.chunk());
+            }
+            PWAIT(&empty[s], st.ph ^ 1u, 0);  // the previous use of this stage is released
             weights(w, n, s);
-            if constexpr (PROF) { __syncwarp(); const long long t2 = clock64(); pacc[1] += t2 - t1; t1 = t2; }
-            acts(w, n, s);
-            if constexpr (PROF) { __syncwarp(); pacc[2] += clock64() - t1; }
+            acts(w, s);
             w.advance(n);
-            if (++s == STAGES) s = 0, ph ^= 1u;
+            st.next();
         }
         if (lane == 0) stamp(p, 2), prof_store(8);
-    } else if (warp == kMmaWarp) {
-        // ===================== MMA issuer (warp-uniform, one lane issues) =====================
+    } else if (warp >= kMmaWarp) {
+        // ===================== MMA issuers (warp-uniform, one lane issues) =====================
+        const int par = warp - kMmaWarp;
         constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
         constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                    (uint32_t(NT >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
@@ -515,129 +582,124 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                                       (uint64_t(128 >> 4) << 32) | (1ull << 46);
         constexpr uint32_t kStep = (2 * NT * 16) >> 4;  // one k16 step = 2 k-chunks
         const uint32_t act0 = smem_u32(smem + GG::ACT_OFF);
-        const uint32_t d_base = tmem + GG::D_COL0;
-        Walker w(u0, u1, p.KBLK);
-        int s = 0, slot = 0, ord = 0;
-        uint32_t ph = 0, pha = 0;
-        uint32_t acc_flag = 0;  // 0: the next MMA starts a group
-        while (w.more()) {
-            PT_BEGIN(tu);
+        const uint32_t d_base = tmem + tsp.d_col0;
+        Walker<KPU> w(u0, u1, p.KBLK);
+        Ring st(STAGES), sl(RA);
+        int ob0 = 0;  // first accumulator ordinal of the unit (gpu per unit)
+        for (int i = 0; w.more(); ++i, st.next(), sl.next(), ob0 += gpu) {
             const int n = w.chunk();
-            const bool seg_end = w.seg_end(n);
-            const int steps = n * 4, kbase = w.kb * kKB;
-            // k16 steps after which a group's accumulator is complete
-            const uint32_t ends = unit_ends(kbase, steps, seg_end, p.log2g, gmask, p.full_k);
-            PT_END(tu, 3);
-            PWAIT(&full[s], ph, 0);
-            PWAIT(&a_full[slot], pha, 1);
-            tc_fence_after();
-            PT_BEGIN(tm);
-            const uint64_t bdesc0 = bdesc_hi | uint64_t(((act0 + s * GG::STAGE_BYTES) >> 4) & 0x3FFFu);
-            const uint32_t a_base = tmem + slot * (kKPU * 32);
-            if ((ends & ~(1u << (steps - 1))) == 0) {
-                // fast path: the whole unit feeds one group accumulator (g >= 128)
-                const int buf = ord & (ND - 1);
-                if (acc_flag == 0 && ord >= ND) {
-                    PWAIT(&d_empty[buf], uint32_t((ord / ND - 1) & 1), 2);
-                    tc_fence_after();
-                }
-                if (!(p.debug & 4)) {
-                    if (steps == 8)
-                        umma_unit_elect<8, kStep>(d_base + buf * NT, a_base, bdesc0, idesc, acc_flag);
-                    else
-                        umma_unit_elect<4, kStep>(d_base + buf * NT, a_base, bdesc0, idesc, acc_flag);
-                }
-                acc_flag = 1;
-                if (ends) {
-                    tc_commit_elect(&d_full[buf]);
-                    ++ord;
-                    acc_flag = 0;
-                }
-            } else
-#pragma unroll
-            for (int kk = 0; kk < kKPU * 4; ++kk) {
-                if (kk < steps) {
-                    const int buf = ord & (ND - 1);
-                    if (acc_flag == 0 && ord >= ND) {  // buffer reuse: wait for its epilogue
-                        PWAIT(&d_empty[buf], uint32_t((ord / ND - 1) & 1), 2);
+            if ((i & 1) == par) {
+                const int s = st.idx, slot = sl.idx;
+                const int kbase = w.kb * kKB, kend = kbase + n * kKB, blk = kbase & ~(GG::BLK - 1);
+                PWAIT(&full[s], st.ph, 0);
+                PWAIT(&a_full[slot], sl.ph, 1);
+                tc_fence_after();
+                const uint64_t bdesc0 =
+                    bdesc_hi | uint64_t(((act0 + s * GG::STAGE_BYTES) >> 4) & 0x3FFFu);
+                const uint32_t a_base = tmem + slot * GG::SLOT_COLS;
+                for (int j = 0; j < gpu; ++j) {
+                    const int ob = ob0 + j, buf = ob & (ND - 1);
+                    if (ob >= ND) {  // accumulator reuse: wait for the epilogue to drain it
+                        PWAIT(&d_empty[buf], uint32_t((ob >> lnd) - 1) & 1u, 2);
                         tc_fence_after();
                     }
-                    if (!(p.debug & 4))
-                        umma_f16_elect(d_base + buf * NT, a_base + kk * 8,
-                                       bdesc0 + uint64_t(kk * kStep), idesc, acc_flag);
-                    acc_flag = 1;
-                    if (ends & (1u << kk)) {
-                        tc_commit_elect(&d_full[buf]);
-                        ++ord;
-                        acc_flag = 0;
-                    }
+                    int k0, cnt;
+                    subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
+                    if (cnt > 0 && !(p.debug & 4))
+                        issue_steps<kStep>(d_base + buf * NT, a_base + k0 * 8,
+                                           bdesc0 + uint64_t(k0 * kStep), idesc, cnt);
+                    tc_commit_elect(&d_full[buf]);
                 }
+                tc_commit_elect(&a_empty[slot]);
+                tc_commit_elect(&empty[s]);  // activations of this stage consumed
             }
-            PT_END(tm, 4);
-            PT_BEGIN(tc);
-            tc_commit_elect(&a_empty[slot]);
-            tc_commit_elect(&empty[s]);  // activations of this stage consumed
-            PT_END(tc, 5);
             w.advance(n);
-            if (++s == STAGES) s = 0, ph ^= 1u;
-            if (++slot == kRA) slot = 0, pha ^= 1u;
         }
-        if (lane == 0) stamp(p, 3), prof_store(20);
+        if (lane == 0 && par == 0) stamp(p, 3), prof_store(20);
     } else if (warp < kDequantWarps) {
         // ===================== dequantizers =====================
         const int q = warp & 3, par = warp >> 2;
         const int row = q * 32 + lane;  // row within the row-block = TMEM lane
         const uint32_t lane_base = uint32_t(q * 32) << 16;
-        Walker w(u0, u1, p.KBLK);
-        int i = 0;  // unit index within this CTA
-        while (w.more()) {
+        Walker<KPU> w(u0, u1, p.KBLK);
+        Ring st(STAGES), sl(RA), me(MB);
+        for (int i = 0; w.more(); ++i, st.next(), sl.next(), me.next()) {
             const int n = w.chunk();
             if ((i & 1) == par) {
-                const int s = i % STAGES, slot = i % kRA;
-                const uint32_t ph = uint32_t(i / STAGES) & 1u, pha = uint32_t(i / kRA) & 1u;
+                const int s = st.idx, slot = sl.idx;
                 const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
-                PWAIT(&full[s], ph, 0);
+                PWAIT(&full[s], st.ph, 0);
                 const uint8_t* st = smem + s * GG::STAGE_BYTES + row * 16;
-                uint4 v[kKPU * CPR];
+                const uint32_t ta = tmem + lane_base + slot * GG::SLOT_COLS;
 #pragma unroll
-                for (int j = 0; j < kKPU * CPR; ++j)
-                    if (j < n * CPR) v[j] = *reinterpret_cast<const uint4*>(st + j * rows * 16);
-                uint32_t col[kKPU * 32];
+                for (int h = 0; h < KPU / 2; ++h) {  // two k-blocks (64 columns) at a time
+                    if (2 * h < n) {
+                        PT_BEGIN(tq);
+                        uint4 v[2 * CPR];
 #pragma unroll
-                for (int j = 0; j < kKPU * CPR; ++j) {
-                    if constexpr (BITS == 4) {
-                        dequant4<AT>(v[j].x, col + j * 16 + 0);
-                        dequant4<AT>(v[j].y, col + j * 16 + 4);
-                        dequant4<AT>(v[j].z, col + j * 16 + 8);
-                        dequant4<AT>(v[j].w, col + j * 16 + 12);
-                    } else {
-                        dequant8<AT>(v[j].x, col + j * 8 + 0);
-                        dequant8<AT>(v[j].y, col + j * 8 + 2);
-                        dequant8<AT>(v[j].z, col + j * 8 + 4);
-                        dequant8<AT>(v[j].w, col + j * 8 + 6);
+                        for (int j = 0; j < 2 * CPR; ++j)
+                            if (2 * h * CPR + j < n * CPR)
+                                v[j] = *reinterpret_cast<const uint4*>(st + (2 * h * CPR + j) * rows * 16);
+                        uint32_t col[64];
+#pragma unroll
+                        for (int j = 0; j < 2 * CPR; ++j) {
+                            if constexpr (BITS == 4) {
+                                dequant4<AT>(v[j].x, col + j * 16 + 0);
+                                dequant4<AT>(v[j].y, col + j * 16 + 4);
+                                dequant4<AT>(v[j].z, col + j * 16 + 8);
+                                dequant4<AT>(v[j].w, col + j * 16 + 12);
+                            } else {
+                                dequant8<AT>(v[j].x, col + j * 8 + 0);
+                                dequant8<AT>(v[j].y, col + j * 8 + 2);
+                                dequant8<AT>(v[j].z, col + j * 8 + 4);
+                                dequant8<AT>(v[j].w, col + j * 8 + 6);
+                            }
+                        }
+                        if constexpr (PROF) asm volatile("" ::"r"(col[0]), "r"(col[63]));
+                        PT_END(tq, 2);
+                        if (h == 0) {
+                            if (i >= RA) {  // slot free? (its MMA overlapped this dequant)
+                                PWAIT(&a_empty[slot], sl.ph ^ 1u, 1);
+                                tc_fence_after();
+                            }
+                            // this row's group scales -> the epilogue's mailbox entry
+                            const int kbase = w.kb * kKB, kend = kbase + n * kKB;
+                            const int blk = kbase & ~(GG::BLK - 1), g0 = kbase >> p.log2g;
+                            const int rows8 = (rows + 7) / 8 * 8;
+                            const __half* sc_st = reinterpret_cast<const __half*>(
+                                                      smem + s * GG::STAGE_BYTES + GG::SCALE_OFF) + row;
+                            __half* mb = mbox + me.idx * gpu * kRows + row;
+                            for (int j = 0; j < gpu; ++j) {
+                                int k0, cnt;
+                                subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
+                                int grp = (blk + (j << lg)) >> p.log2g;
+                                grp = grp < p.GPR ? grp : p.GPR - 1;
+                                mb[j * kRows] = cnt > 0 && row < rows ? sc_st[(grp - g0) * rows8]
+                                                                      : __float2half(0.0f);
+                            }
+                        }
+                        PT_BEGIN(tw);
+                        if (!(p.debug & 8)) {
+                            tmem_st32(ta + h * 64, col);
+                            if (2 * h + 1 < n) tmem_st32(ta + h * 64 + 32, col + 32);
+                        }
+                        PT_END(tw, 3);
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);  // codes of this unit consumed
-                if (i >= kRA) {
-                    PWAIT(&a_empty[slot], pha ^ 1u, 1);
-                    tc_fence_after();
-                }
-                const uint32_t ta = tmem + lane_base + slot * (kKPU * 32);
-                if (!(p.debug & 8)) {
-                    tmem_st32(ta, col);
-                    if (n > 1) tmem_st32(ta + 32, col + 32);
-                }
+                PT_BEGIN(tw2);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                PT_END(tw2, 3);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&a_full[slot]);
+                if (lane == 0) {
+                    mbar_arrive(&a_full[slot]);
+                    mbar_arrive(&empty[s]);  // codes and scales of this unit consumed
+                    mbar_arrive(&m_full[me.idx]);
+                }
             }
             w.advance(n);
-            ++i;
         }
-        if (threadIdx.x == 0) stamp(p, 4);
-        if (threadIdx.x == 0) prof_store(32);
+        if (threadIdx.x == 0) stamp(p, 4), prof_store(32);
     } else if (warp < kEpiWarp0 + kEpiWarps) {
         // ===================== epilogue =====================
         const int q = warp & 3;  // TMEM lane quadrant
@@ -701,45 +763,44 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
             write(sum);
         };
 
-        Walker w(u0, u1, p.KBLK);
+        Walker<KPU> w(u0, u1, p.KBLK);
         int seg_kb0 = w.kb;
-        int ord = 0;
-        while (w.more()) {
+        Ring me(MB);
+        int ob0 = 0;
+        for (; w.more(); me.next(), ob0 += gpu) {
             const int n = w.chunk();
             const bool seg_end = w.seg_end(n);
             const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
             const int rows8 = (rows + 7) / 8 * 8;
-            const __half* sc_row =
-                reinterpret_cast<const __half*>(p.scales) + int64_t(w.b) * kRows * p.GPR + row;
-            const int steps = n * 4, kbase = w.kb * kKB;
-            uint32_t ends = unit_ends(kbase, steps, seg_end, p.log2g, gmask, p.full_k);
-            while (ends) {
-                const int kk = __ffs(ends) - 1;
-                ends &= ends - 1;
-                const int knext = kbase + (kk + 1) * 16;
-                int grp = (knext - 1) >> p.log2g;
-                grp = grp < p.GPR ? grp : p.GPR - 1;
-                // the scale a few groups ahead goes to L1 now, so this load hits later
-                if (grp + 4 < p.GPR && row < rows)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(sc_row + int64_t(grp + 4) * rows8));
-                const float sc =
-                    row < rows ? __half2float(__ldg(sc_row + int64_t(grp) * rows8)) : 0.0f;
-                const int buf = ord & (ND - 1);
-                PWAIT(&d_full[buf], uint32_t((ord / ND) & 1), 0);
+            const int kbase = w.kb * kKB, kend = kbase + n * kKB, blk = kbase & ~(GG::BLK - 1);
+            // this unit's scales, handed over by its dequant warps
+            PWAIT(&m_full[me.idx], me.ph, 1);
+            const __half* mb = mbox + me.idx * gpu * kRows + row;
+            for (int j = 0; j < gpu; ++j) {
+                const int ob = ob0 + j, buf = ob & (ND - 1);
+                int k0, cnt;
+                subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
+                const float sc = __half2float(mb[j * kRows]);
+                PWAIT(&d_full[buf], uint32_t(ob >> lnd) & 1u, 0);
                 tc_fence_after();
+                if (cnt == 0) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&d_empty[buf]);
+                    continue;
+                }
 #pragma unroll
-                for (int j = 0; j < NT; j += 32) {
+                for (int jj = 0; jj < NT; jj += 32) {
                     uint32_t v[32];
                     if (!(p.debug & 16)) {
-                        tmem_ld16_nw(tmem + lane_base + GG::D_COL0 + buf * NT + j, v);
+                        tmem_ld16_nw(tmem + lane_base + tsp.d_col0 + buf * NT + jj, v);
                         if constexpr (NT >= 32)
-                            tmem_ld16_nw(tmem + lane_base + GG::D_COL0 + buf * NT + j + 16, v + 16);
+                            tmem_ld16_nw(tmem + lane_base + tsp.d_col0 + buf * NT + jj + 16, v + 16);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     } else {
 #pragma unroll
                         for (int e = 0; e < 32; ++e) v[e] = 0;
                     }
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (j + 32 >= NT) {  // last read of this buffer: hand it back
+                    if (jj + 32 >= NT) {  // last read of this accumulator: hand it back
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&d_empty[buf]);
@@ -747,15 +808,13 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                     constexpr int W = NT < 32 ? NT : 32;
 #pragma unroll
                     for (int e = 0; e < W; ++e)
-                        acc[j + e] = fmaf(sc, __uint_as_float(v[e]), acc[j + e]);
+                        acc[jj + e] = fmaf(sc, __uint_as_float(v[e]), acc[jj + e]);
                 }
-                ++ord;
             }
             if (seg_end) {
                 if (et == 0) stamp(p, 5);
                 epilogue(w.b, seg_kb0 == 0 && w.kb + n == p.KBLK);
-                if (et == 0) stamp(p, 6);
-                if (et == 0) prof_store(44);
+                if (et == 0) stamp(p, 6), prof_store(44);
 #pragma unroll
                 for (int j = 0; j < NT; ++j) acc[j] = 0.0f;
                 w.advance(n);
@@ -786,11 +845,17 @@ int sm_count() {
     return n;
 }
 
-// Token tile = the MMA N (M=128 UMMA needs N % 16 == 0).
-int nt_for(int64_t m) { return m <= 16 ? 16 : m <= 32 ? 32 : 64; }
+// Token tile = the MMA N (M=128 UMMA needs N % 16 == 0).  A unit needs one accumulator
+// per group-sized piece of its block (blk/g), and TMEM holds 256/NT of them.
+int nt_for(int64_t m, int64_t g, int bits) {
+    const int64_t blk = bits == 4 ? 256 : 128;
+    const int64_t per_unit = g >= blk ? 1 : blk / g;
+    int nt = m <= 16 ? 16 : m <= 32 ? 32 : 64;
+    while (nt > 16 && 256 / nt < per_unit) nt /= 2;
+    return nt;
+}
 
-int ctas_for(int64_t U, int nt) {
-    (void)nt;
+int ctas_for(int64_t U) {
     int G = sm_count();  // persistent: one CTA per SM (it owns all 512 TMEM columns)
     if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
     if (G < 1) G = 1;
@@ -869,10 +934,9 @@ size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t 
     const int64_t NB = (n + tc::kRows - 1) / tc::kRows;
     const int64_t U = NB * ((k + 63) / 64 > 0 ? (k + 63) / 64 : 1);
     size_t part = 0;
-    (void)g;
     for (int nt : {16, 32, 64}) {  // every tile a call may launch
-        if (nt > tc::nt_for(m)) break;
-        const int G = tc::ctas_for(U, nt);
+        if (nt > tc::nt_for(m, g, bits)) break;
+        const int G = tc::ctas_for(U);
         const size_t need = size_t(G) * 2 * tc::kRows * nt * sizeof(float);
         part = need > part ? need : part;
     }
@@ -880,13 +944,13 @@ size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t 
 }
 
 // Activations [m][k] viewed as a 3-D tensor (8 elements, token, k-chunk) so one TMA box
-// {8, nt, 16} lands in shared memory as [k-chunk][token][16 B] -- UMMA K-major core
+// {8, nt, chunks per unit} lands in shared memory as [k-chunk][token][16 B] -- UMMA K-major core
 // matrices.  Tokens >= m and chunks past k are out of bounds and arrive as zeros.
 static cudaError_t encode_act_map(CUtensorMap* map, const void* a, int a_dtype, int64_t m,
-                                  int64_t k, int nt) {
+                                  int64_t k, int nt, int chunks) {
     const cuuint64_t dims[3] = {8, cuuint64_t(m), cuuint64_t(k / 8)};
     const cuuint64_t strides[2] = {cuuint64_t(k * 2), 16};
-    const cuuint32_t box[3] = {8, cuuint32_t(nt), 16};
+    const cuuint32_t box[3] = {8, cuuint32_t(nt), cuuint32_t(chunks)};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = cuTensorMapEncodeTiled(
         map, a_dtype == RTNQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
@@ -904,7 +968,6 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
     p.K = A.k;
     p.NB = int((A.n + tc::kRows - 1) / tc::kRows);
     p.KBLK = int((A.k + 63) / 64);
-    p.full_k = int((A.k + 15) / 16 * 16);
     p.GPR = int(A.g >= A.k ? 1 : (A.k + A.g - 1) / A.g);
     p.log2g = A.g >= A.k ? 30 : __builtin_ctzll(uint64_t(A.g));
     p.out_dtype = A.out_dtype;
@@ -915,15 +978,15 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
         return cudaErrorInvalidValue;
     p.U = p.NB * p.KBLK;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
-    const int nt_max = tc::nt_for(A.m);
+    const int nt_max = tc::nt_for(A.m, A.g, A.bits);
     for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {  // one pass per token tile
         p.M = int(A.m - m0 < nt_max ? A.m - m0 : nt_max);
-        p.a = static_cast<const char*>(A.a) + m0 * A.k * 2;
         p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
-        const int nt = tc::nt_for(p.M);
+        const int nt = tc::nt_for(p.M, A.g, A.bits);
         p.m0 = int(m0);
-        if (cudaError_t e = encode_act_map(&p.tmap_a, A.a, A.a_dtype, A.m, A.k, nt)) return e;
-        p.G = tc::ctas_for(p.U, nt);
+        if (cudaError_t e = encode_act_map(&p.tmap_a, A.a, A.a_dtype, A.m, A.k, nt,
+                                             A.bits == 4 ? 32 : 16)) return e;
+        p.G = tc::ctas_for(p.U);
         const bool pdl = A.pdl || m0 > 0;
         cudaError_t e;
         if (A.bits == 4)
