@@ -61,7 +61,8 @@ enum { RTNQ_F32 = 0, RTNQ_F16 = 1, RTNQ_BF16 = 2 };
 enum { RTNQ_ROW_MAJOR = 0, RTNQ_KERNEL_INTERLEAVED = 1, RTNQ_NATIVE_SM100 = 2 };
 
 /* Scale orders: REF = [row][group] as in QuantTensor::scales (quant.hpp:33);
- * NATIVE = [group][strip16][gid][half]. */
+ * NATIVE = per 128-row row-block, [group][row padded to 8], so a
+ * unit's scales are one contiguous 16-byte-aligned run. */
 enum { RTNQ_SCALES_REF = 0, RTNQ_SCALES_NATIVE = 1 };
 
 /* GEMM paths.  FUSED/DEQUANT_FIRST mirror rtnq::GemmPath (gemm.hpp:12); AUTO
@@ -132,9 +133,10 @@ rtnq_status rtnq_dev_dequantize(const uint8_t* codes, rtnq_layout layout, int bi
 /* The quantized linear: out (m x n) = a (m x k) * W^T, W = codes * scales
  * (gemm.hpp:18-49).  Kernel selection:
  *   FUSED, NATIVE_SM100 codes, a in BF16/F16, scales F16 native order:
- *       sm_100a tensor-core W4A16/W8A16 kernel (TMA bulk-copy pipeline,
- *       register dequant, stream-K with deterministic fixup).  Needs
- *       g % 16 == 0 or g >= k, and k a multiple of 64 (4-bit) / 32 (8-bit).
+ *       sm_100a tensor-core W4A16/W8A16 kernel (tcgen05.mma with the weights
+ *       dequantized into TMEM, TMA pipeline, stream-K with a deterministic
+ *       fixup).  Needs g % 16 == 0 or g >= k, k % 8 == 0 and
+ *       16-byte aligned a / codes / scales.
  *   FUSED, any layout, a in F32, scales F32 reference order:
  *       reference-exact CUDA-core kernel, bit-identical to gemm_fused
  *       (gemm.cpp:46-92).

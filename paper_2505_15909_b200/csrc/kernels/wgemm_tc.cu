@@ -952,7 +952,23 @@ static cudaError_t encode_act_map(CUtensorMap* map, const void* a, int a_dtype, 
     const cuuint64_t strides[2] = {cuuint64_t(k * 2), 16};
     const cuuint32_t box[3] = {8, cuuint32_t(nt), cuuint32_t(chunks)};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = cuTensorMapEncodeTiled(
+    // the driver entry point is fetched through the runtime, so the library does not link
+    // libcuda (it must load on a machine without a driver, e.g. for the CPU test suite)
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<EncodeFn>(fn);
+    }();
+    if (!encode) return cudaErrorNotSupported;
+    const CUresult r = encode(
         map, a_dtype == RTNQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
         3, const_cast<void*>(a), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
