@@ -211,6 +211,10 @@ rtnq_status rtnq_gemm(int path, const float* a, int64_t m, int64_t k, const uint
                       int64_t nbytes, rtnq_layout layout, int bits, int64_t n, int64_t g,
                       int ragged, const float* scales, int64_t threshold, int* chosen,
                       float* out);
+/* f32_to_f16 / f16_to_f32 (f16.hpp:13-16, f16.cpp:8-63) over arrays: RNE narrowing
+ * (quiet NaN kept), exact widening.  Pure host functions (no device needed). */
+rtnq_status rtnq_f32_to_f16(const float* in, int64_t n, uint16_t* out);
+rtnq_status rtnq_f16_to_f32(const uint16_t* in, int64_t n, float* out);
 /* gemm_float (gemm.hpp:46-49). */
 rtnq_status rtnq_gemm_float(const float* a, int64_t m, int64_t k, const float* w, int64_t n,
                             int64_t block, float* out);

@@ -98,6 +98,8 @@ def lib():
     L.rtnq_gemm.argtypes = [_i32, _p, _i64, _i64, _p, _i64, Layout, _i32, _i64, _i64, _i32, _p,
                             _i64, _p, _p]
     L.rtnq_gemm_float.argtypes = [_p, _i64, _i64, _p, _i64, _i64, _p]
+    L.rtnq_f32_to_f16.argtypes = [_p, _i64, _p]
+    L.rtnq_f16_to_f32.argtypes = [_p, _i64, _p]
     L.rtnq_plan_resolve.argtypes = [C.c_char_p, _i64, _p, C.c_char_p, _i64, _p]
     L.rtnq_effective_bits.argtypes = [_p, _i64, _p, _p, _i64, _i32, _p]
     _lib = L
@@ -403,6 +405,22 @@ def gemm_oracle(a, data, lay, bits, n, g, scales, ragged=False):
 def gemm_auto(a, data, lay, bits, n, g, scales, threshold=DEFAULT_THRESHOLD, ragged=False):
     """-> (out, chosen path: 0 fused / 1 dequant_first) (gemm.hpp:38-40)."""
     return _gemm(PATH_AUTO, a, data, lay, bits, n, g, scales, ragged, threshold)
+
+
+def f32_to_f16(values):
+    """f32 -> binary16 bits, RNE (f16.cpp:8-41)."""
+    v = _f32(values).ravel()
+    out = np.zeros(v.size, np.uint16)
+    _check(lib().rtnq_f32_to_f16(_np(v), v.size, _np(out)))
+    return out
+
+
+def f16_to_f32(bits):
+    """binary16 bits -> f32, exact (f16.cpp:43-63)."""
+    b = np.ascontiguousarray(bits, dtype=np.uint16).ravel()
+    out = np.zeros(b.size, np.float32)
+    _check(lib().rtnq_f16_to_f32(_np(b), b.size, _np(out)))
+    return out
 
 
 def gemm_float(a, w, block: int):

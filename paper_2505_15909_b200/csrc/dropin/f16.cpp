@@ -5,6 +5,8 @@
 
 #include <bit>
 
+#include "rtnq_capi.h"
+
 namespace rtnq {
 
 std::uint16_t f32_to_f16(float value) {
@@ -19,3 +21,13 @@ float f16_to_f32(std::uint16_t bits) {
 }
 
 }  // namespace rtnq
+
+extern "C" rtnq_status rtnq_f32_to_f16(const float* in, int64_t n, uint16_t* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = rtnq::f32_to_f16(in[i]);
+    return RTNQ_OK;
+}
+
+extern "C" rtnq_status rtnq_f16_to_f32(const uint16_t* in, int64_t n, float* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = rtnq::f16_to_f32(in[i]);
+    return RTNQ_OK;
+}

@@ -111,3 +111,15 @@ def test_effective_bits(golden_plan):
     t, _ = rq.plan.resolve("first:1 modules:1+3+4", 80)
     e1 = rq.plan.effective_bits(t, r70, c70, 128)
     assert e1 == eff[2] and abs((e1 - 4.0) - 47.0 / 1020.0) < 1e-12
+
+
+def test_f16_conversions_match_reference_golden(golden_f16):
+    # f16.cpp:8-63 through the C-ABI, against the reference-generated fixture
+    # (tests/golden/f16.npz: narrowed xs, and every one of the 65536 encodings widened)
+    xs = golden_f16["xs"].astype(np.float32)
+    assert np.array_equal(rq.f32_to_f16(xs), golden_f16["narrowed"].astype(np.uint16))
+    allbits = np.arange(65536, dtype=np.uint16)
+    widened = rq.f16_to_f32(allbits)
+    ref = golden_f16["widened"].view(np.float32)  # stored as f32 bit patterns
+    same = widened.view(np.uint32) == ref.view(np.uint32)
+    assert np.all(same | (np.isnan(widened) & np.isnan(ref)))
