@@ -174,6 +174,20 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
 rtnq_status rtnq_dev_gemm_float(const float* a, int64_t m, int64_t k, const float* w, int64_t n,
                                 int64_t block, float* out, void* stream);
 
+/* ---- decode layer (the callers around the linear; SURVEY §3C toy.cpp:91-117, with
+ * Llama-3.1 GQA/RoPE/KV cache).  bf16 device tensors, f32 math, async on `stream`. */
+/* x (m x h) += delta (nullable), then out = rmsnorm(x) * weight (toy.cpp:19-30). */
+rtnq_status rtnq_dev_add_rmsnorm(void* x, const void* delta, const void* weight, void* out,
+                                 int64_t m, int64_t h, float eps, void* stream);
+/* act (m x f) = silu(gate_up[:, :f]) * gate_up[:, f:] (toy.cpp:108-112). */
+rtnq_status rtnq_dev_silu_mul(const void* gate_up, void* act, int64_t m, int64_t f, void* stream);
+/* One decode step of GQA attention: qkv rows [hq*d | hkv*d | hkv*d]; the rotated key and
+ * the value are appended to the caches ([batch][max_len][hkv][d]) at `pos`, then each
+ * query head attends over positions [0, pos].  head_dim 128, hq/hkv <= 32. */
+rtnq_status rtnq_dev_decode_attention(const void* qkv, void* k_cache, void* v_cache, void* out,
+                                      int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                      int64_t max_len, int64_t pos, float rope_theta,
+                                      void* stream);
 /* Synchronizes `stream`, reads and clears *err_flag (device), returns
  * RTNQ_E_INVALID_INPUT if it was set. */
 rtnq_status rtnq_dev_check_flag(int32_t* err_flag, void* stream);

@@ -98,6 +98,10 @@ def lib():
     L.rtnq_gemm.argtypes = [_i32, _p, _i64, _i64, _p, _i64, Layout, _i32, _i64, _i64, _i32, _p,
                             _i64, _p, _p]
     L.rtnq_gemm_float.argtypes = [_p, _i64, _i64, _p, _i64, _i64, _p]
+    L.rtnq_dev_add_rmsnorm.argtypes = [_p, _p, _p, _p, _i64, _i64, C.c_float, _p]
+    L.rtnq_dev_silu_mul.argtypes = [_p, _p, _i64, _i64, _p]
+    L.rtnq_dev_decode_attention.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
+                                            C.c_float, _p]
     L.rtnq_f32_to_f16.argtypes = [_p, _i64, _p]
     L.rtnq_f16_to_f32.argtypes = [_p, _i64, _p]
     L.rtnq_plan_resolve.argtypes = [C.c_char_p, _i64, _p, C.c_char_p, _i64, _p]
@@ -292,6 +296,31 @@ def linear_raw(a, a_dtype, m, k, codes, lay, bits, n, g, ragged, scales, s_dtype
                                  out_dtype, path, threshold, C.byref(chosen), _ptr(err),
                                  _ptr(ws), ws_bytes, _stream(stream)))
     return chosen.value
+
+
+def add_rmsnorm(x, weight, out, delta=None, eps=1e-5, stream=None):
+    """x += delta (if given); out = rmsnorm(x) * weight.  bf16 [m, h] (rtnq_dev_add_rmsnorm)."""
+    m, h = x.shape
+    _check(lib().rtnq_dev_add_rmsnorm(_ptr(x), _ptr(delta), _ptr(weight), _ptr(out), m, h, eps,
+                                      _stream(stream)))
+    return out
+
+
+def silu_mul(gate_up, act, stream=None):
+    """act[m, f] = silu(gate_up[:, :f]) * gate_up[:, f:] (rtnq_dev_silu_mul)."""
+    m, f = act.shape
+    _check(lib().rtnq_dev_silu_mul(_ptr(gate_up), _ptr(act), m, f, _stream(stream)))
+    return act
+
+
+def decode_attention(qkv, k_cache, v_cache, out, hq, hkv, pos, head_dim=128, theta=500000.0,
+                     stream=None):
+    """GQA decode attention with RoPE over a KV cache (rtnq_dev_decode_attention)."""
+    batch, max_len = k_cache.shape[0], k_cache.shape[1]
+    _check(lib().rtnq_dev_decode_attention(_ptr(qkv), _ptr(k_cache), _ptr(v_cache), _ptr(out),
+                                           batch, hq, hkv, head_dim, max_len, pos, theta,
+                                           _stream(stream)))
+    return out
 
 
 def relayout(src, frm: Layout, to: Layout, bits, rows, cols, stream=None):

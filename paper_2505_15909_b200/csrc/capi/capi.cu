@@ -326,6 +326,37 @@ rtnq_status rtnq_dev_gemm_float(const float* a, int64_t m, int64_t k, const floa
     return RTNQ_OK;
 }
 
+// ---- decode-layer kernels (decode.cu) ------------------------------------------------
+
+rtnq_status rtnq_dev_add_rmsnorm(void* x, const void* delta, const void* weight, void* out,
+                                 int64_t m, int64_t h, float eps, void* stream) {
+    if (m < 0 || h <= 0 || h % 8) return fail(RTNQ_E_SHAPE, "rmsnorm needs h % 8 == 0");
+    if (m == 0) return RTNQ_OK;
+    RTNQ_CUDA(launch_add_rmsnorm(x, delta, weight, out, m, h, eps, static_cast<cudaStream_t>(stream)));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_silu_mul(const void* gate_up, void* act, int64_t m, int64_t f, void* stream) {
+    if (m < 0 || f <= 0 || f % 8) return fail(RTNQ_E_SHAPE, "silu_mul needs f % 8 == 0");
+    if (m == 0) return RTNQ_OK;
+    RTNQ_CUDA(launch_silu_mul(gate_up, act, m, f, static_cast<cudaStream_t>(stream)));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_decode_attention(const void* qkv, void* k_cache, void* v_cache, void* out,
+                                      int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                      int64_t max_len, int64_t pos, float rope_theta,
+                                      void* stream) {
+    if (head_dim != 128) return fail(RTNQ_E_UNSUPPORTED, "decode attention needs head_dim 128");
+    if (hkv <= 0 || hq % hkv || hq / hkv > 32)
+        return fail(RTNQ_E_SHAPE, "query heads must be a multiple (<= 32x) of kv heads");
+    if (pos < 0 || pos >= max_len) return fail(RTNQ_E_INVALID_INPUT, "position outside the cache");
+    if (batch == 0) return RTNQ_OK;
+    RTNQ_CUDA(launch_decode_attention(qkv, k_cache, v_cache, out, batch, hq, hkv, head_dim, max_len,
+                                      pos, rope_theta, static_cast<cudaStream_t>(stream)));
+    return RTNQ_OK;
+}
+
 rtnq_status rtnq_dev_check_flag(int32_t* err, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int32_t h = 0;

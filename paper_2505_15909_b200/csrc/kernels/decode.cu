@@ -1,0 +1,213 @@
+// decode.cu -- the non-GEMM kernels of one decode layer (toy.cpp:91-117,
+// generalized to Llama-3.1: GQA, RoPE, a KV cache): fused residual-add + RMSNorm,
+// decode attention over the cache, SiLU-gated FFN activation.  All bf16 in HBM, f32
+// math.  These are small next to the weight stream and are written for
+// HBM efficiency: 16-byte loads, one pass over the data.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+
+namespace rtnq_b200 {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// x <- x + delta (if delta), out <- rmsnorm(x) * w.  One CTA per token row (toy.cpp:19-30:
+// mean of squares, 1/sqrt(ms + eps), times the norm weight).
+__global__ void add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                                   const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out,
+                                   int h, float eps) {
+    extern __shared__ float red[];
+    const int row = blockIdx.x;
+    __nv_bfloat16* xr = x + int64_t(row) * h;
+    const __nv_bfloat16* dr = delta ? delta + int64_t(row) * h : nullptr;
+    float ss = 0.0f;
+    for (int i = threadIdx.x * 8; i < h; i += blockDim.x * 8) {
+        uint4 xv = *reinterpret_cast<const uint4*>(xr + i);
+        __nv_bfloat162* xp = reinterpret_cast<__nv_bfloat162*>(&xv);
+        if (dr) {
+            const uint4 dv = *reinterpret_cast<const uint4*>(dr + i);
+            const __nv_bfloat162* dp = reinterpret_cast<const __nv_bfloat162*>(&dv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 a = __bfloat1622float2(xp[j]), b = __bfloat1622float2(dp[j]);
+                xp[j] = __floats2bfloat162_rn(a.x + b.x, a.y + b.y);
+            }
+            *reinterpret_cast<uint4*>(xr + i) = xv;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 a = __bfloat1622float2(xp[j]);
+            ss += a.x * a.x + a.y * a.y;
+        }
+    }
+    ss = warp_sum(ss);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (warp == 0) {
+        float v = lane < nw ? red[lane] : 0.0f;
+        v = warp_sum(v);
+        if (lane == 0) red[0] = rsqrtf(v / float(h) + eps);
+    }
+    __syncthreads();
+    const float inv = red[0];
+    for (int i = threadIdx.x * 8; i < h; i += blockDim.x * 8) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(xr + i);
+        const uint4 wv = *reinterpret_cast<const uint4*>(w + i);
+        const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&xv);
+        const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&wv);
+        uint4 ov;
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&ov);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 a = __bfloat1622float2(xp[j]), b = __bfloat1622float2(wp[j]);
+            op[j] = __floats2bfloat162_rn(a.x * inv * b.x, a.y * inv * b.y);
+        }
+        *reinterpret_cast<uint4*>(out + int64_t(row) * h + i) = ov;
+    }
+}
+
+// act[t][j] = silu(gu[t][j]) * gu[t][f + j]: gate in columns [0, f), up in [f, 2f)
+// (toy.cpp:108-112 keeps the same fused [gate | up] output).
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
+                                int64_t m, int f) {
+    const int64_t n8 = m * f / 8;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t e = i * 8, t = e / f, j = e % f;
+        const uint4 gv = *reinterpret_cast<const uint4*>(gu + t * 2 * f + j);
+        const uint4 uv = *reinterpret_cast<const uint4*>(gu + t * 2 * f + f + j);
+        const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gv);
+        const __nv_bfloat162* up = reinterpret_cast<const __nv_bfloat162*>(&uv);
+        uint4 ov;
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&ov);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 g = __bfloat1622float2(gp[q]), u = __bfloat1622float2(up[q]);
+            op[q] = __floats2bfloat162_rn(g.x / (1.0f + __expf(-g.x)) * u.x,
+                                          g.y / (1.0f + __expf(-g.y)) * u.y);
+        }
+        *reinterpret_cast<uint4*>(act + e) = ov;
+    }
+}
+
+// Rotate-half RoPE of one head vector element pair (d, d + D/2) at position pos.
+__device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, float theta) {
+    const float inv = __powf(theta, -2.0f * float(d) / float(D));
+    float s, c;
+    __sincosf(float(pos) * inv, &s, &c);
+    return make_float2(a * c - b * s, b * c + a * s);
+}
+
+// Decode attention for one (token b, kv head): the group's query heads attend over cache
+// positions [0, pos] after the new k/v (rotated k) are appended at `pos`.
+// qkv row layout: [Hq*D | Hkv*D | Hkv*D] (the column-split QKV output of one rank).
+// cache layout: [B][Lmax][Hkv][D] for K and for V.  One CTA = G warps (G = Hq/Hkv <= 32);
+// warp w owns query head kvh * G + w; head_dim D = 128 (4 elements per lane).
+constexpr int kD = 128;
+__global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                        __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+                                        __nv_bfloat16* __restrict__ out, int hq, int hkv, int lmax,
+                                        int pos, float theta) {
+    const int b = blockIdx.y, kvh = blockIdx.x, G = hq / hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row = int64_t(b) * (hq + 2 * hkv) * kD;
+    const __nv_bfloat16* kn = qkv + row + int64_t(hq) * kD + int64_t(kvh) * kD;
+    const __nv_bfloat16* vn = kn + int64_t(hkv) * kD;
+    const int64_t cstride = int64_t(hkv) * kD;  // between positions
+    __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
+    __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
+    // append the new (rotated) key and the value at `pos` -- warp 0, lanes own d = lane,
+    // lane+32 (first half) and their rotation partners in the second half
+    if (warp == 0) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int d = lane + 32 * h2;
+            const float2 r = rope(__bfloat162float(kn[d]), __bfloat162float(kn[d + kD / 2]), d, kD,
+                                  pos, theta);
+            kcb[int64_t(pos) * cstride + d] = __float2bfloat16_rn(r.x);
+            kcb[int64_t(pos) * cstride + d + kD / 2] = __float2bfloat16_rn(r.y);
+            vcb[int64_t(pos) * cstride + d] = vn[d];
+            vcb[int64_t(pos) * cstride + d + kD / 2] = vn[d + kD / 2];
+        }
+    }
+    __syncthreads();
+    if (warp >= G) return;
+    const int qh = kvh * G + warp;
+    const __nv_bfloat16* qp = qkv + row + int64_t(qh) * kD;
+    // this lane's query elements: d = lane, lane+32 (rotated with lane+64, lane+96)
+    float q[4];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+        const int d = lane + 32 * h2;
+        const float2 r = rope(__bfloat162float(qp[d]), __bfloat162float(qp[d + kD / 2]), d, kD, pos,
+                              theta);
+        q[h2] = r.x;
+        q[h2 + 2] = r.y;
+    }
+    const float scale = rsqrtf(float(kD));
+    float m = -INFINITY, l = 0.0f, acc[4] = {0, 0, 0, 0};
+    for (int t = 0; t <= pos; ++t) {
+        const __nv_bfloat16* kt = kcb + int64_t(t) * cstride;
+        float s = q[0] * __bfloat162float(kt[lane]) + q[1] * __bfloat162float(kt[lane + 32]) +
+                  q[2] * __bfloat162float(kt[lane + 64]) + q[3] * __bfloat162float(kt[lane + 96]);
+        s = warp_sum(s) * scale;
+        const float mn = fmaxf(m, s), corr = __expf(m - mn), pw = __expf(s - mn);
+        l = l * corr + pw;
+        const __nv_bfloat16* vt = vcb + int64_t(t) * cstride;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = acc[j] * corr + pw * __bfloat162float(vt[lane + 32 * j]);
+        m = mn;
+    }
+    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) op[lane + 32 * j] = __float2bfloat16_rn(acc[j] / l);
+}
+
+}  // namespace
+
+cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
+                               int64_t h, float eps, cudaStream_t st) {
+    if (h % 8) return cudaErrorInvalidValue;
+    add_rmsnorm_kernel<<<unsigned(m), 256, 8 * sizeof(float), st>>>(
+        static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta),
+        static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st) {
+    if (f % 8) return cudaErrorInvalidValue;
+    const int64_t n8 = m * f / 8;
+    const unsigned blocks = unsigned(n8 / 256 + 1 < 1184 ? n8 / 256 + 1 : 1184);
+    silu_mul_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(gu),
+                                            static_cast<__nv_bfloat16*>(act), m, int(f));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
+                                    int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                    int64_t lmax, int64_t pos, float theta, cudaStream_t st) {
+    if (head_dim != kD || hkv <= 0 || hq % hkv || hq / hkv > 32 || pos < 0 || pos >= lmax)
+        return cudaErrorInvalidValue;
+    decode_attention_kernel<<<dim3(unsigned(hkv), unsigned(batch)), unsigned(32 * (hq / hkv)), 0,
+                              st>>>(
+        static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(kcache),
+        static_cast<__nv_bfloat16*>(vcache), static_cast<__nv_bfloat16*>(out), int(hq), int(hkv),
+        int(lmax), int(pos), theta);
+    return cudaGetLastError();
+}
+
+}  // namespace rtnq_b200

@@ -64,4 +64,12 @@ const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t
 size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t g);
 cudaError_t launch_wgemm(const WgemmArgs& args, cudaStream_t st);
 
+// decode.cu: the non-GEMM kernels of a decode layer (bf16 activations)
+cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
+                               int64_t h, float eps, cudaStream_t st);
+cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st);
+cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
+                                    int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                    int64_t lmax, int64_t pos, float theta, cudaStream_t st);
+
 }  // namespace rtnq_b200

@@ -1,0 +1,248 @@
+"""Tensor-parallel decode stack over the rtnq kernels.
+
+Megatron-style sharding of a Llama-3.1 decoder layer across ``world`` ranks (one
+process per GPU, ``torch.distributed`` NCCL for the two sum-allreduces per layer):
+
+* column split (no communication) -- ``qkv_proj`` by heads (each rank owns
+  ``heads/world`` query heads and ``kv_heads/world`` KV heads) and ``ffn_up`` (the
+  fused [gate | up] rows of toy.cpp:108-112: each rank keeps the matching slices of
+  both halves);
+* row split -- ``attn_out_proj`` and ``ffn_down`` along K, at quantization-group
+  boundaries, each rank producing a partial [batch x hidden] that is summed by an
+  allreduce.
+
+Quantize-then-shard equals shard-then-quantize for every split here: rows are quantized
+independently (quant.cpp:118-136) and the K split falls on group boundaries, so no
+group straddles two ranks (checked in tests/test_tp.py).
+
+The per-(layer, module) bit width comes from the selective-precision table
+(plan.resolve, plan.cpp:189-224): the same table on every rank picks the W4 or W8
+kernel for each linear.
+
+The sharding functions work on numpy or torch tensors and need no GPU; the layer and
+stack need CUDA (and librtnq_b200.so) -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+MODULES = ("qkv_proj", "attn_out_proj", "ffn_up", "ffn_down")  # ModuleId 1..4 (types.hpp:46-51)
+
+
+@dataclass(frozen=True)
+class LlamaShape:
+    name: str
+    hidden: int
+    heads: int
+    kv_heads: int
+    head_dim: int
+    ffn: int
+    layers: int
+    rope_theta: float = 500000.0
+    eps: float = 1e-5
+
+
+LLAMA_8B = LlamaShape("Llama-3.1-8B", 4096, 32, 8, 128, 14336, 32)
+LLAMA_70B = LlamaShape("Llama-3.1-70B", 8192, 64, 8, 128, 28672, 80)
+LLAMA_405B = LlamaShape("Llama-3.1-405B", 16384, 128, 8, 128, 53248, 126)
+SHAPES = {"8b": LLAMA_8B, "70b": LLAMA_70B, "405b": LLAMA_405B}
+
+
+@dataclass(frozen=True)
+class LocalDims:
+    """One rank's share of a layer."""
+    hq: int       # query heads
+    hkv: int      # kv heads
+    ffn: int      # ffn columns (per half of gate_up)
+    qkv_rows: int
+    attn_cols: int
+
+    def module_shape(self, shape: LlamaShape, module: str):
+        """(N, K) of this rank's weight for `module` (rows = output channels)."""
+        return {"qkv_proj": (self.qkv_rows, shape.hidden),
+                "attn_out_proj": (shape.hidden, self.attn_cols),
+                "ffn_up": (2 * self.ffn, shape.hidden),
+                "ffn_down": (shape.hidden, self.ffn)}[module]
+
+
+def local_dims(shape: LlamaShape, world: int, group: int = 128) -> LocalDims:
+    if shape.heads % world or shape.kv_heads % world or shape.ffn % world:
+        raise ValueError(f"{shape.name}: heads/kv_heads/ffn must divide by TP={world}")
+    hq, hkv, f = shape.heads // world, shape.kv_heads // world, shape.ffn // world
+    for k in (hq * shape.head_dim, f):  # row-split K extents must be whole groups
+        if group < k and k % group:
+            raise ValueError(f"row-split width {k} is not a multiple of the group size {group}")
+    return LocalDims(hq, hkv, f, (hq + 2 * hkv) * shape.head_dim, hq * shape.head_dim)
+
+
+# ---- sharding of full (unsharded) weights ------------------------------------------------
+
+def shard_qkv(w, shape: LlamaShape, rank: int, world: int):
+    """Rows of this rank's heads from the full [ (H + 2 Hkv) D, hidden ] QKV weight."""
+    d, hq, hkv = shape.head_dim, shape.heads // world, shape.kv_heads // world
+    q0 = rank * hq * d
+    k0 = shape.heads * d + rank * hkv * d
+    v0 = (shape.heads + shape.kv_heads) * d + rank * hkv * d
+    parts = [w[q0:q0 + hq * d], w[k0:k0 + hkv * d], w[v0:v0 + hkv * d]]
+    return _cat(parts)
+
+
+def shard_gate_up(w, shape: LlamaShape, rank: int, world: int):
+    """Matching gate and up slices of the fused [gate | up] rows (toy.cpp:108-112)."""
+    f = shape.ffn // world
+    return _cat([w[rank * f:(rank + 1) * f], w[shape.ffn + rank * f:shape.ffn + (rank + 1) * f]])
+
+
+def shard_cols(w, rank: int, world: int):
+    """K-split (row-parallel linear): columns [rank*K/world, (rank+1)*K/world)."""
+    k = w.shape[1] // world
+    return w[:, rank * k:(rank + 1) * k]
+
+
+def shard_module(w, module: str, shape: LlamaShape, rank: int, world: int):
+    if module == "qkv_proj":
+        return shard_qkv(w, shape, rank, world)
+    if module == "ffn_up":
+        return shard_gate_up(w, shape, rank, world)
+    return shard_cols(w, rank, world)
+
+
+def _cat(parts):
+    if isinstance(parts[0], np.ndarray):
+        return np.ascontiguousarray(np.concatenate(parts, axis=0))
+    import torch
+    return torch.cat(parts, dim=0).contiguous()
+
+
+def module_bits(table, layer: int):
+    """Per-module bit widths of one layer from a plan table (plan.resolve)."""
+    return {m: int(table[layer][i]) for i, m in enumerate(MODULES)}
+
+
+def group_for(bits: int, k: int, group: int = 128, w8_per_channel: bool = False) -> int:
+    """W8 per-channel (configs[2]) is one group per row: next power of two >= k, ragged."""
+    if bits == 8 and w8_per_channel:
+        return 1 << (k - 1).bit_length()
+    return group
+
+
+# ---- the layer (CUDA) ------------------------------------------------------------------------
+
+class TPDecodeLayer:
+    """One rank's shard of a decoder layer, all weights quantized on the GPU.
+
+    ``weights`` (optional) maps module -> full bf16 CUDA weight; without it the rank's
+    shards are drawn from a seeded generator (synthetic weights of the same shapes).
+    The forward pass is split at the two allreduce points so a caller can either run
+    NCCL between the halves (``TPDecodeStack``) or simulate TP on one GPU by summing
+    the partials of several rank objects (tests).
+    """
+
+    def __init__(self, shape: LlamaShape, layer: int, world: int, rank: int, bits: dict,
+                 batch: int, max_len: int, pos: int, group: int = 128, weights=None, seed=0,
+                 device="cuda", w8_per_channel=False):
+        import torch
+
+        import paper_2505_15909_b200 as rq
+        self.shape, self.layer, self.world, self.rank = shape, layer, world, rank
+        self.dims = local_dims(shape, world, group)
+        self.batch, self.max_len, self.pos = batch, max_len, pos
+        self.bits = bits
+        dev = torch.device(device)
+        gen = torch.Generator(device=dev).manual_seed(seed * 1000003 + layer * 101 + rank)
+        self.q = {}
+        for m in MODULES:
+            n, k = self.dims.module_shape(shape, m)
+            if weights is not None:
+                w = shard_module(weights[m], m, shape, rank, world)
+            else:
+                w = ((torch.rand(n, k, device=dev, generator=gen) * 2 - 1) * (3.0 / k) ** 0.5
+                     ).to(torch.bfloat16)
+            g = group_for(bits[m], k, group, w8_per_channel)
+            self.q[m] = rq.quantize_pack(w.contiguous(), bits[m], g, ragged=k % g != 0,
+                                         check=False)
+            del w
+        h, d = shape.hidden, shape.head_dim
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        norm_gen = torch.Generator(device=dev).manual_seed(seed * 7919 + layer)
+        self.attn_norm = (1 + 0.1 * torch.rand(h, device=dev, generator=norm_gen)).to(torch.bfloat16)
+        self.ffn_norm = (1 + 0.1 * torch.rand(h, device=dev, generator=norm_gen)).to(torch.bfloat16)
+        # synthetic KV cache: positions [0, pos) filled, the step appends at `pos`
+        kv_gen = torch.Generator(device=dev).manual_seed(seed * 31 + layer * 7 + rank)
+        self.k_cache = (torch.rand(batch, max_len, self.dims.hkv, d, device=dev, generator=kv_gen)
+                        - 0.5).to(torch.bfloat16)
+        self.v_cache = (torch.rand(batch, max_len, self.dims.hkv, d, device=dev, generator=kv_gen)
+                        - 0.5).to(torch.bfloat16)
+        self.y = torch.empty(batch, h, **bf)
+        self.qkv = torch.empty(batch, self.dims.qkv_rows, **bf)
+        self.attn = torch.empty(batch, self.dims.attn_cols, **bf)
+        self.o = torch.empty(batch, h, **bf)
+        self.gu = torch.empty(batch, 2 * self.dims.ffn, **bf)
+        self.act = torch.empty(batch, self.dims.ffn, **bf)
+        self.d = torch.empty(batch, h, **bf)
+
+    @property
+    def weight_bytes(self):
+        return sum(q.weight_bytes for q in self.q.values())
+
+    def attn_half(self, x, delta, ws, stream=None, pdl=False):
+        """x += delta; y = rmsnorm(x); qkv; attention; o = partial attn_out_proj."""
+        import paper_2505_15909_b200 as rq
+        s = self.shape
+        rq.add_rmsnorm(x, self.attn_norm, self.y, delta=delta, eps=s.eps, stream=stream)
+        rq.linear(self.y, self.q["qkv_proj"], out=self.qkv, workspace=ws, stream=stream, pdl=pdl)
+        rq.decode_attention(self.qkv, self.k_cache, self.v_cache, self.attn, self.dims.hq,
+                            self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream)
+        rq.linear(self.attn, self.q["attn_out_proj"], out=self.o, workspace=ws, stream=stream,
+                  pdl=pdl)
+        return self.o
+
+    def mlp_half(self, x, o_sum, ws, stream=None, pdl=False):
+        """x += o_sum; y = rmsnorm(x); gate_up; silu*up; d = partial ffn_down."""
+        import paper_2505_15909_b200 as rq
+        rq.add_rmsnorm(x, self.ffn_norm, self.y, delta=o_sum, eps=self.shape.eps, stream=stream)
+        rq.linear(self.y, self.q["ffn_up"], out=self.gu, workspace=ws, stream=stream, pdl=pdl)
+        rq.silu_mul(self.gu, self.act, stream=stream)
+        rq.linear(self.act, self.q["ffn_down"], out=self.d, workspace=ws, stream=stream, pdl=pdl)
+        return self.d
+
+
+class TPDecodeStack:
+    """All layers of one rank plus the step driver (NCCL allreduce between halves)."""
+
+    def __init__(self, shape: LlamaShape, table, world: int, rank: int, batch: int,
+                 max_len: int = 257, pos: int = 256, group: int = 128, layers=None, seed=0,
+                 device="cuda"):
+        import torch
+
+        import paper_2505_15909_b200 as rq
+        n = shape.layers if layers is None else layers
+        self.world, self.rank, self.shape = world, rank, shape
+        self.layers = [TPDecodeLayer(shape, li, world, rank, module_bits(table, li), batch,
+                                     max_len, pos, group, seed=seed, device=device)
+                       for li in range(n)]
+        self.x = torch.zeros(batch, shape.hidden, dtype=torch.bfloat16, device=device)
+        self.ws = rq.Workspace(device=device)
+
+    @property
+    def weight_bytes(self):
+        return sum(l.weight_bytes for l in self.layers)
+
+    def _allreduce(self, t):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t)
+        return t
+
+    def step(self, x0, stream=None, pdl=True):
+        """One decode step for the batch; returns the residual stream after all layers."""
+        self.x.copy_(x0)
+        delta = None
+        for layer in self.layers:
+            o = self._allreduce(layer.attn_half(self.x, delta, self.ws, stream, pdl))
+            delta = self._allreduce(layer.mlp_half(self.x, o, self.ws, stream, pdl))
+        # fold the last layer's down-projection into the residual stream
+        self.x.add_(delta)
+        return self.x
