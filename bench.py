@@ -1,17 +1,23 @@
 #!/usr/bin/env python
 """bench.py -- W4/W8 weight-only GEMM weight-streaming throughput on B200.
 
-Workload (BASELINE.json configs[1]): the four linears of every Llama-3.1-8B
-decoder layer (32 layers x {qkv 6144x4096, o 4096x4096, gate_up 28672x4096,
-down 4096x14336}), W4A16 g128 (or W8A16 per-channel with --bits 8), bf16
-activations, one decode batch per step.  A step streams all 32 x 112.46 MB of
-packed weights once (3.6 GB >> 126 MB L2, so no L2 flush is needed between
-steps).  value = algorithmic weight bytes (codes + f16 scales) / step time.
+Workload (BASELINE.json configs[1]; --bits 8 for configs[2]): one decode step of
+Llama-3.1-8B -- every quantized linear of its 32 layers (qkv 6144x4096, o 4096x4096,
+gate_up 28672x4096, down 4096x14336), W4A16 g128 (W8A16 per-channel with --bits 8), bf16
+activations, one decode batch.  Under torchrun the same model runs tensor parallel
+(TP=N, Megatron column/row split, the row-parallel outputs sum-allreduced over NCCL), so
+every N streams the same 3.6 GB (W4) of weights per step: "scaling" is strong.
+The weights never fit in L2 (126 MB), so no flush is needed between steps.
+value = algorithmic weight bytes of the whole job (codes + f16 scales) / step time
+(CUDA events, max over ranks).  The full decode step (RMSNorm, attention over a 256-token
+KV cache, SiLU, allreduces) is timed as well and reported as decode_layer_us /
+decode_us_per_token.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--bits 4|8]
+                  [--model 8b|70b|405b] [--plan "explicit:0 modules:4"]
   python bench.py --impl reference     # the reference CPU gemm_fused, same metric
 
-Prints ONE JSON line (rank 0).  See DESIGN.md §6 for every field.
+Prints ONE JSON line (rank 0).  DESIGN.md §5 describes every field.
 """
 from __future__ import annotations
 
@@ -119,6 +125,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import paper_2505_15909_b200 as rq
+    from paper_2505_15909_b200 import tp
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -128,42 +135,70 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     bits, B = args.bits, args.batch
-    g_of = group_for(bits)
+    shape = tp.SHAPES[args.model]
+    nl = args.layers or shape.layers
+    if args.plan:
+        table, plan = rq.plan.resolve(args.plan, nl)
+    else:  # uniform precision (configs[1] / configs[2])
+        import numpy as np
+        table, plan = np.full((nl, 4), bits, np.uint8), f"uniform W{bits}"
+    w8pc = bits == 8 and not args.plan  # configs[2]: W8 per-channel
 
-    # ---- weights: synthetic bf16, quantized + packed on the GPU (our own kernel) ----
-    torch.manual_seed(1234 + rank)
-    layers = []
-    for li in range(LAYERS):
-        mods = []
-        for name, n, k in LLAMA8B:
-            w = ((torch.rand(n, k, device=dev) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
-            mods.append(rq.quantize_pack(w, bits, g_of(k), ragged=k % g_of(k) != 0,
-                                         check=(li == 0)))
-            del w
-        layers.append(mods)
+    # ---- this rank's tensor-parallel shard of every layer, quantized on the GPU ----
+    stack = tp.TPDecodeStack(shape, table, world, rank, B, max_len=args.ctx + 1, pos=args.ctx,
+                             layers=nl, seed=1234, device=dev, w8_per_channel=w8pc)
     torch.cuda.synchronize()
-    step_bytes = sum(weight_bytes(n, k, bits, g_of(k)) for _, n, k in LLAMA8B) * LAYERS
-
-    x = torch.empty(B, 4096, device=dev).uniform_(-1, 1).to(torch.bfloat16)
-    h = torch.empty(B, 14336, device=dev).uniform_(-1, 1).to(torch.bfloat16)
-    outs = {name: torch.empty(B, n, device=dev, dtype=torch.bfloat16) for name, n, _ in LLAMA8B}
+    dims = stack.layers[0].dims
+    step_bytes_rank = stack.weight_bytes
     ws = rq.Workspace(device=dev)
     stream = torch.cuda.Stream(device=dev)
 
-    def step():
-        for mods in layers:
-            for (name, n, k), q in zip(LLAMA8B, mods):
-                rq.linear(x if k == 4096 else h, q, out=outs[name], workspace=ws, stream=stream,
-                          pdl=args.pdl)
+    def bufs(b):
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        return {"x": torch.empty(b, shape.hidden, **bf).uniform_(-1, 1),
+                "attn": torch.empty(b, dims.attn_cols, **bf).uniform_(-1, 1),
+                "act": torch.empty(b, dims.ffn, **bf).uniform_(-1, 1),
+                "qkv": torch.empty(b, dims.qkv_rows, **bf), "o": torch.empty(b, shape.hidden, **bf),
+                "gu": torch.empty(b, 2 * dims.ffn, **bf), "d": torch.empty(b, shape.hidden, **bf)}
 
-    # warm up once eagerly (sizes the workspace), then capture one step in a CUDA graph
-    with torch.cuda.stream(stream):
-        step()
-    stream.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        step()
-    launches_per_step = LAYERS * len(LLAMA8B) * (-(-B // 64))
+    # The weight-streaming step (the metric): every quantized linear of every layer, with
+    # the row-parallel outputs (attn_out_proj, ffn_down) sum-allreduced across ranks.
+    def gemm_step(bb):
+        for layer in stack.layers:
+            q = layer.q
+            rq.linear(bb["x"], q["qkv_proj"], out=bb["qkv"], workspace=ws, stream=stream, pdl=args.pdl)
+            rq.linear(bb["attn"], q["attn_out_proj"], out=bb["o"], workspace=ws, stream=stream,
+                      pdl=args.pdl)
+            if world > 1:
+                dist.all_reduce(bb["o"])
+            rq.linear(bb["x"], q["ffn_up"], out=bb["gu"], workspace=ws, stream=stream, pdl=args.pdl)
+            rq.linear(bb["act"], q["ffn_down"], out=bb["d"], workspace=ws, stream=stream,
+                      pdl=args.pdl)
+            if world > 1:
+                dist.all_reduce(bb["d"])
+
+    def capture(fn):
+        """CUDA graph of one step (NCCL collectives included); None if capture fails."""
+        with torch.cuda.stream(stream):
+            fn()
+        stream.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+            return g
+        except Exception:  # noqa: BLE001 -- fall back to eager launches, reported in config
+            torch.cuda.synchronize()
+            return None
+
+    def runner(g, fn):
+        def run():
+            with torch.cuda.stream(stream):
+                if g is not None:
+                    g.replay()
+                else:
+                    fn()
+        return run
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -181,99 +216,108 @@ def run_gpu(args):
         e1.synchronize()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        if world > 1:
+        if world > 1:  # max over ranks
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = t.item()
         return ms / steps
 
-    def replay(gr):
-        with torch.cuda.stream(stream):  # CUDAGraph.replay() uses the current stream
-            gr.replay()
+    # total weight bytes streamed per step by the whole job (all ranks' shards)
+    step_bytes = step_bytes_rank
+    if world > 1:
+        t = torch.tensor([float(step_bytes_rank)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        step_bytes = int(t.item())
 
+    main = bufs(B)
+    graph = capture(lambda: gemm_step(main))
     with ClockSampler(local) as clk:
-        ms = timed(lambda: replay(graph), args.steps, args.warmup)
-    value = step_bytes * world / (ms * 1e-3) / 1e9
+        ms = timed(runner(graph, lambda: gemm_step(main)), args.steps, args.warmup)
+    value = step_bytes / (ms * 1e-3) / 1e9
     peak, peak_src = peaks()
 
-    # per-batch sweep (same graph structure, re-captured per batch)
     sweep = {}
     for b in args.sweep:
         if b == B:
-            sweep[str(b)] = round(value / world, 1)
+            sweep[str(b)] = round(value, 1)
             continue
-        xb = torch.empty(b, 4096, device=dev).uniform_(-1, 1).to(torch.bfloat16)
-        hb = torch.empty(b, 14336, device=dev).uniform_(-1, 1).to(torch.bfloat16)
-        ob = {name: torch.empty(b, n, device=dev, dtype=torch.bfloat16) for name, n, _ in LLAMA8B}
-
-        def stepb():
-            for mods in layers:
-                for (name, n, k), q in zip(LLAMA8B, mods):
-                    rq.linear(xb if k == 4096 else hb, q, out=ob[name], workspace=ws,
-                              stream=stream, pdl=args.pdl)
-        with torch.cuda.stream(stream):
-            stepb()
-        stream.synchronize()
-        gb = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gb, stream=stream):
-            stepb()
-        msb = timed(lambda: replay(gb), max(3, args.steps // 2), args.warmup)
+        bb = bufs(b)
+        gb = capture(lambda: gemm_step(bb))
+        msb = timed(runner(gb, lambda: gemm_step(bb)), max(3, args.steps // 2), args.warmup)
         sweep[str(b)] = round(step_bytes / (msb * 1e-3) / 1e9, 1)
+        del gb
 
     # ---- e2e: pinned host activations in, host outputs back, through the public API ----
-    hx = torch.empty(B, 4096, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory()
-    hh = torch.empty(B, 14336, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory()
-    hout = {name: torch.empty(B, n, dtype=torch.bfloat16).pin_memory() for name, n, _ in LLAMA8B}
-    h2d = (hx.numel() + hh.numel()) * 2
+    hin = {k: torch.empty_like(main[k], device="cpu").uniform_(-1, 1).pin_memory()
+           for k in ("x", "attn", "act")}
+    hout = {k: torch.empty_like(main[k], device="cpu").pin_memory() for k in ("qkv", "o", "gu", "d")}
+    h2d = sum(t.numel() for t in hin.values()) * 2
     d2h = sum(t.numel() for t in hout.values()) * 2
 
     def e2e_step():
         with torch.cuda.stream(stream):
-            x.copy_(hx, non_blocking=True)
-            h.copy_(hh, non_blocking=True)
-            graph.replay()
-            for name, t in hout.items():
-                t.copy_(outs[name], non_blocking=True)
+            for k, t in hin.items():
+                main[k].copy_(t, non_blocking=True)
+            if graph is not None:
+                graph.replay()
+            else:
+                gemm_step(main)
+            for k, t in hout.items():
+                t.copy_(main[k], non_blocking=True)
 
     ms_e2e = timed(e2e_step, args.steps, args.warmup)
-    e2e = step_bytes * world / (ms_e2e * 1e-3) / 1e9
+    e2e = step_bytes / (ms_e2e * 1e-3) / 1e9
 
-    # dominant kernel = the tensor-core GEMM: every launch in the step is one of them
-    per_launch_bytes = step_bytes / (LAYERS * len(LLAMA8B))
-    achieved = step_bytes / (ms * 1e-3) / 1e9
+    # ---- the full decode step (norms, attention over the KV cache, SiLU, allreduces) ----
+    x0 = torch.empty(B, shape.hidden, dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
+    dgraph = capture(lambda: stack.step(x0, stream=stream, pdl=args.pdl))
+    ms_dec = timed(runner(dgraph, lambda: stack.step(x0, stream=stream, pdl=args.pdl)),
+                   max(3, args.steps // 2), args.warmup)
+
+    linears = nl * 4
+    achieved = step_bytes_rank / (ms * 1e-3) / 1e9  # one GPU's share of the step
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": f"u{bits} weights x bf16 activations, f32 accumulate", "data": "synthetic",
-        "config": {"workload": f"Llama-3.1-8B decoder-layer linears x{LAYERS} layers, W{bits}A16 "
-                               f"{'g128' if bits == 4 else 'per-channel'}, decode batch {B}",
-                   "batch": B, "layers": LAYERS, "bits": bits,
-                   "group": 128 if bits == 4 else "per-channel",
+        "config": {"workload": f"{shape.name} decode step, {nl} layers x 4 quantized linears, "
+                               f"W{bits}A16 {'per-channel' if w8pc else 'g128'}, decode batch {B}, "
+                               f"tensor parallel TP={world}",
+                   "model": shape.name, "batch": B, "layers": nl, "bits": bits,
+                   "plan": plan, "group": "per-channel" if w8pc else 128,
                    "weight_bytes_per_step": step_bytes,
-                   "l2": "inputs larger than L2 (3.6 GB of weights per step), no flush",
-                   "parallelism": f"dp{world} (independent replicas)" if world > 1 else "single GPU",
-                   "pct_of_hbm_peak": round(100 * achieved / peak, 1),
-                   "sweep_gbs_by_batch": sweep},
+                   "l2": "inputs larger than L2 (weights per step >> 126 MB), no flush",
+                   "parallelism": f"tp{world}" if world > 1 else "single GPU",
+                   "cuda_graph": graph is not None,
+                   "pct_of_hbm_peak_per_gpu": round(100 * achieved / peak, 1),
+                   "sweep_gbs_by_batch": sweep,
+                   "decode_step_ms": round(ms_dec, 4),
+                   "decode_layer_us": round(ms_dec * 1e3 / nl, 2),
+                   "decode_us_per_token": round(ms_dec * 1e3 / B, 2),
+                   "decode_ctx_len": args.ctx,
+                   "decode_cuda_graph": dgraph is not None},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(bits, B), "peak_source": peak_src,
+                     "traffic": ncu_traffic(bits, B) if world == 1 and args.model == "8b" else None,
+                     "peak_source": peak_src,
                      "kernel": "rtnq_b200::tc::wgemm_tc_kernel",
-                     "algorithmic_bytes_per_launch": round(per_launch_bytes)},
+                     "algorithmic_bytes_per_launch": round(step_bytes_rank / linears)},
         "e2e": {"value": round(e2e, 1), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": linears * (-(-B // 64)) * args.steps,
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, layers_cpu=layers[0], bits=bits, B=B, g_of=g_of)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "8b":
+        g_of = group_for(bits)
+        line["cpu_baseline"] = cpu_baseline(args, bits=bits, B=B, g_of=g_of)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, layers_cpu, bits, B, g_of, budget_s=None):
+def cpu_baseline(args, bits, B, g_of, budget_s=None):
     """Reference gemm_fused (oracle/_ref) on the host cores, one layer's 4 linears per rep."""
     import numpy as np
     import torch
@@ -376,6 +420,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--bits", type=int, default=4, choices=(4, 8))
+    ap.add_argument("--model", default="8b", choices=("8b", "70b", "405b"))
+    ap.add_argument("--layers", type=int, default=0, help="0: all layers of the model")
+    ap.add_argument("--plan", default="", help="selective-precision plan (plan.hpp grammar)")
+    ap.add_argument("--ctx", type=int, default=256, help="KV-cache length of the decode step")
     ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",")], default=[1, 4, 16])
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

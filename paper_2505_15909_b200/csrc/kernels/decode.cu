@@ -106,9 +106,10 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
 
 // Rotate-half RoPE of one head vector element pair (d, d + D/2) at position pos.
 __device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, float theta) {
-    const float inv = __powf(theta, -2.0f * float(d) / float(D));
+    // accurate sincos: angles reach pos (thousands of radians) at the low frequencies
+    const float inv = powf(theta, -2.0f * float(d) / float(D));
     float s, c;
-    __sincosf(float(pos) * inv, &s, &c);
+    sincosf(float(pos) * inv, &s, &c);
     return make_float2(a * c - b * s, b * c + a * s);
 }
 
@@ -116,22 +117,33 @@ __device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, 
 // positions [0, pos] after the new k/v (rotated k) are appended at `pos`.
 // qkv row layout: [Hq*D | Hkv*D | Hkv*D] (the column-split QKV output of one rank).
 // cache layout: [B][Lmax][Hkv][D] for K and for V.  One CTA = G warps (G = Hq/Hkv <= 32);
-// warp w owns query head kvh * G + w; head_dim D = 128 (4 elements per lane).
+// warp w owns query head kvh * G + w; head_dim D = 128.
+// Flash-decoding over chunks of kChunk positions: the CTA stages the chunk's K and V rows
+// in shared memory (16-byte loads, rows padded to 65 words so a lane-per-row walk is
+// bank-conflict free), each warp scores its positions lane-parallel, then updates its
+// online softmax and the P*V accumulator (lanes own 4 head dims).
 constexpr int kD = 128;
+constexpr int kChunk = 128;
+constexpr int kRowW = kD / 2 + 1;  // 32-bit words per staged row (64 + 1 pad)
+
 __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                         __nv_bfloat16* __restrict__ out, int hq, int hkv, int lmax,
                                         int pos, float theta) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* ks = sm;                       // [kChunk][kRowW] bf16x2
+    uint32_t* vs = ks + kChunk * kRowW;      // [kChunk][kRowW]
+    float* qs = reinterpret_cast<float*>(vs + kChunk * kRowW);  // [G][kD] rotated queries
+    float* ps = qs + (blockDim.x / 32) * kD;                     // [G][kChunk] probabilities
     const int b = blockIdx.y, kvh = blockIdx.x, G = hq / hkv;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
     const int64_t row = int64_t(b) * (hq + 2 * hkv) * kD;
     const __nv_bfloat16* kn = qkv + row + int64_t(hq) * kD + int64_t(kvh) * kD;
     const __nv_bfloat16* vn = kn + int64_t(hkv) * kD;
     const int64_t cstride = int64_t(hkv) * kD;  // between positions
     __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
-    // append the new (rotated) key and the value at `pos` -- warp 0, lanes own d = lane,
-    // lane+32 (first half) and their rotation partners in the second half
+    // append the new (rotated) key and the value at `pos`
     if (warp == 0) {
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -144,37 +156,79 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
             vcb[int64_t(pos) * cstride + d + kD / 2] = vn[d + kD / 2];
         }
     }
-    __syncthreads();
-    if (warp >= G) return;
+    // rotated, pre-scaled query of this warp's head
     const int qh = kvh * G + warp;
     const __nv_bfloat16* qp = qkv + row + int64_t(qh) * kD;
-    // this lane's query elements: d = lane, lane+32 (rotated with lane+64, lane+96)
-    float q[4];
+    const float scale = rsqrtf(float(kD));
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
         const int d = lane + 32 * h2;
         const float2 r = rope(__bfloat162float(qp[d]), __bfloat162float(qp[d + kD / 2]), d, kD, pos,
                               theta);
-        q[h2] = r.x;
-        q[h2 + 2] = r.y;
+        qs[warp * kD + d] = r.x * scale;
+        qs[warp * kD + d + kD / 2] = r.y * scale;
     }
-    const float scale = rsqrtf(float(kD));
+    __threadfence_block();
+    __syncthreads();  // the appended row is visible to the staging loads below
     float m = -INFINITY, l = 0.0f, acc[4] = {0, 0, 0, 0};
-    for (int t = 0; t <= pos; ++t) {
-        const __nv_bfloat16* kt = kcb + int64_t(t) * cstride;
-        float s = q[0] * __bfloat162float(kt[lane]) + q[1] * __bfloat162float(kt[lane + 32]) +
-                  q[2] * __bfloat162float(kt[lane + 64]) + q[3] * __bfloat162float(kt[lane + 96]);
-        s = warp_sum(s) * scale;
-        const float mn = fmaxf(m, s), corr = __expf(m - mn), pw = __expf(s - mn);
-        l = l * corr + pw;
-        const __nv_bfloat16* vt = vcb + int64_t(t) * cstride;
+    const float* qw = qs + warp * kD;
+    float* pw = ps + warp * kChunk;
+    for (int t0 = 0; t0 <= pos; t0 += kChunk) {
+        const int n = min(kChunk, pos + 1 - t0);
+        // stage K and V rows [t0, t0 + n): 16 chunks of 16 B per row
+        for (int i = threadIdx.x; i < n * 16; i += nthr) {
+            const int t = i >> 4, c = i & 15;
+            const uint4 kv = *reinterpret_cast<const uint4*>(kcb + int64_t(t0 + t) * cstride + c * 8);
+            const uint4 vv = *reinterpret_cast<const uint4*>(vcb + int64_t(t0 + t) * cstride + c * 8);
+            uint32_t* kd = ks + t * kRowW + c * 4;
+            uint32_t* vd = vs + t * kRowW + c * 4;
+            kd[0] = kv.x, kd[1] = kv.y, kd[2] = kv.z, kd[3] = kv.w;
+            vd[0] = vv.x, vd[1] = vv.y, vd[2] = vv.z, vd[3] = vv.w;
+        }
+        __syncthreads();
+        // scores: lane owns positions t = lane + 32 j
+        float cmax = -INFINITY;
+        for (int t = lane; t < n; t += 32) {
+            const uint32_t* kr = ks + t * kRowW;
+            float sacc = 0.0f;
+#pragma unroll 8
+            for (int w2 = 0; w2 < kD / 2; ++w2) {
+                const float2 kk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2));
+                sacc = fmaf(qw[2 * w2], kk.x, fmaf(qw[2 * w2 + 1], kk.y, sacc));
+            }
+            pw[t] = sacc;
+            cmax = fmaxf(cmax, sacc);
+        }
+        cmax = warp_max(cmax);
+        const float mn = fmaxf(m, cmax), corr = __expf(m - mn);
+        float csum = 0.0f;
+        for (int t = lane; t < n; t += 32) {
+            const float e = __expf(pw[t] - mn);
+            pw[t] = e;
+            csum += e;
+        }
+        l = l * corr + warp_sum(csum);
+        __syncwarp();
+        // P * V: lane owns head dims 4*lane .. 4*lane+3 (two bf16x2 words)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] = acc[j] * corr + pw * __bfloat162float(vt[lane + 32 * j]);
+        for (int j = 0; j < 4; ++j) acc[j] *= corr;
+        for (int t = 0; t < n; ++t) {
+            const float pt = pw[t];
+            const uint32_t* vr = vs + t * kRowW + 2 * lane;
+            const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+            const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + 1));
+            acc[0] = fmaf(pt, v0.x, acc[0]);
+            acc[1] = fmaf(pt, v0.y, acc[1]);
+            acc[2] = fmaf(pt, v1.x, acc[2]);
+            acc[3] = fmaf(pt, v1.y, acc[3]);
+        }
         m = mn;
+        __syncthreads();  // before the next chunk overwrites K/V
     }
-    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) op[lane + 32 * j] = __float2bfloat16_rn(acc[j] / l);
+    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+    const float inv = 1.0f / l;
+    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
+    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
 }
 
 }  // namespace
@@ -202,8 +256,15 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
                                     int64_t lmax, int64_t pos, float theta, cudaStream_t st) {
     if (head_dim != kD || hkv <= 0 || hq % hkv || hq / hkv > 32 || pos < 0 || pos >= lmax)
         return cudaErrorInvalidValue;
-    decode_attention_kernel<<<dim3(unsigned(hkv), unsigned(batch)), unsigned(32 * (hq / hkv)), 0,
-                              st>>>(
+    const int G = int(hq / hkv);
+    const size_t smem = size_t(2 * kChunk * kRowW) * 4 + size_t(G) * (kD + kChunk) * 4;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(2 * kChunk * kRowW * 4 + 32 * (kD + kChunk) * 4));
+        configured = true;
+    }
+    decode_attention_kernel<<<dim3(unsigned(hkv), unsigned(batch)), unsigned(32 * G), smem, st>>>(
         static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(kcache),
         static_cast<__nv_bfloat16*>(vcache), static_cast<__nv_bfloat16*>(out), int(hq), int(hkv),
         int(lmax), int(pos), theta);

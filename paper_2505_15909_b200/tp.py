@@ -214,14 +214,15 @@ class TPDecodeStack:
 
     def __init__(self, shape: LlamaShape, table, world: int, rank: int, batch: int,
                  max_len: int = 257, pos: int = 256, group: int = 128, layers=None, seed=0,
-                 device="cuda"):
+                 device="cuda", w8_per_channel=False):
         import torch
 
         import paper_2505_15909_b200 as rq
         n = shape.layers if layers is None else layers
         self.world, self.rank, self.shape = world, rank, shape
         self.layers = [TPDecodeLayer(shape, li, world, rank, module_bits(table, li), batch,
-                                     max_len, pos, group, seed=seed, device=device)
+                                     max_len, pos, group, seed=seed, device=device,
+                                     w8_per_channel=w8_per_channel)
                        for li in range(n)]
         self.x = torch.zeros(batch, shape.hidden, dtype=torch.bfloat16, device=device)
         self.ws = rq.Workspace(device=device)
