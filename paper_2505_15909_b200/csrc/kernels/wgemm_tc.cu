@@ -429,13 +429,20 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);
-    uint64_t* full = bars;                  // [STAGES] producer -> dequant, MMA, epilogue
-    uint64_t* empty = full + STAGES;        // [STAGES] dequant + MMA + epilogue -> producer
-    uint64_t* a_full = empty + STAGES;      // [RA] dequant -> MMA
-    uint64_t* a_empty = a_full + GG::RA_MAX;  // [RA] MMA -> dequant
-    uint64_t* d_full = a_empty + GG::RA_MAX;  // [ND] MMA -> epilogue
-    uint64_t* d_empty = d_full + GG::ND_MAX;  // [ND] epilogue -> MMA
-    uint64_t* m_full = d_empty + GG::ND_MAX;  // [MB] dequant -> epilogue (scale mailbox)
+    // Barrier protocol (one tcgen05.commit per unit):
+    //   full[s]    producer (TMA complete_tx) -> dequant, MMA
+    //   a_full[r]  the unit's 4 dequant warps -> MMA (A-ring slot r written)
+    //   done[u]    MMA commit of unit u -> producer (stage reusable), dequant (A slot
+    //              reusable), epilogue (accumulators ready); u & 31, parity (u >> 5) & 1
+    //   d_free[u]  epilogue (4 warps) -> MMA: unit u's accumulators have been read
+    //   m_full[e]  dequant -> epilogue: the unit's group scales are in mailbox entry e
+    // Rings indexed by the unit number modulo 32 are safe because no waiter ever lags the
+    // newest completed phase of its slot by 32 units (stages <= 8, accumulators <= 16 units).
+    uint64_t* full = bars;                    // [STAGES]
+    uint64_t* a_full = full + STAGES;         // [RA]
+    uint64_t* done = a_full + GG::RA_MAX;     // [32]
+    uint64_t* d_free = done + 32;             // [32]
+    uint64_t* m_full = d_free + 32;           // [MB]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_full + GG::MB_MAX);
     __half* mbox = reinterpret_cast<__half*>(smem + GG::MB_OFF);  // [MB][gpu][128 rows]
     volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
@@ -449,24 +456,18 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     const int gpu = 1 << (GG::LOG2BLK - lg);
     const TmemSplit tsp = tmem_split(NT, GG::SLOT_COLS, gpu);
     const int ND = tsp.nd, RA = tsp.ra;
+    const int NU = ND / gpu;  // units whose accumulators can be in flight
     // Mailbox entry e = unit % MB carries the unit's group scales from its dequant warps
     // to the epilogue.  Reusing it for unit i needs the epilogue done with unit i - MB:
-    // dequant(i) follows a_empty(i - RA) <- MMA(i - RA) <- d_empty of unit i - RA - ND/gpu.
-    const int MB = RA + ND / gpu;
-    const int lnd = __ffs(ND) - 1;  // ND is a power of two
+    // dequant(i) follows done(i - RA) <- MMA(i - RA) <- d_free(i - RA - NU).
+    const int MB = RA + NU;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);                          // producer's arrive.expect_tx
-            mbar_init(&empty[s], 4 + 1);                     // dequant parity + MMA
-        }
-        for (int i = 0; i < RA; ++i) {
-            mbar_init(&a_full[i], 4);
-            mbar_init(&a_empty[i], 1);
-        }
-        for (int i = 0; i < ND; ++i) {
-            mbar_init(&d_full[i], 1);
-            mbar_init(&d_empty[i], kEpiWarps);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);  // producer's arrive.expect_tx
+        for (int i = 0; i < RA; ++i) mbar_init(&a_full[i], 4);
+        for (int i = 0; i < 32; ++i) {
+            mbar_init(&done[i], 1);
+            mbar_init(&d_free[i], kEpiWarps);
         }
         for (int i = 0; i < MB; ++i) mbar_init(&m_full[i], 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -494,7 +495,38 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         }
     };
 
-    if (warp == kProducerWarp) {
+    if (p.debug & 1024) {
+        // profiling: the MMA issue stream alone (no other role, no barrier waits)
+        if (warp == kMmaWarp) {
+            constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
+            constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                                       (uint32_t(NT >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
+            constexpr uint64_t bdesc_hi = (uint64_t((NT * 16) >> 4) << 16) |
+                                          (uint64_t(128 >> 4) << 32) | (1ull << 46);
+            constexpr uint32_t kStep = (2 * NT * 16) >> 4;
+            const uint32_t act0 = smem_u32(smem + GG::ACT_OFF);
+            const long long t0 = clock64();
+            const int units = (u1 - u0 + KPU - 1) / KPU;
+            for (int i = 0; i < units; ++i) {
+                const int s = (p.debug & 4096) ? 0 : i % STAGES;
+                const int slot = (p.debug & 8192) ? 0 : i % RA;
+                const uint64_t bdesc0 = bdesc_hi | uint64_t(((act0 + s * GG::STAGE_BYTES) >> 4) & 0x3FFFu);
+                for (int j = 0; j < gpu; ++j)
+                    issue_steps<kStep>(tmem + tsp.d_col0 + (((p.debug & 16384) ? 0 : (i * gpu + j)) & (ND - 1)) * NT,
+                                       tmem + slot * GG::SLOT_COLS + j * (GG::STEPS / gpu) * 8,
+                                       bdesc0 + uint64_t(j * (GG::STEPS / gpu) * kStep), idesc,
+                                       GG::STEPS / gpu);
+                if (!(p.debug & 2048)) {
+                    tc_commit_elect(&done[i & 31]);
+                    if (i >= 4) mbar_wait(&done[(i - 4) & 31], uint32_t((i - 4) >> 5) & 1u);
+                }
+            }
+            tc_commit_elect(&done[31]);
+            mbar_wait(&done[31], (p.debug & 2048) ? 0u : uint32_t(units > 31 ? 1 : 0));
+            const long long t1 = clock64();
+            if (lane == 0 && (p.debug & 32)) g_wgemm_dbg[blockIdx.x * 64 + 60] = (t1 - t0) / (units ? units : 1);
+        }
+    } else if (warp == kProducerWarp) {
         // ===================== producer =====================
         // Codes and the unit's group scales: bulk copies of contiguous runs.  Activations:
         // one TMA box of BLK/8 k-chunks x NT tokens.  All complete on full[s].
@@ -543,6 +575,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         }
         Ring st(STAGES);  // stage ring position of unit `pro` onward
         for (int i = 0; i < pro; ++i) st.next();
+        int iu = pro;     // unit number
         // L2 prefetch runs kPrefetch units ahead of the stage ring, so DRAM latency is
         // covered by L2 rather than by shared-memory stages
         constexpr int kPrefetch = 8;
@@ -563,16 +596,21 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                 prefetch_unit(pf);
                 pf.advance(pf.chunk());
             }
-            PWAIT(&empty[s], st.ph ^ 1u, 0);  // the previous use of this stage is released
+            {  // the previous use of this stage (unit iu - STAGES) is done
+                const int v = iu - STAGES;
+                PWAIT(&done[v & 31], uint32_t(v >> 5) & 1u, 0);
+            }
             weights(w, n, s);
             acts(w, s);
             w.advance(n);
             st.next();
+            ++iu;
         }
         if (lane == 0) stamp(p, 2), prof_store(8);
     } else if (warp >= kMmaWarp) {
         // ===================== MMA issuers (warp-uniform, one lane issues) =====================
         const int par = warp - kMmaWarp;
+        const int mmask = (p.debug & 512) ? 0 : 1;  // profiling: one MMA warp issues all units
         constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
         constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                    (uint32_t(NT >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
@@ -588,7 +626,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         int ob0 = 0;  // first accumulator ordinal of the unit (gpu per unit)
         for (int i = 0; w.more(); ++i, st.next(), sl.next(), ob0 += gpu) {
             const int n = w.chunk();
-            if ((i & 1) == par) {
+            if ((i & mmask) == par) {
                 const int s = st.idx, slot = sl.idx;
                 const int kbase = w.kb * kKB, kend = kbase + n * kKB, blk = kbase & ~(GG::BLK - 1);
                 PWAIT(&full[s], st.ph, 0);
@@ -597,21 +635,23 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                 const uint64_t bdesc0 =
                     bdesc_hi | uint64_t(((act0 + s * GG::STAGE_BYTES) >> 4) & 0x3FFFu);
                 const uint32_t a_base = tmem + slot * GG::SLOT_COLS;
+                if (i >= NU) {  // accumulator reuse: the epilogue has read unit i - NU
+                    const int v = i - NU;
+                    PWAIT(&d_free[v & 31], uint32_t(v >> 5) & 1u, 2);
+                    tc_fence_after();
+                }
+                PT_BEGIN(tiss);
                 for (int j = 0; j < gpu; ++j) {
-                    const int ob = ob0 + j, buf = ob & (ND - 1);
-                    if (ob >= ND) {  // accumulator reuse: wait for the epilogue to drain it
-                        PWAIT(&d_empty[buf], uint32_t((ob >> lnd) - 1) & 1u, 2);
-                        tc_fence_after();
-                    }
+                    const int buf = (ob0 + j) & (ND - 1);
                     int k0, cnt;
                     subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
                     if (cnt > 0 && !(p.debug & 4))
                         issue_steps<kStep>(d_base + buf * NT, a_base + k0 * 8,
                                            bdesc0 + uint64_t(k0 * kStep), idesc, cnt);
-                    tc_commit_elect(&d_full[buf]);
                 }
-                tc_commit_elect(&a_empty[slot]);
-                tc_commit_elect(&empty[s]);  // activations of this stage consumed
+                // one commit: stage, A slot and accumulators of unit i all complete together
+                tc_commit_elect(&done[i & 31]);
+                PT_END(tiss, 3);
             }
             w.advance(n);
         }
@@ -632,6 +672,9 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                 const uint8_t* st = smem + s * GG::STAGE_BYTES + row * 16;
                 const uint32_t ta = tmem + lane_base + slot * GG::SLOT_COLS;
 #pragma unroll
+                if (p.debug & 256) {  // profiling: barrier protocol only
+                    if (i >= RA) PWAIT(&done[(i - RA) & 31], uint32_t((i - RA) >> 5) & 1u, 1);
+                } else
                 for (int h = 0; h < KPU / 2; ++h) {  // two k-blocks (64 columns) at a time
                     if (2 * h < n) {
                         PT_BEGIN(tq);
@@ -659,7 +702,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                         PT_END(tq, 2);
                         if (h == 0) {
                             if (i >= RA) {  // slot free? (its MMA overlapped this dequant)
-                                PWAIT(&a_empty[slot], sl.ph ^ 1u, 1);
+                                PWAIT(&done[(i - RA) & 31], uint32_t((i - RA) >> 5) & 1u, 1);
                                 tc_fence_after();
                             }
                             // this row's group scales -> the epilogue's mailbox entry
@@ -693,7 +736,6 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&a_full[slot]);
-                    mbar_arrive(&empty[s]);  // codes and scales of this unit consumed
                     mbar_arrive(&m_full[me.idx]);
                 }
             }
@@ -767,27 +809,21 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         int seg_kb0 = w.kb;
         Ring me(MB);
         int ob0 = 0;
-        for (; w.more(); me.next(), ob0 += gpu) {
+        for (int i = 0; w.more(); ++i, me.next(), ob0 += gpu) {
             const int n = w.chunk();
             const bool seg_end = w.seg_end(n);
-            const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
-            const int rows8 = (rows + 7) / 8 * 8;
             const int kbase = w.kb * kKB, kend = kbase + n * kKB, blk = kbase & ~(GG::BLK - 1);
-            // this unit's scales, handed over by its dequant warps
+            // this unit's scales, handed over by its dequant warps, then its accumulators
             PWAIT(&m_full[me.idx], me.ph, 1);
             const __half* mb = mbox + me.idx * gpu * kRows + row;
+            PWAIT(&done[i & 31], uint32_t(i >> 5) & 1u, 0);
+            tc_fence_after();
             for (int j = 0; j < gpu; ++j) {
-                const int ob = ob0 + j, buf = ob & (ND - 1);
                 int k0, cnt;
                 subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
+                if (cnt == 0) continue;
+                const int buf = (ob0 + j) & (ND - 1);
                 const float sc = __half2float(mb[j * kRows]);
-                PWAIT(&d_full[buf], uint32_t(ob >> lnd) & 1u, 0);
-                tc_fence_after();
-                if (cnt == 0) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&d_empty[buf]);
-                    continue;
-                }
 #pragma unroll
                 for (int jj = 0; jj < NT; jj += 32) {
                     uint32_t v[32];
@@ -800,17 +836,15 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
 #pragma unroll
                         for (int e = 0; e < 32; ++e) v[e] = 0;
                     }
-                    if (jj + 32 >= NT) {  // last read of this accumulator: hand it back
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&d_empty[buf]);
-                    }
                     constexpr int W = NT < 32 ? NT : 32;
 #pragma unroll
                     for (int e = 0; e < W; ++e)
                         acc[jj + e] = fmaf(sc, __uint_as_float(v[e]), acc[jj + e]);
                 }
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_free[i & 31]);  // accumulators of unit i read
             if (seg_end) {
                 if (et == 0) stamp(p, 5);
                 epilogue(w.b, seg_kb0 == 0 && w.kb + n == p.KBLK);

@@ -21,14 +21,14 @@ __global__ void micro(long long* out, int iters, int fill) {
   __shared__ uint64_t bar[4];
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 32 * 1024; i += blockDim.x) act[i] = (fill ? uint8_t((i * 2654435761u) >> 24) & 0x3F : 0);
+  for (int i = threadIdx.x; i < 32 * 1024; i += blockDim.x) act[i] = (fill == 2 ? uint8_t((i * 2654435761u) >> 24) : fill ? uint8_t((i * 2654435761u) >> 24) & 0x3F : 0);
   if (threadIdx.x == 0) { for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
   if (warp == 0) { asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tslot))); asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;"); }
   asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads(); asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tslot;
   if (fill && warp < 4) {
     uint32_t v[32];
-    for (int i = 0; i < 32; ++i) v[i] = 0x3F803F80u ^ ((threadIdx.x * 131 + i * 7) & 0x007F007F);
+    for (int i = 0; i < 32; ++i) v[i] = fill == 2 ? (0x7FC07F81u ^ (threadIdx.x * 2654435761u + i * 40503u)) : 0x3F803F80u ^ ((threadIdx.x * 131 + i * 7) & 0x007F007F);
     for (int c = 0; c < 256; c += 32)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tmem + (uint32_t(warp * 32) << 16) + c),
         "r"(v[0]),"r"(v[1]),"r"(v[2]),"r"(v[3]),"r"(v[4]),"r"(v[5]),"r"(v[6]),"r"(v[7]),"r"(v[8]),"r"(v[9]),"r"(v[10]),"r"(v[11]),"r"(v[12]),"r"(v[13]),"r"(v[14]),"r"(v[15]),
@@ -112,16 +112,17 @@ int main() {
   long long* d; cudaMalloc(&d, 16 * 8);
   const char* names[] = {"commit+wait (idle)", "mma issue (A tmem)", "8 mma+commit+wait", "mma thrpt (A tmem)", "mma thrpt (A smem)",
                          "arrive+wait", "STTM x32 + wait::st", "LDTM x16 + wait::ld", "fence::after", "1 mma+commit+wait", "mma thrpt rotating"};
-  for (int fill : {0, 1})
-  for (int nt : {16, 64}) {
+  for (int grid : {1, 148})
+  for (int fill : {1, 2})
+  for (int nt : {16}) {
     long long h[16];
     for (int rep = 0; rep < 2; ++rep) {
-      if (nt == 16) micro<16><<<1, 128>>>(d, 200, fill); else micro<64><<<1, 128>>>(d, 200, fill);
+      if (nt == 16) micro<16><<<grid, 128>>>(d, 200, fill); else micro<64><<<grid, 128>>>(d, 200, fill);
       cudaError_t e = cudaDeviceSynchronize(); if (e) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("NT=%d fill=%d\n", nt, fill);
-    for (int i = 0; i < 11; ++i) printf("  %-24s %lld cycles\n", names[i], h[i]);
+    printf("NT=%d fill=%d grid=%d\n", nt, fill, grid);
+    for (int i : {3, 10}) printf("  %-24s %lld cycles\n", names[i], h[i]);
   }
   return 0;
 }

@@ -15,6 +15,44 @@ __device__ __forceinline__ void mma(uint32_t d, uint32_t a, uint64_t bd, uint32_
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc) {
   asm volatile("{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(ad), "l"(bd), "r"(id), "r"(acc) : "memory"); }
 
+template <int STEPS, uint32_t BSTEP>
+__device__ __forceinline__ void umma_unit_elect(uint32_t d_addr, uint32_t a_addr, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+    static_assert(STEPS == 4 || STEPS == 8, "");
+    if constexpr (STEPS == 4)
+        asm volatile(
+            "{\n.reg .pred e, p, t;\n.reg .b32 a1, a2, a3;\n.reg .b64 b1, b2, b3;\n"
+            "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
+            "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\n"
+            "add.u64 b1, %2, %5;\nadd.u64 b2, b1, %5;\nadd.u64 b3, b2, %5;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n}\n" ::"r"(d_addr),
+            "r"(a_addr), "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(BSTEP)
+            : "memory");
+    else
+        asm volatile(
+            "{\n.reg .pred e, p, t;\n.reg .b32 a1, a2, a3, a4, a5, a6, a7;\n"
+            ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
+            "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
+            "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\nadd.u32 a4, %1, 32;\n"
+            "add.u32 a5, %1, 40;\nadd.u32 a6, %1, 48;\nadd.u32 a7, %1, 56;\n"
+            "add.u64 b1, %2, %5;\nadd.u64 b2, b1, %5;\nadd.u64 b3, b2, %5;\nadd.u64 b4, b3, %5;\n"
+            "add.u64 b5, b4, %5;\nadd.u64 b6, b5, %5;\nadd.u64 b7, b6, %5;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, t;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, t;\n}\n" ::"r"(d_addr),
+            "r"(a_addr), "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(BSTEP)
+            : "memory");
+}
+
+
 template <int NT>
 __global__ void micro(long long* out, int iters, int fill) {
   __shared__ __align__(1024) uint8_t act[32 * 1024];
@@ -42,6 +80,14 @@ __global__ void micro(long long* out, int iters, int fill) {
     const uint64_t adesc = uint64_t((su32(act) >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) | (1ull << 46);
     uint32_t ph = 0, ph1 = 0;
     long long t0, t1;
+    // (13) passes of the kernel's pattern (48 unit-asms = 384 MMAs, commit+wait per pass)
+    for (int pass = 0; pass < 10; ++pass) {
+      t0 = clock64();
+      for (int u = 0; u < 48; ++u)
+        umma_unit_elect<8, uint32_t((2 * NT * 16) / 16)>(tmem + 384 + (u & 1) * NT, tmem + (u & 3) * 64, bdesc + (u & 7) * 8 * 2 * NT, idesc, (pass & 1) ? 0u : 1u);
+      commit(&bar[2]); mbar_wait(&bar[2], pass & 1);
+      t1 = clock64(); if (lane == 0) out[16 + pass] = (t1 - t0) / (48 * 8);
+    }
     // (1) commit + wait round trip with nothing in flight
     t0 = clock64();
     for (int i = 0; i < iters; ++i) { commit(&bar[0]); mbar_wait(&bar[0], ph); ph ^= 1; }
@@ -99,6 +145,14 @@ __global__ void micro(long long* out, int iters, int fill) {
     for (int i = 0; i < iters; ++i) { for (int k = 0; k < 64; ++k) mma(tmem + 256 + ((k >> 3) & 1) * NT, tmem + (k & 31) * 8, bdesc + ((k * 2 * NT) & 1023), idesc, (k & 7) != 0); }
     commit(&bar[0]); mbar_wait(&bar[0], ph); ph ^= 1;
     t1 = clock64(); if (lane == 0) out[10] = (t1 - t0) / (iters * 64);
+    // (12) the kernel's 8-MMA asm block, A/B/D rotating like the kernel (D at 384)
+    t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      for (int u = 0; u < 8; ++u)
+        umma_unit_elect<8, uint32_t((2 * NT * 16) / 16)>(tmem + 384 + (u & 1) * NT, tmem + (u & 3) * 64, bdesc + u * 8 * 2 * NT, idesc, 0);
+    }
+    commit(&bar[0]); mbar_wait(&bar[0], ph); ph ^= 1;
+    t1 = clock64(); if (lane == 0) out[11] = (t1 - t0) / (iters * 64);
     // (10) one UMMA latency: mma + commit + wait
     t0 = clock64();
     for (int i = 0; i < iters; ++i) { mma(tmem + 256, tmem, bdesc, idesc, 1); commit(&bar[0]); mbar_wait(&bar[0], ph); ph ^= 1; }
@@ -109,19 +163,24 @@ __global__ void micro(long long* out, int iters, int fill) {
 }
 
 int main() {
-  long long* d; cudaMalloc(&d, 16 * 8);
+  long long* d; cudaMalloc(&d, 32 * 8);
   const char* names[] = {"commit+wait (idle)", "mma issue (A tmem)", "8 mma+commit+wait", "mma thrpt (A tmem)", "mma thrpt (A smem)",
-                         "arrive+wait", "STTM x32 + wait::st", "LDTM x16 + wait::ld", "fence::after", "1 mma+commit+wait", "mma thrpt rotating"};
-  for (int fill : {0, 1})
-  for (int nt : {16, 64}) {
-    long long h[16];
+                         "arrive+wait", "STTM x32 + wait::st", "LDTM x16 + wait::ld", "fence::after", "1 mma+commit+wait", "mma thrpt rotating", "kernel unit asm (per MMA)", "COLD 384 MMAs (per MMA)", "then warm (per MMA)"};
+  cudaFuncSetAttribute(micro<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
+  for (int cfg = 0; cfg < 1; ++cfg)
+  for (int fill : {1})
+  for (int nt : {16}) {
+    const int threads = (cfg & 1) ? 480 : 128;
+    const int dyn = (cfg & 2) ? 180 * 1024 : 0;
+    long long h[32];
     for (int rep = 0; rep < 2; ++rep) {
-      if (nt == 16) micro<16><<<1, 128>>>(d, 200, fill); else micro<64><<<1, 128>>>(d, 200, fill);
+      if (nt == 16) micro<16><<<1, threads, dyn>>>(d, 200, fill); else micro<64><<<1, threads, dyn>>>(d, 200, fill);
       cudaError_t e = cudaDeviceSynchronize(); if (e) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("NT=%d fill=%d\n", nt, fill);
-    for (int i = 0; i < 11; ++i) printf("  %-24s %lld cycles\n", names[i], h[i]);
+    printf("NT=%d fill=%d threads=%d dyn=%d\n", nt, fill, threads, dyn);
+    for (int i = 0; i < 12; ++i) printf("  %-24s %lld cycles\n", names[i], h[i]);
+    for (int i = 16; i < 26; ++i) printf("  pass %d: %lld cycles/MMA\n", i - 16, h[i]);
   }
   return 0;
 }

@@ -9,8 +9,8 @@ a = torch.randn(8192, 8192, device="cuda")
 for _ in range(30): a @ a
 names = ["start", "tmem", "prod_end", "mma_end", "deq_end", "epi_seg_end", "combine_end"]
 waits = {8: "prod wait empty", 12: "prod total", 20: "mma wait full", 21: "mma wait a_full",
-         22: "mma wait d_empty", 24: "mma total", 32: "deq0 wait full", 33: "deq0 wait a_empty", 34: "deq0 lds+alu", 35: "deq0 sttm+wait",
-         36: "deq0 total", 44: "epi0 wait d_full", 45: "epi0 wait full", 48: "epi0 total(last seg)"}
+         22: "mma wait d_empty", 23: "mma issue+commit", 24: "mma total", 32: "deq0 wait full", 33: "deq0 wait a_empty", 34: "deq0 lds+alu", 35: "deq0 sttm+wait",
+         36: "deq0 total", 60: "isolated MMA cycles/unit", 44: "epi0 wait d_full", 45: "epi0 wait full", 48: "epi0 total(last seg)"}
 buf = np.zeros(1024 * 64, np.uint64)
 for name, n, k in [x for x in [("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)] if x[0] in os.environ.get("ONLY", "o,gate_up,down")]:
     w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
