@@ -45,8 +45,9 @@ constexpr int kDequantWarps = 8;    // warps 0-7: quadrant w & 3, unit parity w 
 constexpr int kEpiWarps = 4;        // warps 8-11: quadrant w & 3
 constexpr int kEpiWarp0 = 8;
 constexpr int kProducerWarp = 12;
-constexpr int kMmaWarp = 13;        // warps 13-14: MMA issuers, unit parity w - 13
-constexpr int kThreads = 15 * 32;
+constexpr int kMmaWarp = 13;        // warps 13..13+kMmaWarps-1: MMA issuers, unit i % kMmaWarps
+constexpr int kMmaWarps = 2;  // <= 16 warps in all: 4 per SM sub-partition (its 16K-register file)
+constexpr int kThreads = (13 + kMmaWarps) * 32;
 constexpr int kTmemCols = 512;      // one CTA per SM owns all of TMEM
 constexpr int kACols = 256;         // A ring; accumulators use the other 256 columns
 
@@ -67,6 +68,7 @@ struct Params {
     int G;      // CTAs
     int out_dtype;
     int log2g;  // log2(group); 30 when one group spans the row
+    int csize;  // > 1: cluster split-K (csize CTAs per row-block, DSMEM reduction); 1: stream-K
     int debug;  // RTNQ_WGEMM_DEBUG bits (profiling only): 2 no copies, 4 no MMA, 8 no tcgen05.st,
                 //   16 no tcgen05.ld, 32 per-role timing (rtnq_wgemm_debug_read)
 };
@@ -420,6 +422,32 @@ __device__ __forceinline__ void issue_steps(uint32_t d, uint32_t a, uint64_t bd,
         umma_f16_elect(d, a + done * 8, bd + uint64_t(done * KSTEP), idesc, done);
 }
 
+// A full, block-aligned unit: STEPS k16 MMAs, accumulator slot k / GS (GS steps per
+// quantization group), every offset a compile-time constant added to three per-unit bases.
+// One single-MMA asm per step keeps the issue stream short (measured: ~26 cycles/MMA,
+// against ~70 for one asm block with runtime-derived operands).
+template <int STEPS, int GS, int NT, uint32_t KSTEP>
+__device__ __forceinline__ void issue_unit(uint32_t d0, uint32_t a0, uint64_t b0, uint32_t idesc) {
+#pragma unroll
+    for (int k = 0; k < STEPS; ++k)
+        umma_f16_elect(d0 + uint32_t((k / GS) * NT), a0 + uint32_t(k * 8),
+                       b0 + uint64_t(k * KSTEP), idesc, (k % GS) != 0 ? 1u : 0u);
+}
+
+template <int STEPS, int NT, uint32_t KSTEP>
+__device__ __forceinline__ void issue_unit_lg(int lg, uint32_t d0, uint32_t a0, uint64_t b0,
+                                              uint32_t idesc) {
+    const int gs = (1 << lg) >> 4;  // k16 steps per group piece (<= STEPS)
+    switch (gs) {
+        case 16: if constexpr (STEPS >= 16) { issue_unit<STEPS, 16, NT, KSTEP>(d0, a0, b0, idesc); break; }
+                 [[fallthrough]];
+        case 8: issue_unit<STEPS, 8, NT, KSTEP>(d0, a0, b0, idesc); break;
+        case 4: issue_unit<STEPS, 4, NT, KSTEP>(d0, a0, b0, idesc); break;
+        case 2: issue_unit<STEPS, 2, NT, KSTEP>(d0, a0, b0, idesc); break;
+        default: issue_unit<STEPS, 1, NT, KSTEP>(d0, a0, b0, idesc); break;
+    }
+}
+
 // PROF=true (RTNQ_WGEMM_DEBUG & 32) accumulates per-role wait cycles in registers.
 template <int BITS, int AT, int NT, bool PROF>
 __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params p) {
@@ -450,7 +478,17 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     if (threadIdx.x == 0) stamp(p, 0);
-    const int u0 = int(int64_t(c) * p.U / p.G), u1 = int(int64_t(c + 1) * p.U / p.G);
+    // stream-K: an even share of all (row-block, k-block) pairs; cluster split-K: row-block
+    // c / csize, k-blocks [r, r + 1) * KBLK / csize of it for cluster rank r = c % csize
+    int u0, u1;
+    if (p.csize > 1) {
+        const int b = c / p.csize, r = c % p.csize;
+        u0 = b * p.KBLK + r * p.KBLK / p.csize;
+        u1 = b * p.KBLK + (r + 1) * p.KBLK / p.csize;
+    } else {
+        u0 = int(int64_t(c) * p.U / p.G);
+        u1 = int(int64_t(c + 1) * p.U / p.G);
+    }
     // accumulator slots per unit: one per group-sized piece of the aligned block
     const int lg = p.log2g < GG::LOG2BLK ? p.log2g : GG::LOG2BLK;
     const int gpu = 1 << (GG::LOG2BLK - lg);
@@ -507,6 +545,14 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
             const uint32_t act0 = smem_u32(smem + GG::ACT_OFF);
             const long long t0 = clock64();
             const int units = (u1 - u0 + KPU - 1) / KPU;
+            if (p.debug & 65536) {
+                // the microbenchmark's loop verbatim (scratch/tc_micro.cu "rotating")
+                const uint64_t bdesc = bdesc_hi | uint64_t((act0 >> 4) & 0x3FFFu);
+                for (int i = 0; i < units; ++i)
+                    for (int k = 0; k < 16; ++k)
+                        umma_f16_elect(tmem + 256 + ((k >> 3) & 1) * NT, tmem + (k & 31) * 8,
+                                       bdesc + ((k * 2 * NT) & 1023), idesc, (k & 7) != 0);
+            } else
             for (int i = 0; i < units; ++i) {
                 const int s = (p.debug & 4096) ? 0 : i % STAGES;
                 const int slot = (p.debug & 8192) ? 0 : i % RA;
@@ -610,7 +656,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     } else if (warp >= kMmaWarp) {
         // ===================== MMA issuers (warp-uniform, one lane issues) =====================
         const int par = warp - kMmaWarp;
-        const int mmask = (p.debug & 512) ? 0 : 1;  // profiling: one MMA warp issues all units
+        const int nmma = (p.debug & 512) ? 1 : kMmaWarps;  // profiling: one warp issues all
         constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
         constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                    (uint32_t(NT >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
@@ -624,9 +670,10 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         Walker<KPU> w(u0, u1, p.KBLK);
         Ring st(STAGES), sl(RA);
         int ob0 = 0;  // first accumulator ordinal of the unit (gpu per unit)
-        for (int i = 0; w.more(); ++i, st.next(), sl.next(), ob0 += gpu) {
+        int mi = 0;  // i % nmma, kept incrementally
+        for (int i = 0; w.more(); ++i, st.next(), sl.next(), ob0 += gpu, mi = mi + 1 == nmma ? 0 : mi + 1) {
             const int n = w.chunk();
-            if ((i & mmask) == par) {
+            if (mi == par) {
                 const int s = st.idx, slot = sl.idx;
                 const int kbase = w.kb * kKB, kend = kbase + n * kKB, blk = kbase & ~(GG::BLK - 1);
                 PWAIT(&full[s], st.ph, 0);
@@ -641,13 +688,22 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                     tc_fence_after();
                 }
                 PT_BEGIN(tiss);
-                for (int j = 0; j < gpu; ++j) {
-                    const int buf = (ob0 + j) & (ND - 1);
-                    int k0, cnt;
-                    subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
-                    if (cnt > 0 && !(p.debug & 4))
-                        issue_steps<kStep>(d_base + buf * NT, a_base + k0 * 8,
-                                           bdesc0 + uint64_t(k0 * kStep), idesc, cnt);
+                if (p.debug & 4) {
+                } else if (n == KPU && kbase == blk) {  // full aligned unit: unrolled issue
+                    const uint32_t a_use = (p.debug & 131072) ? tmem : a_base;  // profiling knobs
+                    const uint64_t b_use =
+                        (p.debug & 262144) ? (bdesc_hi | uint64_t((act0 >> 4) & 0x3FFFu)) : bdesc0;
+                    issue_unit_lg<GG::STEPS, NT, kStep>(lg, d_base + (ob0 & (ND - 1)) * NT, a_use,
+                                                        b_use, idesc);
+                } else {
+                    for (int j = 0; j < gpu; ++j) {
+                        const int buf = (ob0 + j) & (ND - 1);
+                        int k0, cnt;
+                        subgroup(kbase, kend, blk, lg, j, &k0, &cnt);
+                        if (cnt > 0)
+                            issue_steps<kStep>(d_base + buf * NT, a_base + k0 * 8,
+                                               bdesc0 + uint64_t(k0 * kStep), idesc, cnt);
+                    }
                 }
                 // one commit: stage, A slot and accumulators of unit i all complete together
                 tc_commit_elect(&done[i & 31]);
@@ -789,17 +845,31 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
 #pragma unroll
             for (int j = 0; j < NT; ++j) sum[j] = 0.0f;
             const int first_bit = int(int64_t(c_first) * p.U / p.G) / p.KBLK == b ? 0 : 1;
-            for (int cc = c_first; cc <= c_last; ++cc) {  // fixed order: deterministic
-                const int cs = 2 * cc + (cc == c_first ? first_bit : 0);
-                const float4* src =
-                    reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * kRows + row) * NT);
+            // partials in batches of PB: all loads of a batch are in flight together (one L2
+            // round trip per batch), then summed in CTA order -- deterministic
+            constexpr int PB = NT <= 16 ? 4 : NT <= 32 ? 2 : 1;
+            for (int c0 = c_first; c0 <= c_last; c0 += PB) {
+                float4 x[PB][NT / 4];
 #pragma unroll
-                for (int j = 0; j < NT / 4; ++j) {
-                    const float4 x = __ldcg(src + j);
-                    sum[4 * j] += x.x;
-                    sum[4 * j + 1] += x.y;
-                    sum[4 * j + 2] += x.z;
-                    sum[4 * j + 3] += x.w;
+                for (int q = 0; q < PB; ++q) {
+                    const int cc = c0 + q;
+                    if (cc > c_last) break;
+                    const int cs = 2 * cc + (cc == c_first ? first_bit : 0);
+                    const float4* src =
+                        reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * kRows + row) * NT);
+#pragma unroll
+                    for (int j = 0; j < NT / 4; ++j) x[q][j] = __ldcg(src + j);
+                }
+#pragma unroll
+                for (int q = 0; q < PB; ++q) {
+                    if (c0 + q > c_last) break;
+#pragma unroll
+                    for (int j = 0; j < NT / 4; ++j) {
+                        sum[4 * j] += x[q][j].x;
+                        sum[4 * j + 1] += x[q][j].y;
+                        sum[4 * j + 2] += x[q][j].z;
+                        sum[4 * j + 3] += x[q][j].w;
+                    }
                 }
             }
             write(sum);
@@ -845,7 +915,14 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_free[i & 31]);  // accumulators of unit i read
-            if (seg_end) {
+            if (seg_end && p.csize > 1) {
+                // cluster split-K: park this CTA's partial in its own shared memory (stage 0
+                // is idle once the last unit is done); the cluster reduces it below
+                float* red = reinterpret_cast<float*>(smem);
+#pragma unroll
+                for (int m = 0; m < NT; ++m) red[m * kRows + row] = acc[m];
+                w.advance(n);
+            } else if (seg_end) {
                 if (et == 0) stamp(p, 5);
                 epilogue(w.b, seg_kb0 == 0 && w.kb + n == p.KBLK);
                 if (et == 0) stamp(p, 6), prof_store(44);
@@ -860,6 +937,39 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     }
     tc_fence_before();
     __syncthreads();
+    if (p.csize > 1) {
+        // DSMEM reduction: rank 0 of the cluster sums every rank's partial, in rank order
+        // (deterministic), and writes the row-block's output; the second barrier keeps the
+        // other ranks' shared memory alive until rank 0 has read it.
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (c % p.csize == 0 && warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
+            const int row = (warp & 3) * 32 + lane;
+            const int b = c / p.csize;
+            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
+            float sum[NT];
+#pragma unroll
+            for (int m = 0; m < NT; ++m) sum[m] = 0.0f;
+            const uint32_t red = smem_u32(smem);
+            for (int r = 0; r < p.csize; ++r) {
+                uint32_t rbase;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbase) : "r"(red), "r"(r));
+#pragma unroll
+                for (int m = 0; m < NT; ++m) {
+                    float v;
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                                 : "=f"(v)
+                                 : "r"(rbase + uint32_t((m * kRows + row) * 4)));
+                    sum[m] += v;
+                }
+            }
+            if (row < rows)
+#pragma unroll
+                for (int m = 0; m < NT; ++m)
+                    if (m < p.M)
+                        store_out(p.out, p.out_dtype, int64_t(m) * p.N + int64_t(b) * kRows + row, sum[m]);
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -889,6 +999,21 @@ int nt_for(int64_t m, int64_t g, int bits) {
     return nt;
 }
 
+// Cluster split-K when the row-blocks are few (at most half the SMs): S CTAs per row-block,
+// S <= 8 (portable cluster), S <= k-blocks.  0/1 = stream-K.  RTNQ_WGEMM_CTAS (an explicit
+// stream-K grid, used by the split-invariance tests) or RTNQ_WGEMM_CLUSTER=0 disable it.
+int cluster_size_for(int64_t NB, int64_t KBLK) {
+    if (std::getenv("RTNQ_WGEMM_CTAS")) return 1;
+    if (const char* e = std::getenv("RTNQ_WGEMM_CLUSTER"))
+        if (std::atoi(e) == 0) return 1;
+    const int sms = sm_count();
+    if (NB * 2 > sms) return 1;
+    int S = int(sms / NB);
+    S = S > 8 ? 8 : S;
+    S = S > KBLK ? int(KBLK) : S;
+    return S < 2 ? 1 : S;
+}
+
 int ctas_for(int64_t U) {
     int G = sm_count();  // persistent: one CTA per SM (it owns all 512 TMEM columns)
     if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
@@ -897,26 +1022,61 @@ int ctas_for(int64_t U) {
 }
 
 template <int BITS, int AT, int NT, bool PROF>
-cudaError_t launch_t(const Params& p, cudaStream_t st, bool pdl) {
+cudaError_t launch_t(const Params& p_in, cudaStream_t st, bool pdl) {
     using GG = Geo<BITS, NT>;
     auto kern = wgemm_tc_kernel<BITS, AT, NT, PROF>;
     static bool configured = false;
+    static int max_clusters[9] = {0};  // per cluster size: clusters resident at once
     if (!configured) {
         cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GG::SMEM);
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    Params p = p_in;
+    // cluster split-K only if all NB clusters are resident at once; else a smaller cluster
+    while (p.csize > 1) {
+        int& mc = max_clusters[p.csize];
+        if (mc == 0) {
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3(unsigned(p.NB * p.csize));
+            q.blockDim = dim3(kThreads);
+            q.dynamicSmemBytes = GG::SMEM;
+            cudaLaunchAttribute ca;
+            ca.id = cudaLaunchAttributeClusterDimension;
+            ca.val.clusterDim.x = unsigned(p.csize);
+            ca.val.clusterDim.y = ca.val.clusterDim.z = 1;
+            q.attrs = &ca;
+            q.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc < 1) mc = -1;
+            cudaGetLastError();
+        }
+        if (mc >= p.NB) break;
+        --p.csize;
+    }
+    if (p.csize > 1) p.G = p.NB * p.csize;
+    else p.csize = 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(p.G));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = GG::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.csize > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = unsigned(p.csize);
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
@@ -1037,6 +1197,7 @@ cudaError_t launch_wgemm(const WgemmArgs& A, cudaStream_t st) {
         if (cudaError_t e = encode_act_map(&p.tmap_a, A.a, A.a_dtype, A.m, A.k, nt,
                                              A.bits == 4 ? 32 : 16)) return e;
         p.G = tc::ctas_for(p.U);
+        p.csize = tc::cluster_size_for(p.NB, p.KBLK);
         const bool pdl = A.pdl || m0 > 0;
         cudaError_t e;
         if (A.bits == 4)

@@ -252,3 +252,22 @@ def test_linear_llama_shapes_vs_dequant_reference(name, bits):
         ref = a.double() @ wd.double().t()
         err = ((out.double() - ref).norm() / ref.norm()).item()
         assert err <= TOL, (name, bits, m, err)
+
+
+@pytest.mark.parametrize("n,k,bits,g,m", [(4096, 4096, 4, 128, 16), (512, 1024, 4, 128, 1),
+                                          (4096, 14336, 8, 16384, 5), (1000, 2048, 8, 128, 33),
+                                          (2304, 16384, 4, 128, 7)])
+def test_cluster_split_k_matches_stream_k(oracle, monkeypatch, n, k, bits, g, m):
+    """Small-N shapes run cluster split-K (DSMEM reduction); it must agree with the
+    stream-K path and be run-to-run deterministic."""
+    q, codes, s16w = _make(oracle, n, k, bits, g, seed=n + k, ragged=k % g != 0)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+    o1 = rq.linear(a, q, out_dtype=torch.float32)
+    o2 = rq.linear(a, q, out_dtype=torch.float32)
+    assert torch.equal(o1, o2)
+    monkeypatch.setenv("RTNQ_WGEMM_CLUSTER", "0")
+    o3 = rq.linear(a, q, out_dtype=torch.float32, workspace=rq.Workspace(device="cuda"))
+    assert rel_frob(o1.cpu().numpy(), o3.cpu().numpy()) <= 1e-6
+    if n * k <= 4096 * 4096:
+        ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+        assert rel_frob(o1.cpu().numpy(), ref) <= TOL
