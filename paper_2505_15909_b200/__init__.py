@@ -31,7 +31,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "librtnq_b200.so")
 
 F32, F16, BF16 = 0, 1, 2
-ROW_MAJOR, KERNEL_INTERLEAVED, NATIVE = 0, 1, 2
+ROW_MAJOR, KERNEL_INTERLEAVED, NATIVE, NATIVE_I8 = 0, 1, 2, 3
 SCALES_REF, SCALES_NATIVE = 0, 1
 PATH_FUSED, PATH_DEQUANT_FIRST, PATH_AUTO, PATH_ORACLE = 0, 1, 2, 3
 DEFAULT_THRESHOLD = 1024  # kDefaultGemmThreshold, gemm.hpp:16
@@ -184,8 +184,9 @@ class QuantWeight:
     bits: int
     group: int
     ragged: bool
-    codes: "object"            # uint8 native-layout codes
+    codes: "object"            # uint8 codes in `layout` (native, or row-major for W8 per-channel)
     scales: "object"           # f16 bits (int16 tensor) in native order
+    layout: int = NATIVE       # NATIVE: tcgen05 kind::f16 kernel; NATIVE_I8: kind::i8 kernel
     codes_row_major: "object" = None
     codes_kernel: "object" = None
     scales_f32: "object" = None  # reference order
@@ -201,10 +202,14 @@ class QuantWeight:
         return self.rows * self.cols * self.bits // 8 + self.rows * self.gpr * 2
 
 
-def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=True,
+def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None,
                   row_major=False, kernel=False, scales_f32=False, scales_f16=False,
                   check=True, stream=None) -> QuantWeight:
-    """RTN quantize-and-pack on the GPU (rtnq_dev_quantize_pack)."""
+    """RTN quantize-and-pack on the GPU (rtnq_dev_quantize_pack).
+
+    The linear's operand is ``codes`` in ``layout``: the native tcgen05 order, except
+    for W8 per-channel (one group per row), whose kernel streams the reference's own
+    row-major bytes (tcgen05 kind::i8, no dequantization)."""
     torch = _torch()
     assert w.is_cuda and w.dim() == 2 and w.is_contiguous()
     rows, cols = w.shape
@@ -212,6 +217,14 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=True
     dev = w.device
     u8 = dict(dtype=torch.uint8, device=dev)
     out = QuantWeight(rows, cols, bits, group, ragged, None, None)
+    # default operand: W8 per-channel -> row-major (kind::i8 kernel), else native
+    pc8 = native is None and bits == 8 and group >= cols
+    native = (not pc8) if native is None else native
+    if pc8:
+        native = False
+        rm_requested, row_major = row_major, True
+        out.layout = NATIVE_I8
+        out.scales = torch.empty(native_scale_count(rows, gpr), dtype=torch.int16, device=dev)
     if native:
         out.codes = torch.empty(layout_bytes(layout(NATIVE), bits, rows, cols), **u8)
         out.scales = torch.empty(native_scale_count(rows, gpr), dtype=torch.int16, device=dev)
@@ -234,6 +247,11 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=True
         _ptr(out.scales), _ptr(err), _ptr(ws), wsb, st))
     if check:
         _check(lib().rtnq_dev_check_flag(_ptr(err), st))
+    if out.layout == NATIVE_I8:  # pre-swizzled int8-MMA tiles, from the row-major bytes
+        out.codes = relayout(out.codes_row_major, layout(ROW_MAJOR), layout(NATIVE_I8), bits, rows,
+                             cols, stream=stream)
+        if not rm_requested:
+            out.codes_row_major = None
     return out
 
 
@@ -272,7 +290,7 @@ def linear(a, qw: QuantWeight, out=None, out_dtype=None, *, path=PATH_FUSED,
     m = a.shape[0]
     if out is None:
         out = torch.empty(m, qw.rows, dtype=out_dtype or a.dtype, device=a.device)
-    lay = layout(NATIVE)
+    lay = layout(qw.layout)
     wsb = lib().rtnq_dev_linear_workspace_bytes(m, qw.rows, qw.cols, qw.bits, qw.group, path, lay)
     if workspace is None:
         workspace = _default_ws.setdefault(a.device, Workspace(wsb, a.device))

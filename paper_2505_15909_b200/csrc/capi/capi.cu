@@ -37,7 +37,7 @@ Layout to_layout(rtnq_layout l) { return Layout{l.kind, l.tile_rows, l.tile_cols
 bool valid_bits(int bits) { return bits == 4 || bits == 8; }
 
 rtnq_status check_layout(rtnq_layout l) {
-    if (l.kind < RTNQ_ROW_MAJOR || l.kind > RTNQ_NATIVE_SM100)
+    if (l.kind < RTNQ_ROW_MAJOR || l.kind > RTNQ_NATIVE_I8)
         return fail(RTNQ_E_INVALID_INPUT, "unknown layout kind");
     if (l.kind == RTNQ_KERNEL_INTERLEAVED && (l.tile_rows <= 0 || l.tile_cols <= 0))
         return fail(RTNQ_E_INVALID_INPUT, "kernel tile dimensions must be positive");
@@ -229,6 +229,12 @@ rtnq_status rtnq_dev_dequantize(const uint8_t* codes, rtnq_layout layout, int bi
     return RTNQ_OK;
 }
 
+// W8 per-channel over the reference's row-major bytes: the int8 tensor-core kernel.
+static bool i8_path(int a_dtype, rtnq_layout layout, int bits, int64_t g, int64_t k, int sdtype) {
+    return layout.kind == RTNQ_NATIVE_I8 && bits == 8 && g >= k &&
+           (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) && sdtype == RTNQ_F16;
+}
+
 static bool tensor_path(int a_dtype, rtnq_layout layout, int sdtype, int sorder) {
     return layout.kind == RTNQ_NATIVE_SM100 && (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) &&
            sdtype == RTNQ_F16 && sorder == RTNQ_SCALES_NATIVE;
@@ -239,6 +245,7 @@ size_t rtnq_dev_linear_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits
     size_t ws = 0;
     if (path == RTNQ_PATH_FUSED || path == RTNQ_PATH_AUTO) {
         if (layout.kind == RTNQ_NATIVE_SM100) ws = wgemm_workspace_bytes(m, n, k, bits, g);
+        if (layout.kind == RTNQ_NATIVE_I8 && bits == 8 && g >= k) ws = wgemm_i8_workspace_bytes(m, n, k);
     }
     if (path == RTNQ_PATH_DEQUANT_FIRST || path == RTNQ_PATH_AUTO) {
         const size_t d = size_t(n) * size_t(k) * sizeof(float);
@@ -290,6 +297,21 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
         WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
                     out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
         RTNQ_CUDA(launch_wgemm(A, st));
+        return RTNQ_OK;
+    }
+    if (path == RTNQ_PATH_FUSED && i8_path(a_dtype, layout, bits, g, k, sdtype)) {
+        if (const char* why = wgemm_i8_unsupported(m, n, k, bits, g, a_dtype))
+            return fail(RTNQ_E_UNSUPPORTED, why);
+        const size_t need = wgemm_i8_workspace_bytes(m, n, k);
+        if (ws_bytes < need)
+            return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " +
+                                                  std::to_string(need) + " bytes");
+        if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(codes) |
+             reinterpret_cast<uintptr_t>(scales)) & 15)
+            return fail(RTNQ_E_INVALID_INPUT, "tensor-core path needs 16-byte aligned operands");
+        WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
+                    out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
+        RTNQ_CUDA(launch_wgemm_i8(A, st));
         return RTNQ_OK;
     }
     // Reference-exact CUDA-core paths: f32 activations, f32 reference-order scales.

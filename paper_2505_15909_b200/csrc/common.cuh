@@ -140,9 +140,32 @@ __host__ __device__ __forceinline__ bool native_coords(int bits, int64_t rows, i
     return *r < rows && *c < cols;
 }
 
+// Native int8-MMA layout (RTNQ_NATIVE_I8): 128-row x 128-code tiles, row-blocks
+// outer and k-tiles inner (a row-block is one contiguous run along K), each tile stored
+// exactly as a 128-byte-swizzled UMMA K-major operand: code (r, k) of a tile sits at
+// r * 128 + ((k / 16) ^ (r % 8)) * 16 + k % 16.  Padding (rows to 128, K to 128) is zero.
+constexpr int kI8Tile = 128;
+__host__ __device__ __forceinline__ int64_t i8_slot(int64_t cols, int64_t r, int64_t c) {
+    const int64_t kt = (cols + kI8Tile - 1) / kI8Tile;
+    const int64_t tile = (r / kI8Tile) * kt + c / kI8Tile;
+    const int64_t rr = r % kI8Tile, kk = c % kI8Tile;
+    return tile * (kI8Tile * kI8Tile) + rr * kI8Tile + ((((kk >> 4) ^ (rr & 7)) << 4) | (kk & 15));
+}
+__host__ __device__ __forceinline__ bool i8_coords(int64_t rows, int64_t cols, int64_t slot,
+                                                   int64_t* r, int64_t* c) {
+    const int64_t kt = (cols + kI8Tile - 1) / kI8Tile;
+    const int64_t tile = slot / (kI8Tile * kI8Tile), within = slot % (kI8Tile * kI8Tile);
+    const int64_t rr = within / kI8Tile, pos = within % kI8Tile;
+    const int64_t kk = ((((pos >> 4) ^ (rr & 7))) << 4) | (pos & 15);
+    *r = (tile / kt) * kI8Tile + rr;
+    *c = (tile % kt) * kI8Tile + kk;
+    return *r < rows && *c < cols;
+}
+
 __host__ __device__ __forceinline__ int64_t layout_slot(const Layout& L, int bits, int64_t rows,
                                                         int64_t cols, int64_t r, int64_t c) {
     if (L.kind == RTNQ_ROW_MAJOR) return r * cols + c;
+    if (L.kind == RTNQ_NATIVE_I8) return i8_slot(cols, r, c);
     if (L.kind == RTNQ_NATIVE_SM100) return native_slot(bits, rows, cols, r, c);
     const int64_t tpr = (cols + L.tc - 1) / L.tc;  // packing.cpp:62-65
     const int64_t tile = (r / L.tr) * tpr + c / L.tc;
@@ -158,6 +181,7 @@ __host__ __device__ __forceinline__ bool layout_coords(const Layout& L, int bits
         return *r < rows;
     }
     if (L.kind == RTNQ_NATIVE_SM100) return native_coords(bits, rows, cols, slot, r, c);
+    if (L.kind == RTNQ_NATIVE_I8) return i8_coords(rows, cols, slot, r, c);
     const int64_t tt = int64_t(L.tr) * L.tc, tpr = (cols + L.tc - 1) / L.tc;
     const int64_t tile = slot / tt, within = slot % tt;
     *r = (tile / tpr) * L.tr + within % L.tr;
@@ -170,6 +194,8 @@ __host__ __device__ __forceinline__ int64_t layout_slots_of(const Layout& L, int
     if (L.kind == RTNQ_ROW_MAJOR) return rows * cols;
     if (L.kind == RTNQ_NATIVE_SM100)
         return rows * ((cols + kNativeKB - 1) / kNativeKB * kNativeKB);
+    if (L.kind == RTNQ_NATIVE_I8)
+        return (rows + kI8Tile - 1) / kI8Tile * kI8Tile * ((cols + kI8Tile - 1) / kI8Tile * kI8Tile);
     return ((rows + L.tr - 1) / L.tr * L.tr) * ((cols + L.tc - 1) / L.tc * L.tc);
 }
 

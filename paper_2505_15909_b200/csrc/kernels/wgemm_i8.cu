@@ -1,0 +1,764 @@
+// wgemm_i8.cu -- W8A16 per-channel linear on tcgen05.mma.kind::i8.
+//
+// out[m][n] = S[n] * sum_k a[m][k] * code[n][k]        (gemm.hpp:18-27, one group per row)
+//
+// The 8-bit codes need no dequantization at all.  They are the reference's offset-binary
+// bytes (u = c + 128, packing.cpp:19-22) in the RTNQ_NATIVE_I8 layout (common.cuh): 16 KiB
+// tiles of 128 rows x 128 codes, contiguous and pre-swizzled.  One bulk copy moves a tile
+// into 1024-aligned shared memory, where it already is the 128-byte-swizzled K-major u8 A
+// operand of the tensor core.
+//
+// The bf16/f16 activations become three exact int8 planes, done once per call by
+// act_planes_kernel:
+//   a = 2^s * (P0 + P1 / 2^7 + P2 / 2^14),  |Pi| <= 64.
+// This is exact for every element within 2^13 of the token's largest magnitude.  Smaller
+// ones round at 2^-21 of that maximum, far inside the 1e-5 parity bar.  The planes are
+// the s8 B operand: N = 3 * tokens.
+//
+// The int32 accumulators are exact.  They run over a CTA's whole K range in TMEM; the
+// scale S[n] is per row, so it is applied once at the end.  The offset is removed with
+// per-plane prefix sums of the activations:
+//   sum_k u*P = sum_k c*P + 128 * sum_k P.
+//
+// Warp roles: warp 0 is the TMA producer, warp 1 the single-thread MMA issuer, and
+// warps 4-7 the epilogue (TMEM lane quadrants).  Work is partitioned with stream-K or,
+// for few row-blocks, cluster split-K with a DSMEM reduction, as in wgemm_tc.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "../common.cuh"
+#include "kernels.cuh"
+
+namespace rtnq_b200 {
+namespace i8 {
+
+constexpr int kRows = 128;     // UMMA M = one row-block
+constexpr int kKB = 64;        // stream-K bookkeeping unit (k-block of 64 codes)
+constexpr int kUnit = 128;     // codes per unit = one 128-byte swizzle row
+constexpr int kThreads = 256;  // warp 0 producer, warp 1 MMA, warps 4-7 epilogue
+constexpr int kEpi0 = 4;
+
+struct Params {
+    CUtensorMap tmap_p;  // planes [3][M][K] s8, box {128, NT, 3}, SWIZZLE_128B
+    const uint8_t* codes;  // RTNQ_NATIVE_I8: 16 KiB pre-swizzled 128 x 128 tiles, row-block major
+    const uint16_t* scales;  // f16 per row
+    const int32_t* texp;     // [M] token exponents s
+    const int32_t* pre;      // [3][M][KBLK + 1] prefix sums of each plane over 64-code blocks
+    void* out;
+    float* partials;
+    int* counters;
+    int64_t N, K;
+    int M, Mtot, m0, NB, KBLK, U, G, csize, out_dtype;
+    int debug;  // profiling: 4 = no MMA issued, 2 = no loads (arrive only)
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+    asm volatile(
+        "{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra W_%=;\n}\n" ::"r"(su32(b)),
+        "r"(ph)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                      uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit(uint64_t* b) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t* d) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+          "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+          "=r"(d[14]), "=r"(d[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void store_out(void* out, int dt, int64_t i, float v) {
+    if (dt == RTNQ_F32) static_cast<float*>(out)[i] = v;
+    else if (dt == RTNQ_BF16) static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    else static_cast<__half*>(out)[i] = __float2half_rn(v);
+}
+// K-major, 128-byte swizzle: 8-row atoms of 128 B (SBO = 1024), layout type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+           (1ull << 46) | (2ull << 61);
+}
+// The unit sequence of a CTA: runs of <= 2 k-blocks inside one row-block and one 128-code
+// block, tracked incrementally (no division on the issue path).
+struct Cursor {
+    int u, u1, b, kb, KBLK;
+    __device__ Cursor(int u0, int u1_, int KBLK_) : u(u0), u1(u1_), KBLK(KBLK_) {
+        b = u0 / KBLK_;
+        kb = u0 - b * KBLK_;
+    }
+    __device__ bool more() const { return u < u1; }
+    __device__ int chunk() const {
+        const int left_seg = KBLK - kb, left = u1 - u, cap = 2 - (kb & 1);
+        const int n = left_seg < left ? left_seg : left;
+        return n < cap ? n : cap;
+    }
+    __device__ bool seg_end(int n) const { return kb + n == KBLK || u + n == u1; }
+    __device__ void advance(int n) {
+        u += n;
+        kb += n;
+        if (kb == KBLK) kb = 0, ++b;
+    }
+};
+__device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                             uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* b) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void elect_arrive(uint64_t* b) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+            su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void elect_bulk(void* dst, const void* src, uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void elect_tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                            uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%6], %5;\n"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%6];\n}\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+
+__device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
+    return int(((u + 1) * G - 1) / U);
+}
+
+template <int NT>
+struct Geo {
+    static constexpr int CODE_BYTES = kRows * kUnit;             // 16 KiB
+    static constexpr int PLANE_BYTES = 3 * NT * kUnit;           // 6 / 12 / 24 KiB
+    static constexpr int STAGE_BYTES = CODE_BYTES + PLANE_BYTES;  // multiple of 1 KiB
+    static constexpr int STAGES_FIT = (208 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int COR_OFF = BAR_OFF + 1024;                // [3][NT] corrections + [NT] exps
+    static constexpr int SMEM = COR_OFF + 4 * NT * 4 + 1024;
+    static constexpr int DN = 3 * NT;                             // accumulator columns
+    static_assert(STAGES >= 3, "");
+};
+
+__device__ unsigned long long g_i8_dbg[1024 * 8];  // profiling (debug & 32)
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_constant__ Params p) {
+    using GG = Geo<NT>;
+    constexpr int STAGES = GG::STAGES, DN = GG::DN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);  // [STAGES]
+    uint64_t* empty = full + STAGES;                                  // [STAGES]
+    uint64_t* dfull = empty + STAGES;                                 // [2]
+    uint64_t* dempty = dfull + 2;                                     // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+    volatile int* flag = reinterpret_cast<volatile int*>(tslot + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
+
+    int u0, u1;
+    if (p.csize > 1) {
+        const int b = c / p.csize, r = c % p.csize;
+        u0 = b * p.KBLK + r * p.KBLK / p.csize;
+        u1 = b * p.KBLK + (r + 1) * p.KBLK / p.csize;
+    } else {
+        u0 = int(int64_t(c) * p.U / p.G);
+        u1 = int(int64_t(c + 1) * p.U / p.G);
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
+        for (int i = 0; i < 2; ++i) mbar_init(&dfull[i], 1), mbar_init(&dempty[i], 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            su32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+    asm volatile("griddepcontrol.launch_dependents;");
+
+    // units: runs of <= 2 k-blocks inside one row-block and one 128-code block
+    auto chunk = [&](int u, int kb) {
+        const int left_seg = p.KBLK - kb, left = u1 - u, cap = 2 - (kb & 1);
+        const int n = left_seg < left ? left_seg : left;
+        return n < cap ? n : cap;
+    };
+
+    if (warp == 0 || warp == 2) {
+        // ===================== producers: warp 0 codes, warp 2 activation planes ===========
+        // Warp-uniform loops (one elected lane issues), incremental row-block / k-block.
+        const bool codes = warp == 0;
+        Cursor cu(u0, u1, p.KBLK);
+        int s = 0;
+        uint32_t ph = 0;
+        const long long t0 = clock64();
+        long long tw = 0;
+        if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes come from the previous kernel
+        for (int i = 0; cu.more(); ++i) {
+            const int n = cu.chunk();
+            if (i >= STAGES) {
+                const long long a0 = clock64();
+                mbar_wait(&empty[s], ph ^ 1u);
+                tw += clock64() - a0;
+            }
+            uint8_t* st = smem + s * GG::STAGE_BYTES;
+            // a half unit (one 64-code k-block) still loads a full 128-code box: the other
+            // half belongs to a later unit or is out of bounds (zeros); the MMA uses one half
+            if (p.debug & 2) {
+                elect_arrive(&full[s]);
+            } else if (codes) {  // one contiguous, pre-swizzled 16 KiB tile
+                const int64_t tile = int64_t(cu.b) * ((p.KBLK + 1) >> 1) + (cu.kb >> 1);
+                elect_bulk(st, p.codes + tile * GG::CODE_BYTES, &full[s], GG::CODE_BYTES);
+            } else {
+                elect_tma3d(st + GG::CODE_BYTES, &p.tmap_p, (cu.kb & ~1) * kKB, p.m0, 0, &full[s],
+                            GG::PLANE_BYTES);
+            }
+            cu.advance(n);
+            if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+        if ((p.debug & 32) && lane == 0 && codes) {
+            g_i8_dbg[c * 8 + 0] = clock64() - t0;
+            g_i8_dbg[c * 8 + 1] = tw;
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
+        // D s32, A u8 (offset-binary codes), B s8 (planes), M = 128, N = 3 * NT
+        constexpr uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) |
+                                   (uint32_t(DN >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
+        constexpr uint64_t kHi = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
+                                 (2ull << 61);  // K-major SWIZZLE_128B, SBO = 1024
+        const uint32_t lo0 = su32(smem) >> 4;   // descriptor address field of stage 0
+        Cursor cu(u0, u1, p.KBLK);
+        int s = 0, db = 0, seg = 0;
+        uint32_t ph = 0, lo = lo0;
+        bool first = true;
+        const long long t0 = clock64();
+        long long tw = 0, ti = 0;
+        while (cu.more()) {
+            const int n = cu.chunk();
+            const bool seg_end = cu.seg_end(n);
+            if (first && seg >= 2) {  // accumulator reuse: the epilogue drained it
+                mbar_wait(&dempty[db], uint32_t((seg >> 1) - 1) & 1u);
+                fence_after();
+            }
+            const long long a0 = clock64();
+            mbar_wait(&full[s], ph);
+            fence_after();
+            const long long a1 = clock64();
+            tw += a1 - a0;
+            const uint32_t alo = lo + ((cu.kb & 1) ? 4u : 0u);  // second 64-code half: +64 B
+            const uint32_t blo = alo + (GG::CODE_BYTES >> 4);
+            const uint32_t d = tmem + db * DN;
+            if (!(p.debug & 4)) {
+                if (n == 2) {
+                    mma_i8_elect(d, kHi | alo, kHi | blo, idesc, first ? 0u : 1u);
+                    mma_i8_elect(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
+                    mma_i8_elect(d, kHi | (alo + 4), kHi | (blo + 4), idesc, 1u);
+                    mma_i8_elect(d, kHi | (alo + 6), kHi | (blo + 6), idesc, 1u);
+                } else {
+                    mma_i8_elect(d, kHi | alo, kHi | blo, idesc, first ? 0u : 1u);
+                    mma_i8_elect(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
+                }
+            }
+            first = false;
+            commit_elect(&empty[s]);
+            ti += clock64() - a1;
+            if (seg_end) {
+                commit_elect(&dfull[db]);
+                db ^= 1;
+                ++seg;
+                first = true;
+            }
+            cu.advance(n);
+            if (++s == STAGES) s = 0, ph ^= 1u, lo = lo0;
+            else lo += GG::STAGE_BYTES >> 4;
+        }
+        if ((p.debug & 32) && lane == 0) {
+            g_i8_dbg[c * 8 + 2] = clock64() - t0;
+            g_i8_dbg[c * 8 + 3] = tw;
+            g_i8_dbg[c * 8 + 4] = ti;
+        }
+    } else if (warp >= kEpi0) {
+        // ===================== epilogue =====================
+        const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        const int kb1 = p.KBLK + 1;
+        int db = 0, seg = 0, u = u0;
+        while (u < u1) {
+            // walk to this segment's end
+            const int b = u / p.KBLK, kb0 = u - b * p.KBLK;
+            int kbe = kb0, uu = u;
+            while (true) {
+                const int kb = uu - b * p.KBLK, n = chunk(uu, kb);
+                uu += n, kbe = kb + n;
+                if (kbe == p.KBLK || uu == u1) break;
+            }
+            const bool sole = kb0 == 0 && kbe == p.KBLK;
+            // per-token bias corrections and exponents of this segment, loaded once by the
+            // 128 epilogue threads (they are the same for every row)
+            int32_t* cor_s = reinterpret_cast<int32_t*>(smem + GG::COR_OFF);
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous segment done reading
+            for (int x = et; x < 4 * NT; x += 128) {
+                const int pl = x / NT, t = x % NT;
+                int32_t v = 0;
+                if (t < p.M) {
+                    if (pl < 3) {
+                        const int32_t* pr = p.pre + (int64_t(pl) * p.Mtot + p.m0 + t) * kb1;
+                        v = 128 * (__ldg(pr + kbe) - __ldg(pr + kb0));
+                    } else {
+                        v = __ldg(p.texp + p.m0 + t);
+                    }
+                }
+                cor_s[x] = v;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&dfull[db], uint32_t(seg >> 1) & 1u);
+            fence_after();
+            float acc[NT];
+            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
+            const float srow = row < rows ? __half2float(__ushort_as_half(p.scales[int64_t(b) * kRows + row])) : 0.0f;
+#pragma unroll
+            for (int j = 0; j < NT; j += 16) {
+                uint32_t d0[16], d1[16], d2[16];
+                ld16(tmem + lane_base + db * DN + j, d0);
+                ld16(tmem + lane_base + db * DN + NT + j, d1);
+                ld16(tmem + lane_base + db * DN + 2 * NT + j, d2);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int t = j + e;
+                    float v = 0.0f;
+                    if (t < p.M) {
+                        // remove the offset-binary bias: sum u*P = sum c*P + 128 * sum P
+                        const float x = float(int32_t(d0[e]) - cor_s[t]) +
+                                        float(int32_t(d1[e]) - cor_s[NT + t]) * 0.0078125f +
+                                        float(int32_t(d2[e]) - cor_s[2 * NT + t]) * 6.103515625e-05f;
+                        v = ldexpf(x, cor_s[3 * NT + t]) * srow;
+                    }
+                    acc[t] = v;
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dempty[db]);
+            const int64_t n0 = int64_t(b) * kRows;
+            if (p.csize > 1) {
+                float* red = reinterpret_cast<float*>(smem);  // stages are idle by now
+#pragma unroll
+                for (int m = 0; m < NT; ++m) red[m * kRows + row] = acc[m];
+            } else if (sole) {
+                if (row < rows)
+#pragma unroll
+                    for (int m = 0; m < NT; ++m)
+                        if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+            } else {
+                const int slot = 2 * c + (b == u0 / p.KBLK ? 0 : 1);
+                float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(slot) * kRows + row) * NT);
+#pragma unroll
+                for (int j = 0; j < NT / 4; ++j)
+                    mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
+                const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
+                if (et == 0) {
+                    int prev;
+                    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                                 : "=r"(prev)
+                                 : "l"(p.counters + b)
+                                 : "memory");
+                    const int last = prev == c_last - c_first;
+                    if (last) p.counters[b] = 0;
+                    *flag = last;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (*flag) {
+                    float sum[NT];
+#pragma unroll
+                    for (int m = 0; m < NT; ++m) sum[m] = 0.0f;
+                    const int first_bit = int(int64_t(c_first) * p.U / p.G) / p.KBLK == b ? 0 : 1;
+                    for (int cc = c_first; cc <= c_last; ++cc) {  // fixed order: deterministic
+                        const int cs = 2 * cc + (cc == c_first ? first_bit : 0);
+                        const float4* src =
+                            reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * kRows + row) * NT);
+#pragma unroll
+                        for (int j = 0; j < NT / 4; ++j) {
+                            const float4 x = __ldcg(src + j);
+                            sum[4 * j] += x.x, sum[4 * j + 1] += x.y, sum[4 * j + 2] += x.z, sum[4 * j + 3] += x.w;
+                        }
+                    }
+                    if (row < rows)
+#pragma unroll
+                        for (int m = 0; m < NT; ++m)
+                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, sum[m]);
+                }
+            }
+            u = uu;
+            db ^= 1;
+            ++seg;
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (p.csize > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (c % p.csize == 0 && warp >= kEpi0) {
+            const int row = (warp & 3) * 32 + lane, b = c / p.csize;
+            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
+            float sum[NT];
+#pragma unroll
+            for (int m = 0; m < NT; ++m) sum[m] = 0.0f;
+            const uint32_t red = su32(smem);
+            for (int r = 0; r < p.csize; ++r) {  // rank order: deterministic
+                uint32_t rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(red), "r"(r));
+#pragma unroll
+                for (int m = 0; m < NT; ++m) {
+                    float v;
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(rb + uint32_t((m * kRows + row) * 4)));
+                    sum[m] += v;
+                }
+            }
+            if (row < rows)
+#pragma unroll
+                for (int m = 0; m < NT; ++m)
+                    if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + int64_t(b) * kRows + row, sum[m]);
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+// ---- activation planes ------------------------------------------------------------------
+// One CTA per token: s = exponent(max|a|) - 5 so |a| / 2^s < 64; three exact int8 planes;
+// per-64-code-block prefix sums of each plane (for the offset-binary correction).
+template <int AT>
+__global__ void act_planes_kernel(const void* __restrict__ a, int K, int M, int8_t* __restrict__ planes,
+                                  int32_t* __restrict__ texp, int32_t* __restrict__ bsum, int kblk) {
+    // grid (M, ceil(kblk / 8)): each CTA re-reduces its token's max (the row is L2-resident),
+    // then its warps own one 64-code block each: planes + per-block plane sums
+    __shared__ float wmax[8];
+    const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto ld = [&](int k) -> float {
+        if constexpr (AT == RTNQ_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(a)[int64_t(t) * K + k]);
+        else return __half2float(static_cast<const __half*>(a)[int64_t(t) * K + k]);
+    };
+    float mx = 0.0f;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(ld(k)));
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.0f;
+        for (int i = 0; i < int(blockDim.x / 32); ++i) m = fmaxf(m, wmax[i]);
+        wmax[0] = m;
+    }
+    __syncthreads();
+    const float amax = wmax[0];
+    int e = 0;
+    if (amax > 0.0f) frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
+    const int s = e - 6;                 // |a| / 2^s < 64
+    if (threadIdx.x == 0 && blockIdx.y == 0) texp[t] = s;
+    // planes and per-block sums (a warp per 64-code block, 2 codes per lane)
+    for (int blk = blockIdx.y * 8 + warp; blk < kblk && blk < (int(blockIdx.y) + 1) * 8; blk += 8) {
+        int32_t ps[3] = {0, 0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = blk * 64 + h * 32 + lane;
+            int p0 = 0, p1 = 0, p2 = 0;
+            if (k < K) {
+                const float x = ldexpf(ld(k), -s);  // exact
+                const float r0 = rintf(x);
+                const float y1 = (x - r0) * 128.0f;  // exact
+                const float r1 = rintf(y1);
+                const float r2 = rintf((y1 - r1) * 128.0f);
+                p0 = int(r0), p1 = int(r1), p2 = int(r2);
+                planes[(int64_t(0) * M + t) * K + k] = int8_t(p0);
+                planes[(int64_t(1) * M + t) * K + k] = int8_t(p1);
+                planes[(int64_t(2) * M + t) * K + k] = int8_t(p2);
+            }
+            ps[0] += p0, ps[1] += p1, ps[2] += p2;
+        }
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) {
+            int v = ps[pl];
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) bsum[(int64_t(pl) * M + t) * kblk + blk] = v;
+        }
+    }
+}
+
+// Exclusive prefix over the 64-code blocks: pre[pl][t][0..kblk] (one warp per (plane, token)).
+__global__ void plane_prefix_kernel(const int32_t* __restrict__ bsum, int32_t* __restrict__ pre,
+                                    int M, int kblk) {
+    const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= 3 * M) return;
+    const int32_t* in = bsum + int64_t(row) * kblk;
+    int32_t* out = pre + int64_t(row) * (kblk + 1);
+    int32_t carry = 0;
+    if (lane == 0) out[0] = 0;
+    for (int base = 0; base < kblk; base += 32) {
+        int32_t v = base + lane < kblk ? in[base + lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive warp scan
+            const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (base + lane < kblk) out[base + lane + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+}
+
+// ---- host ----------------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+static EncodeFn encoder() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+int sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int NT>
+cudaError_t launch_nt(Params p, cudaStream_t st, bool pdl) {
+    using GG = Geo<NT>;
+    auto kern = wgemm_i8_kernel<NT>;
+    static bool configured = false;
+    static int max_clusters[9] = {0};
+    if (!configured) {
+        if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GG::SMEM))
+            return e;
+        configured = true;
+    }
+    while (p.csize > 1) {
+        int& mc = max_clusters[p.csize];
+        if (mc == 0) {
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3(unsigned(p.NB * p.csize));
+            q.blockDim = dim3(kThreads);
+            q.dynamicSmemBytes = GG::SMEM;
+            cudaLaunchAttribute ca;
+            ca.id = cudaLaunchAttributeClusterDimension;
+            ca.val.clusterDim.x = unsigned(p.csize);
+            ca.val.clusterDim.y = ca.val.clusterDim.z = 1;
+            q.attrs = &ca;
+            q.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc < 1) mc = -1;
+            cudaGetLastError();
+        }
+        if (mc >= p.NB) break;
+        --p.csize;
+    }
+    if (p.csize > 1) p.G = p.NB * p.csize;
+    else p.csize = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(p.G));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = GG::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.csize > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = unsigned(p.csize);
+        attr[na].val.clusterDim.y = attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+}  // namespace i8
+
+constexpr size_t kI8Counters = 64 * 1024;
+
+extern "C" int rtnq_i8_debug_read(void* host, size_t bytes) {
+    if (bytes > sizeof(i8::g_i8_dbg)) bytes = sizeof(i8::g_i8_dbg);
+    return cudaMemcpyFromSymbol(host, i8::g_i8_dbg, bytes) == cudaSuccess ? 0 : 1;
+}
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t wgemm_i8_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+    const int64_t kblk = (k + 63) / 64;
+    const size_t part = size_t(i8::sms()) * 2 * i8::kRows * 64 * sizeof(float);
+    return kI8Counters + align256(part) + align256(size_t(3 * m * k)) + align256(size_t(m) * 4) +
+           align256(size_t(3 * m * (kblk + 1)) * 4) + align256(size_t(3 * m * kblk) * 4);
+}
+
+const char* wgemm_i8_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype) {
+    (void)m, (void)n;
+    if (bits != 8 || g < k) return "the int8 tensor-core path is W8 per-channel (one group per row)";
+    if (a_dtype != RTNQ_BF16 && a_dtype != RTNQ_F16) return "activations must be bf16 or f16";
+    if (k % 16 != 0) return "k must be a multiple of 16 for the int8 tensor-core path";
+    return nullptr;
+}
+
+cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
+    i8::EncodeFn enc = i8::encoder();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t kblk = (A.k + 63) / 64;
+    char* ws = static_cast<char*>(A.workspace);
+    i8::Params p{};
+    p.counters = reinterpret_cast<int*>(ws);
+    const size_t part = size_t(i8::sms()) * 2 * i8::kRows * 64 * sizeof(float);
+    p.partials = reinterpret_cast<float*>(ws + kI8Counters);
+    int8_t* planes = reinterpret_cast<int8_t*>(ws + kI8Counters + align256(part));
+    int32_t* texp = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes) + align256(size_t(3 * A.m * A.k)));
+    int32_t* pre = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(texp) + align256(size_t(A.m) * 4));
+    int32_t* bsum = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(pre) +
+                                               align256(size_t(3 * A.m * (kblk + 1)) * 4));
+    // 1. activation planes (once per call): planes + block sums, then their prefix
+    const dim3 pg(unsigned(A.m), unsigned((kblk + 7) / 8));
+    if (A.a_dtype == RTNQ_BF16)
+        i8::act_planes_kernel<RTNQ_BF16><<<pg, 256, 0, st>>>(A.a, int(A.k), int(A.m), planes, texp, bsum, int(kblk));
+    else
+        i8::act_planes_kernel<RTNQ_F16><<<pg, 256, 0, st>>>(A.a, int(A.k), int(A.m), planes, texp, bsum, int(kblk));
+    i8::plane_prefix_kernel<<<unsigned((3 * A.m + 7) / 8), 256, 0, st>>>(bsum, pre, int(A.m), int(kblk));
+    if (cudaError_t e = cudaGetLastError()) return e;
+    // 2. the GEMM
+    p.codes = A.codes;
+    p.scales = A.scales;
+    p.texp = texp;
+    p.pre = pre;
+    p.N = A.n;
+    p.K = A.k;
+    p.Mtot = int(A.m);
+    p.NB = int((A.n + i8::kRows - 1) / i8::kRows);
+    p.KBLK = int(kblk);
+    p.U = p.NB * p.KBLK;
+    p.out_dtype = A.out_dtype;
+    if (const char* e = std::getenv("RTNQ_WGEMM_DEBUG")) p.debug = std::atoi(e);
+    const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
+    const int nt_max = A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
+    for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {
+        p.M = int(A.m - m0 < nt_max ? A.m - m0 : nt_max);
+        p.m0 = int(m0);
+        p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
+        const int nt = p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64;
+        {
+            const cuuint64_t dims[3] = {cuuint64_t(A.k), cuuint64_t(A.m), 3};
+            const cuuint64_t strides[2] = {cuuint64_t(A.k), cuuint64_t(A.m * A.k)};
+            const cuuint32_t box[3] = {128, cuuint32_t(nt), 3};
+            const cuuint32_t es[3] = {1, 1, 1};
+            if (enc(&p.tmap_p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return cudaErrorInvalidValue;
+        }
+        // partition: cluster split-K for few row-blocks, else stream-K over all SMs
+        p.csize = 1;
+        if (!std::getenv("RTNQ_WGEMM_CTAS") && int64_t(p.NB) * 2 <= i8::sms()) {
+            const char* ce = std::getenv("RTNQ_WGEMM_CLUSTER");
+            if (!ce || std::atoi(ce) != 0) {
+                int S = i8::sms() / p.NB;
+                S = S > 8 ? 8 : S;
+                S = S > p.KBLK ? p.KBLK : S;
+                p.csize = S < 2 ? 1 : S;
+            }
+        }
+        int G = i8::sms();
+        if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
+        G = G < 1 ? 1 : G;
+        p.G = int(p.U < G ? p.U : G);
+        const bool pdl = true;  // the planes kernel precedes it in the stream
+        cudaError_t e = nt == 16 ? i8::launch_nt<16>(p, st, pdl)
+                      : nt == 32 ? i8::launch_nt<32>(p, st, pdl)
+                                 : i8::launch_nt<64>(p, st, pdl);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace rtnq_b200

@@ -244,7 +244,7 @@ def test_linear_llama_shapes_vs_dequant_reference(name, bits):
     g = 128 if bits == 4 else 1 << (k - 1).bit_length()  # W8 per-channel (configs[2])
     w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
     q = rq.quantize_pack(w, bits, g, ragged=k % g != 0)
-    wd = rq.dequantize(q.codes, rq.layout(rq.NATIVE), bits, n, k, g, q.scales, rq.F16,
+    wd = rq.dequantize(q.codes, rq.layout(q.layout), bits, n, k, g, q.scales, rq.F16,
                        rq.SCALES_NATIVE, torch.float32)
     for m in (1, 4, 16):
         a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
@@ -271,3 +271,24 @@ def test_cluster_split_k_matches_stream_k(oracle, monkeypatch, n, k, bits, g, m)
     if n * k <= 4096 * 4096:
         ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
         assert rel_frob(o1.cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("n,k,m", [(4096, 4096, 1), (4096, 14336, 16), (6144, 4096, 64),
+                                   (1000, 2048, 5), (200, 96, 33), (28672, 4096, 16)])
+def test_w8_per_channel_int8_path(oracle, n, k, m):
+    """W8 per-channel runs tcgen05 kind::i8 over the row-major codes with exact int8
+    activation planes; against the f64 oracle (small) or an f64 GEMM over the exactly
+    dequantized weights (large)."""
+    g = 1 << (k - 1).bit_length()
+    gen = torch.Generator(device="cuda").manual_seed(n + k + m)
+    w = ((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+    q = rq.quantize_pack(w, 8, g, ragged=k % g != 0)
+    assert q.layout == rq.NATIVE_I8
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1, generator=gen).to(torch.bfloat16)
+    a[0, : k // 3] *= 1e-3  # a wide dynamic range inside one token
+    out = rq.linear(a, q, out_dtype=torch.float32)
+    assert torch.equal(out, rq.linear(a, q, out_dtype=torch.float32))  # deterministic
+    wd = rq.dequantize(q.codes, rq.layout(rq.NATIVE_I8), 8, n, k, g, q.scales, rq.F16,
+                       rq.SCALES_NATIVE, torch.float32)
+    ref = a.double() @ wd.double().t()
+    assert ((out.double() - ref).norm() / ref.norm()).item() <= TOL
