@@ -143,7 +143,8 @@ __host__ __device__ __forceinline__ bool native_coords(int bits, int64_t rows, i
 // Native int8-MMA layout (RTNQ_NATIVE_I8): 128-row x 128-code tiles, row-blocks
 // outer and k-tiles inner (a row-block is one contiguous run along K), each tile stored
 // exactly as a 128-byte-swizzled UMMA K-major operand: code (r, k) of a tile sits at
-// r * 128 + ((k / 16) ^ (r % 8)) * 16 + k % 16.  Padding (rows to 128, K to 128) is zero.
+// r * 128 + ((k / 16) ^ (r % 8)) * 16 + k % 16.  Codes are two's-complement bytes (code_at_slot);
+// padding (rows to 128, K to 128) is code 0.
 constexpr int kI8Tile = 128;
 __host__ __device__ __forceinline__ int64_t i8_slot(int64_t cols, int64_t r, int64_t c) {
     const int64_t kt = (cols + kI8Tile - 1) / kI8Tile;
@@ -199,11 +200,16 @@ __host__ __device__ __forceinline__ int64_t layout_slots_of(const Layout& L, int
     return ((rows + L.tr - 1) / L.tr * L.tr) * ((cols + L.tc - 1) / L.tc * L.tc);
 }
 
-// Signed code at a storage slot (offset-binary, packing.cpp:19-30).
-__device__ __forceinline__ int code_at_slot(const uint8_t* data, int bits, int64_t slot) {
-    if (bits == 8) return int(data[slot]) - 128;
+// Signed code at a storage slot (offset-binary, packing.cpp:19-30).  RTNQ_NATIVE_I8 stores the
+// 8-bit code as a two's-complement byte instead (the s8 operand of the int8 MMA, no offset).
+__device__ __forceinline__ int code_at_slot(const uint8_t* data, int bits, int64_t slot,
+                                            int kind = RTNQ_ROW_MAJOR) {
+    if (bits == 8) return kind == RTNQ_NATIVE_I8 ? int(int8_t(data[slot])) : int(data[slot]) - 128;
     const uint8_t b = data[slot >> 1];
     return int((slot & 1) ? (b >> 4) : (b & 0x0F)) - 8;
+}
+__device__ __forceinline__ uint8_t code_byte8(int code, int kind) {
+    return kind == RTNQ_NATIVE_I8 ? uint8_t(int8_t(code)) : uint8_t(code + 128);
 }
 
 // Native scale order: per 128-row row-block, [group][row] with the row count

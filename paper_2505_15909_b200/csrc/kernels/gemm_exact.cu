@@ -35,7 +35,7 @@ __global__ void gemm_fused_exact_kernel(const float* __restrict__ a, int64_t m, 
         float block = 0.0f;
         for (int64_t kk = k0; kk < k1; ++kk) {
             const int64_t slot = inter ? base + kk * L.tr : layout_slot(L, bits, n, k, j, kk);
-            block = __fadd_rn(block, __fmul_rn(arow[kk], float(code_at_slot(codes, bits, slot))));
+            block = __fadd_rn(block, __fmul_rn(arow[kk], float(code_at_slot(codes, bits, slot, L.kind))));
         }
         acc = __fadd_rn(acc, __fmul_rn(srow[q], block));
     }
@@ -70,7 +70,7 @@ __global__ void gemm_oracle_kernel(const float* __restrict__ a, int64_t m, int64
     const int64_t i = e / n, j = e % n;
     double acc = 0.0;
     for (int64_t kk = 0; kk < k; ++kk) {
-        const int code = code_at_slot(codes, bits, layout_slot(L, bits, n, k, j, kk));
+        const int code = code_at_slot(codes, bits, layout_slot(L, bits, n, k, j, kk), L.kind);
         const double wv = __dmul_rn(double(code), double(scales[j * gpr + kk / g]));
         acc = __dadd_rn(acc, __dmul_rn(double(a[i * k + kk]), wv));
     }

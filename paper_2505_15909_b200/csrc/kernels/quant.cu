@@ -68,7 +68,7 @@ struct CodeSource {
 __device__ __forceinline__ int source_code(const CodeSource& S, int bits, int64_t rows,
                                            int64_t cols, int64_t r, int64_t c) {
     if (S.logical) return S.logical[r * cols + c];
-    return code_at_slot(S.packed, bits, layout_slot(S.src_l, bits, rows, cols, r, c));
+    return code_at_slot(S.packed, bits, layout_slot(S.src_l, bits, rows, cols, r, c), S.src_l.kind);
 }
 
 // One thread per output byte: gathers its 1 (8-bit) or 2 (4-bit) slots,
@@ -81,7 +81,7 @@ __global__ void encode_layout_kernel(CodeSource S, Layout dst, int bits, int64_t
         if (bits == 8) {
             const int code = layout_coords(dst, bits, rows, cols, b, &r, &c)
                                  ? source_code(S, bits, rows, cols, r, c) : 0;
-            out[b] = uint8_t(code + 128);
+            out[b] = code_byte8(code, dst.kind);
         } else {
             const int64_t nslots = layout_slots_of(dst, bits, rows, cols);
             uint32_t v = 0;
@@ -108,7 +108,7 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ codes, Layout L, int 
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = i / cols, c = i % cols;
-        const int code = code_at_slot(codes, bits, layout_slot(L, bits, rows, cols, r, c));
+        const int code = code_at_slot(codes, bits, layout_slot(L, bits, rows, cols, r, c), L.kind);
         const float s = load_scale(scales, sdtype, sorder, rows, gpr, r, c / g);
         store_elem(out, odtype, i, __fmul_rn(float(code), s));
     }
@@ -140,7 +140,7 @@ __global__ void decode_kernel(const uint8_t* __restrict__ src, Layout L, int bit
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = i / cols, c = i % cols;
-        out[i] = int8_t(code_at_slot(src, bits, layout_slot(L, bits, rows, cols, r, c)));
+        out[i] = int8_t(code_at_slot(src, bits, layout_slot(L, bits, rows, cols, r, c), L.kind));
     }
 }
 

@@ -2,11 +2,11 @@
 //
 // out[m][n] = S[n] * sum_k a[m][k] * code[n][k]        (gemm.hpp:18-27, one group per row)
 //
-// The 8-bit codes need no dequantization at all.  They are the reference's offset-binary
-// bytes (u = c + 128, packing.cpp:19-22) in the RTNQ_NATIVE_I8 layout (common.cuh): 16 KiB
-// tiles of 128 rows x 128 codes, contiguous and pre-swizzled.  One bulk copy moves a tile
-// into 1024-aligned shared memory, where it already is the 128-byte-swizzled K-major u8 A
-// operand of the tensor core.
+// The 8-bit codes need no dequantization at all.  The RTNQ_NATIVE_I8 layout (common.cuh)
+// holds the signed codes c (the reference's offset-binary byte u = c + 128, packing.cpp:19-22,
+// minus the offset) as two's-complement bytes in 16 KiB tiles of 128 rows x 128 codes,
+// contiguous and pre-swizzled.  One bulk copy moves a tile into 1024-aligned shared memory,
+// where it already is the 128-byte-swizzled K-major s8 A operand of the tensor core.
 //
 // The bf16/f16 activations become three exact int8 planes, done once per call by
 // act_planes_kernel:
@@ -16,9 +16,8 @@
 // the s8 B operand: N = 3 * tokens.
 //
 // The int32 accumulators are exact.  They run over a CTA's whole K range in TMEM; the
-// scale S[n] is per row, so it is applied once at the end.  The offset is removed with
-// per-plane prefix sums of the activations:
-//   sum_k u*P = sum_k c*P + 128 * sum_k P.
+// scale S[n] is per row, so it is applied once at the end:
+//   out = S[n] * 2^s * (D0 + D1 / 2^7 + D2 / 2^14).
 //
 // Warp roles: warp 0 is the TMA producer, warp 1 the single-thread MMA issuer, and
 // warps 4-7 the epilogue (TMEM lane quadrants).  Work is partitioned with stream-K or,
@@ -45,12 +44,12 @@ struct Params {
     const uint8_t* codes;  // RTNQ_NATIVE_I8: 16 KiB pre-swizzled 128 x 128 tiles, row-block major
     const uint16_t* scales;  // f16 per row
     const int32_t* texp;     // [M] token exponents s
-    const int32_t* pre;      // [3][M][KBLK + 1] prefix sums of each plane over 64-code blocks
     void* out;
     float* partials;
     int* counters;
     int64_t N, K;
     int M, Mtot, m0, NB, KBLK, U, G, csize, out_dtype;
+    int pf;     // L2 prefetch distance in tiles (0 = off)
     int debug;  // profiling: 4 = no MMA issued, 2 = no loads (arrive only)
 };
 
@@ -126,6 +125,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 }
 // The unit sequence of a CTA: runs of <= 2 k-blocks inside one row-block and one 128-code
 // block, tracked incrementally (no division on the issue path).
+template <int SPAN>  // k-blocks per stage (2 per 16 KiB tile)
 struct Cursor {
     int u, u1, b, kb, KBLK;
     __device__ Cursor(int u0, int u1_, int KBLK_) : u(u0), u1(u1_), KBLK(KBLK_) {
@@ -134,7 +134,7 @@ struct Cursor {
     }
     __device__ bool more() const { return u < u1; }
     __device__ int chunk() const {
-        const int left_seg = KBLK - kb, left = u1 - u, cap = 2 - (kb & 1);
+        const int left_seg = KBLK - kb, left = u1 - u, cap = SPAN - (kb & (SPAN - 1));
         const int n = left_seg < left ? left_seg : left;
         return n < cap ? n : cap;
     }
@@ -174,6 +174,12 @@ __device__ __forceinline__ void elect_bulk(void* dst, const void* src, uint64_t*
         "l"(src), "r"(bytes), "r"(su32(b))
         : "memory");
 }
+__device__ __forceinline__ void elect_prefetch(const void* src, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.prefetch.L2.global [%0], %1;\n}\n" ::"l"(src), "r"(bytes)
+        : "memory");
+}
 __device__ __forceinline__ void elect_tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
                                             uint64_t* b, uint32_t bytes) {
     asm volatile(
@@ -185,25 +191,55 @@ __device__ __forceinline__ void elect_tma3d(void* dst, const CUtensorMap* m, int
         : "memory");
 }
 
+// expect_tx once for all boxes of a stage, then the box loads (no further arrivals)
+__device__ __forceinline__ void elect_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(su32(b)), "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void elect_tma3d_tx(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                               uint64_t* b) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];\n}\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(b))
+        : "memory");
+}
+
 __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
     return int(((u + 1) * G - 1) / U);
 }
 
 template <int NT>
 struct Geo {
-    static constexpr int CODE_BYTES = kRows * kUnit;             // 16 KiB
-    static constexpr int PLANE_BYTES = 3 * NT * kUnit;           // 6 / 12 / 24 KiB
-    static constexpr int STAGE_BYTES = CODE_BYTES + PLANE_BYTES;  // multiple of 1 KiB
+    static constexpr int CODE_BYTES = kRows * kUnit;             // 16 KiB tile
+    static constexpr int PLANE_BYTES = 3 * NT * kUnit;           // 6 / 12 / 24 KiB per tile
+    // Two tiles per stage (one barrier round trip per 32 KiB of codes): a CTA's TMA ring
+    // streams markedly faster with >= 32 KiB per stage than with 16 KiB (scratch/stream_bench3).
+    static constexpr int TPS = NT <= 32 ? 2 : 1;                 // tiles per stage
+    static constexpr int SPAN = 2 * TPS;                         // k-blocks per stage
+    static constexpr int PLANE_OFF = TPS * CODE_BYTES;
+    static constexpr int STAGE_BYTES = TPS * (CODE_BYTES + PLANE_BYTES);  // multiple of 1 KiB
     static constexpr int STAGES_FIT = (208 * 1024) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-    static constexpr int COR_OFF = BAR_OFF + 1024;                // [3][NT] corrections + [NT] exps
-    static constexpr int SMEM = COR_OFF + 4 * NT * 4 + 1024;
+    static constexpr int SMEM = BAR_OFF + 1024 + 1024;
     static constexpr int DN = 3 * NT;                             // accumulator columns
+    // cluster split-K: the leader's stage area holds csize - 1 pushed partials
+    static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (NT * kRows * 4);
+    static constexpr int MAXC = MAXC_FIT > 8 ? 8 : MAXC_FIT;
     static_assert(STAGES >= 3, "");
 };
 
-__device__ unsigned long long g_i8_dbg[1024 * 8];  // profiling (debug & 32)
+__device__ unsigned long long g_i8_dbg[1024 * 16];  // profiling (debug & 32; & 64: globaltimer stamps)
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_constant__ Params p) {
@@ -216,9 +252,11 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     uint64_t* empty = full + STAGES;                                  // [STAGES]
     uint64_t* dfull = empty + STAGES;                                 // [2]
     uint64_t* dempty = dfull + 2;                                     // [2]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
-    volatile int* flag = reinterpret_cast<volatile int*>(tslot + 1);
+    uint64_t* go = dempty + 2;      // cluster split-K: the leader is ready for partials
+    uint64_t* rfull = dempty + 3;   // cluster split-K: all partials landed in the leader
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
+    if ((p.debug & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 5] = gtime();
 
     int u0, u1;
     if (p.csize > 1) {
@@ -232,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
         for (int i = 0; i < 2; ++i) mbar_init(&dfull[i], 1), mbar_init(&dempty[i], 4);
+        mbar_init(go, 1), mbar_init(rfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -242,12 +281,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     fence_before();
     __syncthreads();
     fence_after();
+    // cluster peers touch each other's barriers only at the end: arrive now, wait there
+    if (p.csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const uint32_t tmem = *tslot;
     asm volatile("griddepcontrol.launch_dependents;");
 
-    // units: runs of <= 2 k-blocks inside one row-block and one 128-code block
+    // units: runs of <= SPAN k-blocks inside one row-block and one SPAN-aligned k-range
     auto chunk = [&](int u, int kb) {
-        const int left_seg = p.KBLK - kb, left = u1 - u, cap = 2 - (kb & 1);
+        const int left_seg = p.KBLK - kb, left = u1 - u, cap = GG::SPAN - (kb & (GG::SPAN - 1));
         const int n = left_seg < left ? left_seg : left;
         return n < cap ? n : cap;
     };
@@ -256,11 +297,16 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
         // ===================== producers: warp 0 codes, warp 2 activation planes ===========
         // Warp-uniform loops (one elected lane issues), incremental row-block / k-block.
         const bool codes = warp == 0;
-        Cursor cu(u0, u1, p.KBLK);
+        Cursor<GG::SPAN> cu(u0, u1, p.KBLK);
         int s = 0;
         uint32_t ph = 0;
         const long long t0 = clock64();
         long long tw = 0;
+        // The CTA's tiles are one contiguous run of the NATIVE_I8 array: keep an L2 prefetch
+        // window of p.pf tiles ahead of the smem ring (more bytes in flight than the ring holds).
+        const int64_t kt = (p.KBLK + 1) >> 1;
+        const int64_t t_last = u1 > u0 ? int64_t((u1 - 1) / p.KBLK) * kt + ((u1 - 1) % p.KBLK >> 1) : -1;
+        int64_t pf_next = int64_t(cu.b) * kt + (cu.kb >> 1);
         if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes come from the previous kernel
         for (int i = 0; cu.more(); ++i) {
             const int n = cu.chunk();
@@ -270,16 +316,27 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                 tw += clock64() - a0;
             }
             uint8_t* st = smem + s * GG::STAGE_BYTES;
-            // a half unit (one 64-code k-block) still loads a full 128-code box: the other
-            // half belongs to a later unit or is out of bounds (zeros); the MMA uses one half
+            // the tiles this unit touches (1 or TPS, same row-block): tile t goes to stage slot
+            // t % TPS. A half tile (one 64-code k-block) still loads the whole tile and its
+            // 128-code planes box; the MMA uses one half.
+            const int ta = cu.kb >> 1, tb = (cu.kb + n - 1) >> 1;
+            const int slot0 = ta & (GG::TPS - 1);
             if (p.debug & 2) {
                 elect_arrive(&full[s]);
-            } else if (codes) {  // one contiguous, pre-swizzled 16 KiB tile
-                const int64_t tile = int64_t(cu.b) * ((p.KBLK + 1) >> 1) + (cu.kb >> 1);
-                elect_bulk(st, p.codes + tile * GG::CODE_BYTES, &full[s], GG::CODE_BYTES);
+            } else if (codes) {  // contiguous, pre-swizzled 16 KiB tiles
+                const int64_t tile = int64_t(cu.b) * kt + ta;
+                if (p.pf > 0 && pf_next <= t_last && pf_next <= tile + p.pf) {
+                    const int64_t nt4 = t_last - pf_next + 1 < 4 ? t_last - pf_next + 1 : 4;
+                    elect_prefetch(p.codes + pf_next * GG::CODE_BYTES, uint32_t(nt4 * GG::CODE_BYTES));
+                    pf_next += nt4;
+                }
+                elect_bulk(st + slot0 * GG::CODE_BYTES, p.codes + tile * GG::CODE_BYTES, &full[s],
+                           uint32_t(tb - ta + 1) * GG::CODE_BYTES);
             } else {
-                elect_tma3d(st + GG::CODE_BYTES, &p.tmap_p, (cu.kb & ~1) * kKB, p.m0, 0, &full[s],
-                            GG::PLANE_BYTES);
+                elect_expect(&full[s], uint32_t(tb - ta + 1) * GG::PLANE_BYTES);
+                for (int t = ta; t <= tb; ++t)
+                    elect_tma3d_tx(st + GG::PLANE_OFF + (t & (GG::TPS - 1)) * GG::PLANE_BYTES, &p.tmap_p,
+                                   t * kUnit, p.m0, 0, &full[s]);
             }
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
@@ -288,15 +345,16 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             g_i8_dbg[c * 8 + 0] = clock64() - t0;
             g_i8_dbg[c * 8 + 1] = tw;
         }
+        if ((p.debug & 64) && lane == 0 && codes) g_i8_dbg[c * 16 + 0] = gtime();
     } else if (warp == 1) {
         // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
-        // D s32, A u8 (offset-binary codes), B s8 (planes), M = 128, N = 3 * NT
-        constexpr uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) |
+        // D s32, A s8 (codes), B s8 (planes), M = 128, N = 3 * NT
+        constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                    (uint32_t(DN >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
         constexpr uint64_t kHi = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
                                  (2ull << 61);  // K-major SWIZZLE_128B, SBO = 1024
         const uint32_t lo0 = su32(smem) >> 4;   // descriptor address field of stage 0
-        Cursor cu(u0, u1, p.KBLK);
+        Cursor<GG::SPAN> cu(u0, u1, p.KBLK);
         int s = 0, db = 0, seg = 0;
         uint32_t ph = 0, lo = lo0;
         bool first = true;
@@ -313,18 +371,19 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             mbar_wait(&full[s], ph);
             fence_after();
             const long long a1 = clock64();
+            if ((p.debug & 64) && lane == 0 && first && seg == 0) g_i8_dbg[c * 16 + 6] = gtime();
             tw += a1 - a0;
-            const uint32_t alo = lo + ((cu.kb & 1) ? 4u : 0u);  // second 64-code half: +64 B
-            const uint32_t blo = alo + (GG::CODE_BYTES >> 4);
             const uint32_t d = tmem + db * DN;
             if (!(p.debug & 4)) {
-                if (n == 2) {
-                    mma_i8_elect(d, kHi | alo, kHi | blo, idesc, first ? 0u : 1u);
-                    mma_i8_elect(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
-                    mma_i8_elect(d, kHi | (alo + 4), kHi | (blo + 4), idesc, 1u);
-                    mma_i8_elect(d, kHi | (alo + 6), kHi | (blo + 6), idesc, 1u);
-                } else {
-                    mma_i8_elect(d, kHi | alo, kHi | blo, idesc, first ? 0u : 1u);
+                // k-block kb: tile slot (kb >> 1) % TPS, second 64-code half at +64 B
+                for (int j = 0; j < n; ++j) {
+                    const int kb = cu.kb + j;
+                    const uint32_t alo = lo + uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::CODE_BYTES >> 4)) +
+                                         ((kb & 1) ? 4u : 0u);
+                    const uint32_t blo = lo + uint32_t(GG::PLANE_OFF >> 4) +
+                                         uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::PLANE_BYTES >> 4)) +
+                                         ((kb & 1) ? 4u : 0u);
+                    mma_i8_elect(d, kHi | alo, kHi | blo, idesc, (first && j == 0) ? 0u : 1u);
                     mma_i8_elect(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
                 }
             }
@@ -346,12 +405,16 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             g_i8_dbg[c * 8 + 3] = tw;
             g_i8_dbg[c * 8 + 4] = ti;
         }
+        if ((p.debug & 64) && lane == 0) g_i8_dbg[c * 16 + 1] = gtime();
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
         const uint32_t lane_base = uint32_t(q * 32) << 16;
-        const int kb1 = p.KBLK + 1;
         int db = 0, seg = 0, u = u0;
+        __shared__ float pow_s[NT];  // 2^s per token (s >= -126: a normal float)
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // texp comes from the planes kernel
+        for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
         while (u < u1) {
             // walk to this segment's end
             const int b = u / p.KBLK, kb0 = u - b * p.KBLK;
@@ -362,137 +425,153 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                 if (kbe == p.KBLK || uu == u1) break;
             }
             const bool sole = kb0 == 0 && kbe == p.KBLK;
-            // per-token bias corrections and exponents of this segment, loaded once by the
-            // 128 epilogue threads (they are the same for every row)
-            int32_t* cor_s = reinterpret_cast<int32_t*>(smem + GG::COR_OFF);
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous segment done reading
-            for (int x = et; x < 4 * NT; x += 128) {
-                const int pl = x / NT, t = x % NT;
-                int32_t v = 0;
-                if (t < p.M) {
-                    if (pl < 3) {
-                        const int32_t* pr = p.pre + (int64_t(pl) * p.Mtot + p.m0 + t) * kb1;
-                        v = 128 * (__ldg(pr + kbe) - __ldg(pr + kb0));
-                    } else {
-                        v = __ldg(p.texp + p.m0 + t);
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 8] = gtime();
+            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
+            const float srow = row < rows ? __half2float(__ushort_as_half(__ldg(p.scales + int64_t(b) * kRows + row))) : 0.0f;
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 9] = gtime();
+            // Stream-K: the row-block's owner is the CTA holding its first k-block (for that
+            // CTA it is the last segment, finished last); the other contributors hand over
+            // partials from their first segment, usually long before. The owner collects them
+            // while its own MMAs drain.
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 9] = gtime();
+            const bool split = p.csize == 1 && !sole;
+            const int c_first = split ? cta_of(int64_t(b) * p.KBLK, p.U, p.G) : c;
+            const int c_last = split ? cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G) : c;
+            const bool owner = split && c == c_first;
+            float psum[NT];
+#pragma unroll
+            for (int m = 0; m < NT; ++m) psum[m] = 0.0f;
+            if (owner) {
+                if (et == 0) {
+                    const int want = c_last - c_first;
+                    int got;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(p.counters + b) : "memory");
+                    } while (got < want);
+                    p.counters[b] = 0;  // ready for the next launch (stream-ordered after this one)
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                for (int cc = c_first + 1; cc <= c_last; ++cc) {  // fixed order: deterministic
+                    const float4* src = reinterpret_cast<const float4*>(p.partials + (int64_t(cc) * kRows + row) * NT);
+#pragma unroll
+                    for (int j = 0; j < NT / 4; ++j) {
+                        const float4 x = __ldcg(src + j);
+                        psum[4 * j] += x.x, psum[4 * j + 1] += x.y, psum[4 * j + 2] += x.z, psum[4 * j + 3] += x.w;
                     }
                 }
-                cor_s[x] = v;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 2] = gtime();
             mbar_wait(&dfull[db], uint32_t(seg >> 1) & 1u);
             fence_after();
-            float acc[NT];
-            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
-            const float srow = row < rows ? __half2float(__ushort_as_half(p.scales[int64_t(b) * kRows + row])) : 0.0f;
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 3] = gtime();
+            float acc[NT], pw[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) pw[t] = pow_s[t];
+            const long long ck0 = clock64();
+            long long ck1 = 0;
 #pragma unroll
             for (int j = 0; j < NT; j += 16) {
                 uint32_t d0[16], d1[16], d2[16];
-                ld16(tmem + lane_base + db * DN + j, d0);
-                ld16(tmem + lane_base + db * DN + NT + j, d1);
-                ld16(tmem + lane_base + db * DN + 2 * NT + j, d2);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (p.debug & 16) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) d0[e] = d1[e] = d2[e] = uint32_t(e + row);
+                } else {
+                    ld16(tmem + lane_base + db * DN + j, d0);
+                    ld16(tmem + lane_base + db * DN + NT + j, d1);
+                    ld16(tmem + lane_base + db * DN + 2 * NT + j, d2);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
+                if (j == 0) ck1 = clock64();
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                    const int t = j + e;
-                    float v = 0.0f;
-                    if (t < p.M) {
-                        // remove the offset-binary bias: sum u*P = sum c*P + 128 * sum P
-                        const float x = float(int32_t(d0[e]) - cor_s[t]) +
-                                        float(int32_t(d1[e]) - cor_s[NT + t]) * 0.0078125f +
-                                        float(int32_t(d2[e]) - cor_s[2 * NT + t]) * 6.103515625e-05f;
-                        v = ldexpf(x, cor_s[3 * NT + t]) * srow;
-                    }
-                    acc[t] = v;
+                    // branch-free: pow_s is 0 for the padding tokens t >= M
+                    const float x = float(int32_t(d0[e])) + float(int32_t(d1[e])) * 0.0078125f +
+                                    float(int32_t(d2[e])) * 6.103515625e-05f;
+                    acc[j + e] = x * pw[j + e] * srow;
                 }
             }
+            const long long ck2 = clock64();
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&dempty[db]);
+            if ((p.debug & 64) && et == 0) {
+                g_i8_dbg[c * 16 + 12] = ck1 - ck0;
+                g_i8_dbg[c * 16 + 13] = ck2 - ck1;
+                g_i8_dbg[c * 16 + 14] = clock64() - ck2;
+            }
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 10] = gtime();
             const int64_t n0 = int64_t(b) * kRows;
             if (p.csize > 1) {
-                float* red = reinterpret_cast<float*>(smem);  // stages are idle by now
-#pragma unroll
-                for (int m = 0; m < NT; ++m) red[m * kRows + row] = acc[m];
-            } else if (sole) {
-                if (row < rows)
-#pragma unroll
-                    for (int m = 0; m < NT; ++m)
-                        if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
-            } else {
-                const int slot = 2 * c + (b == u0 / p.KBLK ? 0 : 1);
-                float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(slot) * kRows + row) * NT);
-#pragma unroll
-                for (int j = 0; j < NT / 4; ++j)
-                    mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
-                const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
-                if (et == 0) {
-                    int prev;
-                    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
-                                 : "=r"(prev)
-                                 : "l"(p.counters + b)
-                                 : "memory");
-                    const int last = prev == c_last - c_first;
-                    if (last) p.counters[b] = 0;
-                    *flag = last;
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (*flag) {
-                    float sum[NT];
-#pragma unroll
-                    for (int m = 0; m < NT; ++m) sum[m] = 0.0f;
-                    const int first_bit = int(int64_t(c_first) * p.U / p.G) / p.KBLK == b ? 0 : 1;
-                    for (int cc = c_first; cc <= c_last; ++cc) {  // fixed order: deterministic
-                        const int cs = 2 * cc + (cc == c_first ? first_bit : 0);
-                        const float4* src =
-                            reinterpret_cast<const float4*>(p.partials + (int64_t(cs) * kRows + row) * NT);
+                // Cluster split-K (one segment per CTA): the leader (rank 0) opens its idle
+                // stage area once its own MMAs are done; the peers push their partials there
+                // with st.async, completing on the leader's rfull barrier.
+                const int rank = c % p.csize;
+                constexpr uint32_t kSlot = uint32_t(NT) * kRows * 4;
+                asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+                if (rank == 0) {
+                    if (et == 0) {
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull)),
+                                     "r"(uint32_t(p.csize - 1) * kSlot)
+                                     : "memory");
+                        for (int r = 1; r < p.csize; ++r) {
+                            uint32_t ra;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(go)), "r"(r));
+                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+                        }
+                    }
+                    mbar_wait(rfull, 0);
+                    const float4* red = reinterpret_cast<const float4*>(smem);
+                    for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
 #pragma unroll
                         for (int j = 0; j < NT / 4; ++j) {
-                            const float4 x = __ldcg(src + j);
-                            sum[4 * j] += x.x, sum[4 * j + 1] += x.y, sum[4 * j + 2] += x.z, sum[4 * j + 3] += x.w;
+                            const float4 x = red[((r - 1) * kRows + row) * (NT / 4) + j];
+                            acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
                         }
                     }
                     if (row < rows)
 #pragma unroll
                         for (int m = 0; m < NT; ++m)
-                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, sum[m]);
+                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                } else {
+                    mbar_wait(go, 0);
+                    uint32_t dst, rb;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst)
+                                 : "r"(su32(smem) + uint32_t(((rank - 1) * kRows + row) * NT * 4)));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(su32(rfull)));
+#pragma unroll
+                    for (int j = 0; j < NT / 4; ++j)
+                        asm volatile(
+                            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                                dst + 16u * j),
+                            "f"(acc[4 * j]), "f"(acc[4 * j + 1]), "f"(acc[4 * j + 2]), "f"(acc[4 * j + 3]), "r"(rb)
+                            : "memory");
+                }
+            } else if (!split || owner) {
+                if (row < rows)
+#pragma unroll
+                    for (int m = 0; m < NT; ++m)
+                        if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m] + psum[m]);
+            } else {  // contributor: this is the CTA's first segment, partial slot c
+                float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
+#pragma unroll
+                for (int j = 0; j < NT / 4; ++j)
+                    mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (et == 0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + b) : "memory");
                 }
             }
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 11] = gtime();
             u = uu;
             db ^= 1;
             ++seg;
         }
     }
+    if ((p.debug & 64) && threadIdx.x == kEpi0 * 32) g_i8_dbg[c * 16 + 4] = gtime();
     fence_before();
     __syncthreads();
-    if (p.csize > 1) {
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        if (c % p.csize == 0 && warp >= kEpi0) {
-            const int row = (warp & 3) * 32 + lane, b = c / p.csize;
-            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
-            float sum[NT];
-#pragma unroll
-            for (int m = 0; m < NT; ++m) sum[m] = 0.0f;
-            const uint32_t red = su32(smem);
-            for (int r = 0; r < p.csize; ++r) {  // rank order: deterministic
-                uint32_t rb;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(red), "r"(r));
-#pragma unroll
-                for (int m = 0; m < NT; ++m) {
-                    float v;
-                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(rb + uint32_t((m * kRows + row) * 4)));
-                    sum[m] += v;
-                }
-            }
-            if (row < rows)
-#pragma unroll
-                for (int m = 0; m < NT; ++m)
-                    if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + int64_t(b) * kRows + row, sum[m]);
-        }
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    }
+    if ((p.debug & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 7] = gtime();
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -500,82 +579,101 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
 }
 
 // ---- activation planes ------------------------------------------------------------------
-// One CTA per token: s = exponent(max|a|) - 5 so |a| / 2^s < 64; three exact int8 planes;
-// per-64-code-block prefix sums of each plane (for the offset-binary correction).
-template <int AT>
-__global__ void act_planes_kernel(const void* __restrict__ a, int K, int M, int8_t* __restrict__ planes,
-                                  int32_t* __restrict__ texp, int32_t* __restrict__ bsum, int kblk) {
-    // grid (M, ceil(kblk / 8)): each CTA re-reduces its token's max (the row is L2-resident),
-    // then its warps own one 64-code block each: planes + per-block plane sums
-    __shared__ float wmax[8];
-    const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto ld = [&](int k) -> float {
-        if constexpr (AT == RTNQ_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(a)[int64_t(t) * K + k]);
-        else return __half2float(static_cast<const __half*>(a)[int64_t(t) * K + k]);
+// One CTA per token (PDL secondary of whatever produced the activations):
+//   s = exponent(max|a|) - 6 so |a| / 2^s < 64; three exact int8 planes.
+// 16-byte loads of 8 activations; up to kVPT vectors per thread stay in registers between
+// the max and the split (one pass over memory for K <= 512 * 8 * kVPT), longer rows reload.
+constexpr int kPlaneThreads = 512, kVPT = 4;
+template <int AT, bool VEC>
+__global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* __restrict__ a, int K, int M,
+                                                                   int8_t* __restrict__ planes,
+                                                                   int32_t* __restrict__ texp, int stamp) {
+    __shared__ float wmax[kPlaneThreads / 32];
+    if (stamp && threadIdx.x == 0 && blockIdx.x == 0) g_i8_dbg[1023 * 16] = gtime();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (stamp && threadIdx.x == 0 && blockIdx.x == 0) g_i8_dbg[1023 * 16 + 1] = gtime();
+    const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint16_t* rowp = static_cast<const uint16_t*>(a) + int64_t(t) * K;
+    const int nv = K / 8;
+    auto load4 = [&](int v) -> uint4 {
+        if constexpr (VEC) return __ldg(reinterpret_cast<const uint4*>(rowp) + v);
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = uint32_t(rowp[v * 8 + 2 * i]) | (uint32_t(rowp[v * 8 + 2 * i + 1]) << 16);
+        return make_uint4(w[0], w[1], w[2], w[3]);
     };
+    auto cvt = [](uint32_t h) -> float {
+        if constexpr (AT == RTNQ_BF16) return __uint_as_float(h << 16);
+        else return __half2float(__ushort_as_half(static_cast<unsigned short>(h)));
+    };
+    auto vmax = [&](const uint4& q, float m) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m = fmaxf(m, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+        return m;
+    };
+    uint4 keep[kVPT];
     float mx = 0.0f;
-    for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(ld(k)));
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+        const int v = tid + j * kPlaneThreads;
+        keep[j] = v < nv ? load4(v) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) mx = vmax(keep[j], mx);
+    for (int v = tid + kVPT * kPlaneThreads; v < nv; v += kPlaneThreads) mx = vmax(load4(v), mx);
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) wmax[warp] = mx;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        float m = 0.0f;
-        for (int i = 0; i < int(blockDim.x / 32); ++i) m = fmaxf(m, wmax[i]);
-        wmax[0] = m;
-    }
-    __syncthreads();
-    const float amax = wmax[0];
+    float amax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kPlaneThreads / 32; ++i) amax = fmaxf(amax, wmax[i]);
     int e = 0;
     if (amax > 0.0f) frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
-    const int s = e - 6;                 // |a| / 2^s < 64
-    if (threadIdx.x == 0 && blockIdx.y == 0) texp[t] = s;
-    // planes and per-block sums (a warp per 64-code block, 2 codes per lane)
-    for (int blk = blockIdx.y * 8 + warp; blk < kblk && blk < (int(blockIdx.y) + 1) * 8; blk += 8) {
-        int32_t ps[3] = {0, 0, 0};
+    const int s = max(e - 6, -126);      // |a| / 2^s < 64; 2^s stays a normal float
+    if (tid == 0) texp[t] = s;
+    auto split = [&](const uint4& q, int v) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int k = blk * 64 + h * 32 + lane;
-            int p0 = 0, p1 = 0, p2 = 0;
-            if (k < K) {
-                const float x = ldexpf(ld(k), -s);  // exact
-                const float r0 = rintf(x);
-                const float y1 = (x - r0) * 128.0f;  // exact
-                const float r1 = rintf(y1);
-                const float r2 = rintf((y1 - r1) * 128.0f);
-                p0 = int(r0), p1 = int(r1), p2 = int(r2);
-                planes[(int64_t(0) * M + t) * K + k] = int8_t(p0);
-                planes[(int64_t(1) * M + t) * K + k] = int8_t(p1);
-                planes[(int64_t(2) * M + t) * K + k] = int8_t(p2);
-            }
-            ps[0] += p0, ps[1] += p1, ps[2] += p2;
+        for (int i = 0; i < 8; ++i) {
+            const float y = ldexpf(cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu), -s);  // exact
+            const float r0 = rintf(y);
+            const float y1 = (y - r0) * 128.0f;  // exact
+            const float r1 = rintf(y1);
+            const float r2 = rintf((y1 - r1) * 128.0f);
+            pk[0][i >> 2] |= (uint32_t(int(r0)) & 0xffu) << (8 * (i & 3));
+            pk[1][i >> 2] |= (uint32_t(int(r1)) & 0xffu) << (8 * (i & 3));
+            pk[2][i >> 2] |= (uint32_t(int(r2)) & 0xffu) << (8 * (i & 3));
         }
 #pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
-            int v = ps[pl];
-            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) bsum[(int64_t(pl) * M + t) * kblk + blk] = v;
-        }
+        for (int pl = 0; pl < 3; ++pl)
+            *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
+                make_uint2(pk[pl][0], pk[pl][1]);
+    };
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+        const int v = tid + j * kPlaneThreads;
+        if (v < nv) split(keep[j], v);
     }
+    for (int v = tid + kVPT * kPlaneThreads; v < nv; v += kPlaneThreads) split(load4(v), v);
+    if (stamp && threadIdx.x == 0 && blockIdx.x == 0) g_i8_dbg[1023 * 16 + 2] = gtime();
 }
 
-// Exclusive prefix over the 64-code blocks: pre[pl][t][0..kblk] (one warp per (plane, token)).
-__global__ void plane_prefix_kernel(const int32_t* __restrict__ bsum, int32_t* __restrict__ pre,
-                                    int M, int kblk) {
-    const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (row >= 3 * M) return;
-    const int32_t* in = bsum + int64_t(row) * kblk;
-    int32_t* out = pre + int64_t(row) * (kblk + 1);
-    int32_t carry = 0;
-    if (lane == 0) out[0] = 0;
-    for (int base = 0; base < kblk; base += 32) {
-        int32_t v = base + lane < kblk ? in[base + lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {  // inclusive warp scan
-            const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
-        }
-        if (base + lane < kblk) out[base + lane + 1] = carry + v;
-        carry += __shfl_sync(0xffffffffu, v, 31);
-    }
+template <int AT, bool VEC>
+static cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, int32_t* texp, int stamp,
+                                 cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(M));
+    cfg.blockDim = dim3(kPlaneThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamp);
 }
 
 // ---- host ----------------------------------------------------------------------------------
@@ -615,6 +713,7 @@ cudaError_t launch_nt(Params p, cudaStream_t st, bool pdl) {
             return e;
         configured = true;
     }
+    if (p.csize > GG::MAXC) p.csize = GG::MAXC;
     while (p.csize > 1) {
         int& mc = max_clusters[p.csize];
         if (mc == 0) {
@@ -671,10 +770,9 @@ extern "C" int rtnq_i8_debug_read(void* host, size_t bytes) {
 static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 size_t wgemm_i8_workspace_bytes(int64_t m, int64_t n, int64_t k) {
-    const int64_t kblk = (k + 63) / 64;
+    (void)n;
     const size_t part = size_t(i8::sms()) * 2 * i8::kRows * 64 * sizeof(float);
-    return kI8Counters + align256(part) + align256(size_t(3 * m * k)) + align256(size_t(m) * 4) +
-           align256(size_t(3 * m * (kblk + 1)) * 4) + align256(size_t(3 * m * kblk) * 4);
+    return kI8Counters + align256(part) + align256(size_t(3 * m * k)) + align256(size_t(m) * 4);
 }
 
 const char* wgemm_i8_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype) {
@@ -696,22 +794,22 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     p.partials = reinterpret_cast<float*>(ws + kI8Counters);
     int8_t* planes = reinterpret_cast<int8_t*>(ws + kI8Counters + align256(part));
     int32_t* texp = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes) + align256(size_t(3 * A.m * A.k)));
-    int32_t* pre = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(texp) + align256(size_t(A.m) * 4));
-    int32_t* bsum = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(pre) +
-                                               align256(size_t(3 * A.m * (kblk + 1)) * 4));
-    // 1. activation planes (once per call): planes + block sums, then their prefix
-    const dim3 pg(unsigned(A.m), unsigned((kblk + 7) / 8));
-    if (A.a_dtype == RTNQ_BF16)
-        i8::act_planes_kernel<RTNQ_BF16><<<pg, 256, 0, st>>>(A.a, int(A.k), int(A.m), planes, texp, bsum, int(kblk));
-    else
-        i8::act_planes_kernel<RTNQ_F16><<<pg, 256, 0, st>>>(A.a, int(A.k), int(A.m), planes, texp, bsum, int(kblk));
-    i8::plane_prefix_kernel<<<unsigned((3 * A.m + 7) / 8), 256, 0, st>>>(bsum, pre, int(A.m), int(kblk));
-    if (cudaError_t e = cudaGetLastError()) return e;
+    // 1. activation planes (once per call): planes and token exponents
+    const char* dbg_env = std::getenv("RTNQ_WGEMM_DEBUG");
+    const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+    {
+        const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
+        cudaError_t e = A.a_dtype == RTNQ_BF16
+            ? (vec ? i8::launch_planes<RTNQ_BF16, true> : i8::launch_planes<RTNQ_BF16, false>)(
+                  A.a, int(A.k), int(A.m), planes, texp, dbg & 64, st)
+            : (vec ? i8::launch_planes<RTNQ_F16, true> : i8::launch_planes<RTNQ_F16, false>)(
+                  A.a, int(A.k), int(A.m), planes, texp, dbg & 64, st);
+        if (e != cudaSuccess) return e;
+    }
     // 2. the GEMM
     p.codes = A.codes;
     p.scales = A.scales;
     p.texp = texp;
-    p.pre = pre;
     p.N = A.n;
     p.K = A.k;
     p.Mtot = int(A.m);
@@ -719,7 +817,9 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     p.KBLK = int(kblk);
     p.U = p.NB * p.KBLK;
     p.out_dtype = A.out_dtype;
-    if (const char* e = std::getenv("RTNQ_WGEMM_DEBUG")) p.debug = std::atoi(e);
+    p.debug = dbg;
+    p.pf = 0;
+    if (const char* e = std::getenv("RTNQ_I8_PF")) p.pf = std::atoi(e);
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
     const int nt_max = A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
     for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {
