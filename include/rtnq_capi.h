@@ -59,7 +59,8 @@ enum { RTNQ_F32 = 0, RTNQ_F16 = 1, RTNQ_BF16 = 2 };
  * LayoutTag kinds (types.hpp:62-83); NATIVE_SM100 is the tensor-core operand
  * order of this library. */
 enum { RTNQ_ROW_MAJOR = 0, RTNQ_KERNEL_INTERLEAVED = 1, RTNQ_NATIVE_SM100 = 2,
-       RTNQ_NATIVE_I8 = 3 /* 128x128 pre-swizzled tiles: the int8-MMA operand of W8 per-channel */ };
+       RTNQ_NATIVE_I8 = 3, /* 128x128 pre-swizzled tiles: the int8-MMA operand of W8 per-channel */
+       RTNQ_NATIVE_I4 = 4  /* 128-row x 128-code nibble tiles: the int8-MMA operand of W4 group-128 */ };
 
 /* Scale orders: REF = [row][group] as in QuantTensor::scales (quant.hpp:33);
  * NATIVE = per 128-row row-block, [group][row padded to 8], so a
@@ -72,7 +73,7 @@ enum { RTNQ_PATH_FUSED = 0, RTNQ_PATH_DEQUANT_FIRST = 1, RTNQ_PATH_AUTO = 2,
        RTNQ_PATH_ORACLE = 3 };
 
 typedef struct {
-    int32_t kind;      /* RTNQ_ROW_MAJOR | RTNQ_KERNEL_INTERLEAVED | RTNQ_NATIVE_SM100 | RTNQ_NATIVE_I8 */
+    int32_t kind;      /* RTNQ_ROW_MAJOR | RTNQ_KERNEL_INTERLEAVED | RTNQ_NATIVE_SM100 | RTNQ_NATIVE_I8 | RTNQ_NATIVE_I4 */
     int32_t tile_rows; /* KERNEL_INTERLEAVED only (LayoutTag::tile_rows, default 16) */
     int32_t tile_cols; /* KERNEL_INTERLEAVED only (LayoutTag::tile_cols, default 4) */
 } rtnq_layout;

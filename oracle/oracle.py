@@ -36,6 +36,49 @@ def _build_oracle():
     subprocess.run(["make", "-s", "-C", HERE, "_build/librtnq_oracle.so"], check=True)
 
 
+# ---- the int8-MMA native layouts (numpy restatement of common.cuh i8_slot / i4_slot) ----------
+# These are the product's own tensor-core operand orders, not reference
+# formats: a fixed permutation (plus re-encoding) of the reference's logical codes.
+
+def _pad128(codes):
+    rows, cols = codes.shape
+    R, Cc = -(-rows // 128) * 128, -(-cols // 128) * 128
+    out = np.zeros((R, Cc), np.int8)
+    out[:rows, :cols] = codes
+    return out
+
+
+def encode_native_i8(codes):
+    """Signed codes -> NATIVE_I8 bytes: 128x128 tiles (row-blocks outer), byte (r, k) of a
+    tile at r*128 + ((k/16) ^ (r%8))*16 + k%16, two's complement."""
+    t = _pad128(np.asarray(codes, np.int8))
+    R, Cc = t.shape
+    t = t.reshape(R // 128, 128, Cc // 128, 128).transpose(0, 2, 1, 3)  # [rb][kt][r][k]
+    t = t.reshape(R // 128, Cc // 128, 128, 8, 16)                       # k = 16 * chunk + i
+    r = np.arange(128)[:, None]
+    phys = np.arange(8)[None, :] ^ (r & 7)                               # [r][chunk] -> slot
+    out = np.zeros_like(t)
+    out[:, :, r, phys, :] = t[:, :, r, np.arange(8)[None, :], :]
+    return out.view(np.uint8).ravel()
+
+
+def encode_native_i4(codes):
+    """Signed 4-bit codes -> NATIVE_I4 bytes: one 8 KiB tile per 128 rows x 128-code group
+    (row-blocks outer); row r is 64 bytes, byte p = (code(r, p) << 4) | (code(r, 64 + p) & 15)
+    stored at 16 * ((p/16) ^ ((r/2) % 4)) + p % 16."""
+    t = _pad128(np.asarray(codes, np.int8))
+    R, Cc = t.shape
+    nib = (t.astype(np.int16) & 15).astype(np.uint8)
+    nib = nib.reshape(R // 128, 128, Cc // 128, 128).transpose(0, 2, 1, 3)
+    byte = (nib[..., :64] << 4) | nib[..., 64:]                          # [rb][kt][r][p]
+    byte = byte.reshape(R // 128, Cc // 128, 128, 4, 16)
+    r = np.arange(128)[:, None]
+    phys = np.arange(4)[None, :] ^ ((r >> 1) & 3)
+    out = np.zeros_like(byte)
+    out[:, :, r, phys, :] = byte[:, :, r, np.arange(4)[None, :], :]
+    return out.ravel()
+
+
 class OracleError(RuntimeError):
     def __init__(self, status, msg=""):
         super().__init__(f"status {status}: {msg}")

@@ -31,7 +31,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "librtnq_b200.so")
 
 F32, F16, BF16 = 0, 1, 2
-ROW_MAJOR, KERNEL_INTERLEAVED, NATIVE, NATIVE_I8 = 0, 1, 2, 3
+ROW_MAJOR, KERNEL_INTERLEAVED, NATIVE, NATIVE_I8, NATIVE_I4 = 0, 1, 2, 3, 4
 SCALES_REF, SCALES_NATIVE = 0, 1
 PATH_FUSED, PATH_DEQUANT_FIRST, PATH_AUTO, PATH_ORACLE = 0, 1, 2, 3
 DEFAULT_THRESHOLD = 1024  # kDefaultGemmThreshold, gemm.hpp:16
@@ -186,7 +186,7 @@ class QuantWeight:
     ragged: bool
     codes: "object"            # uint8 codes in `layout` (native, or row-major for W8 per-channel)
     scales: "object"           # f16 bits (int16 tensor) in native order
-    layout: int = NATIVE       # NATIVE: tcgen05 kind::f16 kernel; NATIVE_I8: kind::i8 kernel
+    layout: int = NATIVE       # NATIVE: tcgen05 kind::f16 kernel; NATIVE_I8/I4: kind::i8 kernels
     codes_row_major: "object" = None
     codes_kernel: "object" = None
     scales_f32: "object" = None  # reference order
@@ -207,9 +207,10 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
                   check=True, stream=None) -> QuantWeight:
     """RTN quantize-and-pack on the GPU (rtnq_dev_quantize_pack).
 
-    The linear's operand is ``codes`` in ``layout``: the native tcgen05 order, except
-    for W8 per-channel (one group per row), whose kernel streams the reference's own
-    row-major bytes (tcgen05 kind::i8, no dequantization)."""
+    The linear's operand is ``codes`` in ``out.layout``.  With ``native=None`` that is the
+    layout of the fastest kernel for the shape: NATIVE_I8 for W8 per-channel and NATIVE_I4
+    for W4 group-128 (tcgen05 kind::i8 kernels, relaid out from the reference's row-major
+    bytes), else NATIVE (tcgen05 kind::f16 kernel).  ``native=True`` forces NATIVE."""
     torch = _torch()
     assert w.is_cuda and w.dim() == 2 and w.is_contiguous()
     rows, cols = w.shape
@@ -217,13 +218,20 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
     dev = w.device
     u8 = dict(dtype=torch.uint8, device=dev)
     out = QuantWeight(rows, cols, bits, group, ragged, None, None)
-    # default operand: W8 per-channel -> row-major (kind::i8 kernel), else native
-    pc8 = native is None and bits == 8 and group >= cols
-    native = (not pc8) if native is None else native
-    if pc8:
+    # default operand: W8 per-channel -> NATIVE_I8, W4 group-128 -> NATIVE_I4 (kind::i8
+    # kernels, from the row-major bytes), else NATIVE (kind::f16 kernel)
+    imma = None
+    if native is None:
+        if bits == 8 and group >= cols:
+            imma = NATIVE_I8
+        elif bits == 4 and group == 128:
+            imma = NATIVE_I4
+    native = (imma is None) if native is None else native
+    rm_requested = row_major
+    if imma is not None:
         native = False
-        rm_requested, row_major = row_major, True
-        out.layout = NATIVE_I8
+        row_major = True
+        out.layout = imma
         out.scales = torch.empty(native_scale_count(rows, gpr), dtype=torch.int16, device=dev)
     if native:
         out.codes = torch.empty(layout_bytes(layout(NATIVE), bits, rows, cols), **u8)
@@ -247,8 +255,8 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
         _ptr(out.scales), _ptr(err), _ptr(ws), wsb, st))
     if check:
         _check(lib().rtnq_dev_check_flag(_ptr(err), st))
-    if out.layout == NATIVE_I8:  # pre-swizzled int8-MMA tiles, from the row-major bytes
-        out.codes = relayout(out.codes_row_major, layout(ROW_MAJOR), layout(NATIVE_I8), bits, rows,
+    if imma is not None:  # int8-MMA tiles, from the row-major bytes
+        out.codes = relayout(out.codes_row_major, layout(ROW_MAJOR), layout(imma), bits, rows,
                              cols, stream=stream)
         if not rm_requested:
             out.codes_row_major = None

@@ -37,7 +37,7 @@ Layout to_layout(rtnq_layout l) { return Layout{l.kind, l.tile_rows, l.tile_cols
 bool valid_bits(int bits) { return bits == 4 || bits == 8; }
 
 rtnq_status check_layout(rtnq_layout l) {
-    if (l.kind < RTNQ_ROW_MAJOR || l.kind > RTNQ_NATIVE_I8)
+    if (l.kind < RTNQ_ROW_MAJOR || l.kind > RTNQ_NATIVE_I4)
         return fail(RTNQ_E_INVALID_INPUT, "unknown layout kind");
     if (l.kind == RTNQ_KERNEL_INTERLEAVED && (l.tile_rows <= 0 || l.tile_cols <= 0))
         return fail(RTNQ_E_INVALID_INPUT, "kernel tile dimensions must be positive");
@@ -235,6 +235,13 @@ static bool i8_path(int a_dtype, rtnq_layout layout, int bits, int64_t g, int64_
            (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) && sdtype == RTNQ_F16;
 }
 
+// W4 group-128 over RTNQ_NATIVE_I4 nibble tiles: the int8 tensor-core kernel.
+static bool i4_path(int a_dtype, rtnq_layout layout, int bits, int64_t g, int sdtype, int sorder) {
+    return layout.kind == RTNQ_NATIVE_I4 && bits == 4 && g == 128 &&
+           (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) && sdtype == RTNQ_F16 &&
+           sorder == RTNQ_SCALES_NATIVE;
+}
+
 static bool tensor_path(int a_dtype, rtnq_layout layout, int sdtype, int sorder) {
     return layout.kind == RTNQ_NATIVE_SM100 && (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) &&
            sdtype == RTNQ_F16 && sorder == RTNQ_SCALES_NATIVE;
@@ -246,6 +253,7 @@ size_t rtnq_dev_linear_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits
     if (path == RTNQ_PATH_FUSED || path == RTNQ_PATH_AUTO) {
         if (layout.kind == RTNQ_NATIVE_SM100) ws = wgemm_workspace_bytes(m, n, k, bits, g);
         if (layout.kind == RTNQ_NATIVE_I8 && bits == 8 && g >= k) ws = wgemm_i8_workspace_bytes(m, n, k);
+        if (layout.kind == RTNQ_NATIVE_I4 && bits == 4 && g == 128) ws = wgemm_i4_workspace_bytes(m, n, k);
     }
     if (path == RTNQ_PATH_DEQUANT_FIRST || path == RTNQ_PATH_AUTO) {
         const size_t d = size_t(n) * size_t(k) * sizeof(float);
@@ -312,6 +320,21 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
         WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
                     out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
         RTNQ_CUDA(launch_wgemm_i8(A, st));
+        return RTNQ_OK;
+    }
+    if (path == RTNQ_PATH_FUSED && i4_path(a_dtype, layout, bits, g, sdtype, sorder)) {
+        if (const char* why = wgemm_i4_unsupported(m, n, k, bits, g, a_dtype))
+            return fail(RTNQ_E_UNSUPPORTED, why);
+        const size_t need = wgemm_i4_workspace_bytes(m, n, k);
+        if (ws_bytes < need)
+            return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " +
+                                                  std::to_string(need) + " bytes");
+        if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(codes) |
+             reinterpret_cast<uintptr_t>(scales)) & 15)
+            return fail(RTNQ_E_INVALID_INPUT, "tensor-core path needs 16-byte aligned operands");
+        WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
+                    out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
+        RTNQ_CUDA(launch_wgemm_i4(A, st));
         return RTNQ_OK;
     }
     // Reference-exact CUDA-core paths: f32 activations, f32 reference-order scales.

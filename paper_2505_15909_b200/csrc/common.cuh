@@ -163,10 +163,36 @@ __host__ __device__ __forceinline__ bool i8_coords(int64_t rows, int64_t cols, i
     return *r < rows && *c < cols;
 }
 
+// Native W4 int8-MMA layout (RTNQ_NATIVE_I4): one 8 KiB tile per 128 rows x one
+// 128-code group, row-blocks outer and groups inner.  Row r of a tile is 64 bytes; byte p
+// holds code (r, p) in its high nibble and code (r, 64 + p) in its low nibble, as 4-bit two's
+// complement, so (byte & 0xF0) and (byte << 4 & 0xF0) are the s8 values 16 * code.  The four
+// 16-byte chunks of a row are XOR-swizzled by (r / 2) % 4 (conflict-free 16-byte reads of 8
+// consecutive rows).  Padding is code 0.
+constexpr int kI4Tile = 128;
+__host__ __device__ __forceinline__ int64_t i4_slot(int64_t cols, int64_t r, int64_t c) {
+    const int64_t kt = (cols + kI4Tile - 1) / kI4Tile;
+    const int64_t tile = (r / kI4Tile) * kt + c / kI4Tile;
+    const int64_t rr = r % kI4Tile, kk = c % kI4Tile, pos = kk & 63;
+    const int64_t byte = tile * (kI4Tile * 64) + rr * 64 + ((((pos >> 4) ^ ((rr >> 1) & 3))) << 4) + (pos & 15);
+    return 2 * byte + (kk < 64 ? 1 : 0);  // odd slot = high nibble
+}
+__host__ __device__ __forceinline__ bool i4_coords(int64_t rows, int64_t cols, int64_t slot,
+                                                   int64_t* r, int64_t* c) {
+    const int64_t kt = (cols + kI4Tile - 1) / kI4Tile;
+    const int64_t byte = slot >> 1, tile = byte / (kI4Tile * 64), within = byte % (kI4Tile * 64);
+    const int64_t rr = within / 64, off = within % 64;
+    const int64_t pos = ((((off >> 4) ^ ((rr >> 1) & 3))) << 4) | (off & 15);
+    *r = (tile / kt) * kI4Tile + rr;
+    *c = (tile % kt) * kI4Tile + ((slot & 1) ? pos : 64 + pos);
+    return *r < rows && *c < cols;
+}
+
 __host__ __device__ __forceinline__ int64_t layout_slot(const Layout& L, int bits, int64_t rows,
                                                         int64_t cols, int64_t r, int64_t c) {
     if (L.kind == RTNQ_ROW_MAJOR) return r * cols + c;
     if (L.kind == RTNQ_NATIVE_I8) return i8_slot(cols, r, c);
+    if (L.kind == RTNQ_NATIVE_I4) return i4_slot(cols, r, c);
     if (L.kind == RTNQ_NATIVE_SM100) return native_slot(bits, rows, cols, r, c);
     const int64_t tpr = (cols + L.tc - 1) / L.tc;  // packing.cpp:62-65
     const int64_t tile = (r / L.tr) * tpr + c / L.tc;
@@ -183,6 +209,7 @@ __host__ __device__ __forceinline__ bool layout_coords(const Layout& L, int bits
     }
     if (L.kind == RTNQ_NATIVE_SM100) return native_coords(bits, rows, cols, slot, r, c);
     if (L.kind == RTNQ_NATIVE_I8) return i8_coords(rows, cols, slot, r, c);
+    if (L.kind == RTNQ_NATIVE_I4) return i4_coords(rows, cols, slot, r, c);
     const int64_t tt = int64_t(L.tr) * L.tc, tpr = (cols + L.tc - 1) / L.tc;
     const int64_t tile = slot / tt, within = slot % tt;
     *r = (tile / tpr) * L.tr + within % L.tr;
@@ -195,7 +222,7 @@ __host__ __device__ __forceinline__ int64_t layout_slots_of(const Layout& L, int
     if (L.kind == RTNQ_ROW_MAJOR) return rows * cols;
     if (L.kind == RTNQ_NATIVE_SM100)
         return rows * ((cols + kNativeKB - 1) / kNativeKB * kNativeKB);
-    if (L.kind == RTNQ_NATIVE_I8)
+    if (L.kind == RTNQ_NATIVE_I8 || L.kind == RTNQ_NATIVE_I4)
         return (rows + kI8Tile - 1) / kI8Tile * kI8Tile * ((cols + kI8Tile - 1) / kI8Tile * kI8Tile);
     return ((rows + L.tr - 1) / L.tr * L.tr) * ((cols + L.tc - 1) / L.tc * L.tc);
 }
@@ -206,7 +233,11 @@ __device__ __forceinline__ int code_at_slot(const uint8_t* data, int bits, int64
                                             int kind = RTNQ_ROW_MAJOR) {
     if (bits == 8) return kind == RTNQ_NATIVE_I8 ? int(int8_t(data[slot])) : int(data[slot]) - 128;
     const uint8_t b = data[slot >> 1];
-    return int((slot & 1) ? (b >> 4) : (b & 0x0F)) - 8;
+    const int v = (slot & 1) ? (b >> 4) : (b & 0x0F);
+    return kind == RTNQ_NATIVE_I4 ? ((v ^ 8) - 8) : v - 8;  // two's complement / offset-binary
+}
+__device__ __forceinline__ uint32_t code_nib4(int code, int kind) {
+    return kind == RTNQ_NATIVE_I4 ? uint32_t(code) & 0xFu : uint32_t(code + 8);
 }
 __device__ __forceinline__ uint8_t code_byte8(int code, int kind) {
     return kind == RTNQ_NATIVE_I8 ? uint8_t(int8_t(code)) : uint8_t(code + 128);

@@ -1,0 +1,305 @@
+// int8_mma.cuh -- shared pieces of the tcgen05 kind::i8 weight-only GEMMs (wgemm_i8.cu: W8
+// per-channel, wgemm_i4.cu: W4 group-128): PTX wrappers (mbarrier, TMA, tcgen05), the
+// work cursor, and the activation-planes kernel that turns bf16/f16 activations into three
+// exact int8 planes.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../common.cuh"
+
+namespace rtnq_b200 {
+namespace imma {
+
+constexpr int kRows = 128;  // UMMA M = one row-block
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+    asm volatile(
+        "{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra W_%=;\n}\n" ::"r"(su32(b)),
+        "r"(ph)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                      uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit(uint64_t* b) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t* d) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+          "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+          "=r"(d[14]), "=r"(d[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void store_out(void* out, int dt, int64_t i, float v) {
+    if (dt == RTNQ_F32) static_cast<float*>(out)[i] = v;
+    else if (dt == RTNQ_BF16) static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    else static_cast<__half*>(out)[i] = __float2half_rn(v);
+}
+// K-major, 128-byte swizzle: 8-row atoms of 128 B (SBO = 1024), layout type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+           (1ull << 46) | (2ull << 61);
+}
+// The unit sequence of a CTA: runs of <= 2 k-blocks inside one row-block and one 128-code
+// block, tracked incrementally (no division on the issue path).
+template <int SPAN>  // k-blocks per stage (2 per 16 KiB tile)
+struct Cursor {
+    int u, u1, b, kb, KBLK;
+    __device__ Cursor(int u0, int u1_, int KBLK_) : u(u0), u1(u1_), KBLK(KBLK_) {
+        b = u0 / KBLK_;
+        kb = u0 - b * KBLK_;
+    }
+    __device__ bool more() const { return u < u1; }
+    __device__ int chunk() const {
+        const int left_seg = KBLK - kb, left = u1 - u, cap = SPAN - (kb & (SPAN - 1));
+        const int n = left_seg < left ? left_seg : left;
+        return n < cap ? n : cap;
+    }
+    __device__ bool seg_end(int n) const { return kb + n == KBLK || u + n == u1; }
+    __device__ void advance(int n) {
+        u += n;
+        kb += n;
+        if (kb == KBLK) kb = 0, ++b;
+    }
+};
+__device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                             uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* b) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void elect_arrive(uint64_t* b) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+            su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void elect_bulk(void* dst, const void* src, uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void elect_prefetch(const void* src, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.prefetch.L2.global [%0], %1;\n}\n" ::"l"(src), "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void elect_tma3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                            uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%6], %5;\n"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%6];\n}\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+
+// expect_tx once for all boxes of a stage, then the box loads (no further arrivals)
+__device__ __forceinline__ void elect_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(su32(b)), "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void elect_tma3d_tx(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                               uint64_t* b) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];\n}\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(b))
+        : "memory");
+}
+
+__device__ __forceinline__ int cta_of(int64_t u, int64_t U, int G) {
+    return int(((u + 1) * G - 1) / U);
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---- activation planes ------------------------------------------------------------------
+// One CTA per token (PDL secondary of whatever produced the activations):
+//   s = exponent(max|a|) - 6 so |a| / 2^s < 64; three exact int8 planes.
+// 16-byte loads of 8 activations; up to kVPT vectors per thread stay in registers between
+// the max and the split (one pass over memory for K <= 512 * 8 * kVPT), longer rows reload.
+constexpr int kPlaneThreads = 512, kVPT = 4;
+template <int AT, bool VEC>
+__global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* __restrict__ a, int K, int M,
+                                                                   int8_t* __restrict__ planes,
+                                                                   int32_t* __restrict__ texp, unsigned long long* stamps) {
+    __shared__ float wmax[kPlaneThreads / 32];
+    if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[0] = gtime();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[1] = gtime();
+    const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint16_t* rowp = static_cast<const uint16_t*>(a) + int64_t(t) * K;
+    const int nv = K / 8;
+    auto load4 = [&](int v) -> uint4 {
+        if constexpr (VEC) return __ldg(reinterpret_cast<const uint4*>(rowp) + v);
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = uint32_t(rowp[v * 8 + 2 * i]) | (uint32_t(rowp[v * 8 + 2 * i + 1]) << 16);
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    };
+    auto cvt = [](uint32_t h) -> float {
+        if constexpr (AT == RTNQ_BF16) return __uint_as_float(h << 16);
+        else return __half2float(__ushort_as_half(static_cast<unsigned short>(h)));
+    };
+    auto vmax = [&](const uint4& q, float m) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m = fmaxf(m, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+        return m;
+    };
+    uint4 keep[kVPT];
+    float mx = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+        const int v = tid + j * kPlaneThreads;
+        keep[j] = v < nv ? load4(v) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) mx = vmax(keep[j], mx);
+    for (int v = tid + kVPT * kPlaneThreads; v < nv; v += kPlaneThreads) mx = vmax(load4(v), mx);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    float amax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kPlaneThreads / 32; ++i) amax = fmaxf(amax, wmax[i]);
+    int e = 0;
+    if (amax > 0.0f) frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
+    const int s = max(e - 6, -126);      // |a| / 2^s < 64; 2^s stays a normal float
+    if (tid == 0) texp[t] = s;
+    auto split = [&](const uint4& q, int v) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float y = ldexpf(cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu), -s);  // exact
+            const float r0 = rintf(y);
+            const float y1 = (y - r0) * 128.0f;  // exact
+            const float r1 = rintf(y1);
+            const float r2 = rintf((y1 - r1) * 128.0f);
+            pk[0][i >> 2] |= (uint32_t(int(r0)) & 0xffu) << (8 * (i & 3));
+            pk[1][i >> 2] |= (uint32_t(int(r1)) & 0xffu) << (8 * (i & 3));
+            pk[2][i >> 2] |= (uint32_t(int(r2)) & 0xffu) << (8 * (i & 3));
+        }
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+            *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
+                make_uint2(pk[pl][0], pk[pl][1]);
+    };
+#pragma unroll
+    for (int j = 0; j < kVPT; ++j) {
+        const int v = tid + j * kPlaneThreads;
+        if (v < nv) split(keep[j], v);
+    }
+    for (int v = tid + kVPT * kPlaneThreads; v < nv; v += kPlaneThreads) split(load4(v), v);
+    if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[2] = gtime();
+}
+
+template <int AT, bool VEC>
+inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, int32_t* texp, unsigned long long* stamps,
+                                 cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(M));
+    cfg.blockDim = dim3(kPlaneThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+inline EncodeFn encoder() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+inline int sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+}  // namespace imma
+}  // namespace rtnq_b200

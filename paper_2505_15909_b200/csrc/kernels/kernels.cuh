@@ -64,10 +64,15 @@ const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t
 size_t wgemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits, int64_t g);
 cudaError_t launch_wgemm(const WgemmArgs& args, cudaStream_t st);
 
-// wgemm_i8.cu: W8 per-channel on tcgen05.mma.kind::i8 over row-major codes (no dequant)
+// wgemm_i8.cu: W8 per-channel on tcgen05.mma.kind::i8 over RTNQ_NATIVE_I8 tiles (no dequant)
 const char* wgemm_i8_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);
 size_t wgemm_i8_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_wgemm_i8(const WgemmArgs& args, cudaStream_t st);
+
+// wgemm_i4.cu: W4 group-128 on tcgen05.mma.kind::i8 over RTNQ_NATIVE_I4 nibble tiles
+const char* wgemm_i4_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);
+size_t wgemm_i4_workspace_bytes(int64_t m, int64_t n, int64_t k);
+cudaError_t launch_wgemm_i4(const WgemmArgs& args, cudaStream_t st);
 
 // decode.cu: the non-GEMM kernels of a decode layer (bf16 activations)
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,

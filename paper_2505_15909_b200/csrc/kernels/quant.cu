@@ -92,7 +92,7 @@ __global__ void encode_layout_kernel(CodeSource S, Layout dst, int bits, int64_t
                 if (slot < nslots && layout_coords(dst, bits, rows, cols, slot, &r, &c))
                     code = source_code(S, bits, rows, cols, r, c);
                 // pack(): an odd tail leaves the high nibble 0 (packing.cpp:28-29)
-                if (slot < nslots) v |= uint32_t(code + 8) << (4 * h);
+                if (slot < nslots) v |= code_nib4(code, dst.kind) << (4 * h);
             }
             out[b] = uint8_t(v);
         }

@@ -1,0 +1,559 @@
+// wgemm_i4.cu -- W4A16 group-128 linear on tcgen05.mma.kind::i8.
+//
+// out[m][n] = sum_g S[n][g] * sum_{k in g} a[m][k] * code[n][k]     (gemm.hpp:18-27, g = 128)
+//
+// Weights: RTNQ_NATIVE_I4 (common.cuh), one 8 KiB nibble tile per 128 rows x one group.  Each
+// byte carries two codes as 4-bit two's complement, so the expansion to the s8 A operand is
+// three ALU ops per 4 bytes and needs no offset correction:
+//   hi = w & 0xF0F0F0F0          -> 16 * code(r, p)        (k = p)
+//   lo = (w << 4) & 0xF0F0F0F0   -> 16 * code(r, 64 + p)   (k = 64 + p)
+// The factor 16 is folded into the group scale.
+//
+// Activations: the three exact int8 planes of int8_mma.cuh (a = 2^s (P0 + P1/2^7 + P2/2^14)),
+// the s8 B operand with N = 3 * NT.
+//
+// Each group has its own int32 accumulator in TMEM (a ring of NS slots): the epilogue reads
+// it once, applies S[n][g] / 16 * 2^s and adds into per-row float accumulators.
+//
+// Warp roles (384 threads):
+//   warp 0      TMA producer: codes (contiguous tiles) + the group scales of the stage
+//   warp 2      TMA producer: activation planes (after the planes kernel, PDL)
+//   warp 1      MMA issuer: 4 x (M128, N 3NT, K32) per group, A = expanded tile (smem)
+//   warps 8-11  expansion: nibble tile -> 16 KiB 128B-swizzled s8 tile; group scale / 16
+//   warps 4-7   epilogue: per-group TMEM reads, scaling, stream-K / cluster output
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "int8_mma.cuh"
+#include "kernels.cuh"
+
+namespace rtnq_b200 {
+namespace i4 {
+using namespace imma;
+
+constexpr int kKB = 128;              // k-block = one quantization group = one tile
+constexpr int kTile = kRows * 64;     // 8 KiB of nibbles
+constexpr int kATile = kRows * 128;   // 16 KiB of s8 after expansion
+constexpr int kThreads = 384;
+constexpr int kEpi0 = 4, kExp0 = 8;
+
+struct Params {
+    CUtensorMap tmap_p;      // planes [3][M][K] s8, box {128, NT, 3}, SWIZZLE_128B
+    const uint8_t* codes;    // RTNQ_NATIVE_I4
+    const uint16_t* scales;  // f16, native order [row-block][group][rows8]
+    const int32_t* texp;     // [M] token exponents s
+    void* out;
+    float* partials;
+    int* counters;
+    int64_t N, K;
+    int M, Mtot, m0, NB, KBLK, U, G, csize, out_dtype;
+    int debug;
+};
+
+template <int NT>
+struct Geo {
+    static constexpr int PLANE_BYTES = 3 * NT * 128;       // one group's planes box
+    static constexpr int TPS = NT <= 32 ? 2 : 1;            // groups (tiles) per stage
+    static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
+    static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
+    static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
+    static constexpr int AS = 4;                            // expanded A tiles
+    static constexpr int STAGES_FIT = (214 * 1024 - AS * kATile) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
+    static constexpr int A_OFF = STAGES * STAGE_BYTES;
+    static constexpr int DN = 3 * NT;                       // accumulator columns per group
+    static constexpr int NS_FIT = 512 / DN;
+    static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;    // TMEM group slots
+    static constexpr int BAR_OFF = A_OFF + AS * kATile;
+    static constexpr int SR_OFF = BAR_OFF + 1024;           // [NS][128] f32 group scale / 16
+    static constexpr int SMEM = SR_OFF + NS * kRows * 4 + 1024;
+    static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (NT * kRows * 4);
+    static constexpr int MAXC = MAXC_FIT > 8 ? 8 : MAXC_FIT;
+    static_assert(STAGES >= 3, "");
+    static_assert(SMEM <= 227 * 1024, "");
+};
+
+__device__ unsigned long long g_i4_dbg[1024 * 16];  // profiling (debug & 64: globaltimer stamps)
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
+    using GG = Geo<NT>;
+    constexpr int STAGES = GG::STAGES, DN = GG::DN, NS = GG::NS, AS = GG::AS, TPS = GG::TPS;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);  // [STAGES] TMA landed
+    uint64_t* empty = full + STAGES;    // [STAGES] expansion (4) + MMA commit (1) done with it
+    uint64_t* afull = empty + STAGES;   // [AS] expanded tile ready (4 warps)
+    uint64_t* aempty = afull + AS;      // [AS] MMA done reading it (commit)
+    uint64_t* tfull = aempty + AS;      // [NS] group accumulator ready (commit)
+    uint64_t* tfree = tfull + NS;       // [NS] epilogue has read it (4 warps)
+    uint64_t* sfull = tfree + NS;       // [NS] group scales in the scale ring (4 warps)
+    uint64_t* go = sfull + NS;          // cluster split-K: leader ready for partials
+    uint64_t* rfull = go + 1;           // cluster split-K: partials landed in the leader
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(rfull + 1);
+    float* sring = reinterpret_cast<float*>(smem + GG::SR_OFF);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
+    if ((p.debug & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 5] = gtime();
+
+    int u0, u1;
+    if (p.csize > 1) {
+        const int b = c / p.csize, r = c % p.csize;
+        u0 = b * p.KBLK + r * p.KBLK / p.csize;
+        u1 = b * p.KBLK + (r + 1) * p.KBLK / p.csize;
+    } else {
+        u0 = int(int64_t(c) * p.U / p.G);
+        u1 = int(int64_t(c + 1) * p.U / p.G);
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 5);
+        for (int i = 0; i < AS; ++i) mbar_init(&afull[i], 4), mbar_init(&aempty[i], 1);
+        for (int i = 0; i < NS; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4), mbar_init(&sfull[i], 4);
+        mbar_init(go, 1), mbar_init(rfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            su32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (p.csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    const uint32_t tmem = *tslot;
+    asm volatile("griddepcontrol.launch_dependents;");
+
+    if (warp == 0 || warp == 2) {
+        // ===================== producers: warp 0 codes + scales, warp 2 planes ============
+        const bool codes = warp == 0;
+        Cursor<TPS> cu(u0, u1, p.KBLK);
+        int s = 0;
+        uint32_t ph = 0;
+        if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes kernel
+        for (int i = 0; cu.more(); ++i) {
+            const int n = cu.chunk();
+            if (i >= STAGES) mbar_wait(&empty[s], ph ^ 1u);
+            uint8_t* st = smem + s * GG::STAGE_BYTES;
+            const int slot0 = cu.kb & (TPS - 1);
+            if (codes) {
+                // the row-block's rows padded to 8: the stride of its native scale groups
+                const int64_t left = p.N - int64_t(cu.b) * kRows;
+                const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
+                elect_expect(&full[s], uint32_t(n) * (kTile + uint32_t(r8) * 2));
+                elect_bulk_tx(st + GG::CODE_OFF + slot0 * kTile,
+                              p.codes + (int64_t(cu.b) * p.KBLK + cu.kb) * kTile, &full[s], uint32_t(n) * kTile);
+                elect_bulk_tx(st + GG::SC_OFF + slot0 * 256,
+                              p.scales + int64_t(cu.b) * kRows * p.KBLK + int64_t(cu.kb) * r8, &full[s],
+                              uint32_t(n * r8 * 2));
+            } else {
+                elect_expect(&full[s], uint32_t(n) * GG::PLANE_BYTES);
+                for (int j = 0; j < n; ++j)
+                    elect_tma3d_tx(st + (slot0 + j) * GG::PLANE_BYTES, &p.tmap_p, (cu.kb + j) * kKB, p.m0, 0,
+                                   &full[s]);
+            }
+            cu.advance(n);
+            if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+    } else if (warp >= kExp0) {
+        // ===================== expansion: nibbles -> s8 (16 x code), 128B-swizzled =======
+        const int row = threadIdx.x - kExp0 * 32;  // one row of the tile per thread
+        const uint32_t sw_in = uint32_t((row >> 1) & 3), sw_out = uint32_t(row & 7);
+        Cursor<TPS> cu(u0, u1, p.KBLK);
+        int s = 0, gi = 0;
+        uint32_t ph = 0;
+        while (cu.more()) {
+            const int n = cu.chunk();
+            const int slot0 = cu.kb & (TPS - 1);
+            const int64_t left = p.N - int64_t(cu.b) * kRows;
+            const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
+            mbar_wait(&full[s], ph);
+            const uint8_t* st = smem + s * GG::STAGE_BYTES;
+            for (int j = 0; j < n; ++j, ++gi) {
+                const int ai = gi % AS, ni = gi % NS;
+                if (gi >= AS) mbar_wait(&aempty[ai], uint32_t(gi / AS - 1) & 1u);
+                if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
+                const uint8_t* src = st + GG::CODE_OFF + (slot0 + j) * kTile + row * 64;
+                uint8_t* dst = smem + GG::A_OFF + ai * kATile + row * 128;
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
+                    const uint4 hi = make_uint4(w.x & 0xF0F0F0F0u, w.y & 0xF0F0F0F0u, w.z & 0xF0F0F0F0u,
+                                                w.w & 0xF0F0F0F0u);
+                    const uint4 lo = make_uint4((w.x << 4) & 0xF0F0F0F0u, (w.y << 4) & 0xF0F0F0F0u,
+                                                (w.z << 4) & 0xF0F0F0F0u, (w.w << 4) & 0xF0F0F0F0u);
+                    *reinterpret_cast<uint4*>(dst + ((q ^ sw_out) << 4)) = hi;
+                    *reinterpret_cast<uint4*>(dst + (((q + 4) ^ sw_out) << 4)) = lo;
+                }
+                const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
+                sring[ni * kRows + row] =
+                    row < r8 ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
+                fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[ai]), mbar_arrive(&sfull[ni]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // codes and scales of the stage consumed
+            cu.advance(n);
+            if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
+        // D s32, A s8 (16 x codes), B s8 (planes), M = 128, N = 3 * NT
+        constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                   (uint32_t(DN >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
+        constexpr uint64_t kHi = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
+                                 (2ull << 61);  // K-major SWIZZLE_128B, SBO = 1024
+        const uint32_t base = su32(smem) >> 4;
+        Cursor<TPS> cu(u0, u1, p.KBLK);
+        int s = 0, gi = 0;
+        uint32_t ph = 0;
+        while (cu.more()) {
+            const int n = cu.chunk();
+            const int slot0 = cu.kb & (TPS - 1);
+            mbar_wait(&full[s], ph);  // the planes of this stage
+            const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
+            for (int j = 0; j < n; ++j, ++gi) {
+                const int ai = gi % AS, ni = gi % NS;
+                mbar_wait(&afull[ai], uint32_t(gi / AS) & 1u);
+                if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
+                fence_after();
+                const uint32_t alo = base + uint32_t((GG::A_OFF + ai * kATile) >> 4);
+                const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
+                const uint32_t d = tmem + uint32_t(ni * DN);
+                if (!(p.debug & 4)) {
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k)  // K = 32 bytes per MMA: +2 in descriptor units
+                        mma_i8_elect(d, kHi | (alo + 2 * k), kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                }
+                commit_elect(&aempty[ai]);
+                commit_elect(&tfull[ni]);
+            }
+            commit_elect(&empty[s]);
+            cu.advance(n);
+            if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+    } else if (warp >= kEpi0) {
+        // ===================== epilogue =====================
+        const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        __shared__ float pow_s[NT];  // 2^s per token, 0 for padding tokens
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // texp comes from the planes kernel
+        for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        float acc[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+        Cursor<TPS> cu(u0, u1, p.KBLK);
+        int gi = 0, seg_kb0 = cu.kb;
+        while (cu.more()) {
+            const int n = cu.chunk();
+            const bool seg_end = cu.seg_end(n);
+            const int b = cu.b;
+            for (int j = 0; j < n; ++j, ++gi) {
+                const int ni = gi % NS;
+                mbar_wait(&sfull[ni], uint32_t(gi / NS) & 1u);
+                mbar_wait(&tfull[ni], uint32_t(gi / NS) & 1u);
+                fence_after();
+                const float sc = sring[ni * kRows + row];
+#pragma unroll
+                for (int jj = 0; jj < NT; jj += 16) {
+                    uint32_t d0[16], d1[16], d2[16];
+                    const uint32_t ta = tmem + lane_base + uint32_t(ni * DN + jj);
+                    ld16(ta, d0);
+                    ld16(ta + NT, d1);
+                    ld16(ta + 2 * NT, d2);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const float x = float(int32_t(d0[e])) + float(int32_t(d1[e])) * 0.0078125f +
+                                        float(int32_t(d2[e])) * 6.103515625e-05f;
+                        acc[jj + e] = fmaf(x, sc * pow_s[jj + e], acc[jj + e]);
+                    }
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tfree[ni]);
+            }
+            if (seg_end) {
+                const int kbe = cu.kb + n;
+                const bool sole = seg_kb0 == 0 && kbe == p.KBLK;
+                const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
+                const int64_t n0 = int64_t(b) * kRows;
+                if (p.csize > 1) {
+                    // cluster split-K (one segment per CTA): push partials into the leader
+                    const int rank = c % p.csize;
+                    constexpr uint32_t kSlot = uint32_t(NT) * kRows * 4;
+                    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+                    if (rank == 0) {
+                        if (et == 0) {
+                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull)),
+                                         "r"(uint32_t(p.csize - 1) * kSlot)
+                                         : "memory");
+                            for (int r = 1; r < p.csize; ++r) {
+                                uint32_t ra;
+                                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(go)), "r"(r));
+                                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra)
+                                             : "memory");
+                            }
+                        }
+                        mbar_wait(rfull, 0);
+                        const float4* red = reinterpret_cast<const float4*>(smem);
+                        for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
+#pragma unroll
+                            for (int j = 0; j < NT / 4; ++j) {
+                                const float4 x = red[((r - 1) * kRows + row) * (NT / 4) + j];
+                                acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
+                            }
+                        }
+                        if (row < rows)
+#pragma unroll
+                            for (int m = 0; m < NT; ++m)
+                                if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                    } else {
+                        mbar_wait(go, 0);
+                        uint32_t dst, rb;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst)
+                                     : "r"(su32(smem) + uint32_t(((rank - 1) * kRows + row) * NT * 4)));
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(su32(rfull)));
+#pragma unroll
+                        for (int j = 0; j < NT / 4; ++j)
+                            asm volatile(
+                                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                                    dst + 16u * j),
+                                "f"(acc[4 * j]), "f"(acc[4 * j + 1]), "f"(acc[4 * j + 2]), "f"(acc[4 * j + 3]), "r"(rb)
+                                : "memory");
+                    }
+                } else if (sole) {
+                    if (row < rows)
+#pragma unroll
+                        for (int m = 0; m < NT; ++m)
+                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                } else {
+                    // stream-K: the owner holds the row-block's first k-block (its last segment);
+                    // the others hand over partials from their first segment (slot = CTA)
+                    const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
+                    const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
+                    if (c == c_first) {
+                        if (et == 0) {
+                            const int want = c_last - c_first;
+                            int got;
+                            do {
+                                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(p.counters + b) : "memory");
+                            } while (got < want);
+                            p.counters[b] = 0;  // ready for the next launch (stream-ordered)
+                        }
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        for (int cc = c_first + 1; cc <= c_last; ++cc) {  // fixed order: deterministic
+                            const float4* src = reinterpret_cast<const float4*>(p.partials + (int64_t(cc) * kRows + row) * NT);
+#pragma unroll
+                            for (int j = 0; j < NT / 4; ++j) {
+                                const float4 x = __ldcg(src + j);
+                                acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
+                            }
+                        }
+                        if (row < rows)
+#pragma unroll
+                            for (int m = 0; m < NT; ++m)
+                                if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                    } else {
+                        float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
+#pragma unroll
+                        for (int j = 0; j < NT / 4; ++j)
+                            mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (et == 0) {
+                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                            asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + b) : "memory");
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+                seg_kb0 = kbe == p.KBLK ? 0 : kbe;
+            }
+            cu.advance(n);
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if ((p.debug & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 7] = gtime();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <int NT>
+cudaError_t launch_nt(Params p, cudaStream_t st) {
+    using GG = Geo<NT>;
+    auto kern = wgemm_i4_kernel<NT>;
+    static bool configured = false;
+    static int max_clusters[9] = {0};
+    if (!configured) {
+        if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GG::SMEM))
+            return e;
+        configured = true;
+    }
+    if (p.csize > GG::MAXC) p.csize = GG::MAXC;
+    while (p.csize > 1) {
+        int& mc = max_clusters[p.csize];
+        if (mc == 0) {
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3(unsigned(p.NB * p.csize));
+            q.blockDim = dim3(kThreads);
+            q.dynamicSmemBytes = GG::SMEM;
+            cudaLaunchAttribute ca;
+            ca.id = cudaLaunchAttributeClusterDimension;
+            ca.val.clusterDim.x = unsigned(p.csize);
+            ca.val.clusterDim.y = ca.val.clusterDim.z = 1;
+            q.attrs = &ca;
+            q.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc < 1) mc = -1;
+            cudaGetLastError();
+        }
+        if (mc >= p.NB) break;
+        --p.csize;
+    }
+    if (p.csize > 1) p.G = p.NB * p.csize;
+    else p.csize = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(p.G));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = GG::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.csize > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = unsigned(p.csize);
+        attr[na].val.clusterDim.y = attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // after the planes kernel
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+}  // namespace i4
+
+constexpr size_t kI4Counters = 64 * 1024;
+
+extern "C" int rtnq_i4_debug_read(void* host, size_t bytes) {
+    if (bytes > sizeof(i4::g_i4_dbg)) bytes = sizeof(i4::g_i4_dbg);
+    return cudaMemcpyFromSymbol(host, i4::g_i4_dbg, bytes) == cudaSuccess ? 0 : 1;
+}
+
+static size_t align256_i4(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t wgemm_i4_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+    (void)n;
+    const size_t part = size_t(imma::sms()) * i4::kRows * 64 * sizeof(float);
+    return kI4Counters + align256_i4(part) + align256_i4(size_t(3 * m * k)) + align256_i4(size_t(m) * 4);
+}
+
+const char* wgemm_i4_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype) {
+    (void)m, (void)n;
+    if (bits != 4 || g != 128) return "the W4 int8 tensor-core path is group size 128";
+    if (a_dtype != RTNQ_BF16 && a_dtype != RTNQ_F16) return "activations must be bf16 or f16";
+    if (k % 16 != 0) return "k must be a multiple of 16 for the int8 tensor-core path";
+    return nullptr;
+}
+
+cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
+    imma::EncodeFn enc = imma::encoder();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t kblk = (A.k + i4::kKB - 1) / i4::kKB;
+    char* ws = static_cast<char*>(A.workspace);
+    i4::Params p{};
+    p.counters = reinterpret_cast<int*>(ws);
+    const size_t part = size_t(imma::sms()) * i4::kRows * 64 * sizeof(float);
+    p.partials = reinterpret_cast<float*>(ws + kI4Counters);
+    int8_t* planes = reinterpret_cast<int8_t*>(ws + kI4Counters + align256_i4(part));
+    int32_t* texp = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes) + align256_i4(size_t(3 * A.m * A.k)));
+    const char* dbg_env = std::getenv("RTNQ_WGEMM_DEBUG");
+    const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+    unsigned long long* stamps = nullptr;
+    if (dbg & 64) {
+        void* base = nullptr;
+        if (cudaGetSymbolAddress(&base, i4::g_i4_dbg) == cudaSuccess)
+            stamps = static_cast<unsigned long long*>(base) + 1023 * 16;
+    }
+    {
+        const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
+        cudaError_t e = A.a_dtype == RTNQ_BF16
+            ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, st)
+            : (vec ? imma::launch_planes<RTNQ_F16, true> : imma::launch_planes<RTNQ_F16, false>)(
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, st);
+        if (e != cudaSuccess) return e;
+    }
+    p.codes = A.codes;
+    p.scales = A.scales;
+    p.texp = texp;
+    p.N = A.n;
+    p.K = A.k;
+    p.Mtot = int(A.m);
+    p.NB = int((A.n + i4::kRows - 1) / i4::kRows);
+    p.KBLK = int(kblk);
+    p.U = p.NB * p.KBLK;
+    p.out_dtype = A.out_dtype;
+    p.debug = dbg;
+    const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
+    const int nt_max = A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
+    for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {
+        p.M = int(A.m - m0 < nt_max ? A.m - m0 : nt_max);
+        p.m0 = int(m0);
+        p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
+        const int nt = p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64;
+        {
+            const cuuint64_t dims[3] = {cuuint64_t(A.k), cuuint64_t(A.m), 3};
+            const cuuint64_t strides[2] = {cuuint64_t(A.k), cuuint64_t(A.m * A.k)};
+            const cuuint32_t box[3] = {128, cuuint32_t(nt), 3};
+            const cuuint32_t es[3] = {1, 1, 1};
+            if (enc(&p.tmap_p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return cudaErrorInvalidValue;
+        }
+        // partition: cluster split-K for few row-blocks, else stream-K over all SMs
+        p.csize = 1;
+        if (!std::getenv("RTNQ_WGEMM_CTAS") && int64_t(p.NB) * 2 <= imma::sms()) {
+            const char* ce = std::getenv("RTNQ_WGEMM_CLUSTER");
+            if (!ce || std::atoi(ce) != 0) {
+                int S = imma::sms() / p.NB;
+                S = S > 8 ? 8 : S;
+                S = S > p.KBLK ? p.KBLK : S;
+                p.csize = S < 2 ? 1 : S;
+            }
+        }
+        int G = imma::sms();
+        if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
+        G = G < 1 ? 1 : G;
+        p.G = int(p.U < G ? p.U : G);
+        cudaError_t e = nt == 16 ? i4::launch_nt<16>(p, st)
+                      : nt == 32 ? i4::launch_nt<32>(p, st)
+                                 : i4::launch_nt<64>(p, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace rtnq_b200

@@ -11,6 +11,7 @@ import pytest
 import paper_2505_15909_b200 as rq
 from conftest import ROOT, has_gpu
 from oracle import KERNEL, NATIVE, ROW_MAJOR
+from oracle import encode_native_i4, encode_native_i8
 
 
 def declared_symbols():
@@ -123,3 +124,25 @@ def test_f16_conversions_match_reference_golden(golden_f16):
     ref = golden_f16["widened"].view(np.float32)  # stored as f32 bit patterns
     same = widened.view(np.uint32) == ref.view(np.uint32)
     assert np.all(same | (np.isnan(widened) & np.isnan(ref)))
+
+
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("rows,cols", [(130, 208), (128, 128), (5, 96), (256, 384)])
+def test_int8_mma_layouts_match_numpy_restatement(bits, rows, cols):
+    """NATIVE_I8 / NATIVE_I4 (the kind::i8 kernels' operands): the host layout index of
+    every sampled code agrees with the numpy restatement's encoding, sizes included."""
+    rng = np.random.default_rng(rows * cols + bits)
+    lo, hi = (-128, 127) if bits == 8 else (-8, 7)
+    codes = rng.integers(lo, hi + 1, (rows, cols)).astype(np.int8)
+    kind, enc = (rq.NATIVE_I8, encode_native_i8) if bits == 8 else (rq.NATIVE_I4, encode_native_i4)
+    e = enc(codes)
+    lay = rq.layout(kind)
+    assert e.size == rq.layout_bytes(lay, bits, rows, cols)
+    for r, c in zip(rng.integers(0, rows, 400), rng.integers(0, cols, 400)):
+        idx = rq.layout_index(lay, bits, rows, cols, int(r), int(c))
+        if bits == 8:
+            v = int(e[idx].astype(np.int8))
+        else:
+            b = int(e[idx >> 1])
+            v = (((b >> 4) if idx & 1 else (b & 15)) ^ 8) - 8
+        assert v == int(codes[r, c]), (r, c)

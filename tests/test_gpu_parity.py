@@ -10,6 +10,7 @@ import pytest
 
 import paper_2505_15909_b200 as rq
 from oracle import KERNEL, NATIVE, ROW_MAJOR
+from oracle import encode_native_i4, encode_native_i8
 
 pytestmark = pytest.mark.gpu
 
@@ -292,3 +293,61 @@ def test_w8_per_channel_int8_path(oracle, n, k, m):
                        rq.SCALES_NATIVE, torch.float32)
     ref = a.double() @ wd.double().t()
     assert ((out.double() - ref).norm() / ref.norm()).item() <= TOL
+
+
+@pytest.mark.parametrize("n,k,m,act", [(4096, 4096, 1, "bfloat16"), (4096, 14336, 16, "bfloat16"),
+                                       (6144, 4096, 33, "float16"), (1000, 2048, 5, "bfloat16"),
+                                       (200, 208, 17, "float16"), (28672, 4096, 16, "bfloat16"),
+                                       (520, 1024, 80, "bfloat16"), (300, 4096, 64, "float16")])
+def test_w4_group128_int8_path(oracle, n, k, m, act):
+    """W4 group-128 runs tcgen05 kind::i8 over NATIVE_I4 nibble tiles (16 x code as s8,
+    one TMEM accumulator per group) with exact int8 activation planes: packing bit-exact
+    against the numpy restatement; output against the f64 oracle (small) or an f64 GEMM
+    over the exactly dequantized weights (large)."""
+    g = 128
+    gen = torch.Generator(device="cuda").manual_seed(n * 3 + k + m)
+    w = ((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+    q = rq.quantize_pack(w, 4, g, ragged=k % g != 0, row_major=True)
+    assert q.layout == rq.NATIVE_I4
+    logical = oracle.unpack(q.codes_row_major.cpu().numpy(), n * k, 4).reshape(n, k)
+    assert np.array_equal(q.codes.cpu().numpy(), encode_native_i4(logical))
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1, generator=gen).to(getattr(torch, act))
+    a[0, : k // 3] *= 1e-3  # a wide dynamic range inside one token
+    out = rq.linear(a, q, out_dtype=torch.float32)
+    assert torch.equal(out, rq.linear(a, q, out_dtype=torch.float32))  # deterministic
+    if n * k <= 1 << 22:
+        codes, scales = oracle.quantize(w.float().cpu().numpy(), 4, g, k % g != 0)
+        assert np.array_equal(codes, logical)
+        s16w = oracle.f16_round(scales).view(np.float16).astype(np.float32)
+        ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+        assert rel_frob(out.cpu().numpy(), ref) <= TOL
+    else:
+        wd = rq.dequantize(q.codes, rq.layout(rq.NATIVE_I4), 4, n, k, g, q.scales, rq.F16,
+                           rq.SCALES_NATIVE, torch.float32)
+        ref = a.double() @ wd.double().t()
+        assert ((out.double() - ref).norm() / ref.norm()).item() <= TOL
+
+
+def test_int8_mma_codes_bit_exact(oracle):
+    """The kind::i8 operands hold exactly the reference's codes, re-encoded (W8: two's
+    complement in 128x128 swizzled tiles; W4: nibble pairs in 128x128 group tiles)."""
+    for bits, g, enc, kind in ((8, 1024, encode_native_i8, rq.NATIVE_I8), (4, 128, encode_native_i4, rq.NATIVE_I4)):
+        n, k = 333, 1024
+        w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
+        q = rq.quantize_pack(w, bits, g)
+        assert q.layout == kind
+        codes, _ = oracle.quantize(w.float().cpu().numpy(), bits, g, False)
+        assert np.array_equal(q.codes.cpu().numpy(), enc(codes))
+
+
+def test_w4_group128_tc_kernel_still_reachable(oracle):
+    """native=True keeps W4 group-128 on the kind::f16 kernel (NATIVE layout); both
+    kernels agree."""
+    n, k, m = 1024, 2048, 7
+    w = ((torch.rand(n, k, device="cuda") * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+    q1 = rq.quantize_pack(w, 4, 128)
+    q2 = rq.quantize_pack(w, 4, 128, native=True)
+    assert (q1.layout, q2.layout) == (rq.NATIVE_I4, rq.NATIVE)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+    o1, o2 = rq.linear(a, q1, out_dtype=torch.float32), rq.linear(a, q2, out_dtype=torch.float32)
+    assert rel_frob(o1.cpu().numpy(), o2.cpu().numpy()) <= 2 * TOL
