@@ -18,8 +18,14 @@
 // Warp roles (384 threads):
 //   warp 0      TMA producer: codes (contiguous tiles) + the group scales of the stage
 //   warp 2      TMA producer: activation planes (after the planes kernel, PDL)
-//   warp 1      MMA issuer: 4 x (M128, N 3NT, K32) per group, A = expanded tile (smem)
-//   warps 8-11  expansion: nibble tile -> 16 KiB 128B-swizzled s8 tile; group scale / 16
+//   warp 1      MMA issuer: 4 x (M128, N 3NT, K32) per group, A = expanded tile (TMEM)
+//   warps 8-11  expansion: nibble tile (smem) -> registers -> tcgen05.st into a TMEM A slot
+//               (32 columns of 4 s8 each per row); group scale / 16 into the scale ring
+//
+// Shared-memory bandwidth (128 B/clk/SM) is the budget that shapes this: per 8 KiB group the
+// smem carries the TMA writes (codes 8 KiB + planes 3*NT*128) and the reads (codes 8 KiB +
+// planes by the MMA).  An expanded A tile staged in smem would add 32 KiB more per group;
+// in TMEM it costs no smem bandwidth at all.
 //   warps 4-7   epilogue: per-group TMEM reads, scaling, stream-K / cluster output
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -35,7 +41,6 @@ using namespace imma;
 
 constexpr int kKB = 128;              // k-block = one quantization group = one tile
 constexpr int kTile = kRows * 64;     // 8 KiB of nibbles
-constexpr int kATile = kRows * 128;   // 16 KiB of s8 after expansion
 constexpr int kThreads = 384;
 constexpr int kEpi0 = 4, kExp0 = 8;
 
@@ -59,14 +64,14 @@ struct Geo {
     static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
     static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
-    static constexpr int AS = 4;                            // expanded A tiles
-    static constexpr int STAGES_FIT = (214 * 1024 - AS * kATile) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
-    static constexpr int A_OFF = STAGES * STAGE_BYTES;
+    static constexpr int STAGES_FIT = (212 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int DN = 3 * NT;                       // accumulator columns per group
-    static constexpr int NS_FIT = 512 / DN;
-    static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;    // TMEM group slots
-    static constexpr int BAR_OFF = A_OFF + AS * kATile;
+    static constexpr int AS = NT <= 32 ? 4 : 2;             // expanded A tiles in TMEM
+    static constexpr int A_COL = 512 - AS * 32;             // A slots: 32 columns each
+    static constexpr int NS_FIT = A_COL / DN;
+    static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;    // TMEM group accumulators
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr int SR_OFF = BAR_OFF + 1024;           // [NS][128] f32 group scale / 16
     static constexpr int SMEM = SR_OFF + NS * kRows * 4 + 1024;
     static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (NT * kRows * 4);
@@ -77,8 +82,25 @@ struct Geo {
 
 __device__ unsigned long long g_i4_dbg[1024 * 16];  // profiling (debug & 64: globaltimer stamps)
 
-__device__ __forceinline__ void fence_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+// A from TMEM (32-bit columns of 4 s8 along K), B from shared memory
+__device__ __forceinline__ void mma_i8_ts_elect(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc,
+                                                uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+        "r"(a), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+        "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+        "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+        "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
 }
 __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64_t* b, uint32_t bytes) {
     asm volatile(
@@ -88,6 +110,10 @@ __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64
         "l"(src), "r"(bytes), "r"(su32(b))
         : "memory");
 }
+
+// debug & 32: per-role blocked/busy cycles (lane 0 of the first warp of each role)
+#define I4_T0() const long long _t0 = (p.debug & 32) ? clock64() : 0
+#define I4_ACC(var) if (p.debug & 32) var += clock64() - _t0
 
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
@@ -145,9 +171,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
         int s = 0;
         uint32_t ph = 0;
         if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes kernel
+        long long w_empty = 0;
         for (int i = 0; cu.more(); ++i) {
             const int n = cu.chunk();
-            if (i >= STAGES) mbar_wait(&empty[s], ph ^ 1u);
+            if (i >= STAGES) {
+                I4_T0();
+                mbar_wait(&empty[s], ph ^ 1u);
+                I4_ACC(w_empty);
+            }
             uint8_t* st = smem + s * GG::STAGE_BYTES;
             const int slot0 = cu.kb & (TPS - 1);
             if (codes) {
@@ -169,47 +200,74 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
+        if ((p.debug & 32) && lane == 0 && codes) g_i4_dbg[c * 16] = w_empty;
     } else if (warp >= kExp0) {
         // ===================== expansion: nibbles -> s8 (16 x code), 128B-swizzled =======
-        const int row = threadIdx.x - kExp0 * 32;  // one row of the tile per thread
-        const uint32_t sw_in = uint32_t((row >> 1) & 3), sw_out = uint32_t(row & 7);
+        const int row = threadIdx.x - kExp0 * 32;  // one row of the tile per thread = TMEM lane
+        const uint32_t sw_in = uint32_t((row >> 1) & 3);
+        const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
         Cursor<TPS> cu(u0, u1, p.KBLK);
         int s = 0, gi = 0;
         uint32_t ph = 0;
+        long long x_full = 0, x_aempty = 0, x_tfree = 0, x_work = 0;
         while (cu.more()) {
             const int n = cu.chunk();
             const int slot0 = cu.kb & (TPS - 1);
             const int64_t left = p.N - int64_t(cu.b) * kRows;
             const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
-            mbar_wait(&full[s], ph);
+            {
+                I4_T0();
+                mbar_wait(&full[s], ph);
+                I4_ACC(x_full);
+            }
             const uint8_t* st = smem + s * GG::STAGE_BYTES;
             for (int j = 0; j < n; ++j, ++gi) {
                 const int ai = gi % AS, ni = gi % NS;
-                if (gi >= AS) mbar_wait(&aempty[ai], uint32_t(gi / AS - 1) & 1u);
-                if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
+                {
+                    I4_T0();
+                    if (gi >= AS) mbar_wait(&aempty[ai], uint32_t(gi / AS - 1) & 1u);
+                    I4_ACC(x_aempty);
+                }
+                {
+                    I4_T0();
+                    if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
+                    I4_ACC(x_tfree);
+                }
+                const long long _tw = (p.debug & 32) ? clock64() : 0;
                 const uint8_t* src = st + GG::CODE_OFF + (slot0 + j) * kTile + row * 64;
-                uint8_t* dst = smem + GG::A_OFF + ai * kATile + row * 128;
+                uint32_t v[32];  // TMEM column c of this row holds k = 4c .. 4c + 3
 #pragma unroll
                 for (uint32_t q = 0; q < 4; ++q) {
                     const uint4 w = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
-                    const uint4 hi = make_uint4(w.x & 0xF0F0F0F0u, w.y & 0xF0F0F0F0u, w.z & 0xF0F0F0F0u,
-                                                w.w & 0xF0F0F0F0u);
-                    const uint4 lo = make_uint4((w.x << 4) & 0xF0F0F0F0u, (w.y << 4) & 0xF0F0F0F0u,
-                                                (w.z << 4) & 0xF0F0F0F0u, (w.w << 4) & 0xF0F0F0F0u);
-                    *reinterpret_cast<uint4*>(dst + ((q ^ sw_out) << 4)) = hi;
-                    *reinterpret_cast<uint4*>(dst + (((q + 4) ^ sw_out) << 4)) = lo;
+                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        v[4 * q + e] = ww[e] & 0xF0F0F0F0u;              // k = 16q + 4e ..
+                        v[16 + 4 * q + e] = (ww[e] << 4) & 0xF0F0F0F0u;  // k = 64 + 16q + 4e ..
+                    }
+                }
+                if (!(p.debug & 8)) {
+                    tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + ai * 32), v);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                } else if (v[0] == 0x12345u) {
+                    g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
                 }
                 const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
                 sring[ni * kRows + row] =
                     row < r8 ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
-                fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+                fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[ai]), mbar_arrive(&sfull[ni]);
+                if (p.debug & 32) x_work += clock64() - _tw;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // codes and scales of the stage consumed
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+        if ((p.debug & 32) && threadIdx.x == kExp0 * 32) {
+            g_i4_dbg[c * 16 + 2] = x_full, g_i4_dbg[c * 16 + 3] = x_aempty;
+            g_i4_dbg[c * 16 + 4] = x_tfree, g_i4_dbg[c * 16 + 6] = x_work;
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
@@ -222,31 +280,55 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
         Cursor<TPS> cu(u0, u1, p.KBLK);
         int s = 0, gi = 0;
         uint32_t ph = 0;
+        long long m_full = 0, m_afull = 0, m_tfree = 0, m_issue = 0, m_lat = 0;
         while (cu.more()) {
             const int n = cu.chunk();
             const int slot0 = cu.kb & (TPS - 1);
-            mbar_wait(&full[s], ph);  // the planes of this stage
+            {
+                I4_T0();
+                mbar_wait(&full[s], ph);  // the planes of this stage
+                I4_ACC(m_full);
+            }
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
             for (int j = 0; j < n; ++j, ++gi) {
                 const int ai = gi % AS, ni = gi % NS;
-                mbar_wait(&afull[ai], uint32_t(gi / AS) & 1u);
-                if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
+                {
+                    I4_T0();
+                    mbar_wait(&afull[ai], uint32_t(gi / AS) & 1u);
+                    I4_ACC(m_afull);
+                }
+                {
+                    I4_T0();
+                    if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
+                    I4_ACC(m_tfree);
+                }
                 fence_after();
-                const uint32_t alo = base + uint32_t((GG::A_OFF + ai * kATile) >> 4);
+                const long long _ti = (p.debug & 32) ? clock64() : 0;
+                const uint32_t a = tmem + uint32_t(GG::A_COL + ai * 32);
                 const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
                 const uint32_t d = tmem + uint32_t(ni * DN);
                 if (!(p.debug & 4)) {
 #pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k)  // K = 32 bytes per MMA: +2 in descriptor units
-                        mma_i8_elect(d, kHi | (alo + 2 * k), kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                    for (uint32_t k = 0; k < 4; ++k)  // K = 32 per MMA: A +8 columns, B +32 bytes
+                        mma_i8_ts_elect(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
                 }
                 commit_elect(&aempty[ai]);
                 commit_elect(&tfull[ni]);
+                if (p.debug & 32) {
+                    m_issue += clock64() - _ti;
+                    if (p.debug & 1024) {  // MMA completion latency (serialises the pipeline)
+                        mbar_wait(&tfull[ni], uint32_t(gi / NS) & 1u);
+                        m_lat += clock64() - _ti;
+                    }
+                }
             }
             commit_elect(&empty[s]);
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
+        if ((p.debug & 32) && lane == 0)
+            g_i4_dbg[c * 16 + 8] = m_full, g_i4_dbg[c * 16 + 9] = m_afull, g_i4_dbg[c * 16 + 10] = m_tfree,
+            g_i4_dbg[c * 16 + 1] = m_issue, g_i4_dbg[c * 16 + 7] = m_lat;
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
@@ -260,24 +342,36 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
         for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
         Cursor<TPS> cu(u0, u1, p.KBLK);
         int gi = 0, seg_kb0 = cu.kb;
+        long long e_wait = 0, e_work = 0;
+        const long long e_t0 = clock64();
         while (cu.more()) {
             const int n = cu.chunk();
             const bool seg_end = cu.seg_end(n);
             const int b = cu.b;
             for (int j = 0; j < n; ++j, ++gi) {
                 const int ni = gi % NS;
-                mbar_wait(&sfull[ni], uint32_t(gi / NS) & 1u);
-                mbar_wait(&tfull[ni], uint32_t(gi / NS) & 1u);
+                {
+                    I4_T0();
+                    mbar_wait(&sfull[ni], uint32_t(gi / NS) & 1u);
+                    mbar_wait(&tfull[ni], uint32_t(gi / NS) & 1u);
+                    I4_ACC(e_wait);
+                }
+                const long long _tw = (p.debug & 32) ? clock64() : 0;
                 fence_after();
                 const float sc = sring[ni * kRows + row];
 #pragma unroll
                 for (int jj = 0; jj < NT; jj += 16) {
                     uint32_t d0[16], d1[16], d2[16];
                     const uint32_t ta = tmem + lane_base + uint32_t(ni * DN + jj);
-                    ld16(ta, d0);
-                    ld16(ta + NT, d1);
-                    ld16(ta + 2 * NT, d2);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (!(p.debug & 16)) {
+                        ld16(ta, d0);
+                        ld16(ta + NT, d1);
+                        ld16(ta + 2 * NT, d2);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) d0[e] = d1[e] = d2[e] = uint32_t(row + e);
+                    }
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
                         const float x = float(int32_t(d0[e])) + float(int32_t(d1[e])) * 0.0078125f +
@@ -288,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tfree[ni]);
+                if (p.debug & 32) e_work += clock64() - _tw;
             }
             if (seg_end) {
                 const int kbe = cu.kb + n;
@@ -388,6 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
             }
             cu.advance(n);
         }
+        if ((p.debug & 32) && et == 0)
+            g_i4_dbg[c * 16 + 11] = e_wait, g_i4_dbg[c * 16 + 12] = e_work, g_i4_dbg[c * 16 + 13] = clock64() - e_t0,
+            g_i4_dbg[c * 16 + 14] = gi;
     }
     fence_before();
     __syncthreads();

@@ -10,6 +10,8 @@ __device__ __forceinline__ void commit(uint64_t* b) {
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(b)) : "memory"); }
 __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc) {
   asm volatile("{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(ad), "l"(bd), "r"(id), "r"(acc) : "memory"); }
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a, uint64_t bd, uint32_t id, uint32_t acc) {
+  asm volatile("{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(bd), "r"(id), "r"(acc) : "memory"); }
 __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc) {
   asm volatile("{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(ad), "l"(bd), "r"(id), "r"(acc) : "memory"); }
 template <int N>
@@ -48,6 +50,19 @@ __global__ void k(long long* out) {
       long long t1 = clock64();
       if (lane == 0) out[3] = (t1 - t0) / 256;
     }
+    {
+      // TS: A from TMEM (cols 256.. : 4 slots x 32 cols), B SW128 from smem
+      const uint64_t bhs = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+      long long t0 = clock64();
+      for (int i = 0; i < 256; ++i) {
+        const int slot = (i >> 2) & 3, ks = i & 3;
+        const uint64_t bd = bhs | (((b0 + ks * 32) >> 4) & 0x3FFF);
+        mma_i8_ts(tmem + ((i >> 2) & 1) * 128, tmem + 256 + slot * 32 + ks * 8, bd, id_i8, ks);
+      }
+      commit(&bar); mbar_wait(&bar, ph); ph ^= 1;
+      long long t1 = clock64();
+      if (lane == 0) out[4] = (t1 - t0) / 256;
+    }
     for (int pass = 0; pass < 3; ++pass) {
       long long t0 = clock64();
       for (int i = 0; i < 256; ++i) {
@@ -65,13 +80,13 @@ __global__ void k(long long* out) {
   if (warp == 0) { asm volatile("tcgen05.fence::after_thread_sync;"); asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)); }
 }
 int main() {
-  long long* d; cudaMalloc(&d, 64); long long h[4];
+  long long* d; cudaMalloc(&d, 64); long long h[5];
   auto run = [&](auto kern, int n) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     kern<<<1, 128, 100 * 1024>>>(d); cudaError_t e = cudaDeviceSynchronize();
     if (e) { printf("N=%d err %s\n", n, cudaGetErrorString(e)); return; }
-    cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
-    printf("N=%3d: kind::i8 SS (K=32) %lld / %lld cycles/MMA; kind::f16 SS (K=16) %lld; i8 SW128 A %lld\n", n, h[0], h[1], h[2], h[3]);
+    cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
+    printf("N=%3d: kind::i8 SS (K=32) %lld / %lld cycles/MMA; kind::f16 SS (K=16) %lld; i8 SW128 A %lld; i8 TS %lld\n", n, h[0], h[1], h[2], h[3], h[4]);
   };
   run(k<16>, 16); run(k<48>, 48); run(k<96>, 96);
   return 0;
