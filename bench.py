@@ -120,6 +120,11 @@ def ncu_traffic(bits, batch):
 
 
 # ---------------------------------------------------------------------------------------
+def _trace(msg):
+    if os.environ.get("BENCH_TRACE"):
+        print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -230,11 +235,14 @@ def run_gpu(args):
         step_bytes = int(t.item())
 
     main = bufs(B)
+    _trace("stack built")
     graph = capture(lambda: gemm_step(main))
+    _trace(f"captured (graph={graph is not None})")
     with ClockSampler(local) as clk:
         ms = timed(runner(graph, lambda: gemm_step(main)), args.steps, args.warmup)
     value = step_bytes / (ms * 1e-3) / 1e9
     peak, peak_src = peaks()
+    _trace(f"timed step {ms:.3f} ms")
 
     sweep = {}
     for b in args.sweep:
@@ -246,6 +254,7 @@ def run_gpu(args):
         msb = timed(runner(gb, lambda: gemm_step(bb)), max(3, args.steps // 2), args.warmup)
         sweep[str(b)] = round(step_bytes / (msb * 1e-3) / 1e9, 1)
         del gb
+        _trace(f"sweep {b} done")
 
     # ---- e2e: pinned host activations in, host outputs back, through the public API ----
     hin = {k: torch.empty_like(main[k], device="cpu").uniform_(-1, 1).pin_memory()
@@ -266,6 +275,7 @@ def run_gpu(args):
                 t.copy_(main[k], non_blocking=True)
 
     ms_e2e = timed(e2e_step, args.steps, args.warmup)
+    _trace("e2e done")
     e2e = step_bytes / (ms_e2e * 1e-3) / 1e9
 
     # ---- the full decode step (norms, attention over the KV cache, SiLU, allreduces) ----
@@ -274,6 +284,7 @@ def run_gpu(args):
     ms_dec = timed(runner(dgraph, lambda: stack.step(x0, stream=stream, pdl=args.pdl)),
                    max(3, args.steps // 2), args.warmup)
 
+    _trace("decode step done")
     linears = nl * 4
     # ---- roofline of the dominant kernel: the largest linear (ffn_up), 20 back-to-back
     # launches over 4 weight copies (> L2) in a CUDA graph, CUDA events on its stream ----

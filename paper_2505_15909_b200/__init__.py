@@ -270,11 +270,15 @@ class Workspace:
     def __init__(self, nbytes: int = 0, device="cuda"):
         torch = _torch()
         self.device = device
+        self._retired = []
         self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
 
     def ensure(self, nbytes: int):
         torch = _torch()
         if self.buf.numel() < nbytes:
+            # keep the old buffer alive: a CUDA graph captured earlier still launches kernels
+            # whose stream-K counters and partials live in it
+            self._retired.append(self.buf)
             self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         return self.buf
 
