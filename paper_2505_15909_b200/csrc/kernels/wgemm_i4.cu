@@ -41,8 +41,7 @@ using namespace imma;
 
 constexpr int kKB = 128;              // k-block = one quantization group = one tile
 constexpr int kTile = kRows * 64;     // 8 KiB of nibbles
-constexpr int kThreads = 384;
-constexpr int kEpi0 = 4, kExp0 = 8;
+constexpr int kEpi0 = 4, kExp0 = 8, kEpiB0 = 12;  // epilogue warpgroup B: warps 12-15
 
 struct Params {
     CUtensorMap tmap_p;      // planes [3][M][K] s8, box {128, NT, 3}, SWIZZLE_128B
@@ -64,16 +63,23 @@ struct Geo {
     static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
     static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
-    static constexpr int STAGES_FIT = (212 * 1024) / STAGE_BYTES;
+    // two epilogue warpgroups (one per group of a stage) when a stage holds two groups
+    static constexpr int EW = 1;  // 2 (a warpgroup per group of a stage) measured slower: TMEM reads are the limit
+    static constexpr int THREADS = EW == 2 ? 512 : 384;
+    static constexpr int SCR_BYTES = EW == 2 ? NT * kRows * 4 : 0;  // warpgroup B's partial sums
+    static constexpr int STAGES_FIT = (212 * 1024 - SCR_BYTES) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int DN = 3 * NT;                       // accumulator columns per group
     static constexpr int AS = NT <= 32 ? 4 : 2;             // expanded A tiles in TMEM
+    static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
     static constexpr int A_COL = 512 - AS * 32;             // A slots: 32 columns each
     static constexpr int NS_FIT = A_COL / DN;
     static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;    // TMEM group accumulators
+    static constexpr int NP = NS / TPS;                     // ... in stage-sized slots
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr int SR_OFF = BAR_OFF + 1024;           // [NS][128] f32 group scale / 16
-    static constexpr int SMEM = SR_OFF + NS * kRows * 4 + 1024;
+    static constexpr int SCR_OFF = SR_OFF + NS * kRows * 4;
+    static constexpr int SMEM = SCR_OFF + SCR_BYTES + 1024;
     static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (NT * kRows * 4);
     static constexpr int MAXC = MAXC_FIT > 8 ? 8 : MAXC_FIT;
     static_assert(STAGES >= 3, "");
@@ -116,22 +122,24 @@ __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64
 #define I4_ACC(var) if (p.debug & 32) var += clock64() - _t0
 
 template <int NT>
-__global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
     using GG = Geo<NT>;
-    constexpr int STAGES = GG::STAGES, DN = GG::DN, NS = GG::NS, AS = GG::AS, TPS = GG::TPS;
+    constexpr int STAGES = GG::STAGES, DN = GG::DN, AP = GG::AP, NP = GG::NP, TPS = GG::TPS, EW = GG::EW;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // align by indexing the __shared__ array (keeps the shared address space: LDS/STS, not
+    // generic loads)
+    uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);  // [STAGES] TMA landed
     uint64_t* empty = full + STAGES;    // [STAGES] expansion (4) + MMA commit (1) done with it
-    uint64_t* afull = empty + STAGES;   // [AS] expanded tile ready (4 warps)
-    uint64_t* aempty = afull + AS;      // [AS] MMA done reading it (commit)
-    uint64_t* tfull = aempty + AS;      // [NS] group accumulator ready (commit)
-    uint64_t* tfree = tfull + NS;       // [NS] epilogue has read it (4 warps)
-    uint64_t* sfull = tfree + NS;       // [NS] group scales in the scale ring (4 warps)
-    uint64_t* go = sfull + NS;          // cluster split-K: leader ready for partials
+    uint64_t* afull = empty + STAGES;   // [AP] a stage's expanded tiles ready (4 warps)
+    uint64_t* aempty = afull + AP;      // [AP] MMA done reading them (commit)
+    uint64_t* tfull = aempty + AP;      // [NP] a stage's group accumulators ready (commit)
+    uint64_t* tfree = tfull + NP;       // [NP] epilogue has read them (4 warps)
+    uint64_t* sfull = tfree + NP;       // [NP] their group scales in the scale ring (4 warps)
+    uint64_t* go = sfull + NP;          // cluster split-K: leader ready for partials
     uint64_t* rfull = go + 1;           // cluster split-K: partials landed in the leader
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(rfull + 1);
+    uint64_t* pub = rfull + 1;          // stream-K contributor partials stored (4 warps)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(pub + 1);
     float* sring = reinterpret_cast<float*>(smem + GG::SR_OFF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
     if ((p.debug & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 5] = gtime();
@@ -147,9 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 5);
-        for (int i = 0; i < AS; ++i) mbar_init(&afull[i], 4), mbar_init(&aempty[i], 1);
-        for (int i = 0; i < NS; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4), mbar_init(&sfull[i], 4);
-        mbar_init(go, 1), mbar_init(rfull, 1);
+        for (int i = 0; i < AP; ++i) mbar_init(&afull[i], 4), mbar_init(&aempty[i], 1);
+        for (int i = 0; i < NP; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4 * EW), mbar_init(&sfull[i], 4);
+        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -181,7 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
             }
             uint8_t* st = smem + s * GG::STAGE_BYTES;
             const int slot0 = cu.kb & (TPS - 1);
-            if (codes) {
+            if ((p.debug & 2) || (codes && (p.debug & 8192)) || (!codes && (p.debug & 4096))) {
+                elect_arrive(&full[s]);  // profiling: no copy
+            } else if (codes) {
                 // the row-block's rows padded to 8: the stride of its native scale groups
                 const int64_t left = p.N - int64_t(cu.b) * kRows;
                 const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
@@ -201,13 +211,23 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
         if ((p.debug & 32) && lane == 0 && codes) g_i4_dbg[c * 16] = w_empty;
-    } else if (warp >= kExp0) {
-        // ===================== expansion: nibbles -> s8 (16 x code), 128B-swizzled =======
+    } else if (warp == 3) {
+        // ===================== stream-K publisher =====================
+        if (p.csize == 1 && u0 < u1 && u0 % p.KBLK != 0) {
+            mbar_wait(pub, 0);
+            if (lane == 0) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + u0 / p.KBLK) : "memory");
+            }
+        }
+    } else if (warp >= kExp0 && warp < kExp0 + 4) {
+        // ===================== expansion: nibbles -> s8 (16 x code) in TMEM ===============
+        // One handshake per stage (TPS groups): A pair slot si % AP, accumulator slot si % NP.
         const int row = threadIdx.x - kExp0 * 32;  // one row of the tile per thread = TMEM lane
         const uint32_t sw_in = uint32_t((row >> 1) & 3);
         const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
         Cursor<TPS> cu(u0, u1, p.KBLK);
-        int s = 0, gi = 0;
+        int s = 0, si = 0;
         uint32_t ph = 0;
         long long x_full = 0, x_aempty = 0, x_tfree = 0, x_work = 0;
         while (cu.more()) {
@@ -215,54 +235,69 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
             const int slot0 = cu.kb & (TPS - 1);
             const int64_t left = p.N - int64_t(cu.b) * kRows;
             const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
+            const int ap = si % AP, np = si % NP;
             {
                 I4_T0();
                 mbar_wait(&full[s], ph);
                 I4_ACC(x_full);
             }
-            const uint8_t* st = smem + s * GG::STAGE_BYTES;
-            for (int j = 0; j < n; ++j, ++gi) {
-                const int ai = gi % AS, ni = gi % NS;
-                {
-                    I4_T0();
-                    if (gi >= AS) mbar_wait(&aempty[ai], uint32_t(gi / AS - 1) & 1u);
-                    I4_ACC(x_aempty);
-                }
-                {
-                    I4_T0();
-                    if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
-                    I4_ACC(x_tfree);
-                }
-                const long long _tw = (p.debug & 32) ? clock64() : 0;
-                const uint8_t* src = st + GG::CODE_OFF + (slot0 + j) * kTile + row * 64;
-                uint32_t v[32];  // TMEM column c of this row holds k = 4c .. 4c + 3
-#pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    const uint4 w = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
-                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        v[4 * q + e] = ww[e] & 0xF0F0F0F0u;              // k = 16q + 4e ..
-                        v[16 + 4 * q + e] = (ww[e] << 4) & 0xF0F0F0F0u;  // k = 64 + 16q + 4e ..
-                    }
-                }
-                if (!(p.debug & 8)) {
-                    tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + ai * 32), v);
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                } else if (v[0] == 0x12345u) {
-                    g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
-                }
-                const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
-                sring[ni * kRows + row] =
-                    row < r8 ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&afull[ai]), mbar_arrive(&sfull[ni]);
-                if (p.debug & 32) x_work += clock64() - _tw;
+            {
+                I4_T0();
+                if (si >= AP) mbar_wait(&aempty[ap], uint32_t(si / AP - 1) & 1u);
+                I4_ACC(x_aempty);
             }
+            {
+                I4_T0();
+                if (si >= NP) mbar_wait(&tfree[np], uint32_t(si / NP - 1) & 1u);
+                I4_ACC(x_tfree);
+            }
+            const long long _tw = (p.debug & 32) ? clock64() : 0;
+            const uint8_t* st = smem + s * GG::STAGE_BYTES;
+            if (!(p.debug & 65536)) {
+                // all of the stage's code loads first (latency overlap), then expand and store
+                uint4 w[TPS][4];
+#pragma unroll
+                for (int j = 0; j < TPS; ++j)
+                    if (j < n) {
+                        const uint8_t* src = st + GG::CODE_OFF + (slot0 + j) * kTile + row * 64;
+#pragma unroll
+                        for (uint32_t q = 0; q < 4; ++q)
+                            w[j][q] = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
+                    }
+                float scv[TPS];
+#pragma unroll
+                for (int j = 0; j < TPS; ++j) {
+                    const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
+                    scv[j] = (j < n && row < r8) ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
+                }
+#pragma unroll
+                for (int j = 0; j < TPS; ++j) {
+                    if (j >= n) break;
+                    uint32_t v[32];  // TMEM column c of this row holds k = 4c .. 4c + 3
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q) {
+                        const uint32_t ww[4] = {w[j][q].x, w[j][q].y, w[j][q].z, w[j][q].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            v[4 * q + e] = ww[e] & 0xF0F0F0F0u;               // k = 16q + 4e ..
+                            v[16 + 4 * q + e] = (ww[e] & 0x0F0F0F0Fu) * 16u;  // k = 64 + 16q + 4e ..
+                        }
+                    }
+                    if (!(p.debug & 8)) {
+                        tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + (ap * TPS + j) * 32), v);
+                    } else if (v[0] == 0x12345u) {
+                        g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
+                    }
+                    sring[(np * TPS + j) * kRows + row] = scv[j];
+                }
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // codes and scales of the stage consumed
+            if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
+            if (p.debug & 32) x_work += clock64() - _tw;
             cu.advance(n);
+            ++si;
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
         if ((p.debug & 32) && threadIdx.x == kExp0 * 32) {
@@ -271,120 +306,164 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
-        // D s32, A s8 (16 x codes), B s8 (planes), M = 128, N = 3 * NT
+        // D s32, A s8 (16 x codes, TMEM), B s8 (planes, smem), M = 128, N = 3 * NT
         constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                    (uint32_t(DN >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
         constexpr uint64_t kHi = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
                                  (2ull << 61);  // K-major SWIZZLE_128B, SBO = 1024
         const uint32_t base = su32(smem) >> 4;
         Cursor<TPS> cu(u0, u1, p.KBLK);
-        int s = 0, gi = 0;
+        int s = 0, si = 0;
         uint32_t ph = 0;
-        long long m_full = 0, m_afull = 0, m_tfree = 0, m_issue = 0, m_lat = 0;
+        long long m_full = 0, m_afull = 0, m_tfree = 0, m_issue = 0;
         while (cu.more()) {
             const int n = cu.chunk();
             const int slot0 = cu.kb & (TPS - 1);
+            const int ap = si % AP, np = si % NP;
             {
                 I4_T0();
                 mbar_wait(&full[s], ph);  // the planes of this stage
                 I4_ACC(m_full);
             }
+            {
+                I4_T0();
+                mbar_wait(&afull[ap], uint32_t(si / AP) & 1u);
+                I4_ACC(m_afull);
+            }
+            {
+                I4_T0();
+                if (si >= NP) mbar_wait(&tfree[np], uint32_t(si / NP - 1) & 1u);
+                I4_ACC(m_tfree);
+            }
+            fence_after();
+            const long long _ti = (p.debug & 32) ? clock64() : 0;
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
-            for (int j = 0; j < n; ++j, ++gi) {
-                const int ai = gi % AS, ni = gi % NS;
-                {
-                    I4_T0();
-                    mbar_wait(&afull[ai], uint32_t(gi / AS) & 1u);
-                    I4_ACC(m_afull);
-                }
-                {
-                    I4_T0();
-                    if (gi >= NS) mbar_wait(&tfree[ni], uint32_t(gi / NS - 1) & 1u);
-                    I4_ACC(m_tfree);
-                }
-                fence_after();
-                const long long _ti = (p.debug & 32) ? clock64() : 0;
-                const uint32_t a = tmem + uint32_t(GG::A_COL + ai * 32);
-                const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
-                const uint32_t d = tmem + uint32_t(ni * DN);
-                if (!(p.debug & 4)) {
+            if (!(p.debug & 4)) {
+                for (int j = 0; j < n; ++j) {
+                    const uint32_t a = tmem + uint32_t(GG::A_COL + (ap * TPS + j) * 32);
+                    const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
+                    const uint32_t d = tmem + uint32_t((np * TPS + j) * DN);
 #pragma unroll
                     for (uint32_t k = 0; k < 4; ++k)  // K = 32 per MMA: A +8 columns, B +32 bytes
                         mma_i8_ts_elect(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
                 }
-                commit_elect(&aempty[ai]);
-                commit_elect(&tfull[ni]);
-                if (p.debug & 32) {
-                    m_issue += clock64() - _ti;
-                    if (p.debug & 1024) {  // MMA completion latency (serialises the pipeline)
-                        mbar_wait(&tfull[ni], uint32_t(gi / NS) & 1u);
-                        m_lat += clock64() - _ti;
-                    }
-                }
             }
+            commit_elect(&aempty[ap]);
+            commit_elect(&tfull[np]);
             commit_elect(&empty[s]);
+            if (p.debug & 32) m_issue += clock64() - _ti;
             cu.advance(n);
+            ++si;
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
         if ((p.debug & 32) && lane == 0)
             g_i4_dbg[c * 16 + 8] = m_full, g_i4_dbg[c * 16 + 9] = m_afull, g_i4_dbg[c * 16 + 10] = m_tfree,
-            g_i4_dbg[c * 16 + 1] = m_issue, g_i4_dbg[c * 16 + 7] = m_lat;
+            g_i4_dbg[c * 16 + 1] = m_issue;
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
+        // warpgroup A (warps 4-7) takes group 0 of every stage and does all output; with two
+        // groups per stage, warpgroup B (warps 12-15) takes group 1 and hands its sums over
+        // through shared memory at each segment end.
+        const int eg = warp >= kEpiB0 ? 1 : 0;
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
         const uint32_t lane_base = uint32_t(q * 32) << 16;
+        float* scr = reinterpret_cast<float*>(smem + GG::SCR_OFF);
         __shared__ float pow_s[NT];  // 2^s per token, 0 for padding tokens
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // texp comes from the planes kernel
-        for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (eg == 0) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");  // texp comes from the planes kernel
+            for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         float acc[NT];
 #pragma unroll
         for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
         Cursor<TPS> cu(u0, u1, p.KBLK);
-        int gi = 0, seg_kb0 = cu.kb;
-        long long e_wait = 0, e_work = 0;
+        int si = 0, seg_kb0 = cu.kb;
+        long long e_wait = 0, e_work = 0, e_ld = 0;
         const long long e_t0 = clock64();
         while (cu.more()) {
             const int n = cu.chunk();
             const bool seg_end = cu.seg_end(n);
             const int b = cu.b;
-            for (int j = 0; j < n; ++j, ++gi) {
-                const int ni = gi % NS;
-                {
-                    I4_T0();
-                    mbar_wait(&sfull[ni], uint32_t(gi / NS) & 1u);
-                    mbar_wait(&tfull[ni], uint32_t(gi / NS) & 1u);
-                    I4_ACC(e_wait);
-                }
-                const long long _tw = (p.debug & 32) ? clock64() : 0;
-                fence_after();
-                const float sc = sring[ni * kRows + row];
+            const int np = si % NP;
+            {
+                I4_T0();
+                mbar_wait(&sfull[np], uint32_t(si / NP) & 1u);
+                mbar_wait(&tfull[np], uint32_t(si / NP) & 1u);
+                I4_ACC(e_wait);
+            }
+            const long long _tw = (p.debug & 32) ? clock64() : 0;
+            fence_after();
+            float scg[TPS];
 #pragma unroll
-                for (int jj = 0; jj < NT; jj += 16) {
-                    uint32_t d0[16], d1[16], d2[16];
-                    const uint32_t ta = tmem + lane_base + uint32_t(ni * DN + jj);
+            for (int j = 0; j < TPS; ++j) scg[j] = j < n ? sring[(np * TPS + j) * kRows + row] : 0.0f;
+            // this warpgroup's groups of the stage: [j0, j1)
+            const int j0 = EW == 2 ? eg : 0, j1 = EW == 2 ? (eg < n ? eg + 1 : eg) : n;
+#pragma unroll
+            for (int jj = 0; jj < ((p.debug & 131072) ? 0 : NT); jj += 16) {
+                // the 16-token chunk of every group of the stage: all TMEM loads, one wait
+                uint32_t d[TPS][3][16];
+#pragma unroll
+                for (int j = 0; j < TPS; ++j) {
+                    if (j < j0 || j >= j1) continue;
+                    const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
                     if (!(p.debug & 16)) {
-                        ld16(ta, d0);
-                        ld16(ta + NT, d1);
-                        ld16(ta + 2 * NT, d2);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        ld16(ta, d[j][0]);
+                        ld16(ta + NT, d[j][1]);
+                        ld16(ta + 2 * NT, d[j][2]);
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) d0[e] = d1[e] = d2[e] = uint32_t(row + e);
-                    }
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float x = float(int32_t(d0[e])) + float(int32_t(d1[e])) * 0.0078125f +
-                                        float(int32_t(d2[e])) * 6.103515625e-05f;
-                        acc[jj + e] = fmaf(x, sc * pow_s[jj + e], acc[jj + e]);
+                        for (int e = 0; e < 16; ++e) d[j][0][e] = d[j][1][e] = d[j][2][e] = uint32_t(row + e);
                     }
                 }
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tfree[ni]);
-                if (p.debug & 32) e_work += clock64() - _tw;
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (p.debug & 32) {
+                    const long long t = clock64();
+                    e_ld += t - _tw;
+                }
+#pragma unroll
+                for (int j = 0; j < TPS; ++j) {
+                    if (j < j0 || j >= j1) continue;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {  // 2^s per token is applied at the segment end
+                        // |D| < 2^21 per group: int -> float as (bits(D + 1.5 * 2^23) - 1.5 * 2^23),
+                        // two full-rate ops instead of the 1/8-rate I2F
+                        const float x0 = __int_as_float(int32_t(d[j][0][e]) + 0x4B400000) - 12582912.0f;
+                        const float x1 = __int_as_float(int32_t(d[j][1][e]) + 0x4B400000) - 12582912.0f;
+                        const float x2 = __int_as_float(int32_t(d[j][2][e]) + 0x4B400000) - 12582912.0f;
+                        const float x = fmaf(x2, 6.103515625e-05f, fmaf(x1, 0.0078125f, x0));
+                        acc[jj + e] = fmaf(x, scg[j], acc[jj + e]);
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tfree[np]);
+            if (p.debug & 32) e_work += clock64() - _tw;
+            ++si;
+            if (seg_end && EW == 2) {  // warpgroup B -> A through shared memory
+                float4* sc4 = reinterpret_cast<float4*>(scr) + row * (NT / 4);
+                if (eg == 1) {
+#pragma unroll
+                    for (int j = 0; j < NT / 4; ++j)
+                        sc4[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                }
+                asm volatile("bar.sync 2, 256;" ::: "memory");
+                if (eg == 1) {
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+                    cu.advance(n);
+                    continue;
+                }
+#pragma unroll
+                for (int j = 0; j < NT / 4; ++j) {
+                    const float4 x = sc4[j];
+                    acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
+                }
             }
             if (seg_end) {
+#pragma unroll
+                for (int t = 0; t < NT; ++t) acc[t] *= pow_s[t];
                 const int kbe = cu.kb + n;
                 const bool sole = seg_kb0 == 0 && kbe == p.KBLK;
                 const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
@@ -466,15 +545,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
                             for (int m = 0; m < NT; ++m)
                                 if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
                     } else {
+                        // contributor (its first segment): store the partial; warp 3 publishes it
+                        // (gpu-scope fence + counter), off this pipeline's critical path
                         float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
 #pragma unroll
                         for (int j = 0; j < NT / 4; ++j)
                             mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-                        asm volatile("bar.sync 1, 128;" ::: "memory");
-                        if (et == 0) {
-                            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                            asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + b) : "memory");
-                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(pub);
                     }
                 }
 #pragma unroll
@@ -483,9 +561,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i4_kernel(const __grid_cons
             }
             cu.advance(n);
         }
-        if ((p.debug & 32) && et == 0)
+        if ((p.debug & 32) && et == 0 && eg == 0)
             g_i4_dbg[c * 16 + 11] = e_wait, g_i4_dbg[c * 16 + 12] = e_work, g_i4_dbg[c * 16 + 13] = clock64() - e_t0,
-            g_i4_dbg[c * 16 + 14] = gi;
+            g_i4_dbg[c * 16 + 14] = si, g_i4_dbg[c * 16 + 15] = e_ld;
     }
     fence_before();
     __syncthreads();
@@ -513,7 +591,7 @@ cudaError_t launch_nt(Params p, cudaStream_t st) {
         if (mc == 0) {
             cudaLaunchConfig_t q{};
             q.gridDim = dim3(unsigned(p.NB * p.csize));
-            q.blockDim = dim3(kThreads);
+            q.blockDim = dim3(GG::THREADS);
             q.dynamicSmemBytes = GG::SMEM;
             cudaLaunchAttribute ca;
             ca.id = cudaLaunchAttributeClusterDimension;
@@ -531,7 +609,7 @@ cudaError_t launch_nt(Params p, cudaStream_t st) {
     else p.csize = 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(p.G));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(GG::THREADS);
     cfg.dynamicSmemBytes = GG::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];

@@ -84,15 +84,17 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     using GG = Geo<NT>;
     constexpr int STAGES = GG::STAGES, DN = GG::DN;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // align by indexing the __shared__ array (keeps the shared address space: LDS/STS, not
+    // generic loads)
+    uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);  // [STAGES]
     uint64_t* empty = full + STAGES;                                  // [STAGES]
     uint64_t* dfull = empty + STAGES;                                 // [2]
     uint64_t* dempty = dfull + 2;                                     // [2]
     uint64_t* go = dempty + 2;      // cluster split-K: the leader is ready for partials
     uint64_t* rfull = dempty + 3;   // cluster split-K: all partials landed in the leader
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 4);
+    uint64_t* pub = dempty + 4;     // stream-K contributor partials stored (4 warps)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 5);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
     if ((p.debug & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 5] = gtime();
 
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
         for (int i = 0; i < 2; ++i) mbar_init(&dfull[i], 1), mbar_init(&dempty[i], 4);
-        mbar_init(go, 1), mbar_init(rfull, 1);
+        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -184,6 +186,15 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             g_i8_dbg[c * 8 + 1] = tw;
         }
         if ((p.debug & 64) && lane == 0 && codes) g_i8_dbg[c * 16 + 0] = gtime();
+    } else if (warp == 3) {
+        // ===================== stream-K publisher (off the epilogue's critical path) =======
+        if (p.csize == 1 && u0 < u1 && u0 % p.KBLK != 0) {
+            mbar_wait(pub, 0);
+            if (lane == 0) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + u0 / p.KBLK) : "memory");
+            }
+        }
     } else if (warp == 1) {
         // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
         // D s32, A s8 (codes), B s8 (planes), M = 128, N = 3 * NT
@@ -394,11 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
 #pragma unroll
                 for (int j = 0; j < NT / 4; ++j)
                     mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (et == 0) {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + b) : "memory");
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(pub);  // warp 3 publishes (gpu-scope fence + counter)
             }
             if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 11] = gtime();
             u = uu;

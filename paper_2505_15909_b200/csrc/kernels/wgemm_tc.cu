@@ -454,8 +454,9 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     using GG = Geo<BITS, NT>;
     constexpr int CPR = GG::CPR, STAGES = GG::STAGES, KPU = GG::KPU;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // align by indexing the __shared__ array (keeps the shared address space: LDS/STS, not
+    // generic loads)
+    uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GG::BAR_OFF);
     // Barrier protocol (one tcgen05.commit per unit):
     //   full[s]    producer (TMA complete_tx) -> dequant, MMA

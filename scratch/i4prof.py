@@ -9,7 +9,7 @@ a = torch.randn(8192, 8192, device="cuda")
 for _ in range(30): a @ a
 names = {0: "prod wait empty", 1: "mma issue", 7: "mma lat(1024)", 2: "exp wait full", 3: "exp wait aempty", 4: "exp wait tfree",
          6: "exp work", 8: "mma wait full", 9: "mma wait afull", 10: "mma wait tfree", 11: "epi wait", 12: "epi work",
-         13: "epi total", 14: "groups"}
+         13: "epi total", 14: "stages", 15: "epi ld (incl. sring)"}
 for name, n, k in [("qkv", 6144, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]:
     w = (torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16)
     q = rq.quantize_pack(w, 4, 128)
