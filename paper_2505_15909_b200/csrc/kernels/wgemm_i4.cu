@@ -10,7 +10,10 @@
 // The factor 16 is folded into the group scale.
 //
 // Activations: the three exact int8 planes of int8_mma.cuh (a = 2^s (P0 + P1/2^7 + P2/2^14)),
-// the s8 B operand with N = 3 * NT.
+// the s8 B operand.  PT tokens per launch chunk (5, 10, 16, 32 or 64): B row p * PT + t is plane
+// p of token t, N = 3 * PT rounded up to 16 (the rows past 3 * PT are zero).  Small batches
+// get small N: the epilogue reads back N accumulator columns per group, and TMEM reads (64 B
+// per clock per SM) are the budget that binds this kernel (A reads of the MMA + readback).
 //
 // Each group has its own int32 accumulator in TMEM (a ring of NS slots): the epilogue reads
 // it once, applies S[n][g] / 16 * 2^s and adds into per-row float accumulators.
@@ -18,12 +21,12 @@
 // Warp roles (384 threads):
 //   warp 0      TMA producer: codes (contiguous tiles) + the group scales of the stage
 //   warp 2      TMA producer: activation planes (after the planes kernel, PDL)
-//   warp 1      MMA issuer: 4 x (M128, N 3NT, K32) per group, A = expanded tile (TMEM)
+//   warp 1      MMA issuer: 4 x (M128, N, K32) per group, A = expanded tile (TMEM)
 //   warps 8-11  expansion: nibble tile (smem) -> registers -> tcgen05.st into a TMEM A slot
 //               (32 columns of 4 s8 each per row); group scale / 16 into the scale ring
 //
 // Shared-memory bandwidth (128 B/clk/SM) is the budget that shapes this: per 8 KiB group the
-// smem carries the TMA writes (codes 8 KiB + planes 3*NT*128) and the reads (codes 8 KiB +
+// smem carries the TMA writes (codes 8 KiB + planes N*128) and the reads (codes 8 KiB +
 // planes by the MMA).  An expanded A tile staged in smem would add 32 KiB more per group;
 // in TMEM it costs no smem bandwidth at all.
 //   warps 4-7   epilogue: per-group TMEM reads, scaling, stream-K / cluster output
@@ -44,7 +47,7 @@ constexpr int kTile = kRows * 64;     // 8 KiB of nibbles
 constexpr int kEpi0 = 4, kExp0 = 8, kEpiB0 = 12;  // epilogue warpgroup B: warps 12-15
 
 struct Params {
-    CUtensorMap tmap_p;      // planes [3][M][K] s8, box {128, NT, 3}, SWIZZLE_128B
+    CUtensorMap tmap_p;      // planes [3][M][K] s8, box {128, PT, 3}, SWIZZLE_128B
     const uint8_t* codes;    // RTNQ_NATIVE_I4
     const uint16_t* scales;  // f16, native order [row-block][group][rows8]
     const int32_t* texp;     // [M] token exponents s
@@ -56,31 +59,40 @@ struct Params {
     int debug;
 };
 
-template <int NT>
+template <int PT>
 struct Geo {
-    static constexpr int PLANE_BYTES = 3 * NT * 128;       // one group's planes box
-    static constexpr int TPS = NT <= 32 ? 2 : 1;            // groups (tiles) per stage
+    static constexpr int ACC = (PT + 3) / 4 * 4;            // per-row accumulators (float4 I/O)
+    static constexpr int DN = (3 * PT + 15) / 16 * 16;      // accumulator columns per group
+    static constexpr int BOX_BYTES = 3 * PT * 128;          // one group's planes box
+    static constexpr int PLANE_BYTES = DN * 128;            // ... its smem slot (zero rows past it)
+    static constexpr int TPS = PT <= 32 ? 2 : 1;            // groups (tiles) per stage
     static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
     static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
     // two epilogue warpgroups (one per group of a stage) when a stage holds two groups
     static constexpr int EW = 1;  // 2 (a warpgroup per group of a stage) measured slower: TMEM reads are the limit
     static constexpr int THREADS = EW == 2 ? 512 : 384;
-    static constexpr int SCR_BYTES = EW == 2 ? NT * kRows * 4 : 0;  // warpgroup B's partial sums
-    static constexpr int STAGES_FIT = (212 * 1024 - SCR_BYTES) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int DN = 3 * NT;                       // accumulator columns per group
-    static constexpr int AS = NT <= 32 ? 4 : 2;             // expanded A tiles in TMEM
+    static constexpr int SCR_BYTES = EW == 2 ? ACC * kRows * 4 : 0;  // warpgroup B's partial sums
+    // The A operand of a group is 4 k-steps of 32 codes.  The first KT come from TMEM (tcgen05.st
+    // by the expansion; the MMA's A reads share the 64 B/clk TMEM read port with the epilogue's
+    // accumulator readback), the rest from a 128B-swizzled smem tile (128 B/clk smem port,
+    // shared with TMA and the planes).  KT balances the two ports for the batch size.
+    static constexpr int KT = PT <= 16 ? 4 : 0;
+    static constexpr int AS = PT <= 10 ? 8 : PT <= 32 ? 4 : 2;  // expanded A slots (groups)
     static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
-    static constexpr int A_COL = 512 - AS * 32;             // A slots: 32 columns each
+    static constexpr int A_SMEM = KT < 4 ? kRows * 128 : 0;  // smem A tile per slot (16 KiB)
+    static constexpr int STAGES_FIT = (212 * 1024 - SCR_BYTES - AS * A_SMEM) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
+    static constexpr int A_OFF = STAGES * STAGE_BYTES;      // smem A slots (1024-aligned)
+    static constexpr int A_COL = 512 - AS * KT * 8;         // TMEM A slots: 8 columns per k-step
     static constexpr int NS_FIT = A_COL / DN;
     static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;    // TMEM group accumulators
     static constexpr int NP = NS / TPS;                     // ... in stage-sized slots
-    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int BAR_OFF = A_OFF + AS * A_SMEM;
     static constexpr int SR_OFF = BAR_OFF + 1024;           // [NS][128] f32 group scale / 16
     static constexpr int SCR_OFF = SR_OFF + NS * kRows * 4;
     static constexpr int SMEM = SCR_OFF + SCR_BYTES + 1024;
-    static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (NT * kRows * 4);
+    static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (ACC * kRows * 4);
     static constexpr int MAXC = MAXC_FIT > 8 ? 8 : MAXC_FIT;
     static_assert(STAGES >= 3, "");
     static_assert(SMEM <= 227 * 1024, "");
@@ -95,6 +107,19 @@ __device__ __forceinline__ void mma_i8_ts_elect(uint32_t d, uint32_t a, uint64_t
         "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
         "r"(a), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
@@ -121,9 +146,10 @@ __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64
 #define I4_T0() const long long _t0 = (p.debug & 32) ? clock64() : 0
 #define I4_ACC(var) if (p.debug & 32) var += clock64() - _t0
 
-template <int NT>
-__global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
-    using GG = Geo<NT>;
+template <int PT>
+__global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
+    using GG = Geo<PT>;
+    constexpr int NT = GG::ACC;
     constexpr int STAGES = GG::STAGES, DN = GG::DN, AP = GG::AP, NP = GG::NP, TPS = GG::TPS, EW = GG::EW;
     extern __shared__ uint8_t smem_raw[];
     // align by indexing the __shared__ array (keeps the shared address space: LDS/STS, not
@@ -159,6 +185,15 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
         for (int i = 0; i < NP; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4 * EW), mbar_init(&sfull[i], 4);
         mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (GG::DN > 3 * PT) {  // B rows past 3 * PT: zero once, never written by TMA
+        constexpr int PAD = (GG::DN - 3 * PT) * 128 / 16;  // uint4 per slot
+        for (int i = threadIdx.x; i < STAGES * TPS * PAD; i += blockDim.x) {
+            const int slot = i / PAD, k = i % PAD;
+            uint8_t* dst = smem + (slot / TPS) * GG::STAGE_BYTES + (slot % TPS) * GG::PLANE_BYTES + 3 * PT * 128;
+            reinterpret_cast<uint4*>(dst)[k] = make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -202,7 +237,7 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
                               p.scales + int64_t(cu.b) * kRows * p.KBLK + int64_t(cu.kb) * r8, &full[s],
                               uint32_t(n * r8 * 2));
             } else {
-                elect_expect(&full[s], uint32_t(n) * GG::PLANE_BYTES);
+                elect_expect(&full[s], uint32_t(n) * GG::BOX_BYTES);
                 for (int j = 0; j < n; ++j)
                     elect_tma3d_tx(st + (slot0 + j) * GG::PLANE_BYTES, &p.tmap_p, (cu.kb + j) * kKB, p.m0, 0,
                                    &full[s]);
@@ -283,15 +318,27 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
                             v[16 + 4 * q + e] = (ww[e] & 0x0F0F0F0Fu) * 16u;  // k = 64 + 16q + 4e ..
                         }
                     }
+                    const int slot = ap * TPS + j;
                     if (!(p.debug & 8)) {
-                        tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + (ap * TPS + j) * 32), v);
+                        // k-steps [0, KT): TMEM columns (4 codes each); [KT, 4): smem chunks
+                        if constexpr (GG::KT == 4) tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + slot * 32), v);
+                        if constexpr (GG::KT == 2) tmem_st16(tmem + lane_base + uint32_t(GG::A_COL + slot * 16), v);
+                        if constexpr (GG::KT == 1) tmem_st8(tmem + lane_base + uint32_t(GG::A_COL + slot * 8), v);
+                        if constexpr (GG::KT < 4) {
+                            uint8_t* arow = smem + GG::A_OFF + slot * GG::A_SMEM + row * 128;
+#pragma unroll
+                            for (int qc = 2 * GG::KT; qc < 8; ++qc)
+                                *reinterpret_cast<uint4*>(arow + ((uint32_t(qc) ^ uint32_t(row & 7)) << 4)) =
+                                    make_uint4(v[4 * qc], v[4 * qc + 1], v[4 * qc + 2], v[4 * qc + 3]);
+                        }
                     } else if (v[0] == 0x12345u) {
                         g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
                     }
                     sring[(np * TPS + j) * kRows + row] = scv[j];
                 }
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if constexpr (GG::KT > 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if constexpr (GG::KT < 4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
@@ -306,7 +353,7 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (warp-uniform, one elected lane issues) ==========
-        // D s32, A s8 (16 x codes, TMEM), B s8 (planes, smem), M = 128, N = 3 * NT
+        // D s32, A s8 (16 x codes, TMEM), B s8 (planes, smem), M = 128, N = DN
         constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                    (uint32_t(DN >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
         constexpr uint64_t kHi = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
@@ -340,12 +387,18 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
             if (!(p.debug & 4)) {
                 for (int j = 0; j < n; ++j) {
-                    const uint32_t a = tmem + uint32_t(GG::A_COL + (ap * TPS + j) * 32);
+                    const int slot = ap * TPS + j;
+                    const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
+                    const uint32_t alo = base + uint32_t((GG::A_OFF + slot * GG::A_SMEM) >> 4);
                     const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
                     const uint32_t d = tmem + uint32_t((np * TPS + j) * DN);
 #pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k)  // K = 32 per MMA: A +8 columns, B +32 bytes
-                        mma_i8_ts_elect(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                    for (uint32_t k = 0; k < 4; ++k) {  // K = 32 per MMA: TMEM +8 columns, smem +32 bytes
+                        if (int(k) < GG::KT)
+                            mma_i8_ts_elect(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                        else
+                            mma_i8_elect(d, kHi | (alo + 2 * k), kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                    }
                 }
             }
             commit_elect(&aempty[ap]);
@@ -400,20 +453,31 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
             // this warpgroup's groups of the stage: [j0, j1)
             const int j0 = EW == 2 ? eg : 0, j1 = EW == 2 ? (eg < n ? eg + 1 : eg) : n;
 #pragma unroll
-            for (int jj = 0; jj < ((p.debug & 131072) ? 0 : NT); jj += 16) {
-                // the 16-token chunk of every group of the stage: all TMEM loads, one wait
-                uint32_t d[TPS][3][16];
+            // token chunks of CH: plane q of token t is accumulator column q * PT + t
+            constexpr int CH = PT >= 16 ? 16 : PT;
+            constexpr int LDC = PT >= 16 ? 16 : GG::DN;  // columns loaded per plane/chunk
+#pragma unroll
+            for (int jj = 0; jj < ((p.debug & 131072) ? 0 : PT); jj += CH) {
+                // the chunk of every group of the stage: all TMEM loads, one wait
+                uint32_t d[TPS][PT >= 16 ? 3 : 1][LDC];
 #pragma unroll
                 for (int j = 0; j < TPS; ++j) {
                     if (j < j0 || j >= j1) continue;
                     const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
                     if (!(p.debug & 16)) {
-                        ld16(ta, d[j][0]);
-                        ld16(ta + NT, d[j][1]);
-                        ld16(ta + 2 * NT, d[j][2]);
+                        if constexpr (PT >= 16) {
+                            ld16(ta, d[j][0]);
+                            ld16(ta + PT, d[j][1]);
+                            ld16(ta + 2 * PT, d[j][2]);
+                        } else {
+#pragma unroll
+                            for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, d[j][0] + 16 * h);
+                        }
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) d[j][0][e] = d[j][1][e] = d[j][2][e] = uint32_t(row + e);
+                        for (int e = 0; e < LDC; ++e)
+#pragma unroll
+                            for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[j][q3][e] = uint32_t(row + e);
                     }
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -425,12 +489,17 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
                 for (int j = 0; j < TPS; ++j) {
                     if (j < j0 || j >= j1) continue;
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {  // 2^s per token is applied at the segment end
-                        // |D| < 2^21 per group: int -> float as (bits(D + 1.5 * 2^23) - 1.5 * 2^23),
-                        // two full-rate ops instead of the 1/8-rate I2F
-                        const float x0 = __int_as_float(int32_t(d[j][0][e]) + 0x4B400000) - 12582912.0f;
-                        const float x1 = __int_as_float(int32_t(d[j][1][e]) + 0x4B400000) - 12582912.0f;
-                        const float x2 = __int_as_float(int32_t(d[j][2][e]) + 0x4B400000) - 12582912.0f;
+                    for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
+                        // |D| < 2^21 per group: int -> float as (bits(D + 1.5 * 2^23) - 1.5 * 2^23)
+                        uint32_t u0v, u1v, u2v;
+                        if constexpr (PT >= 16) {
+                            u0v = d[j][0][e], u1v = d[j][PT >= 16 ? 1 : 0][e], u2v = d[j][PT >= 16 ? 2 : 0][e];
+                        } else {
+                            u0v = d[j][0][e], u1v = d[j][0][(PT + e) % LDC], u2v = d[j][0][(2 * PT + e) % LDC];
+                        }
+                        const float x0 = __int_as_float(int32_t(u0v) + 0x4B400000) - 12582912.0f;
+                        const float x1 = __int_as_float(int32_t(u1v) + 0x4B400000) - 12582912.0f;
+                        const float x2 = __int_as_float(int32_t(u2v) + 0x4B400000) - 12582912.0f;
                         const float x = fmaf(x2, 6.103515625e-05f, fmaf(x1, 0.0078125f, x0));
                         acc[jj + e] = fmaf(x, scg[j], acc[jj + e]);
                     }
@@ -574,10 +643,10 @@ __global__ void __launch_bounds__(Geo<NT>::THREADS, 1) wgemm_i4_kernel(const __g
     }
 }
 
-template <int NT>
+template <int PT>
 cudaError_t launch_nt(Params p, cudaStream_t st) {
-    using GG = Geo<NT>;
-    auto kern = wgemm_i4_kernel<NT>;
+    using GG = Geo<PT>;
+    auto kern = wgemm_i4_kernel<PT>;
     static bool configured = false;
     static int max_clusters[9] = {0};
     if (!configured) {
@@ -693,12 +762,13 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     p.out_dtype = A.out_dtype;
     p.debug = dbg;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
-    const int nt_max = A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
-    for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {
-        p.M = int(A.m - m0 < nt_max ? A.m - m0 : nt_max);
+    // tokens per chunk: the smallest PT >= M (B operand N = 3 * PT rounded up to 16)
+    const int pt = A.m <= 5 ? 5 : A.m <= 10 ? 10 : A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
+    for (int64_t m0 = 0; m0 < A.m; m0 += pt) {
+        p.M = int(A.m - m0 < pt ? A.m - m0 : pt);
         p.m0 = int(m0);
         p.out = static_cast<char*>(A.out) + m0 * A.n * esz;
-        const int nt = p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64;
+        const int nt = pt;
         {
             const cuuint64_t dims[3] = {cuuint64_t(A.k), cuuint64_t(A.m), 3};
             const cuuint64_t strides[2] = {cuuint64_t(A.k), cuuint64_t(A.m * A.k)};
@@ -724,7 +794,9 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
         G = G < 1 ? 1 : G;
         p.G = int(p.U < G ? p.U : G);
-        cudaError_t e = nt == 16 ? i4::launch_nt<16>(p, st)
+        cudaError_t e = nt == 5    ? i4::launch_nt<5>(p, st)
+                      : nt == 10 ? i4::launch_nt<10>(p, st)
+                      : nt == 16 ? i4::launch_nt<16>(p, st)
                       : nt == 32 ? i4::launch_nt<32>(p, st)
                                  : i4::launch_nt<64>(p, st);
         if (e != cudaSuccess) return e;

@@ -63,6 +63,51 @@ __global__ void k(long long* out) {
       long long t1 = clock64();
       if (lane == 0) out[4] = (t1 - t0) / 256;
     }
+    {
+      // 8 TS MMAs per asm block (one elect), precomputed operands
+      const uint64_t bhs = (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+      const uint64_t bd0 = bhs | (((b0) >> 4) & 0x3FFF);
+      long long t0 = clock64();
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t d = tmem + (i & 1) * 128, a = tmem + 256 + (i & 3) * 32;
+        asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3;\nelect.sync _|e, 0xffffffff;\n"
+                     "add.u64 b1, %2, 2;\nadd.u64 b2, %2, 4;\nadd.u64 b3, %2, 6;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 0;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%4], b1, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%5], b2, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%6], b3, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%4], b1, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%5], b2, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%6], b3, %3, 1;\n}\n"
+                     :: "r"(d), "r"(a), "l"(bd0), "r"(id_i8), "r"(a + 8), "r"(a + 16), "r"(a + 24) : "memory");
+      }
+      commit(&bar); mbar_wait(&bar, ph); ph ^= 1;
+      long long t1 = clock64();
+      if (lane == 0) out[5] = (t1 - t0) / 256;
+      // same with SS (A SW128 from smem)
+      const uint64_t ad0 = ahs | (((a0) >> 4) & 0x3FFF);
+      t0 = clock64();
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t d = tmem + (i & 1) * 128;
+        const uint64_t ad = ad0 + (i & 3) * (16384 >> 4);
+        asm volatile("{\n.reg .pred e;\n.reg .b64 a1, a2, a3, b1, b2, b3;\nelect.sync _|e, 0xffffffff;\n"
+                     "add.u64 a1, %1, 2;\nadd.u64 a2, %1, 4;\nadd.u64 a3, %1, 6;\n"
+                     "add.u64 b1, %2, 2;\nadd.u64 b2, %2, 4;\nadd.u64 b3, %2, 6;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, 1;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n}\n"
+                     :: "r"(d), "l"(ad), "l"(bd0), "r"(id_i8) : "memory");
+      }
+      commit(&bar); mbar_wait(&bar, ph); ph ^= 1;
+      t1 = clock64();
+      if (lane == 0) out[6] = (t1 - t0) / 256;
+    }
     for (int pass = 0; pass < 3; ++pass) {
       long long t0 = clock64();
       for (int i = 0; i < 256; ++i) {
@@ -80,13 +125,13 @@ __global__ void k(long long* out) {
   if (warp == 0) { asm volatile("tcgen05.fence::after_thread_sync;"); asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)); }
 }
 int main() {
-  long long* d; cudaMalloc(&d, 64); long long h[5];
+  long long* d; cudaMalloc(&d, 64); long long h[7];
   auto run = [&](auto kern, int n) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     kern<<<1, 128, 100 * 1024>>>(d); cudaError_t e = cudaDeviceSynchronize();
     if (e) { printf("N=%d err %s\n", n, cudaGetErrorString(e)); return; }
-    cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
-    printf("N=%3d: kind::i8 SS (K=32) %lld / %lld cycles/MMA; kind::f16 SS (K=16) %lld; i8 SW128 A %lld; i8 TS %lld\n", n, h[0], h[1], h[2], h[3], h[4]);
+    cudaMemcpy(h, d, 56, cudaMemcpyDeviceToHost);
+    printf("N=%3d: i8 SS noswz %lld; f16 SS %lld; i8 SS SW128 %lld; i8 TS %lld | batched x8: TS %lld SS %lld cycles/MMA\n", n, h[0], h[2], h[3], h[4], h[5], h[6]);
   };
   run(k<16>, 16); run(k<48>, 48); run(k<96>, 96);
   return 0;
