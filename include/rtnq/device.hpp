@@ -45,6 +45,9 @@ public:
     GroupSpec group() const { return group_; }
     const std::uint8_t* codes() const { return codes_; }
     const std::uint16_t* scales() const { return scales_; }
+    // codes layout: RTNQ_NATIVE_I4 (W4 group 128), RTNQ_NATIVE_I8 (W8 per-channel) -- the
+    // operands of the int8 tensor-core kernels -- else RTNQ_NATIVE_SM100
+    int layout_kind() const { return kind_; }
 
 private:
     std::int64_t rows_ = 0, cols_ = 0;
@@ -52,6 +55,7 @@ private:
     GroupSpec group_;
     std::uint8_t* codes_ = nullptr;
     std::uint16_t* scales_ = nullptr;
+    int kind_ = 2;
 };
 
 // Scratch for linear(): stream-K partials and self-resetting counters (zeroed once).
