@@ -183,19 +183,22 @@ __device__ __forceinline__ unsigned long long gtime() {
 //   s = exponent(max|a|) - 6 so |a| / 2^s < 64; three exact int8 planes.
 // 16-byte loads of 8 activations; up to kVPT vectors per thread stay in registers between
 // the max and the split (one pass over memory for K <= 512 * 8 * kVPT), longer rows reload.
-constexpr int kPlaneThreads = 512, kVPT = 4;
+constexpr int kPlaneThreads = 256, kSliceV = 2 * kPlaneThreads;  // 16-byte vectors per CTA slice
+// grid (M, ceil(K / 8 / kSliceV)): every CTA of a token re-reduces the token's max over the
+// whole row (L2-resident, loads all in flight), then splits its own slice into planes.
 template <int AT, bool VEC>
 __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* __restrict__ a, int K, int M,
                                                                    int8_t* __restrict__ planes,
                                                                    int32_t* __restrict__ texp, unsigned long long* stamps) {
     __shared__ float wmax[kPlaneThreads / 32];
-    if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[0] = gtime();
+    const bool first = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+    if (stamps && first) stamps[0] = gtime();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
-    if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[1] = gtime();
+    if (stamps && first) stamps[1] = gtime();
     const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint16_t* rowp = static_cast<const uint16_t*>(a) + int64_t(t) * K;
-    const int nv = K / 8;
+    const int nv = K / 8, v0 = blockIdx.y * kSliceV;
     auto load4 = [&](int v) -> uint4 {
         if constexpr (VEC) return __ldg(reinterpret_cast<const uint4*>(rowp) + v);
         uint32_t w[4];
@@ -213,16 +216,24 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
         for (int i = 0; i < 4; ++i) m = fmaxf(m, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
         return m;
     };
-    uint4 keep[kVPT];
-    float mx = 0.0f;
+    // this CTA's slice stays in registers; the rest of the row is only max-reduced
+    uint4 keep[2];
 #pragma unroll
-    for (int j = 0; j < kVPT; ++j) {
-        const int v = tid + j * kPlaneThreads;
+    for (int j = 0; j < 2; ++j) {
+        const int v = v0 + tid + j * kPlaneThreads;
         keep[j] = v < nv ? load4(v) : make_uint4(0, 0, 0, 0);
     }
+    float mx = fmaxf(vmax(keep[0], 0.0f), vmax(keep[1], 0.0f));
+    for (int v = tid; v < nv; v += 4 * kPlaneThreads) {
+        uint4 q[4];
 #pragma unroll
-    for (int j = 0; j < kVPT; ++j) mx = vmax(keep[j], mx);
-    for (int v = tid + kVPT * kPlaneThreads; v < nv; v += kPlaneThreads) mx = vmax(load4(v), mx);
+        for (int j = 0; j < 4; ++j) {
+            const int vv = v + j * kPlaneThreads;
+            q[j] = (vv < nv && (vv < v0 || vv >= v0 + kSliceV)) ? load4(vv) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mx = vmax(q[j], mx);
+    }
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) wmax[warp] = mx;
     __syncthreads();
@@ -232,20 +243,29 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
     int e = 0;
     if (amax > 0.0f) frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
     const int s = max(e - 6, -126);      // |a| / 2^s < 64; 2^s stays a normal float
-    if (tid == 0) texp[t] = s;
+    if (tid == 0 && blockIdx.y == 0) texp[t] = s;
+    const float inv = __int_as_float((127 - s) << 23);  // 2^-s, exact scaling
+    // round to nearest even and the integer bits in one add: for |y| < 2^22,
+    // bits(y + 1.5 * 2^23) - bits(1.5 * 2^23) = rint(y)
+    auto rnd = [](float y, float& r) {
+        const float b = y + 12582912.0f;
+        r = b - 12582912.0f;
+        return uint32_t(__float_as_int(b) - 0x4B400000);
+    };
     auto split = [&](const uint4& q, int v) {
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
         uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const float y = ldexpf(cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu), -s);  // exact
-            const float r0 = rintf(y);
+            const float y = cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu) * inv;  // exact
+            float r0, r1, r2;
+            const uint32_t q0 = rnd(y, r0);
             const float y1 = (y - r0) * 128.0f;  // exact
-            const float r1 = rintf(y1);
-            const float r2 = rintf((y1 - r1) * 128.0f);
-            pk[0][i >> 2] |= (uint32_t(int(r0)) & 0xffu) << (8 * (i & 3));
-            pk[1][i >> 2] |= (uint32_t(int(r1)) & 0xffu) << (8 * (i & 3));
-            pk[2][i >> 2] |= (uint32_t(int(r2)) & 0xffu) << (8 * (i & 3));
+            const uint32_t q1 = rnd(y1, r1);
+            const uint32_t q2 = rnd((y1 - r1) * 128.0f, r2);
+            pk[0][i >> 2] |= (q0 & 0xffu) << (8 * (i & 3));
+            pk[1][i >> 2] |= (q1 & 0xffu) << (8 * (i & 3));
+            pk[2][i >> 2] |= (q2 & 0xffu) << (8 * (i & 3));
         }
 #pragma unroll
         for (int pl = 0; pl < 3; ++pl)
@@ -253,19 +273,18 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
                 make_uint2(pk[pl][0], pk[pl][1]);
     };
 #pragma unroll
-    for (int j = 0; j < kVPT; ++j) {
-        const int v = tid + j * kPlaneThreads;
+    for (int j = 0; j < 2; ++j) {
+        const int v = v0 + tid + j * kPlaneThreads;
         if (v < nv) split(keep[j], v);
     }
-    for (int v = tid + kVPT * kPlaneThreads; v < nv; v += kPlaneThreads) split(load4(v), v);
-    if (stamps && threadIdx.x == 0 && blockIdx.x == 0) stamps[2] = gtime();
+    if (stamps && first) stamps[2] = gtime();
 }
 
 template <int AT, bool VEC>
 inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, int32_t* texp, unsigned long long* stamps,
                                  cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(M));
+    cfg.gridDim = dim3(unsigned(M), unsigned((K / 8 + kSliceV - 1) / kSliceV));
     cfg.blockDim = dim3(kPlaneThreads);
     cfg.stream = st;
     cudaLaunchAttribute attr;

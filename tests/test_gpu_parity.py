@@ -351,3 +351,9 @@ def test_w4_group128_tc_kernel_still_reachable(oracle):
     a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
     o1, o2 = rq.linear(a, q1, out_dtype=torch.float32), rq.linear(a, q2, out_dtype=torch.float32)
     assert rel_frob(o1.cpu().numpy(), o2.cpu().numpy()) <= 2 * TOL
+
+
+def test_graft_smoke_entry():
+    """The driver's smoke() (one small W4 linear on cuda:0 checked against the oracle)."""
+    import __graft_entry__
+    __graft_entry__.smoke()
