@@ -118,24 +118,28 @@ __device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, 
 // qkv row layout: [Hq*D | Hkv*D | Hkv*D] (the column-split QKV output of one rank).
 // cache layout: [B][Lmax][Hkv][D] for K and for V.  One CTA = G warps (G = Hq/Hkv <= 32);
 // warp w owns query head kvh * G + w; head_dim D = 128.
-// Flash-decoding over chunks of kChunk positions: the CTA stages the chunk's K and V rows
-// in shared memory (16-byte loads, rows padded to 65 words so a lane-per-row walk is
-// bank-conflict free), each warp scores its positions lane-parallel, then updates its
-// online softmax and the P*V accumulator (lanes own 4 head dims).
+// Flash-decoding split across CTAs: grid (Hkv, B, ceil((pos + 1) / kChunk)).  A CTA stages its
+// chunk's K and V rows in shared memory (16-byte loads, all in flight; rows padded to 65 words
+// so a lane-per-row walk is bank-conflict free); each warp scores its positions lane-parallel,
+// exponentiates against the chunk max and accumulates P*V (lanes own 4 head dims, 4 chains),
+// writing a (max, sum, P*V) partial.  attention_combine_kernel merges the partials.
 constexpr int kD = 128;
-constexpr int kChunk = 128;
+constexpr int kChunk = 64;  // positions per CTA (split-context)
 constexpr int kRowW = kD / 2 + 1;  // 32-bit words per staged row (64 + 1 pad)
+constexpr int kPart = kD + 4;      // floats per split partial: max, sum, 2 pad, P*V (16-B aligned)
 
 __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
-                                        __nv_bfloat16* __restrict__ out, int hq, int hkv, int lmax,
+                                        float* __restrict__ part, int hq, int hkv, int lmax,
                                         int pos, float theta) {
+    // grid (hkv, batch, split): this CTA covers positions [t0, t0 + n) of one KV head and its
+    // G query heads (a warp each) and writes the split's (max, sum, unnormalised P.V) partial
     extern __shared__ uint32_t sm[];
     uint32_t* ks = sm;                       // [kChunk][kRowW] bf16x2
     uint32_t* vs = ks + kChunk * kRowW;      // [kChunk][kRowW]
     float* qs = reinterpret_cast<float*>(vs + kChunk * kRowW);  // [G][kD] rotated queries
     float* ps = qs + (blockDim.x / 32) * kD;                     // [G][kChunk] probabilities
-    const int b = blockIdx.y, kvh = blockIdx.x, G = hq / hkv;
+    const int b = blockIdx.y, kvh = blockIdx.x, sp = blockIdx.z, nsp = gridDim.z, G = hq / hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
     const int64_t row = int64_t(b) * (hq + 2 * hkv) * kD;
     const __nv_bfloat16* kn = qkv + row + int64_t(hq) * kD + int64_t(kvh) * kD;
@@ -143,8 +147,9 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     const int64_t cstride = int64_t(hkv) * kD;  // between positions
     __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
-    // append the new (rotated) key and the value at `pos`
-    if (warp == 0) {
+    const int t0 = sp * kChunk, n = min(kChunk, pos + 1 - t0);
+    // the split holding `pos` appends the new (rotated) key and the value there
+    if (sp == nsp - 1 && warp == 0) {
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             const int d = lane + 32 * h2;
@@ -170,65 +175,93 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     }
     __threadfence_block();
     __syncthreads();  // the appended row is visible to the staging loads below
-    float m = -INFINITY, l = 0.0f, acc[4] = {0, 0, 0, 0};
+    // stage K and V rows [t0, t0 + n): 16 chunks of 16 B per row, all loads in flight
+    for (int i = threadIdx.x; i < n * 16; i += nthr) {
+        const int t = i >> 4, c = i & 15;
+        const uint4 kv = *reinterpret_cast<const uint4*>(kcb + int64_t(t0 + t) * cstride + c * 8);
+        const uint4 vv = *reinterpret_cast<const uint4*>(vcb + int64_t(t0 + t) * cstride + c * 8);
+        uint32_t* kd = ks + t * kRowW + c * 4;
+        uint32_t* vd = vs + t * kRowW + c * 4;
+        kd[0] = kv.x, kd[1] = kv.y, kd[2] = kv.z, kd[3] = kv.w;
+        vd[0] = vv.x, vd[1] = vv.y, vd[2] = vv.z, vd[3] = vv.w;
+    }
+    __syncthreads();
     const float* qw = qs + warp * kD;
     float* pw = ps + warp * kChunk;
-    for (int t0 = 0; t0 <= pos; t0 += kChunk) {
-        const int n = min(kChunk, pos + 1 - t0);
-        // stage K and V rows [t0, t0 + n): 16 chunks of 16 B per row
-        for (int i = threadIdx.x; i < n * 16; i += nthr) {
-            const int t = i >> 4, c = i & 15;
-            const uint4 kv = *reinterpret_cast<const uint4*>(kcb + int64_t(t0 + t) * cstride + c * 8);
-            const uint4 vv = *reinterpret_cast<const uint4*>(vcb + int64_t(t0 + t) * cstride + c * 8);
-            uint32_t* kd = ks + t * kRowW + c * 4;
-            uint32_t* vd = vs + t * kRowW + c * 4;
-            kd[0] = kv.x, kd[1] = kv.y, kd[2] = kv.z, kd[3] = kv.w;
-            vd[0] = vv.x, vd[1] = vv.y, vd[2] = vv.z, vd[3] = vv.w;
-        }
-        __syncthreads();
-        // scores: lane owns positions t = lane + 32 j
-        float cmax = -INFINITY;
-        for (int t = lane; t < n; t += 32) {
-            const uint32_t* kr = ks + t * kRowW;
-            float sacc = 0.0f;
+    // scores: lane owns positions t = lane + 32 j
+    float cmax = -INFINITY;
+    for (int t = lane; t < n; t += 32) {
+        const uint32_t* kr = ks + t * kRowW;
+        float sacc = 0.0f;
 #pragma unroll 8
-            for (int w2 = 0; w2 < kD / 2; ++w2) {
-                const float2 kk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2));
-                sacc = fmaf(qw[2 * w2], kk.x, fmaf(qw[2 * w2 + 1], kk.y, sacc));
-            }
-            pw[t] = sacc;
-            cmax = fmaxf(cmax, sacc);
+        for (int w2 = 0; w2 < kD / 2; ++w2) {
+            const float2 kk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2));
+            sacc = fmaf(qw[2 * w2], kk.x, fmaf(qw[2 * w2 + 1], kk.y, sacc));
         }
-        cmax = warp_max(cmax);
-        const float mn = fmaxf(m, cmax), corr = __expf(m - mn);
-        float csum = 0.0f;
-        for (int t = lane; t < n; t += 32) {
-            const float e = __expf(pw[t] - mn);
-            pw[t] = e;
-            csum += e;
-        }
-        l = l * corr + warp_sum(csum);
-        __syncwarp();
-        // P * V: lane owns head dims 4*lane .. 4*lane+3 (two bf16x2 words)
+        pw[t] = sacc;
+        cmax = fmaxf(cmax, sacc);
+    }
+    cmax = warp_max(cmax);
+    float csum = 0.0f;
+    for (int t = lane; t < n; t += 32) {
+        const float e = __expf(pw[t] - cmax);
+        pw[t] = e;
+        csum += e;
+    }
+    csum = warp_sum(csum);
+    __syncwarp();
+    // P * V: lane owns head dims 4*lane .. 4*lane+3; four independent accumulator chains
+    float acc[4][4] = {};
+    int t = 0;
+    for (; t + 4 <= n; t += 4) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] *= corr;
-        for (int t = 0; t < n; ++t) {
-            const float pt = pw[t];
-            const uint32_t* vr = vs + t * kRowW + 2 * lane;
+        for (int u = 0; u < 4; ++u) {
+            const float pt = pw[t + u];
+            const uint32_t* vr = vs + (t + u) * kRowW + 2 * lane;
             const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
             const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + 1));
-            acc[0] = fmaf(pt, v0.x, acc[0]);
-            acc[1] = fmaf(pt, v0.y, acc[1]);
-            acc[2] = fmaf(pt, v1.x, acc[2]);
-            acc[3] = fmaf(pt, v1.y, acc[3]);
+            acc[u][0] = fmaf(pt, v0.x, acc[u][0]);
+            acc[u][1] = fmaf(pt, v0.y, acc[u][1]);
+            acc[u][2] = fmaf(pt, v1.x, acc[u][2]);
+            acc[u][3] = fmaf(pt, v1.y, acc[u][3]);
         }
-        m = mn;
-        __syncthreads();  // before the next chunk overwrites K/V
     }
+    for (; t < n; ++t) {
+        const float pt = pw[t];
+        const uint32_t* vr = vs + t * kRowW + 2 * lane;
+        const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+        const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + 1));
+        acc[0][0] = fmaf(pt, v0.x, acc[0][0]);
+        acc[0][1] = fmaf(pt, v0.y, acc[0][1]);
+        acc[0][2] = fmaf(pt, v1.x, acc[0][2]);
+        acc[0][3] = fmaf(pt, v1.y, acc[0][3]);
+    }
+    // partial: [b][qh][split] -> {max, sum, acc[kD]}
+    float* pr = part + ((int64_t(b) * hq + qh) * nsp + sp) * kPart;
+    if (lane == 0) pr[0] = cmax, pr[1] = csum;
+    *reinterpret_cast<float4*>(pr + 4 + 4 * lane) =
+        make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
+                    acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]);
+}
+
+// out[b][qh] = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s   (grid (hq, batch), one warp)
+__global__ void attention_combine_kernel(const float* __restrict__ part, __nv_bfloat16* __restrict__ out,
+                                         int hq, int nsp) {
+    const int qh = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
+    const float* pr = part + (int64_t(b) * hq + qh) * nsp * kPart;
+    float M = -INFINITY;
+    for (int s = 0; s < nsp; ++s) M = fmaxf(M, pr[s * kPart]);
+    float L = 0.0f, a[4] = {0, 0, 0, 0};
+    for (int s = 0; s < nsp; ++s) {
+        const float w = __expf(pr[s * kPart] - M);
+        L = fmaf(w, pr[s * kPart + 1], L);
+        const float4 x = *reinterpret_cast<const float4*>(pr + s * kPart + 4 + 4 * lane);
+        a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
+    }
+    const float inv = 1.0f / L;
     __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
-    const float inv = 1.0f / l;
-    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
-    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
+    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
+    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
 }
 
 }  // namespace
@@ -264,10 +297,24 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
                              int(2 * kChunk * kRowW * 4 + 32 * (kD + kChunk) * 4));
         configured = true;
     }
-    decode_attention_kernel<<<dim3(unsigned(hkv), unsigned(batch)), unsigned(32 * G), smem, st>>>(
+    // split-context partials (the scratch grows before any graph capture: the first call of a
+    // shape runs eagerly; capture of a larger shape would fail loudly, not corrupt)
+    const int nsp = int((pos + 1 + kChunk - 1) / kChunk);
+    static float* part = nullptr;
+    static size_t part_bytes = 0;
+    const size_t need = size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float);
+    if (need > part_bytes) {
+        if (part) cudaFree(part);
+        part = nullptr;
+        const size_t want = need * 2;
+        if (cudaError_t e = cudaMalloc(&part, want)) return e;
+        part_bytes = want;
+    }
+    decode_attention_kernel<<<dim3(unsigned(hkv), unsigned(batch), unsigned(nsp)), unsigned(32 * G), smem, st>>>(
         static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(kcache),
-        static_cast<__nv_bfloat16*>(vcache), static_cast<__nv_bfloat16*>(out), int(hq), int(hkv),
-        int(lmax), int(pos), theta);
+        static_cast<__nv_bfloat16*>(vcache), part, int(hq), int(hkv), int(lmax), int(pos), theta);
+    attention_combine_kernel<<<dim3(unsigned(hq), unsigned(batch)), 32, 0, st>>>(
+        part, static_cast<__nv_bfloat16*>(out), int(hq), nsp);
     return cudaGetLastError();
 }
 

@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&full[s], ph);  // the planes of this stage
                 I4_ACC(m_full);
             }
+            if ((p.debug & 64) && si == 0 && lane == 0) g_i4_dbg[c * 16 + 6] = gtime();
             {
                 I4_T0();
                 mbar_wait(&afull[ap], uint32_t(si / AP) & 1u);
@@ -630,6 +631,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             }
             cu.advance(n);
         }
+        if ((p.debug & 64) && et == 0) g_i4_dbg[c * 16 + 4] = gtime();
         if ((p.debug & 32) && et == 0 && eg == 0)
             g_i4_dbg[c * 16 + 11] = e_wait, g_i4_dbg[c * 16 + 12] = e_work, g_i4_dbg[c * 16 + 13] = clock64() - e_t0,
             g_i4_dbg[c * 16 + 14] = si, g_i4_dbg[c * 16 + 15] = e_ld;

@@ -4,13 +4,13 @@ sys.path.insert(0, os.getcwd())
 os.environ["RTNQ_WGEMM_DEBUG"] = str(64 | int(os.environ.get("DBG", "0")))
 import paper_2505_15909_b200 as rq
 L = rq.lib()
-B = int(os.environ.get("B", "16"))
+B = int(os.environ.get("B", "16")); BITS = int(os.environ.get("BITS", "8"))
 a = torch.randn(8192, 8192, device="cuda")
 for _ in range(30): a @ a
 buf = np.zeros(1024 * 16, np.uint64)
 for name, n, k in [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]:
-    qs = [rq.quantize_pack((torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16), 8,
-                           1 << (k - 1).bit_length(), ragged=True) for _ in range(3)]
+    qs = [rq.quantize_pack((torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16), BITS,
+                           (1 << (k - 1).bit_length()) if BITS == 8 else 128, ragged=BITS == 8) for _ in range(3)]
     x = torch.empty(B, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
     ws = rq.Workspace(device="cuda")
     out = torch.empty(B, n, device="cuda", dtype=torch.bfloat16)
@@ -22,7 +22,7 @@ for name, n, k in [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 40
         for i in range(6): rq.linear(x, qs[i % 3], out=out, workspace=ws, pdl=True, stream=st)
     g.replay(); torch.cuda.synchronize()
     buf[:] = 0
-    L.rtnq_i8_debug_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
+    (L.rtnq_i8_debug_read if BITS == 8 else L.rtnq_i4_debug_read)(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
     d = buf.reshape(1024, 16).astype(np.float64)
     pl = d[1023, :3]
     g = d[:1023][d[:1023, 5] > 0]
