@@ -70,14 +70,14 @@ struct Geo {
     static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
     // two epilogue warpgroups (one per group of a stage) when a stage holds two groups
-    static constexpr int EW = 1;  // 2 (a warpgroup per group of a stage) measured slower: TMEM reads are the limit
+    static constexpr int EW = 1;  // 2 (a warpgroup per group of a stage) measured slower
     static constexpr int THREADS = EW == 2 ? 512 : 384;
     static constexpr int SCR_BYTES = EW == 2 ? ACC * kRows * 4 : 0;  // warpgroup B's partial sums
     // The A operand of a group is 4 k-steps of 32 codes.  The first KT come from TMEM (tcgen05.st
     // by the expansion; the MMA's A reads share the 64 B/clk TMEM read port with the epilogue's
     // accumulator readback), the rest from a 128B-swizzled smem tile (128 B/clk smem port,
     // shared with TMA and the planes).  KT balances the two ports for the batch size.
-    static constexpr int KT = PT <= 16 ? 4 : 0;
+    static constexpr int KT = 0;
     static constexpr int AS = PT <= 10 ? 8 : PT <= 32 ? 4 : 2;  // expanded A slots (groups)
     static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
     static constexpr int A_SMEM = KT < 4 ? kRows * 128 : 0;  // smem A tile per slot (16 KiB)
