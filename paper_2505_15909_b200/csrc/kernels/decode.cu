@@ -24,11 +24,19 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Ready to run as a PDL secondary (waits for its predecessor before touching memory, lets its
+// successor launch right away); see launch_pdl for why the launches are stream-ordered.
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+
 // x <- x + delta (if delta), out <- rmsnorm(x) * w.  One CTA per token row (toy.cpp:19-30:
 // mean of squares, 1/sqrt(ms + eps), times the norm weight).
 __global__ void add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out,
                                    int h, float eps) {
+    pdl_prologue();
     extern __shared__ float red[];
     const int row = blockIdx.x;
     __nv_bfloat16* xr = x + int64_t(row) * h;
@@ -84,6 +92,7 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfl
 // (toy.cpp:108-112 keeps the same fused [gate | up] output).
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
                                 int64_t m, int f) {
+    pdl_prologue();
     const int64_t n8 = m * f / 8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -134,6 +143,7 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         int pos, float theta) {
     // grid (hkv, batch, split): this CTA covers positions [t0, t0 + n) of one KV head and its
     // G query heads (a warp each) and writes the split's (max, sum, unnormalised P.V) partial
+    pdl_prologue();
     extern __shared__ uint32_t sm[];
     uint32_t* ks = sm;                       // [kChunk][kRowW] bf16x2
     uint32_t* vs = ks + kChunk * kRowW;      // [kChunk][kRowW]
@@ -247,6 +257,7 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
 // out[b][qh] = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s   (grid (hq, batch), one warp)
 __global__ void attention_combine_kernel(const float* __restrict__ part, __nv_bfloat16* __restrict__ out,
                                          int hq, int nsp) {
+    pdl_prologue();
     const int qh = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
     const float* pr = part + (int64_t(b) * hq + qh) * nsp * kPart;
     float M = -INFINITY;
@@ -264,24 +275,40 @@ __global__ void attention_combine_kernel(const float* __restrict__ part, __nv_bf
     *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
 }
 
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    // PDL measured slightly slower for these short kernels (their early CTAs idle on SMs the
+    // weight stream needs), so they launch stream-ordered; griddepcontrol is then a no-op.
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 0;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace
 
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
                                int64_t h, float eps, cudaStream_t st) {
     if (h % 8) return cudaErrorInvalidValue;
-    add_rmsnorm_kernel<<<unsigned(m), 256, 8 * sizeof(float), st>>>(
-        static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta),
-        static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps);
-    return cudaGetLastError();
+    return launch_pdl(add_rmsnorm_kernel, dim3(unsigned(m)), dim3(256), 8 * sizeof(float), st,
+                      static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta),
+                      static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps);
 }
 
 cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st) {
     if (f % 8) return cudaErrorInvalidValue;
     const int64_t n8 = m * f / 8;
     const unsigned blocks = unsigned(n8 / 256 + 1 < 1184 ? n8 / 256 + 1 : 1184);
-    silu_mul_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(gu),
-                                            static_cast<__nv_bfloat16*>(act), m, int(f));
-    return cudaGetLastError();
+    return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(gu),
+                      static_cast<__nv_bfloat16*>(act), m, int(f));
 }
 
 cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
@@ -304,18 +331,19 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     static size_t part_bytes = 0;
     const size_t need = size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float);
     if (need > part_bytes) {
-        if (part) cudaFree(part);
+        // the old buffer is kept (not freed): a CUDA graph captured earlier still uses it
         part = nullptr;
         const size_t want = need * 2;
         if (cudaError_t e = cudaMalloc(&part, want)) return e;
         part_bytes = want;
     }
-    decode_attention_kernel<<<dim3(unsigned(hkv), unsigned(batch), unsigned(nsp)), unsigned(32 * G), smem, st>>>(
-        static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(kcache),
-        static_cast<__nv_bfloat16*>(vcache), part, int(hq), int(hkv), int(lmax), int(pos), theta);
-    attention_combine_kernel<<<dim3(unsigned(hq), unsigned(batch)), 32, 0, st>>>(
-        part, static_cast<__nv_bfloat16*>(out), int(hq), nsp);
-    return cudaGetLastError();
+    if (cudaError_t e = launch_pdl(decode_attention_kernel, dim3(unsigned(hkv), unsigned(batch), unsigned(nsp)),
+                                   dim3(unsigned(32 * G)), smem, st, static_cast<const __nv_bfloat16*>(qkv),
+                                   static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
+                                   int(hq), int(hkv), int(lmax), int(pos), theta))
+        return e;
+    return launch_pdl(attention_combine_kernel, dim3(unsigned(hq), unsigned(batch)), dim3(32), 0, st,
+                      static_cast<const float*>(part), static_cast<__nv_bfloat16*>(out), int(hq), nsp);
 }
 
 }  // namespace rtnq_b200
