@@ -184,15 +184,48 @@ __device__ __forceinline__ unsigned long long gtime() {
 // 16-byte loads of 8 activations; up to kVPT vectors per thread stay in registers between
 // the max and the split (one pass over memory for K <= 512 * 8 * kVPT), longer rows reload.
 constexpr int kPlaneThreads = 256, kSliceV = 2 * kPlaneThreads;  // 16-byte vectors per CTA slice
+
+// While the activations are split, pull the head of every GEMM CTA's weight range into L2
+// (cp.async.bulk.prefetch.L2): the GEMM that follows then finds its first stages on chip
+// instead of paying a DRAM round trip after launch.  The unit -> byte map is the layout's:
+// NATIVE_I8 (kind 8): a 16 KiB tile per 2 units, NATIVE_I4 (kind 4): an 8 KiB tile per unit.
+struct WeightPrefetch {
+    const uint8_t* base = nullptr;  // nullptr: none
+    int64_t bytes = 0;              // the whole codes array (clamp)
+    int kind = 0, U = 0, G = 0, csize = 1, KBLK = 0;
+    uint32_t head = 0;              // bytes per CTA
+};
+__device__ __forceinline__ void prefetch_weight_heads(const WeightPrefetch& w) {
+    if (!w.base) return;
+    const int nthr = blockDim.x * gridDim.x * gridDim.y;
+    const int gt = (blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    for (int c = gt; c < w.G; c += nthr) {
+        int u0;
+        if (w.csize > 1) {
+            const int b = c / w.csize, r = c % w.csize;
+            u0 = b * w.KBLK + r * w.KBLK / w.csize;
+        } else {
+            u0 = int(int64_t(c) * w.U / w.G);
+        }
+        const int64_t off = w.kind == 8
+            ? (int64_t(u0 / w.KBLK) * ((w.KBLK + 1) >> 1) + ((u0 % w.KBLK) >> 1)) * 16384
+            : int64_t(u0) * 8192;
+        if (off >= w.bytes) continue;
+        const uint32_t n = uint32_t(w.bytes - off < int64_t(w.head) ? w.bytes - off : int64_t(w.head));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w.base + off), "r"(n & ~15u) : "memory");
+    }
+}
 // grid (M, ceil(K / 8 / kSliceV)): every CTA of a token re-reduces the token's max over the
 // whole row (L2-resident, loads all in flight), then splits its own slice into planes.
 template <int AT, bool VEC>
 __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* __restrict__ a, int K, int M,
                                                                    int8_t* __restrict__ planes,
-                                                                   int32_t* __restrict__ texp, unsigned long long* stamps) {
+                                                                   int32_t* __restrict__ texp, unsigned long long* stamps,
+                                                                   const WeightPrefetch pf) {
     __shared__ float wmax[kPlaneThreads / 32];
     const bool first = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
     if (stamps && first) stamps[0] = gtime();
+    prefetch_weight_heads(pf);  // weights are read-only: no need to wait for the predecessor
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     if (stamps && first) stamps[1] = gtime();
@@ -282,6 +315,7 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
 
 template <int AT, bool VEC>
 inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, int32_t* texp, unsigned long long* stamps,
+                                 const WeightPrefetch& pf,
                                  cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(M), unsigned((K / 8 + kSliceV - 1) / kSliceV));
@@ -292,7 +326,7 @@ inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, in
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps);
+    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps, pf);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -743,13 +743,39 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         if (cudaGetSymbolAddress(&base, i4::g_i4_dbg) == cudaSuccess)
             stamps = static_cast<unsigned long long*>(base) + 1023 * 16;
     }
+    // Optional (RTNQ_WEIGHT_PREFETCH=1): L2 prefetch of each GEMM CTA's first 64 KiB, issued by
+    // the planes kernel (same partition rule as the launch below; a hint, so the occupancy clamp
+    // of cluster sizes is ignored).  Measured 2x slower end to end on B200 (the prefetches hold
+    // up the planes kernel), so it is off by default.
+    imma::WeightPrefetch pf;
+    if (std::getenv("RTNQ_WEIGHT_PREFETCH")) {
+        const int nb = int((A.n + 127) / 128), kb = int((A.k + 127) / 128);
+        int csize = 1;
+        if (!std::getenv("RTNQ_WGEMM_CTAS") && int64_t(nb) * 2 <= imma::sms()) {
+            const char* ce = std::getenv("RTNQ_WGEMM_CLUSTER");
+            if (!ce || std::atoi(ce) != 0) {
+                int S = imma::sms() / nb;
+                S = S > 8 ? 8 : S;
+                S = S > kb ? kb : S;
+                csize = S < 2 ? 1 : S;
+            }
+        }
+        pf.base = A.codes;
+        pf.kind = 4;
+        pf.KBLK = kb;
+        pf.U = nb * kb;
+        pf.csize = csize;
+        pf.G = csize > 1 ? nb * csize : (pf.U < imma::sms() ? pf.U : imma::sms());
+        pf.bytes = int64_t(nb) * kb * 8192;
+        pf.head = 64 * 1024;
+    }
     {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, st)
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st)
             : (vec ? imma::launch_planes<RTNQ_F16, true> : imma::launch_planes<RTNQ_F16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, st);
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st);
         if (e != cudaSuccess) return e;
     }
     p.codes = A.codes;

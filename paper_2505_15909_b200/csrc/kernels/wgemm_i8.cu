@@ -526,13 +526,39 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
         if (cudaGetSymbolAddress(&base, i8::g_i8_dbg) == cudaSuccess)
             stamps = static_cast<unsigned long long*>(base) + 1023 * 16;
     }
+    // Optional (RTNQ_WEIGHT_PREFETCH=1): L2 prefetch of each GEMM CTA's first 64 KiB, issued by
+    // the planes kernel (same partition rule as the launch below; a hint, so the occupancy clamp
+    // of cluster sizes is ignored).  Measured 2x slower end to end on B200 (the prefetches hold
+    // up the planes kernel), so it is off by default.
+    imma::WeightPrefetch pf;
+    if (std::getenv("RTNQ_WEIGHT_PREFETCH")) {
+        const int nb = int((A.n + 127) / 128), kb = int((A.k + 63) / 64);
+        int csize = 1;
+        if (!std::getenv("RTNQ_WGEMM_CTAS") && int64_t(nb) * 2 <= i8::sms()) {
+            const char* ce = std::getenv("RTNQ_WGEMM_CLUSTER");
+            if (!ce || std::atoi(ce) != 0) {
+                int S = i8::sms() / nb;
+                S = S > 8 ? 8 : S;
+                S = S > kb ? kb : S;
+                csize = S < 2 ? 1 : S;
+            }
+        }
+        pf.base = A.codes;
+        pf.kind = 8;
+        pf.KBLK = kb;
+        pf.U = nb * kb;
+        pf.csize = csize;
+        pf.G = csize > 1 ? nb * csize : (pf.U < i8::sms() ? pf.U : i8::sms());
+        pf.bytes = int64_t(nb) * ((kb + 1) >> 1) * 16384;
+        pf.head = 64 * 1024;
+    }
     {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? i8::launch_planes<RTNQ_BF16, true> : i8::launch_planes<RTNQ_BF16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, st)
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st)
             : (vec ? i8::launch_planes<RTNQ_F16, true> : i8::launch_planes<RTNQ_F16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, st);
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st);
         if (e != cudaSuccess) return e;
     }
     // 2. the GEMM
