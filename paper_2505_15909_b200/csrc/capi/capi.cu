@@ -256,7 +256,10 @@ size_t rtnq_dev_linear_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits
         if (layout.kind == RTNQ_NATIVE_I4 && bits == 4 && g == 128) ws = wgemm_i4_workspace_bytes(m, n, k);
     }
     if (path == RTNQ_PATH_DEQUANT_FIRST || path == RTNQ_PATH_AUTO) {
-        const size_t d = size_t(n) * size_t(k) * sizeof(float);
+        // f32 reference-exact materialization, or the tensor-core hi/lo split (+ f32 C)
+        size_t d = size_t(n) * size_t(k) * sizeof(float);
+        const size_t t = dequant_first_workspace_bytes(m, n, k, RTNQ_BF16);
+        d = d > t ? d : t;
         ws = ws > d ? ws : d;
     }
     return ws;
@@ -335,6 +338,20 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
         WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
                     out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
         RTNQ_CUDA(launch_wgemm_i4(A, st));
+        return RTNQ_OK;
+    }
+    // Dequant-first on the tensor cores: 16-bit activations, f16 scales, any
+    // codes layout; exact hi + lo weight split, two cuBLAS GEMMs with f32 accumulation.
+    if (path == RTNQ_PATH_DEQUANT_FIRST && (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) &&
+        sdtype == RTNQ_F16) {
+        const size_t need = dequant_first_workspace_bytes(m, n, k, odtype);
+        if (ws_bytes < need)
+            return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " +
+                                                  std::to_string(need) + " bytes");
+        if (const char* why = launch_dequant_first(a, a_dtype, m, n, k, codes, L, bits, g, gpr,
+                                                   static_cast<const uint16_t*>(scales), sorder, out,
+                                                   odtype, ws, st))
+            return fail(RTNQ_E_CUDA, why);
         return RTNQ_OK;
     }
     // Reference-exact CUDA-core paths: f32 activations, f32 reference-order scales.

@@ -69,6 +69,13 @@ const char* wgemm_i8_unsupported(int64_t m, int64_t n, int64_t k, int bits, int6
 size_t wgemm_i8_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_wgemm_i8(const WgemmArgs& args, cudaStream_t st);
 
+// dequant_first.cu: exact dequant into hi + lo 16-bit terms, then two cuBLAS GEMMs (f32 C)
+size_t dequant_first_workspace_bytes(int64_t m, int64_t n, int64_t k, int odtype);
+const char* launch_dequant_first(const void* a, int a_dtype, int64_t m, int64_t n, int64_t k,
+                                 const uint8_t* codes, Layout L, int bits, int64_t g, int64_t gpr,
+                                 const uint16_t* scales, int sorder, void* out, int odtype, void* ws,
+                                 cudaStream_t st);
+
 // wgemm_i4.cu: W4 group-128 on tcgen05.mma.kind::i8 over RTNQ_NATIVE_I4 nibble tiles
 const char* wgemm_i4_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);
 size_t wgemm_i4_workspace_bytes(int64_t m, int64_t n, int64_t k);

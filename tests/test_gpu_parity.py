@@ -357,3 +357,32 @@ def test_graft_smoke_entry():
     """The driver's smoke() (one small W4 linear on cuda:0 checked against the oracle)."""
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("bits,g,m", [(4, 128, 1), (4, 128, 300), (8, 4096, 64), (4, 64, 96), (8, 128, 130)])
+def test_dequant_first_tensor_path(oracle, bits, g, m):
+    """dequant-first on the tensor cores (exact hi + lo 16-bit weight split,
+    two cuBLAS GEMMs with f32 accumulation), any codes layout, against the f64 oracle."""
+    n, k = 520, 4096 if g == 4096 else 1024
+    q, codes, s16w = _make(oracle, n, k, bits, g, seed=m + bits + g)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+    ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+    out = rq.linear(a, q, out_dtype=torch.float32, path=rq.PATH_DEQUANT_FIRST)
+    assert rel_frob(out.cpu().numpy(), ref) <= TOL
+    o16 = rq.linear(a, q, out_dtype=torch.bfloat16, path=rq.PATH_DEQUANT_FIRST)
+    assert rel_frob(o16.float().cpu().numpy(), ref) <= 8e-3
+
+
+def test_gemm_auto_dispatch_tensor_paths(oracle):
+    """gemm_auto (gemm.cpp:100-109) on the tensor paths: m >= threshold takes dequant-first,
+    below it the fused kernel; both agree with the oracle."""
+    n, k, bits, g = 256, 1024, 4, 128
+    q, codes, s16w = _make(oracle, n, k, bits, g, seed=77)
+    for m, want in ((40, rq.PATH_FUSED), (64, rq.PATH_DEQUANT_FIRST), (200, rq.PATH_DEQUANT_FIRST)):
+        a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+        out = rq.linear(a, q, out_dtype=torch.float32, path=rq.PATH_AUTO, threshold=64)
+        ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+        assert rel_frob(out.cpu().numpy(), ref) <= TOL, m
+        # the chosen path reproduces its own output exactly
+        again = rq.linear(a, q, out_dtype=torch.float32, path=want)
+        assert torch.equal(out, again), m
