@@ -242,6 +242,10 @@ static bool i4_path(int a_dtype, rtnq_layout layout, int bits, int64_t g, int sd
            sorder == RTNQ_SCALES_NATIVE;
 }
 
+// The first 64 KiB of a linear workspace hold the fused kernels' per-row-block counters, which
+// must stay zero between launches; the dequant-first paths put their scratch after them.
+constexpr size_t kCountersReserve = 64 * 1024;
+
 static bool tensor_path(int a_dtype, rtnq_layout layout, int sdtype, int sorder) {
     return layout.kind == RTNQ_NATIVE_SM100 && (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) &&
            sdtype == RTNQ_F16 && sorder == RTNQ_SCALES_NATIVE;
@@ -256,10 +260,11 @@ size_t rtnq_dev_linear_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits
         if (layout.kind == RTNQ_NATIVE_I4 && bits == 4 && g == 128) ws = wgemm_i4_workspace_bytes(m, n, k);
     }
     if (path == RTNQ_PATH_DEQUANT_FIRST || path == RTNQ_PATH_AUTO) {
-        // f32 reference-exact materialization, or the tensor-core hi/lo split (+ f32 C)
+        // f32 reference-exact materialization, or the tensor-core hi/lo split (+ f32 C), after
+        // the fused kernels' self-resetting counters (never overwritten)
         size_t d = size_t(n) * size_t(k) * sizeof(float);
         const size_t t = dequant_first_workspace_bytes(m, n, k, RTNQ_BF16);
-        d = d > t ? d : t;
+        d = (d > t ? d : t) + kCountersReserve;
         ws = ws > d ? ws : d;
     }
     return ws;
@@ -344,13 +349,13 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
     // codes layout; exact hi + lo weight split, two cuBLAS GEMMs with f32 accumulation.
     if (path == RTNQ_PATH_DEQUANT_FIRST && (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) &&
         sdtype == RTNQ_F16) {
-        const size_t need = dequant_first_workspace_bytes(m, n, k, odtype);
+        const size_t need = dequant_first_workspace_bytes(m, n, k, odtype) + kCountersReserve;
         if (ws_bytes < need)
             return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " +
                                                   std::to_string(need) + " bytes");
         if (const char* why = launch_dequant_first(a, a_dtype, m, n, k, codes, L, bits, g, gpr,
                                                    static_cast<const uint16_t*>(scales), sorder, out,
-                                                   odtype, ws, st))
+                                                   odtype, static_cast<char*>(ws) + kCountersReserve, st))
             return fail(RTNQ_E_CUDA, why);
         return RTNQ_OK;
     }
@@ -366,9 +371,9 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
     if (path == RTNQ_PATH_FUSED) {
         launch_gemm_fused_exact(af, m, k, codes, L, bits, n, g, gpr, sf, of, st);
     } else if (path == RTNQ_PATH_DEQUANT_FIRST) {
-        const size_t need = size_t(n) * size_t(k) * sizeof(float);
+        const size_t need = size_t(n) * size_t(k) * sizeof(float) + kCountersReserve;
         if (ws_bytes < need) return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small");
-        float* wf = static_cast<float*>(ws);
+        float* wf = reinterpret_cast<float*>(static_cast<char*>(ws) + kCountersReserve);
         launch_dequant(codes, L, bits, n, k, g, gpr, sf, RTNQ_F32, RTNQ_SCALES_REF, wf, RTNQ_F32, st);
         launch_dense_blocked(af, m, k, wf, n, g, of, st);
     } else if (path == RTNQ_PATH_ORACLE) {
@@ -653,7 +658,7 @@ rtnq_status rtnq_gemm(int path, const float* a, int64_t m, int64_t k, const uint
     if (path == RTNQ_PATH_FUSED && layout.kind != RTNQ_KERNEL_INTERLEAVED)
         return fail(RTNQ_E_SHAPE, "fused GEMM requires the kernel_interleaved layout");
     if (m * n == 0) return RTNQ_OK;
-    const size_t wsb = path == RTNQ_PATH_DEQUANT_FIRST ? size_t(n * k) * 4 : 0;
+    const size_t wsb = path == RTNQ_PATH_DEQUANT_FIRST ? size_t(n * k) * 4 + kCountersReserve : 0;
     RTNQ_ALLOC(dd, size_t(nbytes));
     RTNQ_ALLOC(ds, size_t(n * gpr) * 4);
     RTNQ_ALLOC(dout, size_t(m * n) * 4);
