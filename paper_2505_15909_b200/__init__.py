@@ -263,6 +263,25 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
     return out
 
 
+def from_row_major(codes_rm, scales_f16, rows: int, cols: int, bits: int, group: int,
+                   ragged: bool = False, stream=None) -> QuantWeight:
+    """A QuantWeight from the reference's file form (checkpoint.py): row-major offset-binary
+    codes and per-(row, group) IEEE-half scale bits, both already on the device.  The codes
+    are relaid out into the layout quantize_pack would pick (NATIVE_I4 / NATIVE_I8 / NATIVE)
+    and the scales reordered into the native order."""
+    gpr = groups_per_row(group, ragged, cols)
+    kind = NATIVE
+    if bits == 8 and group >= cols:
+        kind = NATIVE_I8
+    elif bits == 4 and group == 128:
+        kind = NATIVE_I4
+    out = QuantWeight(rows, cols, bits, group, ragged, None, None)
+    out.layout = kind
+    out.codes = relayout(codes_rm, layout(ROW_MAJOR), layout(kind), bits, rows, cols, stream=stream)
+    out.scales = native_scales(scales_f16, rows, gpr, stream=stream)
+    return out
+
+
 class Workspace:
     """Zero-initialised scratch for rtnq_dev_linear (stream-K partials and the
     self-resetting per-row-block counters).  Reuse one per stream."""
