@@ -459,11 +459,10 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             constexpr int LDC = PT >= 16 ? 16 : GG::DN;  // columns loaded per plane/chunk
 #pragma unroll
             for (int jj = 0; jj < ((p.debug & 131072) ? 0 : PT); jj += CH) {
-                // the chunk of every group of the stage: all TMEM loads, one wait
+                // chunk jj of every group of the stage; group j + 1's TMEM loads are in flight
+                // while group j's accumulators are combined
                 uint32_t d[TPS][PT >= 16 ? 3 : 1][LDC];
-#pragma unroll
-                for (int j = 0; j < TPS; ++j) {
-                    if (j < j0 || j >= j1) continue;
+                auto load = [&](int j) {
                     const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
                     if (!(p.debug & 16)) {
                         if constexpr (PT >= 16) {
@@ -480,15 +479,8 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
 #pragma unroll
                             for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[j][q3][e] = uint32_t(row + e);
                     }
-                }
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (p.debug & 32) {
-                    const long long t = clock64();
-                    e_ld += t - _tw;
-                }
-#pragma unroll
-                for (int j = 0; j < TPS; ++j) {
-                    if (j < j0 || j >= j1) continue;
+                };
+                auto combine = [&](int j) {
 #pragma unroll
                     for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
                         // |D| < 2^21 per group: int -> float as (bits(D + 1.5 * 2^23) - 1.5 * 2^23)
@@ -503,6 +495,21 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                         const float x2 = __int_as_float(int32_t(u2v) + 0x4B400000) - 12582912.0f;
                         const float x = fmaf(x2, 6.103515625e-05f, fmaf(x1, 0.0078125f, x0));
                         acc[jj + e] = fmaf(x, scg[j], acc[jj + e]);
+                    }
+                };
+                if (j0 < j1) {
+                    load(j0);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (p.debug & 32) {
+                        const long long t = clock64();
+                        e_ld += t - _tw;
+                    }
+#pragma unroll
+                    for (int j = 0; j < TPS; ++j) {
+                        if (j < j0 || j >= j1) continue;
+                        if (j + 1 < j1) load(j + 1);
+                        combine(j);
+                        if (j + 1 < j1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
                 }
             }
