@@ -183,6 +183,23 @@ rtnq_status rtnq_dev_add_rmsnorm(void* x, const void* delta, const void* weight,
                                  int64_t m, int64_t h, float eps, void* stream);
 /* act (m x f) = silu(gate_up[:, :f]) * gate_up[:, f:] (toy.cpp:108-112). */
 rtnq_status rtnq_dev_silu_mul(const void* gate_up, void* act, int64_t m, int64_t f, void* stream);
+/* The int8 kernels' activation planes (a = 2^s (P0 + P1/2^7 + P2/2^14)):
+ * planes [3][m][k] int8 and exponents [m] int32, device buffers.  rtnq_dev_act_planes computes
+ * them from a bf16/f16 activation; the _planes variants of add+RMSNorm and SiLU*up emit them
+ * for their bf16 output rows in the same kernel; rtnq_dev_linear_planes then runs the W4
+ * (RTNQ_NATIVE_I4) or W8 (RTNQ_NATIVE_I8) linear on them without recomputing. */
+rtnq_status rtnq_dev_act_planes(const void* a, int a_dtype, int64_t m, int64_t k, int8_t* planes,
+                                int32_t* texp, void* stream);
+rtnq_status rtnq_dev_add_rmsnorm_planes(void* x, const void* delta, const void* weight, void* out,
+                                        int64_t m, int64_t h, float eps, int8_t* planes, int32_t* texp,
+                                        void* stream);
+rtnq_status rtnq_dev_silu_mul_planes(const void* gate_up, void* act, int64_t m, int64_t f,
+                                     int8_t* planes, int32_t* texp, void* stream);
+rtnq_status rtnq_dev_linear_planes(const int8_t* planes, const int32_t* texp, int64_t m, int64_t k,
+                                   const uint8_t* codes, rtnq_layout layout, int bits, int64_t n,
+                                   int64_t g, int ragged, const void* scales, int sdtype, int sorder,
+                                   void* out, int odtype, void* ws, size_t ws_bytes, void* stream,
+                                   unsigned flags);
 /* One decode step of GQA attention: qkv rows [hq*d | hkv*d | hkv*d]; the rotated key and
  * the value are appended to the caches ([batch][max_len][hkv][d]) at `pos`, then each
  * query head attends over positions [0, pos].  head_dim 128, hq/hkv <= 32. */

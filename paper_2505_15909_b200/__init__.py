@@ -100,6 +100,11 @@ def lib():
     L.rtnq_gemm_float.argtypes = [_p, _i64, _i64, _p, _i64, _i64, _p]
     L.rtnq_dev_add_rmsnorm.argtypes = [_p, _p, _p, _p, _i64, _i64, C.c_float, _p]
     L.rtnq_dev_silu_mul.argtypes = [_p, _p, _i64, _i64, _p]
+    L.rtnq_dev_add_rmsnorm_planes.argtypes = [_p, _p, _p, _p, _i64, _i64, C.c_float, _p, _p, _p]
+    L.rtnq_dev_silu_mul_planes.argtypes = [_p, _p, _i64, _i64, _p, _p, _p]
+    L.rtnq_dev_act_planes.argtypes = [_p, _i32, _i64, _i64, _p, _p, _p]
+    L.rtnq_dev_linear_planes.argtypes = [_p, _p, _i64, _i64, _p, Layout, _i32, _i64, _i64, _i32, _p,
+                                         _i32, _i32, _p, _i32, _p, _sz, _p, C.c_uint]
     L.rtnq_dev_decode_attention.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
                                             C.c_float, _p]
     L.rtnq_f32_to_f16.argtypes = [_p, _i64, _p]
@@ -347,19 +352,66 @@ def linear_raw(a, a_dtype, m, k, codes, lay, bits, n, g, ragged, scales, s_dtype
     return chosen.value
 
 
-def add_rmsnorm(x, weight, out, delta=None, eps=1e-5, stream=None):
-    """x += delta (if given); out = rmsnorm(x) * weight.  bf16 [m, h] (rtnq_dev_add_rmsnorm)."""
+class Planes:
+    """The int8 kernels' activation planes of an [m, k] activation: int8
+    [3, m, k] and int32 exponents [m], filled by act_planes or by the fused producers."""
+
+    def __init__(self, m: int, k: int, device="cuda"):
+        torch = _torch()
+        self.m, self.k = m, k
+        self.planes = torch.empty(3, m, k, dtype=torch.int8, device=device)
+        self.texp = torch.empty(m, dtype=torch.int32, device=device)
+
+
+def act_planes(a, planes: Planes, stream=None):
+    m, k = a.shape
+    _check(lib().rtnq_dev_act_planes(_ptr(a), _dt(a), m, k, _ptr(planes.planes), _ptr(planes.texp),
+                                     _stream(stream)))
+    return planes
+
+
+def add_rmsnorm(x, weight, out, delta=None, eps=1e-5, stream=None, planes: Planes | None = None):
+    """x += delta (if given); out = rmsnorm(x) * weight.  bf16 [m, h] (rtnq_dev_add_rmsnorm).
+    With ``planes`` the same kernel also writes the activation planes of ``out``."""
     m, h = x.shape
+    if planes is not None:
+        _check(lib().rtnq_dev_add_rmsnorm_planes(_ptr(x), _ptr(delta), _ptr(weight), _ptr(out), m, h,
+                                                 eps, _ptr(planes.planes), _ptr(planes.texp),
+                                                 _stream(stream)))
+        return out
     _check(lib().rtnq_dev_add_rmsnorm(_ptr(x), _ptr(delta), _ptr(weight), _ptr(out), m, h, eps,
                                       _stream(stream)))
     return out
 
 
-def silu_mul(gate_up, act, stream=None):
-    """act[m, f] = silu(gate_up[:, :f]) * gate_up[:, f:] (rtnq_dev_silu_mul)."""
+def silu_mul(gate_up, act, stream=None, planes: Planes | None = None):
+    """act[m, f] = silu(gate_up[:, :f]) * gate_up[:, f:] (rtnq_dev_silu_mul).  With ``planes``
+    the same kernel also writes the activation planes of ``act``."""
     m, f = act.shape
+    if planes is not None:
+        _check(lib().rtnq_dev_silu_mul_planes(_ptr(gate_up), _ptr(act), m, f, _ptr(planes.planes),
+                                              _ptr(planes.texp), _stream(stream)))
+        return act
     _check(lib().rtnq_dev_silu_mul(_ptr(gate_up), _ptr(act), m, f, _stream(stream)))
     return act
+
+
+def linear_planes(planes: Planes, qw: QuantWeight, out, *, workspace: Workspace | None = None,
+                  stream=None, pdl=False):
+    """The int8 tensor-core linear (NATIVE_I4 / NATIVE_I8 weights) on precomputed planes
+    (rtnq_dev_linear_planes): no planes kernel of its own."""
+    m, k = planes.m, planes.k
+    assert k == qw.cols and qw.layout in (NATIVE_I4, NATIVE_I8)
+    wsb = lib().rtnq_dev_linear_workspace_bytes(m, qw.rows, qw.cols, qw.bits, qw.group, PATH_FUSED,
+                                                layout(qw.layout))
+    if workspace is None:
+        workspace = _default_ws.setdefault(out.device, Workspace(wsb, out.device))
+    buf = workspace.ensure(wsb)
+    _check(lib().rtnq_dev_linear_planes(
+        _ptr(planes.planes), _ptr(planes.texp), m, k, _ptr(qw.codes), layout(qw.layout), qw.bits, qw.rows,
+        qw.group, int(qw.ragged), _ptr(qw.scales), F16, SCALES_NATIVE, _ptr(out), _dt(out), _ptr(buf),
+        buf.numel(), _stream(stream), FLAG_PDL if pdl else 0))
+    return out
 
 
 def decode_attention(qkv, k_cache, v_cache, out, hq, hkv, pos, head_dim=128, theta=500000.0,

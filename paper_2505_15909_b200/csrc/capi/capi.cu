@@ -403,6 +403,66 @@ rtnq_status rtnq_dev_add_rmsnorm(void* x, const void* delta, const void* weight,
     return RTNQ_OK;
 }
 
+rtnq_status rtnq_dev_add_rmsnorm_planes(void* x, const void* delta, const void* weight, void* out,
+                                        int64_t m, int64_t h, float eps, int8_t* planes, int32_t* texp,
+                                        void* stream) {
+    if (m < 0 || h <= 0 || h % 16) return fail(RTNQ_E_SHAPE, "rmsnorm with planes needs h % 16 == 0");
+    if (!planes || !texp) return fail(RTNQ_E_INVALID_INPUT, "planes and texp are required");
+    if (m == 0) return RTNQ_OK;
+    RTNQ_CUDA(launch_add_rmsnorm(x, delta, weight, out, m, h, eps, static_cast<cudaStream_t>(stream), planes,
+                                 texp));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_silu_mul_planes(const void* gate_up, void* act, int64_t m, int64_t f, int8_t* planes,
+                                     int32_t* texp, void* stream) {
+    if (m < 0 || f <= 0 || f % 16) return fail(RTNQ_E_SHAPE, "silu_mul with planes needs f % 16 == 0");
+    if (!planes || !texp) return fail(RTNQ_E_INVALID_INPUT, "planes and texp are required");
+    if (m == 0) return RTNQ_OK;
+    RTNQ_CUDA(launch_silu_mul(gate_up, act, m, f, static_cast<cudaStream_t>(stream), planes, texp));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_act_planes(const void* a, int a_dtype, int64_t m, int64_t k, int8_t* planes,
+                                int32_t* texp, void* stream) {
+    if (a_dtype != RTNQ_BF16 && a_dtype != RTNQ_F16) return fail(RTNQ_E_INVALID_INPUT, "bf16/f16 activations");
+    if (m < 0 || k <= 0 || k % 16) return fail(RTNQ_E_SHAPE, "activation planes need k % 16 == 0");
+    if (m == 0) return RTNQ_OK;
+    RTNQ_CUDA(launch_act_planes(a, a_dtype, m, k, planes, texp, static_cast<cudaStream_t>(stream)));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_linear_planes(const int8_t* planes, const int32_t* texp, int64_t m, int64_t k,
+                                   const uint8_t* codes, rtnq_layout layout, int bits, int64_t n, int64_t g,
+                                   int ragged, const void* scales, int sdtype, int sorder, void* out,
+                                   int odtype, void* ws, size_t ws_bytes, void* stream, unsigned flags) {
+    if (!valid_bits(bits)) return fail(RTNQ_E_INVALID_INPUT, "bits must be 4 or 8");
+    RTNQ_TRY(check_layout(layout));
+    if (m < 0 || n < 0 || k < 0) return fail(RTNQ_E_SHAPE, "negative tensor dimension");
+    const int64_t gpr = rtnq_groups_per_row(g, ragged, k);
+    if (gpr < 0) return rtnq_status(-gpr);
+    if (!planes || !texp) return fail(RTNQ_E_INVALID_INPUT, "planes and texp are required");
+    if (m * n == 0) return RTNQ_OK;
+    const bool i8 = i8_path(RTNQ_BF16, layout, bits, g, k, sdtype);
+    const bool i4 = i4_path(RTNQ_BF16, layout, bits, g, sdtype, sorder);
+    if (!i8 && !i4)
+        return fail(RTNQ_E_UNSUPPORTED, "precomputed planes feed the int8 kernels: RTNQ_NATIVE_I4 (W4 g128) or "
+                                        "RTNQ_NATIVE_I8 (W8 per-channel) codes, native f16 scales");
+    if (const char* why = i8 ? wgemm_i8_unsupported(m, n, k, bits, g, RTNQ_BF16)
+                             : wgemm_i4_unsupported(m, n, k, bits, g, RTNQ_BF16))
+        return fail(RTNQ_E_UNSUPPORTED, why);
+    const size_t need = i8 ? wgemm_i8_workspace_bytes(m, n, k) : wgemm_i4_workspace_bytes(m, n, k);
+    if (ws_bytes < need)
+        return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " + std::to_string(need) + " bytes");
+    WgemmArgs A{nullptr, RTNQ_BF16, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
+                out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
+    A.planes = planes;
+    A.texp = texp;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    RTNQ_CUDA(i8 ? launch_wgemm_i8(A, st) : launch_wgemm_i4(A, st));
+    return RTNQ_OK;
+}
+
 rtnq_status rtnq_dev_silu_mul(const void* gate_up, void* act, int64_t m, int64_t f, void* stream) {
     if (m < 0 || f <= 0 || f % 8) return fail(RTNQ_E_SHAPE, "silu_mul needs f % 8 == 0");
     if (m == 0) return RTNQ_OK;

@@ -8,6 +8,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "int8_mma.cuh"
 #include "kernels.cuh"
 
 namespace rtnq_b200 {
@@ -35,7 +36,7 @@ __device__ __forceinline__ void pdl_prologue() {
 // mean of squares, 1/sqrt(ms + eps), times the norm weight).
 __global__ void add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
                                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out,
-                                   int h, float eps) {
+                                   int h, float eps, int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
     pdl_prologue();
     extern __shared__ float red[];
     const int row = blockIdx.x;
@@ -86,6 +87,35 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfl
         }
         *reinterpret_cast<uint4*>(out + int64_t(row) * h + i) = ov;
     }
+    if (planes) {  // the int8 GEMMs' activation planes of this output row, straight away
+        __syncthreads();
+        imma::row_to_planes(reinterpret_cast<const uint16_t*>(out + int64_t(row) * h), h, row, gridDim.x,
+                            planes, texp);
+    }
+}
+
+// One CTA per token: the SiLU*up row, then its activation planes (row_to_planes).
+__global__ void silu_mul_planes_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
+                                       int f, int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
+    pdl_prologue();
+    const int t = blockIdx.x;
+    for (int j = threadIdx.x * 8; j < f; j += blockDim.x * 8) {
+        const uint4 gv = *reinterpret_cast<const uint4*>(gu + int64_t(t) * 2 * f + j);
+        const uint4 uv = *reinterpret_cast<const uint4*>(gu + int64_t(t) * 2 * f + f + j);
+        const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gv);
+        const __nv_bfloat162* up = reinterpret_cast<const __nv_bfloat162*>(&uv);
+        uint4 ov;
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&ov);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 g = __bfloat1622float2(gp[q]), u = __bfloat1622float2(up[q]);
+            op[q] = __floats2bfloat162_rn(g.x / (1.0f + __expf(-g.x)) * u.x,
+                                          g.y / (1.0f + __expf(-g.y)) * u.y);
+        }
+        *reinterpret_cast<uint4*>(act + int64_t(t) * f + j) = ov;
+    }
+    __syncthreads();
+    imma::row_to_planes(reinterpret_cast<const uint16_t*>(act + int64_t(t) * f), f, t, gridDim.x, planes, texp);
 }
 
 // act[t][j] = silu(gu[t][j]) * gu[t][f + j]: gate in columns [0, f), up in [f, 2f)
@@ -296,15 +326,21 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }  // namespace
 
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
-                               int64_t h, float eps, cudaStream_t st) {
+                               int64_t h, float eps, cudaStream_t st, int8_t* planes, int32_t* texp) {
     if (h % 8) return cudaErrorInvalidValue;
     return launch_pdl(add_rmsnorm_kernel, dim3(unsigned(m)), dim3(256), 8 * sizeof(float), st,
                       static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta),
-                      static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps);
+                      static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps,
+                      planes, texp);
 }
 
-cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st) {
+cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st, int8_t* planes,
+                            int32_t* texp) {
     if (f % 8) return cudaErrorInvalidValue;
+    if (planes)
+        return launch_pdl(silu_mul_planes_kernel, dim3(unsigned(m)), dim3(256), 0, st,
+                          static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(act), int(f), planes,
+                          texp);
     const int64_t n8 = m * f / 8;
     const unsigned blocks = unsigned(n8 / 256 + 1 < 1184 ? n8 / 256 + 1 : 1184);
     return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(gu),

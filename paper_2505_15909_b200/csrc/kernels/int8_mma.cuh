@@ -313,6 +313,54 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
     if (stamps && first) stamps[2] = gtime();
 }
 
+// The whole bf16 row `rowp` (K values, K % 8 == 0, 16-byte aligned, written by this CTA before
+// a __syncthreads) -> planes of token t and its exponent: the planes kernel's arithmetic for
+// the kernels that produce activations (add+RMSNorm, SiLU*up) and emit the planes themselves.
+__device__ __forceinline__ void row_to_planes(const uint16_t* __restrict__ rowp, int K, int t, int M,
+                                              int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
+    __shared__ float wmax_r[32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    const int nv = K / 8;
+    auto cvt = [](uint32_t h) -> float { return __uint_as_float(h << 16); };
+    float mx = 0.0f;
+    for (int v = tid; v < nv; v += blockDim.x) {
+        const uint4 q = *reinterpret_cast<const uint4*>(rowp + v * 8);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mx = fmaxf(mx, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) wmax_r[warp] = mx;
+    __syncthreads();
+    float amax = 0.0f;
+    for (int i = 0; i < nw; ++i) amax = fmaxf(amax, wmax_r[i]);
+    int e = 0;
+    if (amax > 0.0f) frexpf(amax, &e);
+    const int s = max(e - 6, -126);
+    if (tid == 0) texp[t] = s;
+    const float inv = __int_as_float((127 - s) << 23);
+    for (int v = tid; v < nv; v += blockDim.x) {
+        const uint4 q = *reinterpret_cast<const uint4*>(rowp + v * 8);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float y = cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu) * inv;
+            const float b0 = y + 12582912.0f, r0 = b0 - 12582912.0f;
+            const float y1 = (y - r0) * 128.0f;
+            const float b1 = y1 + 12582912.0f, r1 = b1 - 12582912.0f;
+            const float b2 = (y1 - r1) * 128.0f + 12582912.0f;
+            pk[0][i >> 2] |= (uint32_t(__float_as_int(b0) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+            pk[1][i >> 2] |= (uint32_t(__float_as_int(b1) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+            pk[2][i >> 2] |= (uint32_t(__float_as_int(b2) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+        }
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+            *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
+                make_uint2(pk[pl][0], pk[pl][1]);
+    }
+}
+
 template <int AT, bool VEC>
 inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, int32_t* texp, unsigned long long* stamps,
                                  const WeightPrefetch& pf,

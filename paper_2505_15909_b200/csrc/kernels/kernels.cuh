@@ -58,6 +58,10 @@ struct WgemmArgs {
     void* workspace;
     size_t ws_bytes;
     bool pdl;              // launch with programmatic dependent launch (RTNQ_FLAG_PDL)
+    // int8 kernels: activation planes computed by the producer of `a` (nullptr: the linear
+    // computes them itself); [3][m][k] int8 and [m] exponents
+    const int8_t* planes = nullptr;
+    const int32_t* texp = nullptr;
 };
 // Validates the shape for the tensor-core path; returns a message or nullptr.
 const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);
@@ -82,9 +86,15 @@ size_t wgemm_i4_workspace_bytes(int64_t m, int64_t n, int64_t k);
 cudaError_t launch_wgemm_i4(const WgemmArgs& args, cudaStream_t st);
 
 // decode.cu: the non-GEMM kernels of a decode layer (bf16 activations)
+// planes/texp (optional, bf16 rows): also write the int8 GEMMs' activation planes of the output
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
-                               int64_t h, float eps, cudaStream_t st);
-cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st);
+                               int64_t h, float eps, cudaStream_t st, int8_t* planes = nullptr,
+                               int32_t* texp = nullptr);
+cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st,
+                            int8_t* planes = nullptr, int32_t* texp = nullptr);
+// the activation planes alone ([3][m][k] int8, [m] exponents) of a bf16/f16 activation
+cudaError_t launch_act_planes(const void* a, int a_dtype, int64_t m, int64_t k, int8_t* planes,
+                              int32_t* texp, cudaStream_t st);
 cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
                                     int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                     int64_t lmax, int64_t pos, float theta, cudaStream_t st);

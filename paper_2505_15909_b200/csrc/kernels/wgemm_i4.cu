@@ -740,8 +740,12 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     p.counters = reinterpret_cast<int*>(ws);
     const size_t part = size_t(imma::sms()) * i4::kRows * 64 * sizeof(float);
     p.partials = reinterpret_cast<float*>(ws + kI4Counters);
-    int8_t* planes = reinterpret_cast<int8_t*>(ws + kI4Counters + align256_i4(part));
-    int32_t* texp = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes) + align256_i4(size_t(3 * A.m * A.k)));
+    int8_t* planes_ws = reinterpret_cast<int8_t*>(ws + kI4Counters + align256_i4(part));
+    int32_t* texp_ws = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes_ws) + align256_i4(size_t(3 * A.m * A.k)));
+    // planes from the producer of the activations (fused into add+RMSNorm / SiLU*up), or ours
+    const bool own_planes = A.planes == nullptr;
+    int8_t* planes = own_planes ? planes_ws : const_cast<int8_t*>(A.planes);
+    int32_t* texp = own_planes ? texp_ws : const_cast<int32_t*>(A.texp);
     const char* dbg_env = std::getenv("RTNQ_WGEMM_DEBUG");
     const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
     unsigned long long* stamps = nullptr;
@@ -776,7 +780,7 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         pf.bytes = int64_t(nb) * kb * 8192;
         pf.head = 64 * 1024;
     }
-    {
+    if (own_planes) {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(

@@ -506,6 +506,17 @@ const char* wgemm_i8_unsupported(int64_t m, int64_t n, int64_t k, int bits, int6
     return nullptr;
 }
 
+cudaError_t launch_act_planes(const void* a, int a_dtype, int64_t m, int64_t k, int8_t* planes,
+                              int32_t* texp, cudaStream_t st) {
+    const bool vec = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+    imma::WeightPrefetch none;
+    return a_dtype == RTNQ_BF16
+        ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(
+              a, int(k), int(m), planes, texp, nullptr, none, st)
+        : (vec ? imma::launch_planes<RTNQ_F16, true> : imma::launch_planes<RTNQ_F16, false>)(
+              a, int(k), int(m), planes, texp, nullptr, none, st);
+}
+
 cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     i8::EncodeFn enc = i8::encoder();
     if (!enc) return cudaErrorNotSupported;
@@ -515,8 +526,12 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     p.counters = reinterpret_cast<int*>(ws);
     const size_t part = size_t(i8::sms()) * 2 * i8::kRows * 64 * sizeof(float);
     p.partials = reinterpret_cast<float*>(ws + kI8Counters);
-    int8_t* planes = reinterpret_cast<int8_t*>(ws + kI8Counters + align256(part));
-    int32_t* texp = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes) + align256(size_t(3 * A.m * A.k)));
+    int8_t* planes_ws = reinterpret_cast<int8_t*>(ws + kI8Counters + align256(part));
+    int32_t* texp_ws = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(planes_ws) + align256(size_t(3 * A.m * A.k)));
+    // planes from the producer of the activations (fused into add+RMSNorm / SiLU*up), or ours
+    const bool own_planes = A.planes == nullptr;
+    int8_t* planes = own_planes ? planes_ws : const_cast<int8_t*>(A.planes);
+    int32_t* texp = own_planes ? texp_ws : const_cast<int32_t*>(A.texp);
     // 1. activation planes (once per call): planes and token exponents
     const char* dbg_env = std::getenv("RTNQ_WGEMM_DEBUG");
     const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
@@ -552,7 +567,7 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
         pf.bytes = int64_t(nb) * ((kb + 1) >> 1) * 16384;
         pf.head = 64 * 1024;
     }
-    {
+    if (own_planes) {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? i8::launch_planes<RTNQ_BF16, true> : i8::launch_planes<RTNQ_BF16, false>)(

@@ -142,7 +142,7 @@ class TPDecodeLayer:
 
     def __init__(self, shape: LlamaShape, layer: int, world: int, rank: int, bits: dict,
                  batch: int, max_len: int, pos: int, group: int = 128, weights=None, seed=0,
-                 device="cuda", w8_per_channel=False):
+                 device="cuda", w8_per_channel=False, fuse_planes=True):
         import torch
 
         import paper_2505_15909_b200 as rq
@@ -182,17 +182,30 @@ class TPDecodeLayer:
         self.gu = torch.empty(batch, 2 * self.dims.ffn, **bf)
         self.act = torch.empty(batch, self.dims.ffn, **bf)
         self.d = torch.empty(batch, h, **bf)
+        # int8-kernel linears read activation planes; the norms and SiLU*up emit them directly
+        self.fuse = fuse_planes
+        imma = (rq.NATIVE_I4, rq.NATIVE_I8)
+        self.py = rq.Planes(batch, h, dev) if fuse_planes and (
+            self.q["qkv_proj"].layout in imma or self.q["ffn_up"].layout in imma) else None
+        self.pa = rq.Planes(batch, self.dims.ffn, dev) if fuse_planes and self.q["ffn_down"].layout in imma else None
 
     @property
     def weight_bytes(self):
         return sum(q.weight_bytes for q in self.q.values())
 
+    def _linear(self, module, a, planes, out, ws, stream, pdl):
+        import paper_2505_15909_b200 as rq
+        q = self.q[module]
+        if planes is not None and q.layout in (rq.NATIVE_I4, rq.NATIVE_I8):
+            return rq.linear_planes(planes, q, out, workspace=ws, stream=stream, pdl=pdl)
+        return rq.linear(a, q, out=out, workspace=ws, stream=stream, pdl=pdl)
+
     def attn_half(self, x, delta, ws, stream=None, pdl=False):
         """x += delta; y = rmsnorm(x); qkv; attention; o = partial attn_out_proj."""
         import paper_2505_15909_b200 as rq
         s = self.shape
-        rq.add_rmsnorm(x, self.attn_norm, self.y, delta=delta, eps=s.eps, stream=stream)
-        rq.linear(self.y, self.q["qkv_proj"], out=self.qkv, workspace=ws, stream=stream, pdl=pdl)
+        rq.add_rmsnorm(x, self.attn_norm, self.y, delta=delta, eps=s.eps, stream=stream, planes=self.py)
+        self._linear("qkv_proj", self.y, self.py, self.qkv, ws, stream, pdl)
         rq.decode_attention(self.qkv, self.k_cache, self.v_cache, self.attn, self.dims.hq,
                             self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream)
         rq.linear(self.attn, self.q["attn_out_proj"], out=self.o, workspace=ws, stream=stream,
@@ -202,10 +215,11 @@ class TPDecodeLayer:
     def mlp_half(self, x, o_sum, ws, stream=None, pdl=False):
         """x += o_sum; y = rmsnorm(x); gate_up; silu*up; d = partial ffn_down."""
         import paper_2505_15909_b200 as rq
-        rq.add_rmsnorm(x, self.ffn_norm, self.y, delta=o_sum, eps=self.shape.eps, stream=stream)
-        rq.linear(self.y, self.q["ffn_up"], out=self.gu, workspace=ws, stream=stream, pdl=pdl)
-        rq.silu_mul(self.gu, self.act, stream=stream)
-        rq.linear(self.act, self.q["ffn_down"], out=self.d, workspace=ws, stream=stream, pdl=pdl)
+        rq.add_rmsnorm(x, self.ffn_norm, self.y, delta=o_sum, eps=self.shape.eps, stream=stream,
+                       planes=self.py)
+        self._linear("ffn_up", self.y, self.py, self.gu, ws, stream, pdl)
+        rq.silu_mul(self.gu, self.act, stream=stream, planes=self.pa)
+        self._linear("ffn_down", self.act, self.pa, self.d, ws, stream, pdl)
         return self.d
 
 
@@ -214,7 +228,7 @@ class TPDecodeStack:
 
     def __init__(self, shape: LlamaShape, table, world: int, rank: int, batch: int,
                  max_len: int = 257, pos: int = 256, group: int = 128, layers=None, seed=0,
-                 device="cuda", w8_per_channel=False):
+                 device="cuda", w8_per_channel=False, fuse_planes=True):
         import torch
 
         import paper_2505_15909_b200 as rq
@@ -222,7 +236,7 @@ class TPDecodeStack:
         self.world, self.rank, self.shape = world, rank, shape
         self.layers = [TPDecodeLayer(shape, li, world, rank, module_bits(table, li), batch,
                                      max_len, pos, group, seed=seed, device=device,
-                                     w8_per_channel=w8_per_channel)
+                                     w8_per_channel=w8_per_channel, fuse_planes=fuse_planes)
                        for li in range(n)]
         self.x = torch.zeros(batch, shape.hidden, dtype=torch.bfloat16, device=device)
         self.ws = rq.Workspace(device=device)

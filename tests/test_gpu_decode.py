@@ -135,3 +135,45 @@ def test_tp_stack_step_runs_llama8b_two_layers():
     x = st.step(torch.randn(4, 4096, device="cuda").to(torch.bfloat16))
     torch.cuda.synchronize()
     assert torch.isfinite(x.float()).all()
+
+
+@pytest.mark.parametrize("m", [1, 5, 16])
+def test_fused_planes_match_the_planes_kernel(m):
+    """add+RMSNorm and SiLU*up emit the int8 kernels' activation planes in the same kernel:
+    bit-identical to the standalone planes kernel on their outputs, and the linear on them is
+    bit-identical to the linear that computes its own planes."""
+    g = torch.Generator(device="cuda").manual_seed(m)
+    h, f = 4096, 1536
+    x = (torch.randn(m, h, device="cuda", generator=g)).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.rand(h, device="cuda", generator=g)).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    pf = rq.Planes(m, h)
+    rq.add_rmsnorm(x.clone(), w, y, eps=1e-5, planes=pf)
+    ps = rq.act_planes(y, rq.Planes(m, h))
+    assert torch.equal(pf.planes, ps.planes) and torch.equal(pf.texp, ps.texp)
+    gu = torch.randn(m, 2 * f, device="cuda", generator=g).to(torch.bfloat16)
+    act = torch.empty(m, f, device="cuda", dtype=torch.bfloat16)
+    pa = rq.Planes(m, f)
+    rq.silu_mul(gu, act, planes=pa)
+    act_ref = rq.silu_mul(gu, torch.empty_like(act))
+    assert torch.equal(act, act_ref)
+    pas = rq.act_planes(act, rq.Planes(m, f))
+    assert torch.equal(pa.planes, pas.planes) and torch.equal(pa.texp, pas.texp)
+    for bits, k, p, a in ((4, h, pf, y), (8, h, pf, y), (4, f, pa, act)):
+        g_ = 128 if bits == 4 else 1 << (k - 1).bit_length()
+        wq = rq.quantize_pack((torch.rand(1024, k, device="cuda") * 2 - 1).to(torch.bfloat16), bits, g_,
+                              ragged=k % g_ != 0)
+        o1 = rq.linear(a, wq, out_dtype=torch.float32)
+        o2 = rq.linear_planes(p, wq, torch.empty(m, 1024, device="cuda", dtype=torch.float32))
+        assert torch.equal(o1, o2), (bits, k)
+
+
+def test_decode_step_fused_planes_is_bit_identical():
+    table, _ = rq.plan.resolve("explicit:0 modules:4", 2)
+    outs = []
+    for fuse in (True, False):
+        st = tp.TPDecodeStack(tp.LLAMA_8B, table, world=1, rank=0, batch=4, layers=2, fuse_planes=fuse)
+        x0 = torch.randn(4, 4096, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)
+                         ).to(torch.bfloat16)
+        outs.append(st.step(x0).clone())
+    assert torch.equal(outs[0], outs[1])
