@@ -2,6 +2,7 @@
 // quantization rules, and the three code layouts.
 #pragma once
 
+#include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -9,6 +10,19 @@
 #include "../../include/rtnq_capi.h"
 
 namespace rtnq_b200 {
+
+// Bit of the current CUDA device in a per-process "done on this device" mask (kernel attributes
+// and launch caches are per device; a process may drive several GPUs).
+inline unsigned long long current_device_bit() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return 1ull << (dev & 63);
+}
+inline int current_device_index() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev & 63;
+}
 
 // ---- element loads/stores ------------------------------------------------------------
 __device__ __forceinline__ float load_elem(const void* p, int dtype, int64_t i) {

@@ -354,17 +354,19 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
         return cudaErrorInvalidValue;
     const int G = int(hq / hkv);
     const size_t smem = size_t(2 * kChunk * kRowW) * 4 + size_t(G) * (kD + kChunk) * 4;
-    static bool configured = false;
-    if (!configured) {
+    static unsigned long long configured = 0;  // per device
+    if (!(configured & current_device_bit())) {
         cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(2 * kChunk * kRowW * 4 + 32 * (kD + kChunk) * 4));
-        configured = true;
+        configured |= current_device_bit();
     }
     // split-context partials (the scratch grows before any graph capture: the first call of a
     // shape runs eagerly; capture of a larger shape would fail loudly, not corrupt)
     const int nsp = int((pos + 1 + kChunk - 1) / kChunk);
-    static float* part = nullptr;
-    static size_t part_bytes = 0;
+    static float* part_dev[64] = {};
+    static size_t part_bytes_dev[64] = {};
+    float*& part = part_dev[current_device_index()];
+    size_t& part_bytes = part_bytes_dev[current_device_index()];
     const size_t need = size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float);
     if (need > part_bytes) {
         // the old buffer is kept (not freed): a CUDA graph captured earlier still uses it

@@ -429,12 +429,13 @@ template <int NT>
 cudaError_t launch_nt(Params p, cudaStream_t st, bool pdl) {
     using GG = Geo<NT>;
     auto kern = wgemm_i8_kernel<NT>;
-    static bool configured = false;
-    static int max_clusters[9] = {0};
-    if (!configured) {
+    static unsigned long long configured = 0;  // per device
+    static int max_clusters_dev[64][9] = {};
+    int* max_clusters = max_clusters_dev[current_device_index()];
+    if (!(configured & current_device_bit())) {
         if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GG::SMEM))
             return e;
-        configured = true;
+        configured |= current_device_bit();
     }
     if (p.csize > GG::MAXC) p.csize = GG::MAXC;
     while (p.csize > 1) {

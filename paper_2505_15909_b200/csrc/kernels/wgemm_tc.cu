@@ -1026,13 +1026,14 @@ template <int BITS, int AT, int NT, bool PROF>
 cudaError_t launch_t(const Params& p_in, cudaStream_t st, bool pdl) {
     using GG = Geo<BITS, NT>;
     auto kern = wgemm_tc_kernel<BITS, AT, NT, PROF>;
-    static bool configured = false;
-    static int max_clusters[9] = {0};  // per cluster size: clusters resident at once
-    if (!configured) {
+    static unsigned long long configured = 0;  // per device
+    static int max_clusters_dev[64][9] = {};
+    int* max_clusters = max_clusters_dev[current_device_index()];  // per cluster size: clusters resident at once
+    if (!(configured & current_device_bit())) {
         cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GG::SMEM);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured |= current_device_bit();
     }
     Params p = p_in;
     // cluster split-K only if all NB clusters are resident at once; else a smaller cluster
