@@ -490,11 +490,12 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                         } else {
                             u0v = d[j][0][e], u1v = d[j][0][(PT + e) % LDC], u2v = d[j][0][(2 * PT + e) % LDC];
                         }
-                        const float x0 = __int_as_float(int32_t(u0v) + 0x4B400000) - 12582912.0f;
-                        const float x1 = __int_as_float(int32_t(u1v) + 0x4B400000) - 12582912.0f;
-                        const float x2 = __int_as_float(int32_t(u2v) + 0x4B400000) - 12582912.0f;
-                        const float x = fmaf(x2, 6.103515625e-05f, fmaf(x1, 0.0078125f, x0));
-                        acc[jj + e] = fmaf(x, scg[j], acc[jj + e]);
+                        // planes 1 and 2 combined exactly in int32 (|D1 * 128 + D2| < 2^28); D0
+                        // (< 2^21) converts exactly, D12's rounding (2^-24 of it) sits 2^-30 below
+                        // D0 after the 2^-14 weight
+                        const float x0 = float(int32_t(u0v));
+                        const float x12 = float(int32_t(u1v) * 128 + int32_t(u2v));
+                        acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), scg[j], acc[jj + e]);
                     }
                 };
                 if (j0 < j1) {
