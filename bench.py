@@ -435,12 +435,16 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 activations, u4/u8 codes (reference CPU)",
         "data": "synthetic",
-        "config": {"workload": f"Llama-3.1-8B decoder-layer linears, W{bits}A16, decode batch {B}; "
-                               "each reference step = one layer's 4 linears (bounded sample)",
-                   "batch": B, "bits": bits},
+        # the same workload as our arm's line; each reference step is a bounded sample of it
+        # (one layer's 4 linears: the metric is bytes per second, so the sample is comparable)
+        "config": {"workload": f"Llama-3.1-8B decode step, 32 layers x 4 quantized linears, "
+                               f"W{bits}A16 {'per-channel' if bits == 8 and not args.plan else 'g128'}, "
+                               f"decode batch {B}, tensor parallel TP={world}",
+                   "model": "Llama-3.1-8B", "batch": B, "bits": bits,
+                   "reference_sample": "each step = one layer's 4 linears through gemm_fused"},
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} steps x one layer's 4 linears via gemm_fused"},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
