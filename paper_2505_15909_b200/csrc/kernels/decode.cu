@@ -170,7 +170,8 @@ constexpr int kPart = kD + 4;      // floats per split partial: max, sum, 2 pad,
 __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                         float* __restrict__ part, int hq, int hkv, int lmax,
-                                        int pos, float theta) {
+                                        int pos, float theta, __nv_bfloat16* __restrict__ out,
+                                        int* __restrict__ arrivals) {
     // grid (hkv, batch, split): this CTA covers positions [t0, t0 + n) of one KV head and its
     // G query heads (a warp each) and writes the split's (max, sum, unnormalised P.V) partial
     pdl_prologue();
@@ -215,15 +216,32 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     }
     __threadfence_block();
     __syncthreads();  // the appended row is visible to the staging loads below
-    // stage K and V rows [t0, t0 + n): 16 chunks of 16 B per row, all loads in flight
-    for (int i = threadIdx.x; i < n * 16; i += nthr) {
-        const int t = i >> 4, c = i & 15;
-        const uint4 kv = *reinterpret_cast<const uint4*>(kcb + int64_t(t0 + t) * cstride + c * 8);
-        const uint4 vv = *reinterpret_cast<const uint4*>(vcb + int64_t(t0 + t) * cstride + c * 8);
-        uint32_t* kd = ks + t * kRowW + c * 4;
-        uint32_t* vd = vs + t * kRowW + c * 4;
-        kd[0] = kv.x, kd[1] = kv.y, kd[2] = kv.z, kd[3] = kv.w;
-        vd[0] = vv.x, vd[1] = vv.y, vd[2] = vv.z, vd[3] = vv.w;
+    // stage K and V rows [t0, t0 + n): 16 chunks of 16 B per row.  Every load of a batch is
+    // issued before any of its shared-memory stores, so a thread has kBatch loads in flight
+    // instead of one DRAM round trip per chunk.
+    constexpr int kBatch = 8;
+    for (int base = 0; base < n * 16; base += kBatch * nthr) {
+        uint4 kv[kBatch], vv[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int i = base + u * nthr + threadIdx.x;
+            if (i < n * 16) {
+                const int t = i >> 4, c = i & 15;
+                kv[u] = __ldg(reinterpret_cast<const uint4*>(kcb + int64_t(t0 + t) * cstride + c * 8));
+                vv[u] = __ldg(reinterpret_cast<const uint4*>(vcb + int64_t(t0 + t) * cstride + c * 8));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int i = base + u * nthr + threadIdx.x;
+            if (i < n * 16) {
+                const int t = i >> 4, c = i & 15;
+                uint32_t* kd = ks + t * kRowW + c * 4;
+                uint32_t* vd = vs + t * kRowW + c * 4;
+                kd[0] = kv[u].x, kd[1] = kv[u].y, kd[2] = kv[u].z, kd[3] = kv[u].w;
+                vd[0] = vv[u].x, vd[1] = vv[u].y, vd[2] = vv[u].z, vd[3] = vv[u].w;
+            }
+        }
     }
     __syncthreads();
     const float* qw = qs + warp * kD;
@@ -232,12 +250,17 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     float cmax = -INFINITY;
     for (int t = lane; t < n; t += 32) {
         const uint32_t* kr = ks + t * kRowW;
-        float sacc = 0.0f;
+        float sa[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four independent FMA chains
 #pragma unroll 8
-        for (int w2 = 0; w2 < kD / 2; ++w2) {
-            const float2 kk = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2));
-            sacc = fmaf(qw[2 * w2], kk.x, fmaf(qw[2 * w2 + 1], kk.y, sacc));
+        for (int w2 = 0; w2 < kD / 2; w2 += 2) {
+            const float2 k0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2));
+            const float2 k1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2 + 1));
+            sa[0] = fmaf(qw[2 * w2], k0.x, sa[0]);
+            sa[1] = fmaf(qw[2 * w2 + 1], k0.y, sa[1]);
+            sa[2] = fmaf(qw[2 * w2 + 2], k1.x, sa[2]);
+            sa[3] = fmaf(qw[2 * w2 + 3], k1.y, sa[3]);
         }
+        const float sacc = (sa[0] + sa[1]) + (sa[2] + sa[3]);
         pw[t] = sacc;
         cmax = fmaxf(cmax, sacc);
     }
@@ -282,6 +305,32 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     *reinterpret_cast<float4*>(pr + 4 + 4 * lane) =
         make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
                     acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]);
+    // the last split CTA of this (token, KV head) merges the partials (self-resetting counter)
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(arrivals + b * hkv + kvh, 1);
+        last = prev == nsp - 1;
+        if (last) arrivals[b * hkv + kvh] = 0;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const float* ph = part + (int64_t(b) * hq + qh) * nsp * kPart;
+    float M = -INFINITY;
+    for (int q = 0; q < nsp; ++q) M = fmaxf(M, __ldcg(ph + q * kPart));
+    float L = 0.0f, a[4] = {0, 0, 0, 0};
+    for (int q = 0; q < nsp; ++q) {
+        const float w = __expf(__ldcg(ph + q * kPart) - M);
+        L = fmaf(w, __ldcg(ph + q * kPart + 1), L);
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(ph + q * kPart + 4 + 4 * lane));
+        a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
+    }
+    const float inv = 1.0f / L;
+    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
+    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
 }
 
 // out[b][qh] = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s   (grid (hq, batch), one warp)
@@ -365,8 +414,19 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     const int nsp = int((pos + 1 + kChunk - 1) / kChunk);
     static float* part_dev[64] = {};
     static size_t part_bytes_dev[64] = {};
+    static int* arrivals_dev[64] = {};
+    static size_t arrivals_n_dev[64] = {};
     float*& part = part_dev[current_device_index()];
     size_t& part_bytes = part_bytes_dev[current_device_index()];
+    int*& arrivals = arrivals_dev[current_device_index()];
+    size_t& arrivals_n = arrivals_n_dev[current_device_index()];
+    if (size_t(batch * hkv) > arrivals_n) {  // zeroed once; the merging CTA resets its counter
+        arrivals = nullptr;                  // (an older buffer stays valid for captured graphs)
+        const size_t want = size_t(batch * hkv) * 2;
+        if (cudaError_t e = cudaMalloc(&arrivals, want * sizeof(int))) return e;
+        if (cudaError_t e = cudaMemset(arrivals, 0, want * sizeof(int))) return e;
+        arrivals_n = want;
+    }
     const size_t need = size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float);
     if (need > part_bytes) {
         // the old buffer is kept (not freed): a CUDA graph captured earlier still uses it
@@ -378,10 +438,10 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     if (cudaError_t e = launch_pdl(decode_attention_kernel, dim3(unsigned(hkv), unsigned(batch), unsigned(nsp)),
                                    dim3(unsigned(32 * G)), smem, st, static_cast<const __nv_bfloat16*>(qkv),
                                    static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
-                                   int(hq), int(hkv), int(lmax), int(pos), theta))
+                                   int(hq), int(hkv), int(lmax), int(pos), theta,
+                                   static_cast<__nv_bfloat16*>(out), arrivals))
         return e;
-    return launch_pdl(attention_combine_kernel, dim3(unsigned(hq), unsigned(batch)), dim3(32), 0, st,
-                      static_cast<const float*>(part), static_cast<__nv_bfloat16*>(out), int(hq), nsp);
+    return cudaSuccess;
 }
 
 }  // namespace rtnq_b200

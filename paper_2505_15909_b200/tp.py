@@ -187,7 +187,9 @@ class TPDecodeLayer:
         imma = (rq.NATIVE_I4, rq.NATIVE_I8)
         self.py = rq.Planes(batch, h, dev) if fuse_planes and (
             self.q["qkv_proj"].layout in imma or self.q["ffn_up"].layout in imma) else None
-        self.pa = rq.Planes(batch, self.dims.ffn, dev) if fuse_planes and self.q["ffn_down"].layout in imma else None
+        # (SiLU*up + planes in one kernel is a CTA per token over the whole ffn row: slower than
+        #  the two kernels, so the down projection computes its own planes)
+        self.pa = None
 
     @property
     def weight_bytes(self):
