@@ -161,7 +161,8 @@ __device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, 
 // chunk's K and V rows in shared memory (16-byte loads, all in flight; rows padded to 65 words
 // so a lane-per-row walk is bank-conflict free); each warp scores its positions lane-parallel,
 // exponentiates against the chunk max and accumulates P*V (lanes own 4 head dims, 4 chains),
-// writing a (max, sum, P*V) partial.  attention_combine_kernel merges the partials.
+// writing a (max, sum, P*V) partial; the last CTA of a (token, KV head) to finish merges them:
+// out = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s.
 constexpr int kD = 128;
 constexpr int kChunk = 64;  // positions per CTA (split-context)
 constexpr int kRowW = kD / 2 + 1;  // 32-bit words per staged row (64 + 1 pad)
@@ -325,27 +326,6 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
         const float w = __expf(__ldcg(ph + q * kPart) - M);
         L = fmaf(w, __ldcg(ph + q * kPart + 1), L);
         const float4 x = __ldcg(reinterpret_cast<const float4*>(ph + q * kPart + 4 + 4 * lane));
-        a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
-    }
-    const float inv = 1.0f / L;
-    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
-    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
-    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
-}
-
-// out[b][qh] = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s   (grid (hq, batch), one warp)
-__global__ void attention_combine_kernel(const float* __restrict__ part, __nv_bfloat16* __restrict__ out,
-                                         int hq, int nsp) {
-    pdl_prologue();
-    const int qh = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
-    const float* pr = part + (int64_t(b) * hq + qh) * nsp * kPart;
-    float M = -INFINITY;
-    for (int s = 0; s < nsp; ++s) M = fmaxf(M, pr[s * kPart]);
-    float L = 0.0f, a[4] = {0, 0, 0, 0};
-    for (int s = 0; s < nsp; ++s) {
-        const float w = __expf(pr[s * kPart] - M);
-        L = fmaf(w, pr[s * kPart + 1], L);
-        const float4 x = *reinterpret_cast<const float4*>(pr + s * kPart + 4 + 4 * lane);
         a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
     }
     const float inv = 1.0f / L;
