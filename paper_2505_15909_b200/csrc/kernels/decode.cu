@@ -190,13 +190,26 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     const int t0 = sp * kChunk, n = min(kChunk, pos + 1 - t0);
+    // RoPE angles of position `pos`, computed once per CTA (accurate sincosf: the angles reach
+    // thousands of radians at the low frequencies) and shared by the key and every query head
+    __shared__ float2 cs_s[kD / 2];
+    if (threadIdx.x < kD / 2) {
+        const float inv = powf(theta, -2.0f * float(threadIdx.x) / float(kD));
+        float sn, cn;
+        sincosf(float(pos) * inv, &sn, &cn);
+        cs_s[threadIdx.x] = make_float2(cn, sn);
+    }
+    __syncthreads();
+    auto rot = [&](float a, float bb, int d) {
+        const float2 c = cs_s[d];
+        return make_float2(a * c.x - bb * c.y, bb * c.x + a * c.y);
+    };
     // the split holding `pos` appends the new (rotated) key and the value there
     if (sp == nsp - 1 && warp == 0) {
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             const int d = lane + 32 * h2;
-            const float2 r = rope(__bfloat162float(kn[d]), __bfloat162float(kn[d + kD / 2]), d, kD,
-                                  pos, theta);
+            const float2 r = rot(__bfloat162float(kn[d]), __bfloat162float(kn[d + kD / 2]), d);
             kcb[int64_t(pos) * cstride + d] = __float2bfloat16_rn(r.x);
             kcb[int64_t(pos) * cstride + d + kD / 2] = __float2bfloat16_rn(r.y);
             vcb[int64_t(pos) * cstride + d] = vn[d];
@@ -210,8 +223,7 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
         const int d = lane + 32 * h2;
-        const float2 r = rope(__bfloat162float(qp[d]), __bfloat162float(qp[d + kD / 2]), d, kD, pos,
-                              theta);
+        const float2 r = rot(__bfloat162float(qp[d]), __bfloat162float(qp[d + kD / 2]), d);
         qs[warp * kD + d] = r.x * scale;
         qs[warp * kD + d + kD / 2] = r.y * scale;
     }
@@ -299,6 +311,15 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
         acc[0][1] = fmaf(pt, v0.y, acc[0][1]);
         acc[0][2] = fmaf(pt, v1.x, acc[0][2]);
         acc[0][3] = fmaf(pt, v1.y, acc[0][3]);
+    }
+    if (nsp == 1) {  // the whole context in this CTA: normalise and write, no merge
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = (acc[0][j] + acc[1][j] + acc[2][j] + acc[3][j]) / csum;
+        __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+        *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(o[0], o[1]);
+        *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(o[2], o[3]);
+        return;
     }
     // partial: [b][qh][split] -> {max, sum, acc[kD]}
     float* pr = part + ((int64_t(b) * hq + qh) * nsp + sp) * kPart;
