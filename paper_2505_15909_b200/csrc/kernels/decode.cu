@@ -8,6 +8,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "int8_mma.cuh"
 #include "kernels.cuh"
 
@@ -172,7 +174,7 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                         float* __restrict__ part, int hq, int hkv, int lmax,
                                         int pos, float theta, __nv_bfloat16* __restrict__ out,
-                                        int* __restrict__ arrivals) {
+                                        int* __restrict__ arrivals, int cluster_merge) {
     // grid (hkv, batch, split): this CTA covers positions [t0, t0 + n) of one KV head and its
     // G query heads (a warp each) and writes the split's (max, sum, unnormalised P.V) partial
     pdl_prologue();
@@ -321,6 +323,47 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
         *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(o[2], o[3]);
         return;
     }
+    if (cluster_merge) {
+        // the splits of this (token, KV head) are one thread-block cluster: partials stay in
+        // each CTA's shared memory (the idle K stage) and rank 0 merges them over DSMEM
+        __syncthreads();  // every warp is done reading ks
+        float* mine = reinterpret_cast<float*>(ks) + warp * kPart;
+        if (lane == 0) mine[0] = cmax, mine[1] = csum;
+        *reinterpret_cast<float4*>(mine + 4 + 4 * lane) =
+            make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
+                        acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]);
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (sp == 0) {
+            const uint32_t my = static_cast<uint32_t>(__cvta_generic_to_shared(mine));
+            float mq[8], lq[8];
+            float M = -INFINITY;
+            for (int q = 0; q < nsp; ++q) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my), "r"(q));
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(mq[q]) : "r"(ra));
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lq[q]) : "r"(ra + 4));
+                M = fmaxf(M, mq[q]);
+            }
+            float L = 0.0f, a[4] = {0, 0, 0, 0};
+            for (int q = 0; q < nsp; ++q) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my + uint32_t(16 + 16 * lane)), "r"(q));
+                float4 x;
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(ra));
+                const float w = __expf(mq[q] - M);
+                L = fmaf(w, lq[q], L);
+                a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
+            }
+            const float inv = 1.0f / L;
+            __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+            *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
+            *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+        }
+        // peers keep their shared memory alive until rank 0 has read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
     // partial: [b][qh][split] -> {max, sum, acc[kD]}
     float* pr = part + ((int64_t(b) * hq + qh) * nsp + sp) * kPart;
     if (lane == 0) pr[0] = cmax, pr[1] = csum;
@@ -436,13 +479,28 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
         if (cudaError_t e = cudaMalloc(&part, want)) return e;
         part_bytes = want;
     }
-    if (cudaError_t e = launch_pdl(decode_attention_kernel, dim3(unsigned(hkv), unsigned(batch), unsigned(nsp)),
-                                   dim3(unsigned(32 * G)), smem, st, static_cast<const __nv_bfloat16*>(qkv),
-                                   static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
-                                   int(hq), int(hkv), int(lmax), int(pos), theta,
-                                   static_cast<__nv_bfloat16*>(out), arrivals))
-        return e;
-    return cudaSuccess;
+    // 2..8 splits on a small grid: one thread-block cluster per (token, KV head), merged over
+    // DSMEM (saves the global round trips of the merge).  Large grids (e.g. batch 16) measured
+    // faster without clusters (scheduling freedom), and > 8 splits cannot form one: those merge
+    // through global memory (the last CTA to arrive).
+    const int64_t ctas = hkv * batch * nsp;
+    const int cluster = nsp >= 2 && nsp <= 8 && ctas <= 2 * 148 && !std::getenv("RTNQ_ATTN_NO_CLUSTER") ? 1 : 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(hkv), unsigned(batch), unsigned(nsp));
+    cfg.blockDim = dim3(unsigned(32 * G));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 1;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = unsigned(nsp);
+    cfg.attrs = &attr;
+    cfg.numAttrs = cluster ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, decode_attention_kernel, static_cast<const __nv_bfloat16*>(qkv),
+                              static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
+                              int(hq), int(hkv), int(lmax), int(pos), theta, static_cast<__nv_bfloat16*>(out),
+                              arrivals, cluster);
 }
 
 }  // namespace rtnq_b200

@@ -177,3 +177,27 @@ def test_decode_step_fused_planes_is_bit_identical():
                          ).to(torch.bfloat16)
         outs.append(st.step(x0).clone())
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("batch,pos", [(1, 100), (2, 300), (16, 256), (1, 700)])
+def test_decode_attention_merge_paths(batch, pos):
+    """The split-context merges (thread-block cluster over DSMEM on small grids, last-CTA global
+    merge otherwise) agree with each other and with the single-CTA path's math."""
+    import os
+    hq, hkv, d = 32, 8, 128
+    g = torch.Generator(device="cuda").manual_seed(batch * 1000 + pos)
+    qkv = torch.randn(batch, (hq + 2 * hkv) * d, device="cuda", generator=g).to(torch.bfloat16)
+    kc = torch.randn(batch, pos + 1, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(batch, pos + 1, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for no_cluster in ("", "1"):
+        if no_cluster:
+            os.environ["RTNQ_ATTN_NO_CLUSTER"] = "1"
+        try:
+            o = torch.empty(batch, hq * d, device="cuda", dtype=torch.bfloat16)
+            rq.decode_attention(qkv, kc.clone(), vc.clone(), o, hq, hkv, pos)
+            outs.append(o)
+        finally:
+            os.environ.pop("RTNQ_ATTN_NO_CLUSTER", None)
+    torch.cuda.synchronize()
+    assert rel(outs[0], outs[1].float()) < 1e-2
