@@ -386,3 +386,26 @@ def test_gemm_auto_dispatch_tensor_paths(oracle):
         # the chosen path reproduces its own output exactly
         again = rq.linear(a, q, out_dtype=torch.float32, path=want)
         assert torch.equal(out, again), m
+
+
+TP8_SHARDS = {"8b_qkv": (768, 4096), "8b_o": (4096, 512), "8b_down": (4096, 1792),
+              "70b_o": (8192, 1024), "70b_down": (8192, 3584), "405b_qkv": (2304, 16384),
+              "405b_o": (16384, 2048)}
+
+
+@pytest.mark.parametrize("name", list(TP8_SHARDS))
+@pytest.mark.parametrize("bits", [4, 8])
+def test_linear_tp8_shard_shapes(name, bits):
+    """The per-rank weight shards the 8-GPU tensor-parallel step runs,
+    through the default kernels, against an f64 GEMM over the exactly dequantized weights."""
+    n, k = TP8_SHARDS[name]
+    g = 128 if bits == 4 else 1 << (k - 1).bit_length()
+    w = ((torch.rand(n, k, device="cuda") * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+    q = rq.quantize_pack(w, bits, g, ragged=k % g != 0)
+    wd = rq.dequantize(q.codes, rq.layout(q.layout), bits, n, k, g, q.scales, rq.F16,
+                       rq.SCALES_NATIVE, torch.float32)
+    for m in (1, 16):
+        a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
+        out = rq.linear(a, q, out_dtype=torch.float32)
+        ref = a.double() @ wd.double().t()
+        assert ((out.double() - ref).norm() / ref.norm()).item() <= TOL, (name, bits, m)
