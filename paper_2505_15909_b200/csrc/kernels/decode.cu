@@ -27,11 +27,12 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// Ready to run as a PDL secondary (waits for its predecessor before touching memory, lets its
-// successor launch right away); see launch_pdl for why the launches are stream-ordered.
+// Ready to run as a PDL secondary: lets its successor launch right away (every successor waits
+// for this grid's completion before it reads what this grid writes), then waits for its
+// predecessor before touching memory.  A no-op when launched stream-ordered (launch_pdl).
 __device__ __forceinline__ void pdl_prologue() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // x <- x + delta (if delta), out <- rmsnorm(x) * w.  One CTA per token row (toy.cpp:19-30:
@@ -406,11 +407,15 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    // PDL measured slightly slower for these short kernels (their early CTAs idle on SMs the
-    // weight stream needs), so they launch stream-ordered; griddepcontrol is then a no-op.
+    // RTNQ_DECODE_PDL=1 launches these as PDL secondaries; by default they are stream-ordered
+    // (griddepcontrol is then a no-op).
+    static const int pdl = [] {
+        const char* e = std::getenv("RTNQ_DECODE_PDL");
+        return e ? std::atoi(e) : 0;
+    }();
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr.val.programmaticStreamSerializationAllowed = 0;
+    attr.val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);

@@ -221,13 +221,17 @@ template <int AT, bool VEC>
 __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* __restrict__ a, int K, int M,
                                                                    int8_t* __restrict__ planes,
                                                                    int32_t* __restrict__ texp, unsigned long long* stamps,
-                                                                   const WeightPrefetch pf) {
+                                                                   const WeightPrefetch pf, int early) {
     __shared__ float wmax[kPlaneThreads / 32];
     const bool first = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
     if (stamps && first) stamps[0] = gtime();
     prefetch_weight_heads(pf);  // weights are read-only: no need to wait for the predecessor
+    // early: the GEMM that consumes these planes may launch before the predecessor finishes, so
+    // its weight stream overlaps the predecessor's tail.  Safe: everything it writes depends on
+    // the planes, which it reads only after its own griddepcontrol.wait (this grid complete).
+    if (early) asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;");
+    if (!early) asm volatile("griddepcontrol.launch_dependents;");
     if (stamps && first) stamps[1] = gtime();
     const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint16_t* rowp = static_cast<const uint16_t*>(a) + int64_t(t) * K;
@@ -374,7 +378,11 @@ inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, in
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps, pf);
+    static const int early = [] {
+        const char* e = std::getenv("RTNQ_PDL_EARLY");
+        return e ? std::atoi(e) : 1;
+    }();
+    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps, pf, early);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
