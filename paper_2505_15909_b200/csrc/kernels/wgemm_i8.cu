@@ -52,6 +52,7 @@ struct Params {
     int64_t N, K;
     int M, Mtot, m0, NB, KBLK, U, G, csize, out_dtype;
     int pf;     // L2 prefetch distance in tiles (0 = off)
+    int direct;  // cluster split-K: peers push into a dedicated smem region (no go handshake)
     int debug;  // profiling: 4 = no MMA issued, 2 = no loads (arrive only)
 };
 
@@ -69,6 +70,7 @@ struct Geo {
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr int SMEM = BAR_OFF + 1024 + 1024;
+    static constexpr int PUSH_OFF = BAR_OFF + 1024;              // direct-push partials region
     static constexpr int DN = 3 * NT;                             // accumulator columns
     // cluster split-K: the leader's stage area holds csize - 1 pushed partials
     static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (NT * kRows * 4);
@@ -362,14 +364,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull)),
                                      "r"(uint32_t(p.csize - 1) * kSlot)
                                      : "memory");
-                        for (int r = 1; r < p.csize; ++r) {
+                        for (int r = 1; r < p.csize && !p.direct; ++r) {
                             uint32_t ra;
                             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(go)), "r"(r));
                             asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
                         }
                     }
                     mbar_wait(rfull, 0);
-                    const float4* red = reinterpret_cast<const float4*>(smem);
+                    const float4* red = reinterpret_cast<const float4*>(p.direct ? smem + GG::PUSH_OFF : smem);
                     for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
 #pragma unroll
                         for (int j = 0; j < NT / 4; ++j) {
@@ -382,10 +384,13 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                         for (int m = 0; m < NT; ++m)
                             if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
                 } else {
-                    mbar_wait(go, 0);
+                    // direct: a region nobody else uses, so push at once (a complete_tx that lands
+                    // before the leader's expect_tx only drives the tx-count negative meanwhile)
+                    if (!p.direct) mbar_wait(go, 0);
                     uint32_t dst, rb;
                     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst)
-                                 : "r"(su32(smem) + uint32_t(((rank - 1) * kRows + row) * NT * 4)));
+                                 : "r"(su32(p.direct ? smem + GG::PUSH_OFF : smem) +
+                                       uint32_t(((rank - 1) * kRows + row) * NT * 4)));
                     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(su32(rfull)));
 #pragma unroll
                     for (int j = 0; j < NT / 4; ++j)
@@ -432,8 +437,9 @@ cudaError_t launch_nt(Params p, cudaStream_t st, bool pdl) {
     static unsigned long long configured = 0;  // per device
     static int max_clusters_dev[64][9] = {};
     int* max_clusters = max_clusters_dev[current_device_index()];
+    constexpr int kSmemMax = 226 * 1024;  // 227 KiB opt-in less the static __shared__ arrays
     if (!(configured & current_device_bit())) {
-        if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GG::SMEM))
+        if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax))
             return e;
         configured |= current_device_bit();
     }
@@ -459,10 +465,17 @@ cudaError_t launch_nt(Params p, cudaStream_t st, bool pdl) {
     }
     if (p.csize > 1) p.G = p.NB * p.csize;
     else p.csize = 1;
+    // cluster split-K: a dedicated region for the peers' partials when it fits next to the ring
+    static const bool direct_ok = [] {
+        const char* e = std::getenv("RTNQ_I8_DIRECT");
+        return !e || std::atoi(e) != 0;
+    }();
+    const int extra = (p.csize - 1) * NT * kRows * 4;
+    p.direct = p.csize > 1 && direct_ok && GG::SMEM + extra <= kSmemMax;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(p.G));
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = GG::SMEM;
+    cfg.dynamicSmemBytes = GG::SMEM + (p.direct ? extra : 0);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     int na = 0;
