@@ -409,3 +409,56 @@ def test_linear_tp8_shard_shapes(name, bits):
         out = rq.linear(a, q, out_dtype=torch.float32)
         ref = a.double() @ wd.double().t()
         assert ((out.double() - ref).norm() / ref.norm()).item() <= TOL, (name, bits, m)
+
+
+@pytest.mark.parametrize("m", [1, 16])
+def test_chained_linears_pdl_graph_identical(m):
+    """Each linear consumes the previous one's output (W8 cluster, W4 cluster, W8 stream-K, W4
+    stream-K, mixed shapes).  The planes kernel lets the next GEMM launch before the previous
+    GEMM finishes (early PDL trigger) and the W8 cluster peers push without a handshake; the
+    chain run back to back in one CUDA graph must equal the chain run one synchronized linear
+    at a time, bit for bit."""
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    shapes = [(4096, 4096, 8), (4096, 4096, 4), (28672, 4096, 8), (4096, 28672, 4),
+              (6144, 4096, 8), (4096, 6144, 4)]
+    qs = []
+    for n, k, bits in shapes:
+        w = ((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1) * 0.05).to(torch.bfloat16)
+        g = 128 if bits == 4 else 1 << (k - 1).bit_length()
+        qs.append(rq.quantize_pack(w, bits, g, ragged=bits == 8))
+    x = torch.empty(m, 4096, device="cuda").uniform_(-1, 1, generator=gen).to(torch.bfloat16)
+    ws = rq.Workspace(device="cuda")
+    outs = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for n, _, _ in shapes]
+    st = torch.cuda.Stream()
+
+    def chain(sync):
+        a = x
+        for q, o in zip(qs, outs):
+            rq.linear(a, q, out=o, workspace=ws, stream=st, pdl=True)
+            if sync:
+                st.synchronize()
+            a = o
+        return [o.clone() for o in outs] if sync else None
+
+    with torch.cuda.stream(st):
+        ref = chain(True)
+    for o in outs:
+        o.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        chain(False)
+    for _ in range(3):
+        for o in outs:
+            o.zero_()
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        for i, (o, r) in enumerate(zip(outs, ref)):
+            assert torch.equal(o, r), f"linear {i} {shapes[i]} differs in the graph chain"
+    # eager back to back, no synchronization between linears
+    with torch.cuda.stream(st):
+        chain(False)
+    st.synchronize()
+    for i, (o, r) in enumerate(zip(outs, ref)):
+        assert torch.equal(o, r), f"linear {i} {shapes[i]} differs in the eager chain"
+    assert all(torch.isfinite(r.float()).all() for r in ref)
