@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             }
             uint8_t* st = smem + s * GG::STAGE_BYTES;
             const int slot0 = cu.kb & (TPS - 1);
-            if ((p.debug & 256) && codes && lane == 0 && i >= 8 && i < 12) g_i4_dbg[c * 16 + (i - 8)] = gtime();
             if ((p.debug & 2) || (codes && (p.debug & 8192)) || (!codes && (p.debug & 4096))) {
                 elect_arrive(&full[s]);  // profiling: no copy
             } else if (codes) {
@@ -278,7 +277,6 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&full[s], ph);
                 I4_ACC(x_full);
             }
-            if ((p.debug & 256) && row == 0 && si >= 8 && si < 12) g_i4_dbg[c * 16 + 4 + (si - 8)] = gtime();
             {
                 I4_T0();
                 if (si >= AP) mbar_wait(&aempty[ap], uint32_t(si / AP - 1) & 1u);
@@ -345,7 +343,6 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
-            if ((p.debug & 256) && row == 0 && si >= 8 && si < 12) g_i4_dbg[c * 16 + 8 + (si - 8)] = gtime();
             if (p.debug & 32) x_work += clock64() - _tw;
             cu.advance(n);
             ++si;
@@ -376,7 +373,6 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&full[s], ph);  // the planes of this stage
                 I4_ACC(m_full);
             }
-            if ((p.debug & 256) && lane == 0 && si >= 8 && si < 12) g_i4_dbg[c * 16 + 12 + (si - 8)] = gtime();
             if ((p.debug & 64) && si == 0 && lane == 0) g_i4_dbg[c * 16 + 6] = gtime();
             {
                 I4_T0();

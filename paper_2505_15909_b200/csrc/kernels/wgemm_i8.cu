@@ -99,7 +99,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 5);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
     if ((p.debug & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 5] = gtime();
-    if ((p.debug & 128) && threadIdx.x == 0) g_i8_dbg[c * 16 + 9] = gtime();
 
     int u0, u1;
     if (p.csize > 1) {
@@ -151,7 +150,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
         const int64_t t_last = u1 > u0 ? int64_t((u1 - 1) / p.KBLK) * kt + ((u1 - 1) % p.KBLK >> 1) : -1;
         int64_t pf_next = int64_t(cu.b) * kt + (cu.kb >> 1);
         if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes come from the previous kernel
-        if ((p.debug & 128) && lane == 0 && !codes) g_i8_dbg[c * 16 + 8] = gtime();
         for (int i = 0; cu.more(); ++i) {
             const int n = cu.chunk();
             if (i >= STAGES) {
@@ -190,7 +188,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             g_i8_dbg[c * 8 + 1] = tw;
         }
         if ((p.debug & 64) && lane == 0 && codes) g_i8_dbg[c * 16 + 0] = gtime();
-        if ((p.debug & 128) && lane == 0 && codes) g_i8_dbg[c * 16 + 12] = gtime();
     } else if (warp == 3) {
         // ===================== stream-K publisher (off the epilogue's critical path) =======
         if (p.csize == 1 && u0 < u1 && u0 % p.KBLK != 0) {
@@ -226,7 +223,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             fence_after();
             const long long a1 = clock64();
             if ((p.debug & 64) && lane == 0 && first && seg == 0) g_i8_dbg[c * 16 + 6] = gtime();
-            if ((p.debug & 128) && lane == 0 && cu.u - u0 < 8 * GG::SPAN) g_i8_dbg[c * 16 + (cu.u - u0) / GG::SPAN] = gtime();
             tw += a1 - a0;
             const uint32_t d = tmem + db * DN;
             if (!(p.debug & 4)) {
@@ -319,7 +315,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             mbar_wait(&dfull[db], uint32_t(seg >> 1) & 1u);
             fence_after();
             if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 3] = gtime();
-            if ((p.debug & 128) && et == 0) g_i8_dbg[c * 16 + 13] = gtime();
             float acc[NT], pw[NT];
 #pragma unroll
             for (int t = 0; t < NT; ++t) pw[t] = pow_s[t];
@@ -376,7 +371,6 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                         }
                     }
                     mbar_wait(rfull, 0);
-                    if ((p.debug & 128) && et == 0) g_i8_dbg[c * 16 + 10] = gtime();
                     const float4* red = reinterpret_cast<const float4*>(p.direct ? smem + GG::PUSH_OFF : smem);
                     for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
 #pragma unroll
@@ -419,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                 __syncwarp();
                 if (lane == 0) mbar_arrive(pub);  // warp 3 publishes (gpu-scope fence + counter)
             }
-            if ((p.debug & 192) && et == 0) g_i8_dbg[c * 16 + 11] = gtime();
+            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 11] = gtime();
             u = uu;
             db ^= 1;
             ++seg;
@@ -556,7 +550,7 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     const char* dbg_env = std::getenv("RTNQ_WGEMM_DEBUG");
     const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
     unsigned long long* stamps = nullptr;  // planes-kernel globaltimer stamps (debug & 64)
-    if (dbg & 192) {
+    if (dbg & 64) {
         void* base = nullptr;
         if (cudaGetSymbolAddress(&base, i8::g_i8_dbg) == cudaSuccess)
             stamps = static_cast<unsigned long long*>(base) + 1023 * 16;
