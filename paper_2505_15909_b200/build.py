@@ -28,6 +28,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
           "-I", CSRC]
 CUFLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+# RTNQ_KERNEL_DEBUG=1 compiles in the int8 kernels' profiling knobs (RTNQ_WGEMM_DEBUG bits used
+# by scratch/i4prof.py, i8tl.py, ...); off by default because the checks cost a few % per launch
+if os.environ.get("RTNQ_KERNEL_DEBUG"):
+    CUFLAGS = CUFLAGS + ["-DRTNQ_KERNEL_DEBUG"]
 
 
 def sources():

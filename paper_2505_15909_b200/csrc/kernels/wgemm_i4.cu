@@ -144,11 +144,16 @@ __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64
 }
 
 // debug & 32: per-role blocked/busy cycles (lane 0 of the first warp of each role)
-#define I4_T0() const long long _t0 = (p.debug & 32) ? clock64() : 0
-#define I4_ACC(var) if (p.debug & 32) var += clock64() - _t0
+#define I4_T0() const long long _t0 = (dbg_ & 32) ? clock64() : 0
+#define I4_ACC(var) if (dbg_ & 32) var += clock64() - _t0
 
 template <int PT>
 __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
+#ifdef RTNQ_KERNEL_DEBUG
+    const int dbg_ = p.debug;  // profiling knobs (scratch/*prof*.py, *tl.py)
+#else
+    constexpr int dbg_ = 0;  // compiled out: even disabled, the checks cost a few % per launch
+#endif
     using GG = Geo<PT>;
     constexpr int NT = GG::ACC;
     constexpr int STAGES = GG::STAGES, DN = GG::DN, AP = GG::AP, NP = GG::NP, TPS = GG::TPS, EW = GG::EW;
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
     uint32_t* tslot = reinterpret_cast<uint32_t*>(pub + 1);
     float* sring = reinterpret_cast<float*>(smem + GG::SR_OFF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
-    if ((p.debug & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 5] = gtime();
+    if ((dbg_ & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 5] = gtime();
 
     int u0, u1;
     if (p.csize > 1) {
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             }
             uint8_t* st = smem + s * GG::STAGE_BYTES;
             const int slot0 = cu.kb & (TPS - 1);
-            if ((p.debug & 2) || (codes && (p.debug & 8192)) || (!codes && (p.debug & 4096))) {
+            if ((dbg_ & 2) || (codes && (dbg_ & 8192)) || (!codes && (dbg_ & 4096))) {
                 elect_arrive(&full[s]);  // profiling: no copy
             } else if (codes) {
                 // the row-block's rows padded to 8: the stride of its native scale groups
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
-        if ((p.debug & 32) && lane == 0 && codes) g_i4_dbg[c * 16] = w_empty;
+        if ((dbg_ & 32) && lane == 0 && codes) g_i4_dbg[c * 16] = w_empty;
     } else if (warp == 3) {
         // ===================== stream-K publisher =====================
         if (p.csize == 1 && u0 < u1 && u0 % p.KBLK != 0) {
@@ -287,9 +292,9 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 if (si >= NP) mbar_wait(&tfree[np], uint32_t(si / NP - 1) & 1u);
                 I4_ACC(x_tfree);
             }
-            const long long _tw = (p.debug & 32) ? clock64() : 0;
+            const long long _tw = (dbg_ & 32) ? clock64() : 0;
             const uint8_t* st = smem + s * GG::STAGE_BYTES;
-            if (!(p.debug & 65536)) {
+            if (!(dbg_ & 65536)) {
                 // all of the stage's code loads first (latency overlap), then expand and store
                 uint4 w[TPS][4];
 #pragma unroll
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                         }
                     }
                     const int slot = ap * TPS + j;
-                    if (!(p.debug & 8)) {
+                    if (!(dbg_ & 8)) {
                         // k-steps [0, KT): TMEM columns (4 codes each); [KT, 4): smem chunks
                         if constexpr (GG::KT == 4) tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + slot * 32), v);
                         if constexpr (GG::KT == 2) tmem_st16(tmem + lane_base + uint32_t(GG::A_COL + slot * 16), v);
@@ -343,12 +348,12 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
-            if (p.debug & 32) x_work += clock64() - _tw;
+            if (dbg_ & 32) x_work += clock64() - _tw;
             cu.advance(n);
             ++si;
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
-        if ((p.debug & 32) && threadIdx.x == kExp0 * 32) {
+        if ((dbg_ & 32) && threadIdx.x == kExp0 * 32) {
             g_i4_dbg[c * 16 + 2] = x_full, g_i4_dbg[c * 16 + 3] = x_aempty;
             g_i4_dbg[c * 16 + 4] = x_tfree, g_i4_dbg[c * 16 + 6] = x_work;
         }
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&full[s], ph);  // the planes of this stage
                 I4_ACC(m_full);
             }
-            if ((p.debug & 64) && si == 0 && lane == 0) g_i4_dbg[c * 16 + 6] = gtime();
+            if ((dbg_ & 64) && si == 0 && lane == 0) g_i4_dbg[c * 16 + 6] = gtime();
             {
                 I4_T0();
                 mbar_wait(&afull[ap], uint32_t(si / AP) & 1u);
@@ -385,9 +390,9 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 I4_ACC(m_tfree);
             }
             fence_after();
-            const long long _ti = (p.debug & 32) ? clock64() : 0;
+            const long long _ti = (dbg_ & 32) ? clock64() : 0;
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
-            if (!(p.debug & 4)) {
+            if (!(dbg_ & 4)) {
                 for (int j = 0; j < n; ++j) {
                     const int slot = ap * TPS + j;
                     const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
@@ -406,12 +411,12 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             commit_elect(&aempty[ap]);
             commit_elect(&tfull[np]);
             commit_elect(&empty[s]);
-            if (p.debug & 32) m_issue += clock64() - _ti;
+            if (dbg_ & 32) m_issue += clock64() - _ti;
             cu.advance(n);
             ++si;
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
-        if ((p.debug & 32) && lane == 0)
+        if ((dbg_ & 32) && lane == 0)
             g_i4_dbg[c * 16 + 8] = m_full, g_i4_dbg[c * 16 + 9] = m_afull, g_i4_dbg[c * 16 + 10] = m_tfree,
             g_i4_dbg[c * 16 + 1] = m_issue;
     } else if (warp >= kEpi0) {
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&tfull[np], uint32_t(si / NP) & 1u);
                 I4_ACC(e_wait);
             }
-            const long long _tw = (p.debug & 32) ? clock64() : 0;
+            const long long _tw = (dbg_ & 32) ? clock64() : 0;
             fence_after();
             float scg[TPS];
 #pragma unroll
@@ -459,14 +464,14 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             constexpr int CH = PT >= 16 ? 16 : PT;
             constexpr int LDC = PT >= 16 ? 16 : GG::DN;  // columns loaded per plane/chunk
 #pragma unroll
-            for (int jj = 0; jj < ((p.debug & 131072) ? 0 : PT); jj += CH) {
+            for (int jj = 0; jj < ((dbg_ & 131072) ? 0 : PT); jj += CH) {
                 // chunk jj of every group of the stage; group j + 1's TMEM loads are in flight
                 // while group j's accumulators are combined
                 // one warpgroup per group (EW == 2) keeps one group's registers only
                 uint32_t d[EW == 2 ? 1 : TPS][PT >= 16 ? 3 : 1][LDC];
                 auto load = [&](int j) {
                     const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
-                    if (!(p.debug & 16)) {
+                    if (!(dbg_ & 16)) {
                         if constexpr (PT >= 16) {
                             ld16(ta, d[EW == 2 ? 0 : j][0]);
                             ld16(ta + PT, d[EW == 2 ? 0 : j][1]);
@@ -504,7 +509,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 if (j0 < j1) {
                     load(j0);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (p.debug & 32) {
+                    if (dbg_ & 32) {
                         const long long t = clock64();
                         e_ld += t - _tw;
                     }
@@ -520,7 +525,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tfree[np]);
-            if (p.debug & 32) e_work += clock64() - _tw;
+            if (dbg_ & 32) e_work += clock64() - _tw;
             ++si;
             if (seg_end && EW == 2) {  // warpgroup B -> A through shared memory
                 float4* sc4 = reinterpret_cast<float4*>(scr) + row * (NT / 4);
@@ -642,14 +647,14 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             }
             cu.advance(n);
         }
-        if ((p.debug & 64) && et == 0) g_i4_dbg[c * 16 + 4] = gtime();
-        if ((p.debug & 32) && et == 0 && eg == 0)
+        if ((dbg_ & 64) && et == 0) g_i4_dbg[c * 16 + 4] = gtime();
+        if ((dbg_ & 32) && et == 0 && eg == 0)
             g_i4_dbg[c * 16 + 11] = e_wait, g_i4_dbg[c * 16 + 12] = e_work, g_i4_dbg[c * 16 + 13] = clock64() - e_t0,
             g_i4_dbg[c * 16 + 14] = si, g_i4_dbg[c * 16 + 15] = e_ld;
     }
     fence_before();
     __syncthreads();
-    if ((p.debug & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 7] = gtime();
+    if ((dbg_ & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 7] = gtime();
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));

@@ -83,6 +83,11 @@ __device__ unsigned long long g_i8_dbg[1024 * 16];  // profiling (debug & 32; & 
 
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_constant__ Params p) {
+#ifdef RTNQ_KERNEL_DEBUG
+    const int dbg_ = p.debug;  // profiling knobs (scratch/*prof*.py, *tl.py)
+#else
+    constexpr int dbg_ = 0;  // compiled out: even disabled, the checks cost a few % per launch
+#endif
     using GG = Geo<NT>;
     constexpr int STAGES = GG::STAGES, DN = GG::DN;
     extern __shared__ uint8_t smem_raw[];
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     uint64_t* pub = dempty + 4;     // stream-K contributor partials stored (4 warps)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 5);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
-    if ((p.debug & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 5] = gtime();
+    if ((dbg_ & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 5] = gtime();
 
     int u0, u1;
     if (p.csize > 1) {
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             // 128-code planes box; the MMA uses one half.
             const int ta = cu.kb >> 1, tb = (cu.kb + n - 1) >> 1;
             const int slot0 = ta & (GG::TPS - 1);
-            if (p.debug & 2) {
+            if (dbg_ & 2) {
                 elect_arrive(&full[s]);
             } else if (codes) {  // contiguous, pre-swizzled 16 KiB tiles
                 const int64_t tile = int64_t(cu.b) * kt + ta;
@@ -183,11 +188,11 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
-        if ((p.debug & 32) && lane == 0 && codes) {
+        if ((dbg_ & 32) && lane == 0 && codes) {
             g_i8_dbg[c * 8 + 0] = clock64() - t0;
             g_i8_dbg[c * 8 + 1] = tw;
         }
-        if ((p.debug & 64) && lane == 0 && codes) g_i8_dbg[c * 16 + 0] = gtime();
+        if ((dbg_ & 64) && lane == 0 && codes) g_i8_dbg[c * 16 + 0] = gtime();
     } else if (warp == 3) {
         // ===================== stream-K publisher (off the epilogue's critical path) =======
         if (p.csize == 1 && u0 < u1 && u0 % p.KBLK != 0) {
@@ -222,10 +227,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             mbar_wait(&full[s], ph);
             fence_after();
             const long long a1 = clock64();
-            if ((p.debug & 64) && lane == 0 && first && seg == 0) g_i8_dbg[c * 16 + 6] = gtime();
+            if ((dbg_ & 64) && lane == 0 && first && seg == 0) g_i8_dbg[c * 16 + 6] = gtime();
             tw += a1 - a0;
             const uint32_t d = tmem + db * DN;
-            if (!(p.debug & 4)) {
+            if (!(dbg_ & 4)) {
                 // k-block kb: tile slot (kb >> 1) % TPS, second 64-code half at +64 B
                 for (int j = 0; j < n; ++j) {
                     const int kb = cu.kb + j;
@@ -251,12 +256,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             if (++s == STAGES) s = 0, ph ^= 1u, lo = lo0;
             else lo += GG::STAGE_BYTES >> 4;
         }
-        if ((p.debug & 32) && lane == 0) {
+        if ((dbg_ & 32) && lane == 0) {
             g_i8_dbg[c * 8 + 2] = clock64() - t0;
             g_i8_dbg[c * 8 + 3] = tw;
             g_i8_dbg[c * 8 + 4] = ti;
         }
-        if ((p.debug & 64) && lane == 0) g_i8_dbg[c * 16 + 1] = gtime();
+        if ((dbg_ & 64) && lane == 0) g_i8_dbg[c * 16 + 1] = gtime();
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
@@ -276,15 +281,15 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                 if (kbe == p.KBLK || uu == u1) break;
             }
             const bool sole = kb0 == 0 && kbe == p.KBLK;
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 8] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 8] = gtime();
             const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
             const float srow = row < rows ? __half2float(__ushort_as_half(__ldg(p.scales + int64_t(b) * kRows + row))) : 0.0f;
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 9] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 9] = gtime();
             // Stream-K: the row-block's owner is the CTA holding its first k-block (for that
             // CTA it is the last segment, finished last); the other contributors hand over
             // partials from their first segment, usually long before. The owner collects them
             // while its own MMAs drain.
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 9] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 9] = gtime();
             const bool split = p.csize == 1 && !sole;
             const int c_first = split ? cta_of(int64_t(b) * p.KBLK, p.U, p.G) : c;
             const int c_last = split ? cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G) : c;
@@ -311,10 +316,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                     }
                 }
             }
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 2] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 2] = gtime();
             mbar_wait(&dfull[db], uint32_t(seg >> 1) & 1u);
             fence_after();
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 3] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 3] = gtime();
             float acc[NT], pw[NT];
 #pragma unroll
             for (int t = 0; t < NT; ++t) pw[t] = pow_s[t];
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
 #pragma unroll
             for (int j = 0; j < NT; j += 16) {
                 uint32_t d0[16], d1[16], d2[16];
-                if (p.debug & 16) {
+                if (dbg_ & 16) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) d0[e] = d1[e] = d2[e] = uint32_t(e + row);
                 } else {
@@ -345,12 +350,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&dempty[db]);
-            if ((p.debug & 64) && et == 0) {
+            if ((dbg_ & 64) && et == 0) {
                 g_i8_dbg[c * 16 + 12] = ck1 - ck0;
                 g_i8_dbg[c * 16 + 13] = ck2 - ck1;
                 g_i8_dbg[c * 16 + 14] = clock64() - ck2;
             }
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 10] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 10] = gtime();
             const int64_t n0 = int64_t(b) * kRows;
             if (p.csize > 1) {
                 // Cluster split-K (one segment per CTA): the leader (rank 0) opens its idle
@@ -413,16 +418,16 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                 __syncwarp();
                 if (lane == 0) mbar_arrive(pub);  // warp 3 publishes (gpu-scope fence + counter)
             }
-            if ((p.debug & 64) && et == 0) g_i8_dbg[c * 16 + 11] = gtime();
+            if ((dbg_ & 64) && et == 0) g_i8_dbg[c * 16 + 11] = gtime();
             u = uu;
             db ^= 1;
             ++seg;
         }
     }
-    if ((p.debug & 64) && threadIdx.x == kEpi0 * 32) g_i8_dbg[c * 16 + 4] = gtime();
+    if ((dbg_ & 64) && threadIdx.x == kEpi0 * 32) g_i8_dbg[c * 16 + 4] = gtime();
     fence_before();
     __syncthreads();
-    if ((p.debug & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 7] = gtime();
+    if ((dbg_ & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 7] = gtime();
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
