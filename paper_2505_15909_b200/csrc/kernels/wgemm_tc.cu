@@ -36,6 +36,14 @@
 #include "../common.cuh"
 #include "kernels.cuh"
 
+// Profiling knobs (RTNQ_WGEMM_DEBUG bits) are compiled in only with -DRTNQ_KERNEL_DEBUG
+// (RTNQ_KERNEL_DEBUG=1 at build time): even disabled, the checks cost a few % per launch.
+#ifdef RTNQ_KERNEL_DEBUG
+#define RTNQ_DBG(p) ((p).debug)
+#else
+#define RTNQ_DBG(p) 0
+#endif
+
 namespace rtnq_b200 {
 namespace tc {
 
@@ -391,7 +399,7 @@ struct Ring {
 // per-role blocked/total cycles, read back by rtnq_wgemm_debug_read.
 __device__ unsigned long long g_wgemm_dbg[1024 * 64];
 __device__ __forceinline__ void stamp(const Params& p, int slot) {
-    if (!(p.debug & 32)) return;
+    if (!(RTNQ_DBG(p) & 32)) return;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_wgemm_dbg[blockIdx.x * 64 + slot] = t;
@@ -534,7 +542,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         }
     };
 
-    if (p.debug & 1024) {
+    if (RTNQ_DBG(p) & 1024) {
         // profiling: the MMA issue stream alone (no other role, no barrier waits)
         if (warp == kMmaWarp) {
             constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
@@ -546,7 +554,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
             const uint32_t act0 = smem_u32(smem + GG::ACT_OFF);
             const long long t0 = clock64();
             const int units = (u1 - u0 + KPU - 1) / KPU;
-            if (p.debug & 65536) {
+            if (RTNQ_DBG(p) & 65536) {
                 // the microbenchmark's loop verbatim (scratch/tc_micro.cu "rotating")
                 const uint64_t bdesc = bdesc_hi | uint64_t((act0 >> 4) & 0x3FFFu);
                 for (int i = 0; i < units; ++i)
@@ -555,30 +563,30 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                                        bdesc + ((k * 2 * NT) & 1023), idesc, (k & 7) != 0);
             } else
             for (int i = 0; i < units; ++i) {
-                const int s = (p.debug & 4096) ? 0 : i % STAGES;
-                const int slot = (p.debug & 8192) ? 0 : i % RA;
+                const int s = (RTNQ_DBG(p) & 4096) ? 0 : i % STAGES;
+                const int slot = (RTNQ_DBG(p) & 8192) ? 0 : i % RA;
                 const uint64_t bdesc0 = bdesc_hi | uint64_t(((act0 + s * GG::STAGE_BYTES) >> 4) & 0x3FFFu);
                 for (int j = 0; j < gpu; ++j)
-                    issue_steps<kStep>(tmem + tsp.d_col0 + (((p.debug & 16384) ? 0 : (i * gpu + j)) & (ND - 1)) * NT,
+                    issue_steps<kStep>(tmem + tsp.d_col0 + (((RTNQ_DBG(p) & 16384) ? 0 : (i * gpu + j)) & (ND - 1)) * NT,
                                        tmem + slot * GG::SLOT_COLS + j * (GG::STEPS / gpu) * 8,
                                        bdesc0 + uint64_t(j * (GG::STEPS / gpu) * kStep), idesc,
                                        GG::STEPS / gpu);
-                if (!(p.debug & 2048)) {
+                if (!(RTNQ_DBG(p) & 2048)) {
                     tc_commit_elect(&done[i & 31]);
                     if (i >= 4) mbar_wait(&done[(i - 4) & 31], uint32_t((i - 4) >> 5) & 1u);
                 }
             }
             tc_commit_elect(&done[31]);
-            mbar_wait(&done[31], (p.debug & 2048) ? 0u : uint32_t(units > 31 ? 1 : 0));
+            mbar_wait(&done[31], (RTNQ_DBG(p) & 2048) ? 0u : uint32_t(units > 31 ? 1 : 0));
             const long long t1 = clock64();
-            if (lane == 0 && (p.debug & 32)) g_wgemm_dbg[blockIdx.x * 64 + 60] = (t1 - t0) / (units ? units : 1);
+            if (lane == 0 && (RTNQ_DBG(p) & 32)) g_wgemm_dbg[blockIdx.x * 64 + 60] = (t1 - t0) / (units ? units : 1);
         }
     } else if (warp == kProducerWarp) {
         // ===================== producer =====================
         // Codes and the unit's group scales: bulk copies of contiguous runs.  Activations:
         // one TMA box of BLK/8 k-chunks x NT tokens.  All complete on full[s].
         auto weights = [&](const Walker<KPU>& w, int n, int s) {
-            if (lane != 0 || (p.debug & 2)) return;
+            if (lane != 0 || (RTNQ_DBG(p) & 2)) return;
             const int rows = min(kRows, int(p.N - int64_t(w.b) * kRows));
             const int rows8 = (rows + 7) / 8 * 8, kbase = w.kb * kKB;
             const uint32_t code_bytes = uint32_t(n * CPR * rows * 16);
@@ -597,7 +605,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         };
         auto acts = [&](const Walker<KPU>& w, int s) {
             if (lane != 0) return;
-            if (p.debug & 2) {
+            if (RTNQ_DBG(p) & 2) {
                 mbar_arrive(&full[s]);
                 return;
             }
@@ -629,7 +637,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
         Walker<KPU> pf = w;
         auto prefetch_unit = [&](const Walker<KPU>& x) {
             const int n = x.chunk(), rows = min(kRows, int(p.N - int64_t(x.b) * kRows));
-            if (lane == 0 && !(p.debug & 2))
+            if (lane == 0 && !(RTNQ_DBG(p) & 2))
                 prefetch_l2(p.codes + (int64_t(x.b) * kRows * p.KBLK * CPR + int64_t(x.kb) * CPR * rows) * 16,
                             uint32_t(n * CPR * rows * 16));
         };
@@ -657,7 +665,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
     } else if (warp >= kMmaWarp) {
         // ===================== MMA issuers (warp-uniform, one lane issues) =====================
         const int par = warp - kMmaWarp;
-        const int nmma = (p.debug & 512) ? 1 : kMmaWarps;  // profiling: one warp issues all
+        const int nmma = (RTNQ_DBG(p) & 512) ? 1 : kMmaWarps;  // profiling: one warp issues all
         constexpr uint32_t fmt = AT == RTNQ_BF16 ? 1u : 0u;
         constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                    (uint32_t(NT >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
@@ -689,11 +697,11 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                     tc_fence_after();
                 }
                 PT_BEGIN(tiss);
-                if (p.debug & 4) {
+                if (RTNQ_DBG(p) & 4) {
                 } else if (n == KPU && kbase == blk) {  // full aligned unit: unrolled issue
-                    const uint32_t a_use = (p.debug & 131072) ? tmem : a_base;  // profiling knobs
+                    const uint32_t a_use = (RTNQ_DBG(p) & 131072) ? tmem : a_base;  // profiling knobs
                     const uint64_t b_use =
-                        (p.debug & 262144) ? (bdesc_hi | uint64_t((act0 >> 4) & 0x3FFFu)) : bdesc0;
+                        (RTNQ_DBG(p) & 262144) ? (bdesc_hi | uint64_t((act0 >> 4) & 0x3FFFu)) : bdesc0;
                     issue_unit_lg<GG::STEPS, NT, kStep>(lg, d_base + (ob0 & (ND - 1)) * NT, a_use,
                                                         b_use, idesc);
                 } else {
@@ -729,7 +737,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                 const uint8_t* st = smem + s * GG::STAGE_BYTES + row * 16;
                 const uint32_t ta = tmem + lane_base + slot * GG::SLOT_COLS;
 #pragma unroll
-                if (p.debug & 256) {  // profiling: barrier protocol only
+                if (RTNQ_DBG(p) & 256) {  // profiling: barrier protocol only
                     if (i >= RA) PWAIT(&done[(i - RA) & 31], uint32_t((i - RA) >> 5) & 1u, 1);
                 } else
                 for (int h = 0; h < KPU / 2; ++h) {  // two k-blocks (64 columns) at a time
@@ -779,7 +787,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
                             }
                         }
                         PT_BEGIN(tw);
-                        if (!(p.debug & 8)) {
+                        if (!(RTNQ_DBG(p) & 8)) {
                             tmem_st32(ta + h * 64, col);
                             if (2 * h + 1 < n) tmem_st32(ta + h * 64 + 32, col + 32);
                         }
@@ -898,7 +906,7 @@ __global__ void __maxnreg__(128) wgemm_tc_kernel(const __grid_constant__ Params 
 #pragma unroll
                 for (int jj = 0; jj < NT; jj += 32) {
                     uint32_t v[32];
-                    if (!(p.debug & 16)) {
+                    if (!(RTNQ_DBG(p) & 16)) {
                         tmem_ld16_nw(tmem + lane_base + tsp.d_col0 + buf * NT + jj, v);
                         if constexpr (NT >= 32)
                             tmem_ld16_nw(tmem + lane_base + tsp.d_col0 + buf * NT + jj + 16, v + 16);
