@@ -462,3 +462,29 @@ def test_chained_linears_pdl_graph_identical(m):
     for i, (o, r) in enumerate(zip(outs, ref)):
         assert torch.equal(o, r), f"linear {i} {shapes[i]} differs in the eager chain"
     assert all(torch.isfinite(r.float()).all() for r in ref)
+
+
+@pytest.mark.parametrize("bits", [8, 4])
+def test_405b_ffn_up_full_shape(bits):
+    """The largest single-GPU linear of the BASELINE configs (Llama-3.1-405B ffn_up,
+    106496 x 16384, 1.7 GB at W8) at batch 16 through the fused int8 path, against an f64
+    product of the dequantized weights (the f16 scales the kernels use).  Bar: 1e-5 relative
+    Frobenius (measured 7e-8 at W8, 2e-7 at W4)."""
+    n, k, m = 106496, 16384, 16
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    w = ((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1) * 0.02).to(torch.bfloat16)
+    g = k if bits == 8 else 128
+    q = rq.quantize_pack(w, bits, g, ragged=bits == 8, scales_f16=True, row_major=True)
+    del w
+    x = torch.randn(m, k, device="cuda", generator=gen).to(torch.bfloat16)
+    y = rq.linear(x, q, out_dtype=torch.float32)
+    wd = rq.dequantize(q.codes_row_major, rq.layout(rq.ROW_MAJOR), bits, n, k, g, q.scales_f16, rq.F16,
+                       rq.SCALES_REF)
+    num = den = 0.0
+    for i in range(0, n, 8192):
+        r = x.double() @ wd[i:i + 8192].double().t()
+        num += ((y[:, i:i + 8192].double() - r) ** 2).sum().item()
+        den += (r ** 2).sum().item()
+    del q, wd, y
+    torch.cuda.empty_cache()
+    assert (num / den) ** 0.5 < 1e-5
