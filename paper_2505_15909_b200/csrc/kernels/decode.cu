@@ -338,7 +338,9 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
             const uint32_t my = static_cast<uint32_t>(__cvta_generic_to_shared(mine));
             float mq[8], lq[8];
             float M = -INFINITY;
-            for (int q = 0; q < nsp; ++q) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {  // nsp <= 8: fixed trip count keeps mq/lq in registers
+                if (q >= nsp) break;
                 uint32_t ra;
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my), "r"(q));
                 asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(mq[q]) : "r"(ra));
@@ -346,7 +348,9 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                 M = fmaxf(M, mq[q]);
             }
             float L = 0.0f, a[4] = {0, 0, 0, 0};
-            for (int q = 0; q < nsp; ++q) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q >= nsp) break;
                 uint32_t ra;
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my + uint32_t(16 + 16 * lane)), "r"(q));
                 float4 x;
