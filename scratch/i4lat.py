@@ -1,5 +1,6 @@
 """W4 steady-state stage latency (RTNQ_WGEMM_DEBUG=256): issue -> full (seen by the expansion),
--> expansion done, and MMA full pass, for stage iterations 8..11 of gate_up (us, median over CTAs)."""
+-> expansion done, and MMA full pass, for stage iterations 8..11 of gate_up (us, median over CTAs).
+Needs a profiling build: RTNQ_KERNEL_DEBUG=1 python -c "import paper_2505_15909_b200.build as b; b.build()"."""
 import os, sys, ctypes, torch, numpy as np
 sys.path.insert(0, os.getcwd())
 os.environ["RTNQ_WGEMM_DEBUG"] = str(256 | int(os.environ.get("DBG", "0")))

@@ -1,4 +1,5 @@
-"""W4 int8-MMA kernel per-role cycles (RTNQ_WGEMM_DEBUG=32), median over CTAs (kcycles)."""
+"""W4 int8-MMA kernel per-role cycles (RTNQ_WGEMM_DEBUG=32), median over CTAs (kcycles).
+Needs a profiling build: RTNQ_KERNEL_DEBUG=1 python -c "import paper_2505_15909_b200.build as b; b.build()"."""
 import os, sys, ctypes, torch, numpy as np
 sys.path.insert(0, os.getcwd())
 os.environ["RTNQ_WGEMM_DEBUG"] = str(32 | int(os.environ.get("DBG", "0")))

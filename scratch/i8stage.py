@@ -1,5 +1,6 @@
 """W8 per-stage timeline (RTNQ_WGEMM_DEBUG=128) of the last of 6 graph-launched linears, us
-relative to the planes kernel's release (griddepcontrol.wait returning)."""
+relative to the planes kernel's release (griddepcontrol.wait returning).
+Needs a profiling build: RTNQ_KERNEL_DEBUG=1 python -c "import paper_2505_15909_b200.build as b; b.build()"."""
 import os, sys, ctypes, torch, numpy as np
 sys.path.insert(0, os.getcwd())
 os.environ["RTNQ_WGEMM_DEBUG"] = str(128 | int(os.environ.get("DBG", "0")))

@@ -1,4 +1,5 @@
-"""int8 W8 path timeline (RTNQ_WGEMM_DEBUG=64): planes kernel and per-CTA GEMM stamps (us)."""
+"""int8 W8 path timeline (RTNQ_WGEMM_DEBUG=64): planes kernel and per-CTA GEMM stamps (us).
+Needs a profiling build: RTNQ_KERNEL_DEBUG=1 python -c "import paper_2505_15909_b200.build as b; b.build()"."""
 import os, sys, ctypes, torch, numpy as np
 sys.path.insert(0, os.getcwd())
 os.environ["RTNQ_WGEMM_DEBUG"] = str(64 | int(os.environ.get("DBG", "0")))
