@@ -113,6 +113,11 @@ __device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t ad, uint64_t b
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ bool elect_leader() {
+    uint32_t e;
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(e));
+    return e != 0;
+}
 __device__ __forceinline__ void commit_elect(uint64_t* b) {
     asm volatile(
         "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"

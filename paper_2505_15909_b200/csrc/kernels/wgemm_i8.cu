@@ -231,17 +231,22 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             tw += a1 - a0;
             const uint32_t d = tmem + db * DN;
             if (!(dbg_ & 4)) {
-                // k-block kb: tile slot (kb >> 1) % TPS, second 64-code half at +64 B
-                for (int j = 0; j < n; ++j) {
-                    const int kb = cu.kb + j;
-                    const uint32_t alo = lo + uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::CODE_BYTES >> 4)) +
-                                         ((kb & 1) ? 4u : 0u);
-                    const uint32_t blo = lo + uint32_t(GG::PLANE_OFF >> 4) +
-                                         uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::PLANE_BYTES >> 4)) +
-                                         ((kb & 1) ? 4u : 0u);
-                    mma_i8_elect(d, kHi | alo, kHi | blo, idesc, (first && j == 0) ? 0u : 1u);
-                    mma_i8_elect(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
+                // one elected thread issues the stage's MMAs back to back (commit_elect below
+                // elects the same lane); k-block kb: tile slot (kb >> 1) % TPS, second
+                // 64-code half at +64 B
+                if (elect_leader()) {
+                    for (int j = 0; j < n; ++j) {
+                        const int kb = cu.kb + j;
+                        const uint32_t alo = lo + uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::CODE_BYTES >> 4)) +
+                                             ((kb & 1) ? 4u : 0u);
+                        const uint32_t blo = lo + uint32_t(GG::PLANE_OFF >> 4) +
+                                             uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::PLANE_BYTES >> 4)) +
+                                             ((kb & 1) ? 4u : 0u);
+                        mma_i8(d, kHi | alo, kHi | blo, idesc, (first && j == 0) ? 0u : 1u);
+                        mma_i8(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
+                    }
                 }
+                __syncwarp();
             }
             first = false;
             commit_elect(&empty[s]);
