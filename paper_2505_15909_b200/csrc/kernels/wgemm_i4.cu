@@ -110,6 +110,14 @@ __device__ __forceinline__ void mma_i8_ts_elect(uint32_t d, uint32_t a, uint64_t
         "r"(a), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
 }
+// Plain TS issue (the caller is the one elected thread).
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+        "r"(a), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
@@ -393,20 +401,25 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             const long long _ti = (dbg_ & 32) ? clock64() : 0;
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
             if (!(dbg_ & 4)) {
-                for (int j = 0; j < n; ++j) {
-                    const int slot = ap * TPS + j;
-                    const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
-                    const uint32_t alo = base + uint32_t((GG::A_OFF + slot * GG::A_SMEM) >> 4);
-                    const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
-                    const uint32_t d = tmem + uint32_t((np * TPS + j) * DN);
+                // one elected thread issues the stage's MMAs back to back (the commits below
+                // elect the same lane)
+                if (elect_leader()) {
+                    for (int j = 0; j < n; ++j) {
+                        const int slot = ap * TPS + j;
+                        const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
+                        const uint32_t alo = base + uint32_t((GG::A_OFF + slot * GG::A_SMEM) >> 4);
+                        const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
+                        const uint32_t d = tmem + uint32_t((np * TPS + j) * DN);
 #pragma unroll
-                    for (uint32_t k = 0; k < 4; ++k) {  // K = 32 per MMA: TMEM +8 columns, smem +32 bytes
-                        if (int(k) < GG::KT)
-                            mma_i8_ts_elect(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
-                        else
-                            mma_i8_elect(d, kHi | (alo + 2 * k), kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                        for (uint32_t k = 0; k < 4; ++k) {  // K = 32 per MMA: TMEM +8 columns, smem +32 bytes
+                            if (int(k) < GG::KT)
+                                mma_i8_ts(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                            else
+                                mma_i8(d, kHi | (alo + 2 * k), kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
+                        }
                     }
                 }
+                __syncwarp();
             }
             commit_elect(&aempty[ap]);
             commit_elect(&tfull[np]);
