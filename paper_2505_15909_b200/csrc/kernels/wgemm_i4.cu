@@ -400,10 +400,9 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             fence_after();
             const long long _ti = (dbg_ & 32) ? clock64() : 0;
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
-            if (!(dbg_ & 4)) {
-                // one elected thread issues the stage's MMAs back to back (the commits below
-                // elect the same lane)
-                if (elect_leader()) {
+            // one elected thread issues the stage's MMAs back to back and their commits
+            if (elect_leader()) {
+                if (!(dbg_ & 4)) {
                     for (int j = 0; j < n; ++j) {
                         const int slot = ap * TPS + j;
                         const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
@@ -419,11 +418,11 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                         }
                     }
                 }
-                __syncwarp();
+                commit(&aempty[ap]);
+                commit(&tfull[np]);
+                commit(&empty[s]);
             }
-            commit_elect(&aempty[ap]);
-            commit_elect(&tfull[np]);
-            commit_elect(&empty[s]);
+            __syncwarp();
             if (dbg_ & 32) m_issue += clock64() - _ti;
             cu.advance(n);
             ++si;

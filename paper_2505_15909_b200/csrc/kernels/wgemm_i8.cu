@@ -230,11 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             if ((dbg_ & 64) && lane == 0 && first && seg == 0) g_i8_dbg[c * 16 + 6] = gtime();
             tw += a1 - a0;
             const uint32_t d = tmem + db * DN;
-            if (!(dbg_ & 4)) {
-                // one elected thread issues the stage's MMAs back to back (commit_elect below
-                // elects the same lane); k-block kb: tile slot (kb >> 1) % TPS, second
-                // 64-code half at +64 B
-                if (elect_leader()) {
+            // one elected thread issues the stage's MMAs back to back and their commits;
+            // k-block kb: tile slot (kb >> 1) % TPS, second 64-code half at +64 B
+            if (elect_leader()) {
+                if (!(dbg_ & 4)) {
                     for (int j = 0; j < n; ++j) {
                         const int kb = cu.kb + j;
                         const uint32_t alo = lo + uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::CODE_BYTES >> 4)) +
@@ -246,13 +245,13 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                         mma_i8(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
                     }
                 }
-                __syncwarp();
+                commit(&empty[s]);
+                if (seg_end) commit(&dfull[db]);
             }
+            __syncwarp();
             first = false;
-            commit_elect(&empty[s]);
             ti += clock64() - a1;
             if (seg_end) {
-                commit_elect(&dfull[db]);
                 db ^= 1;
                 ++seg;
                 first = true;
