@@ -78,7 +78,7 @@ struct Geo {
     // by the expansion; the MMA's A reads share the 64 B/clk TMEM read port with the epilogue's
     // accumulator readback), the rest from a 128B-swizzled smem tile (128 B/clk smem port,
     // shared with TMA and the planes).  KT balances the two ports for the batch size.
-    static constexpr int KT = PT <= 32 ? 4 : 0;
+    static constexpr int KT = 4;
     static constexpr int AS = PT <= 10 ? 8 : PT <= 32 ? 4 : 2;  // expanded A slots (groups)
     static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
     static constexpr int A_SMEM = KT < 4 ? kRows * 128 : 0;  // smem A tile per slot (16 KiB)
