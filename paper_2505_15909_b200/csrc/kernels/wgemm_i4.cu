@@ -79,7 +79,7 @@ struct Geo {
     // accumulator readback), the rest from a 128B-swizzled smem tile (128 B/clk smem port,
     // shared with TMA and the planes).  KT balances the two ports for the batch size.
     static constexpr int KT = 4;
-    static constexpr int AS = PT <= 10 ? 8 : PT <= 16 ? 6 : PT <= 32 ? 4 : 2;  // expanded A slots (groups)
+    static constexpr int AS = PT <= 16 ? 6 : PT <= 32 ? 4 : 2;  // expanded A slots (groups)
     static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
     static constexpr int A_SMEM = KT < 4 ? kRows * 128 : 0;  // smem A tile per slot (16 KiB)
     static constexpr int STAGES_FIT = (212 * 1024 - SCR_BYTES - AS * A_SMEM) / STAGE_BYTES;
