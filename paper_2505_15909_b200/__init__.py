@@ -313,30 +313,68 @@ _default_ws = {}
 FLAG_PDL = 1
 
 
+def _default_workspace(device, stream, nbytes):
+    """The per-(device, stream) default workspace (its stream-K counters and partials must not
+    be shared by two streams at once)."""
+    key = (str(device), _stream(stream).value)
+    ws = _default_ws.get(key)
+    if ws is None:
+        ws = _default_ws[key] = Workspace(nbytes, device)
+    return ws
+
+
+_err_flags = {}
+
+
+def error_flag(device):
+    """A zeroed device int32 flag for the ``err=`` argument of the device API."""
+    torch = _torch()
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def check_flag(err, stream=None):
+    """Synchronize ``stream`` and raise InvalidInputError if ``err`` was set (then clear it)
+    (rtnq_dev_check_flag)."""
+    _check(lib().rtnq_dev_check_flag(_ptr(err), _stream(stream)))
+
+
 def linear(a, qw: QuantWeight, out=None, out_dtype=None, *, path=PATH_FUSED,
            threshold=DEFAULT_THRESHOLD, workspace: Workspace | None = None, stream=None,
-           pdl=False):
+           pdl=False, err=None, check=None):
     """out[m, n] = a[m, k] @ W^T with W = codes * scales (rtnq_dev_linear_ex).
 
     The tensor-core path runs for bf16/f16 ``a`` against the native layout.
     ``pdl=True`` lets the weight prefetch overlap the previous kernel (the caller
-    asserts that kernel does not write this weight)."""
+    asserts that kernel does not write this weight).
+
+    Non-finite activations are the reference's InvalidInputError (gemm.cpp:13-19).  With
+    ``err`` (a device int32 flag, :func:`error_flag`) the kernels OR 1 into it asynchronously
+    and the caller checks it later (:func:`check_flag`, e.g. once per decode step); without it
+    (``check`` defaults to True outside CUDA-graph capture) the call synchronizes and raises."""
     torch = _torch()
     assert a.is_cuda and a.dim() == 2 and a.is_contiguous() and a.shape[1] == qw.cols
     m = a.shape[0]
     if out is None:
         out = torch.empty(m, qw.rows, dtype=out_dtype or a.dtype, device=a.device)
+    if check is None:
+        check = err is None and not torch.cuda.is_current_stream_capturing()
+    if check and err is None:
+        err = _err_flags.get(str(a.device))
+        if err is None:
+            err = _err_flags[str(a.device)] = error_flag(a.device)
     lay = layout(qw.layout)
     wsb = lib().rtnq_dev_linear_workspace_bytes(m, qw.rows, qw.cols, qw.bits, qw.group, path, lay)
     if workspace is None:
-        workspace = _default_ws.setdefault(a.device, Workspace(wsb, a.device))
+        workspace = _default_workspace(a.device, stream, wsb)
     buf = workspace.ensure(wsb)
     chosen = C.c_int(-1)
     _check(lib().rtnq_dev_linear_ex(
         _ptr(a), _dt(a), m, qw.cols, _ptr(qw.codes), lay, qw.bits, qw.rows, qw.group,
         int(qw.ragged), _ptr(qw.scales), F16, SCALES_NATIVE, _ptr(out), _dt(out), path,
-        threshold, C.byref(chosen), None, _ptr(buf), buf.numel(), _stream(stream),
+        threshold, C.byref(chosen), _ptr(err), _ptr(buf), buf.numel(), _stream(stream),
         FLAG_PDL if pdl else 0))
+    if check:
+        check_flag(err, stream)
     return out
 
 
@@ -405,7 +443,7 @@ def linear_planes(planes: Planes, qw: QuantWeight, out, *, workspace: Workspace 
     wsb = lib().rtnq_dev_linear_workspace_bytes(m, qw.rows, qw.cols, qw.bits, qw.group, PATH_FUSED,
                                                 layout(qw.layout))
     if workspace is None:
-        workspace = _default_ws.setdefault(out.device, Workspace(wsb, out.device))
+        workspace = _default_workspace(out.device, stream, wsb)
     buf = workspace.ensure(wsb)
     _check(lib().rtnq_dev_linear_planes(
         _ptr(planes.planes), _ptr(planes.texp), m, k, _ptr(qw.codes), layout(qw.layout), qw.bits, qw.rows,

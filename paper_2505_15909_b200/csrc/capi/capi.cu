@@ -297,9 +297,14 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
         path = m >= threshold ? RTNQ_PATH_DEQUANT_FIRST : RTNQ_PATH_FUSED;
     }
     if (chosen) *chosen = path;
-    if (err && m * k) launch_check_finite(a, a_dtype, m * k, err, st);
-    if (m * n == 0) return RTNQ_OK;
     const Layout L = to_layout(layout);
+    // the int8 kernels check the activations in their planes pass; every other path runs a
+    // separate finiteness pass (InvalidInputError, gemm.cpp:13-19)
+    const bool planes_check = path == RTNQ_PATH_FUSED && n > 0 &&
+                              (i8_path(a_dtype, layout, bits, g, k, sdtype) ||
+                               i4_path(a_dtype, layout, bits, g, sdtype, sorder));
+    if (err && m * k && !planes_check) launch_check_finite(a, a_dtype, m * k, err, st);
+    if (m * n == 0) return RTNQ_OK;
     if (path == RTNQ_PATH_FUSED && tensor_path(a_dtype, layout, sdtype, sorder)) {
         if (const char* why = wgemm_unsupported(m, n, k, bits, g, a_dtype))
             return fail(RTNQ_E_UNSUPPORTED, why);
@@ -327,6 +332,7 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
             return fail(RTNQ_E_INVALID_INPUT, "tensor-core path needs 16-byte aligned operands");
         WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
                     out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
+        A.err = err;
         RTNQ_CUDA(launch_wgemm_i8(A, st));
         return RTNQ_OK;
     }
@@ -342,6 +348,7 @@ rtnq_status rtnq_dev_linear_ex(const void* a, int a_dtype, int64_t m, int64_t k,
             return fail(RTNQ_E_INVALID_INPUT, "tensor-core path needs 16-byte aligned operands");
         WgemmArgs A{a, a_dtype, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
                     out, odtype, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
+        A.err = err;
         RTNQ_CUDA(launch_wgemm_i4(A, st));
         return RTNQ_OK;
     }

@@ -59,8 +59,8 @@ __device__ __forceinline__ float scale_from_absmax(float absmax, int bits) {
 //                                      exact quotient is just below an integer,
 //                                      where rounding returns k anyway;
 //   n = k + (|v| - (k + 0.5) * S >= 0)  evaluated with one FMA (exact sign).
-// Verified bit-exact against the reference by tests/test_gpu_quant.py on
-// tie-rich inputs (every element on or one ulp beside a tie).
+// Verified bit-exact against the reference by tests/test_gpu_full_shapes.py
+// (test_quantize_f32_ties_bit_exact: f32 weights on or one ulp beside a tie).
 __device__ __forceinline__ int quantize_one(float v, float s, int bits) {
     const float a = fabsf(v);
     const float q = __fdiv_rn(a, s);

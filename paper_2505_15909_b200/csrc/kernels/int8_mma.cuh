@@ -226,7 +226,8 @@ template <int AT, bool VEC>
 __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* __restrict__ a, int K, int M,
                                                                    int8_t* __restrict__ planes,
                                                                    int32_t* __restrict__ texp, unsigned long long* stamps,
-                                                                   const WeightPrefetch pf, int early) {
+                                                                   const WeightPrefetch pf, int early,
+                                                                   int32_t* __restrict__ err) {
     __shared__ float wmax[kPlaneThreads / 32];
     const bool first = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
     if (stamps && first) stamps[0] = gtime();
@@ -252,10 +253,18 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
         if constexpr (AT == RTNQ_BF16) return __uint_as_float(h << 16);
         else return __half2float(__ushort_as_half(static_cast<unsigned short>(h)));
     };
+    // non-finite inputs (InvalidInputError in the reference, gemm.cpp:13-19): an all-ones
+    // exponent field in either half of a word, folded into the max pass
+    constexpr uint32_t kExpMask = AT == RTNQ_BF16 ? 0x7F807F80u : 0x7C007C00u;
+    uint32_t nonfinite = 0;
     auto vmax = [&](const uint4& q, float m) {
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) m = fmaxf(m, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+        for (int i = 0; i < 4; ++i) {
+            m = fmaxf(m, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+            const uint32_t e = w[i] & kExpMask;
+            nonfinite |= ((e & 0xffffu) == (kExpMask & 0xffffu)) | ((e >> 16) == (kExpMask >> 16));
+        }
         return m;
     };
     // this CTA's slice stays in registers; the rest of the row is only max-reduced
@@ -278,6 +287,7 @@ __global__ void __launch_bounds__(kPlaneThreads) act_planes_kernel(const void* _
     }
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) wmax[warp] = mx;
+    if (err && blockIdx.y == 0 && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(err, 1);
     __syncthreads();
     float amax = 0.0f;
 #pragma unroll
@@ -372,7 +382,7 @@ __device__ __forceinline__ void row_to_planes(const uint16_t* __restrict__ rowp,
 
 template <int AT, bool VEC>
 inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, int32_t* texp, unsigned long long* stamps,
-                                 const WeightPrefetch& pf,
+                                 const WeightPrefetch& pf, int32_t* err,
                                  cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(M), unsigned((K / 8 + kSliceV - 1) / kSliceV));
@@ -387,7 +397,7 @@ inline cudaError_t launch_planes(const void* a, int K, int M, int8_t* planes, in
         const char* e = std::getenv("RTNQ_PDL_EARLY");
         return e ? std::atoi(e) : 1;
     }();
-    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps, pf, early);
+    return cudaLaunchKernelEx(&cfg, act_planes_kernel<AT, VEC>, a, K, M, planes, texp, stamps, pf, early, err);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -62,6 +62,9 @@ struct WgemmArgs {
     // computes them itself); [3][m][k] int8 and [m] exponents
     const int8_t* planes = nullptr;
     const int32_t* texp = nullptr;
+    // int8 kernels computing their own planes: |= 1 on a non-finite activation (the planes
+    // kernel's max pass checks it; InvalidInputError in the reference, gemm.cpp:13-19)
+    int32_t* err = nullptr;
 };
 // Validates the shape for the tensor-core path; returns a message or nullptr.
 const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);

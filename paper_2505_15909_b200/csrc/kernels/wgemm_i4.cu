@@ -806,9 +806,9 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st)
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, A.err, st)
             : (vec ? imma::launch_planes<RTNQ_F16, true> : imma::launch_planes<RTNQ_F16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st);
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, A.err, st);
         if (e != cudaSuccess) return e;
     }
     p.codes = A.codes;

@@ -535,9 +535,9 @@ cudaError_t launch_act_planes(const void* a, int a_dtype, int64_t m, int64_t k, 
     imma::WeightPrefetch none;
     return a_dtype == RTNQ_BF16
         ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(
-              a, int(k), int(m), planes, texp, nullptr, none, st)
+              a, int(k), int(m), planes, texp, nullptr, none, nullptr, st)
         : (vec ? imma::launch_planes<RTNQ_F16, true> : imma::launch_planes<RTNQ_F16, false>)(
-              a, int(k), int(m), planes, texp, nullptr, none, st);
+              a, int(k), int(m), planes, texp, nullptr, none, nullptr, st);
 }
 
 cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
@@ -594,9 +594,9 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? i8::launch_planes<RTNQ_BF16, true> : i8::launch_planes<RTNQ_BF16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st)
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, A.err, st)
             : (vec ? i8::launch_planes<RTNQ_F16, true> : i8::launch_planes<RTNQ_F16, false>)(
-                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, st);
+                  A.a, int(A.k), int(A.m), planes, texp, stamps, pf, A.err, st);
         if (e != cudaSuccess) return e;
     }
     // 2. the GEMM

@@ -11,9 +11,13 @@ process per GPU, ``torch.distributed`` NCCL for the two sum-allreduces per layer
   boundaries, each rank producing a partial [batch x hidden] that is summed by an
   allreduce.
 
-Quantize-then-shard equals shard-then-quantize for every split here: rows are quantized
-independently (quant.cpp:118-136) and the K split falls on group boundaries, so no
-group straddles two ranks (checked in tests/test_tp.py).
+Weights are quantized BEFORE sharding: each rank quantizes the full module
+weight once (rq.quantize_pack, the same kernel as TP=1), then keeps its rows (column split)
+or its K slice (row split) of the row-major codes and of the scales (``shard_quantized``) and
+relays them out into the kernels' layout.  For group-128 weights this equals quantizing the
+shard (rows quantize independently, quant.cpp:118-136, and the K split falls on group
+boundaries); for W8 per-channel (one group per full row, configs[2]) it does NOT -- a row-split
+shard keeps the full row's scale, which only the full row's absmax gives (tests/test_tp.py).
 
 The per-(layer, module) bit width comes from the selective-precision table
 (plan.resolve, plan.cpp:189-224): the same table on every rank picks the W4 or W8
@@ -72,7 +76,7 @@ def local_dims(shape: LlamaShape, world: int, group: int = 128) -> LocalDims:
         raise ValueError(f"{shape.name}: heads/kv_heads/ffn must divide by TP={world}")
     hq, hkv, f = shape.heads // world, shape.kv_heads // world, shape.ffn // world
     for k in (hq * shape.head_dim, f):  # row-split K extents must be whole groups
-        if group < k and k % group:
+        if k % group:
             raise ValueError(f"row-split width {k} is not a multiple of the group size {group}")
     return LocalDims(hq, hkv, f, (hq + 2 * hkv) * shape.head_dim, hq * shape.head_dim)
 
@@ -109,6 +113,39 @@ def shard_module(w, module: str, shape: LlamaShape, rank: int, world: int):
     return shard_cols(w, rank, world)
 
 
+def shard_quantized(codes_rm, scales, module: str, shape: LlamaShape, rank: int, world: int,
+                    bits: int, group: int):
+    """This rank's shard of a weight quantized in full (quantize-before-shard).
+
+    ``codes_rm`` are the full weight's row-major packed codes viewed as [rows, cols*bits/8]
+    bytes (QuantTensor::data, quant.cpp:139), ``scales`` its [rows, groups_per_row] scales
+    (any dtype; reference order, quant.hpp:33); ``group`` the full weight's group size.
+    Returns (codes [n, k*bits/8], scales [n, gpr'], k, group', ragged') of the shard:
+    column splits keep whole rows; row splits keep a K slice of every row and the scales of
+    the groups in it -- for one group per row (W8 per-channel) that is the FULL row's scale,
+    and the shard is again one (ragged) group per row."""
+    rows, nbytes = codes_rm.shape
+    k_full = nbytes * 8 // bits
+    if module in ("qkv_proj", "ffn_up"):
+        return (shard_module(codes_rm, module, shape, rank, world),
+                shard_module(scales, module, shape, rank, world), k_full, group,
+                k_full % group != 0)
+    k = k_full // world
+    b0, b1 = rank * k * bits // 8, (rank + 1) * k * bits // 8
+    c = codes_rm[:, b0:b1]
+    c = np.ascontiguousarray(c) if isinstance(c, np.ndarray) else c.contiguous()
+    if group >= k_full:  # one group per row: the shard keeps the full-row scale
+        g = 1 << (k - 1).bit_length()
+        s = scales[:, :1]
+        s = np.ascontiguousarray(s) if isinstance(s, np.ndarray) else s.contiguous()
+        return c, s, k, g, k % g != 0
+    if k % group:
+        raise ValueError(f"row-split width {k} is not a multiple of the group size {group}")
+    s = scales[:, rank * (k // group):(rank + 1) * (k // group)]
+    s = np.ascontiguousarray(s) if isinstance(s, np.ndarray) else s.contiguous()
+    return c, s, k, group, False
+
+
 def _cat(parts):
     if isinstance(parts[0], np.ndarray):
         return np.ascontiguousarray(np.concatenate(parts, axis=0))
@@ -129,6 +166,25 @@ def group_for(bits: int, k: int, group: int = 128, w8_per_channel: bool = False)
 
 
 # ---- the layer (CUDA) ------------------------------------------------------------------------
+
+def quantize_module(w, module: str, shape: LlamaShape, rank: int, world: int, bits: int,
+                    group: int, stream=None):
+    """Quantize the FULL module weight ``w`` (bf16/f16/f32 CUDA, [rows, cols]) on the GPU and
+    return this rank's shard as a QuantWeight in the layout its kernel reads."""
+    import paper_2505_15909_b200 as rq
+    n, k = w.shape
+    ragged = k % group != 0
+    if world == 1:
+        return rq.quantize_pack(w.contiguous(), bits, group, ragged=ragged, check=False,
+                                stream=stream)
+    q = rq.quantize_pack(w.contiguous(), bits, group, ragged=ragged, native=False,
+                         row_major=True, scales_f16=True, check=False, stream=stream)
+    codes = q.codes_row_major.view(n, k * bits // 8)
+    c, s, ks, gs, rg = shard_quantized(codes, q.scales_f16, module, shape, rank, world, bits,
+                                       group)
+    return rq.from_row_major(c.reshape(-1), s.contiguous(), c.shape[0], ks, bits, gs, rg,
+                             stream=stream)
+
 
 class TPDecodeLayer:
     """One rank's shard of a decoder layer, all weights quantized on the GPU.
@@ -151,30 +207,32 @@ class TPDecodeLayer:
         self.batch, self.max_len, self.pos = batch, max_len, pos
         self.bits = bits
         dev = torch.device(device)
-        gen = torch.Generator(device=dev).manual_seed(seed * 1000003 + layer * 101 + rank)
         self.q = {}
-        for m in MODULES:
-            n, k = self.dims.module_shape(shape, m)
+        full = local_dims(shape, 1, group)
+        for mi, m in enumerate(MODULES):
+            n, k = full.module_shape(shape, m)
             if weights is not None:
-                w = shard_module(weights[m], m, shape, rank, world)
-            else:
+                w = weights[m]
+            else:  # synthetic full weight, the same on every rank (seeded by layer and module)
+                gen = torch.Generator(device=dev).manual_seed(seed * 1000003 + layer * 101 + mi)
                 w = ((torch.rand(n, k, device=dev, generator=gen) * 2 - 1) * (3.0 / k) ** 0.5
                      ).to(torch.bfloat16)
-            g = group_for(bits[m], k, group, w8_per_channel)
-            self.q[m] = rq.quantize_pack(w.contiguous(), bits[m], g, ragged=k % g != 0,
-                                         check=False)
+            self.q[m] = quantize_module(w, m, shape, rank, world, bits[m],
+                                        group_for(bits[m], k, group, w8_per_channel))
             del w
         h, d = shape.hidden, shape.head_dim
         bf = dict(dtype=torch.bfloat16, device=dev)
         norm_gen = torch.Generator(device=dev).manual_seed(seed * 7919 + layer)
         self.attn_norm = (1 + 0.1 * torch.rand(h, device=dev, generator=norm_gen)).to(torch.bfloat16)
         self.ffn_norm = (1 + 0.1 * torch.rand(h, device=dev, generator=norm_gen)).to(torch.bfloat16)
-        # synthetic KV cache: positions [0, pos) filled, the step appends at `pos`
-        kv_gen = torch.Generator(device=dev).manual_seed(seed * 31 + layer * 7 + rank)
-        self.k_cache = (torch.rand(batch, max_len, self.dims.hkv, d, device=dev, generator=kv_gen)
-                        - 0.5).to(torch.bfloat16)
-        self.v_cache = (torch.rand(batch, max_len, self.dims.hkv, d, device=dev, generator=kv_gen)
-                        - 0.5).to(torch.bfloat16)
+        # synthetic KV cache: positions [0, pos) filled, the step appends at `pos`; drawn for all
+        # KV heads (the same on every rank), each rank keeps its heads
+        kv_gen = torch.Generator(device=dev).manual_seed(seed * 31 + layer * 7)
+        h0, h1 = rank * self.dims.hkv, (rank + 1) * self.dims.hkv
+        self.k_cache = (torch.rand(batch, max_len, shape.kv_heads, d, device=dev, generator=kv_gen)
+                        - 0.5).to(torch.bfloat16)[:, :, h0:h1].contiguous()
+        self.v_cache = (torch.rand(batch, max_len, shape.kv_heads, d, device=dev, generator=kv_gen)
+                        - 0.5).to(torch.bfloat16)[:, :, h0:h1].contiguous()
         self.y = torch.empty(batch, h, **bf)
         self.qkv = torch.empty(batch, self.dims.qkv_rows, **bf)
         self.attn = torch.empty(batch, self.dims.attn_cols, **bf)
@@ -190,6 +248,9 @@ class TPDecodeLayer:
         # (SiLU*up + planes in one kernel is a CTA per token over the whole ffn row: slower than
         #  the two kernels, so the down projection computes its own planes)
         self.pa = None
+        # non-finite activations (InvalidInputError, gemm.cpp:13-19) are flagged asynchronously
+        # by the int8 kernels' planes pass; the stack checks the flag after a step
+        self.err = None
 
     @property
     def weight_bytes(self):
@@ -200,7 +261,8 @@ class TPDecodeLayer:
         q = self.q[module]
         if planes is not None and q.layout in (rq.NATIVE_I4, rq.NATIVE_I8):
             return rq.linear_planes(planes, q, out, workspace=ws, stream=stream, pdl=pdl)
-        return rq.linear(a, q, out=out, workspace=ws, stream=stream, pdl=pdl)
+        return rq.linear(a, q, out=out, workspace=ws, stream=stream, pdl=pdl, err=self.err,
+                         check=False)
 
     def attn_half(self, x, delta, ws, stream=None, pdl=False):
         """x += delta; y = rmsnorm(x); qkv; attention; o = partial attn_out_proj."""
@@ -211,7 +273,7 @@ class TPDecodeLayer:
         rq.decode_attention(self.qkv, self.k_cache, self.v_cache, self.attn, self.dims.hq,
                             self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream)
         rq.linear(self.attn, self.q["attn_out_proj"], out=self.o, workspace=ws, stream=stream,
-                  pdl=pdl)
+                  pdl=pdl, err=self.err, check=False)
         return self.o
 
     def mlp_half(self, x, o_sum, ws, stream=None, pdl=False):
@@ -242,6 +304,9 @@ class TPDecodeStack:
                        for li in range(n)]
         self.x = torch.zeros(batch, shape.hidden, dtype=torch.bfloat16, device=device)
         self.ws = rq.Workspace(device=device)
+        self.err = rq.error_flag(device)
+        for layer in self.layers:
+            layer.err = self.err
 
     @property
     def weight_bytes(self):
@@ -253,8 +318,15 @@ class TPDecodeStack:
             dist.all_reduce(t)
         return t
 
+    def check(self, stream=None):
+        """Raise InvalidInputError if a step since the last check saw a non-finite activation
+        (synchronizes ``stream``)."""
+        import paper_2505_15909_b200 as rq
+        rq.check_flag(self.err, stream)
+
     def step(self, x0, stream=None, pdl=True):
-        """One decode step for the batch; returns the residual stream after all layers."""
+        """One decode step for the batch; returns the residual stream after all layers.
+        Asynchronous (capturable in a CUDA graph); :meth:`check` reports non-finite inputs."""
         self.x.copy_(x0)
         delta = None
         for layer in self.layers:

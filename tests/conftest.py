@@ -45,3 +45,21 @@ def has_gpu():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def _cases(fname):
+    z = np.load(os.path.join(GOLDEN, fname))
+    return {str(n): {k.split("/", 1)[1]: z[k] for k in z.files if k.startswith(f"{n}/")}
+            for n in z["names"]}
+
+
+@pytest.fixture(scope="session")
+def golden_ties():
+    """f32 near-tie quantize fixtures (tests/golden/make_golden_r2.py)."""
+    return _cases("quant_f32ties.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_gemm_float():
+    """gemm_float fixtures (tests/golden/make_golden_r2.py)."""
+    return _cases("gemm_float.npz")

@@ -1,12 +1,16 @@
 // dropin_example.cpp -- a reference-style consumer of rtnq (the calls below are the
 // README sketch of proj/README.md:156-167 plus the device API), compiled unchanged
-// against the drop-in headers and linked to librtnq_b200.so.  Exit code 0 = parity ok.
+// against the drop-in headers and linked to librtnq_b200.so.  With a directory argument it
+// also dumps its inputs and every result there (raw little-endian arrays), and
+// tests/test_dropin_cpp.py checks them against the CPU oracle (oracle/rtnq_oracle.c),
+// independently of this library.  Exit code 0 = the self-checks below passed.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "rtnq/device.hpp"
@@ -31,7 +35,17 @@ static double rel_frob(const std::vector<float>& x, const std::vector<float>& re
     return den == 0 ? std::sqrt(num) : std::sqrt(num / den);
 }
 
-int main() {
+static void dump(const char* dir, const char* name, const void* p, size_t bytes) {
+    if (!dir) return;
+    std::string path = std::string(dir) + "/" + name;
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) return;
+    std::fwrite(p, 1, bytes, f);
+    std::fclose(f);
+}
+
+int main(int argc, char** argv) {
+    const char* dir = argc > 1 ? argv[1] : nullptr;
     const std::int64_t n = 384, k = 1024, m = 4;
     std::mt19937 gen(7);
     std::uniform_real_distribution<float> u(-1.f, 1.f);
@@ -47,6 +61,13 @@ int main() {
     rtnq::FloatTensor oracle = rtnq::gemm_oracle(a, q);
     const double e_host = rel_frob(fused.data, oracle.data);
     std::printf("host gemm_auto (path %d) vs gemm_oracle: %.3e\n", int(chosen), e_host);
+    dump(dir, "w.f32", w.data.data(), w.data.size() * 4);
+    dump(dir, "a.f32", a.data.data(), a.data.size() * 4);
+    dump(dir, "q_data.u8", q.data.data(), q.data.size());
+    dump(dir, "q_scales.f32", q.scales.data(), q.scales.size() * 4);
+    dump(dir, "qk_data.u8", qk.data.data(), qk.data.size());
+    dump(dir, "gemm_auto.f32", fused.data.data(), fused.data.size() * 4);
+    dump(dir, "gemm_oracle.f32", oracle.data.data(), oracle.data.size() * 4);
     if (chosen != rtnq::GemmPath::fused || e_host > 1e-5) return 1;
 
     // device API: tensor-core linear on the same weights
@@ -70,6 +91,7 @@ int main() {
     for (auto& s : q16.scales) s = float(_Float16(s));  // RNE, == f32_to_f16 (f16.cpp:8-41)
     rtnq::FloatTensor oracle16 = rtnq::gemm_oracle(a, q16);
     const double e_dev = rel_frob(out, oracle16.data);
+    dump(dir, "device_linear.f32", out.data(), out.size() * 4);
     std::printf("device linear (tcgen05) vs gemm_oracle(f16 scales): %.3e\n", e_dev);
 
     // from_host: a reference QuantTensor uploaded into the native layout gives the same result

@@ -206,3 +206,22 @@ def test_oracle_matches_reference_random(oracle):
         assert np.array_equal(oracle.gemm_fused(a, kern, rows, bits, g, scales), fr)
         orr, _ = ref.gemm("oracle", a, data, rows, bits, g, scales, ROW_MAJOR, ragged=ragged)
         assert np.array_equal(oracle.gemm_oracle(a, codes, g, scales), orr)
+
+
+def test_oracle_f32_tie_quantize_matches_reference(oracle, golden_ties):
+    """The C restatement on f32 weights a third of which sit on, or one ulp beside, a rounding
+    tie (not truncated to bf16): bytes and scales equal the reference's (quant.cpp:24-29,49-68)."""
+    for name, z in golden_ties.items():
+        rows, cols, bits, g, ragged = (int(v) for v in z["meta"])
+        codes, scales = oracle.quantize(z["w"], bits, g, bool(ragged))
+        assert np.array_equal(scales, z["scales"]), name
+        assert np.array_equal(oracle.pack(codes, bits), z["data"]), name
+        assert np.array_equal(oracle.f16_round(scales), z["scales_f16"]), name
+
+
+def test_oracle_gemm_float_matches_reference(oracle, golden_gemm_float):
+    """gemm_float (gemm.cpp:111-119), bit-exact."""
+    for name, z in golden_gemm_float.items():
+        m, k, n, block = (int(v) for v in z["meta"])
+        out = oracle.gemm_float(z["a"], z["w"], block)
+        assert np.array_equal(out.view(np.uint32), z["out"].view(np.uint32)), name

@@ -74,6 +74,53 @@ def test_quantize_then_shard_equals_shard_then_quantize(oracle, bits):
                 assert np.array_equal(ss, tp.shard_module(scales, m, TINY, r, 2)), m
 
 
+TINY8 = tp.LlamaShape("tiny8", hidden=512, heads=8, kv_heads=8, head_dim=128, ffn=2048, layers=1)
+
+
+@pytest.mark.parametrize("bits,per_channel", [(8, True), (4, False), (8, False)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_quantize_before_shard_partials_sum_to_full(oracle, bits, per_channel, world):
+    """quantize the full weight, then shard codes and scales (tp.shard_quantized).
+    Row-split shards keep the full row's scale (W8 per-channel: one group per full row), so the
+    row-parallel partials summed over ranks equal the unsharded oracle GEMM; column-split
+    shards are the full output's columns.  Shard-then-quantize is shown to differ for
+    per-channel W8 (its per-shard absmax changes the scales)."""
+    w = full_weights(TINY8, seed=world + bits)
+    rng = np.random.default_rng(world)
+    for m in tp.MODULES:
+        n, k = w[m].shape
+        g = (1 << (k - 1).bit_length()) if per_channel else 128
+        codes, scales = oracle.quantize(w[m], bits, g, k % g != 0)
+        data = oracle.pack(codes, bits).reshape(n, k * bits // 8)
+        x = rng.uniform(-1, 1, (3, k)).astype(np.float32)
+        full = oracle.gemm_oracle_f64(x, codes, g, scales)
+        acc = np.zeros_like(full, dtype=np.float64)
+        differs = False
+        for r in range(world):
+            c, s, ks, gs, rg = tp.shard_quantized(data, scales, m, TINY8, r, world, bits, g)
+            logical = oracle.unpack(c.ravel(), c.shape[0] * ks, bits).reshape(c.shape[0], ks)
+            assert s.shape == (c.shape[0], oracle.groups_per_row(gs, rg, ks)), m
+            if m in ("attn_out_proj", "ffn_down"):
+                assert np.array_equal(logical, codes[:, r * ks:(r + 1) * ks]), m
+                xs = tp.shard_cols(x, r, world)
+                acc += oracle.gemm_oracle_f64(xs, logical, gs, s)
+                sc, ss = oracle.quantize(tp.shard_cols(w[m], r, world), bits, gs, rg)
+                differs |= not np.array_equal(ss, s)
+            else:
+                assert np.array_equal(logical, tp.shard_module(codes, m, TINY8, r, world)), m
+                got = oracle.gemm_oracle_f64(x, logical, gs, s)
+                assert np.array_equal(got, tp.shard_module(full.T, m, TINY8, r, world).T), m
+        if m in ("attn_out_proj", "ffn_down"):
+            assert np.abs(acc - full).max() <= 1e-12 * np.abs(full).max(), (m, world)
+            if per_channel:
+                assert differs, "per-shard absmax should change some per-channel scales"
+
+
+def test_row_split_width_must_be_whole_groups():
+    with pytest.raises(ValueError):
+        tp.local_dims(tp.LlamaShape("bad", 256, 2, 2, 64, 256, 1), 2)  # 64 < group 128
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
