@@ -13,6 +13,12 @@ value = algorithmic weight bytes of the whole job (codes + f16 scales) / step ti
 KV cache, SiLU, allreduces) is timed as well and reported as decode_layer_us /
 decode_us_per_token.
 
+The same JSON line carries sub-records measured in the same run: "w8" (configs[2], W8A16
+per-channel step, batch sweep 1-64 and its ffn_up roofline), "quantize" (the model-load
+quantize-and-pack kernel on the 8B gate_up, W4 and W8), "llama70b" (configs[3]: the 80-layer
+70B stack with plan "explicit:0 modules:4" at TP = N) and "llama405b_tp8_rank_shard"
+(configs[4]: one TP=8 rank's 405B shards, batch 1-32, on one GPU).
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--bits 4|8]
                   [--model 8b|70b|405b] [--plan "explicit:0 modules:4"]
   python bench.py --impl reference     # the reference CPU gemm_fused, same metric
@@ -125,230 +131,320 @@ def _trace(msg):
         print(f"[bench] {msg}", file=sys.stderr, flush=True)
 
 
-def run_gpu(args):
-    import torch
-    import torch.distributed as dist
+def base_config(args, world, shape, nl, bits, plan, w8pc, B, step_bytes):
+    """The workload description, identical for both arms (--impl ours / reference)."""
+    return {"workload": f"{shape.name} decode step, {nl} layers x 4 quantized linears, "
+                        f"W{bits}A16 {'per-channel' if w8pc else 'g128'}, decode batch {B}, "
+                        f"tensor parallel TP={world}",
+            "model": shape.name, "batch": B, "layers": nl, "bits": bits, "plan": plan,
+            "group": "per-channel" if w8pc else 128, "weight_bytes_per_step": step_bytes,
+            "l2": "inputs larger than L2 (weights per step >> 126 MB), no flush",
+            "parallelism": f"tp{world}" if world > 1 else "single GPU"}
 
-    import paper_2505_15909_b200 as rq
-    from paper_2505_15909_b200 import tp
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    bits, B = args.bits, args.batch
-    shape = tp.SHAPES[args.model]
-    nl = args.layers or shape.layers
-    if args.plan:
-        table, plan = rq.plan.resolve(args.plan, nl)
-    else:  # uniform precision (configs[1] / configs[2])
-        import numpy as np
-        table, plan = np.full((nl, 4), bits, np.uint8), f"uniform W{bits}"
-    w8pc = bits == 8 and not args.plan  # configs[2]: W8 per-channel
+class Ctx:
+    """Per-process GPU bench state: stream, workspace, timing helpers."""
 
-    # ---- this rank's tensor-parallel shard of every layer, quantized on the GPU ----
-    stack = tp.TPDecodeStack(shape, table, world, rank, B, max_len=args.ctx + 1, pos=args.ctx,
-                             layers=nl, seed=1234, device=dev, w8_per_channel=w8pc)
-    torch.cuda.synchronize()
-    dims = stack.layers[0].dims
-    step_bytes_rank = stack.weight_bytes
-    ws = rq.Workspace(device=dev)
-    stream = torch.cuda.Stream(device=dev)
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.args = torch, dist, args
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.dev = torch.device("cuda", self.local)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.capture_errors = []
 
-    def bufs(b):
-        bf = dict(dtype=torch.bfloat16, device=dev)
-        return {"x": torch.empty(b, shape.hidden, **bf).uniform_(-1, 1),
-                "attn": torch.empty(b, dims.attn_cols, **bf).uniform_(-1, 1),
-                "act": torch.empty(b, dims.ffn, **bf).uniform_(-1, 1),
-                "qkv": torch.empty(b, dims.qkv_rows, **bf), "o": torch.empty(b, shape.hidden, **bf),
-                "gu": torch.empty(b, 2 * dims.ffn, **bf), "d": torch.empty(b, shape.hidden, **bf)}
-
-    # The weight-streaming step (the metric): every quantized linear of every layer, with
-    # the row-parallel outputs (attn_out_proj, ffn_down) sum-allreduced across ranks.
-    def gemm_step(bb):
-        for layer in stack.layers:
-            q = layer.q
-            rq.linear(bb["x"], q["qkv_proj"], out=bb["qkv"], workspace=ws, stream=stream, pdl=args.pdl,
-                      check=False)
-            rq.linear(bb["attn"], q["attn_out_proj"], out=bb["o"], workspace=ws, stream=stream,
-                      pdl=args.pdl, check=False)
-            if world > 1:
-                dist.all_reduce(bb["o"])
-            rq.linear(bb["x"], q["ffn_up"], out=bb["gu"], workspace=ws, stream=stream, pdl=args.pdl,
-                      check=False)
-            rq.linear(bb["act"], q["ffn_down"], out=bb["d"], workspace=ws, stream=stream,
-                      pdl=args.pdl, check=False)
-            if world > 1:
-                dist.all_reduce(bb["d"])
-
-    def capture(fn):
-        """CUDA graph of one step (NCCL collectives included); None if capture fails."""
-        with torch.cuda.stream(stream):
+    def capture(self, fn):
+        """CUDA graph of one step (NCCL collectives included); None if capture fails -- the
+        failure is reported in the JSON line ("capture_errors") and on stderr."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
             fn()
-        stream.synchronize()
+        self.stream.synchronize()
         try:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
+            with torch.cuda.graph(g, stream=self.stream):
                 fn()
             return g
-        except Exception:  # noqa: BLE001 -- fall back to eager launches, reported in config
+        except Exception as e:  # noqa: BLE001 -- eager launches instead, reported
             torch.cuda.synchronize()
+            msg = f"{type(e).__name__}: {str(e).splitlines()[0][:200] if str(e) else ''}"
+            self.capture_errors.append(msg)
+            print(f"[bench] WARNING: CUDA-graph capture failed, timing eager launches: {msg}",
+                  file=sys.stderr, flush=True)
             return None
 
-    def runner(g, fn):
+    def runner(self, g, fn):
         def run():
-            with torch.cuda.stream(stream):
+            with self.torch.cuda.stream(self.stream):
                 if g is not None:
                     g.replay()
                 else:
                     fn()
         return run
 
-    def timed(fn, steps, warmup):
+    def timed(self, fn, steps, warmup):
+        torch, dist = self.torch, self.dist
         for _ in range(warmup):
             fn()
-        stream.synchronize()
-        if world > 1:
+        self.stream.synchronize()
+        if self.world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        e0.record(self.stream)
         for _ in range(steps):
             fn()
-        e1.record(stream)
+        e1.record(self.stream)
         e1.synchronize()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        if world > 1:  # max over ranks
-            t = torch.tensor([ms], device=dev)
+        if self.world > 1:  # max over ranks
+            t = torch.tensor([ms], device=self.dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = t.item()
         return ms / steps
 
-    # total weight bytes streamed per step by the whole job (all ranks' shards)
-    step_bytes = step_bytes_rank
-    if world > 1:
-        t = torch.tensor([float(step_bytes_rank)], device=dev, dtype=torch.float64)
-        dist.all_reduce(t)
-        step_bytes = int(t.item())
+    def allsum(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t)
+        return t.item()
 
+
+def measure(cx, shape, table, B, nl, w8pc, sweep, steps, warmup, *, sim_world=None, e2e=False,
+            decode=True, roofline=True, ctx_len=256):
+    """Build this rank's shard stack and time its weight-streaming step (every quantized linear
+    of every layer, row-parallel outputs allreduced), the batch sweep, optionally the e2e step
+    (host buffers), the full decode step and the dominant kernel (ffn_up)."""
+    import paper_2505_15909_b200 as rq
+    from paper_2505_15909_b200 import tp
+    torch, dist, args = cx.torch, cx.dist, cx.args
+    world = sim_world or cx.world
+    rank = 0 if sim_world else cx.rank
+    stack = tp.TPDecodeStack(shape, table, world, rank, B, max_len=ctx_len + 1, pos=ctx_len,
+                             layers=nl, seed=1234, device=cx.dev, w8_per_channel=w8pc,
+                             collectives=sim_world is None)
+    torch.cuda.synchronize()
+    dims = stack.layers[0].dims
+    ws = rq.Workspace(device=cx.dev)
+    stream = cx.stream
+    coll = sim_world is None and cx.world > 1
+
+    def bufs(b):
+        bf = dict(dtype=torch.bfloat16, device=cx.dev)
+        return {"x": torch.empty(b, shape.hidden, **bf).uniform_(-1, 1),
+                "attn": torch.empty(b, dims.attn_cols, **bf).uniform_(-1, 1),
+                "act": torch.empty(b, dims.ffn, **bf).uniform_(-1, 1),
+                "qkv": torch.empty(b, dims.qkv_rows, **bf), "o": torch.empty(b, shape.hidden, **bf),
+                "gu": torch.empty(b, 2 * dims.ffn, **bf), "d": torch.empty(b, shape.hidden, **bf)}
+
+    def gemm_step(bb):
+        for layer in stack.layers:
+            q = layer.q
+            kw = dict(workspace=ws, stream=stream, pdl=args.pdl, check=False)
+            rq.linear(bb["x"], q["qkv_proj"], out=bb["qkv"], **kw)
+            rq.linear(bb["attn"], q["attn_out_proj"], out=bb["o"], **kw)
+            if coll:
+                dist.all_reduce(bb["o"])
+            rq.linear(bb["x"], q["ffn_up"], out=bb["gu"], **kw)
+            rq.linear(bb["act"], q["ffn_down"], out=bb["d"], **kw)
+            if coll:
+                dist.all_reduce(bb["d"])
+
+    step_bytes_rank = stack.weight_bytes
+    step_bytes = int(cx.allsum(step_bytes_rank)) if not sim_world else step_bytes_rank
     main = bufs(B)
-    _trace("stack built")
-    graph = capture(lambda: gemm_step(main))
-    _trace(f"captured (graph={graph is not None})")
-    with ClockSampler(local) as clk:
-        ms = timed(runner(graph, lambda: gemm_step(main)), args.steps, args.warmup)
-    value = step_bytes / (ms * 1e-3) / 1e9
-    peak, peak_src = peaks()
-    _trace(f"timed step {ms:.3f} ms")
-
-    sweep = {}
-    for b in args.sweep:
+    graph = cx.capture(lambda: gemm_step(main))
+    with ClockSampler(cx.local) as clk:
+        ms = cx.timed(cx.runner(graph, lambda: gemm_step(main)), steps, warmup)
+    out = {"ms_per_step": round(ms, 4), "gbs": round(step_bytes / (ms * 1e-3) / 1e9, 1),
+           "step_bytes": step_bytes, "step_bytes_rank": step_bytes_rank,
+           "gbs_per_gpu": round(step_bytes_rank / (ms * 1e-3) / 1e9, 1), "cuda_graph": graph is not None,
+           "clocks": clk.summary(), "launches_per_step": nl * 4 * (1 + -(-B // 64))}
+    sw = {}
+    for b in sweep:
         if b == B:
-            sweep[str(b)] = round(value, 1)
+            sw[str(b)] = out["gbs"]
             continue
         bb = bufs(b)
-        gb = capture(lambda: gemm_step(bb))
-        msb = timed(runner(gb, lambda: gemm_step(bb)), max(3, args.steps // 2), args.warmup)
-        sweep[str(b)] = round(step_bytes / (msb * 1e-3) / 1e9, 1)
+        gb = cx.capture(lambda: gemm_step(bb))
+        msb = cx.timed(cx.runner(gb, lambda: gemm_step(bb)), max(3, steps // 2), warmup)
+        sw[str(b)] = round(step_bytes / (msb * 1e-3) / 1e9, 1)
         del gb
-        _trace(f"sweep {b} done")
+    out["sweep_gbs_by_batch"] = sw
+    if e2e:  # pinned host activations in, host outputs back, through the public API
+        hin = {k: torch.empty_like(main[k], device="cpu").uniform_(-1, 1).pin_memory()
+               for k in ("x", "attn", "act")}
+        hout = {k: torch.empty_like(main[k], device="cpu").pin_memory() for k in ("qkv", "o", "gu", "d")}
 
-    # ---- e2e: pinned host activations in, host outputs back, through the public API ----
-    hin = {k: torch.empty_like(main[k], device="cpu").uniform_(-1, 1).pin_memory()
-           for k in ("x", "attn", "act")}
-    hout = {k: torch.empty_like(main[k], device="cpu").pin_memory() for k in ("qkv", "o", "gu", "d")}
-    h2d = sum(t.numel() for t in hin.values()) * 2
-    d2h = sum(t.numel() for t in hout.values()) * 2
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                for k, t in hin.items():
+                    main[k].copy_(t, non_blocking=True)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    gemm_step(main)
+                for k, t in hout.items():
+                    t.copy_(main[k], non_blocking=True)
 
-    def e2e_step():
-        with torch.cuda.stream(stream):
-            for k, t in hin.items():
-                main[k].copy_(t, non_blocking=True)
-            if graph is not None:
-                graph.replay()
-            else:
-                gemm_step(main)
-            for k, t in hout.items():
-                t.copy_(main[k], non_blocking=True)
+        ms_e2e = cx.timed(e2e_step, steps, warmup)
+        out["e2e"] = {"value": round(step_bytes / (ms_e2e * 1e-3) / 1e9, 1), "unit": "GB/s",
+                      "h2d_bytes_per_step": sum(t.numel() for t in hin.values()) * 2,
+                      "d2h_bytes_per_step": sum(t.numel() for t in hout.values()) * 2,
+                      "ms_per_step": round(ms_e2e, 4)}
+    if decode:  # the full decode step (norms, attention over the KV cache, SiLU, allreduces)
+        x0 = torch.empty(B, shape.hidden, dtype=torch.bfloat16, device=cx.dev).uniform_(-1, 1)
+        dgraph = cx.capture(lambda: stack.step(x0, stream=stream, pdl=args.pdl))
+        ms_dec = cx.timed(cx.runner(dgraph, lambda: stack.step(x0, stream=stream, pdl=args.pdl)),
+                          max(3, steps // 2), warmup)
+        stack.check(stream)  # no non-finite activation flagged during the timed steps
+        out.update({"decode_step_ms": round(ms_dec, 4), "decode_layer_us": round(ms_dec * 1e3 / nl, 2),
+                    "decode_us_per_token": round(ms_dec * 1e3 / B, 2), "decode_ctx_len": ctx_len,
+                    "decode_cuda_graph": dgraph is not None})
+    if roofline:  # the dominant kernel: ffn_up, 20 launches over 4 weight copies (> L2), graph
+        q_up = [l.q["ffn_up"] for l in stack.layers[:4]]
 
-    ms_e2e = timed(e2e_step, args.steps, args.warmup)
-    _trace("e2e done")
-    e2e = step_bytes / (ms_e2e * 1e-3) / 1e9
+        def up_step():
+            for i in range(20):
+                rq.linear(main["x"], q_up[i % len(q_up)], out=main["gu"], workspace=ws, stream=stream,
+                          pdl=args.pdl, check=False)
 
-    # ---- the full decode step (norms, attention over the KV cache, SiLU, allreduces) ----
-    x0 = torch.empty(B, shape.hidden, dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
-    dgraph = capture(lambda: stack.step(x0, stream=stream, pdl=args.pdl))
-    ms_dec = timed(runner(dgraph, lambda: stack.step(x0, stream=stream, pdl=args.pdl)),
-                   max(3, args.steps // 2), args.warmup)
+        g_up = cx.capture(up_step)
+        ms_up = cx.timed(cx.runner(g_up, up_step), max(3, steps // 5), warmup) / 20
+        up_bytes = q_up[0].weight_bytes
+        peak, peak_src = peaks()
+        achieved = up_bytes / (ms_up * 1e-3) / 1e9
+        kern = {rq.NATIVE_I4: "rtnq_b200::i4::wgemm_i4_kernel", rq.NATIVE_I8: "rtnq_b200::i8::wgemm_i8_kernel",
+                rq.NATIVE: "rtnq_b200::tc::wgemm_tc_kernel"}[q_up[0].layout]
+        out["roofline"] = {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "peak_source": peak_src, "kernel": kern,
+            "measured_on": f"ffn_up {2 * dims.ffn}x{shape.hidden}, 20 launches in a CUDA graph, CUDA "
+                           f"events on the launch stream; us per launch {ms_up * 1e3:.2f} (planes "
+                           f"kernel included)",
+            "algorithmic_bytes_per_launch": up_bytes,
+            "step_average_gbs": round(step_bytes_rank / (ms * 1e-3) / 1e9, 1)}
+    del stack
+    torch.cuda.empty_cache()
+    return out
 
-    _trace("decode step done")
-    linears = nl * 4
-    # ---- roofline of the dominant kernel: the largest linear (ffn_up), 20 back-to-back
-    # launches over 4 weight copies (> L2) in a CUDA graph, CUDA events on its stream ----
-    q_up = [l.q["ffn_up"] for l in stack.layers[:4]]
-    bb_up = main
 
-    def up_step():
-        for i in range(20):
-            rq.linear(bb_up["x"], q_up[i % len(q_up)], out=bb_up["gu"], workspace=ws, stream=stream,
-                      pdl=args.pdl, check=False)
+def quantize_record(cx, bits, n=28672, k=4096, reps=10):
+    """The model-load pass (rtnq_dev_quantize_pack_ex) on the 8B gate_up weight: bf16 in, the
+    kernel's operand layout + native f16 scales out, CUDA events.  Algorithmic bytes = 2 B read
+    + bits/8 B written per weight + the scales."""
+    import paper_2505_15909_b200 as rq
+    torch = cx.torch
+    g = 128 if bits == 4 else 1 << (k - 1).bit_length()
+    ws = [((torch.rand(n, k, device=cx.dev) * 2 - 1) * 0.02).to(torch.bfloat16) for _ in range(2)]
+    with torch.cuda.stream(cx.stream):
+        q = rq.quantize_pack(ws[0], bits, g, k % g != 0, stream=cx.stream)
+    nbytes = n * k * 2 + n * k * bits // 8 + n * (-(-k // g)) * 2
 
-    g_up = capture(up_step)
-    ms_up = timed(runner(g_up, up_step), max(3, args.steps // 5), args.warmup) / 20
-    up_bytes = q_up[0].weight_bytes
-    achieved = up_bytes / (ms_up * 1e-3) / 1e9
-    step_achieved = step_bytes_rank / (ms * 1e-3) / 1e9  # one GPU's share of the whole step
-    kern = {rq.NATIVE_I4: "rtnq_b200::i4::wgemm_i4_kernel", rq.NATIVE_I8: "rtnq_b200::i8::wgemm_i8_kernel",
-            rq.NATIVE: "rtnq_b200::tc::wgemm_tc_kernel"}[q_up[0].layout]
-    per_linear = 1 + (-(-B // 64))  # the activation-planes kernel + one GEMM per 64 tokens
-    if q_up[0].layout == rq.NATIVE:
-        per_linear = -(-B // 64)
+    def run():
+        for i in range(reps):
+            rq.quantize_pack(ws[i % 2], bits, g, k % g != 0, check=False, stream=cx.stream)
+
+    ms = cx.timed(lambda: cx.runner(None, run)(), 3, 1) / reps
+    peak, _ = peaks()
+    del ws, q
+    return {"shape": f"{n}x{k}", "layout": "NATIVE_I4" if bits == 4 else "NATIVE_I8",
+            "us": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+            "frac": round(nbytes / (ms * 1e-3) / 1e9 / peak, 4), "algorithmic_bytes": nbytes,
+            "note": "one quantize_pack call (allocations + the fused kernel), 2 weight copies alternating"}
+
+
+def run_gpu(args):
+    import numpy as np
+
+    import paper_2505_15909_b200 as rq
+    from paper_2505_15909_b200 import tp
+    cx = Ctx(args)
+    world, rank = cx.world, cx.rank
+    bits, B = args.bits, args.batch
+    shape = tp.SHAPES[args.model]
+    nl = args.layers or shape.layers
+    if args.plan:
+        table, plan = rq.plan.resolve(args.plan, nl)
+    else:  # uniform precision (configs[1] / configs[2])
+        table, plan = np.full((nl, 4), bits, np.uint8), f"uniform W{bits}"
+    w8pc = bits == 8 and not args.plan  # configs[2]: W8 per-channel
+    steps, warmup = args.steps, args.warmup
+    sub_steps = max(5, steps // 5)
+
+    main = measure(cx, shape, table, B, nl, w8pc, args.sweep, steps, warmup, e2e=True)
+    _trace(f"headline step {main['ms_per_step']} ms")
+    peak, peak_src = peaks()
+    value = main["gbs"]
     line = {
-        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": main["ms_per_step"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": f"u{bits} weights x bf16 activations, f32 accumulate", "data": "synthetic",
-        "config": {"workload": f"{shape.name} decode step, {nl} layers x 4 quantized linears, "
-                               f"W{bits}A16 {'per-channel' if w8pc else 'g128'}, decode batch {B}, "
-                               f"tensor parallel TP={world}",
-                   "model": shape.name, "batch": B, "layers": nl, "bits": bits,
-                   "plan": plan, "group": "per-channel" if w8pc else 128,
-                   "weight_bytes_per_step": step_bytes,
-                   "l2": "inputs larger than L2 (weights per step >> 126 MB), no flush",
-                   "parallelism": f"tp{world}" if world > 1 else "single GPU",
-                   "cuda_graph": graph is not None,
-                   "pct_of_hbm_peak_per_gpu": round(100 * step_achieved / peak, 1),
-                   "sweep_gbs_by_batch": sweep,
-                   "decode_step_ms": round(ms_dec, 4),
-                   "decode_layer_us": round(ms_dec * 1e3 / nl, 2),
-                   "decode_us_per_token": round(ms_dec * 1e3 / B, 2),
-                   "decode_ctx_len": args.ctx,
-                   "decode_cuda_graph": dgraph is not None},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(bits, B) if world == 1 and args.model == "8b" else None,
-                     "peak_source": peak_src,
-                     "kernel": kern,
-                     "measured_on": f"ffn_up {2 * dims.ffn}x{shape.hidden}, 20 launches in a CUDA "
-                                    f"graph, CUDA events; us per launch {ms_up * 1e3:.2f} (planes kernel "
-                                    f"included)",
-                     "algorithmic_bytes_per_launch": up_bytes,
-                     "step_average_gbs": round(step_achieved, 1)},
-        "e2e": {"value": round(e2e, 1), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
-        "gpu_launches": linears * per_linear * args.steps,
-        "clocks": clk.summary(),
+        "config": base_config(args, world, shape, nl, bits, plan, w8pc, B, main["step_bytes"]),
+        "roofline": dict(main["roofline"], traffic=ncu_traffic(bits, B) if world == 1 and args.model == "8b" else None),
+        "e2e": main["e2e"],
+        "gpu_launches": main["launches_per_step"] * steps,
+        "clocks": main["clocks"],
+        "details": {k: main[k] for k in ("cuda_graph", "sweep_gbs_by_batch", "decode_step_ms", "decode_layer_us",
+                                         "decode_us_per_token", "decode_ctx_len", "decode_cuda_graph",
+                                         "gbs_per_gpu")},
     }
+    line["details"]["pct_of_hbm_peak_per_gpu"] = round(100 * main["gbs_per_gpu"] / peak, 1)
+    if not args.headline_only and args.model == "8b" and not args.plan:
+        # the other half of the metric: W8A16 per-channel (configs[2]) or W4 (configs[1])
+        other = 8 if bits == 4 else 4
+        t2 = np.full((nl, 4), other, np.uint8)
+        m2 = measure(cx, shape, t2, B, nl, other == 8, [1, 4, 16, 32, 64] if other == 8 else [1, 4, 16],
+                     sub_steps, warmup, decode=False)
+        line[f"w{other}"] = {"value": m2["gbs"], "unit": "GB/s", "ms_per_step": m2["ms_per_step"],
+                             "workload": base_config(args, world, shape, nl, other, f"uniform W{other}",
+                                                     other == 8, B, m2["step_bytes"])["workload"],
+                             "sweep_gbs_by_batch": m2["sweep_gbs_by_batch"], "roofline": m2["roofline"],
+                             "cuda_graph": m2["cuda_graph"]}
+        _trace("second bit width done")
+        if world == 1:
+            line["quantize"] = {f"w{b}": quantize_record(cx, b) for b in (4, 8)}
+        # configs[3]: Llama-3.1-70B, 80 layers, W4 + layer-0 down_proj W8, at TP = world
+        t70, p70 = rq.plan.resolve("explicit:0 modules:4", tp.LLAMA_70B.layers)
+        m70 = measure(cx, tp.LLAMA_70B, t70, 1, tp.LLAMA_70B.layers, False, [1, 4, 16], sub_steps, warmup,
+                      roofline=False)
+        line["llama70b"] = {
+            "workload": f"Llama-3.1-70B decode step, 80 layers, plan '{p70}' (W4 g128 + layer-0 ffn_down W8 g128), "
+                        f"TP={world}, batch 1",
+            "ms_per_token_batch1": m70["ms_per_step"], "gbs": m70["gbs"], "sweep_gbs_by_batch": m70["sweep_gbs_by_batch"],
+            "weight_bytes_per_step": m70["step_bytes"], "floor_ms_at_peak": round(m70["step_bytes_rank"] / peak / 1e6, 4),
+            "decode_step_ms_batch1": m70["decode_step_ms"], "decode_layer_us": m70["decode_layer_us"],
+            "cuda_graph": m70["cuda_graph"]}
+        _trace("70b done")
+        if world == 1:
+            # configs[4]: one rank's shard stack of Llama-3.1-405B at TP=8, batch 1-32 (the per-GPU
+            # work of that configuration; its two allreduces per layer are not on this GPU)
+            t405 = np.full((tp.LLAMA_405B.layers, 4), 4, np.uint8)
+            m405 = measure(cx, tp.LLAMA_405B, t405, 1, tp.LLAMA_405B.layers, False, [1, 4, 16, 32], sub_steps,
+                           warmup, sim_world=8, roofline=False, decode=True)
+            line["llama405b_tp8_rank_shard"] = {
+                "workload": "Llama-3.1-405B, 126 layers, W4 g128, the TP=8 rank-0 shards (qkv 2304x16384, o "
+                            "16384x2048, gate_up 13312x16384, down 16384x6656) on one GPU, allreduces excluded",
+                "ms_per_step_batch1": m405["ms_per_step"], "gbs": m405["gbs"],
+                "sweep_gbs_by_batch": m405["sweep_gbs_by_batch"], "weight_bytes_per_step": m405["step_bytes"],
+                "decode_step_ms_batch1": m405["decode_step_ms"], "cuda_graph": m405["cuda_graph"]}
+            _trace("405b done")
+    if cx.capture_errors:
+        line["capture_errors"] = cx.capture_errors
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "8b":
-        g_of = group_for(bits)
-        line["cpu_baseline"] = cpu_baseline(args, bits=bits, B=B, g_of=g_of)
+        line["cpu_baseline"] = cpu_baseline(args, bits=bits, B=B, g_of=group_for(bits))
     if world > 1:
-        dist.destroy_process_group()
+        cx.dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -395,7 +491,10 @@ def cpu_baseline(args, bits, B, g_of, budget_s=None):
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU implementation, same metric/config."""
+    """--impl reference: the reference's own CPU gemm_fused (oracle/_ref, built from the
+    unmodified sources), all host threads, same metric / unit / config as our arm.  Each step
+    is a bounded sample of the workload: one layer's 4 linears (bytes per second is
+    size-independent, so the sample is comparable)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -403,6 +502,8 @@ def run_reference(args):
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import KERNEL, Ref
+
+    from paper_2505_15909_b200 import tp
     bits, B = args.bits, args.batch
     g_of = group_for(bits)
     if not Ref.available():
@@ -421,7 +522,11 @@ def run_reference(args):
         kern = ref.reshuffle(data, n, k, bits, g_of(k), sc, 0, KERNEL, ragged=rg)
         prep.append((n, k, kern, sc))
     acts = {k: rng.uniform(-1, 1, (B, k)).astype(np.float32) for k in (4096, 14336)}
-    step_bytes = sum(weight_bytes(n, k, bits, g_of(k)) for _, n, k in LLAMA8B)
+    layer_bytes = sum(weight_bytes(n, k, bits, g_of(k)) for _, n, k in LLAMA8B)
+    shape = tp.SHAPES[args.model]
+    nl = args.layers or shape.layers
+    w8pc = bits == 8 and not args.plan
+    plan = args.plan or f"uniform W{bits}"
 
     def step():
         for n, k, kern, sc in prep:
@@ -433,22 +538,18 @@ def run_reference(args):
     for _ in range(args.steps):
         step()
     dt = (time.perf_counter() - t0) / args.steps
-    v = step_bytes / dt / 1e9
+    v = layer_bytes / dt / 1e9
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": round(dt * 1e3 * nl, 2), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 activations, u4/u8 codes (reference CPU)",
         "data": "synthetic",
-        # the same workload as our arm's line; each reference step is a bounded sample of it
-        # (one layer's 4 linears: the metric is bytes per second, so the sample is comparable)
-        "config": {"workload": f"Llama-3.1-8B decode step, 32 layers x 4 quantized linears, "
-                               f"W{bits}A16 {'per-channel' if bits == 8 and not args.plan else 'g128'}, "
-                               f"decode batch {B}, tensor parallel TP={world}",
-                   "model": "Llama-3.1-8B", "batch": B, "bits": bits,
-                   "reference_sample": "each step = one layer's 4 linears through gemm_fused"},
+        "config": base_config(args, world, shape, nl, bits, plan, w8pc, B, layer_bytes * nl),
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} steps x one layer's 4 linears via gemm_fused"},
+                         "sample": f"each of the {args.steps} steps = one Llama-3.1-8B layer's 4 linears "
+                                   f"(batch {B}) through the reference gemm_fused, set_threads({cores}); "
+                                   f"ms_per_step scaled to {nl} layers"},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
 
@@ -470,11 +571,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", dest="pdl", action="store_false",
                     help="launch the GEMMs without programmatic dependent launch")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="skip the W8/W4 sub-record, the quantize pass and the 70B / 405B configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
-        args.steps = min(args.steps, 5)
-        args.warmup = min(args.warmup, 1)
         return run_reference(args)
     run_gpu(args)
 

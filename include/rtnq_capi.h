@@ -116,6 +116,24 @@ rtnq_status rtnq_dev_quantize_pack(const void* w, int w_dtype, int64_t rows, int
                                    uint16_t* scales_f16_native, int32_t* err_flag,
                                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* rtnq_dev_quantize_pack with the layout of `codes_native` chosen by native_kind:
+ * RTNQ_NATIVE_SM100 (== rtnq_dev_quantize_pack), RTNQ_NATIVE_I4 (W4 group 128) or
+ * RTNQ_NATIVE_I8 (W8 per-channel).  For the two int8-MMA layouts, when no
+ * kernel_interleaved output is requested and cols % 128 == 0 (I4) / cols % 16 == 0 (I8),
+ * ONE kernel reads the weights once and writes the native tiles (padding included), the
+ * optional row-major bytes and the scales; otherwise the row-major bytes are quantized first
+ * (caller's codes_row_major or the workspace) and relaid out.  The scales_f16_native of the
+ * general route need scales_f32 or scales_f16 as well. */
+size_t rtnq_dev_quantize_workspace_bytes_ex(int64_t rows, int64_t cols, int bits, int64_t g,
+                                            int ragged, int native_kind);
+rtnq_status rtnq_dev_quantize_pack_ex(const void* w, int w_dtype, int64_t rows, int64_t cols,
+                                      int bits, int64_t g, int ragged, int native_kind,
+                                      uint8_t* codes_row_major, uint8_t* codes_kernel16x4,
+                                      uint8_t* codes_native, float* scales_f32,
+                                      uint16_t* scales_f16, uint16_t* scales_f16_native,
+                                      int32_t* err_flag, void* workspace, size_t workspace_bytes,
+                                      void* stream);
+
 /* Layout conversion of packed codes (reshuffle, packing.cpp:75-92, generalized
  * to any pair of kinds; used to load row-major RTNCKPT1 codes into the native
  * layout).  Pure permutation plus zero padding. */

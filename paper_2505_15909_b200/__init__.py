@@ -75,6 +75,10 @@ def lib():
     L.rtnq_dev_quantize_workspace_bytes.argtypes = [_i64, _i64, _i32, _i64, _i32]
     L.rtnq_dev_quantize_pack.argtypes = [_p, _i32, _i64, _i64, _i32, _i64, _i32, _p, _p, _p, _p,
                                          _p, _p, _p, _p, _sz, _p]
+    L.rtnq_dev_quantize_workspace_bytes_ex.restype = _sz
+    L.rtnq_dev_quantize_workspace_bytes_ex.argtypes = [_i64, _i64, _i32, _i64, _i32, _i32]
+    L.rtnq_dev_quantize_pack_ex.argtypes = [_p, _i32, _i64, _i64, _i32, _i64, _i32, _i32, _p, _p, _p,
+                                            _p, _p, _p, _p, _p, _sz, _p]
     L.rtnq_dev_relayout.argtypes = [_p, Layout, _p, Layout, _i32, _i64, _i64, _p]
     L.rtnq_dev_native_scales.argtypes = [_p, _i32, _i64, _i64, _p, _p]
     L.rtnq_dev_dequantize.argtypes = [_p, Layout, _i32, _i64, _i64, _i64, _p, _i32, _i32, _p,
@@ -210,12 +214,12 @@ class QuantWeight:
 def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None,
                   row_major=False, kernel=False, scales_f32=False, scales_f16=False,
                   check=True, stream=None) -> QuantWeight:
-    """RTN quantize-and-pack on the GPU (rtnq_dev_quantize_pack).
+    """RTN quantize-and-pack on the GPU (rtnq_dev_quantize_pack_ex).
 
     The linear's operand is ``codes`` in ``out.layout``.  With ``native=None`` that is the
     layout of the fastest kernel for the shape: NATIVE_I8 for W8 per-channel and NATIVE_I4
-    for W4 group-128 (tcgen05 kind::i8 kernels, relaid out from the reference's row-major
-    bytes), else NATIVE (tcgen05 kind::f16 kernel).  ``native=True`` forces NATIVE."""
+    for W4 group-128 (tcgen05 kind::i8 kernels; one quantize kernel writes their tiles
+    directly), else NATIVE (tcgen05 kind::f16 kernel).  ``native=True`` forces NATIVE."""
     torch = _torch()
     assert w.is_cuda and w.dim() == 2 and w.is_contiguous()
     rows, cols = w.shape
@@ -232,11 +236,10 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
         elif bits == 4 and group == 128:
             imma = NATIVE_I4
     native = (imma is None) if native is None else native
-    rm_requested = row_major
-    if imma is not None:
+    if imma is not None:  # one kernel writes the int8-MMA tiles (rtnq_dev_quantize_pack_ex)
         native = False
-        row_major = True
         out.layout = imma
+        out.codes = torch.empty(layout_bytes(layout(imma), bits, rows, cols), **u8)
         out.scales = torch.empty(native_scale_count(rows, gpr), dtype=torch.int16, device=dev)
     if native:
         out.codes = torch.empty(layout_bytes(layout(NATIVE), bits, rows, cols), **u8)
@@ -250,21 +253,17 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
         out.scales_f32 = torch.empty(rows, gpr, dtype=torch.float32, device=dev)
     if scales_f16:
         out.scales_f16 = torch.empty(rows, gpr, dtype=torch.int16, device=dev)
-    wsb = lib().rtnq_dev_quantize_workspace_bytes(rows, cols, bits, group, int(ragged))
+    kind = imma if imma is not None else NATIVE
+    wsb = lib().rtnq_dev_quantize_workspace_bytes_ex(rows, cols, bits, group, int(ragged), kind)
     ws = torch.empty(max(wsb, 1), **u8)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     st = _stream(stream)
-    _check(lib().rtnq_dev_quantize_pack(
-        _ptr(w), _dt(w), rows, cols, bits, group, int(ragged), _ptr(out.codes_row_major),
+    _check(lib().rtnq_dev_quantize_pack_ex(
+        _ptr(w), _dt(w), rows, cols, bits, group, int(ragged), kind, _ptr(out.codes_row_major),
         _ptr(out.codes_kernel), _ptr(out.codes), _ptr(out.scales_f32), _ptr(out.scales_f16),
         _ptr(out.scales), _ptr(err), _ptr(ws), wsb, st))
     if check:
         _check(lib().rtnq_dev_check_flag(_ptr(err), st))
-    if imma is not None:  # int8-MMA tiles, from the row-major bytes
-        out.codes = relayout(out.codes_row_major, layout(ROW_MAJOR), layout(imma), bits, rows,
-                             cols, stream=stream)
-        if not rm_requested:
-            out.codes_row_major = None
     return out
 
 

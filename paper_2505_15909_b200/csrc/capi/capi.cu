@@ -199,6 +199,66 @@ rtnq_status rtnq_dev_quantize_pack(const void* w, int w_dtype, int64_t rows, int
     return RTNQ_OK;
 }
 
+size_t rtnq_dev_quantize_workspace_bytes_ex(int64_t rows, int64_t cols, int bits, int64_t g,
+                                            int ragged, int native_kind) {
+    const size_t base = rtnq_dev_quantize_workspace_bytes(rows, cols, bits, g, ragged);
+    if (native_kind != RTNQ_NATIVE_I4 && native_kind != RTNQ_NATIVE_I8) return base;
+    // the general route quantizes into row-major bytes first, then relays them out
+    return base + (size_t(rows * cols * bits / 8) + 255) / 256 * 256;
+}
+
+rtnq_status rtnq_dev_quantize_pack_ex(const void* w, int w_dtype, int64_t rows, int64_t cols,
+                                      int bits, int64_t g, int ragged, int native_kind,
+                                      uint8_t* rm, uint8_t* k164, uint8_t* nat, float* s32,
+                                      uint16_t* s16, uint16_t* s16n, int32_t* err, void* ws,
+                                      size_t ws_bytes, void* stream) {
+    if (native_kind == RTNQ_NATIVE_SM100)
+        return rtnq_dev_quantize_pack(w, w_dtype, rows, cols, bits, g, ragged, rm, k164, nat, s32,
+                                      s16, s16n, err, ws, ws_bytes, stream);
+    if (native_kind != RTNQ_NATIVE_I4 && native_kind != RTNQ_NATIVE_I8)
+        return fail(RTNQ_E_INVALID_INPUT, "native_kind must be RTNQ_NATIVE_SM100, _I4 or _I8");
+    if (!valid_bits(bits)) return fail(RTNQ_E_INVALID_INPUT, "bits must be 4 or 8");
+    if (rows < 0 || cols < 0) return fail(RTNQ_E_SHAPE, "negative tensor dimension");
+    const int64_t gpr = rtnq_groups_per_row(g, ragged, cols);
+    if (gpr < 0) return rtnq_status(-gpr);
+    if (native_kind == RTNQ_NATIVE_I4 && (bits != 4 || g != 128))
+        return fail(RTNQ_E_UNSUPPORTED, "RTNQ_NATIVE_I4 holds W4 group-128 codes");
+    if (native_kind == RTNQ_NATIVE_I8 && (bits != 8 || g < cols))
+        return fail(RTNQ_E_UNSUPPORTED, "RTNQ_NATIVE_I8 holds W8 per-channel codes (one group per row)");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (rows * cols == 0) return RTNQ_OK;
+    if (s16n) RTNQ_CUDA(cudaMemsetAsync(s16n, 0, size_t(rtnq_native_scale_count(rows, gpr)) * 2, st));
+    // one pass straight into the int8-MMA tiles
+    if (!k164 && nat && native_kind == RTNQ_NATIVE_I4 && quant_i4_supported(rows, cols, bits, g)) {
+        launch_quant_i4(w, w_dtype, rows, cols, nat, rm, s32, s16, s16n, err, st);
+        RTNQ_CUDA(cudaGetLastError());
+        return RTNQ_OK;
+    }
+    if (!k164 && nat && native_kind == RTNQ_NATIVE_I8 && quant_rowwise_supported(rows, cols, bits, g)) {
+        launch_quant_rowwise(w, w_dtype, rows, cols, nat, rm, s32, s16, s16n, err, st);
+        RTNQ_CUDA(cudaGetLastError());
+        return RTNQ_OK;
+    }
+    // general route: the reference-layout kernels into row-major bytes, then a relayout
+    const size_t need = rtnq_dev_quantize_workspace_bytes_ex(rows, cols, bits, g, ragged, native_kind);
+    if (!ws || ws_bytes < need)
+        return fail(RTNQ_E_INVALID_INPUT, "quantize workspace too small: need " + std::to_string(need) + " bytes");
+    const size_t base = rtnq_dev_quantize_workspace_bytes(rows, cols, bits, g, ragged);
+    uint8_t* rmb = rm ? rm : static_cast<uint8_t*>(ws) + base;
+    RTNQ_TRY(rtnq_dev_quantize_pack(w, w_dtype, rows, cols, bits, g, ragged, rmb, k164, nullptr, s32,
+                                    s16, nullptr, err, ws, base, stream));
+    if (s16n) {
+        // native scales from the f16 reference-order scales, or f32 (both exact)
+        if (s16) launch_native_scales(s16, RTNQ_F16, rows, gpr, s16n, st);
+        else if (s32) launch_native_scales(s32, RTNQ_F32, rows, gpr, s16n, st);
+        else return fail(RTNQ_E_INVALID_INPUT, "native scales on the general route need scales_f32 or scales_f16");
+    }
+    if (nat)
+        launch_relayout(rmb, Layout{RTNQ_ROW_MAJOR, 16, 4}, nat, Layout{native_kind, 16, 4}, bits, rows, cols, st);
+    RTNQ_CUDA(cudaGetLastError());
+    return RTNQ_OK;
+}
+
 rtnq_status rtnq_dev_relayout(const uint8_t* src, rtnq_layout from, uint8_t* dst, rtnq_layout to,
                               int bits, int64_t rows, int64_t cols, void* stream) {
     if (!valid_bits(bits)) return fail(RTNQ_E_INVALID_INPUT, "bits must be 4 or 8");

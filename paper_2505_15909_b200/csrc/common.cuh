@@ -62,7 +62,11 @@ __device__ __forceinline__ float scale_from_absmax(float absmax, int bits) {
 // Verified bit-exact against the reference by tests/test_gpu_full_shapes.py
 // (test_quantize_f32_ties_bit_exact: f32 weights on or one ulp beside a tie).
 __device__ __forceinline__ int quantize_one(float v, float s, int bits) {
-    const float a = fabsf(v);
+    float a = fabsf(v);
+    if (s < 5.421010862427522e-20f) {  // S < 2^-64: scale both by 2^64 (exact) so the tie
+        a *= 18446744073709551616.0f;  // test below never underflows into -0
+        s *= 18446744073709551616.0f;
+    }
     const float q = __fdiv_rn(a, s);
     float k = floorf(q);
     const float r = __fmaf_rn(-(k + 0.5f), s, a);
@@ -71,6 +75,37 @@ __device__ __forceinline__ int quantize_one(float v, float s, int bits) {
     int n = static_cast<int>(fminf(k, 256.0f));
     int c = v < 0.0f ? -n : n;
     return c < lo ? lo : (c > hi ? hi : c);
+}
+
+// quantize_one without a division (the load-path kernels, quant_native.cu).  inv is any
+// approximation of 1/S good to ~2^-20 (MUFU.RCP): n0 = rint(|v| * inv) is then the reference's
+// code magnitude n = round_half_away(|v| / S) or one off, and only next to a half-integer.  Two
+// FMAs with exact signs fix it: |v| - (n0 - 0.5) S < 0  ->  n0 - 1,  |v| - (n0 + 0.5) S >= 0  ->
+// n0 + 1 (ties go away from zero, quant.cpp:24-29).  |v| / S <= 7.5 (4-bit) or 127.5 (8-bit)
+// by construction of S, so only the positive side needs the qmax clamp.
+// Checked bit-exact on tie-rich f32 inputs (tests/test_gpu_full_shapes.py).
+// Callers pass S >= 2^-64 (else v and S pre-scaled by 2^64, exact: quant_scale_prep), so the
+// remainders of the tie test are far above the subnormal range and never round to -0.
+template <int BITS>
+__device__ __forceinline__ int quantize_fast(float v, float s, float inv) {
+    const float a = fabsf(v);
+    const float b = __fmaf_rn(a, inv, 12582912.0f);  // 1.5 * 2^23 + rint(a * inv)
+    const float n0 = __fsub_rn(b, 12582912.0f);
+    int n = __float_as_int(b) - 0x4B400000;
+    n -= __fmaf_rn(-__fsub_rn(n0, 0.5f), s, a) < 0.0f;
+    n += __fmaf_rn(-__fadd_rn(n0, 0.5f), s, a) >= 0.0f;
+    return v < 0.0f ? -n : min(n, (1 << (BITS - 1)) - 1);
+}
+
+struct QuantScale {
+    float s;    // the scale the tie test uses (S, or S * 2^64 for S < 2^-64)
+    float inv;  // ~1 / s
+    float pre;  // 1, or 2^64: multiply v by it
+};
+__device__ __forceinline__ QuantScale quant_scale_prep(float S) {
+    const bool tiny = S < 5.421010862427522e-20f;
+    const float s = tiny ? S * 18446744073709551616.0f : S;
+    return {s, __frcp_rn(s), tiny ? 18446744073709551616.0f : 1.0f};
 }
 
 // ---- layouts -----------------------------------------------------------------------------

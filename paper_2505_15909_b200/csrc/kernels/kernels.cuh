@@ -30,6 +30,14 @@ void launch_check_finite(const void* p, int dtype, int64_t n, int32_t* err, cuda
 // quant_fused.cu: one-pass quantize+pack for 16 x 128 tiles.  Returns false
 // (launching nothing) when the shape is outside the fused kernel's domain.
 bool quant_fused_supported(int64_t rows, int64_t cols, int bits, int64_t g);
+// quant_native.cu: one-pass quantize straight into RTNQ_NATIVE_I4 (W4 g128) / RTNQ_NATIVE_I8
+// (W8 per-channel), plus row-major bytes and scales
+bool quant_i4_supported(int64_t rows, int64_t cols, int bits, int64_t g);
+bool quant_rowwise_supported(int64_t rows, int64_t cols, int bits, int64_t g);
+void launch_quant_i4(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* ni4, uint8_t* rm, float* s32,
+                     uint16_t* s16, uint16_t* s16n, int32_t* err, cudaStream_t st);
+void launch_quant_rowwise(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* ni8, uint8_t* rm,
+                          float* s32, uint16_t* s16, uint16_t* s16n, int32_t* err, cudaStream_t st);
 void launch_quant_fused(const void* w, int dtype, int64_t rows, int64_t cols, int bits,
                         int64_t g, uint8_t* rm, uint8_t* k164, uint8_t* nat, float* s32,
                         uint16_t* s16, uint16_t* s16n, int32_t* err, cudaStream_t st);

@@ -292,12 +292,16 @@ class TPDecodeStack:
 
     def __init__(self, shape: LlamaShape, table, world: int, rank: int, batch: int,
                  max_len: int = 257, pos: int = 256, group: int = 128, layers=None, seed=0,
-                 device="cuda", w8_per_channel=False, fuse_planes=True):
+                 device="cuda", w8_per_channel=False, fuse_planes=True, collectives=True):
+        """collectives=False builds ONE rank's shard stack of a TP=world model without a
+        process group (the per-GPU work of that configuration on a single GPU; the allreduces
+        are skipped)."""
         import torch
 
         import paper_2505_15909_b200 as rq
         n = shape.layers if layers is None else layers
         self.world, self.rank, self.shape = world, rank, shape
+        self.collectives = collectives
         self.layers = [TPDecodeLayer(shape, li, world, rank, module_bits(table, li), batch,
                                      max_len, pos, group, seed=seed, device=device,
                                      w8_per_channel=w8_per_channel, fuse_planes=fuse_planes)
@@ -313,7 +317,7 @@ class TPDecodeStack:
         return sum(l.weight_bytes for l in self.layers)
 
     def _allreduce(self, t):
-        if self.world > 1:
+        if self.world > 1 and self.collectives:
             import torch.distributed as dist
             dist.all_reduce(t)
         return t

@@ -109,7 +109,7 @@ def test_tp_shards_quantized_before_sharding(oracle, world, bits, per_channel):
             assert rel_frob(acc, ref) <= TOL, m
 
 
-def test_quantize_f32_ties_bit_exact(golden_ties):
+def test_quantize_f32_ties_bit_exact(golden_ties, oracle):
     """f32 weights on / one ulp beside rounding ties: the device quantize equals the reference's
     bytes (row-major and kernel_interleaved) and scales, bit for bit."""
     for name, z in golden_ties.items():
@@ -120,9 +120,43 @@ def test_quantize_f32_ties_bit_exact(golden_ties):
         assert np.array_equal(q.codes_row_major.cpu().numpy(), z["data"]), name
         assert np.array_equal(q.scales_f32.cpu().numpy(), z["scales"]), name
         assert np.array_equal(q.scales_f16.cpu().numpy().view(np.uint16), z["scales_f16"]), name
+        # the default operand layouts: one kernel writes NATIVE_I4 / NATIVE_I8 directly
+        if (bits, g) == (4, 128) or (bits == 8 and g >= cols):
+            qn = rq.quantize_pack(w, bits, g, bool(ragged), row_major=True, scales_f16=True)
+            logical = oracle.unpack(z["data"], rows * cols, bits).reshape(rows, cols)
+            enc = encode_native_i4 if bits == 4 else encode_native_i8
+            assert np.array_equal(qn.codes.cpu().numpy(), enc(logical)), name
+            assert np.array_equal(qn.codes_row_major.cpu().numpy(), z["data"]), name
+            assert np.array_equal(qn.scales.cpu().numpy().view(np.uint16),
+                                  oracle.native_scales(z["scales_f16"], rows, z["scales"].shape[1])), name
         # the host drop-in path (rtnq_quantize_tensor) too
         data, sc = rq.quantize_tensor(z["w"], bits, g, bool(ragged))
         assert np.array_equal(data, z["data"]) and np.array_equal(sc, z["scales"]), name
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("rows,cols", [(1, 128), (129, 256), (200, 4096), (128, 14336), (300, 53248), (7, 48)])
+def test_native_quantize_edges(oracle, bits, rows, cols):
+    """The one-pass native-layout quantize (quant_native.cu) at ragged row counts (zero padding
+    of the last 128-row tile), K past the register window (53248, the 405B ffn_down), K not a
+    multiple of 128 (general route), tiny and subnormal group scales, all-zero groups; against
+    the oracle's codes, re-encoded, and its scales."""
+    g = 128 if bits == 4 else 1 << (cols - 1).bit_length()
+    ragged = cols % g != 0
+    gen = torch.Generator(device="cuda").manual_seed(rows + cols + bits)
+    w = torch.rand(rows, cols, device="cuda", generator=gen) * 2 - 1
+    w[0] *= 1e-39                      # subnormal scale: 1/S overflows f32
+    if rows > 2:
+        w[1] *= 2.0 ** -100
+        w[2, : min(cols, 256)] = 0     # all-zero groups -> S = 1
+    for dt in (torch.float32, torch.bfloat16):
+        x = w.to(dt)
+        q = rq.quantize_pack(x, bits, g, ragged, row_major=True, scales_f32=True)
+        codes, scales = oracle.quantize(x.float().cpu().numpy(), bits, g, ragged)
+        assert np.array_equal(q.scales_f32.cpu().numpy(), scales), dt
+        assert np.array_equal(q.codes_row_major.cpu().numpy(), oracle.pack(codes, bits)), dt
+        enc = encode_native_i4 if bits == 4 else encode_native_i8
+        assert np.array_equal(q.codes.cpu().numpy(), enc(codes)), dt
 
 
 def test_gemm_float_bit_exact(golden_gemm_float, oracle):
