@@ -122,8 +122,7 @@ rtnq_status rtnq_dev_quantize_pack(const void* w, int w_dtype, int64_t rows, int
  * kernel_interleaved output is requested and cols % 128 == 0 (I4) / cols % 16 == 0 (I8),
  * ONE kernel reads the weights once and writes the native tiles (padding included), the
  * optional row-major bytes and the scales; otherwise the row-major bytes are quantized first
- * (caller's codes_row_major or the workspace) and relaid out.  The scales_f16_native of the
- * general route need scales_f32 or scales_f16 as well. */
+ * (caller's codes_row_major or the workspace) and relaid out. */
 size_t rtnq_dev_quantize_workspace_bytes_ex(int64_t rows, int64_t cols, int bits, int64_t g,
                                             int ragged, int native_kind);
 rtnq_status rtnq_dev_quantize_pack_ex(const void* w, int w_dtype, int64_t rows, int64_t cols,

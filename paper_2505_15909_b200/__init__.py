@@ -28,7 +28,8 @@ from .errors import (CorruptDataError, CudaError, Error, InvalidInputError, Plan
                      ShapeError, UnsupportedError, raise_for)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "librtnq_b200.so")
+# RTNQ_LIB: an alternative build of the same library (e.g. the RTNQ_KERNEL_DEBUG profiling build)
+LIB_PATH = os.environ.get("RTNQ_LIB") or os.path.join(PKG, "librtnq_b200.so")
 
 F32, F16, BF16 = 0, 1, 2
 ROW_MAJOR, KERNEL_INTERLEAVED, NATIVE, NATIVE_I8, NATIVE_I4 = 0, 1, 2, 3, 4

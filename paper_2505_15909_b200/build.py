@@ -32,6 +32,8 @@ CUFLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "
 # by scratch/i4prof.py, i8tl.py, ...); off by default because the checks cost a few % per launch
 if os.environ.get("RTNQ_KERNEL_DEBUG"):
     CUFLAGS = CUFLAGS + ["-DRTNQ_KERNEL_DEBUG"]
+# experiments only (A/B builds into another library, scratch/*): extra -D flags
+CUFLAGS = CUFLAGS + os.environ.get("RTNQ_EXTRA_CUFLAGS", "").split()
 
 
 def sources():

@@ -245,14 +245,9 @@ rtnq_status rtnq_dev_quantize_pack_ex(const void* w, int w_dtype, int64_t rows, 
         return fail(RTNQ_E_INVALID_INPUT, "quantize workspace too small: need " + std::to_string(need) + " bytes");
     const size_t base = rtnq_dev_quantize_workspace_bytes(rows, cols, bits, g, ragged);
     uint8_t* rmb = rm ? rm : static_cast<uint8_t*>(ws) + base;
+    // (the native scale order is the same for every native code layout)
     RTNQ_TRY(rtnq_dev_quantize_pack(w, w_dtype, rows, cols, bits, g, ragged, rmb, k164, nullptr, s32,
-                                    s16, nullptr, err, ws, base, stream));
-    if (s16n) {
-        // native scales from the f16 reference-order scales, or f32 (both exact)
-        if (s16) launch_native_scales(s16, RTNQ_F16, rows, gpr, s16n, st);
-        else if (s32) launch_native_scales(s32, RTNQ_F32, rows, gpr, s16n, st);
-        else return fail(RTNQ_E_INVALID_INPUT, "native scales on the general route need scales_f32 or scales_f16");
-    }
+                                    s16, s16n, err, ws, base, stream));
     if (nat)
         launch_relayout(rmb, Layout{RTNQ_ROW_MAJOR, 16, 4}, nat, Layout{native_kind, 16, 4}, bits, rows, cols, st);
     RTNQ_CUDA(cudaGetLastError());

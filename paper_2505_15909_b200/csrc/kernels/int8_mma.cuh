@@ -19,11 +19,17 @@ __device__ __forceinline__ uint32_t su32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
 }
+// The suspend-time hint keeps a waiting warp parked until the phase completes (or ~1 ms)
+// instead of re-polling every few hundred cycles: spinning warps take issue slots from the
+// working warps of the same SM sub-partition (ncu: ~17% of the W4 kernel's instructions).
+#ifndef RTNQ_MBAR_HINT_NS
+#define RTNQ_MBAR_HINT_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
     asm volatile(
-        "{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n"
         "@!P bra W_%=;\n}\n" ::"r"(su32(b)),
-        "r"(ph)
+        "r"(ph), "n"(RTNQ_MBAR_HINT_NS)
         : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -110,6 +116,41 @@ __device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t ad, uint64_t b
     asm volatile(
         "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// Warp-uniform MMA issue: the whole (converged) warp executes the asm, one elected lane issues
+// every MMA of the block.  Measured (scratch/tmem_bw.cu): ~13 cycles per M128 x N16 x K32 MMA,
+// and N = 48 at the tensor-core floor (24 cycles), against ~100 cycles per MMA when one lane
+// inside a divergent branch issues them (the compiler wraps each tcgen05.mma in an elect loop
+// with a register -> uniform-register move).  The same elected lane must issue the commits.
+//
+// 4 k-steps of K = 32 into one accumulator: A from TMEM at a, a + 8, a + 16, a + 24 (32-bit
+// columns of 4 s8), B descriptors bd, bd + 2, bd + 4, bd + 6 (32-byte steps); acc = 0
+// overwrites D with the first product.
+__device__ __forceinline__ void mma4_i8_ts_warp(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p0, p1;\n.reg .b32 a1, a2, a3;\n.reg .b64 b1, b2, b3;\n"
+        "setp.ne.b32 p0, %4, 0;\nsetp.eq.b32 p1, 0, 0;\n"
+        "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\n"
+        "add.u64 b1, %2, 2;\nadd.u64 b2, %2, 4;\nadd.u64 b3, %2, 6;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %3, p1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b2, %3, p1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b3, %3, p1;\n}\n" ::"r"(d),
+        "r"(a), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// 2 k-steps of K = 32, A and B from shared memory (descriptors ad, ad + 2 and bd, bd + 2).
+__device__ __forceinline__ void mma2_i8_ss_warp(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p0, p1;\n.reg .b64 a1, b1;\n"
+        "setp.ne.b32 p0, %4, 0;\nsetp.eq.b32 p1, 0, 0;\n"
+        "add.u64 a1, %1, 2;\nadd.u64 b1, %2, 2;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, p1;\n}\n" ::"r"(d),
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
 }
@@ -378,6 +419,122 @@ __device__ __forceinline__ void row_to_planes(const uint16_t* __restrict__ rowp,
             *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
                 make_uint2(pk[pl][0], pk[pl][1]);
     }
+}
+
+// ---- activation planes computed inside the GEMM (no separate planes kernel) -----------------
+// A stand-alone planes kernel costs each int8 linear ~5 us at batch 16 in a back-to-back chain
+// (launch + two grid dependencies) for ~1 us of work.  Instead, the GEMM CTAs compute the
+// planes of the launch's tokens themselves (CTA c: tokens c, c + G, ...) with their epilogue /
+// expansion warps, which are idle until the first weights land, and publish them through a
+// self-resetting workspace counter; one warp per CTA acquires it before the first planes TMA.
+constexpr int kOwnPlanesMinM = 8;  // fewer tokens: the stand-alone planes kernel
+struct OwnPlanes {
+    const void* a = nullptr;  // activations [Mtot][K], bf16 / f16; nullptr: planes precomputed
+    int a_dtype = 0;
+    int* done = nullptr;      // tokens published by this launch (workspace, starts at 0)
+    int* consumed = nullptr;  // CTAs that have acquired them; the last one resets both
+    int32_t* err = nullptr;   // |= 1 on a non-finite activation (InvalidInputError)
+};
+
+// One token row -> its planes and exponent (act_planes_kernel's arithmetic), by `nthr` threads
+// (tid in [0, nthr)) synchronized with the named barrier `bar`; `red` is nthr / 32 floats of smem.
+template <int AT>
+__device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, int K, int t, int M,
+                                             int8_t* __restrict__ planes, int32_t* __restrict__ texp,
+                                             int32_t* err, int tid, int nthr, int bar, float* red) {
+    auto cvt = [](uint32_t h) -> float {
+        if constexpr (AT == RTNQ_BF16) return __uint_as_float(h << 16);
+        else return __half2float(__ushort_as_half(static_cast<unsigned short>(h)));
+    };
+    constexpr uint32_t kExpMask = AT == RTNQ_BF16 ? 0x7F807F80u : 0x7C007C00u;
+    const int nv = K / 8;
+    float mx = 0.0f;
+    uint32_t nonfinite = 0;
+    for (int v = tid; v < nv; v += nthr) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(rowp) + v);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            mx = fmaxf(mx, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+            const uint32_t e = w[i] & kExpMask;
+            nonfinite |= ((e & 0xffffu) == (kExpMask & 0xffffu)) | ((e >> 16) == (kExpMask >> 16));
+        }
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (err && __any_sync(0xffffffffu, nonfinite) && (tid & 31) == 0) atomicOr(err, 1);
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
+    float amax = 0.0f;
+    for (int i = 0; i < nthr / 32; ++i) amax = fmaxf(amax, red[i]);
+    int e = 0;
+    if (amax > 0.0f) frexpf(amax, &e);
+    const int s = max(e - 6, -126);
+    if (tid == 0) texp[t] = s;
+    const float inv = __int_as_float((127 - s) << 23);
+    for (int v = tid; v < nv; v += nthr) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(rowp) + v);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float y = cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu) * inv;
+            const float b0 = y + 12582912.0f, r0 = b0 - 12582912.0f;
+            const float y1 = (y - r0) * 128.0f;
+            const float b1 = y1 + 12582912.0f, r1 = b1 - 12582912.0f;
+            const float b2 = (y1 - r1) * 128.0f + 12582912.0f;
+            pk[0][i >> 2] |= (uint32_t(__float_as_int(b0) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+            pk[1][i >> 2] |= (uint32_t(__float_as_int(b1) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+            pk[2][i >> 2] |= (uint32_t(__float_as_int(b2) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+        }
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+            *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
+                make_uint2(pk[pl][0], pk[pl][1]);
+    }
+    // every thread's planes stores are done before the caller publishes the token
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
+}
+
+// Producers: CTA c of G computes tokens m0 + t, t = c, c + G, ... < M, after the activations'
+// producer grid has completed (griddepcontrol.wait), and publishes each one.
+__device__ __forceinline__ void own_planes_produce(const OwnPlanes& op, int K, int m0, int M, int Mtot, int c,
+                                                   int G, int8_t* planes, int32_t* texp, int tid, int nthr,
+                                                   int bar, float* red) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int t = c; t < M; t += G) {
+        const uint16_t* rowp = static_cast<const uint16_t*>(op.a) + int64_t(m0 + t) * K;
+        if (op.a_dtype == RTNQ_BF16)
+            token_planes<RTNQ_BF16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red);
+        else
+            token_planes<RTNQ_F16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red);
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // the consumers read them by TMA
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(op.done) : "memory");
+        }
+    }
+}
+
+// Consumer (one whole warp per CTA): returns once all M tokens of this launch are published.  The
+// last of the G CTAs to get here resets both counters; the next launch on this workspace only
+// touches them after its own griddepcontrol.wait, i.e. after this grid has completed.
+__device__ __forceinline__ void own_planes_acquire(const OwnPlanes& op, int M, int G) {
+    // the previous launch on this workspace must be complete before its counters are read: with
+    // PDL (and free SMs) this grid's CTAs can start while it still runs
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if ((threadIdx.x & 31) == 0) {
+        int got;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(op.done) : "memory");
+            if (got >= M) break;
+            __nanosleep(32);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (atomicAdd(op.consumed, 1) == G - 1) {
+            atomicExch(op.done, 0);
+            atomicExch(op.consumed, 0);
+        }
+    }
+    __syncwarp();
 }
 
 template <int AT, bool VEC>

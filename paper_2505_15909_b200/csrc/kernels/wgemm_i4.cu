@@ -57,6 +57,8 @@ struct Params {
     int64_t N, K;
     int M, Mtot, m0, NB, KBLK, U, G, csize, out_dtype;
     int debug;
+    imma::OwnPlanes own;  // own.a != nullptr: this launch computes its tokens' planes itself
+    int8_t* planes_w;     // ... into this [3][Mtot][K] buffer (the TMA source), exponents into texp
 };
 
 template <int PT>
@@ -65,13 +67,22 @@ struct Geo {
     static constexpr int DN = (3 * PT + 15) / 16 * 16;      // accumulator columns per group
     static constexpr int BOX_BYTES = 3 * PT * 128;          // one group's planes box
     static constexpr int PLANE_BYTES = DN * 128;            // ... its smem slot (zero rows past it)
-    static constexpr int TPS = PT <= 32 ? 2 : 1;            // groups (tiles) per stage
+    // groups (tiles) per stage: every stage costs each role a fixed few hundred cycles of
+    // barrier hand-offs (measured: the stage period stays ~1000 cycles with all memory traffic
+    // switched off), so batch <= 16 moves four groups (32 KiB of codes) per stage
+#ifndef RTNQ_I4_TPS16
+#define RTNQ_I4_TPS16 4
+#endif
+    static constexpr int TPS = PT <= 16 ? RTNQ_I4_TPS16 : PT <= 32 ? 2 : 1;
     static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
     static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
     // two epilogue warpgroups (one per group of a stage) when a stage holds two groups
-    static constexpr int EW = 1;  // 2 (a warpgroup per group of a stage, 512 threads) measured slower:
-                                  // both warpgroups share the 64 B/clk TMEM read port
+#ifndef RTNQ_I4_EW
+#define RTNQ_I4_EW 1
+#endif
+    static constexpr int EW = RTNQ_I4_EW;  // 2: a second epilogue warpgroup (512 threads) takes the
+                                           // odd groups of every stage (measured slower)
     static constexpr int THREADS = EW == 2 ? 512 : 384;
     static constexpr int SCR_BYTES = EW == 2 ? ACC * kRows * 4 : 0;  // warpgroup B's partial sums
     // The A operand of a group is 4 k-steps of 32 codes.  The first KT come from TMEM (tcgen05.st
@@ -79,10 +90,14 @@ struct Geo {
     // accumulator readback), the rest from a 128B-swizzled smem tile (128 B/clk smem port,
     // shared with TMA and the planes).  KT balances the two ports for the batch size.
     static constexpr int KT = 4;
-    static constexpr int AS = PT <= 16 ? 6 : PT <= 32 ? 4 : 2;  // expanded A slots (groups)
+    // expanded A slots (groups); TMEM = AS * 32 A columns + NS * DN accumulator columns
+    static constexpr int AS = TPS == 4 ? (PT <= 10 ? 8 : 4) : PT <= 16 ? 6 : PT <= 32 ? 4 : 2;
     static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
     static constexpr int A_SMEM = KT < 4 ? kRows * 128 : 0;  // smem A tile per slot (16 KiB)
-    static constexpr int STAGES_FIT = (212 * 1024 - SCR_BYTES - AS * A_SMEM) / STAGE_BYTES;
+#ifndef RTNQ_I4_SMEM_KB
+#define RTNQ_I4_SMEM_KB 212
+#endif
+    static constexpr int STAGES_FIT = ((PT <= 16 ? RTNQ_I4_SMEM_KB : 212) * 1024 - SCR_BYTES - AS * A_SMEM) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int A_OFF = STAGES * STAGE_BYTES;      // smem A slots (1024-aligned)
     static constexpr int A_COL = 512 - AS * KT * 8;         // TMEM A slots: 8 columns per k-step
@@ -100,6 +115,12 @@ struct Geo {
 };
 
 __device__ unsigned long long g_i4_dbg[1024 * 16];  // profiling (debug & 64: globaltimer stamps)
+// profiling (debug & 512): per-stage clock64 timeline of CTA p.debug >> 16 -- [stage][event]:
+// 0 codes TMA issued, 1 MMAs issued (before the commits), 2 expansion start, 3 expansion done, 4 MMA start,
+// 5 MMA issued, 6 epilogue start, 7 epilogue done
+__device__ long long g_i4_tl[64 * 16];
+#define I4_TL(si, ev) \
+    if ((dbg_ & 512) && c == (dbg_ >> 16) && (si) < 64 && lane == 0) g_i4_tl[(si) * 16 + (ev)] = clock64() - tl0
 
 // A from TMEM (32-bit columns of 4 s8 along K), B from shared memory
 __device__ __forceinline__ void mma_i8_ts_elect(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc,
@@ -179,9 +200,11 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
     uint64_t* go = sfull + NP;          // cluster split-K: leader ready for partials
     uint64_t* rfull = go + 1;           // cluster split-K: partials landed in the leader
     uint64_t* pub = rfull + 1;          // stream-K contributor partials stored (4 warps)
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(pub + 1);
+    uint64_t* pready = pub + 1;         // own planes: this launch's planes / exponents published
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(pready + 1);
     float* sring = reinterpret_cast<float*>(smem + GG::SR_OFF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
+    const long long tl0 = (dbg_ & 512) ? clock64() : 0;
     if ((dbg_ & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 5] = gtime();
 
     int u0, u1;
@@ -197,7 +220,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 5);
         for (int i = 0; i < AP; ++i) mbar_init(&afull[i], 4), mbar_init(&aempty[i], 1);
         for (int i = 0; i < NP; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4 * EW), mbar_init(&sfull[i], 4);
-        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4);
+        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4), mbar_init(pready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if constexpr (GG::DN > 3 * PT) {  // B rows past 3 * PT: zero once, never written by TMA
@@ -220,6 +243,13 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
     if (p.csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const uint32_t tmem = *tslot;
     asm volatile("griddepcontrol.launch_dependents;");
+    if (p.own.a && warp >= kEpi0 && warp < kExp0 + 4) {
+        // the epilogue + expansion warps (idle until the first weights land) compute this CTA's
+        // share of the launch's activation planes (int8_mma.cuh, own_planes_produce)
+        __shared__ float pred[8];
+        own_planes_produce(p.own, int(p.K), p.m0, p.M, p.Mtot, c, int(gridDim.x), p.planes_w,
+                           const_cast<int32_t*>(p.texp), threadIdx.x - kEpi0 * 32, 256, 3, pred);
+    }
 
     if (warp == 0 || warp == 2) {
         // ===================== producers: warp 0 codes + scales, warp 2 planes ============
@@ -227,7 +257,14 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
         Cursor<TPS> cu(u0, u1, p.KBLK);
         int s = 0;
         uint32_t ph = 0;
-        if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes kernel
+        if (!codes) {
+            if (p.own.a) {  // planes computed by this launch's CTAs
+                own_planes_acquire(p.own, p.M, int(gridDim.x));
+                if (lane == 0) mbar_arrive(pready);
+            } else {
+                asm volatile("griddepcontrol.wait;" ::: "memory");  // planes kernel / fused producer
+            }
+        }
         long long w_empty = 0;
         for (int i = 0; cu.more(); ++i) {
             const int n = cu.chunk();
@@ -256,6 +293,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                     elect_tma3d_tx(st + (slot0 + j) * GG::PLANE_BYTES, &p.tmap_p, (cu.kb + j) * kKB, p.m0, 0,
                                    &full[s]);
             }
+            if (codes) I4_TL(i, 0);
             cu.advance(n);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
@@ -290,65 +328,66 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&full[s], ph);
                 I4_ACC(x_full);
             }
+            if (warp == kExp0) I4_TL(si, 11);
             {
                 I4_T0();
                 if (si >= AP) mbar_wait(&aempty[ap], uint32_t(si / AP - 1) & 1u);
                 I4_ACC(x_aempty);
             }
+            if (warp == kExp0) I4_TL(si, 12);
             {
                 I4_T0();
                 if (si >= NP) mbar_wait(&tfree[np], uint32_t(si / NP - 1) & 1u);
                 I4_ACC(x_tfree);
             }
             const long long _tw = (dbg_ & 32) ? clock64() : 0;
+            if (warp == kExp0) I4_TL(si, 2);
             const uint8_t* st = smem + s * GG::STAGE_BYTES;
             if (!(dbg_ & 65536)) {
-                // all of the stage's code loads first (latency overlap), then expand and store
-                uint4 w[TPS][4];
+                // two groups at a time: their code loads first (latency overlap), then expand and store
+                constexpr int JP = TPS < 2 ? TPS : 2;
 #pragma unroll
-                for (int j = 0; j < TPS; ++j)
-                    if (j < n) {
-                        const uint8_t* src = st + GG::CODE_OFF + (slot0 + j) * kTile + row * 64;
+                for (int j0 = 0; j0 < TPS; j0 += JP) {
+                    if (j0 >= n) break;
+                    uint4 w[JP][4];
 #pragma unroll
-                        for (uint32_t q = 0; q < 4; ++q)
-                            w[j][q] = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
-                    }
-                float scv[TPS];
+                    for (int jj = 0; jj < JP; ++jj)
+                        if (j0 + jj < n) {
+                            const uint8_t* src = st + GG::CODE_OFF + (slot0 + j0 + jj) * kTile + row * 64;
 #pragma unroll
-                for (int j = 0; j < TPS; ++j) {
-                    const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
-                    scv[j] = (j < n && row < r8) ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
-                }
-#pragma unroll
-                for (int j = 0; j < TPS; ++j) {
-                    if (j >= n) break;
-                    uint32_t v[32];  // TMEM column c of this row holds k = 4c .. 4c + 3
-#pragma unroll
-                    for (uint32_t q = 0; q < 4; ++q) {
-                        const uint32_t ww[4] = {w[j][q].x, w[j][q].y, w[j][q].z, w[j][q].w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            v[4 * q + e] = ww[e] & 0xF0F0F0F0u;               // k = 16q + 4e ..
-                            v[16 + 4 * q + e] = (ww[e] & 0x0F0F0F0Fu) * 16u;  // k = 64 + 16q + 4e ..
+                            for (uint32_t q = 0; q < 4; ++q)
+                                w[jj][q] = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
                         }
-                    }
-                    const int slot = ap * TPS + j;
-                    if (!(dbg_ & 8)) {
-                        // k-steps [0, KT): TMEM columns (4 codes each); [KT, 4): smem chunks
-                        if constexpr (GG::KT == 4) tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + slot * 32), v);
-                        if constexpr (GG::KT == 2) tmem_st16(tmem + lane_base + uint32_t(GG::A_COL + slot * 16), v);
-                        if constexpr (GG::KT == 1) tmem_st8(tmem + lane_base + uint32_t(GG::A_COL + slot * 8), v);
-                        if constexpr (GG::KT < 4) {
-                            uint8_t* arow = smem + GG::A_OFF + slot * GG::A_SMEM + row * 128;
+                    float scv[JP];
 #pragma unroll
-                            for (int qc = 2 * GG::KT; qc < 8; ++qc)
-                                *reinterpret_cast<uint4*>(arow + ((uint32_t(qc) ^ uint32_t(row & 7)) << 4)) =
-                                    make_uint4(v[4 * qc], v[4 * qc + 1], v[4 * qc + 2], v[4 * qc + 3]);
-                        }
-                    } else if (v[0] == 0x12345u) {
-                        g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
+                    for (int jj = 0; jj < JP; ++jj) {
+                        const uint16_t* sc =
+                            reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + (j0 + jj) * r8;
+                        scv[jj] = (j0 + jj < n && row < r8) ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
                     }
-                    sring[(np * TPS + j) * kRows + row] = scv[j];
+#pragma unroll
+                    for (int jj = 0; jj < JP; ++jj) {
+                        const int j = j0 + jj;
+                        if (j >= n) break;
+                        uint32_t v[32];  // TMEM column c of this row holds k = 4c .. 4c + 3
+#pragma unroll
+                        for (uint32_t q = 0; q < 4; ++q) {
+                            const uint32_t ww[4] = {w[jj][q].x, w[jj][q].y, w[jj][q].z, w[jj][q].w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                v[4 * q + e] = ww[e] & 0xF0F0F0F0u;               // k = 16q + 4e ..
+                                v[16 + 4 * q + e] = (ww[e] & 0x0F0F0F0Fu) * 16u;  // k = 64 + 16q + 4e ..
+                            }
+                        }
+                        const int slot = ap * TPS + j;
+                        static_assert(GG::KT == 4, "A operand entirely from TMEM");
+                        if (!(dbg_ & 8)) {
+                            tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + slot * 32), v);
+                        } else if (v[0] == 0x12345u) {
+                            g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
+                        }
+                        sring[(np * TPS + j) * kRows + row] = scv[jj];
+                    }
                 }
             }
             if constexpr (GG::KT > 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -356,6 +395,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
+            if (warp == kExp0) I4_TL(si, 3);
             if (dbg_ & 32) x_work += clock64() - _tw;
             cu.advance(n);
             ++si;
@@ -386,43 +426,40 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 mbar_wait(&full[s], ph);  // the planes of this stage
                 I4_ACC(m_full);
             }
+            I4_TL(si, 8);
             if ((dbg_ & 64) && si == 0 && lane == 0) g_i4_dbg[c * 16 + 6] = gtime();
             {
                 I4_T0();
                 mbar_wait(&afull[ap], uint32_t(si / AP) & 1u);
                 I4_ACC(m_afull);
             }
+            I4_TL(si, 9);
             {
                 I4_T0();
                 if (si >= NP) mbar_wait(&tfree[np], uint32_t(si / NP - 1) & 1u);
                 I4_ACC(m_tfree);
             }
             fence_after();
+            I4_TL(si, 4);
             const long long _ti = (dbg_ & 32) ? clock64() : 0;
             const uint32_t stage_lo = base + uint32_t(s * GG::STAGE_BYTES >> 4);
-            // one elected thread issues the stage's MMAs back to back and their commits
-            if (elect_leader()) {
-                if (!(dbg_ & 4)) {
-                    for (int j = 0; j < n; ++j) {
-                        const int slot = ap * TPS + j;
-                        const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
-                        const uint32_t alo = base + uint32_t((GG::A_OFF + slot * GG::A_SMEM) >> 4);
-                        const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
-                        const uint32_t d = tmem + uint32_t((np * TPS + j) * DN);
-#pragma unroll
-                        for (uint32_t k = 0; k < 4; ++k) {  // K = 32 per MMA: TMEM +8 columns, smem +32 bytes
-                            if (int(k) < GG::KT)
-                                mma_i8_ts(d, a + 8 * k, kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
-                            else
-                                mma_i8(d, kHi | (alo + 2 * k), kHi | (blo + 2 * k), idesc, k ? 1u : 0u);
-                        }
-                    }
+            // the whole warp issues the stage's MMAs (one elected lane, warp-uniform asm blocks of
+            // a group's 4 k-steps) and their commits
+            static_assert(GG::KT == 4, "A operand entirely from TMEM");
+            if (!(dbg_ & 4)) {
+                for (int j = 0; j < n; ++j) {
+                    const int slot = ap * TPS + j;
+                    const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
+                    const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
+                    mma4_i8_ts_warp(tmem + uint32_t((np * TPS + j) * DN), a, kHi | blo, idesc, 0u);
                 }
-                commit(&aempty[ap]);
-                commit(&tfull[np]);
-                commit(&empty[s]);
             }
+            I4_TL(si, 1);
+            commit_elect(&aempty[ap]);
+            commit_elect(&tfull[np]);
+            commit_elect(&empty[s]);
             __syncwarp();
+            I4_TL(si, 5);
             if (dbg_ & 32) m_issue += clock64() - _ti;
             cu.advance(n);
             ++si;
@@ -442,7 +479,8 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
         float* scr = reinterpret_cast<float*>(smem + GG::SCR_OFF);
         __shared__ float pow_s[NT];  // 2^s per token, 0 for padding tokens
         if (eg == 0) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");  // texp comes from the planes kernel
+            if (p.own.a) mbar_wait(pready, 0);  // texp published by this launch
+            else asm volatile("griddepcontrol.wait;" ::: "memory");  // texp from the planes producer
             for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
             asm volatile("bar.sync 1, 128;" ::: "memory");
         }
@@ -465,8 +503,9 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 I4_ACC(e_wait);
             }
             const long long _tw = (dbg_ & 32) ? clock64() : 0;
+            if (warp == kEpi0) I4_TL(si, 6);
             fence_after();
-            float scg[TPS];
+            float scg[TPS], sg2 = 0.0f;
 #pragma unroll
             for (int j = 0; j < TPS; ++j) scg[j] = j < n ? sring[(np * TPS + j) * kRows + row] : 0.0f;
             // this warpgroup's groups of the stage: [j0, j1)
@@ -480,31 +519,33 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 // chunk jj of every group of the stage; group j + 1's TMEM loads are in flight
                 // while group j's accumulators are combined
                 // one warpgroup per group (EW == 2) keeps one group's registers only
-                uint32_t d[EW == 2 ? 1 : TPS][PT >= 16 ? 3 : 1][LDC];
+                // double-buffered: group j + 1's TMEM loads are in flight while group j is combined
+                constexpr int NB = EW == 2 ? 1 : (TPS < 2 ? 1 : 2);
+                uint32_t d[NB][PT >= 16 ? 3 : 1][LDC];
                 auto load = [&](int j) {
                     const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
+                    const int bj = j % NB;
                     if (!(dbg_ & 16)) {
                         if constexpr (PT >= 16) {
-                            ld16(ta, d[EW == 2 ? 0 : j][0]);
-                            ld16(ta + PT, d[EW == 2 ? 0 : j][1]);
-                            ld16(ta + 2 * PT, d[EW == 2 ? 0 : j][2]);
+                            ld16(ta, d[bj][0]);
+                            ld16(ta + PT, d[bj][1]);
+                            ld16(ta + 2 * PT, d[bj][2]);
                         } else {
 #pragma unroll
-                            for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, d[EW == 2 ? 0 : j][0] + 16 * h);
+                            for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, d[bj][0] + 16 * h);
                         }
                     } else {
 #pragma unroll
                         for (int e = 0; e < LDC; ++e)
 #pragma unroll
-                            for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[EW == 2 ? 0 : j][q3][e] = uint32_t(row + e);
+                            for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[bj][q3][e] = uint32_t(row + e);
                     }
                 };
                 auto combine = [&](int j) {
 #pragma unroll
                     for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
-                        // |D| < 2^21 per group: int -> float as (bits(D + 1.5 * 2^23) - 1.5 * 2^23)
                         uint32_t u0v, u1v, u2v;
-                        const int dj = EW == 2 ? 0 : j;
+                        const int dj = j % NB;
                         if constexpr (PT >= 16) {
                             u0v = d[dj][0][e], u1v = d[dj][PT >= 16 ? 1 : 0][e], u2v = d[dj][PT >= 16 ? 2 : 0][e];
                         } else {
@@ -515,10 +556,21 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                         // D0 after the 2^-14 weight
                         const float x0 = float(int32_t(u0v));
                         const float x12 = float(int32_t(u1v) * 128 + int32_t(u2v));
-                        acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), scg[j], acc[jj + e]);
+                        acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), EW == 2 ? sg2 : scg[j], acc[jj + e]);
                     }
                 };
-                if (j0 < j1) {
+                if constexpr (EW == 2) {
+                    // warpgroup eg takes the stage's groups eg, eg + 2, ... (compile-time local index)
+#pragma unroll
+                    for (int jl = 0; jl < (TPS + 1) / 2; ++jl) {
+                        const int j = 2 * jl + eg;
+                        if (j >= n) break;
+                        sg2 = sring[(np * TPS + j) * kRows + row];
+                        load(j);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        combine(j);
+                    }
+                } else if (j0 < j1) {
                     load(j0);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     if (dbg_ & 32) {
@@ -537,6 +589,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tfree[np]);
+            if (warp == kEpi0) I4_TL(si, 7);
             if (dbg_ & 32) e_work += clock64() - _tw;
             ++si;
             if (seg_end && EW == 2) {  // warpgroup B -> A through shared memory
@@ -732,6 +785,11 @@ cudaError_t launch_nt(Params p, cudaStream_t st) {
 
 constexpr size_t kI4Counters = 64 * 1024;
 
+extern "C" int rtnq_i4_timeline_read(void* host, size_t bytes) {
+    if (bytes > sizeof(i4::g_i4_tl)) bytes = sizeof(i4::g_i4_tl);
+    return cudaMemcpyFromSymbol(host, i4::g_i4_tl, bytes) == cudaSuccess ? 0 : 1;
+}
+
 extern "C" int rtnq_i4_debug_read(void* host, size_t bytes) {
     if (bytes > sizeof(i4::g_i4_dbg)) bytes = sizeof(i4::g_i4_dbg);
     return cudaMemcpyFromSymbol(host, i4::g_i4_dbg, bytes) == cudaSuccess ? 0 : 1;
@@ -802,7 +860,29 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         pf.bytes = int64_t(nb) * kb * 8192;
         pf.head = 64 * 1024;
     }
-    if (own_planes) {
+    // planes inside the GEMM (default) or by the stand-alone planes kernel (RTNQ_PLANES_KERNEL=1,
+    // or unaligned activations)
+    static const bool planes_kernel = [] {
+        const char* e = std::getenv("RTNQ_PLANES_KERNEL");
+        return e && std::atoi(e) != 0;
+    }();
+    // (a handful of tokens: one producing CTA per token is a longer critical path than the
+    // stand-alone kernel's token x slice grid; measured crossover between 1 and 16 tokens)
+    // (and a small weight: its few stages per CTA cannot hide the producing CTAs' critical path;
+    // scratch/shapes_seq.py, batch 16: qkv / o 10.3 / 9.1 us with the planes kernel, 11.8 / 10.4
+    // in the GEMM; gate_up / down 23.7 / 19.4 vs 21.7 / 18.5)
+    const int64_t units = ((A.n + i4::kRows - 1) / i4::kRows) * ((A.k + i4::kKB - 1) / i4::kKB);
+    const bool in_gemm = own_planes && !planes_kernel && A.m >= imma::kOwnPlanesMinM && units >= 2048 &&
+                         (reinterpret_cast<uintptr_t>(A.a) & 15) == 0 && !(dbg & 64);
+    if (in_gemm) {
+        p.own.a = A.a;
+        p.own.a_dtype = A.a_dtype;
+        p.own.done = p.counters + (kI4Counters / sizeof(int) - 2);
+        p.own.consumed = p.counters + (kI4Counters / sizeof(int) - 1);
+        p.own.err = A.err;
+        p.planes_w = planes;
+    }
+    if (own_planes && !in_gemm) {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? imma::launch_planes<RTNQ_BF16, true> : imma::launch_planes<RTNQ_BF16, false>)(

@@ -54,6 +54,8 @@ struct Params {
     int pf;     // L2 prefetch distance in tiles (0 = off)
     int direct;  // cluster split-K: peers push into a dedicated smem region (no go handshake)
     int debug;  // profiling: 4 = no MMA issued, 2 = no loads (arrive only)
+    imma::OwnPlanes own;  // own.a != nullptr: this launch computes its tokens' planes itself
+    int8_t* planes_w;     // ... into this [3][Mtot][K] buffer (the TMA source), exponents into texp
 };
 
 template <int NT>
@@ -101,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     uint64_t* go = dempty + 2;      // cluster split-K: the leader is ready for partials
     uint64_t* rfull = dempty + 3;   // cluster split-K: all partials landed in the leader
     uint64_t* pub = dempty + 4;     // stream-K contributor partials stored (4 warps)
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 5);
+    uint64_t* pready = dempty + 5;  // own planes: this launch's planes / exponents published
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 6);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = blockIdx.x;
     if ((dbg_ & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 5] = gtime();
 
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
         for (int i = 0; i < 2; ++i) mbar_init(&dfull[i], 1), mbar_init(&dempty[i], 4);
-        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4);
+        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4), mbar_init(pready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -132,6 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     if (p.csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const uint32_t tmem = *tslot;
     asm volatile("griddepcontrol.launch_dependents;");
+    if (p.own.a && warp >= kEpi0) {  // the epilogue warps compute this CTA's share of the planes
+        __shared__ float pred[4];
+        own_planes_produce(p.own, int(p.K), p.m0, p.M, p.Mtot, c, int(gridDim.x), p.planes_w,
+                           const_cast<int32_t*>(p.texp), threadIdx.x - kEpi0 * 32, 128, 3, pred);
+    }
 
     // units: runs of <= SPAN k-blocks inside one row-block and one SPAN-aligned k-range
     auto chunk = [&](int u, int kb) {
@@ -154,7 +162,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
         const int64_t kt = (p.KBLK + 1) >> 1;
         const int64_t t_last = u1 > u0 ? int64_t((u1 - 1) / p.KBLK) * kt + ((u1 - 1) % p.KBLK >> 1) : -1;
         int64_t pf_next = int64_t(cu.b) * kt + (cu.kb >> 1);
-        if (!codes) asm volatile("griddepcontrol.wait;" ::: "memory");  // planes come from the previous kernel
+        if (!codes) {
+            if (p.own.a) {  // planes computed by this launch's CTAs
+                own_planes_acquire(p.own, p.M, int(gridDim.x));
+                if (lane == 0) mbar_arrive(pready);
+            } else {
+                asm volatile("griddepcontrol.wait;" ::: "memory");  // planes from the previous kernel
+            }
+        }
         for (int i = 0; cu.more(); ++i) {
             const int n = cu.chunk();
             if (i >= STAGES) {
@@ -232,22 +247,20 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
             const uint32_t d = tmem + db * DN;
             // one elected thread issues the stage's MMAs back to back and their commits;
             // k-block kb: tile slot (kb >> 1) % TPS, second 64-code half at +64 B
-            if (elect_leader()) {
-                if (!(dbg_ & 4)) {
-                    for (int j = 0; j < n; ++j) {
-                        const int kb = cu.kb + j;
-                        const uint32_t alo = lo + uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::CODE_BYTES >> 4)) +
-                                             ((kb & 1) ? 4u : 0u);
-                        const uint32_t blo = lo + uint32_t(GG::PLANE_OFF >> 4) +
-                                             uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::PLANE_BYTES >> 4)) +
-                                             ((kb & 1) ? 4u : 0u);
-                        mma_i8(d, kHi | alo, kHi | blo, idesc, (first && j == 0) ? 0u : 1u);
-                        mma_i8(d, kHi | (alo + 2), kHi | (blo + 2), idesc, 1u);
-                    }
+            // the whole warp issues (one elected lane, warp-uniform asm blocks; int8_mma.cuh)
+            if (!(dbg_ & 4)) {
+                for (int j = 0; j < n; ++j) {
+                    const int kb = cu.kb + j;
+                    const uint32_t alo = lo + uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::CODE_BYTES >> 4)) +
+                                         ((kb & 1) ? 4u : 0u);
+                    const uint32_t blo = lo + uint32_t(GG::PLANE_OFF >> 4) +
+                                         uint32_t(((kb >> 1) & (GG::TPS - 1)) * (GG::PLANE_BYTES >> 4)) +
+                                         ((kb & 1) ? 4u : 0u);
+                    mma2_i8_ss_warp(d, kHi | alo, kHi | blo, idesc, (first && j == 0) ? 0u : 1u);
                 }
-                commit(&empty[s]);
-                if (seg_end) commit(&dfull[db]);
             }
+            commit_elect(&empty[s]);
+            if (seg_end) commit_elect(&dfull[db]);
             __syncwarp();
             first = false;
             ti += clock64() - a1;
@@ -272,7 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         int db = 0, seg = 0, u = u0;
         __shared__ float pow_s[NT];  // 2^s per token (s >= -126: a normal float)
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // texp comes from the planes kernel
+        if (p.own.a) mbar_wait(pready, 0);  // texp published by this launch
+        else asm volatile("griddepcontrol.wait;" ::: "memory");  // texp from the planes producer
         for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         while (u < u1) {
@@ -590,7 +604,24 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
         pf.bytes = int64_t(nb) * ((kb + 1) >> 1) * 16384;
         pf.head = 64 * 1024;
     }
-    if (own_planes) {
+    // measured slower for W8 than the stand-alone planes kernel (scratch/seq8.py: 25.5 vs 23.5 us
+    // per ffn_up launch at batch 16; the W8 CTA has only its 4 epilogue warps to spare), so
+    // opt-in: RTNQ_I8_OWN_PLANES=1
+    static const bool planes_kernel = [] {
+        const char* e = std::getenv("RTNQ_I8_OWN_PLANES");
+        return !(e && std::atoi(e) != 0);
+    }();
+    const bool in_gemm = own_planes && !planes_kernel && A.m >= imma::kOwnPlanesMinM &&
+                         (reinterpret_cast<uintptr_t>(A.a) & 15) == 0 && !(dbg & 64);
+    if (in_gemm) {  // planes inside the GEMM (int8_mma.cuh, OwnPlanes)
+        p.own.a = A.a;
+        p.own.a_dtype = A.a_dtype;
+        p.own.done = p.counters + (kI8Counters / sizeof(int) - 2);
+        p.own.consumed = p.counters + (kI8Counters / sizeof(int) - 1);
+        p.own.err = A.err;
+        p.planes_w = planes;
+    }
+    if (own_planes && !in_gemm) {
         const bool vec = (reinterpret_cast<uintptr_t>(A.a) & 15) == 0;
         cudaError_t e = A.a_dtype == RTNQ_BF16
             ? (vec ? i8::launch_planes<RTNQ_BF16, true> : i8::launch_planes<RTNQ_BF16, false>)(
