@@ -224,6 +224,15 @@ rtnq_status rtnq_dev_decode_attention(const void* qkv, void* k_cache, void* v_ca
                                       int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                       int64_t max_len, int64_t pos, float rope_theta,
                                       void* stream);
+/* The same with the split-context merge scratch (self-resetting counters + partials) from a
+ * caller workspace of rtnq_dev_decode_attention_workspace_bytes(batch, hq, hkv, max_len) bytes,
+ * zero-initialized once and reused per stream; rtnq_dev_decode_attention uses a per-device
+ * buffer instead (one stream at a time). */
+size_t rtnq_dev_decode_attention_workspace_bytes(int64_t batch, int64_t hq, int64_t hkv, int64_t max_len);
+rtnq_status rtnq_dev_decode_attention_ws(const void* qkv, void* k_cache, void* v_cache, void* out,
+                                         int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                         int64_t max_len, int64_t pos, float rope_theta, void* ws,
+                                         size_t ws_bytes, void* stream);
 /* Synchronizes `stream`, reads and clears *err_flag (device), returns
  * RTNQ_E_INVALID_INPUT if it was set. */
 rtnq_status rtnq_dev_check_flag(int32_t* err_flag, void* stream);

@@ -112,6 +112,10 @@ def lib():
                                          _i32, _i32, _p, _i32, _p, _sz, _p, C.c_uint]
     L.rtnq_dev_decode_attention.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
                                             C.c_float, _p]
+    L.rtnq_dev_decode_attention_workspace_bytes.restype = _sz
+    L.rtnq_dev_decode_attention_workspace_bytes.argtypes = [_i64, _i64, _i64, _i64]
+    L.rtnq_dev_decode_attention_ws.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
+                                               C.c_float, _p, _sz, _p]
     L.rtnq_f32_to_f16.argtypes = [_p, _i64, _p]
     L.rtnq_f16_to_f32.argtypes = [_p, _i64, _p]
     L.rtnq_plan_resolve.argtypes = [C.c_char_p, _i64, _p, C.c_char_p, _i64, _p]
@@ -453,12 +457,17 @@ def linear_planes(planes: Planes, qw: QuantWeight, out, *, workspace: Workspace 
 
 
 def decode_attention(qkv, k_cache, v_cache, out, hq, hkv, pos, head_dim=128, theta=500000.0,
-                     stream=None):
-    """GQA decode attention with RoPE over a KV cache (rtnq_dev_decode_attention)."""
+                     stream=None, workspace: Workspace | None = None):
+    """GQA decode attention with RoPE over a KV cache (rtnq_dev_decode_attention_ws).  The split
+    merge scratch comes from ``workspace`` (one per stream; the default per (device, stream))."""
     batch, max_len = k_cache.shape[0], k_cache.shape[1]
-    _check(lib().rtnq_dev_decode_attention(_ptr(qkv), _ptr(k_cache), _ptr(v_cache), _ptr(out),
-                                           batch, hq, hkv, head_dim, max_len, pos, theta,
-                                           _stream(stream)))
+    wsb = lib().rtnq_dev_decode_attention_workspace_bytes(batch, hq, hkv, max_len)
+    if workspace is None:
+        workspace = _default_workspace(qkv.device, stream, wsb)
+    buf = workspace.ensure(wsb)
+    _check(lib().rtnq_dev_decode_attention_ws(_ptr(qkv), _ptr(k_cache), _ptr(v_cache), _ptr(out),
+                                              batch, hq, hkv, head_dim, max_len, pos, theta,
+                                              _ptr(buf), buf.numel(), _stream(stream)))
     return out
 
 

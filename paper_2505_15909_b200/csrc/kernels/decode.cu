@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "int8_mma.cuh"
 #include "kernels.cuh"
@@ -97,6 +98,211 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfl
     }
 }
 
+// ---- register-resident row kernels (one CTA per token row; every element loaded once) -------
+// The row stays in registers (VPT 16-byte vectors per thread) across the passes: sum of squares
+// (or max) -> scale -> output -> activation planes of the output, so a row costs one DRAM round
+// trip plus two block reductions instead of a load per pass.
+constexpr int kRowThreads = 256;
+
+// Sum (or max) over the CL CTAs of a row's thread-block cluster: block reduction, then every CTA
+// reads the CL partials over DSMEM in rank order (deterministic, identical in every CTA).
+template <int CL>
+__device__ __forceinline__ float row_reduce(float v, float* red, float* cpart, bool is_max) {
+    v = is_max ? warp_max(v) : warp_sum(v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();  // red / cpart are reused across calls
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float r = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kRowThreads / 32; ++i) r = is_max ? fmaxf(r, red[i]) : r + red[i];
+    if constexpr (CL == 1) return r;
+    if (threadIdx.x == 0) *cpart = r;
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const uint32_t my = static_cast<uint32_t>(__cvta_generic_to_shared(cpart));
+    float t = 0.0f;
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+        uint32_t ra;
+        float x;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my), "r"(q));
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra));
+        t = is_max ? fmaxf(t, x) : t + x;
+    }
+    // the peers' cpart may be rewritten by the next reduction only after every CTA has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    return t;
+}
+
+// vector v of this thread: CTA `rank` of the row's CL takes vectors rank * 256 + tid + v * 256 * CL
+template <int CL>
+__device__ __forceinline__ int row_vec(int rank, int v) { return rank * kRowThreads + threadIdx.x + v * kRowThreads * CL; }
+
+// planes of a bf16 row held as VPT vectors per thread (row_to_planes' arithmetic, bit-identical)
+template <int VPT, int CL>
+__device__ __forceinline__ void planes_from_regs(const uint4 (&ov)[VPT], int n8, int rank, int t, int M, int K,
+                                                 int8_t* __restrict__ planes, int32_t* __restrict__ texp,
+                                                 float* red, float* cpart) {
+    auto cvt = [](uint32_t h) -> float { return __uint_as_float(h << 16); };
+    float mx = 0.0f;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        if (row_vec<CL>(rank, v) >= n8) break;
+        const uint32_t w[4] = {ov[v].x, ov[v].y, ov[v].z, ov[v].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mx = fmaxf(mx, fmaxf(fabsf(cvt(w[i] & 0xffffu)), fabsf(cvt(w[i] >> 16))));
+    }
+    const float amax = row_reduce<CL>(mx, red, cpart, true);
+    int e = 0;
+    if (amax > 0.0f) frexpf(amax, &e);
+    const int s = max(e - 6, -126);
+    if (threadIdx.x == 0 && rank == 0) texp[t] = s;
+    const float inv = __int_as_float((127 - s) << 23);
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        const int vi = row_vec<CL>(rank, v);
+        if (vi >= n8) break;
+        const uint32_t w[4] = {ov[v].x, ov[v].y, ov[v].z, ov[v].w};
+        uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float y = cvt(i & 1 ? w[i >> 1] >> 16 : w[i >> 1] & 0xffffu) * inv;
+            const float b0 = y + 12582912.0f, r0 = b0 - 12582912.0f;
+            const float y1 = (y - r0) * 128.0f;
+            const float b1 = y1 + 12582912.0f, r1 = b1 - 12582912.0f;
+            const float b2 = (y1 - r1) * 128.0f + 12582912.0f;
+            pk[0][i >> 2] |= (uint32_t(__float_as_int(b0) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+            pk[1][i >> 2] |= (uint32_t(__float_as_int(b1) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+            pk[2][i >> 2] |= (uint32_t(__float_as_int(b2) - 0x4B400000) & 0xffu) << (8 * (i & 3));
+        }
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+            *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(vi) * 8) =
+                make_uint2(pk[pl][0], pk[pl][1]);
+    }
+}
+
+// grid (m * CL): a thread-block cluster of CL CTAs per token row
+template <int VPT, int CL>
+__global__ void __launch_bounds__(kRowThreads) add_rmsnorm_rows_kernel(
+    __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta, const __nv_bfloat16* __restrict__ w,
+    __nv_bfloat16* __restrict__ out, int h, float eps, int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
+    pdl_prologue();
+    __shared__ float red[kRowThreads / 32];
+    __shared__ float cpart;
+    const int row = blockIdx.x / CL, rank = blockIdx.x % CL, n8 = h / 8;
+    __nv_bfloat16* xr = x + int64_t(row) * h;
+    const __nv_bfloat16* dr = delta ? delta + int64_t(row) * h : nullptr;
+    uint4 xv[VPT], dv[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {  // every load of the row in flight at once
+        const int vi = row_vec<CL>(rank, v);
+        if (vi < n8) {
+            xv[v] = *reinterpret_cast<const uint4*>(xr + vi * 8);
+            if (dr) dv[v] = *reinterpret_cast<const uint4*>(dr + vi * 8);
+        }
+    }
+    float ss = 0.0f;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        const int vi = row_vec<CL>(rank, v);
+        if (vi >= n8) break;
+        __nv_bfloat162* xp = reinterpret_cast<__nv_bfloat162*>(&xv[v]);
+        if (dr) {
+            const __nv_bfloat162* dp = reinterpret_cast<const __nv_bfloat162*>(&dv[v]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 a = __bfloat1622float2(xp[j]), b = __bfloat1622float2(dp[j]);
+                xp[j] = __floats2bfloat162_rn(a.x + b.x, a.y + b.y);
+            }
+            *reinterpret_cast<uint4*>(xr + vi * 8) = xv[v];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 a = __bfloat1622float2(xp[j]);
+            ss += a.x * a.x + a.y * a.y;
+        }
+    }
+    const float inv = rsqrtf(row_reduce<CL>(ss, red, &cpart, false) / float(h) + eps);
+    uint4 ov[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        const int vi = row_vec<CL>(rank, v);
+        if (vi >= n8) break;
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(w + vi * 8));
+        const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&xv[v]);
+        const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&wv);
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&ov[v]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 a = __bfloat1622float2(xp[j]), b = __bfloat1622float2(wp[j]);
+            op[j] = __floats2bfloat162_rn(a.x * inv * b.x, a.y * inv * b.y);
+        }
+        *reinterpret_cast<uint4*>(out + int64_t(row) * h + vi * 8) = ov[v];
+    }
+    if (planes) planes_from_regs<VPT, CL>(ov, n8, rank, row, gridDim.x / CL, h, planes, texp, red, &cpart);
+}
+
+template <int VPT, int CL>
+__global__ void __launch_bounds__(kRowThreads) silu_mul_rows_kernel(const __nv_bfloat16* __restrict__ gu,
+                                                                    __nv_bfloat16* __restrict__ act, int f,
+                                                                    int8_t* __restrict__ planes,
+                                                                    int32_t* __restrict__ texp) {
+    pdl_prologue();
+    __shared__ float red[kRowThreads / 32];
+    __shared__ float cpart;
+    const int t = blockIdx.x / CL, rank = blockIdx.x % CL, n8 = f / 8;
+    const __nv_bfloat16* gr = gu + int64_t(t) * 2 * f;
+    uint4 gv[VPT], uv[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        const int vi = row_vec<CL>(rank, v);
+        if (vi < n8) {
+            gv[v] = *reinterpret_cast<const uint4*>(gr + vi * 8);
+            uv[v] = *reinterpret_cast<const uint4*>(gr + f + vi * 8);
+        }
+    }
+    uint4 ov[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        const int vi = row_vec<CL>(rank, v);
+        if (vi >= n8) break;
+        const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gv[v]);
+        const __nv_bfloat162* up = reinterpret_cast<const __nv_bfloat162*>(&uv[v]);
+        __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(&ov[v]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 g = __bfloat1622float2(gp[q]), u = __bfloat1622float2(up[q]);
+            op[q] = __floats2bfloat162_rn(g.x / (1.0f + __expf(-g.x)) * u.x, g.y / (1.0f + __expf(-g.y)) * u.y);
+        }
+        *reinterpret_cast<uint4*>(act + int64_t(t) * f + vi * 8) = ov[v];
+    }
+    if (planes) planes_from_regs<VPT, CL>(ov, n8, rank, t, gridDim.x / CL, f, planes, texp, red, &cpart);
+}
+
+// cluster-launched row kernel: cluster of CL CTAs per row, VPT vectors per thread
+template <typename... KArgs, typename... Args>
+cudaError_t launch_rows(void (*kern)(KArgs...), int64_t m, int cl, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(m * cl));
+    cfg.blockDim = dim3(kRowThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = unsigned(cl);
+    attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = cl > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// CTAs per row (cluster size): enough that ~all SMs share the rows, at most 8 (portable)
+static int row_cluster(int64_t m, int64_t n8) {
+    int cl = 1;
+    while (cl < 8 && m * cl * 2 <= 148 && n8 > 2 * int64_t(cl) * kRowThreads) cl *= 2;
+    return cl;
+}
+
 // One CTA per token: the SiLU*up row, then its activation planes (row_to_planes).
 __global__ void silu_mul_planes_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
                                        int f, int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
@@ -160,30 +366,34 @@ __device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, 
 // qkv row layout: [Hq*D | Hkv*D | Hkv*D] (the column-split QKV output of one rank).
 // cache layout: [B][Lmax][Hkv][D] for K and for V.  One CTA = G warps (G = Hq/Hkv <= 32);
 // warp w owns query head kvh * G + w; head_dim D = 128.
-// Flash-decoding split across CTAs: grid (Hkv, B, ceil((pos + 1) / kChunk)).  A CTA stages its
-// chunk's K and V rows in shared memory (16-byte loads, all in flight; rows padded to 65 words
-// so a lane-per-row walk is bank-conflict free); each warp scores its positions lane-parallel,
+// Flash-decoding split across CTAs: grid (Hkv, B, nsp), nsp chosen so the grid is ~2 waves of the
+// SMs and the context splits evenly (launch_decode_attention).  A CTA stages its chunk's K and V
+// rows in shared memory with cp.async (every 16-byte load in flight at once; 256-byte rows whose
+// 16-byte chunks are XOR-swizzled by the row, so a lane-per-row walk of 16-byte chunks and a
+// row-per-warp walk are both bank-conflict free); each warp scores its positions lane-parallel,
 // exponentiates against the chunk max and accumulates P*V (lanes own 4 head dims, 4 chains),
-// writing a (max, sum, P*V) partial; the last CTA of a (token, KV head) to finish merges them:
+// writing a (max, sum, P*V) partial; the splits merge over DSMEM inside a thread-block cluster
+// (nsp <= 8) or through the caller's workspace (the last CTA to arrive):
 // out = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s.
 constexpr int kD = 128;
-constexpr int kChunk = 64;  // positions per CTA (split-context)
-constexpr int kRowW = kD / 2 + 1;  // 32-bit words per staged row (64 + 1 pad)
-constexpr int kPart = kD + 4;      // floats per split partial: max, sum, 2 pad, P*V (16-B aligned)
+constexpr int kMaxChunk = 256;  // positions per CTA at most (smem)
+constexpr int kPart = kD + 4;   // floats per split partial: max, sum, 2 pad, P*V (16-B aligned)
+
+__device__ __forceinline__ uint32_t swz(int t, int c) { return uint32_t(t * 16 + (c ^ (t & 15))); }  // 16-B chunk
 
 __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                         float* __restrict__ part, int hq, int hkv, int lmax,
                                         int pos, float theta, __nv_bfloat16* __restrict__ out,
-                                        int* __restrict__ arrivals, int cluster_merge) {
+                                        int* __restrict__ arrivals, int cluster_merge, int chunk) {
     // grid (hkv, batch, split): this CTA covers positions [t0, t0 + n) of one KV head and its
     // G query heads (a warp each) and writes the split's (max, sum, unnormalised P.V) partial
     pdl_prologue();
-    extern __shared__ uint32_t sm[];
-    uint32_t* ks = sm;                       // [kChunk][kRowW] bf16x2
-    uint32_t* vs = ks + kChunk * kRowW;      // [kChunk][kRowW]
-    float* qs = reinterpret_cast<float*>(vs + kChunk * kRowW);  // [G][kD] rotated queries
-    float* ps = qs + (blockDim.x / 32) * kD;                     // [G][kChunk] probabilities
+    extern __shared__ uint4 smq[];
+    uint4* ks = smq;                          // [chunk][16] swizzled 16-byte chunks
+    uint4* vs = ks + chunk * 16;              // [chunk][16]
+    float* qs = reinterpret_cast<float*>(vs + chunk * 16);  // [G][kD] rotated, scaled queries
+    float* ps = qs + (blockDim.x / 32) * kD;                // [G][chunk] probabilities
     const int b = blockIdx.y, kvh = blockIdx.x, sp = blockIdx.z, nsp = gridDim.z, G = hq / hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
     const int64_t row = int64_t(b) * (hq + 2 * hkv) * kD;
@@ -192,7 +402,7 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     const int64_t cstride = int64_t(hkv) * kD;  // between positions
     __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
-    const int t0 = sp * kChunk, n = min(kChunk, pos + 1 - t0);
+    const int t0 = sp * chunk, n = min(chunk, pos + 1 - t0);
     // RoPE angles of position `pos`, computed once per CTA (accurate sincosf: the angles reach
     // thousands of radians at the low frequencies) and shared by the key and every query head
     __shared__ float2 cs_s[kD / 2];
@@ -231,50 +441,43 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
         qs[warp * kD + d + kD / 2] = r.y * scale;
     }
     __threadfence_block();
-    __syncthreads();  // the appended row is visible to the staging loads below
-    // stage K and V rows [t0, t0 + n): 16 chunks of 16 B per row.  Every load of a batch is
-    // issued before any of its shared-memory stores, so a thread has kBatch loads in flight
-    // instead of one DRAM round trip per chunk.
-    constexpr int kBatch = 8;
-    for (int base = 0; base < n * 16; base += kBatch * nthr) {
-        uint4 kv[kBatch], vv[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            const int i = base + u * nthr + threadIdx.x;
-            if (i < n * 16) {
-                const int t = i >> 4, c = i & 15;
-                kv[u] = __ldg(reinterpret_cast<const uint4*>(kcb + int64_t(t0 + t) * cstride + c * 8));
-                vv[u] = __ldg(reinterpret_cast<const uint4*>(vcb + int64_t(t0 + t) * cstride + c * 8));
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            const int i = base + u * nthr + threadIdx.x;
-            if (i < n * 16) {
-                const int t = i >> 4, c = i & 15;
-                uint32_t* kd = ks + t * kRowW + c * 4;
-                uint32_t* vd = vs + t * kRowW + c * 4;
-                kd[0] = kv[u].x, kd[1] = kv[u].y, kd[2] = kv[u].z, kd[3] = kv[u].w;
-                vd[0] = vv[u].x, vd[1] = vv[u].y, vd[2] = vv[u].z, vd[3] = vv[u].w;
-            }
-        }
+    __syncthreads();  // the appended row is written before the staging copies below read it
+    // stage K and V rows [t0, t0 + n): cp.async.cg (L2, coherent with the row appended above),
+    // every copy in flight before one wait
+    for (int i = threadIdx.x; i < n * 16; i += nthr) {
+        const int t = i >> 4, c = i & 15;
+        const uint32_t kd = static_cast<uint32_t>(__cvta_generic_to_shared(ks + swz(t, c)));
+        const uint32_t vd = static_cast<uint32_t>(__cvta_generic_to_shared(vs + swz(t, c)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(kd), "l"(kcb + int64_t(t0 + t) * cstride + c * 8)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vd), "l"(vcb + int64_t(t0 + t) * cstride + c * 8)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const float* qw = qs + warp * kD;
-    float* pw = ps + warp * kChunk;
-    // scores: lane owns positions t = lane + 32 j
+    float* pw = ps + warp * chunk;
+    // scores: lane owns positions t = lane + 32 j, reads its row 16 bytes (8 dims) at a time
     float cmax = -INFINITY;
     for (int t = lane; t < n; t += 32) {
-        const uint32_t* kr = ks + t * kRowW;
         float sa[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four independent FMA chains
-#pragma unroll 8
-        for (int w2 = 0; w2 < kD / 2; w2 += 2) {
-            const float2 k0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2));
-            const float2 k1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + w2 + 1));
-            sa[0] = fmaf(qw[2 * w2], k0.x, sa[0]);
-            sa[1] = fmaf(qw[2 * w2 + 1], k0.y, sa[1]);
-            sa[2] = fmaf(qw[2 * w2 + 2], k1.x, sa[2]);
-            sa[3] = fmaf(qw[2 * w2 + 3], k1.y, sa[3]);
+#pragma unroll 4
+        for (int c = 0; c < 16; ++c) {
+            const uint4 kv = ks[swz(t, c)];
+            const float4 q0 = *reinterpret_cast<const float4*>(qw + 8 * c);
+            const float4 q1 = *reinterpret_cast<const float4*>(qw + 8 * c + 4);
+            const float2 k0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kv.x));
+            const float2 k1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kv.y));
+            const float2 k2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kv.z));
+            const float2 k3 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kv.w));
+            sa[0] = fmaf(q0.x, k0.x, sa[0]);
+            sa[1] = fmaf(q0.y, k0.y, sa[1]);
+            sa[2] = fmaf(q0.z, k1.x, sa[2]);
+            sa[3] = fmaf(q0.w, k1.y, sa[3]);
+            sa[0] = fmaf(q1.x, k2.x, sa[0]);
+            sa[1] = fmaf(q1.y, k2.y, sa[1]);
+            sa[2] = fmaf(q1.z, k3.x, sa[2]);
+            sa[3] = fmaf(q1.w, k3.y, sa[3]);
         }
         const float sacc = (sa[0] + sa[1]) + (sa[2] + sa[3]);
         pw[t] = sacc;
@@ -289,31 +492,36 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
     }
     csum = warp_sum(csum);
     __syncwarp();
-    // P * V: lane owns head dims 4*lane .. 4*lane+3; four independent accumulator chains
+    // P * V: lane owns head dims 4*lane .. 4*lane+3 (8 bytes of 16-byte chunk lane/2); four
+    // independent accumulator chains
     float acc[4][4] = {};
+    const int vc8 = lane >> 1, vh = (lane & 1) * 2;  // chunk, 32-bit word within it
+    auto vrow = [&](int t) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(vs + swz(t, vc8)) + vh;
+        return make_float4(__bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w)).x,
+                           __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w)).y,
+                           __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + 1)).x,
+                           __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + 1)).y);
+    };
     int t = 0;
     for (; t + 4 <= n; t += 4) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float pt = pw[t + u];
-            const uint32_t* vr = vs + (t + u) * kRowW + 2 * lane;
-            const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-            const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + 1));
-            acc[u][0] = fmaf(pt, v0.x, acc[u][0]);
-            acc[u][1] = fmaf(pt, v0.y, acc[u][1]);
-            acc[u][2] = fmaf(pt, v1.x, acc[u][2]);
-            acc[u][3] = fmaf(pt, v1.y, acc[u][3]);
+            const float4 v = vrow(t + u);
+            acc[u][0] = fmaf(pt, v.x, acc[u][0]);
+            acc[u][1] = fmaf(pt, v.y, acc[u][1]);
+            acc[u][2] = fmaf(pt, v.z, acc[u][2]);
+            acc[u][3] = fmaf(pt, v.w, acc[u][3]);
         }
     }
     for (; t < n; ++t) {
         const float pt = pw[t];
-        const uint32_t* vr = vs + t * kRowW + 2 * lane;
-        const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-        const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + 1));
-        acc[0][0] = fmaf(pt, v0.x, acc[0][0]);
-        acc[0][1] = fmaf(pt, v0.y, acc[0][1]);
-        acc[0][2] = fmaf(pt, v1.x, acc[0][2]);
-        acc[0][3] = fmaf(pt, v1.y, acc[0][3]);
+        const float4 v = vrow(t);
+        acc[0][0] = fmaf(pt, v.x, acc[0][0]);
+        acc[0][1] = fmaf(pt, v.y, acc[0][1]);
+        acc[0][2] = fmaf(pt, v.z, acc[0][2]);
+        acc[0][3] = fmaf(pt, v.w, acc[0][3]);
     }
     if (nsp == 1) {  // the whole context in this CTA: normalise and write, no merge
         float o[4];
@@ -427,9 +635,30 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 }  // namespace
 
+#define RTNQ_ROWS_VPT(KERN, CL, vpt, m, st, ...)                                                    \
+    ((vpt) <= 1    ? launch_rows(KERN<1, CL>, m, CL, st, __VA_ARGS__)                                 \
+     : (vpt) <= 2  ? launch_rows(KERN<2, CL>, m, CL, st, __VA_ARGS__)                                 \
+     : (vpt) <= 4  ? launch_rows(KERN<4, CL>, m, CL, st, __VA_ARGS__)                                 \
+     : (vpt) <= 8  ? launch_rows(KERN<8, CL>, m, CL, st, __VA_ARGS__)                                 \
+     : (vpt) <= 16 ? launch_rows(KERN<16, CL>, m, CL, st, __VA_ARGS__)                                \
+                   : launch_rows(KERN<32, CL>, m, CL, st, __VA_ARGS__))
+#define RTNQ_ROWS_DISPATCH(KERN, m, n8, st, ...)                                                    \
+    [&]() {                                                                                         \
+        const int cl_ = row_cluster(m, n8);                                                         \
+        const int64_t vpt_ = ((n8) + int64_t(cl_) * kRowThreads - 1) / (int64_t(cl_) * kRowThreads); \
+        return cl_ == 8   ? RTNQ_ROWS_VPT(KERN, 8, vpt_, m, st, __VA_ARGS__)                        \
+               : cl_ == 4 ? RTNQ_ROWS_VPT(KERN, 4, vpt_, m, st, __VA_ARGS__)                        \
+               : cl_ == 2 ? RTNQ_ROWS_VPT(KERN, 2, vpt_, m, st, __VA_ARGS__)                        \
+                          : RTNQ_ROWS_VPT(KERN, 1, vpt_, m, st, __VA_ARGS__);                       \
+    }()
+
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
                                int64_t h, float eps, cudaStream_t st, int8_t* planes, int32_t* texp) {
     if (h % 8) return cudaErrorInvalidValue;
+    if (h / 8 <= 32 * kRowThreads)  // the row in registers (of a cluster of CTAs)
+        return RTNQ_ROWS_DISPATCH(add_rmsnorm_rows_kernel, m, h / 8, st, static_cast<__nv_bfloat16*>(x),
+                                  static_cast<const __nv_bfloat16*>(delta), static_cast<const __nv_bfloat16*>(w),
+                                  static_cast<__nv_bfloat16*>(out), int(h), eps, planes, texp);
     return launch_pdl(add_rmsnorm_kernel, dim3(unsigned(m)), dim3(256), 8 * sizeof(float), st,
                       static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta),
                       static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps,
@@ -439,6 +668,9 @@ cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* 
 cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st, int8_t* planes,
                             int32_t* texp) {
     if (f % 8) return cudaErrorInvalidValue;
+    if (planes && f / 8 <= 32 * kRowThreads)  // the row in registers (of a cluster of CTAs)
+        return RTNQ_ROWS_DISPATCH(silu_mul_rows_kernel, m, f / 8, st, static_cast<const __nv_bfloat16*>(gu),
+                                  static_cast<__nv_bfloat16*>(act), int(f), planes, texp);
     if (planes)
         return launch_pdl(silu_mul_planes_kernel, dim3(unsigned(m)), dim3(256), 0, st,
                           static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(act), int(f), planes,
@@ -449,51 +681,79 @@ cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cud
                       static_cast<__nv_bfloat16*>(act), m, int(f));
 }
 
+// splits of the context: ~2 waves of CTAs over the SMs, chunks of 32..256 positions
+static void attention_split(int64_t batch, int64_t hkv, int64_t pos, int* nsp_out, int* chunk_out) {
+    const int64_t ctx = pos + 1, pairs = batch * hkv;
+    int64_t nsp = (2 * 148 + pairs - 1) / pairs;
+    nsp = nsp < 1 ? 1 : nsp;
+    const int64_t max_sp = (ctx + 31) / 32, min_sp = (ctx + kMaxChunk - 1) / kMaxChunk;
+    nsp = nsp > max_sp ? max_sp : nsp;
+    nsp = nsp < min_sp ? min_sp : nsp;
+    int64_t chunk = (ctx + nsp - 1) / nsp;
+    chunk = (chunk + 7) / 8 * 8;
+    *nsp_out = int((ctx + chunk - 1) / chunk);
+    *chunk_out = int(chunk);
+}
+
+size_t decode_attention_workspace_bytes(int64_t batch, int64_t hq, int64_t hkv, int64_t max_len) {
+    int nsp, chunk;
+    attention_split(batch, hkv, max_len - 1, &nsp, &chunk);  // the largest context of this cache
+    return 256 + size_t(batch * hkv) * sizeof(int) + size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float) + 256;
+}
+
 cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
                                     int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
-                                    int64_t lmax, int64_t pos, float theta, cudaStream_t st) {
+                                    int64_t lmax, int64_t pos, float theta, cudaStream_t st,
+                                    void* ws, size_t ws_bytes) {
     if (head_dim != kD || hkv <= 0 || hq % hkv || hq / hkv > 32 || pos < 0 || pos >= lmax)
         return cudaErrorInvalidValue;
     const int G = int(hq / hkv);
-    const size_t smem = size_t(2 * kChunk * kRowW) * 4 + size_t(G) * (kD + kChunk) * 4;
+    int nsp, chunk;
+    attention_split(batch, hkv, pos, &nsp, &chunk);
+    const size_t smem = size_t(2 * chunk * 16) * 16 + size_t(G) * (kD + chunk) * 4;
     static unsigned long long configured = 0;  // per device
     if (!(configured & current_device_bit())) {
         cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(2 * kChunk * kRowW * 4 + 32 * (kD + kChunk) * 4));
+                             int(2 * kMaxChunk * 16 * 16 + 32 * (kD + kMaxChunk) * 4));
         configured |= current_device_bit();
     }
-    // split-context partials (the scratch grows before any graph capture: the first call of a
-    // shape runs eagerly; capture of a larger shape would fail loudly, not corrupt)
-    const int nsp = int((pos + 1 + kChunk - 1) / kChunk);
-    static float* part_dev[64] = {};
-    static size_t part_bytes_dev[64] = {};
-    static int* arrivals_dev[64] = {};
-    static size_t arrivals_n_dev[64] = {};
-    float*& part = part_dev[current_device_index()];
-    size_t& part_bytes = part_bytes_dev[current_device_index()];
-    int*& arrivals = arrivals_dev[current_device_index()];
-    size_t& arrivals_n = arrivals_n_dev[current_device_index()];
-    if (size_t(batch * hkv) > arrivals_n) {  // zeroed once; the merging CTA resets its counter
-        arrivals = nullptr;                  // (an older buffer stays valid for captured graphs)
-        const size_t want = size_t(batch * hkv) * 2;
-        if (cudaError_t e = cudaMalloc(&arrivals, want * sizeof(int))) return e;
-        if (cudaError_t e = cudaMemset(arrivals, 0, want * sizeof(int))) return e;
-        arrivals_n = want;
+    // split-merge scratch: the counters (zero-initialized, self-resetting) and the partials, from
+    // the caller's workspace; without one, a per-device buffer (single stream only)
+    int* arrivals;
+    float* part;
+    const size_t need_part = size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float);
+    if (ws) {
+        if (ws_bytes < decode_attention_workspace_bytes(batch, hq, hkv, pos + 1)) return cudaErrorInvalidValue;
+        arrivals = static_cast<int*>(ws);
+        part = reinterpret_cast<float*>(static_cast<char*>(ws) + (256 + size_t(batch * hkv) * sizeof(int) + 255) / 256 * 256);
+    } else {
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lock(mu);
+        static float* part_dev[64] = {};
+        static size_t part_bytes_dev[64] = {};
+        static int* arrivals_dev[64] = {};
+        static size_t arrivals_n_dev[64] = {};
+        float*& pd = part_dev[current_device_index()];
+        size_t& pb = part_bytes_dev[current_device_index()];
+        int*& ad = arrivals_dev[current_device_index()];
+        size_t& an = arrivals_n_dev[current_device_index()];
+        if (size_t(batch * hkv) > an) {  // zeroed on this stream; an older buffer stays valid for graphs
+            const size_t want = size_t(batch * hkv) * 2;
+            int* fresh = nullptr;
+            if (cudaError_t e = cudaMalloc(&fresh, want * sizeof(int))) return e;
+            if (cudaError_t e = cudaMemsetAsync(fresh, 0, want * sizeof(int), st)) return e;
+            ad = fresh, an = want;
+        }
+        if (need_part > pb) {
+            float* fresh = nullptr;
+            if (cudaError_t e = cudaMalloc(&fresh, need_part * 2)) return e;
+            pd = fresh, pb = need_part * 2;
+        }
+        arrivals = ad, part = pd;
     }
-    const size_t need = size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float);
-    if (need > part_bytes) {
-        // the old buffer is kept (not freed): a CUDA graph captured earlier still uses it
-        part = nullptr;
-        const size_t want = need * 2;
-        if (cudaError_t e = cudaMalloc(&part, want)) return e;
-        part_bytes = want;
-    }
-    // 2..8 splits on a small grid: one thread-block cluster per (token, KV head), merged over
-    // DSMEM (saves the global round trips of the merge).  Large grids (e.g. batch 16) measured
-    // faster without clusters (scheduling freedom), and > 8 splits cannot form one: those merge
-    // through global memory (the last CTA to arrive).
-    const int64_t ctas = hkv * batch * nsp;
-    const int cluster = nsp >= 2 && nsp <= 8 && ctas <= 2 * 148 && !std::getenv("RTNQ_ATTN_NO_CLUSTER") ? 1 : 0;
+    // 2..8 splits: one thread-block cluster per (token, KV head), merged over DSMEM; more splits
+    // merge through global memory (the last CTA to arrive)
+    const int cluster = nsp >= 2 && nsp <= 8 && !std::getenv("RTNQ_ATTN_NO_CLUSTER") ? 1 : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(hkv), unsigned(batch), unsigned(nsp));
     cfg.blockDim = dim3(unsigned(32 * G));
@@ -509,7 +769,7 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     return cudaLaunchKernelEx(&cfg, decode_attention_kernel, static_cast<const __nv_bfloat16*>(qkv),
                               static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
                               int(hq), int(hkv), int(lmax), int(pos), theta, static_cast<__nv_bfloat16*>(out),
-                              arrivals, cluster);
+                              arrivals, cluster, chunk);
 }
 
 }  // namespace rtnq_b200

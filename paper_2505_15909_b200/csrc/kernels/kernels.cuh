@@ -106,8 +106,10 @@ cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cud
 // the activation planes alone ([3][m][k] int8, [m] exponents) of a bf16/f16 activation
 cudaError_t launch_act_planes(const void* a, int a_dtype, int64_t m, int64_t k, int8_t* planes,
                               int32_t* texp, cudaStream_t st);
+size_t decode_attention_workspace_bytes(int64_t batch, int64_t hq, int64_t hkv, int64_t max_len);
 cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
                                     int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
-                                    int64_t lmax, int64_t pos, float theta, cudaStream_t st);
+                                    int64_t lmax, int64_t pos, float theta, cudaStream_t st,
+                                    void* ws = nullptr, size_t ws_bytes = 0);
 
 }  // namespace rtnq_b200

@@ -245,12 +245,13 @@ class TPDecodeLayer:
         imma = (rq.NATIVE_I4, rq.NATIVE_I8)
         self.py = rq.Planes(batch, h, dev) if fuse_planes and (
             self.q["qkv_proj"].layout in imma or self.q["ffn_up"].layout in imma) else None
-        # (SiLU*up + planes in one kernel is a CTA per token over the whole ffn row: slower than
-        #  the two kernels, so the down projection computes its own planes)
-        self.pa = None
+        # SiLU*up emits the down projection's planes too (a cluster of CTAs per token row)
+        self.pa = rq.Planes(batch, self.dims.ffn, dev) if fuse_planes and self.q["ffn_down"].layout in imma \
+            else None
         # non-finite activations (InvalidInputError, gemm.cpp:13-19) are flagged asynchronously
         # by the int8 kernels' planes pass; the stack checks the flag after a step
         self.err = None
+        self.attn_ws = None  # split-merge scratch of decode_attention (the stack's, or a default)
 
     @property
     def weight_bytes(self):
@@ -271,7 +272,8 @@ class TPDecodeLayer:
         rq.add_rmsnorm(x, self.attn_norm, self.y, delta=delta, eps=s.eps, stream=stream, planes=self.py)
         self._linear("qkv_proj", self.y, self.py, self.qkv, ws, stream, pdl)
         rq.decode_attention(self.qkv, self.k_cache, self.v_cache, self.attn, self.dims.hq,
-                            self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream)
+                            self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream,
+                            workspace=self.attn_ws)
         rq.linear(self.attn, self.q["attn_out_proj"], out=self.o, workspace=ws, stream=stream,
                   pdl=pdl, err=self.err, check=False)
         return self.o
@@ -309,8 +311,10 @@ class TPDecodeStack:
         self.x = torch.zeros(batch, shape.hidden, dtype=torch.bfloat16, device=device)
         self.ws = rq.Workspace(device=device)
         self.err = rq.error_flag(device)
+        self.attn_ws = rq.Workspace(device=device)  # decode attention's split-merge scratch
         for layer in self.layers:
             layer.err = self.err
+            layer.attn_ws = self.attn_ws
 
     @property
     def weight_bytes(self):
