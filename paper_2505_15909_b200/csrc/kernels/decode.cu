@@ -352,14 +352,6 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
     }
 }
 
-// Rotate-half RoPE of one head vector element pair (d, d + D/2) at position pos.
-__device__ __forceinline__ float2 rope(float a, float b, int d, int D, int pos, float theta) {
-    // accurate sincos: angles reach pos (thousands of radians) at the low frequencies
-    const float inv = powf(theta, -2.0f * float(d) / float(D));
-    float s, c;
-    sincosf(float(pos) * inv, &s, &c);
-    return make_float2(a * c - b * s, b * c + a * s);
-}
 
 // Decode attention for one (token b, kv head): the group's query heads attend over cache
 // positions [0, pos] after the new k/v (rotated k) are appended at `pos`.
@@ -380,6 +372,98 @@ constexpr int kMaxChunk = 256;  // positions per CTA at most (smem)
 constexpr int kPart = kD + 4;   // floats per split partial: max, sum, 2 pad, P*V (16-B aligned)
 
 __device__ __forceinline__ uint32_t swz(int t, int c) { return uint32_t(t * 16 + (c ^ (t & 15))); }  // 16-B chunk
+
+// The end of a split CTA, per warp = query head qh (lane: head dims 4 lane .. 4 lane + 3): its
+// (max, sum, unnormalised P.V) partial -> the output (one split), or the DSMEM merge inside the
+// cluster (scratch: kPart floats per warp of idle shared memory), or the last-CTA global merge.
+__device__ __forceinline__ void attn_finish(float cmax, float csum, float4 a4, float* scratch, float* __restrict__ part,
+                                            int* __restrict__ arrivals, __nv_bfloat16* __restrict__ out, int b,
+                                            int kvh, int qh, int hq, int hkv, int sp, int nsp, int cluster_merge) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (nsp == 1) {  // the whole context in this CTA: normalise and write, no merge
+        float o[4];
+        o[0] = a4.x / csum, o[1] = a4.y / csum, o[2] = a4.z / csum, o[3] = a4.w / csum;
+        __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+        *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(o[0], o[1]);
+        *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(o[2], o[3]);
+        return;
+    }
+    if (cluster_merge) {
+        // the splits of this (token, KV head) are one thread-block cluster: partials stay in
+        // each CTA's shared memory (idle scratch) and rank 0 merges them over DSMEM
+        __syncthreads();  // every warp is done reading the staging buffers
+        float* mine = scratch + warp * kPart;
+        if (lane == 0) mine[0] = cmax, mine[1] = csum;
+        *reinterpret_cast<float4*>(mine + 4 + 4 * lane) =
+            a4;
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (sp == 0) {
+            const uint32_t my = static_cast<uint32_t>(__cvta_generic_to_shared(mine));
+            float mq[8], lq[8];
+            float M = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {  // nsp <= 8: fixed trip count keeps mq/lq in registers
+                if (q >= nsp) break;
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my), "r"(q));
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(mq[q]) : "r"(ra));
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lq[q]) : "r"(ra + 4));
+                M = fmaxf(M, mq[q]);
+            }
+            float L = 0.0f, a[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q >= nsp) break;
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my + uint32_t(16 + 16 * lane)), "r"(q));
+                float4 x;
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(ra));
+                const float w = __expf(mq[q] - M);
+                L = fmaf(w, lq[q], L);
+                a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
+            }
+            const float inv = 1.0f / L;
+            __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+            *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
+            *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+        }
+        // peers keep their shared memory alive until rank 0 has read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
+    // partial: [b][qh][split] -> {max, sum, acc[kD]}
+    float* pr = part + ((int64_t(b) * hq + qh) * nsp + sp) * kPart;
+    if (lane == 0) pr[0] = cmax, pr[1] = csum;
+    *reinterpret_cast<float4*>(pr + 4 + 4 * lane) =
+        a4;
+    // the last split CTA of this (token, KV head) merges the partials (self-resetting counter)
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(arrivals + b * hkv + kvh, 1);
+        last = prev == nsp - 1;
+        if (last) arrivals[b * hkv + kvh] = 0;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const float* ph = part + (int64_t(b) * hq + qh) * nsp * kPart;
+    float M = -INFINITY;
+    for (int q = 0; q < nsp; ++q) M = fmaxf(M, __ldcg(ph + q * kPart));
+    float L = 0.0f, a[4] = {0, 0, 0, 0};
+    for (int q = 0; q < nsp; ++q) {
+        const float w = __expf(__ldcg(ph + q * kPart) - M);
+        L = fmaf(w, __ldcg(ph + q * kPart + 1), L);
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(ph + q * kPart + 4 + 4 * lane));
+        a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
+    }
+    const float inv = 1.0f / L;
+    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
+    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
+    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+}
 
 __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
@@ -523,92 +607,182 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
         acc[0][2] = fmaf(pt, v.z, acc[0][2]);
         acc[0][3] = fmaf(pt, v.w, acc[0][3]);
     }
-    if (nsp == 1) {  // the whole context in this CTA: normalise and write, no merge
-        float o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = (acc[0][j] + acc[1][j] + acc[2][j] + acc[3][j]) / csum;
-        __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
-        *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(o[0], o[1]);
-        *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(o[2], o[3]);
-        return;
+    attn_finish(cmax, csum,
+                make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
+                            acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]),
+                reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh, qh, hq, hkv, sp, nsp, cluster_merge);
+}
+
+// Tensor-core variant (G <= 8 query heads per KV head): Q K^T and P V on mma.sync m16n8k16
+// (bf16 x bf16 -> f32).  Queries and probabilities are split into bf16 hi + lo parts stacked in
+// the 16 rows of the A tile (row h: hi part of head h, row 8 + h: lo part), so the products keep
+// ~16 significant bits of q and p; keys and values are bf16 already.  Same staging, splits and
+// merge as decode_attention_kernel; its CUDA-core score and P V loops become ~8 + 16 MMAs per
+// 16 positions per warp.
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                            __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+                                            float* __restrict__ part, int hq, int hkv, int lmax,
+                                            int pos, float theta, __nv_bfloat16* __restrict__ out,
+                                            int* __restrict__ arrivals, int cluster_merge, int chunk) {
+    pdl_prologue();
+    constexpr int kQS = kD + 8;                     // bf16 per A-tile row of the queries (padded)
+    const int chunkp = (chunk + 15) / 16 * 16, kPS = chunkp + 8;
+    extern __shared__ uint4 smq[];
+    uint4* ks = smq;                                 // [chunkp][16] swizzled 16-byte chunks
+    uint4* vs = ks + chunkp * 16;                    // [chunkp][16]
+    __nv_bfloat16* qa = reinterpret_cast<__nv_bfloat16*>(vs + chunkp * 16);  // [16][kQS] q hi / lo
+    __nv_bfloat16* pa = qa + 16 * kQS;               // [16][kPS] p hi / lo
+    float* sc = reinterpret_cast<float*>(pa + 16 * kPS);  // [G][chunkp] scores
+    float* fin = sc + 8 * chunkp;                    // [G][kPart] per-head results
+    const int b = blockIdx.y, kvh = blockIdx.x, sp = blockIdx.z, nsp = gridDim.z, G = hq / hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x, W = nthr >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int64_t row = int64_t(b) * (hq + 2 * hkv) * kD;
+    const __nv_bfloat16* kn = qkv + row + int64_t(hq) * kD + int64_t(kvh) * kD;
+    const __nv_bfloat16* vn = kn + int64_t(hkv) * kD;
+    const int64_t cstride = int64_t(hkv) * kD;
+    __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
+    __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
+    const int t0 = sp * chunk, n = min(chunk, pos + 1 - t0);
+    __shared__ float2 cs_s[kD / 2];
+    if (threadIdx.x < kD / 2) {
+        const float inv = powf(theta, -2.0f * float(threadIdx.x) / float(kD));
+        float sn, cn;
+        sincosf(float(pos) * inv, &sn, &cn);
+        cs_s[threadIdx.x] = make_float2(cn, sn);
     }
-    if (cluster_merge) {
-        // the splits of this (token, KV head) are one thread-block cluster: partials stay in
-        // each CTA's shared memory (the idle K stage) and rank 0 merges them over DSMEM
-        __syncthreads();  // every warp is done reading ks
-        float* mine = reinterpret_cast<float*>(ks) + warp * kPart;
-        if (lane == 0) mine[0] = cmax, mine[1] = csum;
-        *reinterpret_cast<float4*>(mine + 4 + 4 * lane) =
-            make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
-                        acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]);
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        if (sp == 0) {
-            const uint32_t my = static_cast<uint32_t>(__cvta_generic_to_shared(mine));
-            float mq[8], lq[8];
-            float M = -INFINITY;
+    // zero the probability tile (rows of absent heads, positions past n) and the absent query rows
+    for (int i = threadIdx.x; i < 16 * kPS / 2; i += nthr) reinterpret_cast<uint32_t*>(pa)[i] = 0u;
+    for (int i = threadIdx.x; i < 16 * kQS / 2; i += nthr) {
+        const int r = i / (kQS / 2);
+        if ((r & 7) >= G) reinterpret_cast<uint32_t*>(qa)[i] = 0u;
+    }
+    __syncthreads();
+    auto rot = [&](float a, float bb, int d) {
+        const float2 c = cs_s[d];
+        return make_float2(a * c.x - bb * c.y, bb * c.x + a * c.y);
+    };
+    if (sp == nsp - 1 && warp == 0) {  // append the rotated key and the value at pos
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {  // nsp <= 8: fixed trip count keeps mq/lq in registers
-                if (q >= nsp) break;
-                uint32_t ra;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my), "r"(q));
-                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(mq[q]) : "r"(ra));
-                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lq[q]) : "r"(ra + 4));
-                M = fmaxf(M, mq[q]);
-            }
-            float L = 0.0f, a[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (q >= nsp) break;
-                uint32_t ra;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(my + uint32_t(16 + 16 * lane)), "r"(q));
-                float4 x;
-                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(ra));
-                const float w = __expf(mq[q] - M);
-                L = fmaf(w, lq[q], L);
-                a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
-            }
-            const float inv = 1.0f / L;
-            __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
-            *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
-            *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int d = lane + 32 * h2;
+            const float2 r = rot(__bfloat162float(kn[d]), __bfloat162float(kn[d + kD / 2]), d);
+            kcb[int64_t(pos) * cstride + d] = __float2bfloat16_rn(r.x);
+            kcb[int64_t(pos) * cstride + d + kD / 2] = __float2bfloat16_rn(r.y);
+            vcb[int64_t(pos) * cstride + d] = vn[d];
+            vcb[int64_t(pos) * cstride + d + kD / 2] = vn[d + kD / 2];
         }
-        // peers keep their shared memory alive until rank 0 has read it
-        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        return;
     }
-    // partial: [b][qh][split] -> {max, sum, acc[kD]}
-    float* pr = part + ((int64_t(b) * hq + qh) * nsp + sp) * kPart;
-    if (lane == 0) pr[0] = cmax, pr[1] = csum;
-    *reinterpret_cast<float4*>(pr + 4 + 4 * lane) =
-        make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
-                    acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]);
-    // the last split CTA of this (token, KV head) merges the partials (self-resetting counter)
-    __shared__ int last;
+    {  // rotated, pre-scaled query of head `warp`, as bf16 hi (row warp) + lo (row 8 + warp)
+        const __nv_bfloat16* qp = qkv + row + int64_t(kvh * G + warp) * kD;
+        const float scale = rsqrtf(float(kD));
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int d = lane + 32 * h2;
+            const float2 r = rot(__bfloat162float(qp[d]), __bfloat162float(qp[d + kD / 2]), d);
+            const float q0 = r.x * scale, q1 = r.y * scale;
+            const __nv_bfloat16 h0 = __float2bfloat16_rn(q0), h1 = __float2bfloat16_rn(q1);
+            qa[warp * kQS + d] = h0;
+            qa[warp * kQS + d + kD / 2] = h1;
+            qa[(8 + warp) * kQS + d] = __float2bfloat16_rn(q0 - __bfloat162float(h0));
+            qa[(8 + warp) * kQS + d + kD / 2] = __float2bfloat16_rn(q1 - __bfloat162float(h1));
+        }
+    }
+    __threadfence_block();
+    __syncthreads();  // the appended row is written before the staging copies below read it
+    for (int i = threadIdx.x; i < n * 16; i += nthr) {
+        const int t = i >> 4, c = i & 15;
+        const uint32_t kd = static_cast<uint32_t>(__cvta_generic_to_shared(ks + swz(t, c)));
+        const uint32_t vd = static_cast<uint32_t>(__cvta_generic_to_shared(vs + swz(t, c)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(kd), "l"(kcb + int64_t(t0 + t) * cstride + c * 8)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vd), "l"(vcb + int64_t(t0 + t) * cstride + c * 8)
+                     : "memory");
+    }
+    for (int i = n * 16 + threadIdx.x; i < chunkp * 16; i += nthr)  // rows past n: finite zeros
+        ks[swz(i >> 4, i & 15)] = vs[swz(i >> 4, i & 15)] = make_uint4(0, 0, 0, 0);
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const int prev = atomicAdd(arrivals + b * hkv + kvh, 1);
-        last = prev == nsp - 1;
-        if (last) arrivals[b * hkv + kvh] = 0;
+    // S = Q K^T: warp w takes the 8-position tiles w, w + W, ...
+    {
+        uint32_t af[8][4];
+        const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qa);
+#pragma unroll
+        for (int k16 = 0; k16 < 8; ++k16) {
+            af[k16][0] = q32[(g * kQS + 16 * k16 + 2 * t4) >> 1];
+            af[k16][1] = q32[((g + 8) * kQS + 16 * k16 + 2 * t4) >> 1];
+            af[k16][2] = q32[(g * kQS + 16 * k16 + 8 + 2 * t4) >> 1];
+            af[k16][3] = q32[((g + 8) * kQS + 16 * k16 + 8 + 2 * t4) >> 1];
+        }
+        for (int j = warp; j < chunkp / 8; j += W) {
+            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const int r = 8 * j + g;  // this lane's key row (B column)
+#pragma unroll
+            for (int k16 = 0; k16 < 8; ++k16) {
+                const uint32_t b0 = reinterpret_cast<const uint32_t*>(ks + swz(r, 2 * k16))[t4];
+                const uint32_t b1 = reinterpret_cast<const uint32_t*>(ks + swz(r, 2 * k16 + 1))[t4];
+                mma_bf16(c, af[k16][0], af[k16][1], af[k16][2], af[k16][3], b0, b1);
+            }
+            if (g < G) {  // rows g (hi) + g + 8 (lo) of head g, positions 8j + 2t4, + 1
+                const int p0 = 8 * j + 2 * t4;
+                sc[g * chunkp + p0] = c[0] + c[2];
+                sc[g * chunkp + p0 + 1] = c[1] + c[3];
+            }
+        }
     }
     __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const float* ph = part + (int64_t(b) * hq + qh) * nsp * kPart;
-    float M = -INFINITY;
-    for (int q = 0; q < nsp; ++q) M = fmaxf(M, __ldcg(ph + q * kPart));
-    float L = 0.0f, a[4] = {0, 0, 0, 0};
-    for (int q = 0; q < nsp; ++q) {
-        const float w = __expf(__ldcg(ph + q * kPart) - M);
-        L = fmaf(w, __ldcg(ph + q * kPart + 1), L);
-        const float4 x = __ldcg(reinterpret_cast<const float4*>(ph + q * kPart + 4 + 4 * lane));
-        a[0] = fmaf(w, x.x, a[0]), a[1] = fmaf(w, x.y, a[1]), a[2] = fmaf(w, x.z, a[2]), a[3] = fmaf(w, x.w, a[3]);
+    // softmax of head `warp` over its n positions; probabilities as bf16 hi (row h) + lo (8 + h)
+    float cmax = -INFINITY, csum = 0.0f;
+    {
+        const float* sw = sc + warp * chunkp;
+        for (int t = lane; t < n; t += 32) cmax = fmaxf(cmax, sw[t]);
+        cmax = warp_max(cmax);
+        for (int t = lane; t < n; t += 32) {
+            const float e = __expf(sw[t] - cmax);
+            csum += e;
+            const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+            pa[warp * kPS + t] = hi;
+            pa[(8 + warp) * kPS + t] = __float2bfloat16_rn(e - __bfloat162float(hi));
+        }
+        csum = warp_sum(csum);
     }
-    const float inv = 1.0f / L;
-    __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
-    *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
-    *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+    __syncthreads();
+    // O = P V: warp w takes the 8-dim tiles w, w + W, ... over all 16-position k-steps
+    {
+        const uint32_t* p32 = reinterpret_cast<const uint32_t*>(pa);
+        for (int nt = warp; nt < kD / 8; nt += W) {
+            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            for (int k16 = 0; k16 < chunkp / 16; ++k16) {
+                const uint32_t a0 = p32[(g * kPS + 16 * k16 + 2 * t4) >> 1];
+                const uint32_t a1 = p32[((g + 8) * kPS + 16 * k16 + 2 * t4) >> 1];
+                const uint32_t a2 = p32[(g * kPS + 16 * k16 + 8 + 2 * t4) >> 1];
+                const uint32_t a3 = p32[((g + 8) * kPS + 16 * k16 + 8 + 2 * t4) >> 1];
+                // B = V[16 positions][8 dims] (row-major k x n): two 8x8 matrices, transposed load
+                const uint32_t va = static_cast<uint32_t>(
+                    __cvta_generic_to_shared(vs + swz(16 * k16 + (lane & 15), nt)));
+                uint32_t b0, b1;
+                asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                             : "=r"(b0), "=r"(b1) : "r"(va));
+                mma_bf16(c, a0, a1, a2, a3, b0, b1);
+            }
+            if (g < G) {
+                fin[g * kPart + 4 + 8 * nt + 2 * t4] = c[0] + c[2];
+                fin[g * kPart + 4 + 8 * nt + 2 * t4 + 1] = c[1] + c[3];
+            }
+        }
+    }
+    __syncthreads();
+    const float4 a4 = *reinterpret_cast<const float4*>(fin + warp * kPart + 4 + 4 * lane);
+    attn_finish(cmax, csum, a4, reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh, kvh * G + warp, hq, hkv,
+                sp, nsp, cluster_merge);
 }
 
 template <typename... KArgs, typename... Args>
@@ -710,11 +884,21 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     const int G = int(hq / hkv);
     int nsp, chunk;
     attention_split(batch, hkv, pos, &nsp, &chunk);
-    const size_t smem = size_t(2 * chunk * 16) * 16 + size_t(G) * (kD + chunk) * 4;
+    // tensor cores for up to 8 query heads per KV head (hi/lo rows of one m16 tile)
+    static const bool no_mma = std::getenv("RTNQ_ATTN_NO_MMA") != nullptr;
+    const bool mma = G <= 8 && !no_mma;
+    auto mma_smem = [](int ch) {
+        const int chp = (ch + 15) / 16 * 16;
+        return size_t(2 * chp * 16) * 16 + size_t(16) * (kD + 8) * 2 + size_t(16) * (chp + 8) * 2 +
+               size_t(8) * chp * 4 + size_t(8) * kPart * 4;
+    };
+    const size_t smem = mma ? mma_smem(chunk) : size_t(2 * chunk * 16) * 16 + size_t(G) * (kD + chunk) * 4;
     static unsigned long long configured = 0;  // per device
     if (!(configured & current_device_bit())) {
         cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(2 * kMaxChunk * 16 * 16 + 32 * (kD + kMaxChunk) * 4));
+        cudaFuncSetAttribute(decode_attention_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(mma_smem(kMaxChunk)));
         configured |= current_device_bit();
     }
     // split-merge scratch: the counters (zero-initialized, self-resetting) and the partials, from
@@ -766,7 +950,8 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     attr.val.clusterDim.z = unsigned(nsp);
     cfg.attrs = &attr;
     cfg.numAttrs = cluster ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, decode_attention_kernel, static_cast<const __nv_bfloat16*>(qkv),
+    return cudaLaunchKernelEx(&cfg, mma ? decode_attention_mma_kernel : decode_attention_kernel,
+                              static_cast<const __nv_bfloat16*>(qkv),
                               static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
                               int(hq), int(hkv), int(lmax), int(pos), theta, static_cast<__nv_bfloat16*>(out),
                               arrivals, cluster, chunk);
