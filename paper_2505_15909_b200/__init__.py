@@ -222,9 +222,9 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
     """RTN quantize-and-pack on the GPU (rtnq_dev_quantize_pack_ex).
 
     The linear's operand is ``codes`` in ``out.layout``.  With ``native=None`` that is the
-    layout of the fastest kernel for the shape: NATIVE_I8 for W8 per-channel and NATIVE_I4
-    for W4 group-128 (tcgen05 kind::i8 kernels; one quantize kernel writes their tiles
-    directly), else NATIVE (tcgen05 kind::f16 kernel).  ``native=True`` forces NATIVE."""
+    layout of the fastest kernel for the shape: NATIVE_I8 for W8 per-channel and group-128 and
+    NATIVE_I4 for W4 group-128 (tcgen05 kind::i8 kernels; one quantize kernel writes their
+    tiles directly), else NATIVE (tcgen05 kind::f16 kernel).  ``native=True`` forces NATIVE."""
     torch = _torch()
     assert w.is_cuda and w.dim() == 2 and w.is_contiguous()
     rows, cols = w.shape
@@ -236,7 +236,7 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
     # kernels, from the row-major bytes), else NATIVE (kind::f16 kernel)
     imma = None
     if native is None:
-        if bits == 8 and group >= cols:
+        if bits == 8 and (group >= cols or group == 128):
             imma = NATIVE_I8
         elif bits == 4 and group == 128:
             imma = NATIVE_I4
@@ -280,7 +280,7 @@ def from_row_major(codes_rm, scales_f16, rows: int, cols: int, bits: int, group:
     and the scales reordered into the native order."""
     gpr = groups_per_row(group, ragged, cols)
     kind = NATIVE
-    if bits == 8 and group >= cols:
+    if bits == 8 and (group >= cols or group == 128):
         kind = NATIVE_I8
     elif bits == 4 and group == 128:
         kind = NATIVE_I4

@@ -223,8 +223,8 @@ rtnq_status rtnq_dev_quantize_pack_ex(const void* w, int w_dtype, int64_t rows, 
     if (gpr < 0) return rtnq_status(-gpr);
     if (native_kind == RTNQ_NATIVE_I4 && (bits != 4 || g != 128))
         return fail(RTNQ_E_UNSUPPORTED, "RTNQ_NATIVE_I4 holds W4 group-128 codes");
-    if (native_kind == RTNQ_NATIVE_I8 && (bits != 8 || g < cols))
-        return fail(RTNQ_E_UNSUPPORTED, "RTNQ_NATIVE_I8 holds W8 per-channel codes (one group per row)");
+    if (native_kind == RTNQ_NATIVE_I8 && (bits != 8 || (g < cols && g != 128)))
+        return fail(RTNQ_E_UNSUPPORTED, "RTNQ_NATIVE_I8 holds W8 per-channel or group-128 codes");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (rows * cols == 0) return RTNQ_OK;
     if (s16n) RTNQ_CUDA(cudaMemsetAsync(s16n, 0, size_t(rtnq_native_scale_count(rows, gpr)) * 2, st));
@@ -290,9 +290,10 @@ static bool i8_path(int a_dtype, rtnq_layout layout, int bits, int64_t g, int64_
            (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) && sdtype == RTNQ_F16;
 }
 
-// W4 group-128 over RTNQ_NATIVE_I4 nibble tiles: the int8 tensor-core kernel.
+// Group 128 (per-group accumulators, wgemm_i4.cu): W4 over RTNQ_NATIVE_I4 nibble tiles or W8 over
+// RTNQ_NATIVE_I8 tiles, on the int8 tensor-core kernel.
 static bool i4_path(int a_dtype, rtnq_layout layout, int bits, int64_t g, int sdtype, int sorder) {
-    return layout.kind == RTNQ_NATIVE_I4 && bits == 4 && g == 128 &&
+    return ((layout.kind == RTNQ_NATIVE_I4 && bits == 4) || (layout.kind == RTNQ_NATIVE_I8 && bits == 8)) && g == 128 &&
            (a_dtype == RTNQ_BF16 || a_dtype == RTNQ_F16) && sdtype == RTNQ_F16 &&
            sorder == RTNQ_SCALES_NATIVE;
 }
@@ -312,7 +313,9 @@ size_t rtnq_dev_linear_workspace_bytes(int64_t m, int64_t n, int64_t k, int bits
     if (path == RTNQ_PATH_FUSED || path == RTNQ_PATH_AUTO) {
         if (layout.kind == RTNQ_NATIVE_SM100) ws = wgemm_workspace_bytes(m, n, k, bits, g);
         if (layout.kind == RTNQ_NATIVE_I8 && bits == 8 && g >= k) ws = wgemm_i8_workspace_bytes(m, n, k);
-        if (layout.kind == RTNQ_NATIVE_I4 && bits == 4 && g == 128) ws = wgemm_i4_workspace_bytes(m, n, k);
+        if ((layout.kind == RTNQ_NATIVE_I4 && bits == 4 || layout.kind == RTNQ_NATIVE_I8 && bits == 8 && g < k) &&
+            g == 128)
+            ws = wgemm_i4_workspace_bytes(m, n, k);
     }
     if (path == RTNQ_PATH_DEQUANT_FIRST || path == RTNQ_PATH_AUTO) {
         // f32 reference-exact materialization, or the tensor-core hi/lo split (+ f32 C), after

@@ -61,8 +61,11 @@ struct Params {
     int8_t* planes_w;     // ... into this [3][Mtot][K] buffer (the TMA source), exponents into texp
 };
 
-template <int PT>
+template <int PT, int BITS = 4>
 struct Geo {
+    // W4: one 8 KiB NATIVE_I4 nibble tile per 128 rows x group, expanded to s8 in TMEM;
+    // W8 group 128: one 16 KiB NATIVE_I8 tile (pre-swizzled s8, the MMA reads it from smem)
+    static constexpr int TILE = BITS == 4 ? kTile : kRows * 128;
     static constexpr int ACC = (PT + 3) / 4 * 4;            // per-row accumulators (float4 I/O)
     static constexpr int DN = (3 * PT + 15) / 16 * 16;      // accumulator columns per group
     static constexpr int BOX_BYTES = 3 * PT * 128;          // one group's planes box
@@ -73,9 +76,9 @@ struct Geo {
 #ifndef RTNQ_I4_TPS16
 #define RTNQ_I4_TPS16 4
 #endif
-    static constexpr int TPS = PT <= 16 ? RTNQ_I4_TPS16 : PT <= 32 ? 2 : 1;
+    static constexpr int TPS = BITS == 8 ? (PT <= 32 ? 2 : 1) : PT <= 16 ? RTNQ_I4_TPS16 : PT <= 32 ? 2 : 1;
     static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
-    static constexpr int SC_OFF = CODE_OFF + TPS * kTile;
+    static constexpr int SC_OFF = CODE_OFF + TPS * TILE;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
     // two epilogue warpgroups (one per group of a stage) when a stage holds two groups
 #ifndef RTNQ_I4_EW
@@ -91,8 +94,8 @@ struct Geo {
     // shared with TMA and the planes).  KT balances the two ports for the batch size.
     static constexpr int KT = 4;
     // expanded A slots (groups); TMEM = AS * 32 A columns + NS * DN accumulator columns
-    static constexpr int AS = TPS == 4 ? (PT <= 10 ? 8 : 4) : PT <= 16 ? 6 : PT <= 32 ? 4 : 2;
-    static constexpr int AP = AS / TPS;                     // ... in stage-sized slots
+    static constexpr int AS = BITS == 8 ? 0 : TPS == 4 ? (PT <= 10 ? 8 : 4) : PT <= 16 ? 6 : PT <= 32 ? 4 : 2;
+    static constexpr int AP = BITS == 8 ? 1 : AS / TPS;     // ... in stage-sized slots (W8: unused)
     static constexpr int A_SMEM = KT < 4 ? kRows * 128 : 0;  // smem A tile per slot (16 KiB)
 #ifndef RTNQ_I4_SMEM_KB
 #define RTNQ_I4_SMEM_KB 212
@@ -176,14 +179,14 @@ __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64
 #define I4_T0() const long long _t0 = (dbg_ & 32) ? clock64() : 0
 #define I4_ACC(var) if (dbg_ & 32) var += clock64() - _t0
 
-template <int PT>
-__global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
+template <int PT, int BITS>
+__global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
 #ifdef RTNQ_KERNEL_DEBUG
     const int dbg_ = p.debug;  // profiling knobs (scratch/*prof*.py, *tl.py)
 #else
     constexpr int dbg_ = 0;  // compiled out: even disabled, the checks cost a few % per launch
 #endif
-    using GG = Geo<PT>;
+    using GG = Geo<PT, BITS>;
     constexpr int NT = GG::ACC;
     constexpr int STAGES = GG::STAGES, DN = GG::DN, AP = GG::AP, NP = GG::NP, TPS = GG::TPS, EW = GG::EW;
     extern __shared__ uint8_t smem_raw[];
@@ -281,9 +284,9 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                 // the row-block's rows padded to 8: the stride of its native scale groups
                 const int64_t left = p.N - int64_t(cu.b) * kRows;
                 const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
-                elect_expect(&full[s], uint32_t(n) * (kTile + uint32_t(r8) * 2));
-                elect_bulk_tx(st + GG::CODE_OFF + slot0 * kTile,
-                              p.codes + (int64_t(cu.b) * p.KBLK + cu.kb) * kTile, &full[s], uint32_t(n) * kTile);
+                elect_expect(&full[s], uint32_t(n) * (GG::TILE + uint32_t(r8) * 2));
+                elect_bulk_tx(st + GG::CODE_OFF + slot0 * GG::TILE,
+                              p.codes + (int64_t(cu.b) * p.KBLK + cu.kb) * GG::TILE, &full[s], uint32_t(n) * GG::TILE);
                 elect_bulk_tx(st + GG::SC_OFF + slot0 * 256,
                               p.scales + int64_t(cu.b) * kRows * p.KBLK + int64_t(cu.kb) * r8, &full[s],
                               uint32_t(n * r8 * 2));
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             if (warp == kExp0) I4_TL(si, 11);
             {
                 I4_T0();
-                if (si >= AP) mbar_wait(&aempty[ap], uint32_t(si / AP - 1) & 1u);
+                if (BITS == 4 && si >= AP) mbar_wait(&aempty[ap], uint32_t(si / AP - 1) & 1u);
                 I4_ACC(x_aempty);
             }
             if (warp == kExp0) I4_TL(si, 12);
@@ -343,7 +346,15 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             const long long _tw = (dbg_ & 32) ? clock64() : 0;
             if (warp == kExp0) I4_TL(si, 2);
             const uint8_t* st = smem + s * GG::STAGE_BYTES;
-            if (!(dbg_ & 65536)) {
+            if (BITS == 8) {
+                // W8: the MMA reads the s8 tiles from shared memory; only the group scales move
+#pragma unroll
+                for (int j = 0; j < TPS; ++j) {
+                    if (j >= n) break;
+                    const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
+                    sring[(np * TPS + j) * kRows + row] = row < r8 ? __half2float(__ushort_as_half(sc[row])) : 0.0f;
+                }
+            } else if (!(dbg_ & 65536)) {
                 // two groups at a time: their code loads first (latency overlap), then expand and store
                 constexpr int JP = TPS < 2 ? TPS : 2;
 #pragma unroll
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
 #pragma unroll
                     for (int jj = 0; jj < JP; ++jj)
                         if (j0 + jj < n) {
-                            const uint8_t* src = st + GG::CODE_OFF + (slot0 + j0 + jj) * kTile + row * 64;
+                            const uint8_t* src = st + GG::CODE_OFF + (slot0 + j0 + jj) * GG::TILE + row * 64;
 #pragma unroll
                             for (uint32_t q = 0; q < 4; ++q)
                                 w[jj][q] = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
@@ -390,8 +401,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
                     }
                 }
             }
-            if constexpr (GG::KT > 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            if constexpr (GG::KT < 4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if constexpr (BITS == 4) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
@@ -428,7 +438,7 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             }
             I4_TL(si, 8);
             if ((dbg_ & 64) && si == 0 && lane == 0) g_i4_dbg[c * 16 + 6] = gtime();
-            {
+            if (BITS == 4) {
                 I4_T0();
                 mbar_wait(&afull[ap], uint32_t(si / AP) & 1u);
                 I4_ACC(m_afull);
@@ -448,10 +458,16 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
             static_assert(GG::KT == 4, "A operand entirely from TMEM");
             if (!(dbg_ & 4)) {
                 for (int j = 0; j < n; ++j) {
-                    const int slot = ap * TPS + j;
-                    const uint32_t a = tmem + uint32_t(GG::A_COL + slot * GG::KT * 8);
                     const uint32_t blo = stage_lo + uint32_t((slot0 + j) * GG::PLANE_BYTES >> 4);
-                    mma4_i8_ts_warp(tmem + uint32_t((np * TPS + j) * DN), a, kHi | blo, idesc, 0u);
+                    const uint32_t d = tmem + uint32_t((np * TPS + j) * DN);
+                    if constexpr (BITS == 4) {
+                        const uint32_t a = tmem + uint32_t(GG::A_COL + (ap * TPS + j) * GG::KT * 8);
+                        mma4_i8_ts_warp(d, a, kHi | blo, idesc, 0u);
+                    } else {  // the pre-swizzled 128 x 128 s8 tile: K-major SWIZZLE_128B, like the planes
+                        const uint32_t alo = stage_lo + uint32_t((GG::CODE_OFF + (slot0 + j) * GG::TILE) >> 4);
+                        mma2_i8_ss_warp(d, kHi | alo, kHi | blo, idesc, 0u);
+                        mma2_i8_ss_warp(d, kHi | (alo + 4), kHi | (blo + 4), idesc, 1u);
+                    }
                 }
             }
             I4_TL(si, 1);
@@ -726,10 +742,10 @@ __global__ void __launch_bounds__(Geo<PT>::THREADS, 1) wgemm_i4_kernel(const __g
     }
 }
 
-template <int PT>
+template <int PT, int BITS>
 cudaError_t launch_nt(Params p, cudaStream_t st) {
-    using GG = Geo<PT>;
-    auto kern = wgemm_i4_kernel<PT>;
+    using GG = Geo<PT, BITS>;
+    auto kern = wgemm_i4_kernel<PT, BITS>;
     static unsigned long long configured = 0;  // per device
     static int max_clusters_dev[64][9] = {};
     int* max_clusters = max_clusters_dev[current_device_index()];
@@ -805,7 +821,7 @@ size_t wgemm_i4_workspace_bytes(int64_t m, int64_t n, int64_t k) {
 
 const char* wgemm_i4_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype) {
     (void)m, (void)n;
-    if (bits != 4 || g != 128) return "the W4 int8 tensor-core path is group size 128";
+    if ((bits != 4 && bits != 8) || g != 128) return "the group-128 int8 tensor-core path is group size 128";
     if (a_dtype != RTNQ_BF16 && a_dtype != RTNQ_F16) return "activations must be bf16 or f16";
     if (k % 16 != 0) return "k must be a multiple of 16 for the int8 tensor-core path";
     return nullptr;
@@ -872,7 +888,8 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     // scratch/shapes_seq.py, batch 16: qkv / o 10.3 / 9.1 us with the planes kernel, 11.8 / 10.4
     // in the GEMM; gate_up / down 23.7 / 19.4 vs 21.7 / 18.5)
     const int64_t units = ((A.n + i4::kRows - 1) / i4::kRows) * ((A.k + i4::kKB - 1) / i4::kKB);
-    const bool in_gemm = own_planes && !planes_kernel && A.m >= imma::kOwnPlanesMinM && units >= 2048 &&
+    // (W8 group-128: the stand-alone kernel, as for W8 per-channel: 23.4 vs 25.3 us, gate_up batch 16)
+    const bool in_gemm = own_planes && !planes_kernel && A.bits == 4 && A.m >= imma::kOwnPlanesMinM && units >= 2048 &&
                          (reinterpret_cast<uintptr_t>(A.a) & 15) == 0 && !(dbg & 64);
     if (in_gemm) {
         p.own.a = A.a;
@@ -935,11 +952,17 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         if (const char* e = std::getenv("RTNQ_WGEMM_CTAS")) G = std::atoi(e);
         G = G < 1 ? 1 : G;
         p.G = int(p.U < G ? p.U : G);
-        cudaError_t e = nt == 5    ? i4::launch_nt<5>(p, st)
-                      : nt == 10 ? i4::launch_nt<10>(p, st)
-                      : nt == 16 ? i4::launch_nt<16>(p, st)
-                      : nt == 32 ? i4::launch_nt<32>(p, st)
-                                 : i4::launch_nt<64>(p, st);
+        cudaError_t e = A.bits == 8
+            ? (nt == 5    ? i4::launch_nt<5, 8>(p, st)
+               : nt == 10 ? i4::launch_nt<10, 8>(p, st)
+               : nt == 16 ? i4::launch_nt<16, 8>(p, st)
+               : nt == 32 ? i4::launch_nt<32, 8>(p, st)
+                          : i4::launch_nt<64, 8>(p, st))
+            : (nt == 5    ? i4::launch_nt<5, 4>(p, st)
+               : nt == 10 ? i4::launch_nt<10, 4>(p, st)
+               : nt == 16 ? i4::launch_nt<16, 4>(p, st)
+               : nt == 32 ? i4::launch_nt<32, 4>(p, st)
+                          : i4::launch_nt<64, 4>(p, st));
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -5,7 +5,7 @@ sys.path.insert(0, os.getcwd())
 import paper_2505_15909_b200 as rq
 B = int(os.environ.get("B", "16")); BITS = int(os.environ.get("BITS", "8"))
 n, k = 28672, 4096
-g = 128 if BITS == 4 else 4096
+g = int(os.environ.get("G", "128" if BITS == 4 else "4096"))
 qs = [rq.quantize_pack(((torch.rand(n, k, device="cuda") * 2 - 1) * 0.02).to(torch.bfloat16), BITS, g) for _ in range(4)]
 x = torch.empty(B, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
 out = torch.empty(B, n, device="cuda", dtype=torch.bfloat16)

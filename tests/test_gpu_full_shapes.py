@@ -204,3 +204,24 @@ def test_linear_non_finite_activations_raise(kind):
     with pytest.raises(rq.InvalidInputError):
         rq.check_flag(err)
     rq.check_flag(err)  # cleared by the check
+
+
+@pytest.mark.parametrize("n,k,m", [(528, 1024, 1), (528, 1024, 16), (4096, 4096, 5), (2000, 14336, 33), (28672, 4096, 16),
+                                   (300, 256, 70)])
+def test_w8_group128_int8_path(oracle, n, k, m):
+    """W8 with group-128 scales (config 4's selective 8-bit module) on the int8 tensor-core kernel:
+    NATIVE_I8 tiles read from shared memory, one TMEM accumulator per group (wgemm_i4.cu, BITS = 8).
+    Codes bit-exact (re-encoded oracle codes), output within 1e-5 of the f64 oracle."""
+    g = 128
+    gen = torch.Generator(device="cuda").manual_seed(n + k + m)
+    w = ((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
+    q = rq.quantize_pack(w, 8, g, scales_f16=True)
+    assert q.layout == rq.NATIVE_I8
+    codes, scales = oracle.quantize(w.float().cpu().numpy(), 8, g)
+    assert np.array_equal(q.codes.cpu().numpy(), encode_native_i8(codes))
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1, generator=gen).to(torch.bfloat16)
+    out = rq.linear(a, q, out_dtype=torch.float32)
+    assert torch.equal(out, rq.linear(a, q, out_dtype=torch.float32))  # deterministic
+    s16w = oracle.f16_round(scales).view(np.float16).astype(np.float32)
+    ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+    assert rel_frob(out.cpu().numpy(), ref) <= TOL
