@@ -44,7 +44,7 @@ using namespace imma;
 
 constexpr int kKB = 128;              // k-block = one quantization group = one tile
 constexpr int kTile = kRows * 64;     // 8 KiB of nibbles
-constexpr int kEpi0 = 4, kExp0 = 8, kEpiB0 = 12;  // epilogue warpgroup B: warps 12-15
+constexpr int kEpi0 = 4, kExp0 = 8, kEpiB0 = 8;  // epilogue warpgroup B (EW = 2): the expansion warps
 
 struct Params {
     CUtensorMap tmap_p;      // planes [3][M][K] s8, box {128, PT, 3}, SWIZZLE_128B
@@ -84,9 +84,12 @@ struct Geo {
 #ifndef RTNQ_I4_EW
 #define RTNQ_I4_EW 1
 #endif
-    static constexpr int EW = RTNQ_I4_EW;  // 2: a second epilogue warpgroup (512 threads) takes the
-                                           // odd groups of every stage (measured slower)
-    static constexpr int THREADS = EW == 2 ? 512 : 384;
+    // EW = 2: the expansion warps (8-11) are a second epilogue warpgroup as well: they take the odd
+    // groups of every stage's epilogue, interleaved with their expansion work (one stage of
+    // epilogue per stage of expansion, NP stages behind).  Correct (tests pass with it) but
+    // measured slower (gate_up 22.3 vs 21.8 us at batch 16, 17.8 vs 15.5 at batch 1), so off.
+    static constexpr int EW = RTNQ_I4_EW;
+    static constexpr int THREADS = 384;
     static constexpr int SCR_BYTES = EW == 2 ? ACC * kRows * 4 : 0;  // warpgroup B's partial sums
     // The A operand of a group is 4 k-steps of 32 codes.  The first KT come from TMEM (tcgen05.st
     // by the expansion; the MMA's A reads share the 64 B/clk TMEM read port with the epilogue's
@@ -254,6 +257,108 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                            const_cast<int32_t*>(p.texp), threadIdx.x - kEpi0 * 32, 256, 3, pred);
     }
 
+    // ===================== expansion: nibbles -> s8 (16 x code) in TMEM ===============
+    // One handshake per stage (TPS groups): A pair slot xsi % AP, accumulator slot xsi % NP.
+    // exp_step() expands one stage; run by warps 8-11 (alone, or interleaved with their share of
+    // the epilogue when EW == 2).
+    const int xrow = threadIdx.x - kExp0 * 32;  // one xrow of the tile per thread = TMEM lane
+    const uint32_t sw_in = uint32_t((xrow >> 1) & 3);
+    const uint32_t xlane_base = uint32_t((warp & 3) * 32) << 16;
+    Cursor<TPS> xcu(u0, u1, p.KBLK);
+    int xs = 0, xsi = 0;
+    uint32_t xph = 0;
+    long long x_full = 0, x_aempty = 0, x_tfree = 0, x_work = 0;
+    auto exp_step = [&]() {
+        const int n = xcu.chunk();
+        const int slot0 = xcu.kb & (TPS - 1);
+        const int64_t left = p.N - int64_t(xcu.b) * kRows;
+        const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
+        const int ap = xsi % AP, np = xsi % NP;
+        {
+            I4_T0();
+            mbar_wait(&full[xs], xph);
+            I4_ACC(x_full);
+        }
+        if (warp == kExp0) I4_TL(xsi, 11);
+        {
+            I4_T0();
+            if (BITS == 4 && xsi >= AP) mbar_wait(&aempty[ap], uint32_t(xsi / AP - 1) & 1u);
+            I4_ACC(x_aempty);
+        }
+        if (warp == kExp0) I4_TL(xsi, 12);
+        {
+            I4_T0();
+            if (xsi >= NP) mbar_wait(&tfree[np], uint32_t(xsi / NP - 1) & 1u);
+            I4_ACC(x_tfree);
+        }
+        const long long _tw = (dbg_ & 32) ? clock64() : 0;
+        if (warp == kExp0) I4_TL(xsi, 2);
+        const uint8_t* st = smem + xs * GG::STAGE_BYTES;
+        if (BITS == 8) {
+            // W8: the MMA reads the s8 tiles from shared memory; only the group scales move
+#pragma unroll
+            for (int j = 0; j < TPS; ++j) {
+                if (j >= n) break;
+                const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
+                sring[(np * TPS + j) * kRows + xrow] = xrow < r8 ? __half2float(__ushort_as_half(sc[xrow])) : 0.0f;
+            }
+        } else if (!(dbg_ & 65536)) {
+            // two groups at a time: their code loads first (latency overlap), then expand and store
+            constexpr int JP = TPS < 2 ? TPS : 2;
+#pragma unroll
+            for (int j0 = 0; j0 < TPS; j0 += JP) {
+                if (j0 >= n) break;
+                uint4 w[JP][4];
+#pragma unroll
+                for (int jj = 0; jj < JP; ++jj)
+                    if (j0 + jj < n) {
+                        const uint8_t* src = st + GG::CODE_OFF + (slot0 + j0 + jj) * GG::TILE + xrow * 64;
+#pragma unroll
+                        for (uint32_t q = 0; q < 4; ++q)
+                            w[jj][q] = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
+                    }
+                float scv[JP];
+#pragma unroll
+                for (int jj = 0; jj < JP; ++jj) {
+                    const uint16_t* sc =
+                        reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + (j0 + jj) * r8;
+                    scv[jj] = (j0 + jj < n && xrow < r8) ? __half2float(__ushort_as_half(sc[xrow])) * 0.0625f : 0.0f;
+                }
+#pragma unroll
+                for (int jj = 0; jj < JP; ++jj) {
+                    const int j = j0 + jj;
+                    if (j >= n) break;
+                    uint32_t v[32];  // TMEM column c of this xrow holds k = 4c .. 4c + 3
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q) {
+                        const uint32_t ww[4] = {w[jj][q].x, w[jj][q].y, w[jj][q].z, w[jj][q].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            v[4 * q + e] = ww[e] & 0xF0F0F0F0u;               // k = 16q + 4e ..
+                            v[16 + 4 * q + e] = (ww[e] & 0x0F0F0F0Fu) * 16u;  // k = 64 + 16q + 4e ..
+                        }
+                    }
+                    const int slot = ap * TPS + j;
+                    static_assert(GG::KT == 4, "A operand entirely from TMEM");
+                    if (!(dbg_ & 8)) {
+                        tmem_st32(tmem + xlane_base + uint32_t(GG::A_COL + slot * 32), v);
+                    } else if (v[0] == 0x12345u) {
+                        g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
+                    }
+                    sring[(np * TPS + j) * kRows + xrow] = scv[jj];
+                }
+            }
+        }
+        if constexpr (BITS == 4) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[xs]);
+        if (warp == kExp0) I4_TL(xsi, 3);
+        if (dbg_ & 32) x_work += clock64() - _tw;
+        xcu.advance(n);
+        ++xsi;
+        if (++xs == STAGES) xs = 0, xph ^= 1u;
+    };
     if (warp == 0 || warp == 2) {
         // ===================== producers: warp 0 codes + scales, warp 2 planes ============
         const bool codes = warp == 0;
@@ -310,107 +415,8 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                 asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + u0 / p.KBLK) : "memory");
             }
         }
-    } else if (warp >= kExp0 && warp < kExp0 + 4) {
-        // ===================== expansion: nibbles -> s8 (16 x code) in TMEM ===============
-        // One handshake per stage (TPS groups): A pair slot si % AP, accumulator slot si % NP.
-        const int row = threadIdx.x - kExp0 * 32;  // one row of the tile per thread = TMEM lane
-        const uint32_t sw_in = uint32_t((row >> 1) & 3);
-        const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-        Cursor<TPS> cu(u0, u1, p.KBLK);
-        int s = 0, si = 0;
-        uint32_t ph = 0;
-        long long x_full = 0, x_aempty = 0, x_tfree = 0, x_work = 0;
-        while (cu.more()) {
-            const int n = cu.chunk();
-            const int slot0 = cu.kb & (TPS - 1);
-            const int64_t left = p.N - int64_t(cu.b) * kRows;
-            const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
-            const int ap = si % AP, np = si % NP;
-            {
-                I4_T0();
-                mbar_wait(&full[s], ph);
-                I4_ACC(x_full);
-            }
-            if (warp == kExp0) I4_TL(si, 11);
-            {
-                I4_T0();
-                if (BITS == 4 && si >= AP) mbar_wait(&aempty[ap], uint32_t(si / AP - 1) & 1u);
-                I4_ACC(x_aempty);
-            }
-            if (warp == kExp0) I4_TL(si, 12);
-            {
-                I4_T0();
-                if (si >= NP) mbar_wait(&tfree[np], uint32_t(si / NP - 1) & 1u);
-                I4_ACC(x_tfree);
-            }
-            const long long _tw = (dbg_ & 32) ? clock64() : 0;
-            if (warp == kExp0) I4_TL(si, 2);
-            const uint8_t* st = smem + s * GG::STAGE_BYTES;
-            if (BITS == 8) {
-                // W8: the MMA reads the s8 tiles from shared memory; only the group scales move
-#pragma unroll
-                for (int j = 0; j < TPS; ++j) {
-                    if (j >= n) break;
-                    const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + j * r8;
-                    sring[(np * TPS + j) * kRows + row] = row < r8 ? __half2float(__ushort_as_half(sc[row])) : 0.0f;
-                }
-            } else if (!(dbg_ & 65536)) {
-                // two groups at a time: their code loads first (latency overlap), then expand and store
-                constexpr int JP = TPS < 2 ? TPS : 2;
-#pragma unroll
-                for (int j0 = 0; j0 < TPS; j0 += JP) {
-                    if (j0 >= n) break;
-                    uint4 w[JP][4];
-#pragma unroll
-                    for (int jj = 0; jj < JP; ++jj)
-                        if (j0 + jj < n) {
-                            const uint8_t* src = st + GG::CODE_OFF + (slot0 + j0 + jj) * GG::TILE + row * 64;
-#pragma unroll
-                            for (uint32_t q = 0; q < 4; ++q)
-                                w[jj][q] = *reinterpret_cast<const uint4*>(src + ((q ^ sw_in) << 4));
-                        }
-                    float scv[JP];
-#pragma unroll
-                    for (int jj = 0; jj < JP; ++jj) {
-                        const uint16_t* sc =
-                            reinterpret_cast<const uint16_t*>(st + GG::SC_OFF + slot0 * 256) + (j0 + jj) * r8;
-                        scv[jj] = (j0 + jj < n && row < r8) ? __half2float(__ushort_as_half(sc[row])) * 0.0625f : 0.0f;
-                    }
-#pragma unroll
-                    for (int jj = 0; jj < JP; ++jj) {
-                        const int j = j0 + jj;
-                        if (j >= n) break;
-                        uint32_t v[32];  // TMEM column c of this row holds k = 4c .. 4c + 3
-#pragma unroll
-                        for (uint32_t q = 0; q < 4; ++q) {
-                            const uint32_t ww[4] = {w[jj][q].x, w[jj][q].y, w[jj][q].z, w[jj][q].w};
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                v[4 * q + e] = ww[e] & 0xF0F0F0F0u;               // k = 16q + 4e ..
-                                v[16 + 4 * q + e] = (ww[e] & 0x0F0F0F0Fu) * 16u;  // k = 64 + 16q + 4e ..
-                            }
-                        }
-                        const int slot = ap * TPS + j;
-                        static_assert(GG::KT == 4, "A operand entirely from TMEM");
-                        if (!(dbg_ & 8)) {
-                            tmem_st32(tmem + lane_base + uint32_t(GG::A_COL + slot * 32), v);
-                        } else if (v[0] == 0x12345u) {
-                            g_i4_dbg[0] = v[1] + v[31];  // keep the expansion alive
-                        }
-                        sring[(np * TPS + j) * kRows + row] = scv[jj];
-                    }
-                }
-            }
-            if constexpr (BITS == 4) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[ap]), mbar_arrive(&sfull[np]), mbar_arrive(&empty[s]);
-            if (warp == kExp0) I4_TL(si, 3);
-            if (dbg_ & 32) x_work += clock64() - _tw;
-            cu.advance(n);
-            ++si;
-            if (++s == STAGES) s = 0, ph ^= 1u;
-        }
+    } else if (warp >= kExp0 && warp < kExp0 + 4 && EW == 1) {
+        while (xcu.more()) exp_step();
         if ((dbg_ & 32) && threadIdx.x == kExp0 * 32) {
             g_i4_dbg[c * 16 + 2] = x_full, g_i4_dbg[c * 16 + 3] = x_aempty;
             g_i4_dbg[c * 16 + 4] = x_tfree, g_i4_dbg[c * 16 + 6] = x_work;
@@ -507,226 +513,237 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         int si = 0, seg_kb0 = cu.kb;
         long long e_wait = 0, e_work = 0, e_ld = 0;
         const long long e_t0 = clock64();
-        while (cu.more()) {
-            const int n = cu.chunk();
-            const bool seg_end = cu.seg_end(n);
-            const int b = cu.b;
-            const int np = si % NP;
-            {
-                I4_T0();
-                mbar_wait(&sfull[np], uint32_t(si / NP) & 1u);
-                mbar_wait(&tfull[np], uint32_t(si / NP) & 1u);
-                I4_ACC(e_wait);
-            }
-            const long long _tw = (dbg_ & 32) ? clock64() : 0;
-            if (warp == kEpi0) I4_TL(si, 6);
-            fence_after();
-            float scg[TPS], sg2 = 0.0f;
+        // one stage of this warpgroup's epilogue
+        auto epi_step = [&]() {
+        const int n = cu.chunk();
+        const bool seg_end = cu.seg_end(n);
+        const int b = cu.b;
+        const int np = si % NP;
+        {
+            I4_T0();
+            mbar_wait(&sfull[np], uint32_t(si / NP) & 1u);
+            mbar_wait(&tfull[np], uint32_t(si / NP) & 1u);
+            I4_ACC(e_wait);
+        }
+        const long long _tw = (dbg_ & 32) ? clock64() : 0;
+        if (warp == kEpi0) I4_TL(si, 6);
+        fence_after();
+        float scg[TPS], sg2 = 0.0f;
 #pragma unroll
-            for (int j = 0; j < TPS; ++j) scg[j] = j < n ? sring[(np * TPS + j) * kRows + row] : 0.0f;
-            // this warpgroup's groups of the stage: [j0, j1)
-            const int j0 = EW == 2 ? eg : 0, j1 = EW == 2 ? (eg < n ? eg + 1 : eg) : n;
+        for (int j = 0; j < TPS; ++j) scg[j] = j < n ? sring[(np * TPS + j) * kRows + row] : 0.0f;
+        // this warpgroup's groups of the stage: [j0, j1)
+        const int j0 = EW == 2 ? eg : 0, j1 = EW == 2 ? (eg < n ? eg + 1 : eg) : n;
 #pragma unroll
-            // token chunks of CH: plane q of token t is accumulator column q * PT + t
-            constexpr int CH = PT >= 16 ? 16 : PT;
-            constexpr int LDC = PT >= 16 ? 16 : GG::DN;  // columns loaded per plane/chunk
+        // token chunks of CH: plane q of token t is accumulator column q * PT + t
+        constexpr int CH = PT >= 16 ? 16 : PT;
+        constexpr int LDC = PT >= 16 ? 16 : GG::DN;  // columns loaded per plane/chunk
 #pragma unroll
-            for (int jj = 0; jj < ((dbg_ & 131072) ? 0 : PT); jj += CH) {
-                // chunk jj of every group of the stage; group j + 1's TMEM loads are in flight
-                // while group j's accumulators are combined
-                // one warpgroup per group (EW == 2) keeps one group's registers only
-                // double-buffered: group j + 1's TMEM loads are in flight while group j is combined
-                constexpr int NB = EW == 2 ? 1 : (TPS < 2 ? 1 : 2);
-                uint32_t d[NB][PT >= 16 ? 3 : 1][LDC];
-                auto load = [&](int j) {
-                    const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
-                    const int bj = j % NB;
-                    if (!(dbg_ & 16)) {
-                        if constexpr (PT >= 16) {
-                            ld16(ta, d[bj][0]);
-                            ld16(ta + PT, d[bj][1]);
-                            ld16(ta + 2 * PT, d[bj][2]);
-                        } else {
-#pragma unroll
-                            for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, d[bj][0] + 16 * h);
-                        }
+        for (int jj = 0; jj < ((dbg_ & 131072) ? 0 : PT); jj += CH) {
+            // chunk jj of every group of the stage; group j + 1's TMEM loads are in flight
+            // while group j's accumulators are combined
+            // one warpgroup per group (EW == 2) keeps one group's registers only
+            // double-buffered: group j + 1's TMEM loads are in flight while group j is combined
+            constexpr int NB = EW == 2 ? 1 : (TPS < 2 ? 1 : 2);
+            uint32_t d[NB][PT >= 16 ? 3 : 1][LDC];
+            auto load = [&](int j) {
+                const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
+                const int bj = j % NB;
+                if (!(dbg_ & 16)) {
+                    if constexpr (PT >= 16) {
+                        ld16(ta, d[bj][0]);
+                        ld16(ta + PT, d[bj][1]);
+                        ld16(ta + 2 * PT, d[bj][2]);
                     } else {
 #pragma unroll
-                        for (int e = 0; e < LDC; ++e)
-#pragma unroll
-                            for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[bj][q3][e] = uint32_t(row + e);
+                        for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, d[bj][0] + 16 * h);
                     }
-                };
-                auto combine = [&](int j) {
+                } else {
 #pragma unroll
-                    for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
-                        uint32_t u0v, u1v, u2v;
-                        const int dj = j % NB;
-                        if constexpr (PT >= 16) {
-                            u0v = d[dj][0][e], u1v = d[dj][PT >= 16 ? 1 : 0][e], u2v = d[dj][PT >= 16 ? 2 : 0][e];
-                        } else {
-                            u0v = d[dj][0][e], u1v = d[dj][0][(PT + e) % LDC], u2v = d[dj][0][(2 * PT + e) % LDC];
-                        }
-                        // planes 1 and 2 combined exactly in int32 (|D1 * 128 + D2| < 2^28); D0
-                        // (< 2^21) converts exactly, D12's rounding (2^-24 of it) sits 2^-30 below
-                        // D0 after the 2^-14 weight
-                        const float x0 = float(int32_t(u0v));
-                        const float x12 = float(int32_t(u1v) * 128 + int32_t(u2v));
-                        acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), EW == 2 ? sg2 : scg[j], acc[jj + e]);
-                    }
-                };
-                if constexpr (EW == 2) {
-                    // warpgroup eg takes the stage's groups eg, eg + 2, ... (compile-time local index)
+                    for (int e = 0; e < LDC; ++e)
 #pragma unroll
-                    for (int jl = 0; jl < (TPS + 1) / 2; ++jl) {
-                        const int j = 2 * jl + eg;
-                        if (j >= n) break;
-                        sg2 = sring[(np * TPS + j) * kRows + row];
-                        load(j);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        combine(j);
+                        for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[bj][q3][e] = uint32_t(row + e);
+                }
+            };
+            auto combine = [&](int j) {
+#pragma unroll
+                for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
+                    uint32_t u0v, u1v, u2v;
+                    const int dj = j % NB;
+                    if constexpr (PT >= 16) {
+                        u0v = d[dj][0][e], u1v = d[dj][PT >= 16 ? 1 : 0][e], u2v = d[dj][PT >= 16 ? 2 : 0][e];
+                    } else {
+                        u0v = d[dj][0][e], u1v = d[dj][0][(PT + e) % LDC], u2v = d[dj][0][(2 * PT + e) % LDC];
                     }
-                } else if (j0 < j1) {
-                    load(j0);
+                    // planes 1 and 2 combined exactly in int32 (|D1 * 128 + D2| < 2^28); D0
+                    // (< 2^21) converts exactly, D12's rounding (2^-24 of it) sits 2^-30 below
+                    // D0 after the 2^-14 weight
+                    const float x0 = float(int32_t(u0v));
+                    const float x12 = float(int32_t(u1v) * 128 + int32_t(u2v));
+                    acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), EW == 2 ? sg2 : scg[j], acc[jj + e]);
+                }
+            };
+            if constexpr (EW == 2) {
+                // warpgroup eg takes the stage's groups eg, eg + 2, ... (compile-time local index)
+#pragma unroll
+                for (int jl = 0; jl < (TPS + 1) / 2; ++jl) {
+                    const int j = 2 * jl + eg;
+                    if (j >= n) break;
+                    sg2 = sring[(np * TPS + j) * kRows + row];
+                    load(j);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (dbg_ & 32) {
-                        const long long t = clock64();
-                        e_ld += t - _tw;
-                    }
+                    combine(j);
+                }
+            } else if (j0 < j1) {
+                load(j0);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (dbg_ & 32) {
+                    const long long t = clock64();
+                    e_ld += t - _tw;
+                }
 #pragma unroll
-                    for (int j = 0; j < TPS; ++j) {
-                        if (j < j0 || j >= j1) continue;
-                        if (j + 1 < j1) load(j + 1);
-                        combine(j);
-                        if (j + 1 < j1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    }
+                for (int j = 0; j < TPS; ++j) {
+                    if (j < j0 || j >= j1) continue;
+                    if (j + 1 < j1) load(j + 1);
+                    combine(j);
+                    if (j + 1 < j1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 }
             }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tfree[np]);
-            if (warp == kEpi0) I4_TL(si, 7);
-            if (dbg_ & 32) e_work += clock64() - _tw;
-            ++si;
-            if (seg_end && EW == 2) {  // warpgroup B -> A through shared memory
-                float4* sc4 = reinterpret_cast<float4*>(scr) + row * (NT / 4);
-                if (eg == 1) {
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tfree[np]);
+        if (warp == kEpi0) I4_TL(si, 7);
+        if (dbg_ & 32) e_work += clock64() - _tw;
+        ++si;
+        if (seg_end && EW == 2) {  // warpgroup B -> A through shared memory
+            float4* sc4 = reinterpret_cast<float4*>(scr) + row * (NT / 4);
+            if (eg == 1) {
 #pragma unroll
-                    for (int j = 0; j < NT / 4; ++j)
-                        sc4[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-                }
-                asm volatile("bar.sync 2, 256;" ::: "memory");
-                if (eg == 1) {
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
-                    cu.advance(n);
-                    continue;
-                }
-#pragma unroll
-                for (int j = 0; j < NT / 4; ++j) {
-                    const float4 x = sc4[j];
-                    acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
-                }
+                for (int j = 0; j < NT / 4; ++j)
+                    sc4[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
             }
-            if (seg_end) {
+            asm volatile("bar.sync 2, 256;" ::: "memory");
+            if (eg == 1) {
 #pragma unroll
-                for (int t = 0; t < NT; ++t) acc[t] *= pow_s[t];
-                const int kbe = cu.kb + n;
-                const bool sole = seg_kb0 == 0 && kbe == p.KBLK;
-                const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
-                const int64_t n0 = int64_t(b) * kRows;
-                if (p.csize > 1) {
-                    // cluster split-K (one segment per CTA): push partials into the leader
-                    const int rank = c % p.csize;
-                    constexpr uint32_t kSlot = uint32_t(NT) * kRows * 4;
-                    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-                    if (rank == 0) {
-                        if (et == 0) {
-                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull)),
-                                         "r"(uint32_t(p.csize - 1) * kSlot)
+                for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+                cu.advance(n);
+                return;
+            }
+#pragma unroll
+            for (int j = 0; j < NT / 4; ++j) {
+                const float4 x = sc4[j];
+                acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
+            }
+        }
+        if (seg_end) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) acc[t] *= pow_s[t];
+            const int kbe = cu.kb + n;
+            const bool sole = seg_kb0 == 0 && kbe == p.KBLK;
+            const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
+            const int64_t n0 = int64_t(b) * kRows;
+            if (p.csize > 1) {
+                // cluster split-K (one segment per CTA): push partials into the leader
+                const int rank = c % p.csize;
+                constexpr uint32_t kSlot = uint32_t(NT) * kRows * 4;
+                asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+                if (rank == 0) {
+                    if (et == 0) {
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull)),
+                                     "r"(uint32_t(p.csize - 1) * kSlot)
+                                     : "memory");
+                        for (int r = 1; r < p.csize; ++r) {
+                            uint32_t ra;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(go)), "r"(r));
+                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra)
                                          : "memory");
-                            for (int r = 1; r < p.csize; ++r) {
-                                uint32_t ra;
-                                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(go)), "r"(r));
-                                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra)
-                                             : "memory");
-                            }
                         }
-                        mbar_wait(rfull, 0);
-                        const float4* red = reinterpret_cast<const float4*>(smem);
-                        for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
-#pragma unroll
-                            for (int j = 0; j < NT / 4; ++j) {
-                                const float4 x = red[((r - 1) * kRows + row) * (NT / 4) + j];
-                                acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
-                            }
-                        }
-                        if (row < rows)
-#pragma unroll
-                            for (int m = 0; m < NT; ++m)
-                                if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
-                    } else {
-                        mbar_wait(go, 0);
-                        uint32_t dst, rb;
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst)
-                                     : "r"(su32(smem) + uint32_t(((rank - 1) * kRows + row) * NT * 4)));
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(su32(rfull)));
-#pragma unroll
-                        for (int j = 0; j < NT / 4; ++j)
-                            asm volatile(
-                                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                                    dst + 16u * j),
-                                "f"(acc[4 * j]), "f"(acc[4 * j + 1]), "f"(acc[4 * j + 2]), "f"(acc[4 * j + 3]), "r"(rb)
-                                : "memory");
                     }
-                } else if (sole) {
+                    mbar_wait(rfull, 0);
+                    const float4* red = reinterpret_cast<const float4*>(smem);
+                    for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
+#pragma unroll
+                        for (int j = 0; j < NT / 4; ++j) {
+                            const float4 x = red[((r - 1) * kRows + row) * (NT / 4) + j];
+                            acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
+                        }
+                    }
                     if (row < rows)
 #pragma unroll
                         for (int m = 0; m < NT; ++m)
                             if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
                 } else {
-                    // stream-K: the owner holds the row-block's first k-block (its last segment);
-                    // the others hand over partials from their first segment (slot = CTA)
-                    const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
-                    const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
-                    if (c == c_first) {
-                        if (et == 0) {
-                            const int want = c_last - c_first;
-                            int got;
-                            do {
-                                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(p.counters + b) : "memory");
-                            } while (got < want);
-                            p.counters[b] = 0;  // ready for the next launch (stream-ordered)
-                        }
-                        asm volatile("bar.sync 1, 128;" ::: "memory");
-                        for (int cc = c_first + 1; cc <= c_last; ++cc) {  // fixed order: deterministic
-                            const float4* src = reinterpret_cast<const float4*>(p.partials + (int64_t(cc) * kRows + row) * NT);
+                    mbar_wait(go, 0);
+                    uint32_t dst, rb;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst)
+                                 : "r"(su32(smem) + uint32_t(((rank - 1) * kRows + row) * NT * 4)));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(su32(rfull)));
 #pragma unroll
-                            for (int j = 0; j < NT / 4; ++j) {
-                                const float4 x = __ldcg(src + j);
-                                acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
-                            }
-                        }
-                        if (row < rows)
-#pragma unroll
-                            for (int m = 0; m < NT; ++m)
-                                if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
-                    } else {
-                        // contributor (its first segment): store the partial; warp 3 publishes it
-                        // (gpu-scope fence + counter), off this pipeline's critical path
-                        float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
-#pragma unroll
-                        for (int j = 0; j < NT / 4; ++j)
-                            mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(pub);
-                    }
+                    for (int j = 0; j < NT / 4; ++j)
+                        asm volatile(
+                            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                                dst + 16u * j),
+                            "f"(acc[4 * j]), "f"(acc[4 * j + 1]), "f"(acc[4 * j + 2]), "f"(acc[4 * j + 3]), "r"(rb)
+                            : "memory");
                 }
+            } else if (sole) {
+                if (row < rows)
 #pragma unroll
-                for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
-                seg_kb0 = kbe == p.KBLK ? 0 : kbe;
+                    for (int m = 0; m < NT; ++m)
+                        if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+            } else {
+                // stream-K: the owner holds the row-block's first k-block (its last segment);
+                // the others hand over partials from their first segment (slot = CTA)
+                const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
+                const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
+                if (c == c_first) {
+                    if (et == 0) {
+                        const int want = c_last - c_first;
+                        int got;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(p.counters + b) : "memory");
+                        } while (got < want);
+                        p.counters[b] = 0;  // ready for the next launch (stream-ordered)
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    for (int cc = c_first + 1; cc <= c_last; ++cc) {  // fixed order: deterministic
+                        const float4* src = reinterpret_cast<const float4*>(p.partials + (int64_t(cc) * kRows + row) * NT);
+#pragma unroll
+                        for (int j = 0; j < NT / 4; ++j) {
+                            const float4 x = __ldcg(src + j);
+                            acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
+                        }
+                    }
+                    if (row < rows)
+#pragma unroll
+                        for (int m = 0; m < NT; ++m)
+                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                } else {
+                    // contributor (its first segment): store the partial; warp 3 publishes it
+                    // (gpu-scope fence + counter), off this pipeline's critical path
+                    float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
+#pragma unroll
+                    for (int j = 0; j < NT / 4; ++j)
+                        mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(pub);
+                }
             }
-            cu.advance(n);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+            seg_kb0 = kbe == p.KBLK ? 0 : kbe;
+        }
+        cu.advance(n);
+        };
+        if (EW == 2 && eg == 1) {
+            // the expansion warps: expansion of stage xsi, and the epilogue of the stage NP behind
+            // (its accumulators cannot be reused before; the expansion waits for them too)
+            while (xcu.more() || cu.more()) {
+                if (xcu.more() && (!cu.more() || xsi < si + NP)) exp_step();
+                else epi_step();
+            }
+        } else {
+            while (cu.more()) epi_step();
         }
         if ((dbg_ & 64) && et == 0) g_i4_dbg[c * 16 + 4] = gtime();
         if ((dbg_ & 32) && et == 0 && eg == 0)
