@@ -237,6 +237,54 @@ rtnq_status rtnq_dev_decode_attention_ws(const void* qkv, void* k_cache, void* v
  * RTNQ_E_INVALID_INPUT if it was set. */
 rtnq_status rtnq_dev_check_flag(int32_t* err_flag, void* stream);
 
+/* ---- tensor-parallel partial sums over peer memory ------------------
+ * Replaces the allreduce the reference's tensor-parallel split would need after a
+ * row-split linear (no reference counterpart: the reference is single-device; the
+ * sharding follows the Llama TP layout of SURVEY §8e).
+ *
+ * Every rank owns one symmetric buffer of rtnq_peer_buffer_bytes(cap) bytes
+ * (rtnq_peer_alloc: zero-filled, its own allocation; cap = elements per slot, a
+ * multiple of 8, >= tokens x hidden) and maps every peer's buffer: same process (one process
+ * driving several devices, rtnq_peer_enable) or other processes (CUDA IPC:
+ * rtnq_ipc_get_handle -> exchange -> rtnq_ipc_open).  peer_bufs[q] is rank q's
+ * buffer as seen from this rank's device.
+ *
+ * A round: every rank runs rtnq_dev_linear_peer (its row-split partial goes
+ * straight from the GEMM epilogue into its slot of every rank's buffer, bf16, then
+ * a release flag), then one consumer on its own buffer: rtnq_dev_add_rmsnorm_peer
+ * (x += sum of the partials, then RMSNorm, as rtnq_dev_add_rmsnorm with
+ * delta = allreduce(partial)) or rtnq_dev_peer_reduce.  The sum runs over ranks
+ * 0..world-1 in order in f32 with one bf16 rounding, so every rank gets the same
+ * bits.  Consumers wait on the device; a rank's next producer must follow its
+ * consumer in stream order. */
+#define RTNQ_IPC_HANDLE_BYTES 64
+size_t rtnq_peer_buffer_bytes(int64_t cap);
+/* a zero-filled symmetric buffer of its own cudaMalloc allocation on the current device (an IPC
+ * handle maps whole allocations, so the buffer must not be carved out of a pool) */
+rtnq_status rtnq_peer_alloc(int64_t cap, void** dev_ptr);
+rtnq_status rtnq_peer_free(void* dev_ptr);
+rtnq_status rtnq_ipc_get_handle(void* dev_ptr, void* handle);
+rtnq_status rtnq_ipc_open(const void* handle, void** dev_ptr);
+rtnq_status rtnq_ipc_close(void* dev_ptr);
+/* let `device` access `peer`'s memory (one process, several devices; no-op when equal) */
+rtnq_status rtnq_peer_enable(int device, int peer);
+/* rtnq_dev_linear_planes / rtnq_dev_linear with the output pushed to the peers:
+ * either `a` (bf16 m x k) or `planes` + `texp`; m <= 64, m * n <= cap. */
+rtnq_status rtnq_dev_linear_peer(const void* a, const int8_t* planes, const int32_t* texp, int64_t m,
+                                 int64_t k, const uint8_t* codes, rtnq_layout layout, int bits, int64_t n,
+                                 int64_t g, int ragged, const void* scales, int sdtype, int sorder,
+                                 void* const* peer_bufs, int world, int rank, int64_t cap,
+                                 int32_t* err_flag, void* ws, size_t ws_bytes, void* stream,
+                                 unsigned flags);
+/* x (m x h) += sum of the round's partials (this rank's buffer), out = rmsnorm(x) * weight,
+ * optional planes of out (as rtnq_dev_add_rmsnorm_planes). */
+rtnq_status rtnq_dev_add_rmsnorm_peer(void* x, void* peer_buf, int world, int64_t cap,
+                                      const void* weight, void* out, int64_t m, int64_t h, float eps,
+                                      int8_t* planes, int32_t* texp, void* stream);
+/* out[0..n) = (accumulate ? out + : ) sum of the round's partials. */
+rtnq_status rtnq_dev_peer_reduce(void* peer_buf, int world, int64_t cap, void* out, int64_t n,
+                                 int accumulate, void* stream);
+
 /* ---- host API (drop-in parity path; synchronous; host buffers) -------------------- */
 
 /* compute_scale (quant.hpp:48-50). */

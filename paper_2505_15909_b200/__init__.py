@@ -116,6 +116,19 @@ def lib():
     L.rtnq_dev_decode_attention_workspace_bytes.argtypes = [_i64, _i64, _i64, _i64]
     L.rtnq_dev_decode_attention_ws.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
                                                C.c_float, _p, _sz, _p]
+    L.rtnq_peer_buffer_bytes.restype = _sz
+    L.rtnq_peer_buffer_bytes.argtypes = [_i64]
+    L.rtnq_peer_alloc.argtypes = [_i64, C.POINTER(_p)]
+    L.rtnq_peer_free.argtypes = [_p]
+    L.rtnq_ipc_get_handle.argtypes = [_p, _p]
+    L.rtnq_ipc_open.argtypes = [_p, C.POINTER(_p)]
+    L.rtnq_ipc_close.argtypes = [_p]
+    L.rtnq_peer_enable.argtypes = [_i32, _i32]
+    L.rtnq_dev_linear_peer.argtypes = [_p, _p, _p, _i64, _i64, _p, Layout, _i32, _i64, _i64, _i32, _p,
+                                       _i32, _i32, _p, _i32, _i32, _i64, _p, _p, _sz, _p, C.c_uint]
+    L.rtnq_dev_add_rmsnorm_peer.argtypes = [_p, _p, _i32, _i64, _p, _p, _i64, _i64, C.c_float, _p, _p,
+                                            _p]
+    L.rtnq_dev_peer_reduce.argtypes = [_p, _i32, _i64, _p, _i64, _i32, _p]
     L.rtnq_f32_to_f16.argtypes = [_p, _i64, _p]
     L.rtnq_f16_to_f32.argtypes = [_p, _i64, _p]
     L.rtnq_plan_resolve.argtypes = [C.c_char_p, _i64, _p, C.c_char_p, _i64, _p]

@@ -528,6 +528,149 @@ rtnq_status rtnq_dev_linear_planes(const int8_t* planes, const int32_t* texp, in
     return RTNQ_OK;
 }
 
+// ---- tensor-parallel partial sums over peer memory (int8_mma.cuh protocol) --------
+
+size_t rtnq_peer_buffer_bytes(int64_t cap) { return cap < 0 ? 0 : peer_buffer_bytes(cap); }
+
+rtnq_status rtnq_peer_alloc(int64_t cap, void** dev_ptr) {
+    if (!dev_ptr || cap <= 0 || cap % 8) return fail(RTNQ_E_INVALID_INPUT, "cap must be a positive multiple of 8");
+    // a dedicated allocation: an IPC handle maps a whole allocation, so the buffer must start one
+    *dev_ptr = nullptr;
+    RTNQ_CUDA(cudaMalloc(dev_ptr, peer_buffer_bytes(cap)));
+    RTNQ_CUDA(cudaMemset(*dev_ptr, 0, peer_buffer_bytes(cap)));
+    RTNQ_CUDA(cudaDeviceSynchronize());
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_peer_free(void* dev_ptr) {
+    RTNQ_CUDA(cudaFree(dev_ptr));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_ipc_get_handle(void* dev_ptr, void* handle) {
+    if (!dev_ptr || !handle) return fail(RTNQ_E_INVALID_INPUT, "null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == RTNQ_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    RTNQ_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    std::memcpy(handle, &h, sizeof(h));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_ipc_open(const void* handle, void** dev_ptr) {
+    if (!dev_ptr || !handle) return fail(RTNQ_E_INVALID_INPUT, "null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    RTNQ_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_ipc_close(void* dev_ptr) {
+    RTNQ_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_peer_enable(int device, int peer) {
+    if (device == peer) return RTNQ_OK;
+    int can = 0;
+    RTNQ_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return fail(RTNQ_E_UNSUPPORTED, "no peer access between the two devices");
+    int cur = 0;
+    RTNQ_CUDA(cudaGetDevice(&cur));
+    RTNQ_CUDA(cudaSetDevice(device));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError(), e = cudaSuccess;
+    cudaSetDevice(cur);
+    RTNQ_CUDA(e);
+    return RTNQ_OK;
+}
+
+static rtnq_status peer_in(void* buf, int world, int64_t cap, PeerIn* pin) {
+    if (!buf) return fail(RTNQ_E_INVALID_INPUT, "null peer buffer");
+    if (world < 1 || world > kPeerMax) return fail(RTNQ_E_INVALID_INPUT, "peer world must be 1..8");
+    if (cap <= 0 || cap % 8 || (reinterpret_cast<uintptr_t>(buf) & 255))
+        return fail(RTNQ_E_INVALID_INPUT, "peer slot capacity must be a positive multiple of 8 elements, the "
+                                          "buffer 256-byte aligned");
+    pin->buf = static_cast<char*>(buf);
+    pin->world = world;
+    pin->cap = cap;
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_linear_peer(const void* a, const int8_t* planes, const int32_t* texp, int64_t m, int64_t k,
+                                 const uint8_t* codes, rtnq_layout layout, int bits, int64_t n, int64_t g,
+                                 int ragged, const void* scales, int sdtype, int sorder, void* const* peer_bufs,
+                                 int world, int rank, int64_t cap, int32_t* err, void* ws, size_t ws_bytes,
+                                 void* stream, unsigned flags) {
+    if (!valid_bits(bits)) return fail(RTNQ_E_INVALID_INPUT, "bits must be 4 or 8");
+    RTNQ_TRY(check_layout(layout));
+    if (m <= 0 || n <= 0 || k <= 0) return fail(RTNQ_E_SHAPE, "peer linear needs a non-empty output");
+    const int64_t gpr = rtnq_groups_per_row(g, ragged, k);
+    if (gpr < 0) return rtnq_status(-gpr);
+    if (!a == !planes || (planes && !texp))
+        return fail(RTNQ_E_INVALID_INPUT, "give either bf16 activations or their planes + exponents");
+    if (!peer_bufs || rank < 0 || rank >= world) return fail(RTNQ_E_INVALID_INPUT, "rank outside the world");
+    PeerIn own;
+    RTNQ_TRY(peer_in(peer_bufs[rank], world, cap, &own));
+    PeerOut po;
+    po.world = world;
+    po.rank = rank;
+    po.cap = cap;
+    for (int q = 0; q < world; ++q) {
+        if (!peer_bufs[q] || (reinterpret_cast<uintptr_t>(peer_bufs[q]) & 255))
+            return fail(RTNQ_E_INVALID_INPUT, "null or unaligned peer buffer");
+        po.bufs[q] = static_cast<char*>(peer_bufs[q]);
+    }
+    if (m * n > cap) return fail(RTNQ_E_INVALID_INPUT, "output larger than the peer slot");
+    const bool i8 = i8_path(RTNQ_BF16, layout, bits, g, k, sdtype);
+    const bool i4 = i4_path(RTNQ_BF16, layout, bits, g, sdtype, sorder);
+    if (!i8 && !i4)
+        return fail(RTNQ_E_UNSUPPORTED, "peer output comes from the int8 kernels: RTNQ_NATIVE_I4 (W4 g128) or "
+                                        "RTNQ_NATIVE_I8 codes, native f16 scales");
+    if (m > 64) return fail(RTNQ_E_UNSUPPORTED, "peer output: at most 64 tokens per launch");
+    if (const char* why = i8 ? wgemm_i8_unsupported(m, n, k, bits, g, RTNQ_BF16)
+                             : wgemm_i4_unsupported(m, n, k, bits, g, RTNQ_BF16))
+        return fail(RTNQ_E_UNSUPPORTED, why);
+    const size_t need = i8 ? wgemm_i8_workspace_bytes(m, n, k) : wgemm_i4_workspace_bytes(m, n, k);
+    if (ws_bytes < need)
+        return fail(RTNQ_E_INVALID_INPUT, "linear workspace too small: need " + std::to_string(need) + " bytes");
+    if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(codes) | reinterpret_cast<uintptr_t>(scales)) & 15)
+        return fail(RTNQ_E_INVALID_INPUT, "tensor-core path needs 16-byte aligned operands");
+    WgemmArgs A{a, RTNQ_BF16, m, n, k, codes, static_cast<const uint16_t*>(scales), bits, g,
+                nullptr, RTNQ_BF16, ws, ws_bytes, (flags & RTNQ_FLAG_PDL) != 0};
+    A.planes = planes;
+    A.texp = texp;
+    A.err = err;
+    A.peer = po;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    RTNQ_CUDA(i8 ? launch_wgemm_i8(A, st) : launch_wgemm_i4(A, st));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_add_rmsnorm_peer(void* x, void* peer_buf, int world, int64_t cap, const void* weight,
+                                      void* out, int64_t m, int64_t h, float eps, int8_t* planes, int32_t* texp,
+                                      void* stream) {
+    if (m <= 0 || h <= 0 || h % 16 || h / 8 > 32 * 256)
+        return fail(RTNQ_E_SHAPE, "peer rmsnorm needs h % 16 == 0, h <= 65536 and m > 0");
+    if (!planes != !texp) return fail(RTNQ_E_INVALID_INPUT, "planes and texp go together");
+    PeerIn pin;
+    RTNQ_TRY(peer_in(peer_buf, world, cap, &pin));
+    if (m * h > cap) return fail(RTNQ_E_INVALID_INPUT, "rows larger than the peer slot");
+    RTNQ_CUDA(launch_add_rmsnorm(x, nullptr, weight, out, m, h, eps, static_cast<cudaStream_t>(stream), planes,
+                                 texp, pin));
+    return RTNQ_OK;
+}
+
+rtnq_status rtnq_dev_peer_reduce(void* peer_buf, int world, int64_t cap, void* out, int64_t n, int accumulate,
+                                 void* stream) {
+    PeerIn pin;
+    RTNQ_TRY(peer_in(peer_buf, world, cap, &pin));
+    if (n <= 0 || n % 8 || n > cap) return fail(RTNQ_E_SHAPE, "reduce length must be a positive multiple of 8 "
+                                                              "within the slot");
+    if (reinterpret_cast<uintptr_t>(out) & 15) return fail(RTNQ_E_INVALID_INPUT, "out must be 16-byte aligned");
+    RTNQ_CUDA(launch_peer_reduce(pin, out, n, accumulate != 0, static_cast<cudaStream_t>(stream)));
+    return RTNQ_OK;
+}
+
 rtnq_status rtnq_dev_silu_mul(const void* gate_up, void* act, int64_t m, int64_t f, void* stream) {
     if (m < 0 || f <= 0 || f % 8) return fail(RTNQ_E_SHAPE, "silu_mul needs f % 8 == 0");
     if (m == 0) return RTNQ_OK;

@@ -186,7 +186,8 @@ __device__ __forceinline__ void planes_from_regs(const uint4 (&ov)[VPT], int n8,
 template <int VPT, int CL>
 __global__ void __launch_bounds__(kRowThreads) add_rmsnorm_rows_kernel(
     __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta, const __nv_bfloat16* __restrict__ w,
-    __nv_bfloat16* __restrict__ out, int h, float eps, int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
+    __nv_bfloat16* __restrict__ out, int h, float eps, int8_t* __restrict__ planes, int32_t* __restrict__ texp,
+    PeerIn pin) {
     pdl_prologue();
     __shared__ float red[kRowThreads / 32];
     __shared__ float cpart;
@@ -194,21 +195,48 @@ __global__ void __launch_bounds__(kRowThreads) add_rmsnorm_rows_kernel(
     __nv_bfloat16* xr = x + int64_t(row) * h;
     const __nv_bfloat16* dr = delta ? delta + int64_t(row) * h : nullptr;
     uint4 xv[VPT], dv[VPT];
+    if (pin.buf) {  // tensor parallel: delta = sum of every rank's partial of this round
+        const int e = *reinterpret_cast<volatile int*>(imma::peer_epoch(pin.buf)) + 1;
+        if (threadIdx.x == 0) imma::peer_wait(pin.buf, pin.world, e);
+        __syncthreads();
 #pragma unroll
-    for (int v = 0; v < VPT; ++v) {  // every load of the row in flight at once
-        const int vi = row_vec<CL>(rank, v);
-        if (vi < n8) {
-            xv[v] = *reinterpret_cast<const uint4*>(xr + vi * 8);
-            if (dr) dv[v] = *reinterpret_cast<const uint4*>(dr + vi * 8);
+        for (int v = 0; v < VPT; ++v) {
+            const int vi = row_vec<CL>(rank, v);
+            if (vi < n8) {
+                xv[v] = *reinterpret_cast<const uint4*>(xr + vi * 8);
+                float acc[8] = {};
+                for (int q = 0; q < pin.world; ++q) {
+                    const uint4 sv = imma::peer_ld16(imma::peer_slot(pin.buf, pin.cap, e & 1, q) + int64_t(row) * h + vi * 8);
+                    const __nv_bfloat162* sp = reinterpret_cast<const __nv_bfloat162*>(&sv);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float2 f = __bfloat1622float2(sp[j]);
+                        acc[2 * j] += f.x, acc[2 * j + 1] += f.y;
+                    }
+                }
+                __nv_bfloat162* dp = reinterpret_cast<__nv_bfloat162*>(&dv[v]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dp[j] = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {  // every load of the row in flight at once
+            const int vi = row_vec<CL>(rank, v);
+            if (vi < n8) {
+                xv[v] = *reinterpret_cast<const uint4*>(xr + vi * 8);
+                if (dr) dv[v] = *reinterpret_cast<const uint4*>(dr + vi * 8);
+            }
         }
     }
+    const bool has_d = dr || pin.buf;
     float ss = 0.0f;
 #pragma unroll
     for (int v = 0; v < VPT; ++v) {
         const int vi = row_vec<CL>(rank, v);
         if (vi >= n8) break;
         __nv_bfloat162* xp = reinterpret_cast<__nv_bfloat162*>(&xv[v]);
-        if (dr) {
+        if (has_d) {
             const __nv_bfloat162* dp = reinterpret_cast<const __nv_bfloat162*>(&dv[v]);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -241,6 +269,10 @@ __global__ void __launch_bounds__(kRowThreads) add_rmsnorm_rows_kernel(
         *reinterpret_cast<uint4*>(out + int64_t(row) * h + vi * 8) = ov[v];
     }
     if (planes) planes_from_regs<VPT, CL>(ov, n8, rank, row, gridDim.x / CL, h, planes, texp, red, &cpart);
+    if (pin.buf) {  // this CTA's reads of the round are done
+        __syncthreads();
+        if (threadIdx.x == 0) imma::peer_consumed_by(pin.buf, int(gridDim.x));
+    }
 }
 
 template <int VPT, int CL>
@@ -827,12 +859,14 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     }()
 
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
-                               int64_t h, float eps, cudaStream_t st, int8_t* planes, int32_t* texp) {
+                               int64_t h, float eps, cudaStream_t st, int8_t* planes, int32_t* texp,
+                               PeerIn pin) {
     if (h % 8) return cudaErrorInvalidValue;
     if (h / 8 <= 32 * kRowThreads)  // the row in registers (of a cluster of CTAs)
         return RTNQ_ROWS_DISPATCH(add_rmsnorm_rows_kernel, m, h / 8, st, static_cast<__nv_bfloat16*>(x),
                                   static_cast<const __nv_bfloat16*>(delta), static_cast<const __nv_bfloat16*>(w),
-                                  static_cast<__nv_bfloat16*>(out), int(h), eps, planes, texp);
+                                  static_cast<__nv_bfloat16*>(out), int(h), eps, planes, texp, pin);
+    if (pin.buf) return cudaErrorInvalidValue;
     return launch_pdl(add_rmsnorm_kernel, dim3(unsigned(m)), dim3(256), 8 * sizeof(float), st,
                       static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta),
                       static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(out), int(h), eps,

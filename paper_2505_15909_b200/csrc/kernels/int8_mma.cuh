@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "../common.cuh"
+#include "kernels.cuh"
 
 namespace rtnq_b200 {
 namespace imma {
@@ -418,6 +419,73 @@ __device__ __forceinline__ void row_to_planes(const uint16_t* __restrict__ rowp,
         for (int pl = 0; pl < 3; ++pl)
             *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
                 make_uint2(pk[pl][0], pk[pl][1]);
+    }
+}
+
+// ---- tensor-parallel partial sums over peer memory ------------------------------
+// Every rank owns one symmetric buffer (same layout, opened by every peer through CUDA IPC):
+//   header (256 B): int epoch (local), int flags[8] (flags[q]: last round rank q delivered here),
+//                   int done (producer CTAs finished), int consumed (consumer CTAs done)
+//   slots: [2 parities][8 ranks][cap] bf16 -- rank q's partial of round e lands in slot [e & 1][q]
+// A row-split linear of round e = epoch + 1 writes its output rows straight into its slot of
+// EVERY rank's buffer (P2P stores over NVLink; its own buffer too), then its last CTA raises
+// flags[rank] = e on every rank (release, system scope).  The consumer (add+RMSNorm, or a
+// reduce kernel) waits for all flags >= e, sums the slots in rank order -- the same sum on every
+// rank -- and bumps its local epoch.  Two parities: a rank writes round e + 1 only after its own
+// consumer of round e, which waited for everyone's round e, so no slot is overwritten while read.
+using rtnq_b200::kPeerHeader;
+using rtnq_b200::kPeerMax;
+using rtnq_b200::PeerOut;
+__device__ __forceinline__ int* peer_epoch(char* b) { return reinterpret_cast<int*>(b); }
+__device__ __forceinline__ int* peer_flags(char* b) { return reinterpret_cast<int*>(b) + 1; }
+__device__ __forceinline__ int* peer_done(char* b) { return reinterpret_cast<int*>(b) + 1 + kPeerMax; }
+__device__ __forceinline__ int* peer_consumed(char* b) { return reinterpret_cast<int*>(b) + 2 + kPeerMax; }
+__device__ __forceinline__ __nv_bfloat16* peer_slot(char* b, int64_t cap, int parity, int q) {
+    return reinterpret_cast<__nv_bfloat16*>(b + kPeerHeader) + (int64_t(parity) * kPeerMax + q) * cap;
+}
+// the round a producer writes: the local epoch + 1 (its consumer of the previous round bumped it;
+// under programmatic dependent launch that grid may still run, so wait for it first)
+__device__ __forceinline__ int peer_round(const PeerOut& po) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return *reinterpret_cast<volatile int*>(peer_epoch(po.bufs[po.rank])) + 1;
+}
+// element i of this rank's partial -> every rank's slot [e & 1][rank]
+__device__ __forceinline__ void peer_store(const PeerOut& po, int e, int64_t i, float v) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    for (int q = 0; q < po.world; ++q) peer_slot(po.bufs[q], po.cap, e & 1, po.rank)[i] = h;
+}
+// kernel end, thread 0 of each CTA after a CTA-wide barrier: the last of G CTAs flags round e
+// on every rank (the CTA's stores were ordered before the barrier; the fence makes them visible
+// system-wide before the counter, the flags after it)
+__device__ __forceinline__ void peer_complete(const PeerOut& po, int e, int G) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (atomicAdd(peer_done(po.bufs[po.rank]), 1) == G - 1) {
+        *peer_done(po.bufs[po.rank]) = 0;
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int q = 0; q < po.world; ++q)
+            asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(peer_flags(po.bufs[q]) + po.rank), "r"(e)
+                         : "memory");
+    }
+}
+// 16 bytes of a slot (L2, not L1: the same slot address was read two rounds ago)
+__device__ __forceinline__ uint4 peer_ld16(const __nv_bfloat16* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+// consumer: wait until every rank delivered round e into this rank's buffer `b`
+__device__ __forceinline__ void peer_wait(char* b, int world, int e) {
+    for (int q = 0; q < world; ++q) {
+        int got;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(got) : "l"(peer_flags(b) + q) : "memory");
+            if (got >= e) break;
+            __nanosleep(64);
+        }
+    }
+}
+// consumer CTA done reading round e: the last of G bumps the local epoch (the next producer of
+// this rank runs after this grid, stream-ordered)
+__device__ __forceinline__ void peer_consumed_by(char* b, int G) {
+    if (atomicAdd(peer_consumed(b), 1) == G - 1) {
+        *peer_consumed(b) = 0;
+        atomicAdd(peer_epoch(b), 1);
     }
 }
 

@@ -53,6 +53,26 @@ void launch_gemm_oracle(const float* a, int64_t m, int64_t k, const uint8_t* cod
                         float* out, cudaStream_t st);
 
 // wgemm_sm100.cu: tensor-core W4A16 / W8A16 over the native layout.
+// A row-split linear's output pushed into every tensor-parallel rank's symmetric buffer
+// (int8_mma.cuh, "partial sums over peer memory"); world 0: plain local output.
+constexpr int kPeerMax = 8;
+constexpr int kPeerHeader = 256;
+struct PeerOut {
+    int world = 0, rank = 0;
+    char* bufs[kPeerMax] = {};  // every rank's symmetric buffer, mapped into this process
+    int64_t cap = 0;            // elements per slot
+};
+// the consumer side: this rank's own buffer (the slots every rank's partial landed in)
+struct PeerIn {
+    char* buf = nullptr;
+    int world = 0;
+    int64_t cap = 0;
+};
+size_t peer_buffer_bytes(int64_t cap);
+// out[i] (+)= sum over ranks of slot[i], i < n (rank order, f32, one bf16 rounding); then the
+// round is consumed (peer.cu)
+cudaError_t launch_peer_reduce(const PeerIn& pin, void* out, int64_t n, bool accumulate, cudaStream_t st);
+
 struct WgemmArgs {
     const void* a;         // m x k, bf16 or f16, row-major
     int a_dtype;           // RTNQ_BF16 | RTNQ_F16
@@ -73,6 +93,8 @@ struct WgemmArgs {
     // int8 kernels computing their own planes: |= 1 on a non-finite activation (the planes
     // kernel's max pass checks it; InvalidInputError in the reference, gemm.cpp:13-19)
     int32_t* err = nullptr;
+    // tensor parallel: push the output into every rank's slot instead of `out` (world > 0)
+    PeerOut peer{};
 };
 // Validates the shape for the tensor-core path; returns a message or nullptr.
 const char* wgemm_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);
@@ -98,9 +120,10 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& args, cudaStream_t st);
 
 // decode.cu: the non-GEMM kernels of a decode layer (bf16 activations)
 // planes/texp (optional, bf16 rows): also write the int8 GEMMs' activation planes of the output
+// pin.buf: the delta is the sum of the ranks' partials of the current round (peer memory)
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const void* w, void* out, int64_t m,
                                int64_t h, float eps, cudaStream_t st, int8_t* planes = nullptr,
-                               int32_t* texp = nullptr);
+                               int32_t* texp = nullptr, PeerIn pin = PeerIn{});
 cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cudaStream_t st,
                             int8_t* planes = nullptr, int32_t* texp = nullptr);
 // the activation planes alone ([3][m][k] int8, [m] exponents) of a bf16/f16 activation

@@ -59,6 +59,7 @@ struct Params {
     int debug;
     imma::OwnPlanes own;  // own.a != nullptr: this launch computes its tokens' planes itself
     int8_t* planes_w;     // ... into this [3][Mtot][K] buffer (the TMA source), exponents into texp
+    PeerOut peer;         // tensor parallel: output pushed into every rank's slot (world > 0)
 };
 
 template <int PT, int BITS = 4>
@@ -497,6 +498,12 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         // through shared memory at each segment end.
         const int eg = warp >= kEpiB0 ? 1 : 0;
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
+        // the output: local, or (tensor parallel) this rank's slot of every rank's buffer
+        const int pe = p.peer.world ? peer_round(p.peer) : 0;
+        auto emit_out = [&](int m, int64_t col, float v) {
+            if (p.peer.world) peer_store(p.peer, pe, int64_t(p.m0 + m) * p.N + col, v);
+            else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
+        };
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         float* scr = reinterpret_cast<float*>(smem + GG::SCR_OFF);
         __shared__ float pow_s[NT];  // 2^s per token, 0 for padding tokens
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                     if (row < rows)
 #pragma unroll
                         for (int m = 0; m < NT; ++m)
-                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                            if (m < p.M) emit_out(m, n0 + row, acc[m]);
                 } else {
                     mbar_wait(go, 0);
                     uint32_t dst, rb;
@@ -690,7 +697,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                 if (row < rows)
 #pragma unroll
                     for (int m = 0; m < NT; ++m)
-                        if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                        if (m < p.M) emit_out(m, n0 + row, acc[m]);
             } else {
                 // stream-K: the owner holds the row-block's first k-block (its last segment);
                 // the others hand over partials from their first segment (slot = CTA)
@@ -717,7 +724,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                     if (row < rows)
 #pragma unroll
                         for (int m = 0; m < NT; ++m)
-                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                            if (m < p.M) emit_out(m, n0 + row, acc[m]);
                 } else {
                     // contributor (its first segment): store the partial; warp 3 publishes it
                     // (gpu-scope fence + counter), off this pipeline's critical path
@@ -753,6 +760,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
     fence_before();
     __syncthreads();
     if ((dbg_ & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 7] = gtime();
+    if (p.peer.world && threadIdx.x == 0) peer_complete(p.peer, peer_round(p.peer), int(gridDim.x));
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -928,6 +936,7 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     p.codes = A.codes;
     p.scales = A.scales;
     p.texp = texp;
+    p.peer = A.peer;
     p.N = A.n;
     p.K = A.k;
     p.Mtot = int(A.m);
@@ -939,6 +948,10 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
     // tokens per chunk: the smallest PT >= M (B operand N = 3 * PT rounded up to 16)
     const int pt = A.m <= 5 ? 5 : A.m <= 10 ? 10 : A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
+    // peer output: one launch = one allreduce round, so the tokens must fit one chunk and the
+    // slot (int8_mma.cuh peer_*)
+    if (A.peer.world && (A.m > pt || A.m * A.n > A.peer.cap || A.out_dtype != RTNQ_BF16))
+        return cudaErrorInvalidValue;
     for (int64_t m0 = 0; m0 < A.m; m0 += pt) {
         p.M = int(A.m - m0 < pt ? A.m - m0 : pt);
         p.m0 = int(m0);

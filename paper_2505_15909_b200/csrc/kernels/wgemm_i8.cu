@@ -56,6 +56,7 @@ struct Params {
     int debug;  // profiling: 4 = no MMA issued, 2 = no loads (arrive only)
     imma::OwnPlanes own;  // own.a != nullptr: this launch computes its tokens' planes itself
     int8_t* planes_w;     // ... into this [3][Mtot][K] buffer (the TMA source), exponents into texp
+    PeerOut peer;         // tensor parallel: output pushed into every rank's slot (world > 0)
 };
 
 template <int NT>
@@ -282,6 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
+        // the output: local, or (tensor parallel) this rank's slot of every rank's buffer
+        const int pe = p.peer.world ? peer_round(p.peer) : 0;
+        auto emit_out = [&](int m, int64_t col, float v) {
+            if (p.peer.world) peer_store(p.peer, pe, int64_t(p.m0 + m) * p.N + col, v);
+            else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
+        };
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         int db = 0, seg = 0, u = u0;
         __shared__ float pow_s[NT];  // 2^s per token (s >= -126: a normal float)
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                     if (row < rows)
 #pragma unroll
                         for (int m = 0; m < NT; ++m)
-                            if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m]);
+                            if (m < p.M) emit_out(m, n0 + row, acc[m]);
                 } else {
                     // direct: a region nobody else uses, so push at once (a complete_tx that lands
                     // before the leader's expect_tx only drives the tx-count negative meanwhile)
@@ -427,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
                 if (row < rows)
 #pragma unroll
                     for (int m = 0; m < NT; ++m)
-                        if (m < p.M) store_out(p.out, p.out_dtype, int64_t(m) * p.N + n0 + row, acc[m] + psum[m]);
+                        if (m < p.M) emit_out(m, n0 + row, acc[m] + psum[m]);
             } else {  // contributor: this is the CTA's first segment, partial slot c
                 float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
 #pragma unroll
@@ -446,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     fence_before();
     __syncthreads();
     if ((dbg_ & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 7] = gtime();
+    if (p.peer.world && threadIdx.x == 0) peer_complete(p.peer, peer_round(p.peer), int(gridDim.x));
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -634,6 +642,7 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     p.codes = A.codes;
     p.scales = A.scales;
     p.texp = texp;
+    p.peer = A.peer;
     p.N = A.n;
     p.K = A.k;
     p.Mtot = int(A.m);
@@ -651,6 +660,10 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
     p.pf = pf_env;
     const int esz = A.out_dtype == RTNQ_F32 ? 4 : 2;
     const int nt_max = A.m <= 16 ? 16 : A.m <= 32 ? 32 : 64;
+    // peer output: one launch = one allreduce round, so the tokens must fit one chunk and the
+    // slot (int8_mma.cuh peer_*)
+    if (A.peer.world && (A.m > nt_max || A.m * A.n > A.peer.cap || A.out_dtype != RTNQ_BF16))
+        return cudaErrorInvalidValue;
     for (int64_t m0 = 0; m0 < A.m; m0 += nt_max) {
         p.M = int(A.m - m0 < nt_max ? A.m - m0 : nt_max);
         p.m0 = int(m0);

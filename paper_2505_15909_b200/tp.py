@@ -265,26 +265,51 @@ class TPDecodeLayer:
         return rq.linear(a, q, out=out, workspace=ws, stream=stream, pdl=pdl, err=self.err,
                          check=False)
 
-    def attn_half(self, x, delta, ws, stream=None, pdl=False):
-        """x += delta; y = rmsnorm(x); qkv; attention; o = partial attn_out_proj."""
+    def _norm(self, x, weight, delta, peer, stream):
+        import paper_2505_15909_b200 as rq
+        if peer is not None:  # delta = sum of the ranks' partials of the current peer round
+            peer.add_rmsnorm(x, weight, self.y, eps=self.shape.eps, stream=stream, planes=self.py)
+        else:
+            rq.add_rmsnorm(x, weight, self.y, delta=delta, eps=self.shape.eps, stream=stream,
+                           planes=self.py)
+
+    def _row_split(self, module, a, planes, out, ws, stream, pdl, peer):
+        import paper_2505_15909_b200 as rq
+        if peer is None:
+            return self._linear(module, a, planes, out, ws, stream, pdl)
+        q = self.q[module]
+        if planes is not None and q.layout in (rq.NATIVE_I4, rq.NATIVE_I8):
+            peer.linear(q, planes=planes, workspace=ws, stream=stream, pdl=pdl, err=self.err)
+        else:
+            peer.linear(q, a=a, workspace=ws, stream=stream, pdl=pdl, err=self.err)
+        return None
+
+    def attn_half(self, x, delta, ws, stream=None, pdl=False, peer=None, peer_in=False):
+        """x += delta; y = rmsnorm(x); qkv; attention; o = partial attn_out_proj.
+        ``peer`` (peer.PeerGroup): o goes to the peers' slots instead (returns None), and with
+        ``peer_in`` the delta is the previous peer round's sum."""
         import paper_2505_15909_b200 as rq
         s = self.shape
-        rq.add_rmsnorm(x, self.attn_norm, self.y, delta=delta, eps=s.eps, stream=stream, planes=self.py)
+        self._norm(x, self.attn_norm, delta, peer if peer_in else None, stream)
         self._linear("qkv_proj", self.y, self.py, self.qkv, ws, stream, pdl)
         rq.decode_attention(self.qkv, self.k_cache, self.v_cache, self.attn, self.dims.hq,
                             self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream,
                             workspace=self.attn_ws)
+        if peer is not None:
+            return self._row_split("attn_out_proj", self.attn, None, self.o, ws, stream, pdl, peer)
         rq.linear(self.attn, self.q["attn_out_proj"], out=self.o, workspace=ws, stream=stream,
                   pdl=pdl, err=self.err, check=False)
         return self.o
 
-    def mlp_half(self, x, o_sum, ws, stream=None, pdl=False):
-        """x += o_sum; y = rmsnorm(x); gate_up; silu*up; d = partial ffn_down."""
+    def mlp_half(self, x, o_sum, ws, stream=None, pdl=False, peer=None):
+        """x += o_sum; y = rmsnorm(x); gate_up; silu*up; d = partial ffn_down.
+        ``peer``: o_sum is the current peer round's sum and d goes to the peers (returns None)."""
         import paper_2505_15909_b200 as rq
-        rq.add_rmsnorm(x, self.ffn_norm, self.y, delta=o_sum, eps=self.shape.eps, stream=stream,
-                       planes=self.py)
+        self._norm(x, self.ffn_norm, o_sum, peer, stream)
         self._linear("ffn_up", self.y, self.py, self.gu, ws, stream, pdl)
         rq.silu_mul(self.gu, self.act, stream=stream, planes=self.pa)
+        if peer is not None:
+            return self._row_split("ffn_down", self.act, self.pa, self.d, ws, stream, pdl, peer)
         self._linear("ffn_down", self.act, self.pa, self.d, ws, stream, pdl)
         return self.d
 
@@ -294,10 +319,13 @@ class TPDecodeStack:
 
     def __init__(self, shape: LlamaShape, table, world: int, rank: int, batch: int,
                  max_len: int = 257, pos: int = 256, group: int = 128, layers=None, seed=0,
-                 device="cuda", w8_per_channel=False, fuse_planes=True, collectives=True):
+                 device="cuda", w8_per_channel=False, fuse_planes=True, collectives=True,
+                 peer=None):
         """collectives=False builds ONE rank's shard stack of a TP=world model without a
         process group (the per-GPU work of that configuration on a single GPU; the allreduces
-        are skipped)."""
+        are skipped).  collectives="peer": the allreduces run over peer memory, fused into
+        the row-split linears and the following add+RMSNorm (peer.py); ``peer`` is this
+        rank's PeerGroup (default: built over the default process group)."""
         import torch
 
         import paper_2505_15909_b200 as rq
@@ -315,6 +343,10 @@ class TPDecodeStack:
         for layer in self.layers:
             layer.err = self.err
             layer.attn_ws = self.attn_ws
+        self.peer = peer
+        if collectives == "peer" and peer is None and world > 1:
+            from paper_2505_15909_b200.peer import PeerGroup, slot_cap
+            self.peer = PeerGroup.from_process_group(slot_cap(batch * shape.hidden), device=self.x.device)
 
     @property
     def weight_bytes(self):
@@ -335,6 +367,8 @@ class TPDecodeStack:
     def step(self, x0, stream=None, pdl=True):
         """One decode step for the batch; returns the residual stream after all layers.
         Asynchronous (capturable in a CUDA graph); :meth:`check` reports non-finite inputs."""
+        if self.peer is not None:
+            return step_peer([self], [x0], [stream], pdl)[0]
         self.x.copy_(x0)
         delta = None
         for layer in self.layers:
@@ -343,3 +377,26 @@ class TPDecodeStack:
         # fold the last layer's down-projection into the residual stream
         self.x.add_(delta)
         return self.x
+
+
+def step_peer(stacks, x0s, streams=None, pdl=True):
+    """One decode step of the ranks in ``stacks`` whose allreduces run over peer memory
+    (each stack's ``peer``).  One stack per process (torchrun), or all ranks of a group driven
+    by this process (PeerGroup.single_process): the ranks are issued half-layer by half-layer,
+    so every consumer follows, in issue order, the producers it waits for."""
+    streams = streams or [None] * len(stacks)
+    for st, x0, stream in zip(stacks, x0s, streams):
+        if stream is None:
+            st.x.copy_(x0)
+        else:
+            import torch
+            with torch.cuda.stream(stream):
+                st.x.copy_(x0)
+    for li in range(len(stacks[0].layers)):
+        for st, stream in zip(stacks, streams):
+            st.layers[li].attn_half(st.x, None, st.ws, stream, pdl, peer=st.peer, peer_in=li > 0)
+        for st, stream in zip(stacks, streams):
+            st.layers[li].mlp_half(st.x, None, st.ws, stream, pdl, peer=st.peer)
+    for st, stream in zip(stacks, streams):  # fold the last down-projection into the residual
+        st.peer.reduce(st.x, accumulate=True, stream=stream)
+    return [st.x for st in stacks]
