@@ -70,6 +70,12 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t ad, uint64_t bd, uin
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ void ld8(uint32_t taddr, uint32_t* d) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+                 : "r"(taddr)
+                 : "memory");
+}
 __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t* d) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -509,17 +515,27 @@ struct OwnPlanes {
 template <int AT>
 __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, int K, int t, int M,
                                              int8_t* __restrict__ planes, int32_t* __restrict__ texp,
-                                             int32_t* err, int tid, int nthr, int bar, float* red) {
+                                             int32_t* err, int tid, int nthr, int bar, float* red,
+                                             long long* dtl = nullptr, long long dt0 = 0) {
+    if (dtl && tid == 0) dtl[0] = clock64() - dt0;
     auto cvt = [](uint32_t h) -> float {
         if constexpr (AT == RTNQ_BF16) return __uint_as_float(h << 16);
         else return __half2float(__ushort_as_half(static_cast<unsigned short>(h)));
     };
     constexpr uint32_t kExpMask = AT == RTNQ_BF16 ? 0x7F807F80u : 0x7C007C00u;
     const int nv = K / 8;
+    // the first kHold vectors of this thread stay in registers between the two passes (K <= 8 *
+    // kHold * nthr: one load of the row, all in flight at once); longer rows reload the rest
+    constexpr int kHold = 8;
+    uint4 held[kHold];
+#pragma unroll
+    for (int h = 0; h < kHold; ++h) {
+        const int v = tid + h * nthr;
+        if (v < nv) held[h] = __ldcg(reinterpret_cast<const uint4*>(rowp) + v);
+    }
     float mx = 0.0f;
     uint32_t nonfinite = 0;
-    for (int v = tid; v < nv; v += nthr) {
-        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(rowp) + v);
+    auto scan = [&](const uint4& q) {
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -527,7 +543,12 @@ __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, 
             const uint32_t e = w[i] & kExpMask;
             nonfinite |= ((e & 0xffffu) == (kExpMask & 0xffffu)) | ((e >> 16) == (kExpMask >> 16));
         }
-    }
+    };
+#pragma unroll
+    for (int h = 0; h < kHold; ++h)
+        if (tid + h * nthr < nv) scan(held[h]);
+    if (dtl && tid == 0) dtl[1] = clock64() - dt0;
+    for (int v = tid + kHold * nthr; v < nv; v += nthr) scan(__ldcg(reinterpret_cast<const uint4*>(rowp) + v));
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (err && __any_sync(0xffffffffu, nonfinite) && (tid & 31) == 0) atomicOr(err, 1);
     if ((tid & 31) == 0) red[tid >> 5] = mx;
@@ -539,8 +560,8 @@ __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, 
     const int s = max(e - 6, -126);
     if (tid == 0) texp[t] = s;
     const float inv = __int_as_float((127 - s) << 23);
-    for (int v = tid; v < nv; v += nthr) {
-        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(rowp) + v);
+    if (dtl && tid == 0) dtl[2] = clock64() - dt0;
+    auto split = [&](const uint4& q, int v) {
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
         uint32_t pk[3][2] = {{0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
@@ -558,26 +579,34 @@ __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, 
         for (int pl = 0; pl < 3; ++pl)
             *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
                 make_uint2(pk[pl][0], pk[pl][1]);
-    }
+    };
+#pragma unroll
+    for (int h = 0; h < kHold; ++h)
+        if (tid + h * nthr < nv) split(held[h], tid + h * nthr);
+    for (int v = tid + kHold * nthr; v < nv; v += nthr) split(__ldcg(reinterpret_cast<const uint4*>(rowp) + v), v);
+    if (dtl && tid == 0) dtl[3] = clock64() - dt0;
     // every thread's planes stores are done before the caller publishes the token
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
+    if (dtl && tid == 0) dtl[4] = clock64() - dt0;
 }
 
 // Producers: CTA c of G computes tokens m0 + t, t = c, c + G, ... < M, after the activations'
 // producer grid has completed (griddepcontrol.wait), and publishes each one.
 __device__ __forceinline__ void own_planes_produce(const OwnPlanes& op, int K, int m0, int M, int Mtot, int c,
                                                    int G, int8_t* planes, int32_t* texp, int tid, int nthr,
-                                                   int bar, float* red) {
+                                                   int bar, float* red, long long* dtl = nullptr,
+                                                   long long dt0 = 0) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int t = c; t < M; t += G) {
         const uint16_t* rowp = static_cast<const uint16_t*>(op.a) + int64_t(m0 + t) * K;
         if (op.a_dtype == RTNQ_BF16)
-            token_planes<RTNQ_BF16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red);
+            token_planes<RTNQ_BF16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red, dtl, dt0);
         else
             token_planes<RTNQ_F16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red);
         if (tid == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");  // the consumers read them by TMA
             asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(op.done) : "memory");
+            if (dtl) dtl[5] = clock64() - dt0;
         }
     }
 }

@@ -30,6 +30,7 @@
 // planes by the MMA).  An expanded A tile staged in smem would add 32 KiB more per group;
 // in TMEM it costs no smem bandwidth at all.
 //   warps 4-7   epilogue: per-group TMEM reads, scaling, stream-K / cluster output
+//   warps 12-15 (batch >= 16) a second epilogue warpgroup: the other half of the tokens
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -44,7 +45,7 @@ using namespace imma;
 
 constexpr int kKB = 128;              // k-block = one quantization group = one tile
 constexpr int kTile = kRows * 64;     // 8 KiB of nibbles
-constexpr int kEpi0 = 4, kExp0 = 8, kEpiB0 = 8;  // epilogue warpgroup B (EW = 2): the expansion warps
+constexpr int kEpi0 = 4, kExp0 = 8, kEpiB0 = 12;  // epilogue warpgroup B (EH = 2): warps 12-15
 
 struct Params {
     CUtensorMap tmap_p;      // planes [3][M][K] s8, box {128, PT, 3}, SWIZZLE_128B
@@ -81,17 +82,12 @@ struct Geo {
     static constexpr int CODE_OFF = TPS * PLANE_BYTES;      // planes first: 1024-aligned
     static constexpr int SC_OFF = CODE_OFF + TPS * TILE;
     static constexpr int STAGE_BYTES = (SC_OFF + TPS * 256 + 1023) / 1024 * 1024;
-    // two epilogue warpgroups (one per group of a stage) when a stage holds two groups
-#ifndef RTNQ_I4_EW
-#define RTNQ_I4_EW 1
+    // epilogue warpgroups: two (each with half of the tokens) from 16 tokens up
+#ifndef RTNQ_I4_EH
+#define RTNQ_I4_EH 2
 #endif
-    // EW = 2: the expansion warps (8-11) are a second epilogue warpgroup as well: they take the odd
-    // groups of every stage's epilogue, interleaved with their expansion work (one stage of
-    // epilogue per stage of expansion, NP stages behind).  Correct (tests pass with it) but
-    // measured slower (gate_up 22.3 vs 21.8 us at batch 16, 17.8 vs 15.5 at batch 1), so off.
-    static constexpr int EW = RTNQ_I4_EW;
-    static constexpr int THREADS = 384;
-    static constexpr int SCR_BYTES = EW == 2 ? ACC * kRows * 4 : 0;  // warpgroup B's partial sums
+    static constexpr int EH = PT >= 16 ? RTNQ_I4_EH : 1;
+    static constexpr int THREADS = EH == 2 ? 512 : 384;
     // The A operand of a group is 4 k-steps of 32 codes.  The first KT come from TMEM (tcgen05.st
     // by the expansion; the MMA's A reads share the 64 B/clk TMEM read port with the epilogue's
     // accumulator readback), the rest from a 128B-swizzled smem tile (128 B/clk smem port,
@@ -104,7 +100,7 @@ struct Geo {
 #ifndef RTNQ_I4_SMEM_KB
 #define RTNQ_I4_SMEM_KB 212
 #endif
-    static constexpr int STAGES_FIT = ((PT <= 16 ? RTNQ_I4_SMEM_KB : 212) * 1024 - SCR_BYTES - AS * A_SMEM) / STAGE_BYTES;
+    static constexpr int STAGES_FIT = ((PT <= 16 ? RTNQ_I4_SMEM_KB : 212) * 1024 - AS * A_SMEM) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int A_OFF = STAGES * STAGE_BYTES;      // smem A slots (1024-aligned)
     static constexpr int A_COL = 512 - AS * KT * 8;         // TMEM A slots: 8 columns per k-step
@@ -113,8 +109,7 @@ struct Geo {
     static constexpr int NP = NS / TPS;                     // ... in stage-sized slots
     static constexpr int BAR_OFF = A_OFF + AS * A_SMEM;
     static constexpr int SR_OFF = BAR_OFF + 1024;           // [NS][128] f32 group scale / 16
-    static constexpr int SCR_OFF = SR_OFF + NS * kRows * 4;
-    static constexpr int SMEM = SCR_OFF + SCR_BYTES + 1024;
+    static constexpr int SMEM = SR_OFF + NS * kRows * 4 + 1024;
     static constexpr int MAXC_FIT = 1 + STAGES * STAGE_BYTES / (ACC * kRows * 4);
     static constexpr int MAXC = MAXC_FIT > 8 ? 8 : MAXC_FIT;
     static_assert(STAGES >= 3, "");
@@ -192,7 +187,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
 #endif
     using GG = Geo<PT, BITS>;
     constexpr int NT = GG::ACC;
-    constexpr int STAGES = GG::STAGES, DN = GG::DN, AP = GG::AP, NP = GG::NP, TPS = GG::TPS, EW = GG::EW;
+    constexpr int STAGES = GG::STAGES, DN = GG::DN, AP = GG::AP, NP = GG::NP, TPS = GG::TPS, EH = GG::EH;
     extern __shared__ uint8_t smem_raw[];
     // align by indexing the __shared__ array (keeps the shared address space: LDS/STS, not
     // generic loads)
@@ -226,9 +221,10 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 5);
         for (int i = 0; i < AP; ++i) mbar_init(&afull[i], 4), mbar_init(&aempty[i], 1);
-        for (int i = 0; i < NP; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4 * EW), mbar_init(&sfull[i], 4);
-        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4), mbar_init(pready, 1);
+        for (int i = 0; i < NP; ++i) mbar_init(&tfull[i], 1), mbar_init(&tfree[i], 4 * EH), mbar_init(&sfull[i], 4);
+        mbar_init(go, 1), mbar_init(rfull, 1), mbar_init(pub, 4 * EH), mbar_init(pready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if ((dbg_ & 512) && c == (dbg_ >> 16)) g_i4_tl[63 * 16 + 13] = clock64() - tl0;
     }
     if constexpr (GG::DN > 3 * PT) {  // B rows past 3 * PT: zero once, never written by TMA
         constexpr int PAD = (GG::DN - 3 * PT) * 128 / 16;  // uint4 per slot
@@ -243,10 +239,12 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             su32(tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if ((dbg_ & 512) && c == (dbg_ >> 16) && lane == 0) g_i4_tl[63 * 16 + 14] = clock64() - tl0;
     }
     fence_before();
     __syncthreads();
     fence_after();
+    if ((dbg_ & 512) && c == (dbg_ >> 16) && threadIdx.x == 0) g_i4_tl[63 * 16 + 15] = clock64() - tl0;
     if (p.csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const uint32_t tmem = *tslot;
     asm volatile("griddepcontrol.launch_dependents;");
@@ -254,14 +252,16 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         // the epilogue + expansion warps (idle until the first weights land) compute this CTA's
         // share of the launch's activation planes (int8_mma.cuh, own_planes_produce)
         __shared__ float pred[8];
+        if ((dbg_ & 512) && c == (dbg_ >> 16) && threadIdx.x == kEpi0 * 32) g_i4_tl[62 * 16 + 5] = clock64() - tl0;
         own_planes_produce(p.own, int(p.K), p.m0, p.M, p.Mtot, c, int(gridDim.x), p.planes_w,
-                           const_cast<int32_t*>(p.texp), threadIdx.x - kEpi0 * 32, 256, 3, pred);
+                           const_cast<int32_t*>(p.texp), threadIdx.x - kEpi0 * 32, 256, 3, pred,
+                           (dbg_ & 512) && c == (dbg_ >> 16) ? &g_i4_tl[61 * 16] : nullptr, tl0);
+        if ((dbg_ & 512) && c == (dbg_ >> 16) && threadIdx.x == kEpi0 * 32) g_i4_tl[62 * 16 + 6] = clock64() - tl0;
     }
 
     // ===================== expansion: nibbles -> s8 (16 x code) in TMEM ===============
     // One handshake per stage (TPS groups): A pair slot xsi % AP, accumulator slot xsi % NP.
-    // exp_step() expands one stage; run by warps 8-11 (alone, or interleaved with their share of
-    // the epilogue when EW == 2).
+    // exp_step() expands one stage; run by warps 8-11.
     const int xrow = threadIdx.x - kExp0 * 32;  // one xrow of the tile per thread = TMEM lane
     const uint32_t sw_in = uint32_t((xrow >> 1) & 3);
     const uint32_t xlane_base = uint32_t((warp & 3) * 32) << 16;
@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
             }
         }
         long long w_empty = 0;
+        if ((dbg_ & 512) && c == (dbg_ >> 16) && lane == 0) g_i4_tl[62 * 16 + 13 + codes] = clock64() - tl0;
         for (int i = 0; cu.more(); ++i) {
             const int n = cu.chunk();
             if (i >= STAGES) {
@@ -390,9 +391,12 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                 // the row-block's rows padded to 8: the stride of its native scale groups
                 const int64_t left = p.N - int64_t(cu.b) * kRows;
                 const int r8 = left >= kRows ? kRows : int((left + 7) / 8 * 8);
+                if (i == 0 && (dbg_ & 512) && c == (dbg_ >> 16) && lane == 0) g_i4_tl[62 * 16 + 10] = clock64() - tl0;
                 elect_expect(&full[s], uint32_t(n) * (GG::TILE + uint32_t(r8) * 2));
+                if (i == 0 && (dbg_ & 512) && c == (dbg_ >> 16) && lane == 0) g_i4_tl[62 * 16 + 11] = clock64() - tl0;
                 elect_bulk_tx(st + GG::CODE_OFF + slot0 * GG::TILE,
                               p.codes + (int64_t(cu.b) * p.KBLK + cu.kb) * GG::TILE, &full[s], uint32_t(n) * GG::TILE);
+                if (i == 0 && (dbg_ & 512) && c == (dbg_ >> 16) && lane == 0) g_i4_tl[62 * 16 + 12] = clock64() - tl0;
                 elect_bulk_tx(st + GG::SC_OFF + slot0 * 256,
                               p.scales + int64_t(cu.b) * kRows * p.KBLK + int64_t(cu.kb) * r8, &full[s],
                               uint32_t(n * r8 * 2));
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                 asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + u0 / p.KBLK) : "memory");
             }
         }
-    } else if (warp >= kExp0 && warp < kExp0 + 4 && EW == 1) {
+    } else if (warp >= kExp0 && warp < kExp0 + 4) {
         while (xcu.more()) exp_step();
         if ((dbg_ & 32) && threadIdx.x == kExp0 * 32) {
             g_i4_dbg[c * 16 + 2] = x_full, g_i4_dbg[c * 16 + 3] = x_aempty;
@@ -493,11 +497,13 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
             g_i4_dbg[c * 16 + 1] = m_issue;
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
-        // warpgroup A (warps 4-7) takes group 0 of every stage and does all output; with two
-        // groups per stage, warpgroup B (warps 12-15) takes group 1 and hands its sums over
-        // through shared memory at each segment end.
-        const int eg = warp >= kEpiB0 ? 1 : 0;
-        const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
+        // EH warpgroups (warps 4-7; and 12-15 when EH = 2), each owning NH of the tokens: a
+        // warpgroup's TMEM loads of a group are 3 planes x NH columns, so the two warpgroups'
+        // load latencies overlap (measured: the epilogue's ~200-cycle tcgen05.ld round trips bound
+        // the batch-16 stage period with one warpgroup, profiles/r2_w4_limiter.md)
+        constexpr int EH = GG::EH, NH = NT / EH;
+        const int eh = warp >= kEpiB0 ? 1 : 0, t0 = eh * NH;
+        const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - (eh ? kEpiB0 : kEpi0) * 32;
         // the output: local, or (tensor parallel) this rank's slot of every rank's buffer
         const int pe = p.peer.world ? peer_round(p.peer) : 0;
         auto emit_out = [&](int m, int64_t col, float v) {
@@ -505,17 +511,16 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
             else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
         };
         const uint32_t lane_base = uint32_t(q * 32) << 16;
-        float* scr = reinterpret_cast<float*>(smem + GG::SCR_OFF);
         __shared__ float pow_s[NT];  // 2^s per token, 0 for padding tokens
-        if (eg == 0) {
+        if (eh == 0) {
             if (p.own.a) mbar_wait(pready, 0);  // texp published by this launch
             else asm volatile("griddepcontrol.wait;" ::: "memory");  // texp from the planes producer
             for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
-            asm volatile("bar.sync 1, 128;" ::: "memory");
         }
-        float acc[NT];
+        asm volatile("bar.sync 1, %0;" ::"r"(128 * EH) : "memory");
+        float acc[NH];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+        for (int t = 0; t < NH; ++t) acc[t] = 0.0f;
         Cursor<TPS> cu(u0, u1, p.KBLK);
         int si = 0, seg_kb0 = cu.kb;
         long long e_wait = 0, e_work = 0, e_ld = 0;
@@ -535,84 +540,88 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         const long long _tw = (dbg_ & 32) ? clock64() : 0;
         if (warp == kEpi0) I4_TL(si, 6);
         fence_after();
-        float scg[TPS], sg2 = 0.0f;
+        float scg[TPS];
 #pragma unroll
         for (int j = 0; j < TPS; ++j) scg[j] = j < n ? sring[(np * TPS + j) * kRows + row] : 0.0f;
-        // this warpgroup's groups of the stage: [j0, j1)
-        const int j0 = EW == 2 ? eg : 0, j1 = EW == 2 ? (eg < n ? eg + 1 : eg) : n;
+        // token chunks of CH: plane p3 of token t is accumulator column p3 * PT + t
+        constexpr int CH = NH >= 16 ? 16 : NH;
+        constexpr bool SPLIT = PT >= 16;           // planes loaded separately (CH columns each)
+        constexpr int LDC = SPLIT ? CH : GG::DN;   // columns per load buffer
+        // TMEM loads in batches of GL groups per round trip (one tcgen05.wait::ld per batch: the
+        // ~250-cycle round trip, not the bytes, bounds this loop), double-buffered when the
+        // registers allow
+        constexpr int PGR = SPLIT ? 3 * CH : LDC;  // registers per group of a chunk
+        constexpr int GL = TPS >= 4 && 4 * PGR <= 96 ? 4 : TPS >= 2 && 2 * PGR <= 96 ? 2 : 1;
+        constexpr int NBT = (TPS + GL - 1) / GL;
+        constexpr int NB = NBT > 1 && 2 * GL * PGR <= 96 ? 2 : 1;
 #pragma unroll
-        // token chunks of CH: plane q of token t is accumulator column q * PT + t
-        constexpr int CH = PT >= 16 ? 16 : PT;
-        constexpr int LDC = PT >= 16 ? 16 : GG::DN;  // columns loaded per plane/chunk
+        for (int jj = 0; jj < NH; jj += CH) {
+            if (dbg_ & 131072) break;
+            uint32_t d[NB][GL][SPLIT ? 3 : 1][LDC];
+            auto load = [&](int bi) {
 #pragma unroll
-        for (int jj = 0; jj < ((dbg_ & 131072) ? 0 : PT); jj += CH) {
-            // chunk jj of every group of the stage; group j + 1's TMEM loads are in flight
-            // while group j's accumulators are combined
-            // one warpgroup per group (EW == 2) keeps one group's registers only
-            // double-buffered: group j + 1's TMEM loads are in flight while group j is combined
-            constexpr int NB = EW == 2 ? 1 : (TPS < 2 ? 1 : 2);
-            uint32_t d[NB][PT >= 16 ? 3 : 1][LDC];
-            auto load = [&](int j) {
-                const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + jj);
-                const int bj = j % NB;
-                if (!(dbg_ & 16)) {
-                    if constexpr (PT >= 16) {
-                        ld16(ta, d[bj][0]);
-                        ld16(ta + PT, d[bj][1]);
-                        ld16(ta + 2 * PT, d[bj][2]);
-                    } else {
-#pragma unroll
-                        for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, d[bj][0] + 16 * h);
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < LDC; ++e)
-#pragma unroll
-                        for (int q3 = 0; q3 < (PT >= 16 ? 3 : 1); ++q3) d[bj][q3][e] = uint32_t(row + e);
-                }
-            };
-            auto combine = [&](int j) {
-#pragma unroll
-                for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
-                    uint32_t u0v, u1v, u2v;
-                    const int dj = j % NB;
-                    if constexpr (PT >= 16) {
-                        u0v = d[dj][0][e], u1v = d[dj][PT >= 16 ? 1 : 0][e], u2v = d[dj][PT >= 16 ? 2 : 0][e];
-                    } else {
-                        u0v = d[dj][0][e], u1v = d[dj][0][(PT + e) % LDC], u2v = d[dj][0][(2 * PT + e) % LDC];
-                    }
-                    // planes 1 and 2 combined exactly in int32 (|D1 * 128 + D2| < 2^28); D0
-                    // (< 2^21) converts exactly, D12's rounding (2^-24 of it) sits 2^-30 below
-                    // D0 after the 2^-14 weight
-                    const float x0 = float(int32_t(u0v));
-                    const float x12 = float(int32_t(u1v) * 128 + int32_t(u2v));
-                    acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), EW == 2 ? sg2 : scg[j], acc[jj + e]);
-                }
-            };
-            if constexpr (EW == 2) {
-                // warpgroup eg takes the stage's groups eg, eg + 2, ... (compile-time local index)
-#pragma unroll
-                for (int jl = 0; jl < (TPS + 1) / 2; ++jl) {
-                    const int j = 2 * jl + eg;
+                for (int g = 0; g < GL; ++g) {
+                    const int j = bi * GL + g;
                     if (j >= n) break;
-                    sg2 = sring[(np * TPS + j) * kRows + row];
-                    load(j);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    combine(j);
+                    const uint32_t ta = tmem + lane_base + uint32_t((np * TPS + j) * DN + t0 + jj);
+                    uint32_t(&dd)[SPLIT ? 3 : 1][LDC] = d[bi % NB][g];
+                    if (!(dbg_ & 16)) {
+                        if constexpr (SPLIT) {
+#pragma unroll
+                            for (int p3 = 0; p3 < 3; ++p3) {
+                                if constexpr (CH == 16) ld16(ta + p3 * PT, dd[p3]);
+                                else ld8(ta + p3 * PT, dd[p3]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int h = 0; h < GG::DN / 16; ++h) ld16(ta + 16 * h, dd[0] + 16 * h);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < LDC; ++e)
+#pragma unroll
+                            for (int q3 = 0; q3 < (SPLIT ? 3 : 1); ++q3) dd[q3][e] = uint32_t(row + e);
+                    }
                 }
-            } else if (j0 < j1) {
-                load(j0);
+            };
+            auto combine = [&](int bi) {
+#pragma unroll
+                for (int g = 0; g < GL; ++g) {
+                    const int j = bi * GL + g;
+                    if (j >= n) break;
+                    const uint32_t(&dd)[SPLIT ? 3 : 1][LDC] = d[bi % NB][g];
+#pragma unroll
+                    for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
+                        uint32_t u0v, u1v, u2v;
+                        if constexpr (SPLIT) {
+                            u0v = dd[0][e], u1v = dd[SPLIT ? 1 : 0][e], u2v = dd[SPLIT ? 2 : 0][e];
+                        } else {
+                            u0v = dd[0][e], u1v = dd[0][(PT + e) % LDC], u2v = dd[0][(2 * PT + e) % LDC];
+                        }
+                        // planes 1 and 2 combined exactly in int32 (|D1 * 128 + D2| < 2^28); D0
+                        // (< 2^21) converts exactly, D12's rounding (2^-24 of it) sits 2^-30 below
+                        // D0 after the 2^-14 weight
+                        const float x0 = float(int32_t(u0v));
+                        const float x12 = float(int32_t(u1v) * 128 + int32_t(u2v));
+                        acc[jj + e] = fmaf(fmaf(x12, 6.103515625e-05f, x0), scg[j], acc[jj + e]);
+                    }
+                }
+            };
+            if (n > 0) {
+                load(0);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (dbg_ & 32) {
                     const long long t = clock64();
                     e_ld += t - _tw;
                 }
 #pragma unroll
-                for (int j = 0; j < TPS; ++j) {
-                    if (j < j0 || j >= j1) continue;
-                    if (j + 1 < j1) load(j + 1);
-                    combine(j);
-                    if (j + 1 < j1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                for (int bi = 0; bi < NBT; ++bi) {
+                    if (bi * GL >= n) break;
+                    const bool next = (bi + 1) * GL < n;
+                    if (NB == 2 && next) load(bi + 1);
+                    combine(bi);
+                    if (NB == 1 && next) load(bi + 1);
+                    if (next) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 }
             }
         }
@@ -622,40 +631,26 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         if (warp == kEpi0) I4_TL(si, 7);
         if (dbg_ & 32) e_work += clock64() - _tw;
         ++si;
-        if (seg_end && EW == 2) {  // warpgroup B -> A through shared memory
-            float4* sc4 = reinterpret_cast<float4*>(scr) + row * (NT / 4);
-            if (eg == 1) {
-#pragma unroll
-                for (int j = 0; j < NT / 4; ++j)
-                    sc4[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-            }
-            asm volatile("bar.sync 2, 256;" ::: "memory");
-            if (eg == 1) {
-#pragma unroll
-                for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
-                cu.advance(n);
-                return;
-            }
-#pragma unroll
-            for (int j = 0; j < NT / 4; ++j) {
-                const float4 x = sc4[j];
-                acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
-            }
-        }
         if (seg_end) {
 #pragma unroll
-            for (int t = 0; t < NT; ++t) acc[t] *= pow_s[t];
+            for (int t = 0; t < NH; ++t) acc[t] *= pow_s[t0 + t];
             const int kbe = cu.kb + n;
             const bool sole = seg_kb0 == 0 && kbe == p.KBLK;
             const int rows = min(kRows, int(p.N - int64_t(b) * kRows));
             const int64_t n0 = int64_t(b) * kRows;
+            auto emit_all = [&]() {
+                if (row < rows)
+#pragma unroll
+                    for (int m = 0; m < NH; ++m)
+                        if (t0 + m < p.M) emit_out(t0 + m, n0 + row, acc[m]);
+            };
             if (p.csize > 1) {
                 // cluster split-K (one segment per CTA): push partials into the leader
                 const int rank = c % p.csize;
                 constexpr uint32_t kSlot = uint32_t(NT) * kRows * 4;
                 asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
                 if (rank == 0) {
-                    if (et == 0) {
+                    if (et == 0 && eh == 0) {
                         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull)),
                                      "r"(uint32_t(p.csize - 1) * kSlot)
                                      : "memory");
@@ -670,23 +665,20 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                     const float4* red = reinterpret_cast<const float4*>(smem);
                     for (int r = 1; r < p.csize; ++r) {  // rank order: deterministic
 #pragma unroll
-                        for (int j = 0; j < NT / 4; ++j) {
-                            const float4 x = red[((r - 1) * kRows + row) * (NT / 4) + j];
+                        for (int j = 0; j < NH / 4; ++j) {
+                            const float4 x = red[((r - 1) * kRows + row) * (NT / 4) + t0 / 4 + j];
                             acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
                         }
                     }
-                    if (row < rows)
-#pragma unroll
-                        for (int m = 0; m < NT; ++m)
-                            if (m < p.M) emit_out(m, n0 + row, acc[m]);
+                    emit_all();
                 } else {
                     mbar_wait(go, 0);
                     uint32_t dst, rb;
                     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst)
-                                 : "r"(su32(smem) + uint32_t(((rank - 1) * kRows + row) * NT * 4)));
+                                 : "r"(su32(smem) + uint32_t((((rank - 1) * kRows + row) * NT + t0) * 4)));
                     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(su32(rfull)));
 #pragma unroll
-                    for (int j = 0; j < NT / 4; ++j)
+                    for (int j = 0; j < NH / 4; ++j)
                         asm volatile(
                             "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
                                 dst + 16u * j),
@@ -694,17 +686,14 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                             : "memory");
                 }
             } else if (sole) {
-                if (row < rows)
-#pragma unroll
-                    for (int m = 0; m < NT; ++m)
-                        if (m < p.M) emit_out(m, n0 + row, acc[m]);
+                emit_all();
             } else {
                 // stream-K: the owner holds the row-block's first k-block (its last segment);
                 // the others hand over partials from their first segment (slot = CTA)
                 const int c_first = cta_of(int64_t(b) * p.KBLK, p.U, p.G);
                 const int c_last = cta_of(int64_t(b + 1) * p.KBLK - 1, p.U, p.G);
                 if (c == c_first) {
-                    if (et == 0) {
+                    if (et == 0 && eh == 0) {
                         const int want = c_last - c_first;
                         int got;
                         do {
@@ -712,48 +701,37 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                         } while (got < want);
                         p.counters[b] = 0;  // ready for the next launch (stream-ordered)
                     }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    asm volatile("bar.sync 3, %0;" ::"r"(128 * EH) : "memory");
                     for (int cc = c_first + 1; cc <= c_last; ++cc) {  // fixed order: deterministic
-                        const float4* src = reinterpret_cast<const float4*>(p.partials + (int64_t(cc) * kRows + row) * NT);
+                        const float4* src =
+                            reinterpret_cast<const float4*>(p.partials + (int64_t(cc) * kRows + row) * NT + t0);
 #pragma unroll
-                        for (int j = 0; j < NT / 4; ++j) {
+                        for (int j = 0; j < NH / 4; ++j) {
                             const float4 x = __ldcg(src + j);
                             acc[4 * j] += x.x, acc[4 * j + 1] += x.y, acc[4 * j + 2] += x.z, acc[4 * j + 3] += x.w;
                         }
                     }
-                    if (row < rows)
-#pragma unroll
-                        for (int m = 0; m < NT; ++m)
-                            if (m < p.M) emit_out(m, n0 + row, acc[m]);
+                    emit_all();
                 } else {
                     // contributor (its first segment): store the partial; warp 3 publishes it
                     // (gpu-scope fence + counter), off this pipeline's critical path
-                    float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT);
+                    float4* mine = reinterpret_cast<float4*>(p.partials + (int64_t(c) * kRows + row) * NT + t0);
 #pragma unroll
-                    for (int j = 0; j < NT / 4; ++j)
+                    for (int j = 0; j < NH / 4; ++j)
                         mine[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(pub);
                 }
             }
 #pragma unroll
-            for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+            for (int t = 0; t < NH; ++t) acc[t] = 0.0f;
             seg_kb0 = kbe == p.KBLK ? 0 : kbe;
         }
         cu.advance(n);
         };
-        if (EW == 2 && eg == 1) {
-            // the expansion warps: expansion of stage xsi, and the epilogue of the stage NP behind
-            // (its accumulators cannot be reused before; the expansion waits for them too)
-            while (xcu.more() || cu.more()) {
-                if (xcu.more() && (!cu.more() || xsi < si + NP)) exp_step();
-                else epi_step();
-            }
-        } else {
-            while (cu.more()) epi_step();
-        }
-        if ((dbg_ & 64) && et == 0) g_i4_dbg[c * 16 + 4] = gtime();
-        if ((dbg_ & 32) && et == 0 && eg == 0)
+        while (cu.more()) epi_step();
+        if ((dbg_ & 64) && et == 0 && eh == 0) g_i4_dbg[c * 16 + 4] = gtime();
+        if ((dbg_ & 32) && et == 0 && eh == 0)
             g_i4_dbg[c * 16 + 11] = e_wait, g_i4_dbg[c * 16 + 12] = e_work, g_i4_dbg[c * 16 + 13] = clock64() - e_t0,
             g_i4_dbg[c * 16 + 14] = si, g_i4_dbg[c * 16 + 15] = e_ld;
     }

@@ -18,6 +18,9 @@ torch.cuda.synchronize()
 buf = np.zeros(64 * 16, np.int64)
 L.rtnq_i4_timeline_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
 T = buf.reshape(64, 16)
+if os.environ.get("PROLOGUE"):
+    print("prologue: mbar_init", T[63][13], "alloc", T[63][14], "syncthreads", T[63][15], "own planes: start", T[62][5], "produced", T[62][6], "tp: enter/scan/exp/split/bar/released", list(T[61][:6]), "planes producer loop", T[62][13], "codes producer loop", T[62][14], "loop body start", T[62][10], "after expect", T[62][11], "after codes bulk", T[62][12], "first codes TMA", T[0][0], "stage0 exp start", T[0][2], "mma start", T[0][4])
+    sys.exit(0)
 t = T
 ev = ["tmaC", "mmaI", "expS", "expE", "mmaS", "mmaE", "epiS", "epiE"]
 if os.environ.get("FULL"):
