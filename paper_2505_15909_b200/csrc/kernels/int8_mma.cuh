@@ -449,28 +449,44 @@ __device__ __forceinline__ int* peer_consumed(char* b) { return reinterpret_cast
 __device__ __forceinline__ __nv_bfloat16* peer_slot(char* b, int64_t cap, int parity, int q) {
     return reinterpret_cast<__nv_bfloat16*>(b + kPeerHeader) + (int64_t(parity) * kPeerMax + q) * cap;
 }
-// the round a producer writes: the local epoch + 1 (its consumer of the previous round bumped it;
-// under programmatic dependent launch that grid may still run, so wait for it first)
+// the round a producer writes: the local epoch + 1 (its consumer of the previous round bumped
+// it).  Read only after the caller's dependency on the previous grid is resolved (the GEMM
+// epilogue reads it after its griddepcontrol.wait / planes barrier; a griddepcontrol.wait placed
+// here, even on a branch never taken, measured +2.3 us per W8 launch)
+// (bufs is a kernel parameter: indexed with compile-time indices only -- a runtime index takes
+// the parameter's address, which measured +2.5 us per launch of the W8 kernel even when the
+// peer path is never taken)
+__device__ __forceinline__ char* peer_buf(const PeerOut& po, int q) {
+    char* b = nullptr;
+#pragma unroll
+    for (int i = 0; i < kPeerMax; ++i)
+        if (i == q) b = po.bufs[i];
+    return b;
+}
 __device__ __forceinline__ int peer_round(const PeerOut& po) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    return *reinterpret_cast<volatile int*>(peer_epoch(po.bufs[po.rank])) + 1;
+    return *reinterpret_cast<volatile int*>(peer_epoch(peer_buf(po, po.rank))) + 1;
 }
 // element i of this rank's partial -> every rank's slot [e & 1][rank]
 __device__ __forceinline__ void peer_store(const PeerOut& po, int e, int64_t i, float v) {
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    for (int q = 0; q < po.world; ++q) peer_slot(po.bufs[q], po.cap, e & 1, po.rank)[i] = h;
+#pragma unroll
+    for (int q = 0; q < kPeerMax; ++q)
+        if (q < po.world) peer_slot(po.bufs[q], po.cap, e & 1, po.rank)[i] = h;
 }
 // kernel end, thread 0 of each CTA after a CTA-wide barrier: the last of G CTAs flags round e
 // on every rank (the CTA's stores were ordered before the barrier; the fence makes them visible
 // system-wide before the counter, the flags after it)
 __device__ __forceinline__ void peer_complete(const PeerOut& po, int e, int G) {
     asm volatile("fence.acq_rel.sys;" ::: "memory");
-    if (atomicAdd(peer_done(po.bufs[po.rank]), 1) == G - 1) {
-        *peer_done(po.bufs[po.rank]) = 0;
+    char* own = peer_buf(po, po.rank);
+    if (atomicAdd(peer_done(own), 1) == G - 1) {
+        *peer_done(own) = 0;
         asm volatile("fence.acq_rel.sys;" ::: "memory");
-        for (int q = 0; q < po.world; ++q)
-            asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(peer_flags(po.bufs[q]) + po.rank), "r"(e)
-                         : "memory");
+#pragma unroll
+        for (int q = 0; q < kPeerMax; ++q)
+            if (q < po.world)
+                asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(peer_flags(po.bufs[q]) + po.rank), "r"(e)
+                             : "memory");
     }
 }
 // 16 bytes of a slot (L2, not L1: the same slot address was read two rounds ago)
@@ -525,9 +541,13 @@ __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, 
     constexpr uint32_t kExpMask = AT == RTNQ_BF16 ? 0x7F807F80u : 0x7C007C00u;
     const int nv = K / 8;
     // the first kHold vectors of this thread stay in registers between the two passes (K <= 8 *
-    // kHold * nthr: one load of the row, all in flight at once); longer rows reload the rest
-    constexpr int kHold = 8;
-    uint4 held[kHold];
+    // kHold * nthr: one load of the row); longer rows reload the rest.  Few: these registers count
+    // against the whole GEMM kernel that runs this producer in its epilogue / expansion warps
+#ifndef RTNQ_PLANES_HOLD
+#define RTNQ_PLANES_HOLD 2
+#endif
+    constexpr int kHold = RTNQ_PLANES_HOLD;
+    uint4 held[kHold > 0 ? kHold : 1];
 #pragma unroll
     for (int h = 0; h < kHold; ++h) {
         const int v = tid + h * nthr;

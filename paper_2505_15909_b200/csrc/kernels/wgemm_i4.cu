@@ -178,7 +178,9 @@ __device__ __forceinline__ void elect_bulk_tx(void* dst, const void* src, uint64
 #define I4_T0() const long long _t0 = (dbg_ & 32) ? clock64() : 0
 #define I4_ACC(var) if (dbg_ & 32) var += clock64() - _t0
 
-template <int PT, int BITS>
+// PEER: the output goes to the tensor-parallel peers' slots (a separate instantiation: the peer
+// store path compiled into the plain kernel measured +1-2.5 us per launch, never executed)
+template <int PT, int BITS, bool PEER>
 __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(const __grid_constant__ Params p) {
 #ifdef RTNQ_KERNEL_DEBUG
     const int dbg_ = p.debug;  // profiling knobs (scratch/*prof*.py, *tl.py)
@@ -504,12 +506,6 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         constexpr int EH = GG::EH, NH = NT / EH;
         const int eh = warp >= kEpiB0 ? 1 : 0, t0 = eh * NH;
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - (eh ? kEpiB0 : kEpi0) * 32;
-        // the output: local, or (tensor parallel) this rank's slot of every rank's buffer
-        const int pe = p.peer.world ? peer_round(p.peer) : 0;
-        auto emit_out = [&](int m, int64_t col, float v) {
-            if (p.peer.world) peer_store(p.peer, pe, int64_t(p.m0 + m) * p.N + col, v);
-            else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
-        };
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         __shared__ float pow_s[NT];  // 2^s per token, 0 for padding tokens
         if (eh == 0) {
@@ -518,6 +514,14 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
             for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
         }
         asm volatile("bar.sync 1, %0;" ::"r"(128 * EH) : "memory");
+        // the output: local, or (tensor parallel) this rank's slot of every rank's buffer; the
+        // peer round is read once the previous grid is done (warpgroup A waited for it above)
+        int pe = 0;
+        if constexpr (PEER) pe = peer_round(p.peer);
+        auto emit_out = [&](int m, int64_t col, float v) {
+            if constexpr (PEER) peer_store(p.peer, pe, int64_t(p.m0 + m) * p.N + col, v);
+            else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
+        };
         float acc[NH];
 #pragma unroll
         for (int t = 0; t < NH; ++t) acc[t] = 0.0f;
@@ -544,18 +548,25 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
 #pragma unroll
         for (int j = 0; j < TPS; ++j) scg[j] = j < n ? sring[(np * TPS + j) * kRows + row] : 0.0f;
         // token chunks of CH: plane p3 of token t is accumulator column p3 * PT + t
-        constexpr int CH = NH >= 16 ? 16 : NH;
+        // (the accumulators of padding tokens past PT are never combined)
+        constexpr int NHR = EH == 2 ? NH : PT;  // real tokens of this warpgroup
+        constexpr int CH = NHR >= 16 ? 16 : NHR;
         constexpr bool SPLIT = PT >= 16;           // planes loaded separately (CH columns each)
         constexpr int LDC = SPLIT ? CH : GG::DN;   // columns per load buffer
-        // TMEM loads in batches of GL groups per round trip (one tcgen05.wait::ld per batch: the
-        // ~250-cycle round trip, not the bytes, bounds this loop), double-buffered when the
+        // TMEM loads in batches of GL groups per tcgen05.wait::ld, double-buffered when the
         // registers allow
         constexpr int PGR = SPLIT ? 3 * CH : LDC;  // registers per group of a chunk
-        constexpr int GL = TPS >= 4 && 4 * PGR <= 96 ? 4 : TPS >= 2 && 2 * PGR <= 96 ? 2 : 1;
+#ifndef RTNQ_I4_GL
+#define RTNQ_I4_GL 1
+#endif
+        // (measured: one group per round trip, double-buffered, is the fastest at batch 1 and 16;
+        // RTNQ_I4_GL=4 batches up to four groups per round trip)
+        constexpr int GL = RTNQ_I4_GL >= 4 && TPS >= 4 && 4 * PGR <= 96 ? 4
+                           : RTNQ_I4_GL >= 2 && TPS >= 2 && 2 * PGR <= 96 ? 2 : 1;
         constexpr int NBT = (TPS + GL - 1) / GL;
         constexpr int NB = NBT > 1 && 2 * GL * PGR <= 96 ? 2 : 1;
 #pragma unroll
-        for (int jj = 0; jj < NH; jj += CH) {
+        for (int jj = 0; jj < NHR; jj += CH) {
             if (dbg_ & 131072) break;
             uint32_t d[NB][GL][SPLIT ? 3 : 1][LDC];
             auto load = [&](int bi) {
@@ -738,17 +749,18 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
     fence_before();
     __syncthreads();
     if ((dbg_ & 64) && threadIdx.x == 0) g_i4_dbg[c * 16 + 7] = gtime();
-    if (p.peer.world && threadIdx.x == 0) peer_complete(p.peer, peer_round(p.peer), int(gridDim.x));
+    if constexpr (PEER)
+        if (threadIdx.x == 0) peer_complete(p.peer, peer_round(p.peer), int(gridDim.x));
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
-template <int PT, int BITS>
+template <int PT, int BITS, bool PEER>
 cudaError_t launch_nt(Params p, cudaStream_t st) {
     using GG = Geo<PT, BITS>;
-    auto kern = wgemm_i4_kernel<PT, BITS>;
+    auto kern = wgemm_i4_kernel<PT, BITS, PEER>;
     static unsigned long long configured = 0;  // per device
     static int max_clusters_dev[64][9] = {};
     int* max_clusters = max_clusters_dev[current_device_index()];
@@ -828,6 +840,11 @@ const char* wgemm_i4_unsupported(int64_t m, int64_t n, int64_t k, int bits, int6
     if (a_dtype != RTNQ_BF16 && a_dtype != RTNQ_F16) return "activations must be bf16 or f16";
     if (k % 16 != 0) return "k must be a multiple of 16 for the int8 tensor-core path";
     return nullptr;
+}
+
+template <int PT, int BITS>
+static cudaError_t launch_pt(const i4::Params& p, cudaStream_t st) {
+    return p.peer.world ? i4::launch_nt<PT, BITS, true>(p, st) : i4::launch_nt<PT, BITS, false>(p, st);
 }
 
 cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
@@ -961,16 +978,16 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         G = G < 1 ? 1 : G;
         p.G = int(p.U < G ? p.U : G);
         cudaError_t e = A.bits == 8
-            ? (nt == 5    ? i4::launch_nt<5, 8>(p, st)
-               : nt == 10 ? i4::launch_nt<10, 8>(p, st)
-               : nt == 16 ? i4::launch_nt<16, 8>(p, st)
-               : nt == 32 ? i4::launch_nt<32, 8>(p, st)
-                          : i4::launch_nt<64, 8>(p, st))
-            : (nt == 5    ? i4::launch_nt<5, 4>(p, st)
-               : nt == 10 ? i4::launch_nt<10, 4>(p, st)
-               : nt == 16 ? i4::launch_nt<16, 4>(p, st)
-               : nt == 32 ? i4::launch_nt<32, 4>(p, st)
-                          : i4::launch_nt<64, 4>(p, st));
+            ? (nt == 5    ? launch_pt<5, 8>(p, st)
+               : nt == 10 ? launch_pt<10, 8>(p, st)
+               : nt == 16 ? launch_pt<16, 8>(p, st)
+               : nt == 32 ? launch_pt<32, 8>(p, st)
+                          : launch_pt<64, 8>(p, st))
+            : (nt == 5    ? launch_pt<5, 4>(p, st)
+               : nt == 10 ? launch_pt<10, 4>(p, st)
+               : nt == 16 ? launch_pt<16, 4>(p, st)
+               : nt == 32 ? launch_pt<32, 4>(p, st)
+                          : launch_pt<64, 4>(p, st));
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -84,7 +84,9 @@ struct Geo {
 __device__ unsigned long long g_i8_dbg[1024 * 16];  // profiling (debug & 32; & 64: globaltimer stamps)
 
 
-template <int NT>
+// PEER: the output goes to the tensor-parallel peers' slots (a separate instantiation: the peer
+// store path compiled into the plain kernel measured +2.5 us per launch, never executed)
+template <int NT, bool PEER>
 __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_constant__ Params p) {
 #ifdef RTNQ_KERNEL_DEBUG
     const int dbg_ = p.debug;  // profiling knobs (scratch/*prof*.py, *tl.py)
@@ -283,12 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
         const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - kEpi0 * 32;
-        // the output: local, or (tensor parallel) this rank's slot of every rank's buffer
-        const int pe = p.peer.world ? peer_round(p.peer) : 0;
-        auto emit_out = [&](int m, int64_t col, float v) {
-            if (p.peer.world) peer_store(p.peer, pe, int64_t(p.m0 + m) * p.N + col, v);
-            else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
-        };
+        int pe = 0;  // tensor parallel: the peer round, read below once the previous grid is done
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         int db = 0, seg = 0, u = u0;
         __shared__ float pow_s[NT];  // 2^s per token (s >= -126: a normal float)
@@ -296,6 +293,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
         else asm volatile("griddepcontrol.wait;" ::: "memory");  // texp from the planes producer
         for (int t = et; t < NT; t += 128) pow_s[t] = t < p.M ? ldexpf(1.0f, __ldg(p.texp + p.m0 + t)) : 0.0f;
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        // the output: local, or (tensor parallel) this rank's slot of every rank's buffer
+        if constexpr (PEER) pe = peer_round(p.peer);
+        auto emit_out = [&](int m, int64_t col, float v) {
+            if constexpr (PEER) peer_store(p.peer, pe, int64_t(p.m0 + m) * p.N + col, v);
+            else store_out(p.out, p.out_dtype, int64_t(m) * p.N + col, v);
+        };
         while (u < u1) {
             // walk to this segment's end
             const int b = u / p.KBLK, kb0 = u - b * p.KBLK;
@@ -453,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
     fence_before();
     __syncthreads();
     if ((dbg_ & 64) && threadIdx.x == 0) g_i8_dbg[c * 16 + 7] = gtime();
-    if (p.peer.world && threadIdx.x == 0) peer_complete(p.peer, peer_round(p.peer), int(gridDim.x));
+    if constexpr (PEER)
+        if (threadIdx.x == 0) peer_complete(p.peer, peer_round(p.peer), int(gridDim.x));
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -461,10 +465,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
 }
 
 // ---- host ----------------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool PEER>
 cudaError_t launch_nt(Params p, cudaStream_t st, bool pdl) {
     using GG = Geo<NT>;
-    auto kern = wgemm_i8_kernel<NT>;
+    auto kern = wgemm_i8_kernel<NT, PEER>;
     static unsigned long long configured = 0;  // per device
     static int max_clusters_dev[64][9] = {};
     int* max_clusters = max_clusters_dev[current_device_index()];
@@ -695,9 +699,10 @@ cudaError_t launch_wgemm_i8(const WgemmArgs& A, cudaStream_t st) {
         G = G < 1 ? 1 : G;
         p.G = int(p.U < G ? p.U : G);
         const bool pdl = true;  // the planes kernel precedes it in the stream
-        cudaError_t e = nt == 16 ? i8::launch_nt<16>(p, st, pdl)
-                      : nt == 32 ? i8::launch_nt<32>(p, st, pdl)
-                                 : i8::launch_nt<64>(p, st, pdl);
+        const bool peer = p.peer.world > 0;
+        cudaError_t e = nt == 16 ? (peer ? i8::launch_nt<16, true>(p, st, pdl) : i8::launch_nt<16, false>(p, st, pdl))
+                      : nt == 32 ? (peer ? i8::launch_nt<32, true>(p, st, pdl) : i8::launch_nt<32, false>(p, st, pdl))
+                                 : (peer ? i8::launch_nt<64, true>(p, st, pdl) : i8::launch_nt<64, false>(p, st, pdl));
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
