@@ -229,6 +229,21 @@ class QuantWeight:
         return self.rows * self.cols * self.bits // 8 + self.rows * self.gpr * 2
 
 
+_qflags = {}
+
+
+def _quant_flag(device, checked: bool):
+    """Persistent per-device error flags of quantize_pack (no memset per call): the checked one
+    is read and cleared by every check (so it is zero at the next call); the unchecked one only
+    accumulates and is never read."""
+    torch = _torch()
+    key = (str(device), checked)
+    f = _qflags.get(key)
+    if f is None:
+        f = _qflags[key] = torch.zeros(1, dtype=torch.int32, device=device)
+    return f
+
+
 def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None,
                   row_major=False, kernel=False, scales_f32=False, scales_f16=False,
                   check=True, stream=None) -> QuantWeight:
@@ -274,7 +289,7 @@ def quantize_pack(w, bits: int, group: int, ragged: bool = False, *, native=None
     kind = imma if imma is not None else NATIVE
     wsb = lib().rtnq_dev_quantize_workspace_bytes_ex(rows, cols, bits, group, int(ragged), kind)
     ws = torch.empty(max(wsb, 1), **u8)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    err = _quant_flag(dev, check)
     st = _stream(stream)
     _check(lib().rtnq_dev_quantize_pack_ex(
         _ptr(w), _dt(w), rows, cols, bits, group, int(ragged), kind, _ptr(out.codes_row_major),

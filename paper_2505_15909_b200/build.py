@@ -81,7 +81,7 @@ def build(verbose=False, clean=False):
         if log:
             sys.stderr.write(log)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas",
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart",
                "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:

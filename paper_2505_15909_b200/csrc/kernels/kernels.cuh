@@ -112,6 +112,9 @@ const char* launch_dequant_first(const void* a, int a_dtype, int64_t m, int64_t 
                                  const uint8_t* codes, Layout L, int bits, int64_t g, int64_t gpr,
                                  const uint16_t* scales, int sorder, void* out, int odtype, void* ws,
                                  cudaStream_t st);
+// dense_tc.cu: out[m][n] = a . (hi + lo)^T on tcgen05 (16-bit operands, f32 accumulation)
+const char* launch_dense_hilo(const void* a, int64_t lda, const void* hi, const void* lo, int64_t ldw, int a_dtype,
+                              int64_t m, int64_t n, int64_t k, void* out, int odtype, cudaStream_t st);
 
 // wgemm_i4.cu: W4 group-128 on tcgen05.mma.kind::i8 over RTNQ_NATIVE_I4 nibble tiles
 const char* wgemm_i4_unsupported(int64_t m, int64_t n, int64_t k, int bits, int64_t g, int a_dtype);

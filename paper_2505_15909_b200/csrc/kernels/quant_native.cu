@@ -159,16 +159,22 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
 }
 
 constexpr int kI4Threads = 256;  // 8 lanes per row (16 codes each), 32 rows per pass
-constexpr int kI4Pass = 2;       // passes per CTA: 64 rows of one 128-code group
+#ifndef RTNQ_QI4_PASS
+#define RTNQ_QI4_PASS 2
+#endif
+#ifndef RTNQ_QI4_MINB
+#define RTNQ_QI4_MINB 6  // 40 registers: 6 CTAs per SM (measured +2 % over 4)
+#endif
+constexpr int kI4Pass = RTNQ_QI4_PASS;  // passes per CTA: 32 * kI4Pass rows of one 128-code group
 
 }  // namespace
 
-// grid (cols / 128, ceil(rows / 128) * 2): CTA (x, y) quantizes group x of rows [64y, 64y + 64);
+// grid (cols / 128, ceil(rows / 128) * 128 / (32 kI4Pass)): CTA (x, y) quantizes group x of 32 kI4Pass rows;
 // rows >= `rows` (inside the last 128-row tile) only get their zero padding written.
 // Lane j of a row holds codes p..p+7 and p+64..p+71 (p = 8j): exactly the 8 NATIVE_I4 bytes
 // p..p+7 of the row (high nibble code p+i, low nibble code p+64+i).
 template <int DT>
-__global__ void __launch_bounds__(kI4Threads)
+__global__ void __launch_bounds__(kI4Threads, RTNQ_QI4_MINB)
 quant_i4_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uint8_t* __restrict__ ni4,
                 uint8_t* __restrict__ rm, float* __restrict__ s32, uint16_t* __restrict__ s16,
                 uint16_t* __restrict__ s16n, int32_t* __restrict__ err) {
@@ -376,7 +382,7 @@ bool quant_rowwise_supported(int64_t rows, int64_t cols, int bits, int64_t g) {
 
 void launch_quant_i4(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* ni4, uint8_t* rm, float* s32,
                      uint16_t* s16, uint16_t* s16n, int32_t* err, cudaStream_t st) {
-    const dim3 grid(unsigned(cols / 128), unsigned((rows + 127) / 128 * 2));
+    const dim3 grid(unsigned(cols / 128), unsigned((rows + 127) / 128 * (128 / (32 * kI4Pass))));
     if (dtype == RTNQ_F32) quant_i4_kernel<RTNQ_F32><<<grid, kI4Threads, 0, st>>>(w, rows, cols, ni4, rm, s32, s16, s16n, err);
     else if (dtype == RTNQ_F16) quant_i4_kernel<RTNQ_F16><<<grid, kI4Threads, 0, st>>>(w, rows, cols, ni4, rm, s32, s16, s16n, err);
     else quant_i4_kernel<RTNQ_BF16><<<grid, kI4Threads, 0, st>>>(w, rows, cols, ni4, rm, s32, s16, s16n, err);

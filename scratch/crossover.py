@@ -1,4 +1,4 @@
-"""Fused (kind::i8 weight-only) vs dequant-first (hi+lo split + cuBLAS) on the 8B gate_up and
+"""Fused (kind::i8 weight-only) vs dequant-first (hi+lo split + the tcgen05 dense GEMM) on the 8B gate_up and
 qkv shapes, over the batch: the B200 crossover for gemm_auto (bench.cpp:69-192)."""
 import json, os, statistics, sys, torch
 sys.path.insert(0, os.getcwd())
@@ -9,7 +9,7 @@ for bits in (4, 8):
         g = 128 if bits == 4 else 4096
         q = rq.quantize_pack((torch.rand(n, k, device="cuda") * 2 - 1).to(torch.bfloat16), bits, g)
         ws = rq.Workspace(device="cuda")
-        for m in (64, 256, 512, 1024):
+        for m in (64, 256, 512, 1024, 2048, 4096):
             a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
             out = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
             row = {}

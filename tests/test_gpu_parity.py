@@ -361,8 +361,9 @@ def test_graft_smoke_entry():
 
 @pytest.mark.parametrize("bits,g,m", [(4, 128, 1), (4, 128, 300), (8, 4096, 64), (4, 64, 96), (8, 128, 130)])
 def test_dequant_first_tensor_path(oracle, bits, g, m):
-    """dequant-first on the tensor cores (exact hi + lo 16-bit weight split,
-    two cuBLAS GEMMs with f32 accumulation), any codes layout, against the f64 oracle."""
+    """dequant-first on the tensor cores (exact hi + lo 16-bit weight split, both
+    terms accumulated in one hand-written tcgen05 GEMM, dense_tc.cu), any codes layout, against
+    the f64 oracle."""
     n, k = 520, 4096 if g == 4096 else 1024
     q, codes, s16w = _make(oracle, n, k, bits, g, seed=m + bits + g)
     a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
@@ -371,6 +372,24 @@ def test_dequant_first_tensor_path(oracle, bits, g, m):
     assert rel_frob(out.cpu().numpy(), ref) <= TOL
     o16 = rq.linear(a, q, out_dtype=torch.bfloat16, path=rq.PATH_DEQUANT_FIRST)
     assert rel_frob(o16.float().cpu().numpy(), ref) <= 8e-3
+
+
+@pytest.mark.parametrize("m,n,k,g,dt", [(257, 200, 1000, 128, torch.bfloat16),  # k % 8 != 0, ragged
+                                         (130, 136, 520, 8, torch.float16),       # f16, odd tiles
+                                         (1024, 384, 2048, 128, torch.bfloat16)])
+def test_dense_tc_odd_shapes(oracle, m, n, k, g, dt):
+    """The tcgen05 dequant-first GEMM on partial tiles (m, n not multiples of 128), rows not a
+    multiple of 8 elements (padded copies for the TMA), f16 operands, every output type."""
+    ragged = k % g != 0
+    q, codes, s16w = _make(oracle, n, k, 4, g, seed=m + n, ragged=ragged)
+    a = torch.empty(m, k, device="cuda").uniform_(-1, 1).to(dt)
+    ref = oracle.gemm_oracle_f64(a.float().cpu().numpy(), codes, g, s16w)
+    for odt, tol in ((torch.float32, TOL), (torch.bfloat16, 8e-3), (torch.float16, 1e-3)):
+        out = rq.linear(a, q, out_dtype=odt, path=rq.PATH_DEQUANT_FIRST)
+        assert rel_frob(out.float().cpu().numpy(), ref) <= tol, odt
+    # deterministic
+    o1 = rq.linear(a, q, out_dtype=torch.float32, path=rq.PATH_DEQUANT_FIRST)
+    assert torch.equal(o1, rq.linear(a, q, out_dtype=torch.float32, path=rq.PATH_DEQUANT_FIRST))
 
 
 def test_gemm_auto_dispatch_tensor_paths(oracle):
