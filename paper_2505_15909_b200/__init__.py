@@ -345,10 +345,11 @@ _default_ws = {}
 FLAG_PDL = 1
 
 
-def _default_workspace(device, stream, nbytes):
-    """The per-(device, stream) default workspace (its stream-K counters and partials must not
-    be shared by two streams at once)."""
-    key = (str(device), _stream(stream).value)
+def _default_workspace(device, stream, nbytes, kind="linear"):
+    """The per-(kind, device, stream) default workspace: its self-resetting counters and partials
+    must not be shared by two streams at once, nor by two kinds of kernel with different
+    layouts of the buffer (the linears' stream-K counters vs the attention's split merge)."""
+    key = (kind, str(device), _stream(stream).value)
     ws = _default_ws.get(key)
     if ws is None:
         ws = _default_ws[key] = Workspace(nbytes, device)
@@ -491,7 +492,7 @@ def decode_attention(qkv, k_cache, v_cache, out, hq, hkv, pos, head_dim=128, the
     batch, max_len = k_cache.shape[0], k_cache.shape[1]
     wsb = lib().rtnq_dev_decode_attention_workspace_bytes(batch, hq, hkv, max_len)
     if workspace is None:
-        workspace = _default_workspace(qkv.device, stream, wsb)
+        workspace = _default_workspace(qkv.device, stream, wsb, kind="attention")
     buf = workspace.ensure(wsb)
     _check(lib().rtnq_dev_decode_attention_ws(_ptr(qkv), _ptr(k_cache), _ptr(v_cache), _ptr(out),
                                               batch, hq, hkv, head_dim, max_len, pos, theta,

@@ -201,3 +201,23 @@ def test_decode_attention_merge_paths(batch, pos):
             os.environ.pop("RTNQ_ATTN_NO_CLUSTER", None)
     torch.cuda.synchronize()
     assert rel(outs[0], outs[1].float()) < 1e-2
+
+
+def test_default_workspaces_of_attention_and_linear_are_separate():
+    """decode_attention and linear with no explicit workspace on the same stream: each kind gets
+    its own default buffer (the attention's split-merge scratch once overwrote the linears'
+    stream-K counters in a shared default buffer, and the next stream-K linear never finished)."""
+    batch, hq, hkv, d, max_len, pos = 4, 32, 8, 128, 800, 700
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = (torch.rand(batch, (hq + 2 * hkv) * d, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    kc = (torch.rand(batch, max_len, hkv, d, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    vc = (torch.rand(batch, max_len, hkv, d, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    out = torch.empty(batch, hq * d, dtype=torch.bfloat16, device="cuda")
+    w = ((torch.rand(12800, 1024, device="cuda", generator=g) * 2 - 1) * 0.05).to(torch.bfloat16)
+    q = rq.quantize_pack(w, 4, 128)  # 100 row-blocks: stream-K over all SMs
+    a = torch.empty(3, 1024, device="cuda").uniform_(-1, 1, generator=g).to(torch.bfloat16)
+    ref = rq.linear(a, q, workspace=rq.Workspace(device="cuda"))
+    for _ in range(3):
+        rq.decode_attention(qkv, kc, vc, out, hq, hkv, pos)
+        y = rq.linear(a, q)  # default workspace, synchronizing check
+        assert torch.equal(y, ref)
