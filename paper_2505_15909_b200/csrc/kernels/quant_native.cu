@@ -162,10 +162,16 @@ constexpr int kI4Threads = 256;  // 8 lanes per row (16 codes each), 32 rows per
 #ifndef RTNQ_QI4_PASS
 #define RTNQ_QI4_PASS 2
 #endif
-#ifndef RTNQ_QI4_MINB
-#define RTNQ_QI4_MINB 6  // 40 registers: 6 CTAs per SM (measured +2 % over 4)
+#ifndef RTNQ_QI4_LPR
+#define RTNQ_QI4_LPR 8  // 4 (32 codes per lane) measured 6 % slower: more near-tie passes redone
 #endif
-constexpr int kI4Pass = RTNQ_QI4_PASS;  // passes per CTA: 32 * kI4Pass rows of one 128-code group
+#ifndef RTNQ_QI4_MINB  // CTAs per SM the register budget must allow
+#define RTNQ_QI4_MINB (RTNQ_QI4_LPR == 4 ? 4 : 6)
+#endif
+constexpr int kI4Lpr = RTNQ_QI4_LPR;   // lanes per row (4: 32 codes per lane, 8: 16)
+constexpr int kI4Pass = RTNQ_QI4_PASS;  // passes per CTA: (256 / kI4Lpr) * kI4Pass rows of one group
+static_assert(kI4Lpr == 4 || kI4Lpr == 8, "");
+static_assert(128 % (256 / kI4Lpr * kI4Pass) == 0, "a CTA covers a whole divisor of a 128-row tile");
 
 }  // namespace
 
@@ -178,31 +184,39 @@ __global__ void __launch_bounds__(kI4Threads, RTNQ_QI4_MINB)
 quant_i4_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uint8_t* __restrict__ ni4,
                 uint8_t* __restrict__ rm, float* __restrict__ s32, uint16_t* __restrict__ s16,
                 uint16_t* __restrict__ s16n, int32_t* __restrict__ err) {
-    const int t = threadIdx.x, lane = t & 31, j = t & 7, p = 8 * j;
+    // LPR lanes per row; lane j holds V 8-code vectors of each half: codes p .. p + 8V - 1 and
+    // 64 + p .. (p = 8 V j), i.e. exactly the 8V NATIVE_I4 bytes p .. p + 8V - 1 of the row
+    constexpr int LPR = kI4Lpr, V = 8 / LPR, RPP = kI4Threads / LPR;  // rows per pass
+    const int t = threadIdx.x, lane = t & 31, j = t & (LPR - 1), p = 8 * V * j;
     const int64_t grp = blockIdx.x, gpr = cols / 128;
-    const int64_t row0 = int64_t(blockIdx.y) * (kI4Pass * 32) + (t >> 3);
-    Raw8<DT> lo[kI4Pass], hi[kI4Pass];
+    const int64_t row0 = int64_t(blockIdx.y) * (kI4Pass * RPP) + t / LPR;
+    Raw8<DT> lo[kI4Pass][V], hi[kI4Pass][V];
 #pragma unroll
     for (int s = 0; s < kI4Pass; ++s) {  // all loads first
-        const int64_t r = row0 + s * 32;
-        if (r < rows) {
-            const int64_t base = r * cols + grp * 128 + p;
-            lo[s].load(w, base);
-            hi[s].load(w, base + 64);
-        } else {
-            lo[s].zero(), hi[s].zero();
+        const int64_t r = row0 + s * RPP;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (r < rows) {
+                const int64_t base = r * cols + grp * 128 + p + 8 * v;
+                lo[s][v].load(w, base);
+                hi[s][v].load(w, base + 64);
+            } else {
+                lo[s][v].zero(), hi[s][v].zero();
+            }
         }
     }
-    // group absmax keys of every pass (8 lanes per row); then lane j computes the scale of pass
-    // j % kI4Pass once -- the f64 division runs once per warp for all its 16 groups -- and the
+    // group absmax keys of every pass (LPR lanes per row); then lane j computes the scale of pass
+    // j % kI4Pass once -- the f64 division runs once per lane group for all its passes -- and the
     // row's lanes fetch theirs
     uint32_t keys[kI4Pass];
 #pragma unroll
     for (int s = 0; s < kI4Pass; ++s) {
-        uint32_t key = max(mag_key(lo[s]), mag_key(hi[s]));
-        key = max(key, __shfl_xor_sync(0xffffffffu, key, 1));
-        key = max(key, __shfl_xor_sync(0xffffffffu, key, 2));
-        keys[s] = max(key, __shfl_xor_sync(0xffffffffu, key, 4));
+        uint32_t key = 0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) key = max(key, max(mag_key(lo[s][v]), mag_key(hi[s][v])));
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+        keys[s] = key;
     }
     uint32_t mykey = keys[0];
 #pragma unroll
@@ -213,8 +227,8 @@ quant_i4_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uint8_t*
     bool bad = false;
 #pragma unroll
     for (int s = 0; s < kI4Pass; ++s) {
-        const int64_t r = row0 + s * 32;
-        const int src = (lane & ~7) | s;
+        const int64_t r = row0 + s * RPP;
+        const int src = (lane & ~(LPR - 1)) | (s % LPR);
         const bool nonfinite = key_nonfinite<DT>(keys[s]);
         const float m = nonfinite ? 0.0f : key_value<DT>(keys[s]);
         const float sc = __shfl_sync(0xffffffffu, mysc, src);
@@ -222,41 +236,69 @@ quant_i4_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uint8_t*
         qs.s = __shfl_sync(0xffffffffu, myqs.s, src);
         qs.inv = __shfl_sync(0xffffffffu, myqs.inv, src);
         qs.pre = __shfl_sync(0xffffffffu, myqs.pre, src);
-        uint32_t ql[8], qh[8];
-        const float dm = codes_fast8<4>(hi[s], qs.inv, qh, codes_fast8<4>(lo[s], qs.inv, ql, 0.0f));
+        uint32_t ql[V][8], qh[V][8];
+        float dm = 0.0f;
+#pragma unroll
+        for (int v = 0; v < V; ++v) dm = codes_fast8<4>(hi[s][v], qs.inv, qh[v], codes_fast8<4>(lo[s][v], qs.inv, ql[v], dm));
+        // a warp holding any near-tie (common for bf16 weights: an absmax whose mantissa is a
+        // multiple of 5 puts exact half-integers on the bf16 grid; measured ~25 % of the W4
+        // pass time), a non-finite weight or a tiny scale redoes its weights exactly.  (Redoing
+        // only the near-tie weights, one exact test per weight index, measured slower: code size.)
         if (__any_sync(0xffffffffu, !(dm < FastQ<4>::kThr) || nonfinite || qs.pre != 1.0f)) {
-            float vl[8], vh[8];
-            lo[s].get(vl), hi[s].get(vh);
-            bad |= codes_exact8<4>(vl, qs, ql);
-            bad |= codes_exact8<4>(vh, qs, qh);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                float vl[8], vh[8];
+                lo[s][v].get(vl), hi[s][v].get(vh);
+                bad |= codes_exact8<4>(vl, qs, ql[v]);
+                bad |= codes_exact8<4>(vh, qs, qh[v]);
+            }
         } else {
             const float nt = neg_top<4>(m, sc);
             if (__any_sync(0xffffffffu, nt == nt)) {  // absmax == 7.5 S exactly: -absmax -> -8
-                float vl[8], vh[8];
-                lo[s].get(vl), hi[s].get(vh);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    ql[i] = vl[i] == nt ? FastQ<4>::kMinBits : ql[i];
-                    qh[i] = vh[i] == nt ? FastQ<4>::kMinBits : qh[i];
+                for (int v = 0; v < V; ++v) {
+                    float vl[8], vh[8];
+                    lo[s][v].get(vl), hi[s][v].get(vh);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        ql[v][i] = vl[i] == nt ? FastQ<4>::kMinBits : ql[v][i];
+                        qh[v][i] = vh[i] == nt ? FastQ<4>::kMinBits : qh[v][i];
+                    }
                 }
             }
         }
-        const uint32_t L0 = pack4(ql[0], ql[1], ql[2], ql[3]), L1 = pack4(ql[4], ql[5], ql[6], ql[7]);
-        const uint32_t H0 = pack4(qh[0], qh[1], qh[2], qh[3]), H1 = pack4(qh[4], qh[5], qh[6], qh[7]);
+        uint32_t L[V][2], H[V][2];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            L[v][0] = pack4(ql[v][0], ql[v][1], ql[v][2], ql[v][3]), L[v][1] = pack4(ql[v][4], ql[v][5], ql[v][6], ql[v][7]);
+            H[v][0] = pack4(qh[v][0], qh[v][1], qh[v][2], qh[v][3]), H[v][1] = pack4(qh[v][4], qh[v][5], qh[v][6], qh[v][7]);
+        }
         if (ni4) {  // byte i = code(p + i) << 4 | code(p + 64 + i) & 15
-            const uint32_t b0 = ((L0 << 4) & 0xF0F0F0F0u) | (H0 & 0x0F0F0F0Fu);
-            const uint32_t b1 = ((L1 << 4) & 0xF0F0F0F0u) | (H1 & 0x0F0F0F0Fu);
+            uint32_t b[2 * V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                b[2 * v] = ((L[v][0] << 4) & 0xF0F0F0F0u) | (H[v][0] & 0x0F0F0F0Fu);
+                b[2 * v + 1] = ((L[v][1] << 4) & 0xF0F0F0F0u) | (H[v][1] & 0x0F0F0F0Fu);
+            }
             const int64_t rr = r & 127, tile = (r >> 7) * gpr + grp;
-            *reinterpret_cast<uint2*>(ni4 + tile * 8192 + rr * 64 + (((j >> 1) ^ ((rr >> 1) & 3)) << 4) +
-                                      ((j & 1) << 3)) = make_uint2(b0, b1);
+            uint8_t* dst = ni4 + tile * 8192 + rr * 64;
+            if constexpr (V == 2) {  // one whole 16-byte chunk: chunk j
+                *reinterpret_cast<uint4*>(dst + ((j ^ ((rr >> 1) & 3)) << 4)) = make_uint4(b[0], b[1], b[2], b[3]);
+            } else {                 // half a chunk: chunk j / 2, half j % 2
+                *reinterpret_cast<uint2*>(dst + (((j >> 1) ^ ((rr >> 1) & 3)) << 4) + ((j & 1) << 3)) =
+                    make_uint2(b[0], b[1]);
+            }
         }
         if (r < rows) {
             if (rm) {  // offset binary (packing.cpp:24-30): element 2i low nibble, 2i+1 high
-                const uint32_t e0 = __byte_perm(L0, L1, 0x6420), o0 = __byte_perm(L0, L1, 0x7531);
-                const uint32_t e1 = __byte_perm(H0, H1, 0x6420), o1 = __byte_perm(H0, H1, 0x7531);
-                uint8_t* dst = rm + ((r * cols + grp * 128 + p) >> 1);
-                *reinterpret_cast<uint32_t*>(dst) = ((e0 & 0x0F0F0F0Fu) | ((o0 << 4) & 0xF0F0F0F0u)) ^ 0x88888888u;
-                *reinterpret_cast<uint32_t*>(dst + 32) = ((e1 & 0x0F0F0F0Fu) | ((o1 << 4) & 0xF0F0F0F0u)) ^ 0x88888888u;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const uint32_t e0 = __byte_perm(L[v][0], L[v][1], 0x6420), o0 = __byte_perm(L[v][0], L[v][1], 0x7531);
+                    const uint32_t e1 = __byte_perm(H[v][0], H[v][1], 0x6420), o1 = __byte_perm(H[v][0], H[v][1], 0x7531);
+                    uint8_t* dst = rm + ((r * cols + grp * 128 + p + 8 * v) >> 1);
+                    *reinterpret_cast<uint32_t*>(dst) = ((e0 & 0x0F0F0F0Fu) | ((o0 << 4) & 0xF0F0F0F0u)) ^ 0x88888888u;
+                    *reinterpret_cast<uint32_t*>(dst + 32) = ((e1 & 0x0F0F0F0Fu) | ((o1 << 4) & 0xF0F0F0F0u)) ^ 0x88888888u;
+                }
             }
             if (j == 0) {
                 if (s32) s32[r * gpr + grp] = sc;
@@ -373,7 +415,7 @@ quant_rowwise_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uin
 }
 
 bool quant_i4_supported(int64_t rows, int64_t cols, int bits, int64_t g) {
-    return bits == 4 && g == 128 && rows > 0 && cols > 0 && cols % 128 == 0 && (rows + 127) / 128 * 2 <= 65535;
+    return bits == 4 && g == 128 && rows > 0 && cols > 0 && cols % 128 == 0 && (rows + 127) / 128 * 4 <= 65535;
 }
 
 bool quant_rowwise_supported(int64_t rows, int64_t cols, int bits, int64_t g) {
@@ -382,7 +424,7 @@ bool quant_rowwise_supported(int64_t rows, int64_t cols, int bits, int64_t g) {
 
 void launch_quant_i4(const void* w, int dtype, int64_t rows, int64_t cols, uint8_t* ni4, uint8_t* rm, float* s32,
                      uint16_t* s16, uint16_t* s16n, int32_t* err, cudaStream_t st) {
-    const dim3 grid(unsigned(cols / 128), unsigned((rows + 127) / 128 * (128 / (32 * kI4Pass))));
+    const dim3 grid(unsigned(cols / 128), unsigned((rows + 127) / 128 * (128 / (kI4Threads / kI4Lpr * kI4Pass))));
     if (dtype == RTNQ_F32) quant_i4_kernel<RTNQ_F32><<<grid, kI4Threads, 0, st>>>(w, rows, cols, ni4, rm, s32, s16, s16n, err);
     else if (dtype == RTNQ_F16) quant_i4_kernel<RTNQ_F16><<<grid, kI4Threads, 0, st>>>(w, rows, cols, ni4, rm, s32, s16, s16n, err);
     else quant_i4_kernel<RTNQ_BF16><<<grid, kI4Threads, 0, st>>>(w, rows, cols, ni4, rm, s32, s16, s16n, err);

@@ -909,7 +909,11 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     // in the GEMM; gate_up / down 23.7 / 19.4 vs 21.7 / 18.5)
     const int64_t units = ((A.n + i4::kRows - 1) / i4::kRows) * ((A.k + i4::kKB - 1) / i4::kKB);
     // (W8 group-128: the stand-alone kernel, as for W8 per-channel: 23.4 vs 25.3 us, gate_up batch 16)
-    const bool in_gemm = own_planes && !planes_kernel && A.bits == 4 && A.m >= imma::kOwnPlanesMinM && units >= 2048 &&
+    static const int64_t min_units = [] {
+        const char* e = std::getenv("RTNQ_OWN_PLANES_MIN_UNITS");
+        return e ? int64_t(std::atoll(e)) : int64_t(2048);
+    }();
+    const bool in_gemm = own_planes && !planes_kernel && A.bits == 4 && A.m >= imma::kOwnPlanesMinM && units >= min_units &&
                          (reinterpret_cast<uintptr_t>(A.a) & 15) == 0 && !(dbg & 64);
     if (in_gemm) {
         p.own.a = A.a;
