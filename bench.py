@@ -363,6 +363,40 @@ def quantize_record(cx, bits, n=28672, k=4096, reps=10):
             "note": "one quantize_pack call (allocations + the fused kernel), 2 weight copies alternating"}
 
 
+def exact_record(cx, reps=5):
+    """The drop-in path a reference consumer gets (rtnq::gemm_fused: f32 activations, the
+    reference's kernel_interleaved(16, 4) codes and f32 scales, bit-identical to the reference):
+    the four Llama-3.1-8B layer linears at W4 g128, batch 1 and 16, CUDA events."""
+    import paper_2505_15909_b200 as rq
+    torch = cx.torch
+    qs, nbytes = [], 0
+    with torch.cuda.stream(cx.stream):  # inputs made on the stream that uses them
+        for n, k in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)):
+            w = ((torch.rand(n, k, device=cx.dev) * 2 - 1) * 0.02).to(torch.bfloat16)
+            qs.append((n, k, rq.quantize_pack(w, 4, 128, native=True, kernel=True, scales_f32=True,
+                                              stream=cx.stream)))
+            nbytes += n * k // 2 + n * (-(-k // 128)) * 2
+    out = {}
+    for m in (1, 16):
+        args = []
+        for n, k, q in qs:
+            with torch.cuda.stream(cx.stream):
+                a = torch.empty(m, k, device=cx.dev).uniform_(-1, 1)
+                o = torch.empty(m, n, device=cx.dev)
+            args.append((a, rq.F32, m, k, q.codes_kernel, rq.layout(rq.KERNEL_INTERLEAVED), 4, n, 128, 0,
+                         q.scales_f32, rq.F32, rq.SCALES_REF, o, rq.F32))
+
+        def run():
+            for x in args:
+                rq.linear_raw(*x, path=rq.PATH_FUSED, stream=cx.stream)
+
+        ms = cx.timed(lambda: cx.runner(None, run)(), reps, 1)
+        out[f"m{m}"] = {"us_per_layer": round(ms * 1e3, 1), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1)}
+    return {"workload": "one Llama-3.1-8B layer (qkv, o, gate_up, down) W4 g128 through the drop-in gemm_fused "
+                        "(f32 activations, kernel_interleaved(16,4) codes, bit-identical to the reference)",
+            "weight_bytes_per_layer": nbytes, **out}
+
+
 def run_gpu(args):
     import numpy as np
 
@@ -414,6 +448,7 @@ def run_gpu(args):
         _trace("second bit width done")
         if world == 1:
             line["quantize"] = {f"w{b}": quantize_record(cx, b) for b in (4, 8)}
+            line["dropin_exact"] = exact_record(cx)
         # configs[3]: Llama-3.1-70B, 80 layers, W4 + layer-0 down_proj W8, at TP = world
         t70, p70 = rq.plan.resolve("explicit:0 modules:4", tp.LLAMA_70B.layers)
         m70 = measure(cx, tp.LLAMA_70B, t70, 1, tp.LLAMA_70B.layers, False, [1, 4, 16], sub_steps, warmup,

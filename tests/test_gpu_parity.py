@@ -507,3 +507,22 @@ def test_405b_ffn_up_full_shape(bits):
     del q, wd, y
     torch.cuda.empty_cache()
     assert (num / den) ** 0.5 < 1e-5
+
+
+@pytest.mark.parametrize("bits,n,k,g,m", [(4, 40, 14336, 128, 3), (8, 24, 4096, 64, 5), (4, 16, 1001, 16, 1),
+                                          (8, 33, 520, 8, 2)])
+def test_dropin_gemm_fused_group_parallel_bit_exact(oracle, bits, n, k, g, m):
+    """The drop-in gemm_fused on the reference's kernel layout runs the group-parallel exact
+    kernel (one lane per group, block sums folded in group order) for <= 128 groups per row and
+    the one-thread-per-output kernel beyond: both bit-identical to the C oracle (gemm.cpp:46-92),
+    incl. ragged groups, odd row counts and 1..5 tokens."""
+    ragged = k % g != 0
+    rng = np.random.default_rng(n * k + m)
+    w = (rng.standard_normal((n, k)) * 0.05).astype(np.float32)
+    data, scales = rq.quantize_tensor(w, bits, g, ragged)
+    klay = rq.layout(rq.KERNEL_INTERLEAVED)
+    kern = rq.reshuffle(data, rq.layout(), klay, bits, n, k)
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    got = rq.gemm_fused(a, kern, klay, bits, n, g, scales, ragged)
+    want = oracle.gemm_fused(a, kern, n, bits, g, scales)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
