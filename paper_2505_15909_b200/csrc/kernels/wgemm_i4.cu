@@ -601,8 +601,25 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
                     const int j = bi * GL + g;
                     if (j >= n) break;
                     const uint32_t(&dd)[SPLIT ? 3 : 1][LDC] = d[bi % NB][g];
+                    // two tokens per packed FP32 FMA pair (__ffma2_rn: the same two roundings as
+                    // scalar FMAs; measured -1 to -3 % per launch: the epilogue is issue-bound)
+                    auto plane = [&](int p3, int e) -> uint32_t {
+                        if constexpr (SPLIT) return dd[p3][e];
+                        else return dd[0][(p3 * PT + e) % LDC];
+                    };
+                    const float2 c14 = make_float2(6.103515625e-05f, 6.103515625e-05f);
+                    const float2 sg = make_float2(scg[j], scg[j]);
 #pragma unroll
-                    for (int e = 0; e < CH; ++e) {  // 2^s per token is applied at the segment end
+                    for (int e = 0; e + 1 < CH; e += 2) {
+                        const float2 x0 = make_float2(float(int32_t(plane(0, e))), float(int32_t(plane(0, e + 1))));
+                        const float2 x12 = make_float2(float(int32_t(plane(1, e)) * 128 + int32_t(plane(2, e))),
+                                                       float(int32_t(plane(1, e + 1)) * 128 + int32_t(plane(2, e + 1))));
+                        const float2 r = __ffma2_rn(__ffma2_rn(x12, c14, x0), sg, make_float2(acc[jj + e], acc[jj + e + 1]));
+                        acc[jj + e] = r.x, acc[jj + e + 1] = r.y;
+                    }
+                    if constexpr ((CH & 1) == 0) continue;
+#pragma unroll
+                    for (int e = CH & ~1; e < CH; ++e) {  // odd tail; 2^s per token at the segment end
                         uint32_t u0v, u1v, u2v;
                         if constexpr (SPLIT) {
                             u0v = dd[0][e], u1v = dd[SPLIT ? 1 : 0][e], u2v = dd[SPLIT ? 2 : 0][e];
