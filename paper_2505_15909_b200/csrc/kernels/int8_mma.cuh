@@ -236,7 +236,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 //   s = exponent(max|a|) - 6 so |a| / 2^s < 64; three exact int8 planes.
 // 16-byte loads of 8 activations; up to kVPT vectors per thread stay in registers between
 // the max and the split (one pass over memory for K <= 512 * 8 * kVPT), longer rows reload.
-constexpr int kPlaneThreads = 256, kSliceV = 2 * kPlaneThreads;  // 16-byte vectors per CTA slice
+#ifndef RTNQ_PLANES_SLICE_V
+#define RTNQ_PLANES_SLICE_V 512
+#endif
+constexpr int kPlaneThreads = 256, kSliceV = RTNQ_PLANES_SLICE_V;  // 16-byte vectors per CTA slice
 
 // While the activations are split, pull the head of every GEMM CTA's weight range into L2
 // (cp.async.bulk.prefetch.L2): the GEMM that follows then finds its first stages on chip
