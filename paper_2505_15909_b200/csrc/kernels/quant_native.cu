@@ -179,6 +179,12 @@ static_assert(128 % (256 / kI4Lpr * kI4Pass) == 0, "a CTA covers a whole divisor
 // rows >= `rows` (inside the last 128-row tile) only get their zero padding written.
 // Lane j of a row holds codes p..p+7 and p+64..p+71 (p = 8j): exactly the 8 NATIVE_I4 bytes
 // p..p+7 of the row (high nibble code p+i, low nibble code p+64+i).
+#ifdef RTNQ_QI4_COUNT
+__device__ unsigned long long g_qi4_count[4];  // warp passes, passes with a near-tie, near-tie lanes
+extern "C" int rtnq_qi4_count_read(void* host) {
+    return cudaMemcpyFromSymbol(host, g_qi4_count, sizeof(g_qi4_count)) == cudaSuccess ? 0 : 1;
+}
+#endif
 template <int DT>
 __global__ void __launch_bounds__(kI4Threads, RTNQ_QI4_MINB)
 quant_i4_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uint8_t* __restrict__ ni4,
@@ -240,10 +246,21 @@ quant_i4_kernel(const void* __restrict__ w, int64_t rows, int64_t cols, uint8_t*
         float dm = 0.0f;
 #pragma unroll
         for (int v = 0; v < V; ++v) dm = codes_fast8<4>(hi[s][v], qs.inv, qh[v], codes_fast8<4>(lo[s][v], qs.inv, ql[v], dm));
-        // a warp holding any near-tie (common for bf16 weights: an absmax whose mantissa is a
-        // multiple of 5 puts exact half-integers on the bf16 grid; measured ~25 % of the W4
-        // pass time), a non-finite weight or a tiny scale redoes its weights exactly.  (Redoing
-        // only the near-tie weights, one exact test per weight index, measured slower: code size.)
+        // a warp holding any near-tie, a non-finite weight or a tiny scale redoes its weights
+        // exactly.  Near-ties are common for bf16 weights: an absmax mantissa of 1.25, 1.5, ...
+        // puts v / S within 2^-23 of half-integers (S = RU(absmax / 7.5)), ~2e-3 of the weights
+        // and 57 % of the warp passes of random bf16 weights (scratch/qi4_count.py, build with
+        // -DRTNQ_QI4_COUNT); the exact redo costs ~25 % of the kernel.  Measured slower: redoing
+        // only the flagged weights (code size), a one-sided midpoint test on flagged passes or on
+        // every weight (register spills / per-weight integer work), a non-inlined exact path.
+#ifdef RTNQ_QI4_COUNT
+        if (lane == 0) atomicAdd(&g_qi4_count[0], 1ull);
+        {
+            const unsigned tie = __ballot_sync(0xffffffffu, !(dm < FastQ<4>::kThr));
+            if (lane == 0 && tie) atomicAdd(&g_qi4_count[1], 1ull);
+            if (lane == 0) atomicAdd(&g_qi4_count[2], static_cast<unsigned long long>(__popc(tie)));
+        }
+#endif
         if (__any_sync(0xffffffffu, !(dm < FastQ<4>::kThr) || nonfinite || qs.pre != 1.0f)) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
