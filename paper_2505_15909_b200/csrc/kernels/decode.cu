@@ -664,7 +664,6 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
                                             float* __restrict__ part, int hq, int hkv, int lmax,
                                             int pos, float theta, __nv_bfloat16* __restrict__ out,
                                             int* __restrict__ arrivals, int cluster_merge, int chunk) {
-    pdl_prologue();
     constexpr int kQS = kD + 8;                     // bf16 per A-tile row of the queries (padded)
     const int chunkp = (chunk + 15) / 16 * 16, kPS = chunkp + 8;
     extern __shared__ uint4 smq[];
@@ -684,6 +683,22 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
     __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     const int t0 = sp * chunk, n = min(chunk, pos + 1 - t0);
+    // the cached rows (every position but pos, written by earlier steps) first: their DRAM
+    // latency overlaps the RoPE table, the query rotation and the append below
+    for (int i = threadIdx.x; i < n * 16; i += nthr) {
+        const int t = i >> 4, c = i & 15;
+        if (t0 + t == pos) continue;
+        const uint32_t kd = static_cast<uint32_t>(__cvta_generic_to_shared(ks + swz(t, c)));
+        const uint32_t vd = static_cast<uint32_t>(__cvta_generic_to_shared(vs + swz(t, c)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(kd), "l"(kcb + int64_t(t0 + t) * cstride + c * 8)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vd), "l"(vcb + int64_t(t0 + t) * cstride + c * 8)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // only now the dependency on the previous kernel (the qkv linear): with programmatic
+    // dependent launch the cached rows above stream in under its tail
+    pdl_prologue();
     __shared__ float2 cs_s[kD / 2];
     if (threadIdx.x < kD / 2) {
         const float inv = powf(theta, -2.0f * float(threadIdx.x) / float(kD));
@@ -697,20 +712,30 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
         const int r = i / (kQS / 2);
         if ((r & 7) >= G) reinterpret_cast<uint32_t*>(qa)[i] = 0u;
     }
+    for (int i = n * 16 + threadIdx.x; i < chunkp * 16; i += nthr)  // rows past n: finite zeros
+        ks[swz(i >> 4, i & 15)] = vs[swz(i >> 4, i & 15)] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     auto rot = [&](float a, float bb, int d) {
         const float2 c = cs_s[d];
         return make_float2(a * c.x - bb * c.y, bb * c.x + a * c.y);
     };
-    if (sp == nsp - 1 && warp == 0) {  // append the rotated key and the value at pos
+    if (sp == nsp - 1 && warp == 0) {  // append the rotated key and the value at pos (cache + tile)
+        const int tp = pos - t0;
+        __nv_bfloat16* ksh = reinterpret_cast<__nv_bfloat16*>(ks);
+        __nv_bfloat16* vsh = reinterpret_cast<__nv_bfloat16*>(vs);
+        auto sidx = [&](int d) { return int(swz(tp, d >> 3)) * 8 + (d & 7); };
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             const int d = lane + 32 * h2;
             const float2 r = rot(__bfloat162float(kn[d]), __bfloat162float(kn[d + kD / 2]), d);
-            kcb[int64_t(pos) * cstride + d] = __float2bfloat16_rn(r.x);
-            kcb[int64_t(pos) * cstride + d + kD / 2] = __float2bfloat16_rn(r.y);
-            vcb[int64_t(pos) * cstride + d] = vn[d];
-            vcb[int64_t(pos) * cstride + d + kD / 2] = vn[d + kD / 2];
+            const __nv_bfloat16 k0 = __float2bfloat16_rn(r.x), k1 = __float2bfloat16_rn(r.y);
+            const __nv_bfloat16 v0 = vn[d], v1 = vn[d + kD / 2];
+            kcb[int64_t(pos) * cstride + d] = k0;
+            kcb[int64_t(pos) * cstride + d + kD / 2] = k1;
+            vcb[int64_t(pos) * cstride + d] = v0;
+            vcb[int64_t(pos) * cstride + d + kD / 2] = v1;
+            ksh[sidx(d)] = k0, ksh[sidx(d + kD / 2)] = k1;
+            vsh[sidx(d)] = v0, vsh[sidx(d + kD / 2)] = v1;
         }
     }
     {  // rotated, pre-scaled query of head `warp`, as bf16 hi (row warp) + lo (row 8 + warp)
@@ -728,20 +753,7 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
             qa[(8 + warp) * kQS + d + kD / 2] = __float2bfloat16_rn(q1 - __bfloat162float(h1));
         }
     }
-    __threadfence_block();
-    __syncthreads();  // the appended row is written before the staging copies below read it
-    for (int i = threadIdx.x; i < n * 16; i += nthr) {
-        const int t = i >> 4, c = i & 15;
-        const uint32_t kd = static_cast<uint32_t>(__cvta_generic_to_shared(ks + swz(t, c)));
-        const uint32_t vd = static_cast<uint32_t>(__cvta_generic_to_shared(vs + swz(t, c)));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(kd), "l"(kcb + int64_t(t0 + t) * cstride + c * 8)
-                     : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vd), "l"(vcb + int64_t(t0 + t) * cstride + c * 8)
-                     : "memory");
-    }
-    for (int i = n * 16 + threadIdx.x; i < chunkp * 16; i += nthr)  // rows past n: finite zeros
-        ks[swz(i >> 4, i & 15)] = vs[swz(i >> 4, i & 15)] = make_uint4(0, 0, 0, 0);
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // S = Q K^T: warp w takes the 8-position tiles w, w + W, ...
     {
@@ -977,13 +989,28 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     cfg.blockDim = dim3(unsigned(32 * G));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 1;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = unsigned(nsp);
-    cfg.attrs = &attr;
-    cfg.numAttrs = cluster ? 1 : 0;
+    // programmatic dependent launch for the tensor-core kernel: its cached-row loads run before
+    // its griddepcontrol.wait (RTNQ_ATTN_PDL=0: stream-ordered)
+    static const bool attn_pdl = [] {
+        const char* e = std::getenv("RTNQ_ATTN_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    cudaLaunchAttribute attrs[2];
+    int na = 0;
+    if (cluster) {
+        attrs[na].id = cudaLaunchAttributeClusterDimension;
+        attrs[na].val.clusterDim.x = 1;
+        attrs[na].val.clusterDim.y = 1;
+        attrs[na].val.clusterDim.z = unsigned(nsp);
+        ++na;
+    }
+    if (mma && attn_pdl) {
+        attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, mma ? decode_attention_mma_kernel : decode_attention_kernel,
                               static_cast<const __nv_bfloat16*>(qkv),
                               static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
