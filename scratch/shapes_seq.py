@@ -8,7 +8,7 @@ st = torch.cuda.Stream()
 ws = rq.Workspace(device="cuda")
 res = []
 for name, n, k in [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]:
-    g = 128 if BITS == 4 else 1 << (k - 1).bit_length()
+    g = 128 if BITS == 4 or os.environ.get("W8G128") else 1 << (k - 1).bit_length()
     NAT = os.environ.get("NATIVE") == "1" or None
     qs = [rq.quantize_pack(((torch.rand(n, k, device="cuda") * 2 - 1) * 0.02).to(torch.bfloat16), BITS, g, k % g != 0, native=NAT) for _ in range(4)]
     x = torch.empty(B, k, device="cuda").uniform_(-1, 1).to(torch.bfloat16)
