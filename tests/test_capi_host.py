@@ -146,3 +146,31 @@ def test_int8_mma_layouts_match_numpy_restatement(bits, rows, cols):
             b = int(e[idx >> 1])
             v = (((b >> 4) if idx & 1 else (b & 15)) ^ 8) - 8
         assert v == int(codes[r, c]), (r, c)
+
+
+def test_peer_abi_validates_before_touching_a_device():
+    """The tensor-parallel peer C-ABI: buffer sizing, and argument errors reported
+    as statuses before any CUDA call (so they hold without a GPU)."""
+    import ctypes as C
+    L = rq.lib()
+    # header 256 B + [2 parities][8 ranks][cap] bf16 slots
+    assert L.rtnq_peer_buffer_bytes(8) == 256 + 2 * 8 * 8 * 2
+    assert L.rtnq_peer_buffer_bytes(4096 * 16) == 256 + 2 * 8 * 4096 * 16 * 2
+    assert L.rtnq_peer_buffer_bytes(-1) == 0
+    bufs = (C.c_void_p * 2)(None, None)
+    lay = rq.layout(rq.NATIVE_I4)
+    # null peer buffer -> InvalidInputError
+    st = L.rtnq_dev_linear_peer(C.c_void_p(16), None, None, 4, 128, C.c_void_p(16), lay, 4, 128, 128, 0,
+                                C.c_void_p(16), rq.F16, rq.SCALES_NATIVE, bufs, 2, 0, 4096, None, None, 0,
+                                None, 0)
+    assert st == 1 and b"peer" in L.rtnq_last_error()
+    # both activations and planes given -> InvalidInputError
+    st = L.rtnq_dev_linear_peer(C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), 4, 128, C.c_void_p(16), lay, 4,
+                                128, 128, 0, C.c_void_p(16), rq.F16, rq.SCALES_NATIVE, bufs, 2, 0, 4096, None,
+                                None, 0, None, 0)
+    assert st == 1
+    # world outside 1..8, capacity not a multiple of 8
+    assert L.rtnq_dev_peer_reduce(C.c_void_p(256), 9, 4096, C.c_void_p(16), 8, 0, None) == 1
+    assert L.rtnq_dev_peer_reduce(C.c_void_p(256), 2, 4097, C.c_void_p(16), 8, 0, None) == 1
+    assert L.rtnq_dev_add_rmsnorm_peer(C.c_void_p(16), C.c_void_p(256), 2, 4096, C.c_void_p(16), C.c_void_p(16),
+                                       2, 100, 1e-5, None, None, None) == 2  # h % 16 != 0: ShapeError
