@@ -233,6 +233,13 @@ rtnq_status rtnq_dev_decode_attention_ws(const void* qkv, void* k_cache, void* v
                                          int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                          int64_t max_len, int64_t pos, float rope_theta, void* ws,
                                          size_t ws_bytes, void* stream);
+/* The same, also writing the activation planes ([3][batch][hq * head_dim] int8, [batch] exponents)
+ * of `out` for the int8 o-projection (rtnq_dev_linear_planes): the last CTA of each token computes
+ * them from the token's output row, so the o-projection needs no planes kernel. */
+rtnq_status rtnq_dev_decode_attention_planes(const void* qkv, void* k_cache, void* v_cache, void* out,
+                                             int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                             int64_t max_len, int64_t pos, float rope_theta, int8_t* planes,
+                                             int32_t* texp, void* ws, size_t ws_bytes, void* stream);
 /* Synchronizes `stream`, reads and clears *err_flag (device), returns
  * RTNQ_E_INVALID_INPUT if it was set. */
 rtnq_status rtnq_dev_check_flag(int32_t* err_flag, void* stream);

@@ -116,6 +116,8 @@ def lib():
     L.rtnq_dev_decode_attention_workspace_bytes.argtypes = [_i64, _i64, _i64, _i64]
     L.rtnq_dev_decode_attention_ws.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
                                                C.c_float, _p, _sz, _p]
+    L.rtnq_dev_decode_attention_planes.argtypes = [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
+                                                   C.c_float, _p, _p, _p, _sz, _p]
     L.rtnq_peer_buffer_bytes.restype = _sz
     L.rtnq_peer_buffer_bytes.argtypes = [_i64]
     L.rtnq_peer_alloc.argtypes = [_i64, C.POINTER(_p)]
@@ -486,17 +488,20 @@ def linear_planes(planes: Planes, qw: QuantWeight, out, *, workspace: Workspace 
 
 
 def decode_attention(qkv, k_cache, v_cache, out, hq, hkv, pos, head_dim=128, theta=500000.0,
-                     stream=None, workspace: Workspace | None = None):
-    """GQA decode attention with RoPE over a KV cache (rtnq_dev_decode_attention_ws).  The split
-    merge scratch comes from ``workspace`` (one per stream; the default per (device, stream))."""
+                     stream=None, workspace: Workspace | None = None, planes: Planes | None = None):
+    """GQA decode attention with RoPE over a KV cache (rtnq_dev_decode_attention_planes).  The
+    split-merge scratch comes from ``workspace`` (one per stream; the default per (device,
+    stream)).  With ``planes`` the kernel also writes the activation planes of ``out`` for the
+    int8 o-projection (linear_planes)."""
     batch, max_len = k_cache.shape[0], k_cache.shape[1]
     wsb = lib().rtnq_dev_decode_attention_workspace_bytes(batch, hq, hkv, max_len)
     if workspace is None:
         workspace = _default_workspace(qkv.device, stream, wsb, kind="attention")
     buf = workspace.ensure(wsb)
-    _check(lib().rtnq_dev_decode_attention_ws(_ptr(qkv), _ptr(k_cache), _ptr(v_cache), _ptr(out),
-                                              batch, hq, hkv, head_dim, max_len, pos, theta,
-                                              _ptr(buf), buf.numel(), _stream(stream)))
+    _check(lib().rtnq_dev_decode_attention_planes(
+        _ptr(qkv), _ptr(k_cache), _ptr(v_cache), _ptr(out), batch, hq, hkv, head_dim, max_len, pos, theta,
+        None if planes is None else _ptr(planes.planes), None if planes is None else _ptr(planes.texp),
+        _ptr(buf), buf.numel(), _stream(stream)))
     return out
 
 

@@ -700,15 +700,24 @@ rtnq_status rtnq_dev_decode_attention_ws(const void* qkv, void* k_cache, void* v
                                          int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                          int64_t max_len, int64_t pos, float rope_theta, void* ws,
                                          size_t ws_bytes, void* stream) {
+    return rtnq_dev_decode_attention_planes(qkv, k_cache, v_cache, out, batch, hq, hkv, head_dim, max_len, pos,
+                                            rope_theta, nullptr, nullptr, ws, ws_bytes, stream);
+}
+
+rtnq_status rtnq_dev_decode_attention_planes(const void* qkv, void* k_cache, void* v_cache, void* out,
+                                             int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
+                                             int64_t max_len, int64_t pos, float rope_theta, int8_t* planes,
+                                             int32_t* texp, void* ws, size_t ws_bytes, void* stream) {
     if (head_dim != 128) return fail(RTNQ_E_UNSUPPORTED, "decode attention needs head_dim 128");
     if (hkv <= 0 || hq % hkv || hq / hkv > 32)
         return fail(RTNQ_E_SHAPE, "query heads must be a multiple (<= 32x) of kv heads");
     if (pos < 0 || pos >= max_len) return fail(RTNQ_E_INVALID_INPUT, "position outside the cache");
+    if (!planes != !texp) return fail(RTNQ_E_INVALID_INPUT, "planes and texp go together");
     if (ws && ws_bytes < decode_attention_workspace_bytes(batch, hq, hkv, pos + 1))
         return fail(RTNQ_E_INVALID_INPUT, "decode attention workspace too small");
     if (batch == 0) return RTNQ_OK;
     RTNQ_CUDA(launch_decode_attention(qkv, k_cache, v_cache, out, batch, hq, hkv, head_dim, max_len, pos,
-                                      rope_theta, static_cast<cudaStream_t>(stream), ws, ws_bytes));
+                                      rope_theta, static_cast<cudaStream_t>(stream), ws, ws_bytes, planes, texp));
     return RTNQ_OK;
 }
 

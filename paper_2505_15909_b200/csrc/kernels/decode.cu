@@ -408,7 +408,7 @@ __device__ __forceinline__ uint32_t swz(int t, int c) { return uint32_t(t * 16 +
 // The end of a split CTA, per warp = query head qh (lane: head dims 4 lane .. 4 lane + 3): its
 // (max, sum, unnormalised P.V) partial -> the output (one split), or the DSMEM merge inside the
 // cluster (scratch: kPart floats per warp of idle shared memory), or the last-CTA global merge.
-__device__ __forceinline__ void attn_finish(float cmax, float csum, float4 a4, float* scratch, float* __restrict__ part,
+__device__ __forceinline__ bool attn_finish(float cmax, float csum, float4 a4, float* scratch, float* __restrict__ part,
                                             int* __restrict__ arrivals, __nv_bfloat16* __restrict__ out, int b,
                                             int kvh, int qh, int hq, int hkv, int sp, int nsp, int cluster_merge) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,7 +418,7 @@ __device__ __forceinline__ void attn_finish(float cmax, float csum, float4 a4, f
         __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
         *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(o[0], o[1]);
         *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(o[2], o[3]);
-        return;
+        return true;
     }
     if (cluster_merge) {
         // the splits of this (token, KV head) are one thread-block cluster: partials stay in
@@ -462,7 +462,7 @@ __device__ __forceinline__ void attn_finish(float cmax, float csum, float4 a4, f
         }
         // peers keep their shared memory alive until rank 0 has read it
         asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        return;
+        return sp == 0;
     }
     // partial: [b][qh][split] -> {max, sum, acc[kD]}
     float* pr = part + ((int64_t(b) * hq + qh) * nsp + sp) * kPart;
@@ -479,7 +479,7 @@ __device__ __forceinline__ void attn_finish(float cmax, float csum, float4 a4, f
         if (last) arrivals[b * hkv + kvh] = 0;
     }
     __syncthreads();
-    if (!last) return;
+    if (!last) return false;
     __threadfence();
     const float* ph = part + (int64_t(b) * hq + qh) * nsp * kPart;
     float M = -INFINITY;
@@ -495,13 +495,42 @@ __device__ __forceinline__ void attn_finish(float cmax, float csum, float4 a4, f
     __nv_bfloat16* op = out + (int64_t(b) * hq + qh) * kD + 4 * lane;
     *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
     *reinterpret_cast<__nv_bfloat162*>(op + 2) = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+    return true;
+}
+
+// The o-projection's activation planes from the attention output, in the attention kernel: the
+// CTA that wrote the last of a token's hkv head groups (a self-resetting per-token counter)
+// computes the token's planes from its whole output row (token_planes: the planes kernel's
+// arithmetic), so the o-projection needs no planes kernel of its own.
+__device__ __forceinline__ void attn_token_planes(bool wrote, const __nv_bfloat16* __restrict__ out, int b, int hq,
+                                                  int hkv, int batch, int* __restrict__ tok_arrivals,
+                                                  int8_t* __restrict__ planes, int32_t* __restrict__ texp) {
+    __shared__ int tlast;
+    __shared__ float red[32];
+    if (wrote) __threadfence();  // every writing thread: its rows visible device-wide first
+    __syncthreads();             // every warp wrote its head rows
+    if (threadIdx.x == 0) {
+        tlast = 0;
+        if (wrote) {
+            const int prev = atomicAdd(tok_arrivals + b, 1);
+            tlast = prev == hkv - 1;
+            if (tlast) tok_arrivals[b] = 0;
+        }
+    }
+    __syncthreads();
+    if (!tlast) return;
+    __threadfence();
+    imma::token_planes<RTNQ_BF16>(reinterpret_cast<const uint16_t*>(out) + int64_t(b) * hq * kD, hq * kD, b, batch,
+                                  planes, texp, nullptr, int(threadIdx.x), int(blockDim.x), 1, red);
 }
 
 __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                         __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                         float* __restrict__ part, int hq, int hkv, int lmax,
                                         int pos, float theta, __nv_bfloat16* __restrict__ out,
-                                        int* __restrict__ arrivals, int cluster_merge, int chunk) {
+                                        int* __restrict__ arrivals, int cluster_merge, int chunk,
+                                        int8_t* __restrict__ planes, int32_t* __restrict__ texp,
+                                        int* __restrict__ tok_arrivals) {
     // grid (hkv, batch, split): this CTA covers positions [t0, t0 + n) of one KV head and its
     // G query heads (a warp each) and writes the split's (max, sum, unnormalised P.V) partial
     pdl_prologue();
@@ -639,10 +668,12 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
         acc[0][2] = fmaf(pt, v.z, acc[0][2]);
         acc[0][3] = fmaf(pt, v.w, acc[0][3]);
     }
-    attn_finish(cmax, csum,
-                make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
-                            acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]),
-                reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh, qh, hq, hkv, sp, nsp, cluster_merge);
+    const bool wrote = attn_finish(
+        cmax, csum,
+        make_float4(acc[0][0] + acc[1][0] + acc[2][0] + acc[3][0], acc[0][1] + acc[1][1] + acc[2][1] + acc[3][1],
+                    acc[0][2] + acc[1][2] + acc[2][2] + acc[3][2], acc[0][3] + acc[1][3] + acc[2][3] + acc[3][3]),
+        reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh, qh, hq, hkv, sp, nsp, cluster_merge);
+    if (planes) attn_token_planes(wrote, out, b, hq, hkv, int(gridDim.y), tok_arrivals, planes, texp);
 }
 
 // Tensor-core variant (G <= 8 query heads per KV head): Q K^T and P V on mma.sync m16n8k16
@@ -663,7 +694,9 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
                                             __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                             float* __restrict__ part, int hq, int hkv, int lmax,
                                             int pos, float theta, __nv_bfloat16* __restrict__ out,
-                                            int* __restrict__ arrivals, int cluster_merge, int chunk) {
+                                            int* __restrict__ arrivals, int cluster_merge, int chunk,
+                                            int8_t* __restrict__ planes, int32_t* __restrict__ texp,
+                                            int* __restrict__ tok_arrivals) {
     constexpr int kQS = kD + 8;                     // bf16 per A-tile row of the queries (padded)
     const int chunkp = (chunk + 15) / 16 * 16, kPS = chunkp + 8;
     extern __shared__ uint4 smq[];
@@ -825,8 +858,9 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
     }
     __syncthreads();
     const float4 a4 = *reinterpret_cast<const float4*>(fin + warp * kPart + 4 + 4 * lane);
-    attn_finish(cmax, csum, a4, reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh, kvh * G + warp, hq, hkv,
-                sp, nsp, cluster_merge);
+    const bool wrote = attn_finish(cmax, csum, a4, reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh,
+                                   kvh * G + warp, hq, hkv, sp, nsp, cluster_merge);
+    if (planes) attn_token_planes(wrote, out, b, hq, hkv, int(gridDim.y), tok_arrivals, planes, texp);
 }
 
 template <typename... KArgs, typename... Args>
@@ -915,17 +949,23 @@ static void attention_split(int64_t batch, int64_t hkv, int64_t pos, int* nsp_ou
     *chunk_out = int(chunk);
 }
 
+// Workspace: [self-resetting counters: a fixed 64 KiB][partials].  The counters (split merges
+// [batch][hkv], then the o-planes tokens [batch]) sit at the same offsets whatever the call's
+// batch, so calls of different batch sizes can share one workspace: a batch-dependent offset of
+// the partials once put one call's partials over another call's counters.
+constexpr size_t kAttnCounterBytes = 64 * 1024;
 size_t decode_attention_workspace_bytes(int64_t batch, int64_t hq, int64_t hkv, int64_t max_len) {
     int nsp, chunk;
     attention_split(batch, hkv, max_len - 1, &nsp, &chunk);  // the largest context of this cache
-    return 256 + size_t(batch * hkv) * sizeof(int) + size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float) + 256;
+    return kAttnCounterBytes + size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float) + 256;
 }
 
 cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
                                     int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                     int64_t lmax, int64_t pos, float theta, cudaStream_t st,
-                                    void* ws, size_t ws_bytes) {
-    if (head_dim != kD || hkv <= 0 || hq % hkv || hq / hkv > 32 || pos < 0 || pos >= lmax)
+                                    void* ws, size_t ws_bytes, int8_t* planes, int32_t* texp) {
+    if (head_dim != kD || hkv <= 0 || hq % hkv || hq / hkv > 32 || pos < 0 || pos >= lmax ||
+        size_t(batch * hkv + batch) * sizeof(int) > kAttnCounterBytes)
         return cudaErrorInvalidValue;
     const int G = int(hq / hkv);
     int nsp, chunk;
@@ -955,7 +995,7 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     if (ws) {
         if (ws_bytes < decode_attention_workspace_bytes(batch, hq, hkv, pos + 1)) return cudaErrorInvalidValue;
         arrivals = static_cast<int*>(ws);
-        part = reinterpret_cast<float*>(static_cast<char*>(ws) + (256 + size_t(batch * hkv) * sizeof(int) + 255) / 256 * 256);
+        part = reinterpret_cast<float*>(static_cast<char*>(ws) + kAttnCounterBytes);
     } else {
         static std::mutex mu;
         std::lock_guard<std::mutex> lock(mu);
@@ -967,8 +1007,8 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
         size_t& pb = part_bytes_dev[current_device_index()];
         int*& ad = arrivals_dev[current_device_index()];
         size_t& an = arrivals_n_dev[current_device_index()];
-        if (size_t(batch * hkv) > an) {  // zeroed on this stream; an older buffer stays valid for graphs
-            const size_t want = size_t(batch * hkv) * 2;
+        if (size_t(batch * hkv + batch) > an) {  // zeroed on this stream; an older buffer stays valid for graphs
+            const size_t want = size_t(batch * hkv + batch) * 2;
             int* fresh = nullptr;
             if (cudaError_t e = cudaMalloc(&fresh, want * sizeof(int))) return e;
             if (cudaError_t e = cudaMemsetAsync(fresh, 0, want * sizeof(int), st)) return e;
@@ -1015,7 +1055,7 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
                               static_cast<const __nv_bfloat16*>(qkv),
                               static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
                               int(hq), int(hkv), int(lmax), int(pos), theta, static_cast<__nv_bfloat16*>(out),
-                              arrivals, cluster, chunk);
+                              arrivals, cluster, chunk, planes, texp, arrivals + batch * hkv);
 }
 
 }  // namespace rtnq_b200

@@ -136,6 +136,7 @@ size_t decode_attention_workspace_bytes(int64_t batch, int64_t hq, int64_t hkv, 
 cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache, void* out,
                                     int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                     int64_t lmax, int64_t pos, float theta, cudaStream_t st,
-                                    void* ws = nullptr, size_t ws_bytes = 0);
+                                    void* ws = nullptr, size_t ws_bytes = 0, int8_t* planes = nullptr,
+                                    int32_t* texp = nullptr);
 
 }  // namespace rtnq_b200

@@ -28,6 +28,7 @@ stack need CUDA (and librtnq_b200.so) -- there is no CPU fallback.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -248,6 +249,13 @@ class TPDecodeLayer:
         # SiLU*up emits the down projection's planes too (a cluster of CTAs per token row)
         self.pa = rq.Planes(batch, self.dims.ffn, dev) if fuse_planes and self.q["ffn_down"].layout in imma \
             else None
+        # the o-projection's planes: the stand-alone planes kernel (PDL-overlapped).  The attention
+        # can emit them itself (decode_attention(planes=...), its last CTA per token); measured
+        # 1.3 us per layer slower at batch 16 (one CTA per token computes a 4096-wide row in the
+        # attention's tail), so it is opt-in: RTNQ_ATTN_PLANES=1
+        self.pat = rq.Planes(batch, self.dims.attn_cols, dev) \
+            if fuse_planes and self.q["attn_out_proj"].layout in imma and os.environ.get("RTNQ_ATTN_PLANES") == "1" \
+            else None
         # non-finite activations (InvalidInputError, gemm.cpp:13-19) are flagged asynchronously
         # by the int8 kernels' planes pass; the stack checks the flag after a step
         self.err = None
@@ -294,11 +302,10 @@ class TPDecodeLayer:
         self._linear("qkv_proj", self.y, self.py, self.qkv, ws, stream, pdl)
         rq.decode_attention(self.qkv, self.k_cache, self.v_cache, self.attn, self.dims.hq,
                             self.dims.hkv, self.pos, s.head_dim, s.rope_theta, stream=stream,
-                            workspace=self.attn_ws)
+                            workspace=self.attn_ws, planes=self.pat)
         if peer is not None:
-            return self._row_split("attn_out_proj", self.attn, None, self.o, ws, stream, pdl, peer)
-        rq.linear(self.attn, self.q["attn_out_proj"], out=self.o, workspace=ws, stream=stream,
-                  pdl=pdl, err=self.err, check=False)
+            return self._row_split("attn_out_proj", self.attn, self.pat, self.o, ws, stream, pdl, peer)
+        self._linear("attn_out_proj", self.attn, self.pat, self.o, ws, stream, pdl)
         return self.o
 
     def mlp_half(self, x, o_sum, ws, stream=None, pdl=False, peer=None):

@@ -221,3 +221,33 @@ def test_default_workspaces_of_attention_and_linear_are_separate():
         rq.decode_attention(qkv, kc, vc, out, hq, hkv, pos)
         y = rq.linear(a, q)  # default workspace, synchronizing check
         assert torch.equal(y, ref)
+
+
+@pytest.mark.parametrize("batch,pos,hq,hkv", [(1, 100, 32, 8), (2, 300, 32, 8), (16, 256, 32, 8), (1, 700, 32, 8),
+                                              (3, 50, 64, 2)])
+def test_decode_attention_emits_o_proj_planes(batch, pos, hq, hkv):
+    """The attention's last CTA per token writes the o-projection's activation planes: bit-identical
+    to the planes kernel on the attention output, on every merge path (one split, cluster DSMEM,
+    global last-CTA) and on the CUDA-core kernel (32 query heads per KV head)."""
+    import os
+    d = 128
+    g = torch.Generator(device="cuda").manual_seed(batch * 7 + pos)
+    qkv = torch.randn(batch, (hq + 2 * hkv) * d, device="cuda", generator=g).to(torch.bfloat16)
+    kc = torch.randn(batch, pos + 1, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(batch, pos + 1, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    for no_cluster in ("", "1"):
+        if no_cluster:
+            os.environ["RTNQ_ATTN_NO_CLUSTER"] = "1"
+        try:
+            o_ref = torch.empty(batch, hq * d, device="cuda", dtype=torch.bfloat16)
+            rq.decode_attention(qkv, kc.clone(), vc.clone(), o_ref, hq, hkv, pos)
+            for rep in range(2):  # the per-token counters reset themselves
+                o = torch.empty_like(o_ref)
+                p = rq.Planes(batch, hq * d)
+                rq.decode_attention(qkv, kc.clone(), vc.clone(), o, hq, hkv, pos, planes=p)
+                ref = rq.act_planes(o, rq.Planes(batch, hq * d))
+                torch.cuda.synchronize()
+                assert torch.equal(o, o_ref)
+                assert torch.equal(p.planes, ref.planes) and torch.equal(p.texp, ref.texp), (no_cluster, rep)
+        finally:
+            os.environ.pop("RTNQ_ATTN_NO_CLUSTER", None)
