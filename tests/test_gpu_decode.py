@@ -251,3 +251,28 @@ def test_decode_attention_emits_o_proj_planes(batch, pos, hq, hkv):
                 assert torch.equal(p.planes, ref.planes) and torch.equal(p.texp, ref.texp), (no_cluster, rep)
         finally:
             os.environ.pop("RTNQ_ATTN_NO_CLUSTER", None)
+
+
+def test_attention_workspace_shared_across_batch_sizes():
+    """One attention workspace for calls of different batch sizes (global-merge path): the
+    self-resetting counters sit in a fixed region, so a smaller call's partials never land on a
+    larger call's counters (a batch-dependent layout once broke the merge silently)."""
+    import os
+    hq, hkv, d = 32, 8, 128
+    ws = rq.Workspace(device="cuda")
+    os.environ["RTNQ_ATTN_NO_CLUSTER"] = "1"
+    try:
+        for batch, pos in ((1, 700), (2, 300), (16, 700), (1, 700), (16, 700)):
+            g = torch.Generator(device="cuda").manual_seed(batch + pos)
+            qkv = torch.randn(batch, (hq + 2 * hkv) * d, device="cuda", generator=g).to(torch.bfloat16)
+            kc = torch.randn(batch, pos + 1, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+            vc = torch.randn(batch, pos + 1, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+            o = torch.empty(batch, hq * d, device="cuda", dtype=torch.bfloat16)
+            o_fresh = torch.empty_like(o)
+            rq.decode_attention(qkv, kc.clone(), vc.clone(), o, hq, hkv, pos, workspace=ws)
+            rq.decode_attention(qkv, kc.clone(), vc.clone(), o_fresh, hq, hkv, pos,
+                                workspace=rq.Workspace(device="cuda"))
+            torch.cuda.synchronize()
+            assert torch.equal(o, o_fresh), (batch, pos)
+    finally:
+        os.environ.pop("RTNQ_ATTN_NO_CLUSTER", None)
