@@ -219,7 +219,12 @@ rtnq_status rtnq_dev_linear_planes(const int8_t* planes, const int32_t* texp, in
                                    unsigned flags);
 /* One decode step of GQA attention: qkv rows [hq*d | hkv*d | hkv*d]; the rotated key and
  * the value are appended to the caches ([batch][max_len][hkv][d]) at `pos`, then each
- * query head attends over positions [0, pos].  head_dim 128, hq/hkv <= 32. */
+ * query head attends over positions [0, pos].  head_dim 128, hq/hkv <= 32.
+ * With <= 8 query heads per KV head the kernel is launched as a programmatic dependent of the
+ * previous kernel on the stream and reads the cached rows [0, pos) BEFORE waiting for it (they
+ * stream in under that kernel's tail): those rows must not be written by the kernel launched
+ * immediately before this call (a decode stack writes them one step earlier).  RTNQ_ATTN_PDL=0
+ * launches it stream-ordered. */
 rtnq_status rtnq_dev_decode_attention(const void* qkv, void* k_cache, void* v_cache, void* out,
                                       int64_t batch, int64_t hq, int64_t hkv, int64_t head_dim,
                                       int64_t max_len, int64_t pos, float rope_theta,
