@@ -535,7 +535,8 @@ template <int AT>
 __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, int K, int t, int M,
                                              int8_t* __restrict__ planes, int32_t* __restrict__ texp,
                                              int32_t* err, int tid, int nthr, int bar, float* red,
-                                             long long* dtl = nullptr, long long dt0 = 0) {
+                                             long long* dtl = nullptr, long long dt0 = 0, int sv0 = 0,
+                                             int sv1 = -1) {
     if (dtl && tid == 0) dtl[0] = clock64() - dt0;
     auto cvt = [](uint32_t h) -> float {
         if constexpr (AT == RTNQ_BF16) return __uint_as_float(h << 16);
@@ -581,7 +582,7 @@ __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, 
     int e = 0;
     if (amax > 0.0f) frexpf(amax, &e);
     const int s = max(e - 6, -126);
-    if (tid == 0) texp[t] = s;
+    if (tid == 0 && sv0 == 0) texp[t] = s;
     const float inv = __int_as_float((127 - s) << 23);
     if (dtl && tid == 0) dtl[2] = clock64() - dt0;
     auto split = [&](const uint4& q, int v) {
@@ -603,29 +604,52 @@ __device__ __forceinline__ void token_planes(const uint16_t* __restrict__ rowp, 
             *reinterpret_cast<uint2*>(planes + (int64_t(pl) * M + t) * K + int64_t(v) * 8) =
                 make_uint2(pk[pl][0], pk[pl][1]);
     };
+    if (sv0 == 0 && (sv1 < 0 || sv1 >= nv)) {  // the whole row
 #pragma unroll
-    for (int h = 0; h < kHold; ++h)
-        if (tid + h * nthr < nv) split(held[h], tid + h * nthr);
-    for (int v = tid + kHold * nthr; v < nv; v += nthr) split(__ldcg(reinterpret_cast<const uint4*>(rowp) + v), v);
+        for (int h = 0; h < kHold; ++h)
+            if (tid + h * nthr < nv) split(held[h], tid + h * nthr);
+        for (int v = tid + kHold * nthr; v < nv; v += nthr) split(__ldcg(reinterpret_cast<const uint4*>(rowp) + v), v);
+    } else {  // this CTA's slice [sv0, sv1) of the row's vectors (the exponent needs the whole row)
+        for (int v = sv0 + tid; v < sv1; v += nthr) split(__ldcg(reinterpret_cast<const uint4*>(rowp) + v), v);
+    }
     if (dtl && tid == 0) dtl[3] = clock64() - dt0;
     // every thread's planes stores are done before the caller publishes the token
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
     if (dtl && tid == 0) dtl[4] = clock64() - dt0;
 }
 
-// Producers: CTA c of G computes tokens m0 + t, t = c, c + G, ... < M, after the activations'
-// producer grid has completed (griddepcontrol.wait), and publishes each one.
+// Units of the launch's planes work: a token row is cut into S slices so that more of the G CTAs
+// take part (each slice CTA reduces the whole row's max -- L2-resident -- and splits only its
+// slice), with at least RTNQ_PLANES_MIN_SLICE_V 8-element vectors per slice: W4 down (K = 14336)
+// at batch 16 / 32 / 64 gets 1.4 / 1.1 / 0.6 us faster, K = 4096 rows stay whole (r2_w4_limiter.md §9).
+#ifndef RTNQ_PLANES_MIN_SLICE_V
+#define RTNQ_PLANES_MIN_SLICE_V 256
+#endif
+__device__ __forceinline__ int own_planes_slices(int M, int G, int K) {
+    int S = G / (M > 0 ? M : 1);
+    S = S < 1 ? 1 : S;
+    const int cap = (K / 8 + RTNQ_PLANES_MIN_SLICE_V - 1) / RTNQ_PLANES_MIN_SLICE_V;
+    return S > cap ? cap : S;
+}
+
+// Producers: CTA c of G computes units u = c, c + G, ... < M * S (token u % M, slice u / M),
+// after the activations' producer grid has completed (griddepcontrol.wait), and publishes each.
 __device__ __forceinline__ void own_planes_produce(const OwnPlanes& op, int K, int m0, int M, int Mtot, int c,
                                                    int G, int8_t* planes, int32_t* texp, int tid, int nthr,
                                                    int bar, float* red, long long* dtl = nullptr,
                                                    long long dt0 = 0) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int t = c; t < M; t += G) {
+    const int S = own_planes_slices(M, G, K), nv = K / 8;
+    for (int u = c; u < M * S; u += G) {
+        const int t = u % M, sl = u / M;
+        const int sv0 = int(int64_t(sl) * nv / S), sv1 = S == 1 ? -1 : int(int64_t(sl + 1) * nv / S);
         const uint16_t* rowp = static_cast<const uint16_t*>(op.a) + int64_t(m0 + t) * K;
         if (op.a_dtype == RTNQ_BF16)
-            token_planes<RTNQ_BF16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red, dtl, dt0);
+            token_planes<RTNQ_BF16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red, dtl, dt0, sv0,
+                                    sv1);
         else
-            token_planes<RTNQ_F16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red);
+            token_planes<RTNQ_F16>(rowp, K, m0 + t, Mtot, planes, texp, op.err, tid, nthr, bar, red, nullptr, 0, sv0,
+                                   sv1);
         if (tid == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");  // the consumers read them by TMA
             asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(op.done) : "memory");
@@ -637,7 +661,8 @@ __device__ __forceinline__ void own_planes_produce(const OwnPlanes& op, int K, i
 // Consumer (one whole warp per CTA): returns once all M tokens of this launch are published.  The
 // last of the G CTAs to get here resets both counters; the next launch on this workspace only
 // touches them after its own griddepcontrol.wait, i.e. after this grid has completed.
-__device__ __forceinline__ void own_planes_acquire(const OwnPlanes& op, int M, int G) {
+__device__ __forceinline__ void own_planes_acquire(const OwnPlanes& op, int M, int G, int K) {
+    const int units = M * own_planes_slices(M, G, K);
     // the previous launch on this workspace must be complete before its counters are read: with
     // PDL (and free SMs) this grid's CTAs can start while it still runs
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -645,7 +670,7 @@ __device__ __forceinline__ void own_planes_acquire(const OwnPlanes& op, int M, i
         int got;
         for (;;) {
             asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(op.done) : "memory");
-            if (got >= M) break;
+            if (got >= units) break;
             __nanosleep(32);
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(Geo<PT, BITS>::THREADS, 1) wgemm_i4_kernel(con
         uint32_t ph = 0;
         if (!codes) {
             if (p.own.a) {  // planes computed by this launch's CTAs
-                own_planes_acquire(p.own, p.M, int(gridDim.x));
+                own_planes_acquire(p.own, p.M, int(gridDim.x), int(p.K));
                 if (lane == 0) mbar_arrive(pready);
             } else {
                 asm volatile("griddepcontrol.wait;" ::: "memory");  // planes kernel / fused producer

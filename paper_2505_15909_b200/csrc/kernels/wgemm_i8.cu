@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgemm_i8_kernel(const __grid_cons
         int64_t pf_next = int64_t(cu.b) * kt + (cu.kb >> 1);
         if (!codes) {
             if (p.own.a) {  // planes computed by this launch's CTAs
-                own_planes_acquire(p.own, p.M, int(gridDim.x));
+                own_planes_acquire(p.own, p.M, int(gridDim.x), int(p.K));
                 if (lane == 0) mbar_arrive(pready);
             } else {
                 asm volatile("griddepcontrol.wait;" ::: "memory");  // planes from the previous kernel
