@@ -680,8 +680,9 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
 // (bf16 x bf16 -> f32).  Queries and probabilities are split into bf16 hi + lo parts stacked in
 // the 16 rows of the A tile (row h: hi part of head h, row 8 + h: lo part), so the products keep
 // ~16 significant bits of q and p; keys and values are bf16 already.  Same staging, splits and
-// merge as decode_attention_kernel; its CUDA-core score and P V loops become ~8 + 16 MMAs per
-// 16 positions per warp.
+// merge as decode_attention_kernel (a split of <= kMaxChunk positions loaded at once); its
+// CUDA-core score and P V loops become ~8 + 16 MMAs per 16 positions per warp.  Longer splits
+// run decode_attention_mma_stream_kernel below.
 __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                          uint32_t b1) {
     asm volatile(
@@ -863,6 +864,238 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
     if (planes) attn_token_planes(wrote, out, b, hq, hkv, int(gridDim.y), tok_arrivals, planes, texp);
 }
 
+// Long contexts: the same arithmetic, but a split streams its positions through two 64-position
+// cp.async stages (the next stage loads while this one is scored) with an online softmax across
+// the stages, so a split can be any length and three CTAs fit an SM (74 KiB of shared memory
+// each).  The one-shot kernel above stays faster for splits of <= kMaxChunk positions (fewer
+// barriers and no padded stage): B16 ctx 256 8.6 vs 10.1 us; the streaming one is 2x faster
+// from ctx 1024 (B16 ctx 4096: 144 -> 73 us, 57 % of HBM on the KV bytes).
+constexpr int kSub = 64;
+
+__global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
+    const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+    float* __restrict__ part, int hq, int hkv, int lmax, int pos, float theta, __nv_bfloat16* __restrict__ out,
+    int* __restrict__ arrivals, int cluster_merge, int chunk, int8_t* __restrict__ planes,
+    int32_t* __restrict__ texp, int* __restrict__ tok_arrivals) {
+    constexpr int kQS = kD + 8;    // bf16 per A-tile row of the queries (padded)
+    constexpr int kPS = kSub + 8;  // bf16 per A-tile row of the probabilities (padded)
+    extern __shared__ uint4 smq[];
+    uint4* ks = smq;                                                           // [2][kSub][16] swizzled
+    uint4* vs = ks + 2 * kSub * 16;                                            // [2][kSub][16]
+    __nv_bfloat16* qa = reinterpret_cast<__nv_bfloat16*>(vs + 2 * kSub * 16);  // [16][kQS] q hi / lo
+    __nv_bfloat16* pa = qa + 16 * kQS;                                         // [16][kPS] p hi / lo
+    float* sc = reinterpret_cast<float*>(pa + 16 * kPS);                       // [8][kSub] scores
+    float* fin = reinterpret_cast<float*>(ks);  // [G][kPart] per-head results, after the last stage
+    __shared__ float alpha_s[8];
+    const int b = blockIdx.y, kvh = blockIdx.x, sp = blockIdx.z, nsp = gridDim.z, G = hq / hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x, W = nthr >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int64_t row = int64_t(b) * (hq + 2 * hkv) * kD;
+    const __nv_bfloat16* kn = qkv + row + int64_t(hq) * kD + int64_t(kvh) * kD;
+    const __nv_bfloat16* vn = kn + int64_t(hkv) * kD;
+    const int64_t cstride = int64_t(hkv) * kD;
+    __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
+    __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
+    const int t0 = sp * chunk, n = min(chunk, pos + 1 - t0), nsub = (n + kSub - 1) / kSub;
+    // sub-chunk s -> stage s & 1 by cp.async: rows past its end zeroed (finite for the MMAs), the
+    // appended row (pos, not in the cache yet) skipped -- warp 0 writes it before that stage's use
+    auto issue = [&](int s) {
+        const int base = t0 + s * kSub, ns = min(kSub, n - s * kSub);
+        uint4* kst = ks + (s & 1) * kSub * 16;
+        uint4* vst = vs + (s & 1) * kSub * 16;
+        for (int i = threadIdx.x; i < kSub * 16; i += nthr) {
+            const int t = i >> 4, c = i & 15;
+            if (t >= ns) {
+                kst[swz(t, c)] = vst[swz(t, c)] = make_uint4(0, 0, 0, 0);
+                continue;
+            }
+            if (base + t == pos) continue;
+            const uint32_t kd = static_cast<uint32_t>(__cvta_generic_to_shared(kst + swz(t, c)));
+            const uint32_t vd = static_cast<uint32_t>(__cvta_generic_to_shared(vst + swz(t, c)));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(kd),
+                         "l"(kcb + int64_t(base + t) * cstride + c * 8)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vd),
+                         "l"(vcb + int64_t(base + t) * cstride + c * 8)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // the first two stages of cached rows (written by earlier steps) before the dependency on the
+    // previous kernel (the qkv linear): with programmatic dependent launch they stream in under
+    // its tail, and their latency overlaps the RoPE table and the query rotation below
+    issue(0);
+    if (nsub > 1) issue(1);
+    pdl_prologue();
+    __shared__ float2 cs_s[kD / 2];
+    if (threadIdx.x < kD / 2) {
+        const float inv = powf(theta, -2.0f * float(threadIdx.x) / float(kD));
+        float sn, cn;
+        sincosf(float(pos) * inv, &sn, &cn);
+        cs_s[threadIdx.x] = make_float2(cn, sn);
+    }
+    // zero the absent heads' query and probability rows
+    for (int i = threadIdx.x; i < 16 * kPS / 2; i += nthr) reinterpret_cast<uint32_t*>(pa)[i] = 0u;
+    for (int i = threadIdx.x; i < 16 * kQS / 2; i += nthr) {
+        const int r = i / (kQS / 2);
+        if ((r & 7) >= G) reinterpret_cast<uint32_t*>(qa)[i] = 0u;
+    }
+    __syncthreads();
+    auto rot = [&](float a, float bb, int d) {
+        const float2 c = cs_s[d];
+        return make_float2(a * c.x - bb * c.y, bb * c.x + a * c.y);
+    };
+    const bool appender = sp == nsp - 1 && warp == 0;
+    __nv_bfloat16 ak[4], av[4];  // the appended row's rotated key / value at dims lane, +32, +64, +96
+    if (appender) {  // append the rotated key and the value at pos to the cache
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int d = lane + 32 * h2;
+            const float2 r = rot(__bfloat162float(kn[d]), __bfloat162float(kn[d + kD / 2]), d);
+            ak[h2] = __float2bfloat16_rn(r.x), ak[2 + h2] = __float2bfloat16_rn(r.y);
+            av[h2] = vn[d], av[2 + h2] = vn[d + kD / 2];
+            kcb[int64_t(pos) * cstride + d] = ak[h2];
+            kcb[int64_t(pos) * cstride + d + kD / 2] = ak[2 + h2];
+            vcb[int64_t(pos) * cstride + d] = av[h2];
+            vcb[int64_t(pos) * cstride + d + kD / 2] = av[2 + h2];
+        }
+    }
+    {  // rotated, pre-scaled query of head `warp`, as bf16 hi (row warp) + lo (row 8 + warp)
+        const __nv_bfloat16* qp = qkv + row + int64_t(kvh * G + warp) * kD;
+        const float scale = rsqrtf(float(kD));
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int d = lane + 32 * h2;
+            const float2 r = rot(__bfloat162float(qp[d]), __bfloat162float(qp[d + kD / 2]), d);
+            const float q0 = r.x * scale, q1 = r.y * scale;
+            const __nv_bfloat16 h0 = __float2bfloat16_rn(q0), h1 = __float2bfloat16_rn(q1);
+            qa[warp * kQS + d] = h0;
+            qa[warp * kQS + d + kD / 2] = h1;
+            qa[(8 + warp) * kQS + d] = __float2bfloat16_rn(q0 - __bfloat162float(h0));
+            qa[(8 + warp) * kQS + d + kD / 2] = __float2bfloat16_rn(q1 - __bfloat162float(h1));
+        }
+    }
+    __syncthreads();
+    uint32_t af[8][4];  // the query A fragments, for every stage
+    {
+        const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qa);
+#pragma unroll
+        for (int k16 = 0; k16 < 8; ++k16) {
+            af[k16][0] = q32[(g * kQS + 16 * k16 + 2 * t4) >> 1];
+            af[k16][1] = q32[((g + 8) * kQS + 16 * k16 + 2 * t4) >> 1];
+            af[k16][2] = q32[(g * kQS + 16 * k16 + 8 + 2 * t4) >> 1];
+            af[k16][3] = q32[((g + 8) * kQS + 16 * k16 + 8 + 2 * t4) >> 1];
+        }
+    }
+    // online softmax over the stages: warp h keeps head h's running max / sum; the P V
+    // accumulators (warp w: 8-dim tiles w, w + W, ...) are rescaled by e^(m_old - m_new) per stage
+    float m_run = -INFINITY, l_run = 0.0f;
+    float acc[kD / 8][4];
+#pragma unroll
+    for (int i = 0; i < kD / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0f;
+    for (int s = 0; s < nsub; ++s) {
+        if (s + 1 < nsub)
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        const int ns = min(kSub, n - s * kSub);
+        uint4* kst = ks + (s & 1) * kSub * 16;
+        uint4* vst = vs + (s & 1) * kSub * 16;
+        if (appender && s == nsub - 1) {  // the appended row is the split's last position
+            const int tp = pos - t0 - s * kSub;
+            __nv_bfloat16* ksh = reinterpret_cast<__nv_bfloat16*>(kst);
+            __nv_bfloat16* vsh = reinterpret_cast<__nv_bfloat16*>(vst);
+            auto sidx = [&](int d) { return int(swz(tp, d >> 3)) * 8 + (d & 7); };
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int d = lane + 32 * h2;
+                ksh[sidx(d)] = ak[h2], ksh[sidx(d + kD / 2)] = ak[2 + h2];
+                vsh[sidx(d)] = av[h2], vsh[sidx(d + kD / 2)] = av[2 + h2];
+            }
+        }
+        __syncthreads();
+        // S = Q K^T: warp w takes the 8-position tiles w, w + W, ...
+        for (int j = warp; j < kSub / 8; j += W) {
+            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const int r = 8 * j + g;  // this lane's key row (B column)
+#pragma unroll
+            for (int k16 = 0; k16 < 8; ++k16) {
+                const uint32_t b0 = reinterpret_cast<const uint32_t*>(kst + swz(r, 2 * k16))[t4];
+                const uint32_t b1 = reinterpret_cast<const uint32_t*>(kst + swz(r, 2 * k16 + 1))[t4];
+                mma_bf16(c, af[k16][0], af[k16][1], af[k16][2], af[k16][3], b0, b1);
+            }
+            if (g < G) {  // rows g (hi) + g + 8 (lo) of head g, positions 8j + 2t4, + 1
+                const int p0 = 8 * j + 2 * t4;
+                sc[g * kSub + p0] = c[0] + c[2];
+                sc[g * kSub + p0 + 1] = c[1] + c[3];
+            }
+        }
+        __syncthreads();
+        {  // head `warp`: new running max, rescale factor, probabilities as bf16 hi (row h) + lo (8 + h)
+            const float* sw = sc + warp * kSub;
+            float mloc = -INFINITY;
+            for (int t = lane; t < ns; t += 32) mloc = fmaxf(mloc, sw[t]);
+            const float mnew = fmaxf(m_run, warp_max(mloc));
+            const float al = __expf(m_run - mnew);  // 0 at the first stage
+            float ssum = 0.0f;
+            for (int t = lane; t < kSub; t += 32) {
+                const float e = t < ns ? __expf(sw[t] - mnew) : 0.0f;
+                ssum += e;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+                pa[warp * kPS + t] = hi;
+                pa[(8 + warp) * kPS + t] = __float2bfloat16_rn(e - __bfloat162float(hi));
+            }
+            l_run = fmaf(l_run, al, warp_sum(ssum));
+            m_run = mnew;
+            if (lane == 0) alpha_s[warp] = al;
+        }
+        __syncthreads();
+        {  // O = O e^(m_old - m_new) + P V (A rows g and g + 8 are both head g)
+            const float ag = g < G ? alpha_s[g] : 0.0f;
+            const uint32_t* p32 = reinterpret_cast<const uint32_t*>(pa);
+#pragma unroll
+            for (int i = 0; i < kD / 8; ++i) {
+                const int nt = warp + i * W;
+                if (nt >= kD / 8) break;
+                float(&c)[4] = acc[i];
+                c[0] *= ag, c[1] *= ag, c[2] *= ag, c[3] *= ag;
+#pragma unroll
+                for (int k16 = 0; k16 < kSub / 16; ++k16) {
+                    const uint32_t a0 = p32[(g * kPS + 16 * k16 + 2 * t4) >> 1];
+                    const uint32_t a1 = p32[((g + 8) * kPS + 16 * k16 + 2 * t4) >> 1];
+                    const uint32_t a2 = p32[(g * kPS + 16 * k16 + 8 + 2 * t4) >> 1];
+                    const uint32_t a3 = p32[((g + 8) * kPS + 16 * k16 + 8 + 2 * t4) >> 1];
+                    // B = V[16 positions][8 dims] (row-major k x n): two 8x8 matrices, transposed load
+                    const uint32_t va =
+                        static_cast<uint32_t>(__cvta_generic_to_shared(vst + swz(16 * k16 + (lane & 15), nt)));
+                    uint32_t b0, b1;
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                                 : "=r"(b0), "=r"(b1)
+                                 : "r"(va));
+                    mma_bf16(c, a0, a1, a2, a3, b0, b1);
+                }
+            }
+        }
+        __syncthreads();  // this stage, the scores and the probabilities are free again
+        if (s + 2 < nsub) issue(s + 2);
+    }
+    if (g < G) {
+#pragma unroll
+        for (int i = 0; i < kD / 8; ++i) {
+            const int nt = warp + i * W;
+            if (nt >= kD / 8) break;
+            fin[g * kPart + 4 + 8 * nt + 2 * t4] = acc[i][0] + acc[i][2];
+            fin[g * kPart + 4 + 8 * nt + 2 * t4 + 1] = acc[i][1] + acc[i][3];
+        }
+    }
+    __syncthreads();
+    const float4 a4 = *reinterpret_cast<const float4*>(fin + warp * kPart + 4 + 4 * lane);
+    // (attn_finish's cluster scratch reuses the same bytes after its first barrier)
+    const bool wrote = attn_finish(m_run, l_run, a4, reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh,
+                                   kvh * G + warp, hq, hkv, sp, nsp, cluster_merge);
+    if (planes) attn_token_planes(wrote, out, b, hq, hkv, int(gridDim.y), tok_arrivals, planes, texp);
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args... args) {
@@ -935,16 +1168,57 @@ cudaError_t launch_silu_mul(const void* gu, void* act, int64_t m, int64_t f, cud
                       static_cast<__nv_bfloat16*>(act), m, int(f));
 }
 
-// splits of the context: ~2 waves of CTAs over the SMs, chunks of 32..256 positions
-static void attention_split(int64_t batch, int64_t hkv, int64_t pos, int* nsp_out, int* chunk_out) {
+// The tensor-core kernels (up to 8 query heads per KV head) take any chunk (the streaming kernel
+// beyond kMaxChunk positions); the CUDA-core kernel stages a whole chunk of <= kMaxChunk.
+static bool attention_uses_mma(int64_t hq, int64_t hkv) {
+    static const bool no_mma = std::getenv("RTNQ_ATTN_NO_MMA") != nullptr;
+    return hq / hkv <= 8 && !no_mma;
+}
+
+// splits of the context: ~`waves` waves of CTAs over the SMs, chunks of >= 32 positions (and at
+// most kMaxChunk for the CUDA-core kernel)
+constexpr int kStreamExtraSplits = 8;
+static void attention_split(int64_t batch, int64_t hkv, int64_t pos, bool mma, int* nsp_out, int* chunk_out,
+                            bool* stream_out = nullptr) {
+    static const int64_t waves = [] {
+        const char* e = std::getenv("RTNQ_ATTN_WAVES");
+        return e ? int64_t(std::atoi(e)) : int64_t(2);
+    }();
+    static const int64_t max_chunk_env = [] {
+        const char* e = std::getenv("RTNQ_ATTN_MAX_CHUNK");
+        return e ? int64_t(std::atoi(e)) : int64_t(0);
+    }();
+    int64_t max_chunk = mma ? int64_t(1) << 30 : int64_t(kMaxChunk);
+    if (max_chunk_env > 0 && max_chunk_env < max_chunk) max_chunk = max_chunk_env < 32 ? 32 : max_chunk_env;
     const int64_t ctx = pos + 1, pairs = batch * hkv;
-    int64_t nsp = (2 * 148 + pairs - 1) / pairs;
+    int64_t nsp = (waves * 148 + pairs - 1) / pairs;
     nsp = nsp < 1 ? 1 : nsp;
-    const int64_t max_sp = (ctx + 31) / 32, min_sp = (ctx + kMaxChunk - 1) / kMaxChunk;
+    const int64_t max_sp = (ctx + 31) / 32, min_sp = (ctx + max_chunk - 1) / max_chunk;
     nsp = nsp > max_sp ? max_sp : nsp;
     nsp = nsp < min_sp ? min_sp : nsp;
     int64_t chunk = (ctx + nsp - 1) / nsp;
     chunk = (chunk + 7) / 8 * 8;
+    if (stream_out) *stream_out = false;
+    if (mma && chunk > kMaxChunk) {
+        // the streaming kernel (3 CTAs per SM, long-running CTAs): the smallest split count from
+        // here whose grid fills its last wave of 3 x 148 CTAs to >= 1/1.2 -- a grid just past a
+        // whole wave runs a long tail (B32 ctx 4096: 2 splits, 1.15 waves, 196 us; 3 splits, 145 us)
+        const int64_t n0 = nsp;
+        int64_t best = n0;
+        double best_eff = 1e30;
+        for (int64_t n = n0; n <= n0 + kStreamExtraSplits && n <= max_sp; ++n) {
+            const double w = double(pairs * n) / (3.0 * 148.0);
+            const double eff = ceil(w) / w;
+            if (eff < best_eff) best = n, best_eff = eff;
+            if (eff <= 1.2) {
+                best = n;
+                break;
+            }
+        }
+        chunk = (ctx + best - 1) / best;
+        chunk = (chunk + 7) / 8 * 8;
+        if (stream_out) *stream_out = true;
+    }
     *nsp_out = int((ctx + chunk - 1) / chunk);
     *chunk_out = int(chunk);
 }
@@ -956,7 +1230,10 @@ static void attention_split(int64_t batch, int64_t hkv, int64_t pos, int* nsp_ou
 constexpr size_t kAttnCounterBytes = 64 * 1024;
 size_t decode_attention_workspace_bytes(int64_t batch, int64_t hq, int64_t hkv, int64_t max_len) {
     int nsp, chunk;
-    attention_split(batch, hkv, max_len - 1, &nsp, &chunk);  // the largest context of this cache
+    // the largest context of this cache; the streaming kernel's split count may exceed the
+    // default rule's by up to kStreamExtraSplits, whatever the context
+    attention_split(batch, hkv, max_len - 1, hkv > 0 && attention_uses_mma(hq, hkv), &nsp, &chunk);
+    nsp += kStreamExtraSplits;
     return kAttnCounterBytes + size_t(batch) * size_t(hq) * size_t(nsp) * kPart * sizeof(float) + 256;
 }
 
@@ -969,22 +1246,27 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
         return cudaErrorInvalidValue;
     const int G = int(hq / hkv);
     int nsp, chunk;
-    attention_split(batch, hkv, pos, &nsp, &chunk);
-    // tensor cores for up to 8 query heads per KV head (hi/lo rows of one m16 tile)
-    static const bool no_mma = std::getenv("RTNQ_ATTN_NO_MMA") != nullptr;
-    const bool mma = G <= 8 && !no_mma;
+    const bool mma = attention_uses_mma(hq, hkv);
+    bool stream = false;
+    attention_split(batch, hkv, pos, mma, &nsp, &chunk, &stream);
     auto mma_smem = [](int ch) {
         const int chp = (ch + 15) / 16 * 16;
         return size_t(2 * chp * 16) * 16 + size_t(16) * (kD + 8) * 2 + size_t(16) * (chp + 8) * 2 +
                size_t(8) * chp * 4 + size_t(8) * kPart * 4;
     };
-    const size_t smem = mma ? mma_smem(chunk) : size_t(2 * chunk * 16) * 16 + size_t(G) * (kD + chunk) * 4;
+    const size_t stream_smem = size_t(2 * 2 * kSub * 16) * 16 + size_t(16) * (kD + 8) * 2 +
+                               size_t(16) * (kSub + 8) * 2 + size_t(8) * kSub * 4;
+    const size_t smem = stream ? stream_smem
+                        : mma  ? mma_smem(chunk)
+                               : size_t(2 * chunk * 16) * 16 + size_t(G) * (kD + chunk) * 4;
     static unsigned long long configured = 0;  // per device
     if (!(configured & current_device_bit())) {
         cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(2 * kMaxChunk * 16 * 16 + 32 * (kD + kMaxChunk) * 4));
         cudaFuncSetAttribute(decode_attention_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(mma_smem(kMaxChunk)));
+        cudaFuncSetAttribute(decode_attention_mma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(stream_smem));
         configured |= current_device_bit();
     }
     // split-merge scratch: the counters (zero-initialized, self-resetting) and the partials, from
@@ -1023,7 +1305,11 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     }
     // 2..8 splits: one thread-block cluster per (token, KV head), merged over DSMEM; more splits
     // merge through global memory (the last CTA to arrive)
-    const int cluster = nsp >= 2 && nsp <= 8 && !std::getenv("RTNQ_ATTN_NO_CLUSTER") ? 1 : 0;
+    static const int max_cluster = [] {
+        const char* e = std::getenv("RTNQ_ATTN_MAX_CLUSTER");
+        return e ? std::atoi(e) : 8;
+    }();
+    const int cluster = nsp >= 2 && nsp <= max_cluster && !std::getenv("RTNQ_ATTN_NO_CLUSTER") ? 1 : 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(hkv), unsigned(batch), unsigned(nsp));
     cfg.blockDim = dim3(unsigned(32 * G));
@@ -1051,7 +1337,10 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, mma ? decode_attention_mma_kernel : decode_attention_kernel,
+    return cudaLaunchKernelEx(&cfg,
+                              stream ? decode_attention_mma_stream_kernel
+                              : mma  ? decode_attention_mma_kernel
+                                     : decode_attention_kernel,
                               static_cast<const __nv_bfloat16*>(qkv),
                               static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), part,
                               int(hq), int(hkv), int(lmax), int(pos), theta, static_cast<__nv_bfloat16*>(out),

@@ -49,9 +49,16 @@ def rope_ref(x, pos, theta):
     return torch.cat([a * c - b * s, b * c + a * s], -1)
 
 
-@pytest.mark.parametrize("hq,hkv", [(32, 8), (8, 1), (4, 2)])
-def test_decode_attention_matches_torch(hq, hkv):
-    b, lmax, pos, d, theta = 3, 40, 33, 128, 500000.0
+@pytest.mark.parametrize("hq,hkv,b,lmax,pos", [
+    (32, 8, 3, 40, 33), (8, 1, 3, 40, 33), (4, 2, 3, 40, 33),
+    # the tensor-core kernel's 64-position stages: context ends on / next to a stage edge, one
+    # position, long splits (many stages per CTA, online softmax), batch 16 / 32
+    (32, 8, 2, 200, 127), (32, 8, 2, 200, 128), (32, 8, 1, 8, 0), (8, 1, 2, 1300, 1200),
+    (32, 8, 1, 4100, 4095), (32, 8, 16, 300, 256),
+    # splits longer than 256 positions: the streaming kernel (stages of 64, online softmax)
+    (32, 8, 32, 1100, 1023), (32, 8, 16, 1100, 1024), (32, 8, 64, 700, 600), (8, 1, 128, 800, 780)])
+def test_decode_attention_matches_torch(hq, hkv, b, lmax, pos):
+    d, theta = 128, 500000.0
     g = torch.Generator(device="cuda").manual_seed(hq)
     qkv = torch.randn(b, (hq + 2 * hkv) * d, device="cuda", generator=g).to(torch.bfloat16)
     kc = (torch.rand(b, lmax, hkv, d, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
@@ -65,8 +72,10 @@ def test_decode_attention_matches_torch(hq, hkv):
     kref, vref = k0.double(), v0.double()
     kref[:, pos] = rope_ref(kn, pos, theta).to(torch.bfloat16).double()
     vref[:, pos] = vn.double()
-    # rotated key: within one bf16 rounding of the f64 rotation; value copied verbatim
-    assert torch.allclose(kc[:, pos].double(), kref[:, pos], rtol=2 ** -7, atol=1e-6)
+    # rotated key: within one bf16 rounding of the f64 rotation plus the f32 angle's error
+    # (pos * inv rounded: ~pos * 2^-24 rad); value copied verbatim
+    atol = 1e-6 + (pos + 1) * 2.0 ** -22 * float(kn.abs().max())
+    assert torch.allclose(kc[:, pos].double(), kref[:, pos], rtol=2 ** -7, atol=atol)
     assert torch.equal(vc[:, pos], vn)
     assert torch.equal(kc[:, :pos], k0[:, :pos])           # earlier positions untouched
     qr = rope_ref(q, pos, theta)                           # [b, hq, d]
@@ -179,7 +188,7 @@ def test_decode_step_fused_planes_is_bit_identical():
     assert torch.equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("batch,pos", [(1, 100), (2, 300), (16, 256), (1, 700)])
+@pytest.mark.parametrize("batch,pos", [(1, 100), (2, 300), (16, 256), (1, 700), (16, 1100)])
 def test_decode_attention_merge_paths(batch, pos):
     """The split-context merges (thread-block cluster over DSMEM on small grids, last-CTA global
     merge otherwise) agree with each other and with the single-CTA path's math."""
