@@ -397,6 +397,38 @@ def exact_record(cx, reps=5):
             "weight_bytes_per_layer": nbytes, **out}
 
 
+def attention_record(cx, launches=10, reps=5):
+    """GQA decode attention (32 query / 8 KV heads, head dim 128, RoPE, KV append) over a bf16
+    cache: KV bytes per second per (batch, context), `launches` back to back in a CUDA graph."""
+    import paper_2505_15909_b200 as rq
+    torch = cx.torch
+    hq, hkv, d = 32, 8, 128
+    out = {}
+    for b, ctx in ((16, 256), (16, 4096), (32, 4096)):
+        with torch.cuda.stream(cx.stream):
+            qkv = torch.randn(b, (hq + 2 * hkv) * d, device=cx.dev).to(torch.bfloat16)
+            kc = torch.randn(b, ctx + 1, hkv, d, device=cx.dev).to(torch.bfloat16)
+            vc = torch.randn_like(kc)
+            att = torch.empty(b, hq * d, device=cx.dev, dtype=torch.bfloat16)
+            ws = rq.Workspace(0, cx.dev)  # sized by the first call
+
+        def run():
+            for _ in range(launches):
+                rq.decode_attention(qkv, kc, vc, att, hq, hkv, ctx, stream=cx.stream, workspace=ws)
+
+        run()
+        cx.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cx.stream):
+            run()
+        us = cx.timed(cx.runner(g, None), reps, 1) * 1e3 / launches
+        kv = 2 * b * (ctx + 1) * hkv * d * 2
+        out[f"b{b}_ctx{ctx}"] = {"us": round(us, 2), "kv_gbs": round(kv / (us * 1e-6) / 1e9, 1)}
+        del kc, vc
+    return {"workload": "Llama-3.1-8B GQA decode attention (32/8 heads, d 128, RoPE + KV append), bf16 KV cache, "
+                        "CUDA graph of back-to-back launches", **out}
+
+
 def run_gpu(args):
     import numpy as np
 
@@ -449,6 +481,7 @@ def run_gpu(args):
         if world == 1:
             line["quantize"] = {f"w{b}": quantize_record(cx, b) for b in (4, 8)}
             line["dropin_exact"] = exact_record(cx)
+            line["decode_attention"] = attention_record(cx)
         # configs[3]: Llama-3.1-70B, 80 layers, W4 + layer-0 down_proj W8, at TP = world
         t70, p70 = rq.plan.resolve("explicit:0 modules:4", tp.LLAMA_70B.layers)
         m70 = measure(cx, tp.LLAMA_70B, t70, 1, tp.LLAMA_70B.layers, False, [1, 4, 16], sub_steps, warmup,
