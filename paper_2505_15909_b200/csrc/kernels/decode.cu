@@ -680,9 +680,9 @@ __global__ void decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv,
 // (bf16 x bf16 -> f32).  Queries and probabilities are split into bf16 hi + lo parts stacked in
 // the 16 rows of the A tile (row h: hi part of head h, row 8 + h: lo part), so the products keep
 // ~16 significant bits of q and p; keys and values are bf16 already.  Same staging, splits and
-// merge as decode_attention_kernel (a split of <= kMaxChunk positions loaded at once); its
-// CUDA-core score and P V loops become ~8 + 16 MMAs per 16 positions per warp.  Longer splits
-// run decode_attention_mma_stream_kernel below.
+// merge as decode_attention_kernel (a split loaded at once); its CUDA-core score and P V loops
+// become ~8 + 16 MMAs per 16 positions per warp.  Splits of more than 128 positions run
+// decode_attention_mma_warp_kernel below.
 __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                          uint32_t b1) {
     asm volatile(
@@ -864,29 +864,27 @@ __global__ void decode_attention_mma_kernel(const __nv_bfloat16* __restrict__ qk
     if (planes) attn_token_planes(wrote, out, b, hq, hkv, int(gridDim.y), tok_arrivals, planes, texp);
 }
 
-// Long contexts: the same arithmetic, but a split streams its positions through two 64-position
-// cp.async stages (the next stage loads while this one is scored) with an online softmax across
-// the stages, so a split can be any length and three CTAs fit an SM (74 KiB of shared memory
-// each).  The one-shot kernel above stays faster for splits of <= kMaxChunk positions (fewer
-// barriers and no padded stage): B16 ctx 256 8.6 vs 10.1 us; the streaming one is 2x faster
-// from ctx 1024 (B16 ctx 4096: 144 -> 73 us, 57 % of HBM on the KV bytes).
-constexpr int kSub = 64;
-
-__global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
+// Long splits (> 128 positions): the same arithmetic, streamed.  A split's positions pass through
+// kStages cp.async stages of kSub positions (the next loads while this one is scored), so a split
+// can be any length and three CTAs share an SM (68 KiB of shared memory each).  Each warp owns 16
+// positions of a stage: its scores stay in registers and become the P operand of its P V MMAs
+// (the m16n8 C fragments of two 8-position tiles are the m16n8k16 A fragment; rows g / g + 8 =
+// bf16 hi / lo of head g), it keeps its own online softmax, and the warps merge once at the end:
+// one barrier per stage.  B16 ctx 4096: 144 us (one-shot kernel) -> 74 (a block-wide softmax
+// per stage, 4 barriers) -> 55 us, 4.9 TB/s on the KV bytes (profiles/r2_attention_long_ctx.md).
+template <int kSub, int kStages>
+__global__ void __launch_bounds__(256) decode_attention_mma_warp_kernel(
     const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
     float* __restrict__ part, int hq, int hkv, int lmax, int pos, float theta, __nv_bfloat16* __restrict__ out,
     int* __restrict__ arrivals, int cluster_merge, int chunk, int8_t* __restrict__ planes,
     int32_t* __restrict__ texp, int* __restrict__ tok_arrivals) {
-    constexpr int kQS = kD + 8;    // bf16 per A-tile row of the queries (padded)
-    constexpr int kPS = kSub + 8;  // bf16 per A-tile row of the probabilities (padded)
+    constexpr int kQS = kD + 8;  // bf16 per A-tile row of the queries (padded)
     extern __shared__ uint4 smq[];
-    uint4* ks = smq;                                                           // [2][kSub][16] swizzled
-    uint4* vs = ks + 2 * kSub * 16;                                            // [2][kSub][16]
-    __nv_bfloat16* qa = reinterpret_cast<__nv_bfloat16*>(vs + 2 * kSub * 16);  // [16][kQS] q hi / lo
-    __nv_bfloat16* pa = qa + 16 * kQS;                                         // [16][kPS] p hi / lo
-    float* sc = reinterpret_cast<float*>(pa + 16 * kPS);                       // [8][kSub] scores
-    float* fin = reinterpret_cast<float*>(ks);  // [G][kPart] per-head results, after the last stage
-    __shared__ float alpha_s[8];
+    uint4* ks = smq;                                                                 // [kStages][kSub][16] swizzled
+    uint4* vs = ks + kStages * kSub * 16;                                            // [kStages][kSub][16]
+    __nv_bfloat16* qa = reinterpret_cast<__nv_bfloat16*>(vs + kStages * kSub * 16);  // [16][kQS] q hi / lo
+    float* wacc = reinterpret_cast<float*>(ks);  // after the last stage: [warp][head][kD] P V partials
+    __shared__ float wm[8][8], wl[8][8];        // [warp][head]: running max, sum
     const int b = blockIdx.y, kvh = blockIdx.x, sp = blockIdx.z, nsp = gridDim.z, G = hq / hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x, W = nthr >> 5;
     const int g = lane >> 2, t4 = lane & 3;
@@ -897,12 +895,12 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
     __nv_bfloat16* kcb = kc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     __nv_bfloat16* vcb = vc + (int64_t(b) * lmax) * cstride + int64_t(kvh) * kD;
     const int t0 = sp * chunk, n = min(chunk, pos + 1 - t0), nsub = (n + kSub - 1) / kSub;
-    // sub-chunk s -> stage s & 1 by cp.async: rows past its end zeroed (finite for the MMAs), the
-    // appended row (pos, not in the cache yet) skipped -- warp 0 writes it before that stage's use
     auto issue = [&](int s) {
+        // sub-chunk s -> stage s % kStages: rows past its end zeroed (finite for the MMAs), the
+        // appended row (pos, not in the cache yet) skipped -- warp 0 writes it before that stage's use
         const int base = t0 + s * kSub, ns = min(kSub, n - s * kSub);
-        uint4* kst = ks + (s & 1) * kSub * 16;
-        uint4* vst = vs + (s & 1) * kSub * 16;
+        uint4* kst = ks + (s % kStages) * kSub * 16;
+        uint4* vst = vs + (s % kStages) * kSub * 16;
         for (int i = threadIdx.x; i < kSub * 16; i += nthr) {
             const int t = i >> 4, c = i & 15;
             if (t >= ns) {
@@ -921,11 +919,7 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // the first two stages of cached rows (written by earlier steps) before the dependency on the
-    // previous kernel (the qkv linear): with programmatic dependent launch they stream in under
-    // its tail, and their latency overlaps the RoPE table and the query rotation below
-    issue(0);
-    if (nsub > 1) issue(1);
+    for (int i = 0; i < kStages - 1 && i < nsub; ++i) issue(i);
     pdl_prologue();
     __shared__ float2 cs_s[kD / 2];
     if (threadIdx.x < kD / 2) {
@@ -934,9 +928,7 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
         sincosf(float(pos) * inv, &sn, &cn);
         cs_s[threadIdx.x] = make_float2(cn, sn);
     }
-    // zero the absent heads' query and probability rows
-    for (int i = threadIdx.x; i < 16 * kPS / 2; i += nthr) reinterpret_cast<uint32_t*>(pa)[i] = 0u;
-    for (int i = threadIdx.x; i < 16 * kQS / 2; i += nthr) {
+    for (int i = threadIdx.x; i < 16 * kQS / 2; i += nthr) {  // the absent heads' query rows
         const int r = i / (kQS / 2);
         if ((r & 7) >= G) reinterpret_cast<uint32_t*>(qa)[i] = 0u;
     }
@@ -946,8 +938,8 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
         return make_float2(a * c.x - bb * c.y, bb * c.x + a * c.y);
     };
     const bool appender = sp == nsp - 1 && warp == 0;
-    __nv_bfloat16 ak[4], av[4];  // the appended row's rotated key / value at dims lane, +32, +64, +96
-    if (appender) {  // append the rotated key and the value at pos to the cache
+    __nv_bfloat16 ak[4], av[4];
+    if (appender) {
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
             const int d = lane + 32 * h2;
@@ -960,7 +952,7 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
             vcb[int64_t(pos) * cstride + d + kD / 2] = av[2 + h2];
         }
     }
-    {  // rotated, pre-scaled query of head `warp`, as bf16 hi (row warp) + lo (row 8 + warp)
+    {
         const __nv_bfloat16* qp = qkv + row + int64_t(kvh * G + warp) * kD;
         const float scale = rsqrtf(float(kD));
 #pragma unroll
@@ -976,7 +968,7 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
         }
     }
     __syncthreads();
-    uint32_t af[8][4];  // the query A fragments, for every stage
+    uint32_t af[8][4];
     {
         const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qa);
 #pragma unroll
@@ -987,21 +979,24 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
             af[k16][3] = q32[((g + 8) * kQS + 16 * k16 + 8 + 2 * t4) >> 1];
         }
     }
-    // online softmax over the stages: warp h keeps head h's running max / sum; the P V
-    // accumulators (warp w: 8-dim tiles w, w + W, ...) are rescaled by e^(m_old - m_new) per stage
-    float m_run = -INFINITY, l_run = 0.0f;
+    float m_run = -INFINITY, l_part = 0.0f;  // head g's running max (quad-uniform), this lane's sum
     float acc[kD / 8][4];
 #pragma unroll
     for (int i = 0; i < kD / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0f;
     for (int s = 0; s < nsub; ++s) {
-        if (s + 1 < nsub)
+        // committed so far: sub-chunks up to s + kStages - 2 (this iteration's issue comes after
+        // the barrier below); those after s may stay in flight
+        const int pend = min(kStages - 2, nsub - 1 - s);
+        if (pend >= 2)
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+        else if (pend == 1)
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         else
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         const int ns = min(kSub, n - s * kSub);
-        uint4* kst = ks + (s & 1) * kSub * 16;
-        uint4* vst = vs + (s & 1) * kSub * 16;
-        if (appender && s == nsub - 1) {  // the appended row is the split's last position
+        uint4* kst = ks + (s % kStages) * kSub * 16;
+        uint4* vst = vs + (s % kStages) * kSub * 16;
+        if (appender && s == nsub - 1) {
             const int tp = pos - t0 - s * kSub;
             __nv_bfloat16* ksh = reinterpret_cast<__nv_bfloat16*>(kst);
             __nv_bfloat16* vsh = reinterpret_cast<__nv_bfloat16*>(vst);
@@ -1013,85 +1008,84 @@ __global__ void __launch_bounds__(256) decode_attention_mma_stream_kernel(
                 vsh[sidx(d)] = av[h2], vsh[sidx(d + kD / 2)] = av[2 + h2];
             }
         }
+        // stage s is visible to every warp, and every warp is done with stage s - 1: its buffer
+        // takes the sub-chunk kStages - 1 ahead
         __syncthreads();
-        // S = Q K^T: warp w takes the 8-position tiles w, w + W, ...
-        for (int j = warp; j < kSub / 8; j += W) {
-            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-            const int r = 8 * j + g;  // this lane's key row (B column)
+        if (s + kStages - 1 < nsub) issue(s + kStages - 1);
+        for (int sl = warp; sl < kSub / 16; sl += W) {
+            const int p0 = 16 * sl;
+            if (p0 >= ns) break;
+            float c0[4] = {0.0f, 0.0f, 0.0f, 0.0f}, c1[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
             for (int k16 = 0; k16 < 8; ++k16) {
-                const uint32_t b0 = reinterpret_cast<const uint32_t*>(kst + swz(r, 2 * k16))[t4];
-                const uint32_t b1 = reinterpret_cast<const uint32_t*>(kst + swz(r, 2 * k16 + 1))[t4];
-                mma_bf16(c, af[k16][0], af[k16][1], af[k16][2], af[k16][3], b0, b1);
+                const uint32_t* k0 = reinterpret_cast<const uint32_t*>(kst + swz(p0 + g, 2 * k16));
+                const uint32_t* k1 = reinterpret_cast<const uint32_t*>(kst + swz(p0 + g, 2 * k16 + 1));
+                const uint32_t* k2 = reinterpret_cast<const uint32_t*>(kst + swz(p0 + 8 + g, 2 * k16));
+                const uint32_t* k3 = reinterpret_cast<const uint32_t*>(kst + swz(p0 + 8 + g, 2 * k16 + 1));
+                mma_bf16(c0, af[k16][0], af[k16][1], af[k16][2], af[k16][3], k0[t4], k1[t4]);
+                mma_bf16(c1, af[k16][0], af[k16][1], af[k16][2], af[k16][3], k2[t4], k3[t4]);
             }
-            if (g < G) {  // rows g (hi) + g + 8 (lo) of head g, positions 8j + 2t4, + 1
-                const int p0 = 8 * j + 2 * t4;
-                sc[g * kSub + p0] = c[0] + c[2];
-                sc[g * kSub + p0 + 1] = c[1] + c[3];
-            }
-        }
-        __syncthreads();
-        {  // head `warp`: new running max, rescale factor, probabilities as bf16 hi (row h) + lo (8 + h)
-            const float* sw = sc + warp * kSub;
-            float mloc = -INFINITY;
-            for (int t = lane; t < ns; t += 32) mloc = fmaxf(mloc, sw[t]);
-            const float mnew = fmaxf(m_run, warp_max(mloc));
-            const float al = __expf(m_run - mnew);  // 0 at the first stage
-            float ssum = 0.0f;
-            for (int t = lane; t < kSub; t += 32) {
-                const float e = t < ns ? __expf(sw[t] - mnew) : 0.0f;
-                ssum += e;
-                const __nv_bfloat16 hi = __float2bfloat16_rn(e);
-                pa[warp * kPS + t] = hi;
-                pa[(8 + warp) * kPS + t] = __float2bfloat16_rn(e - __bfloat162float(hi));
-            }
-            l_run = fmaf(l_run, al, warp_sum(ssum));
+            // head g's scores at positions p0 + 2 t4, +1, p0 + 8 + 2 t4, +1 (rows g + g + 8)
+            float sv[4] = {c0[0] + c0[2], c0[1] + c0[3], c1[0] + c1[2], c1[1] + c1[3]};
+            const int q0 = p0 + 2 * t4;
+            if (q0 >= ns) sv[0] = -INFINITY;
+            if (q0 + 1 >= ns) sv[1] = -INFINITY;
+            if (q0 + 8 >= ns) sv[2] = -INFINITY;
+            if (q0 + 9 >= ns) sv[3] = -INFINITY;
+            float mloc = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+            mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
+            mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2));
+            const float mnew = fmaxf(m_run, mloc), mref = mnew == -INFINITY ? 0.0f : mnew;
+            const float al = __expf(m_run - mref);
             m_run = mnew;
-            if (lane == 0) alpha_s[warp] = al;
-        }
-        __syncthreads();
-        {  // O = O e^(m_old - m_new) + P V (A rows g and g + 8 are both head g)
-            const float ag = g < G ? alpha_s[g] : 0.0f;
-            const uint32_t* p32 = reinterpret_cast<const uint32_t*>(pa);
+            float pr[4];
 #pragma unroll
-            for (int i = 0; i < kD / 8; ++i) {
-                const int nt = warp + i * W;
-                if (nt >= kD / 8) break;
-                float(&c)[4] = acc[i];
-                c[0] *= ag, c[1] *= ag, c[2] *= ag, c[3] *= ag;
+            for (int j = 0; j < 4; ++j) pr[j] = __expf(sv[j] - mref);
+            l_part = fmaf(l_part, al, (pr[0] + pr[1]) + (pr[2] + pr[3]));
+            const __nv_bfloat162 h01 = __floats2bfloat162_rn(pr[0], pr[1]), h23 = __floats2bfloat162_rn(pr[2], pr[3]);
+            const __nv_bfloat162 l01 = __floats2bfloat162_rn(pr[0] - __low2float(h01), pr[1] - __high2float(h01));
+            const __nv_bfloat162 l23 = __floats2bfloat162_rn(pr[2] - __low2float(h23), pr[3] - __high2float(h23));
+            const uint32_t a0 = *reinterpret_cast<const uint32_t*>(&h01), a1 = *reinterpret_cast<const uint32_t*>(&l01);
+            const uint32_t a2 = *reinterpret_cast<const uint32_t*>(&h23), a3 = *reinterpret_cast<const uint32_t*>(&l23);
+            const uint32_t vrow = static_cast<uint32_t>(__cvta_generic_to_shared(vst)) + uint32_t(p0 + (lane & 15)) * 256u;
+            const int vsw = (p0 + (lane & 15)) & 15;
 #pragma unroll
-                for (int k16 = 0; k16 < kSub / 16; ++k16) {
-                    const uint32_t a0 = p32[(g * kPS + 16 * k16 + 2 * t4) >> 1];
-                    const uint32_t a1 = p32[((g + 8) * kPS + 16 * k16 + 2 * t4) >> 1];
-                    const uint32_t a2 = p32[(g * kPS + 16 * k16 + 8 + 2 * t4) >> 1];
-                    const uint32_t a3 = p32[((g + 8) * kPS + 16 * k16 + 8 + 2 * t4) >> 1];
-                    // B = V[16 positions][8 dims] (row-major k x n): two 8x8 matrices, transposed load
-                    const uint32_t va =
-                        static_cast<uint32_t>(__cvta_generic_to_shared(vst + swz(16 * k16 + (lane & 15), nt)));
-                    uint32_t b0, b1;
-                    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
-                                 : "=r"(b0), "=r"(b1)
-                                 : "r"(va));
-                    mma_bf16(c, a0, a1, a2, a3, b0, b1);
-                }
+            for (int nt = 0; nt < kD / 8; ++nt) {
+                float* c = acc[nt];
+                c[0] *= al, c[1] *= al, c[2] *= al, c[3] *= al;
+                uint32_t b0, b1;
+                asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                             : "=r"(b0), "=r"(b1)
+                             : "r"(vrow + uint32_t((nt ^ vsw) * 16)));
+                mma_bf16(acc[nt], a0, a1, a2, a3, b0, b1);
             }
         }
-        __syncthreads();  // this stage, the scores and the probabilities are free again
-        if (s + 2 < nsub) issue(s + 2);
     }
+    __syncthreads();  // every warp is done with the stages: the partials reuse them
+    float l = l_part + __shfl_xor_sync(0xffffffffu, l_part, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    if (t4 == 0) wm[warp][g] = m_run, wl[warp][g] = l;
     if (g < G) {
+        float* wa = wacc + (warp * 8 + g) * kD;
 #pragma unroll
-        for (int i = 0; i < kD / 8; ++i) {
-            const int nt = warp + i * W;
-            if (nt >= kD / 8) break;
-            fin[g * kPart + 4 + 8 * nt + 2 * t4] = acc[i][0] + acc[i][2];
-            fin[g * kPart + 4 + 8 * nt + 2 * t4 + 1] = acc[i][1] + acc[i][3];
-        }
+        for (int nt = 0; nt < kD / 8; ++nt)
+            *reinterpret_cast<float2*>(wa + 8 * nt + 2 * t4) = make_float2(acc[nt][0] + acc[nt][2], acc[nt][1] + acc[nt][3]);
     }
     __syncthreads();
-    const float4 a4 = *reinterpret_cast<const float4*>(fin + warp * kPart + 4 + 4 * lane);
-    // (attn_finish's cluster scratch reuses the same bytes after its first barrier)
-    const bool wrote = attn_finish(m_run, l_run, a4, reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh,
+    // warp h = head h: merge the warps' partials of this split
+    float M = -INFINITY;
+    for (int w = 0; w < W; ++w) M = fmaxf(M, wm[w][warp]);
+    float L = 0.0f;
+    float4 a4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    for (int w = 0; w < W; ++w) {
+        const float mw = wm[w][warp];
+        const float wt = mw == -INFINITY ? 0.0f : __expf(mw - M);
+        L = fmaf(wt, wl[w][warp], L);
+        const float4 x = *reinterpret_cast<const float4*>(wacc + (w * 8 + warp) * kD + 4 * lane);
+        a4.x = fmaf(wt, x.x, a4.x), a4.y = fmaf(wt, x.y, a4.y), a4.z = fmaf(wt, x.z, a4.z), a4.w = fmaf(wt, x.w, a4.w);
+    }
+    // (attn_finish's cluster scratch reuses these bytes after its first barrier)
+    const bool wrote = attn_finish(M, L, a4, reinterpret_cast<float*>(ks), part, arrivals, out, b, kvh,
                                    kvh * G + warp, hq, hkv, sp, nsp, cluster_merge);
     if (planes) attn_token_planes(wrote, out, b, hq, hkv, int(gridDim.y), tok_arrivals, planes, texp);
 }
@@ -1199,7 +1193,11 @@ static void attention_split(int64_t batch, int64_t hkv, int64_t pos, bool mma, i
     int64_t chunk = (ctx + nsp - 1) / nsp;
     chunk = (chunk + 7) / 8 * 8;
     if (stream_out) *stream_out = false;
-    if (mma && chunk > kMaxChunk) {
+    static const int64_t stream_min = [] {
+        const char* e = std::getenv("RTNQ_ATTN_STREAM_MIN");
+        return e ? int64_t(std::atoi(e)) : int64_t(128);
+    }();
+    if (mma && chunk > stream_min) {
         // the streaming kernel (3 CTAs per SM, long-running CTAs): the smallest split count from
         // here whose grid fills its last wave of 3 x 148 CTAs to >= 1/1.2 -- a grid just past a
         // whole wave runs a long tail (B32 ctx 4096: 2 splits, 1.15 waves, 196 us; 3 splits, 145 us)
@@ -1254,8 +1252,9 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
         return size_t(2 * chp * 16) * 16 + size_t(16) * (kD + 8) * 2 + size_t(16) * (chp + 8) * 2 +
                size_t(8) * chp * 4 + size_t(8) * kPart * 4;
     };
-    const size_t stream_smem = size_t(2 * 2 * kSub * 16) * 16 + size_t(16) * (kD + 8) * 2 +
-                               size_t(16) * (kSub + 8) * 2 + size_t(8) * kSub * 4;
+    constexpr int kStreamSub = 64, kStreamStages = 2;
+    const size_t stream_smem = size_t(2 * kStreamStages * kStreamSub * 16) * 16 + size_t(16) * (kD + 8) * 2;
+    auto stream_kern = decode_attention_mma_warp_kernel<kStreamSub, kStreamStages>;
     const size_t smem = stream ? stream_smem
                         : mma  ? mma_smem(chunk)
                                : size_t(2 * chunk * 16) * 16 + size_t(G) * (kD + chunk) * 4;
@@ -1265,8 +1264,7 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
                              int(2 * kMaxChunk * 16 * 16 + 32 * (kD + kMaxChunk) * 4));
         cudaFuncSetAttribute(decode_attention_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(mma_smem(kMaxChunk)));
-        cudaFuncSetAttribute(decode_attention_mma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(stream_smem));
+        cudaFuncSetAttribute(stream_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(stream_smem));
         configured |= current_device_bit();
     }
     // split-merge scratch: the counters (zero-initialized, self-resetting) and the partials, from
@@ -1338,7 +1336,7 @@ cudaError_t launch_decode_attention(const void* qkv, void* kcache, void* vcache,
     cfg.attrs = attrs;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg,
-                              stream ? decode_attention_mma_stream_kernel
+                              stream ? stream_kern
                               : mma  ? decode_attention_mma_kernel
                                      : decode_attention_kernel,
                               static_cast<const __nv_bfloat16*>(qkv),
