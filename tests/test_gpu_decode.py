@@ -233,11 +233,12 @@ def test_default_workspaces_of_attention_and_linear_are_separate():
 
 
 @pytest.mark.parametrize("batch,pos,hq,hkv", [(1, 100, 32, 8), (2, 300, 32, 8), (16, 256, 32, 8), (1, 700, 32, 8),
-                                              (3, 50, 64, 2)])
+                                              (3, 50, 64, 2), (32, 1023, 32, 8), (16, 1100, 32, 8)])
 def test_decode_attention_emits_o_proj_planes(batch, pos, hq, hkv):
     """The attention's last CTA per token writes the o-projection's activation planes: bit-identical
     to the planes kernel on the attention output, on every merge path (one split, cluster DSMEM,
-    global last-CTA) and on the CUDA-core kernel (32 query heads per KV head)."""
+    global last-CTA), on the CUDA-core kernel (32 query heads per KV head) and on the streaming
+    kernel (splits of more than 128 positions)."""
     import os
     d = 128
     g = torch.Generator(device="cuda").manual_seed(batch * 7 + pos)
