@@ -7,7 +7,11 @@ B = int(os.environ.get("B", "16")); BITS = int(os.environ.get("BITS", "4"))
 st = torch.cuda.Stream()
 ws = rq.Workspace(device="cuda")
 res = []
-for name, n, k in [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]:
+SHAPES = {"8b": [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)],
+          # one TP=8 rank's shards of Llama-3.1-405B / the 70B at TP = 1
+          "405b_tp8": [("qkv", 2304, 16384), ("o", 16384, 2048), ("gate_up", 13312, 16384), ("down", 16384, 6656)],
+          "70b": [("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)]}
+for name, n, k in SHAPES[os.environ.get("MODEL", "8b")]:
     g = 128 if BITS == 4 or os.environ.get("W8G128") else 1 << (k - 1).bit_length()
     NAT = os.environ.get("NATIVE") == "1" or None
     qs = [rq.quantize_pack(((torch.rand(n, k, device="cuda") * 2 - 1) * 0.02).to(torch.bfloat16), BITS, g, k % g != 0, native=NAT) for _ in range(4)]
