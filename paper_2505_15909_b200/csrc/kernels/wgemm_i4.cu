@@ -925,12 +925,15 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
     // scratch/shapes_seq.py, batch 16: qkv / o 10.3 / 9.1 us with the planes kernel, 11.8 / 10.4
     // in the GEMM; gate_up / down 23.7 / 19.4 vs 21.7 / 18.5)
     const int64_t units = ((A.n + i4::kRows - 1) / i4::kRows) * ((A.k + i4::kKB - 1) / i4::kKB);
-    // (W8 group-128: the stand-alone kernel, as for W8 per-channel: 23.4 vs 25.3 us, gate_up batch 16)
+    // W8 group-128 from 16 tokens too: with the sliced hand-off, gate_up / down at batch 16
+    // 27.0 / 19.5 -> 24.9 / 17.2 us, batch 32 29.9 / 24.4 -> 27.7 / 21.7 us; at batch 8 the
+    // stand-alone kernel stays (23.6 vs 24.5 us gate_up)
     static const int64_t min_units = [] {
         const char* e = std::getenv("RTNQ_OWN_PLANES_MIN_UNITS");
         return e ? int64_t(std::atoll(e)) : int64_t(2048);
     }();
-    const bool in_gemm = own_planes && !planes_kernel && A.bits == 4 && A.m >= imma::kOwnPlanesMinM && units >= min_units &&
+    const bool in_gemm = own_planes && !planes_kernel && A.m >= (A.bits == 4 ? imma::kOwnPlanesMinM : 16) &&
+                         units >= min_units &&
                          (reinterpret_cast<uintptr_t>(A.a) & 15) == 0 && !(dbg & 64);
     if (in_gemm) {
         p.own.a = A.a;

@@ -207,10 +207,11 @@ def test_linear_non_finite_activations_raise(kind):
 
 
 @pytest.mark.parametrize("n,k,m", [(528, 1024, 1), (528, 1024, 16), (4096, 4096, 5), (2000, 14336, 33), (28672, 4096, 16),
-                                   (300, 256, 70)])
+                                   (300, 256, 70), (4096, 14336, 16), (4096, 14336, 40), (28672, 4096, 8)])
 def test_w8_group128_int8_path(oracle, n, k, m):
     """W8 with group-128 scales (config 4's selective 8-bit module) on the int8 tensor-core kernel:
-    NATIVE_I8 tiles read from shared memory, one TMEM accumulator per group (wgemm_i4.cu, BITS = 8).
+    NATIVE_I8 tiles read from shared memory, one TMEM accumulator per group (wgemm_i4.cu, BITS = 8);
+    from 16 tokens on large weights the activation planes are made inside the GEMM (OwnPlanes).
     Codes bit-exact (re-encoded oracle codes), output within 1e-5 of the f64 oracle."""
     g = 128
     gen = torch.Generator(device="cuda").manual_seed(n + k + m)
