@@ -520,7 +520,9 @@ __device__ __forceinline__ void peer_consumed_by(char* b, int G) {
 // planes of the launch's tokens themselves (CTA c: tokens c, c + G, ...) with their epilogue /
 // expansion warps, which are idle until the first weights land, and publish them through a
 // self-resetting workspace counter; one warp per CTA acquires it before the first planes TMA.
-constexpr int kOwnPlanesMinM = 8;  // fewer tokens: the stand-alone planes kernel
+// fewer tokens: the stand-alone planes kernel (W4 gate_up at batch 8 / 9 / 10: 17.1 vs 19.0 us;
+// batch 12 / 16: 21.8 vs 23.7 us in the GEMM; env RTNQ_OWN_PLANES_MIN_M overrides for W4)
+constexpr int kOwnPlanesMinM = 11;
 struct OwnPlanes {
     const void* a = nullptr;  // activations [Mtot][K], bf16 / f16; nullptr: planes precomputed
     int a_dtype = 0;

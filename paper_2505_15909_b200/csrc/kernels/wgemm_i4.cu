@@ -932,7 +932,11 @@ cudaError_t launch_wgemm_i4(const WgemmArgs& A, cudaStream_t st) {
         const char* e = std::getenv("RTNQ_OWN_PLANES_MIN_UNITS");
         return e ? int64_t(std::atoll(e)) : int64_t(2048);
     }();
-    const bool in_gemm = own_planes && !planes_kernel && A.m >= (A.bits == 4 ? imma::kOwnPlanesMinM : 16) &&
+    static const int min_m4 = [] {
+        const char* e = std::getenv("RTNQ_OWN_PLANES_MIN_M");
+        return e ? std::atoi(e) : imma::kOwnPlanesMinM;
+    }();
+    const bool in_gemm = own_planes && !planes_kernel && A.m >= (A.bits == 4 ? min_m4 : 16) &&
                          units >= min_units &&
                          (reinterpret_cast<uintptr_t>(A.a) & 15) == 0 && !(dbg & 64);
     if (in_gemm) {
